@@ -1,0 +1,180 @@
+/*
+ * filterreg_b200.h -- C ABI of the B200 FilterReg engine (libfilterreg_b200.so).
+ *
+ * The reference (`twistreg`, /root/reference/pkg/src/twistreg) is pure Python;
+ * its "operator API" for the hot path is the Python lattice / moment / solver
+ * surface.  Each entry point below replaces one of those operators and cites
+ * the reference symbol (file:line, relative to pkg/src/twistreg/).  The Python
+ * package `paper_1811_10136_b200` binds these with ctypes exactly the way a
+ * maintainer would bind them from twistreg.
+ *
+ * Conventions
+ *  - Every pointer argument named d_* is DEVICE memory on the current CUDA
+ *    device, owned by the caller, contiguous, borrowed for the call.
+ *  - Every call is ordered on `stream` (a cudaStream_t passed as void*; NULL =
+ *    legacy default stream) and spawns no host threads.  Calls that must size
+ *    internal buffers (splat, blur) synchronise `stream` internally.
+ *  - Return value: FR_OK or an FR_E* status; fr_last_error() returns the
+ *    thread-local message of the last failure.  Status -> Python exception:
+ *      FR_EINVAL   -> ValueError          (permutohedral.py:57-60, 148-149, 222-225)
+ *      FR_ESTATE   -> RuntimeError        (permutohedral.py:301-302, 331-332)
+ *      FR_EDEGEN   -> DegenerateCorrespondenceError (estep.py:256-257)
+ *      FR_ESOLVER  -> SolverError         (mstep.py:368-369)
+ *      FR_ECAPACITY / FR_ECUDA -> RuntimeError
+ *  - An fr_lattice is single-writer during splat/blur and immutable after
+ *    blur; slicing from several streams concurrently is then safe.
+ */
+#ifndef FILTERREG_B200_H
+#define FILTERREG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    FR_OK = 0,
+    FR_EINVAL = 1,
+    FR_ESTATE = 2,
+    FR_EDEGEN = 3,
+    FR_ESOLVER = 4,
+    FR_ECAPACITY = 5,
+    FR_ECUDA = 6
+};
+
+/* value_mode bits for fr_lattice_splat_points: which observation-derived
+ * columns are splatted, in the reference's order [1, y, (|y|^2), (n)]
+ * (estep.py:153-165). */
+enum {
+    FR_VALUES_M2 = 1,       /* append |y|^2 (update_sigma) */
+    FR_VALUES_NORMALS = 2   /* append the observation normal (point_to_plane) */
+};
+
+/* residual modes (mstep.py:33) */
+enum { FR_POINT_TO_POINT = 0, FR_POINT_TO_PLANE = 1 };
+
+typedef struct fr_lattice fr_lattice;
+
+int fr_abi_version(void);
+const char *fr_last_error(void);
+
+/* ---- permutohedral lattice (permutohedral.py:140-345) ------------------- */
+
+/* PermutohedralLattice(dim, sigma) (permutohedral.py:147-167); sigma has dim
+ * host doubles.  Only dim == 3 (position correspondences) is compiled in this
+ * build; other dims return FR_EINVAL. */
+int fr_lattice_create(int dim, const double *sigma, fr_lattice **out);
+int fr_lattice_destroy(fr_lattice *lat);
+
+/* PermutohedralLattice.splat(features, values) (permutohedral.py:219-251):
+ * d_features n x dim row-major float64, d_values n x nv row-major float64.
+ * Deterministic: per-site sums run in flat (point, vertex) order, bit-identical
+ * to the reference's np.add.at. */
+int fr_lattice_splat(fr_lattice *lat, const double *d_features, const double *d_values,
+                     int64_t n, int nv, void *stream);
+
+/* Same, with the value columns generated on the fly from float32 SoA point
+ * planes (d_pos: 3 planes of n floats; d_normals likewise or NULL):
+ * [1, y, (|y|^2 if FR_VALUES_M2), (n if FR_VALUES_NORMALS)] (estep.py:153-165). */
+int fr_lattice_splat_points(fr_lattice *lat, const float *d_pos, const float *d_normals,
+                            int64_t n, int value_mode, void *stream);
+
+/* PermutohedralLattice.blur() (permutohedral.py:291-327), incl. frontier growth
+ * with the reference's site cap and the final drop of all-zero rows. */
+int fr_lattice_blur(fr_lattice *lat, void *stream);
+
+/* num_sites / value width / blurred flag (permutohedral.py:343-345). */
+int fr_lattice_info(const fr_lattice *lat, int64_t *num_sites, int *nv, int *blurred);
+
+/* Site table export (PermutohedralLattice.keys/.values): d_keys num_sites x
+ * (dim+1) int32, d_values num_sites x nv float64.  Row order is unspecified;
+ * callers sort lexicographically to get the reference order. */
+int fr_lattice_export(const fr_lattice *lat, int32_t *d_keys, double *d_values, void *stream);
+
+/* PermutohedralLattice.slice(query) (permutohedral.py:329-341): d_query m x dim
+ * float64 row-major -> d_out m x nv float64. */
+int fr_lattice_slice(const fr_lattice *lat, const double *d_query, int64_t m, double *d_out,
+                     void *stream);
+
+/* PermutohedralLattice._simplex (permutohedral.py:181-215), bit-exact:
+ * d_keys n x (dim+1) x (dim+1) int32, d_bary n x (dim+1) float64. */
+int fr_simplex(int dim, const double *sigma, const double *d_features, int64_t n,
+               int32_t *d_keys, double *d_bary, void *stream);
+
+/* gaussian_transform_bruteforce (permutohedral.py:64-86): exact sums,
+ * d_q m x dim, d_f n x dim, d_v n x nv, d_out m x nv (all float64). */
+int fr_gauss_bruteforce(const double *d_q, int64_t m, const double *d_f, int64_t n, int dim,
+                        const double *d_v, int nv, const double *sigma, double *d_out,
+                        void *stream);
+
+/* ---- E step (estep.py:186-217) ------------------------------------------ */
+
+/* MomentEngine.moments epilogue fused into the slice: d_x m x 3 float64
+ * positions.  m2_col / normal_col are value-column indices or -1.  Any output
+ * pointer may be NULL except d_m0, d_m1, d_weight, d_target. */
+int fr_moments(const fr_lattice *lat, const double *d_x, int64_t m, double c_prime,
+               int m2_col, int normal_col, double *d_m0, double *d_m1, double *d_weight,
+               double *d_target, double *d_m2, double *d_normal, uint8_t *d_normal_valid,
+               void *stream);
+
+
+/* MomentEngine.moments epilogue alone (estep.py:195-217) over raw kernel sums
+ * d_raw (m x nv float64, from fr_lattice_slice or fr_gauss_bruteforce) at model
+ * positions d_x (m x 3); outputs as fr_moments. */
+int fr_moments_epilogue(const double *d_raw, int64_t m, int nv, const double *d_x,
+                        double c_prime, int m2_col, int normal_col, double *d_m0,
+                        double *d_m1, double *d_weight, double *d_target, double *d_m2,
+                        double *d_normal, uint8_t *d_normal_valid, void *stream);
+
+/* assemble_rigid + objective (mstep.py:102-138, 179-210) over an explicit
+ * ResidualSpec: d_x, d_target, d_normal m x 3 float64, d_weight m, d_valid m
+ * (uint8; point_to_plane only).  d_sums receives 28 doubles:
+ * [upper-triangular H (21, row-major i <= j) | g (6) | sum of squared rows]. */
+int fr_assemble_rigid(const double *d_x, const double *d_weight, const double *d_target,
+                      int64_t m, const double *sigma_inv, int mode, const double *d_normal,
+                      const uint8_t *d_valid, double *d_sums, double *d_scratch, void *stream);
+
+/* ---- fused rigid EM pass (pipeline.py:141-166 + mstep.py:179-210) ------- */
+
+/* Per-iteration pose/kernel constants, all host-side float64. */
+typedef struct fr_rigid_pass_params {
+    double R[9];        /* current rotation, row-major */
+    double c_ref[3];    /* centroid of the reference cloud (xh = x_ref - c_ref) */
+    double c_world[3];  /* R c_ref + t: x = R xh + c_world */
+    double sigma[3];    /* kernel widths of the lattice */
+    double c_prime;     /* outlier constant (estep.py:99-112) */
+    int mode;           /* FR_POINT_TO_POINT / FR_POINT_TO_PLANE */
+    int m2_col;         /* value column of |y|^2 or -1 */
+    int normal_col;     /* value column of the normal sum or -1 */
+    int reserved;
+} fr_rigid_pass_params;
+
+/* Number of float64 partial sums the pass produces for a mode. */
+int fr_rigid_pass_width(int mode, int with_sigma);
+
+/* One E step + M-step assembly over all model points at pose (R, t):
+ * slice at x = R x_ref + t, moments epilogue, residual rows and the
+ * normal-equation sums, reduced deterministically into d_sums
+ * (fr_rigid_pass_width doubles; layout in paper_1811_10136_b200/_rigid.py).
+ * d_ref: 3 float32 planes of m.  d_wtn (point_to_plane only, else NULL):
+ * 7 float32 planes of m receiving weight, target, normal for the candidate
+ * objective pass.  d_scratch: >= fr_rigid_scratch_doubles(mode,...) doubles. */
+int fr_rigid_scratch_doubles(int mode, int with_sigma, int64_t m);
+int fr_rigid_pass(const fr_lattice *lat, const float *d_ref, int64_t m,
+                  const fr_rigid_pass_params *p, double *d_sums, float *d_wtn,
+                  double *d_scratch, void *stream);
+
+/* Objective of k candidate poses (mstep.py:132-138 at mstep.py:443-449) under
+ * the weights/targets/normals stored by the last point_to_plane pass.
+ * cand_R: k x 9, cand_c: k x 3 (R_k c_ref + t_k) host doubles; d_out: k
+ * float64 values 0.5 * sum r^2.  k <= 16. */
+int fr_rigid_objective(const float *d_ref, const float *d_wtn, int64_t m,
+                       const double *c_ref, int k, const double *cand_R,
+                       const double *cand_c, double *d_out, double *d_scratch,
+                       void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FILTERREG_B200_H */

@@ -1,0 +1,125 @@
+"""ctypes binding of libfilterreg_b200.so (the C ABI in include/filterreg_b200.h).
+
+The library is built in-tree by `__graft_entry__.build()` (or
+`python -m paper_1811_10136_b200.build`).  There is no fallback: if the shared
+object or a CUDA device is missing, every operator raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import DegenerateCorrespondenceError, SolverError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfilterreg_b200.so")
+
+FR_OK, FR_EINVAL, FR_ESTATE, FR_EDEGEN, FR_ESOLVER, FR_ECAPACITY, FR_ECUDA = range(7)
+FR_VALUES_M2, FR_VALUES_NORMALS = 1, 2
+FR_POINT_TO_POINT, FR_POINT_TO_PLANE = 0, 1
+
+# every symbol include/filterreg_b200.h declares
+EXPORTED = (
+    "fr_abi_version", "fr_last_error", "fr_lattice_create", "fr_lattice_destroy",
+    "fr_lattice_splat", "fr_lattice_splat_points", "fr_lattice_blur", "fr_lattice_info",
+    "fr_lattice_export", "fr_lattice_slice", "fr_simplex", "fr_gauss_bruteforce",
+    "fr_moments", "fr_rigid_pass_width", "fr_rigid_scratch_doubles", "fr_rigid_pass",
+    "fr_rigid_objective", "fr_moments_epilogue", "fr_assemble_rigid",
+)
+
+
+class RigidPassParams(ctypes.Structure):
+    """fr_rigid_pass_params (include/filterreg_b200.h)."""
+    _fields_ = [("R", ctypes.c_double * 9), ("c_ref", ctypes.c_double * 3),
+                ("c_world", ctypes.c_double * 3), ("sigma", ctypes.c_double * 3),
+                ("c_prime", ctypes.c_double), ("mode", ctypes.c_int),
+                ("m2_col", ctypes.c_int), ("normal_col", ctypes.c_int),
+                ("reserved", ctypes.c_int)]
+
+
+_lib = None
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_D = ctypes.c_double
+_DP = ctypes.POINTER(ctypes.c_double)
+
+_SIGS = {
+    "fr_abi_version": ([], _I),
+    "fr_last_error": ([], ctypes.c_char_p),
+    "fr_lattice_create": ([_I, _DP, ctypes.POINTER(_P)], _I),
+    "fr_lattice_destroy": ([_P], _I),
+    "fr_lattice_splat": ([_P, _P, _P, _L, _I, _P], _I),
+    "fr_lattice_splat_points": ([_P, _P, _P, _L, _I, _P], _I),
+    "fr_lattice_blur": ([_P, _P], _I),
+    "fr_lattice_info": ([_P, ctypes.POINTER(_L), ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "fr_lattice_export": ([_P, _P, _P, _P], _I),
+    "fr_lattice_slice": ([_P, _P, _L, _P, _P], _I),
+    "fr_simplex": ([_I, _DP, _P, _L, _P, _P, _P], _I),
+    "fr_gauss_bruteforce": ([_P, _L, _P, _L, _I, _P, _I, _DP, _P, _P], _I),
+    "fr_moments": ([_P, _P, _L, _D, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P], _I),
+    "fr_moments_epilogue": ([_P, _L, _I, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P], _I),
+    "fr_assemble_rigid": ([_P, _P, _P, _L, _DP, _I, _P, _P, _P, _P, _P], _I),
+    "fr_rigid_pass_width": ([_I, _I], _I),
+    "fr_rigid_scratch_doubles": ([_I, _I, _L], _I),
+    "fr_rigid_pass": ([_P, _P, _L, ctypes.POINTER(RigidPassParams), _P, _P, _P, _P], _I),
+    "fr_rigid_objective": ([_P, _P, _L, _DP, _I, _DP, _DP, _P, _P, _P], _I),
+}
+
+
+def load(path: str = LIB_PATH):
+    """Load the shared library (once) and declare the signatures."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"CUDA extension {path} is missing; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` -- there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    """Map an fr_* status to the reference's exception types."""
+    if status == FR_OK:
+        return
+    msg = load().fr_last_error().decode(errors="replace")
+    if status == FR_EINVAL:
+        raise ValueError(msg)
+    if status == FR_EDEGEN:
+        raise DegenerateCorrespondenceError(msg)
+    if status == FR_ESOLVER:
+        raise SolverError(msg)
+    raise RuntimeError(msg)
+
+
+def dptr(arr) -> ctypes.c_double * 0:
+    """ctypes double* for a small host float64 vector."""
+    import numpy as np
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    return a.ctypes.data_as(_DP), a
+
+
+def device():
+    """The CUDA device the engine runs on (fails loudly without one)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 FilterReg engine needs a CUDA device; none is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)

@@ -1,0 +1,991 @@
+// Permutohedral lattice on B200: deterministic splat, frontier-growing blur,
+// slice table build, generic slice / simplex / brute-force kernels.
+//
+// Reference: permutohedral.py (pkg/src/twistreg).  The build reproduces the
+// reference's site set and float64 values bit for bit:
+//   * keys: fp64 embedding with the reference's operation order (fr_common.cuh)
+//   * splat: entries are grouped per site by a stable radix sort of their hash
+//     slot, then each site's contributions are summed sequentially in flat
+//     (point, vertex) order -- exactly np.add.at's order (permutohedral.py:242)
+//   * blur: Jacobi passes with the same fp64 expression (permutohedral.py:322)
+//     and the same frontier materialisation + site cap (:304-313)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "fr_common.cuh"
+
+namespace fr {
+
+static thread_local char g_err[1024];
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+const char *last_error() { return g_err; }
+
+static const double kScale[13] = {0, 1.00, 1.00, 1.05, 1.05, 1.05, 1.05,
+                                  1.05, 1.10, 1.10, 1.05, 1.05, 1.05};
+static const double kGain[13] = {0,
+                                 2.8952044967493156, 7.26440867477451, 19.65543341118011,
+                                 46.8204989056386,   109.10733236095797, 253.69798361851673,
+                                 585.8878389979589,  1551.3475661281732, 3556.1187473560817,
+                                 7167.31894204168,   16021.44046866235,  36206.979459505295};
+
+int make_consts(int dim, const double *sigma, LatticeConsts *out) {
+    if (dim < 1 || dim > 3) {
+        set_error("feature dimension %d not compiled in this build (supported: 1..3)", dim);
+        return FR_EINVAL;
+    }
+    memset(out, 0, sizeof(*out));
+    out->dim = dim;
+    for (int j = 0; j < dim; ++j) {
+        if (!std::isfinite(sigma[j]) || !(sigma[j] > 0)) {
+            set_error("kernel widths must be finite and positive");
+            return FR_EINVAL;
+        }
+        out->sigma[j] = sigma[j];
+    }
+    // s_d = sqrt(2/3) * (d+1) * SCALE[d]; sf[j] = s_d / sqrt((j+1)(j+2))
+    const double sd = std::sqrt(2.0 / 3.0) * (double)(dim + 1) * kScale[dim];
+    for (int j = 0; j < dim; ++j) out->sf[j] = sd / std::sqrt((double)((j + 1) * (j + 2)));
+    out->gain = kGain[dim];
+    return FR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+struct BuildHash {
+    unsigned long long *keys;
+    int *site;
+    unsigned mask;
+};
+
+// returns slot, or -1 when the table is full; *created = 1 for the CAS winner
+__device__ __forceinline__ int hash_insert(BuildHash h, unsigned long long key, int *created) {
+    unsigned s = (unsigned)mix64(key) & h.mask;
+    *created = 0;
+    for (unsigned it = 0; it <= h.mask; ++it) {
+        unsigned long long k = h.keys[s];
+        if (k == key) return (int)s;
+        if (k == kEmptyKey) {
+            unsigned long long prev = atomicCAS(&h.keys[s], kEmptyKey, key);
+            if (prev == kEmptyKey) { *created = 1; return (int)s; }
+            if (prev == key) return (int)s;
+        }
+        s = (s + 1) & h.mask;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ int hash_find(BuildHash h, unsigned long long key) {
+    unsigned s = (unsigned)mix64(key) & h.mask;
+    for (unsigned it = 0; it <= h.mask; ++it) {
+        unsigned long long k = h.keys[s];
+        if (k == key) return h.site[s];
+        if (k == kEmptyKey) return -1;
+        s = (s + 1) & h.mask;
+    }
+    return -1;
+}
+
+// value sources ------------------------------------------------------------
+
+struct GenericSrc {
+    const double *F;   // n x D
+    const double *V;   // n x nv
+    int nv;
+    template <int D>
+    __device__ __forceinline__ void feat(long long p, double *f) const {
+#pragma unroll
+        for (int j = 0; j < D; ++j) f[j] = F[p * D + j];
+    }
+    __device__ __forceinline__ double value(long long p, int c) const { return V[p * nv + c]; }
+};
+
+// [1, y, (|y|^2), (n)] from float32 SoA planes (estep.py:153-165)
+struct PointSrc {
+    const float *pos;   // 3 planes of n
+    const float *nrm;   // 3 planes of n or null
+    long long n;
+    int m2;             // 1 when the |y|^2 column is present
+    int nv;
+    template <int D>
+    __device__ __forceinline__ void feat(long long p, double *f) const {
+#pragma unroll
+        for (int j = 0; j < D; ++j) f[j] = (double)pos[j * n + p];
+    }
+    __device__ __forceinline__ double value(long long p, int c) const {
+        if (c == 0) return 1.0;
+        if (c <= 3) return (double)pos[(c - 1) * n + p];
+        if (m2 && c == 4) {
+            double y0 = pos[p], y1 = pos[n + p], y2 = pos[2 * n + p];
+            // np.einsum("nd,nd->n") on 3-vectors sums (y0^2 + y2^2) + y1^2
+            return __dadd_rn(__dadd_rn(__dmul_rn(y0, y0), __dmul_rn(y2, y2)), __dmul_rn(y1, y1));
+        }
+        int k = c - 4 - m2;
+        return (double)nrm[k * n + p];
+    }
+};
+
+// splat phase 1: embed, insert keys, record (slot, bary) per (point, vertex)
+template <int D, class Src>
+__global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash h,
+                                unsigned sentinel, unsigned *entry_slot, unsigned *entry_idx,
+                                double *entry_bary, unsigned long long *counters) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+        double f[D];
+        src.template feat<D>(p, f);
+        Simplex<D> s;
+        simplex_exact<D>(f, c, s);
+        if (s.overflow) atomicOr(&counters[2], 1ull);
+        bool any_value = false;
+        for (int cc = 0; cc < src.nv; ++cc) any_value |= (src.value(p, cc) != 0.0);
+#pragma unroll
+        for (int l = 0; l <= D; ++l) {
+            long long e = p * (D + 1) + l;
+            unsigned slot = sentinel;
+            if (s.bary[l] != 0.0 && any_value && !s.overflow) {
+                int created;
+                int sl = hash_insert(h, s.packed(l), &created);
+                if (sl < 0) atomicOr(&counters[2], 2ull);
+                else {
+                    slot = (unsigned)sl;
+                    if (created) atomicAdd(&counters[0], 1ull);
+                }
+            }
+            entry_slot[e] = slot;
+            entry_idx[e] = (unsigned)e;
+            entry_bary[e] = s.bary[l];
+        }
+    }
+}
+
+// splat phase 2: one thread per site, sequential sum in flat order
+template <int D, class Src>
+__global__ void k_splat_segsum(Src src, int n_runs, const unsigned *run_slot,
+                               const int *run_off, const int *run_cnt,
+                               const unsigned *sorted_idx, const double *entry_bary,
+                               unsigned sentinel, int nv, double *run_vals,
+                               unsigned char *run_live) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_runs) return;
+    if (run_slot[r] == sentinel) { run_live[r] = 0; return; }
+    double acc[15];
+#pragma unroll
+    for (int cc = 0; cc < 15; ++cc) acc[cc] = 0.0;
+    const int beg = run_off[r], cnt = run_cnt[r];
+    constexpr int U = 8;
+    int j = 0;
+    for (; j + U <= cnt; j += U) {
+        unsigned e[U];
+        double b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) e[u] = sorted_idx[beg + j + u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) b[u] = entry_bary[e[u]];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            long long p = e[u] / (D + 1);
+            for (int cc = 0; cc < nv; ++cc)
+                acc[cc] = __dadd_rn(acc[cc], __dmul_rn(b[u], src.value(p, cc)));
+        }
+    }
+    for (; j < cnt; ++j) {
+        unsigned e = sorted_idx[beg + j];
+        double b = entry_bary[e];
+        long long p = e / (D + 1);
+        for (int cc = 0; cc < nv; ++cc) acc[cc] = __dadd_rn(acc[cc], __dmul_rn(b, src.value(p, cc)));
+    }
+    bool live = false;
+    for (int cc = 0; cc < nv; ++cc) {
+        run_vals[(long long)r * nv + cc] = acc[cc];
+        live |= acc[cc] != 0.0;
+    }
+    run_live[r] = live;
+}
+
+template <int D>
+__global__ void k_fill_sites(int S, const int *live_runs, const unsigned *run_slot,
+                             const unsigned long long *hkeys, const double *run_vals, int nv,
+                             int *site_keys, double *vals) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    int r = live_runs[i];
+    int k[D + 1];
+    unpack_key<D>(hkeys[run_slot[r]], k);
+#pragma unroll
+    for (int q = 0; q <= D; ++q) site_keys[(long long)i * (D + 1) + q] = k[q];
+    for (int cc = 0; cc < nv; ++cc) vals[(long long)i * nv + cc] = run_vals[(long long)r * nv + cc];
+}
+
+template <int D>
+__global__ void k_hash_sites(long long S, const int *site_keys, BuildHash h,
+                             unsigned long long *counters) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    int created;
+    int sl = hash_insert(h, pack_key<D>(site_keys + i * (D + 1)), &created);
+    if (sl < 0) { atomicOr(&counters[2], 2ull); return; }
+    h.site[sl] = (int)i;
+}
+
+__global__ void k_count_nonzero(long long S, const double *vals, int nv,
+                                unsigned long long *counter) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool nz = false;
+    if (i < S)
+        for (int c = 0; c < nv; ++c) nz |= vals[i * nv + c] != 0.0;
+    unsigned ballot = __ballot_sync(0xffffffffu, nz);
+    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(counter, (unsigned long long)__popc(ballot));
+}
+
+__global__ void k_nonzero_flags(long long S, const double *vals, int nv, unsigned char *flags) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    bool nz = false;
+    for (int c = 0; c < nv; ++c) nz |= vals[i * nv + c] != 0.0;
+    flags[i] = nz;
+}
+
+// blur: materialise the +-1 neighbours along `axis` of every non-zero site
+template <int D>
+__global__ void k_extend(long long S, int axis, const double *vals, int nv, BuildHash h,
+                         int *site_keys, unsigned long long *counters) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    bool nz = false;
+    for (int c = 0; c < nv; ++c) nz |= vals[i * nv + c] != 0.0;
+    if (!nz) return;
+    int k[D + 1];
+#pragma unroll
+    for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
+#pragma unroll
+    for (int sgn = -1; sgn <= 1; sgn += 2) {
+        int nk[D + 1];
+#pragma unroll
+        for (int q = 0; q <= D; ++q) nk[q] = k[q] + sgn;
+        nk[axis] -= sgn * (D + 1);
+        bool ok = true;
+#pragma unroll
+        for (int q = 0; q < D; ++q) ok &= (nk[q] > -kKeyLim) && (nk[q] < kKeyLim);
+        if (!ok) { atomicOr(&counters[2], 1ull); continue; }
+        int created;
+        int sl = hash_insert(h, pack_key<D>(nk), &created);
+        if (sl < 0) { atomicOr(&counters[2], 2ull); continue; }
+        if (created) {
+            long long id = (long long)atomicAdd(&counters[0], 1ull);
+            h.site[sl] = (int)id;
+#pragma unroll
+            for (int q = 0; q <= D; ++q) site_keys[id * (D + 1) + q] = nk[q];
+        }
+    }
+}
+
+// blur: one Jacobi [1,2,1]/4 pass, 0.5*v + 0.25*(v_up + v_dn) (permutohedral.py:314-322)
+template <int D>
+__global__ void k_jacobi(long long S, int axis, const int *site_keys, const double *vin,
+                         double *vout, int nv, BuildHash h) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    int k[D + 1], up[D + 1], dn[D + 1];
+#pragma unroll
+    for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
+#pragma unroll
+    for (int q = 0; q <= D; ++q) { up[q] = k[q] + 1; dn[q] = k[q] - 1; }
+    up[axis] = k[axis] - D;
+    dn[axis] = k[axis] + D;
+    int iu = hash_find(h, pack_key<D>(up));
+    int id = hash_find(h, pack_key<D>(dn));
+    for (int c = 0; c < nv; ++c) {
+        double vu = iu >= 0 ? vin[(long long)iu * nv + c] : 0.0;
+        double vd = id >= 0 ? vin[(long long)id * nv + c] : 0.0;
+        vout[i * nv + c] = __dadd_rn(__dmul_rn(0.5, vin[i * nv + c]),
+                                     __dmul_rn(0.25, __dadd_rn(vu, vd)));
+    }
+}
+
+template <int D>
+__global__ void k_gather_sites(int S, const int *idx, const int *kin, const double *vin,
+                               int nv, int *kout, double *vout) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    int j = idx[i];
+#pragma unroll
+    for (int q = 0; q <= D; ++q) kout[(long long)i * (D + 1) + q] = kin[(long long)j * (D + 1) + q];
+    for (int c = 0; c < nv; ++c) vout[(long long)i * nv + c] = vin[(long long)j * nv + c];
+}
+
+template <int D, int VP>
+__global__ void k_slice_insert(long long S, const int *site_keys, const double *vals, int nv,
+                               SliceSlot<VP> *tab, unsigned mask, unsigned long long *counters) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    unsigned long long key = pack_key<D>(site_keys + i * (D + 1));
+    unsigned s = (unsigned)mix64(key) & mask;
+    for (unsigned it = 0; it <= mask; ++it) {
+        unsigned long long prev = atomicCAS(&tab[s].key, kEmptyKey, key);
+        if (prev == kEmptyKey) {
+#pragma unroll
+            for (int c = 0; c < VP; ++c) tab[s].v[c] = c < nv ? vals[i * nv + c] : 0.0;
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+    atomicOr(&counters[2], 2ull);
+}
+
+// generic slice (permutohedral.py:329-341): gain * sum_l bary_l * value(key_l)
+template <int D, int VP>
+__global__ void k_slice_generic(const double *Q, long long m, LatticeConsts c,
+                                const SliceSlot<VP> *tab, unsigned mask, int nv, double *out) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
+        double f[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) f[j] = Q[p * D + j];
+        Simplex<D> s;
+        simplex_exact<D>(f, c, s);
+        double acc[VP];
+#pragma unroll
+        for (int q = 0; q < VP; ++q) acc[q] = 0.0;
+        if (!s.overflow) {
+#pragma unroll
+            for (int l = 0; l <= D; ++l) {
+                const SliceSlot<VP> *hit = probe<VP>(tab, mask, s.packed(l));
+                double b = s.bary[l];
+                if (hit) {
+#pragma unroll
+                    for (int q = 0; q < VP; ++q)
+                        acc[q] = __dadd_rn(acc[q], __dmul_rn(b, hit->v[q]));
+                }
+            }
+        }
+        for (int q = 0; q < nv; ++q) out[p * nv + q] = __dmul_rn(c.gain, acc[q]);
+    }
+}
+
+template <int D>
+__global__ void k_simplex(const double *F, long long n, LatticeConsts c, int *keys, double *bary,
+                          unsigned long long *flag) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    double f[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) f[j] = F[p * D + j];
+    Simplex<D> s;
+    simplex_exact<D>(f, c, s);
+    if (s.overflow) atomicOr(flag, 1ull);
+#pragma unroll
+    for (int l = 0; l <= D; ++l) {
+        int k[D + 1];
+        s.vertex(l, k);
+#pragma unroll
+        for (int q = 0; q <= D; ++q) keys[(p * (D + 1) + l) * (D + 1) + q] = k[q];
+        bary[p * (D + 1) + l] = s.bary[l];
+    }
+}
+
+// exact Gaussian transform (permutohedral.py:64-86), inputs staged in smem
+constexpr int kBfTile = 128;
+__global__ void k_bruteforce(const double *Q, long long m, const double *F, long long n, int d,
+                             const double *V, int nv, LatticeConsts c, double *out) {
+    extern __shared__ double sm[];
+    double *sF = sm;                        // kBfTile x d
+    double *sV = sm + kBfTile * d;          // kBfTile x nv
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double q[kMaxDim];
+    for (int j = 0; j < d; ++j) q[j] = p < m ? __ddiv_rn(Q[p * d + j], c.sigma[j]) : 0.0;
+    double acc[16];
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    for (long long base = 0; base < n; base += kBfTile) {
+        int cnt = (int)min((long long)kBfTile, n - base);
+        __syncthreads();
+        for (int t = threadIdx.x; t < cnt * d; t += blockDim.x) {
+            int r = t / d, j = t % d;
+            sF[t] = __ddiv_rn(F[(base + r) * d + j], c.sigma[j]);
+        }
+        for (int t = threadIdx.x; t < cnt * nv; t += blockDim.x) sV[t] = V[base * nv + t];
+        __syncthreads();
+        if (p < m) {
+            for (int r = 0; r < cnt; ++r) {
+                double d2 = 0.0;
+                for (int j = 0; j < d; ++j) {
+                    double df = q[j] - sF[r * d + j];
+                    d2 += df * df;
+                }
+                double kv = exp(-0.5 * d2);
+                for (int k = 0; k < nv; ++k) acc[k] += kv * sV[r * nv + k];
+            }
+        }
+    }
+    if (p < m)
+        for (int k = 0; k < nv; ++k) out[p * nv + k] = acc[k];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static inline unsigned grid_for(long long n, int block = 256) {
+    long long g = (n + block - 1) / block;
+    return (unsigned)std::max<long long>(1, std::min<long long>(g, 1LL << 30));
+}
+
+struct Scratch {
+    cudaStream_t s;
+    std::vector<void *> bufs;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    ~Scratch() {
+        for (void *p : bufs) cudaFreeAsync(p, s);
+    }
+    template <class T>
+    int get(T **out, size_t count) {
+        void *p = nullptr;
+        cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), s);
+        if (e != cudaSuccess) {
+            set_error("device allocation of %zu bytes failed: %s", count * sizeof(T),
+                      cudaGetErrorString(e));
+            return FR_ECUDA;
+        }
+        bufs.push_back(p);
+        *out = (T *)p;
+        return FR_OK;
+    }
+};
+
+static int read_counters(fr_lattice *lat, cudaStream_t s, unsigned long long *h) {
+    FR_CUDA(cudaMemcpyAsync(h, lat->d_counters, 3 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    if (h[2] & 1ull) {
+        set_error("lattice coordinate outside the packable range (|key| >= %lld); "
+                  "features / sigma too large", (long long)kKeyLim);
+        return FR_ECAPACITY;
+    }
+    return FR_OK;
+}
+
+static void free_build(fr_lattice *lat) {
+    cudaFree(lat->site_keys);
+    cudaFree(lat->vals);
+    cudaFree(lat->vals_alt);
+    cudaFree(lat->hkeys);
+    cudaFree(lat->hsite);
+    lat->site_keys = nullptr;
+    lat->vals = lat->vals_alt = nullptr;
+    lat->hkeys = nullptr;
+    lat->hsite = nullptr;
+    lat->hmask = 0;
+}
+
+static int alloc_hash(fr_lattice *lat, unsigned cap, cudaStream_t s) {
+    cudaFree(lat->hkeys);
+    cudaFree(lat->hsite);
+    lat->hkeys = nullptr;
+    lat->hsite = nullptr;
+    FR_CUDA(cudaMalloc(&lat->hkeys, (size_t)cap * sizeof(unsigned long long)));
+    FR_CUDA(cudaMalloc(&lat->hsite, (size_t)cap * sizeof(int)));
+    FR_CUDA(cudaMemsetAsync(lat->hkeys, 0xff, (size_t)cap * sizeof(unsigned long long), s));
+    FR_CUDA(cudaMemsetAsync(lat->hsite, 0xff, (size_t)cap * sizeof(int), s));
+    lat->hmask = cap - 1;
+    return FR_OK;
+}
+
+template <int D>
+static int rehash_sites(fr_lattice *lat, unsigned cap, cudaStream_t s) {
+    FR_TRY(alloc_hash(lat, cap, s));
+    FR_CUDA(cudaMemsetAsync(lat->d_counters + 2, 0, sizeof(unsigned long long), s));
+    if (lat->n_sites > 0) {
+        k_hash_sites<D><<<grid_for(lat->n_sites), 256, 0, s>>>(
+            lat->n_sites, lat->site_keys, BuildHash{lat->hkeys, lat->hsite, lat->hmask},
+            lat->d_counters);
+        FR_CHECK_LAUNCH();
+    }
+    return FR_OK;
+}
+
+// grow the site arrays to hold `need` sites, preserving the first n_sites rows
+static int reserve_sites(fr_lattice *lat, long long need, cudaStream_t s) {
+    if (need <= lat->site_cap) return FR_OK;
+    long long cap = std::max<long long>(need, lat->site_cap * 2);
+    const int D1 = lat->dim + 1, nv = lat->nv;
+    int *nk = nullptr;
+    double *nvals = nullptr, *nalt = nullptr;
+    FR_CUDA(cudaMalloc(&nk, (size_t)cap * D1 * sizeof(int)));
+    FR_CUDA(cudaMalloc(&nvals, (size_t)cap * nv * sizeof(double)));
+    FR_CUDA(cudaMalloc(&nalt, (size_t)cap * nv * sizeof(double)));
+    if (lat->n_sites > 0) {
+        FR_CUDA(cudaMemcpyAsync(nk, lat->site_keys, (size_t)lat->n_sites * D1 * sizeof(int),
+                                cudaMemcpyDeviceToDevice, s));
+        FR_CUDA(cudaMemcpyAsync(nvals, lat->vals, (size_t)lat->n_sites * nv * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+    }
+    FR_CUDA(cudaStreamSynchronize(s));
+    cudaFree(lat->site_keys);
+    cudaFree(lat->vals);
+    cudaFree(lat->vals_alt);
+    lat->site_keys = nk;
+    lat->vals = nvals;
+    lat->vals_alt = nalt;
+    lat->site_cap = cap;
+    return FR_OK;
+}
+
+template <int D, class Src>
+static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cudaStream_t s) {
+    if (lat->blurred || lat->splatted) {
+        // the reference allows re-splatting an unblurred lattice (it replaces the table)
+    }
+    if (nv < 1 || nv > 15) {
+        set_error("value width %d unsupported (1..15 columns per lattice)", nv);
+        return FR_EINVAL;
+    }
+    free_build(lat);
+    cudaFree(lat->slots);
+    lat->slots = nullptr;
+    lat->nv = nv;
+    lat->n_sites = 0;
+    lat->site_cap = 0;
+    lat->blurred = 0;
+    lat->splatted = 1;
+    if (n == 0) return reserve_sites(lat, 1, s);
+    const long long E = n * (D + 1);
+    if (E >= (1LL << 31) - 1) {
+        set_error("too many points for one splat (%lld)", n);
+        return FR_EINVAL;
+    }
+    Scratch sc(s);
+    unsigned *entry_slot, *entry_idx, *sorted_slot, *sorted_idx;
+    double *entry_bary;
+    FR_TRY(sc.get(&entry_slot, E));
+    FR_TRY(sc.get(&entry_idx, E));
+    FR_TRY(sc.get(&sorted_slot, E));
+    FR_TRY(sc.get(&sorted_idx, E));
+    FR_TRY(sc.get(&entry_bary, E));
+    // hash sized for the unique-key count; grown x4 on overflow
+    unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
+    unsigned long long hc[3];
+    for (;;) {
+        FR_TRY(alloc_hash(lat, (unsigned)cap, s));
+        FR_CUDA(cudaMemsetAsync(lat->d_counters, 0, 3 * sizeof(unsigned long long), s));
+        BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
+        k_splat_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, n, lat->c, h, (unsigned)cap,
+                                                            entry_slot, entry_idx, entry_bary,
+                                                            lat->d_counters);
+        FR_CHECK_LAUNCH();
+        FR_TRY(read_counters(lat, s, hc));
+        bool full = (hc[2] & 2ull) || hc[0] * 2 > cap;
+        if (!full) break;
+        if (cap >= (1ull << 31)) {
+            set_error("splat hash table exceeded 2^31 slots");
+            return FR_ECAPACITY;
+        }
+        cap *= 4;
+    }
+    const int end_bit = 1 + (int)std::log2((double)cap);
+    // stable radix sort of entries by slot: per-site groups in flat order
+    size_t tmp_bytes = 0, t2 = 0;
+    FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, entry_slot, sorted_slot,
+                                            entry_idx, sorted_idx, (int)E, 0, end_bit, s));
+    unsigned *run_slot;
+    int *run_cnt, *run_off, *d_nruns;
+    FR_TRY(sc.get(&run_slot, E));
+    FR_TRY(sc.get(&run_cnt, E));
+    FR_TRY(sc.get(&run_off, E));
+    FR_TRY(sc.get(&d_nruns, 1));
+    FR_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, sorted_slot, run_slot, run_cnt,
+                                               d_nruns, (int)E, s));
+    tmp_bytes = std::max(tmp_bytes, t2);
+    FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_cnt, run_off, (int)E, s));
+    tmp_bytes = std::max(tmp_bytes, t2);
+    void *tmp;
+    FR_TRY(sc.get((char **)&tmp, tmp_bytes));
+    FR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, entry_slot, sorted_slot, entry_idx,
+                                            sorted_idx, (int)E, 0, end_bit, s));
+    FR_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tmp_bytes, sorted_slot, run_slot, run_cnt,
+                                               d_nruns, (int)E, s));
+    int nruns = 0;
+    FR_CUDA(cudaMemcpyAsync(&nruns, d_nruns, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, run_cnt, run_off, nruns, s));
+    double *run_vals;
+    unsigned char *run_live;
+    int *live_runs, *iota, *d_nlive;
+    FR_TRY(sc.get(&run_vals, (size_t)nruns * nv));
+    FR_TRY(sc.get(&run_live, nruns));
+    FR_TRY(sc.get(&live_runs, nruns));
+    FR_TRY(sc.get(&iota, nruns));
+    FR_TRY(sc.get(&d_nlive, 1));
+    k_splat_segsum<D, Src><<<grid_for(nruns, 128), 128, 0, s>>>(
+        src, nruns, run_slot, run_off, run_cnt, sorted_idx, entry_bary, (unsigned)cap, nv,
+        run_vals, run_live);
+    FR_CHECK_LAUNCH();
+    // live runs -> dense site rows
+    {
+        std::vector<int> h_iota(nruns);
+        for (int i = 0; i < nruns; ++i) h_iota[i] = i;
+        FR_CUDA(cudaMemcpyAsync(iota, h_iota.data(), nruns * sizeof(int),
+                                cudaMemcpyHostToDevice, s));
+        size_t t3 = 0;
+        FR_CUDA(cub::DeviceSelect::Flagged(nullptr, t3, iota, run_live, live_runs, d_nlive,
+                                           nruns, s));
+        void *tmp3;
+        FR_TRY(sc.get((char **)&tmp3, t3));
+        FR_CUDA(cub::DeviceSelect::Flagged(tmp3, t3, iota, run_live, live_runs, d_nlive, nruns,
+                                           s));
+        int S = 0;
+        FR_CUDA(cudaMemcpyAsync(&S, d_nlive, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FR_CUDA(cudaStreamSynchronize(s));
+        unsigned long long *old_keys = lat->hkeys;
+        lat->hkeys = nullptr;   // keep the splat hash alive for k_fill_sites
+        FR_TRY(reserve_sites(lat, std::max(S, 1), s));
+        if (S > 0) {
+            k_fill_sites<D><<<grid_for(S), 256, 0, s>>>(S, live_runs, run_slot, old_keys,
+                                                        run_vals, nv, lat->site_keys, lat->vals);
+            FR_CHECK_LAUNCH();
+        }
+        FR_CUDA(cudaStreamSynchronize(s));
+        cudaFree(old_keys);
+        lat->n_sites = S;
+    }
+    FR_TRY(rehash_sites<D>(lat, next_pow2(2ull * (unsigned long long)lat->n_sites), s));
+    FR_TRY(read_counters(lat, s, hc));
+    return FR_OK;
+}
+
+template <int D>
+static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
+    long long S = lat->n_sites;
+    if (S == 0) return FR_OK;
+    Scratch sc(s);
+    unsigned char *flags;
+    int *iota, *sel, *d_n;
+    FR_TRY(sc.get(&flags, S));
+    FR_TRY(sc.get(&iota, S));
+    FR_TRY(sc.get(&sel, S));
+    FR_TRY(sc.get(&d_n, 1));
+    k_nonzero_flags<<<grid_for(S), 256, 0, s>>>(S, lat->vals, lat->nv, flags);
+    FR_CHECK_LAUNCH();
+    std::vector<int> h_iota(S);
+    for (long long i = 0; i < S; ++i) h_iota[i] = (int)i;
+    FR_CUDA(cudaMemcpyAsync(iota, h_iota.data(), S * sizeof(int), cudaMemcpyHostToDevice, s));
+    size_t t = 0;
+    FR_CUDA(cub::DeviceSelect::Flagged(nullptr, t, iota, flags, sel, d_n, (int)S, s));
+    void *tmp;
+    FR_TRY(sc.get((char **)&tmp, t));
+    FR_CUDA(cub::DeviceSelect::Flagged(tmp, t, iota, flags, sel, d_n, (int)S, s));
+    int keep = 0;
+    FR_CUDA(cudaMemcpyAsync(&keep, d_n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    if (keep == S) return FR_OK;
+    int *nk;
+    double *nvls;
+    FR_TRY(sc.get(&nk, (size_t)std::max(keep, 1) * (D + 1)));
+    FR_TRY(sc.get(&nvls, (size_t)std::max(keep, 1) * lat->nv));
+    if (keep > 0) {
+        k_gather_sites<D><<<grid_for(keep), 256, 0, s>>>(keep, sel, lat->site_keys, lat->vals,
+                                                         lat->nv, nk, nvls);
+        FR_CHECK_LAUNCH();
+        FR_CUDA(cudaMemcpyAsync(lat->site_keys, nk, (size_t)keep * (D + 1) * sizeof(int),
+                                cudaMemcpyDeviceToDevice, s));
+        FR_CUDA(cudaMemcpyAsync(lat->vals, nvls, (size_t)keep * lat->nv * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+    }
+    FR_CUDA(cudaStreamSynchronize(s));
+    lat->n_sites = keep;
+    return FR_OK;
+}
+
+template <int D, int VP>
+static int build_slice_table(fr_lattice *lat, cudaStream_t s) {
+    cudaFree(lat->slots);
+    lat->slots = nullptr;
+    unsigned cap = next_pow2(2ull * (unsigned long long)std::max<long long>(lat->n_sites, 1));
+    FR_CUDA(cudaMalloc(&lat->slots, (size_t)cap * sizeof(SliceSlot<VP>)));
+    FR_CUDA(cudaMemsetAsync(lat->slots, 0xff, (size_t)cap * sizeof(SliceSlot<VP>), s));
+    lat->smask = cap - 1;
+    lat->vp = VP;
+    FR_CUDA(cudaMemsetAsync(lat->d_counters + 2, 0, sizeof(unsigned long long), s));
+    if (lat->n_sites > 0) {
+        k_slice_insert<D, VP><<<grid_for(lat->n_sites), 256, 0, s>>>(
+            lat->n_sites, lat->site_keys, lat->vals, lat->nv, (SliceSlot<VP> *)lat->slots,
+            lat->smask, lat->d_counters);
+        FR_CHECK_LAUNCH();
+    }
+    unsigned long long hc[3];
+    FR_TRY(read_counters(lat, s, hc));
+    if (hc[2] & 2ull) {
+        set_error("slice table overflow");
+        return FR_ECAPACITY;
+    }
+    return FR_OK;
+}
+
+template <int D>
+static int blur_impl(fr_lattice *lat, cudaStream_t s) {
+    if (!lat->splatted) {
+        set_error("blur requires a splatted lattice");
+        return FR_ESTATE;
+    }
+    if (lat->blurred) {
+        set_error("lattice already blurred");
+        return FR_ESTATE;
+    }
+    const int nv = lat->nv;
+    const long long cap = std::max<long long>(64 * lat->n_sites, 200000);   // permutohedral.py:304
+    unsigned long long hc[3];
+    for (int axis = 0; axis <= D; ++axis) {
+        long long S = lat->n_sites;
+        FR_CUDA(cudaMemsetAsync(lat->d_counters, 0, 3 * sizeof(unsigned long long), s));
+        if (S > 0) {
+            k_count_nonzero<<<grid_for(S), 256, 0, s>>>(S, lat->vals, nv, lat->d_counters + 1);
+            FR_CHECK_LAUNCH();
+        }
+        FR_TRY(read_counters(lat, s, hc));
+        long long nsrc = (long long)hc[1];
+        if (S + 2 * nsrc <= cap && nsrc > 0) {
+            long long need = S + 2 * nsrc;
+            FR_TRY(reserve_sites(lat, need, s));
+            if ((unsigned long long)need * 2 > (unsigned long long)lat->hmask + 1)
+                FR_TRY(rehash_sites<D>(lat, next_pow2(4ull * (unsigned long long)need), s));
+            FR_CUDA(cudaMemsetAsync(lat->vals + S * nv, 0, (size_t)2 * nsrc * nv * sizeof(double), s));
+            unsigned long long init[3] = {(unsigned long long)S, 0ull, 0ull};
+            FR_CUDA(cudaMemcpyAsync(lat->d_counters, init, sizeof(init), cudaMemcpyHostToDevice, s));
+            k_extend<D><<<grid_for(S), 256, 0, s>>>(S, axis, lat->vals, nv,
+                                                    BuildHash{lat->hkeys, lat->hsite, lat->hmask},
+                                                    lat->site_keys, lat->d_counters);
+            FR_CHECK_LAUNCH();
+            FR_TRY(read_counters(lat, s, hc));
+            if (hc[2] & 2ull) {
+                set_error("blur hash table overflow");
+                return FR_ECAPACITY;
+            }
+            lat->n_sites = (long long)hc[0];
+        }
+        S = lat->n_sites;
+        if (S > 0) {
+            k_jacobi<D><<<grid_for(S), 256, 0, s>>>(S, axis, lat->site_keys, lat->vals,
+                                                    lat->vals_alt, nv,
+                                                    BuildHash{lat->hkeys, lat->hsite, lat->hmask});
+            FR_CHECK_LAUNCH();
+            std::swap(lat->vals, lat->vals_alt);
+        }
+    }
+    FR_TRY(compact_nonzero<D>(lat, s));
+    cudaFree(lat->hkeys);
+    cudaFree(lat->hsite);
+    lat->hkeys = nullptr;
+    lat->hsite = nullptr;
+    lat->hmask = 0;
+    int vp = vp_for(nv);
+    if (vp == 3) FR_TRY((build_slice_table<D, 3>(lat, s)));
+    else if (vp == 7) FR_TRY((build_slice_table<D, 7>(lat, s)));
+    else FR_TRY((build_slice_table<D, 15>(lat, s)));
+    lat->blurred = 1;
+    return FR_OK;
+}
+
+template <int D, int VP>
+static int slice_impl(const fr_lattice *lat, const double *Q, long long m, double *out,
+                      cudaStream_t s) {
+    if (m == 0) return FR_OK;
+    unsigned grid = (unsigned)std::min<long long>((m + 255) / 256, 148LL * 16);
+    k_slice_generic<D, VP><<<grid, 256, 0, s>>>(Q, m, lat->c, (const SliceSlot<VP> *)lat->slots,
+                                               lat->smask, lat->nv, out);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+}  // namespace fr
+
+// ===========================================================================
+// C ABI
+
+using namespace fr;
+
+#define FR_DISPATCH_D(dim, CALL)                                               \
+    switch (dim) {                                                             \
+        case 1: { constexpr int D = 1; CALL; } break;                          \
+        case 2: { constexpr int D = 2; CALL; } break;                          \
+        case 3: { constexpr int D = 3; CALL; } break;                          \
+        default: set_error("dimension %d not compiled", dim); return FR_EINVAL; \
+    }
+
+extern "C" {
+
+int fr_abi_version(void) { return 1; }
+
+const char *fr_last_error(void) { return fr::last_error(); }
+
+int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
+    if (!out || !sigma) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    LatticeConsts c;
+    FR_TRY(make_consts(dim, sigma, &c));
+    fr_lattice *lat = new fr_lattice();
+    lat->c = c;
+    lat->dim = dim;
+    if (cudaMalloc(&lat->d_counters, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+        delete lat;
+        set_error("cudaMalloc failed for lattice counters");
+        return FR_ECUDA;
+    }
+    *out = lat;
+    return FR_OK;
+}
+
+int fr_lattice_destroy(fr_lattice *lat) {
+    if (!lat) return FR_OK;
+    free_build(lat);
+    cudaFree(lat->slots);
+    cudaFree(lat->d_counters);
+    delete lat;
+    return FR_OK;
+}
+
+int fr_lattice_splat(fr_lattice *lat, const double *F, const double *V, int64_t n, int nv,
+                     void *stream) {
+    if (!lat || (n > 0 && (!F || !V))) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    GenericSrc src{F, V, nv};
+    FR_DISPATCH_D(lat->dim, FR_TRY((splat_impl<D, GenericSrc>(lat, src, n, nv, s))));
+    return FR_OK;
+}
+
+int fr_lattice_splat_points(fr_lattice *lat, const float *pos, const float *nrm, int64_t n,
+                            int value_mode, void *stream) {
+    if (!lat || (n > 0 && !pos)) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    if (lat->dim != 3) {
+        set_error("point splat needs a 3-D lattice");
+        return FR_EINVAL;
+    }
+    if ((value_mode & FR_VALUES_NORMALS) && !nrm) {
+        set_error("observation cloud has no normals");
+        return FR_EINVAL;
+    }
+    int m2 = (value_mode & FR_VALUES_M2) ? 1 : 0;
+    int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
+    PointSrc src{pos, nrm, n, m2, nv};
+    return splat_impl<3, PointSrc>(lat, src, n, nv, (cudaStream_t)stream);
+}
+
+int fr_lattice_blur(fr_lattice *lat, void *stream) {
+    if (!lat) {
+        set_error("null lattice");
+        return FR_EINVAL;
+    }
+    FR_DISPATCH_D(lat->dim, FR_TRY(blur_impl<D>(lat, (cudaStream_t)stream)));
+    return FR_OK;
+}
+
+int fr_lattice_info(const fr_lattice *lat, int64_t *num_sites, int *nv, int *blurred) {
+    if (!lat) {
+        set_error("null lattice");
+        return FR_EINVAL;
+    }
+    if (num_sites) *num_sites = lat->n_sites;
+    if (nv) *nv = lat->nv;
+    if (blurred) *blurred = lat->blurred;
+    return FR_OK;
+}
+
+int fr_lattice_export(const fr_lattice *lat, int32_t *keys, double *values, void *stream) {
+    if (!lat) {
+        set_error("null lattice");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (lat->n_sites == 0) return FR_OK;
+    if (keys)
+        FR_CUDA(cudaMemcpyAsync(keys, lat->site_keys,
+                                (size_t)lat->n_sites * (lat->dim + 1) * sizeof(int),
+                                cudaMemcpyDeviceToDevice, s));
+    if (values)
+        FR_CUDA(cudaMemcpyAsync(values, lat->vals, (size_t)lat->n_sites * lat->nv * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+    return FR_OK;
+}
+
+int fr_lattice_slice(const fr_lattice *lat, const double *Q, int64_t m, double *out,
+                     void *stream) {
+    if (!lat) {
+        set_error("null lattice");
+        return FR_EINVAL;
+    }
+    if (!lat->blurred) {
+        set_error("slice requires a blurred lattice");
+        return FR_ESTATE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    int dim = lat->dim;
+    switch (lat->vp) {
+        case 3: FR_DISPATCH_D(dim, FR_TRY((slice_impl<D, 3>(lat, Q, m, out, s)))); break;
+        case 7: FR_DISPATCH_D(dim, FR_TRY((slice_impl<D, 7>(lat, Q, m, out, s)))); break;
+        default: FR_DISPATCH_D(dim, FR_TRY((slice_impl<D, 15>(lat, Q, m, out, s)))); break;
+    }
+    return FR_OK;
+}
+
+int fr_simplex(int dim, const double *sigma, const double *F, int64_t n, int32_t *keys,
+               double *bary, void *stream) {
+    LatticeConsts c;
+    FR_TRY(make_consts(dim, sigma, &c));
+    if (n == 0) return FR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *flag = nullptr;
+    FR_CUDA(cudaMallocAsync(&flag, sizeof(unsigned long long), s));
+    FR_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned long long), s));
+    FR_DISPATCH_D(dim, (k_simplex<D><<<grid_for(n), 256, 0, s>>>(F, n, c, keys, bary, flag)));
+    unsigned long long h = 0;
+    FR_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaFreeAsync(flag, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    FR_CHECK_LAUNCH();
+    if (h) {
+        set_error("lattice coordinate outside the packable range");
+        return FR_ECAPACITY;
+    }
+    return FR_OK;
+}
+
+int fr_gauss_bruteforce(const double *Q, int64_t m, const double *F, int64_t n, int dim,
+                        const double *V, int nv, const double *sigma, double *out,
+                        void *stream) {
+    if (dim < 1 || dim > kMaxDim || nv < 1 || nv > 16) {
+        set_error("bruteforce supports dim 1..12 and 1..16 value columns");
+        return FR_EINVAL;
+    }
+    LatticeConsts c;
+    memset(&c, 0, sizeof(c));
+    for (int j = 0; j < dim; ++j) {
+        if (!std::isfinite(sigma[j]) || !(sigma[j] > 0)) {
+            set_error("kernel widths must be finite and positive");
+            return FR_EINVAL;
+        }
+        c.sigma[j] = sigma[j];
+    }
+    if (m == 0) return FR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t smem = (size_t)kBfTile * (dim + nv) * sizeof(double);
+    k_bruteforce<<<grid_for(m, 128), 128, smem, s>>>(Q, m, F, n, dim, V, nv, c, out);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+}  // extern "C"

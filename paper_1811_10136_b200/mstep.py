@@ -1,0 +1,279 @@
+"""Weighted Gauss-Newton over twist-parameterised kinematics (drop-in for
+mstep.py, pkg/src/twistreg/mstep.py:1-459).
+
+The per-point work (residual rows, J^T J / J^T r reductions, objectives) runs
+in device kernels; the (6+DOF)^2 solves with the reference's damping
+escalation stay float64 on the host (they are microseconds).  Inside
+`register` the rigid M step never re-reads the points: the fused EM pass
+returns sufficient statistics from which assembly, step halving and extra GN
+iterations follow in closed form (see _rigid.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse
+import scipy.sparse.linalg
+
+from . import _lib
+from .errors import SolverError
+from .geometry import PointCloud, point_twist_jacobian
+from .kinematics import RigidModel, forward_points
+
+RESIDUAL_MODES = ("point_to_point", "point_to_plane")
+_DENSE_SOLVE_MAX = 360
+
+
+@dataclass(frozen=True)
+class ResidualSpec:
+    """Per-point correspondence residuals for one M step (mstep.py:39-84)."""
+
+    weights: np.ndarray
+    targets: np.ndarray
+    sigma_inv: np.ndarray
+    mode: str = "point_to_point"
+    normals: np.ndarray | None = None
+    normal_valid: np.ndarray | None = None
+
+    def __post_init__(self):
+        w = np.asarray(self.weights, dtype=float).reshape(-1)
+        t = np.asarray(self.targets, dtype=float)
+        if t.shape != (len(w), 3):
+            raise ValueError(f"targets must be ({len(w)}, 3), got {t.shape}")
+        if np.any(w < 0) or np.any(w > 1) or not np.all(np.isfinite(w)):
+            raise ValueError("weights must lie in [0, 1]")
+        if not np.all(np.isfinite(t)):
+            raise ValueError("non-finite targets")
+        s = np.atleast_1d(np.asarray(self.sigma_inv, dtype=float))
+        if s.size == 1:
+            s = np.full(3, s[0])
+        if s.shape != (3,) or np.any(s <= 0) or not np.all(np.isfinite(s)):
+            raise ValueError("sigma_inv must be a positive scalar or 3-vector")
+        if self.mode not in RESIDUAL_MODES:
+            raise ValueError(f"unknown residual mode {self.mode!r}")
+        object.__setattr__(self, "weights", w)
+        object.__setattr__(self, "targets", t)
+        object.__setattr__(self, "sigma_inv", s)
+        if self.mode == "point_to_plane":
+            if self.normals is None:
+                raise ValueError("point-to-plane residuals need normals")
+            n = np.asarray(self.normals, dtype=float)
+            if n.shape != t.shape:
+                raise ValueError("normals must match targets")
+            valid = (np.ones(len(w), dtype=bool) if self.normal_valid is None
+                     else np.asarray(self.normal_valid, dtype=bool).reshape(len(w)))
+            lengths = np.linalg.norm(n[valid], axis=1)
+            if len(lengths) and np.max(np.abs(lengths - 1.0)) > 1e-6:
+                raise ValueError("normals must be unit length where valid")
+            object.__setattr__(self, "normals", n)
+            object.__setattr__(self, "normal_valid", valid)
+
+    def __len__(self) -> int:
+        return len(self.weights)
+
+
+def residuals_from_moments(moments, sigma, mode: str = "point_to_point") -> ResidualSpec:
+    """mstep.py:87-99"""
+    s = np.atleast_1d(np.asarray(sigma, dtype=float))
+    if s.size == 1:
+        s = np.full(3, s[0])
+    normals = valid = None
+    if mode == "point_to_plane":
+        if moments.normal is None:
+            raise ValueError("moments were computed without the normal channel")
+        normals, valid = moments.normal, moments.normal_valid
+    return ResidualSpec(moments.weight, moments.target, 1.0 / s, mode, normals, valid)
+
+
+@dataclass
+class NormalEquations:
+    """Dense or 6x6-block-sparse A and b (mstep.py:154-176)."""
+
+    n_params: int
+    b: np.ndarray
+    A: np.ndarray | None = None
+    blocks: dict | None = None
+
+    def to_dense(self) -> np.ndarray:
+        if self.A is not None:
+            return self.A
+        full = np.zeros((self.n_params, self.n_params))
+        for (k, l), blk in self.blocks.items():
+            full[6 * k:6 * k + 6, 6 * l:6 * l + 6] += blk
+            if k != l:
+                full[6 * l:6 * l + 6, 6 * k:6 * k + 6] += blk.T
+        return full
+
+    def trace(self) -> float:
+        if self.A is not None:
+            return float(np.trace(self.A))
+        return float(sum(np.trace(b) for (k, l), b in self.blocks.items() if k == l))
+
+
+def _device_rigid_sums(spec: ResidualSpec, x) -> np.ndarray:
+    """fr_assemble_rigid over an explicit spec: [H upper 21 | g 6 | sum r^2]."""
+    import torch
+    from .permutohedral import _to_device
+    lib = _lib.load()
+    m = len(spec)
+    dev = _lib.device()
+    sums = torch.empty(28, dtype=torch.float64, device=dev)
+    scratch = torch.empty(lib.fr_rigid_scratch_doubles(0, 0, m), dtype=torch.float64, device=dev)
+    dX = _to_device(np.asarray(x, dtype=float))
+    dW = _to_device(spec.weights)
+    dT = _to_device(spec.targets)
+    pl = spec.mode == "point_to_plane"
+    dN = _to_device(spec.normals) if pl else None
+    dV = _to_device(spec.normal_valid, np.uint8) if pl else None
+    si, _keep = _lib.dptr(spec.sigma_inv)
+    _lib.check(lib.fr_assemble_rigid(_lib.ptr(dX), _lib.ptr(dW), _lib.ptr(dT), m, si,
+                                     int(pl), _lib.ptr(dN), _lib.ptr(dV), _lib.ptr(sums),
+                                     _lib.ptr(scratch), _lib.stream_handle()))
+    return sums.cpu().numpy()
+
+
+def objective(spec: ResidualSpec, current_positions) -> float:
+    """E = 1/2 sum ||r||^2 (mstep.py:132-138), on the device."""
+    x = np.asarray(current_positions, dtype=float)
+    if len(x) != len(spec):
+        raise ValueError("residual count does not match point count")
+    return 0.5 * float(_device_rigid_sums(spec, x)[27])
+
+
+def assemble_rigid(spec: ResidualSpec, current_positions) -> NormalEquations:
+    """mstep.py:205-210, reduction on the device."""
+    from ._rigid import unpack_upper6
+    x = np.asarray(current_positions, dtype=float)
+    if len(x) != len(spec):
+        raise ValueError("residual count does not match point count")
+    s = _device_rigid_sums(spec, x)
+    return NormalEquations(6, b=s[21:27].copy(), A=unpack_upper6(s[:21]))
+
+
+def _factor_solve(eq: NormalEquations, lam: float, method: str) -> np.ndarray:
+    """mstep.py:317-345"""
+    sparse = method == "sparse" or (method == "auto" and eq.A is None
+                                    and eq.n_params > _DENSE_SOLVE_MAX)
+    if sparse and eq.blocks is not None:
+        rows, cols, vals = [], [], []
+        rr, cc = np.meshgrid(np.arange(6), np.arange(6), indexing="ij")
+        for (k, l), blk in eq.blocks.items():
+            rows.append((6 * k + rr).ravel())
+            cols.append((6 * l + cc).ravel())
+            vals.append(blk.ravel())
+            if k != l:
+                rows.append((6 * l + rr).ravel())
+                cols.append((6 * k + cc).ravel())
+                vals.append(blk.T.ravel())
+        rows.append(np.arange(eq.n_params))
+        cols.append(np.arange(eq.n_params))
+        vals.append(np.full(eq.n_params, lam))
+        A = scipy.sparse.csc_matrix((np.concatenate(vals), (np.concatenate(rows),
+                                                           np.concatenate(cols))),
+                                    shape=(eq.n_params, eq.n_params))
+        sol = scipy.sparse.linalg.splu(A).solve(eq.b)
+        if not np.all(np.isfinite(sol)):
+            raise scipy.linalg.LinAlgError("sparse factorization produced non-finite values")
+        return sol
+    A = eq.to_dense() + lam * np.eye(eq.n_params)
+    return scipy.linalg.cho_solve(scipy.linalg.cho_factor(A), eq.b)
+
+
+def gn_solve(eq: NormalEquations, damping: float | None = None, method: str = "auto",
+             _stats: dict | None = None) -> np.ndarray:
+    """(A + lam I) step = -b with tenfold escalation (mstep.py:348-369)."""
+    if method not in ("auto", "dense", "sparse"):
+        raise ValueError(f"unknown solve method {method!r}")
+    if not np.any(eq.b):
+        if _stats is not None:
+            _stats.update(damping=0.0, attempts=0)
+        return np.zeros(eq.n_params)
+    tr = eq.trace()
+    lam = damping if damping is not None else 1e-6 * tr / eq.n_params
+    for attempt in range(6):
+        try:
+            sol = _factor_solve(eq, lam, method)
+        except (scipy.linalg.LinAlgError, RuntimeError):
+            lam = lam * 10.0 if lam > 0 else max(tr / eq.n_params, 1.0) * 1e-10
+            continue
+        if _stats is not None:
+            _stats.update(damping=lam, attempts=attempt + 1)
+        return -sol
+    raise SolverError(f"normal equations not factorizable after damping escalation "
+                      f"(final damping {lam:.3e})")
+
+
+@dataclass(frozen=True)
+class MStepOptions:
+    """mstep.py:372-379"""
+
+    max_gn_iters: int = 1
+    damping: float | None = None
+    max_halvings: int = 10
+    step_tolerance: float = 0.0
+    lambda_reg: float = 0.0
+    solve_method: str = "auto"
+
+
+@dataclass
+class MStepDiagnostics:
+    objectives: list = field(default_factory=list)
+    step_norms: list = field(default_factory=list)
+    halvings: list = field(default_factory=list)
+    dampings: list = field(default_factory=list)
+
+
+def _accepts(cand: float, value: float) -> bool:
+    """Non-increase test of mstep.py:446."""
+    return cand <= value * (1.0 + 1e-12) + 1e-300
+
+
+def m_step(spec: ResidualSpec, reference: PointCloud, model, options: MStepOptions | None = None):
+    """Damped GN with step halving over an explicit spec (mstep.py:421-459).
+
+    Rigid models run every point reduction on the device; articulated and
+    node-graph models are dispatched by their own modules.
+    """
+    opts = options if options is not None else MStepOptions()
+    if not isinstance(model, RigidModel):
+        from . import kinematics
+        return kinematics.m_step_model(spec, reference, model, opts)
+    current = model
+    value = objective(spec, forward_points(reference, current).positions)
+    diag = MStepDiagnostics(objectives=[value])
+    for _ in range(opts.max_gn_iters):
+        x = forward_points(reference, current).positions
+        eq = assemble_rigid(spec, x)
+        if not np.any(eq.b):
+            break
+        stats: dict = {}
+        step = gn_solve(eq, opts.damping, opts.solve_method, _stats=stats)
+        diag.dampings.append(stats.get("damping", 0.0))
+        scale = 1.0
+        accepted = None
+        for halving in range(opts.max_halvings + 1):
+            cand = current.updated(scale * step)
+            cv = objective(spec, forward_points(reference, cand).positions)
+            if _accepts(cv, value):
+                accepted = (cand, cv, halving)
+                break
+            scale *= 0.5
+        if accepted is None:
+            break
+        current, value, halvings = accepted
+        diag.objectives.append(value)
+        diag.halvings.append(halvings)
+        sn = float(np.linalg.norm(scale * step))
+        diag.step_norms.append(sn)
+        if sn <= opts.step_tolerance:
+            break
+    return current, diag
+
+
+__all__ = ["RESIDUAL_MODES", "ResidualSpec", "residuals_from_moments", "NormalEquations",
+           "objective", "assemble_rigid", "gn_solve", "MStepOptions", "MStepDiagnostics",
+           "m_step", "point_twist_jacobian"]

@@ -1,0 +1,253 @@
+"""EM registration driver (drop-in for pipeline.py, pkg/src/twistreg/
+pipeline.py:1-181).
+
+`register` keeps the reference's loop and bookkeeping verbatim in meaning --
+degenerate / converged / max_iters termination, drop-the-last-update on
+convergence, sigma re-estimation with a lattice rebuild, the per-iteration
+objective / twist-norm / inlier-mass / sigma traces and the `timing` keys --
+while each iteration's point work is one fused device pass
+(`_rigid.RigidDevicePath.run_pass`).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._rigid import RigidDevicePath, RigidMoments, unpack_upper6
+from .errors import DegenerateCorrespondenceError
+from .estep import GmmConfig, M0_FLOOR  # noqa: F401  (re-exported constants)
+from .geometry import PointCloud, RigidTransform, rotation_angle
+from .kinematics import RigidModel
+from .mstep import (RESIDUAL_MODES, MStepDiagnostics, MStepOptions, NormalEquations,
+                    _accepts, gn_solve)
+
+DEGENERATE_MASS_FRACTION = 1e-9
+
+
+@dataclass(frozen=True)
+class RegistrationConfig:
+    """pipeline.py:29-47"""
+
+    gmm: GmmConfig = GmmConfig()
+    residual_mode: str = "point_to_point"
+    backend: str = "lattice"
+    max_em_iters: int = 50
+    twist_tolerance: float = 1e-4
+    mstep: MStepOptions = MStepOptions()
+    record_states: bool = False
+
+    def __post_init__(self):
+        if self.residual_mode not in RESIDUAL_MODES:
+            raise ValueError(f"unknown residual mode {self.residual_mode!r}")
+        if self.backend not in ("lattice", "bruteforce"):
+            raise ValueError(f"unknown backend {self.backend!r}")
+        if self.max_em_iters < 1:
+            raise ValueError("max_em_iters must be at least 1")
+        if not self.twist_tolerance > 0:
+            raise ValueError("twist_tolerance must be positive")
+
+
+@dataclass
+class RegistrationResult:
+    """pipeline.py:50-59"""
+
+    kinematics: object
+    iterations: int
+    objectives: list = field(default_factory=list)
+    twist_norms: list = field(default_factory=list)
+    inlier_masses: list = field(default_factory=list)
+    sigmas: list = field(default_factory=list)
+    termination: str = "max_iters"
+    states: list | None = None
+
+
+def default_sigma(observation: PointCloud) -> float:
+    """5% of the observation bounding-box diagonal (pipeline.py:62-65)."""
+    span = observation.positions.max(axis=0) - observation.positions.min(axis=0)
+    return 0.05 * float(np.linalg.norm(span))
+
+
+def _poses(model):
+    if isinstance(model, RigidModel):
+        return [(model.pose.rotation, model.pose.translation)]
+    if hasattr(model, "pose_list"):
+        return model.pose_list()
+    raise TypeError(f"unsupported kinematic model {type(model).__name__}")
+
+
+def update_magnitude(before, after, diameter: float) -> float:
+    """Largest per-body angle + shift / diameter (pipeline.py:79-86)."""
+    worst = 0.0
+    for (Rb, tb), (Ra, ta) in zip(_poses(before), _poses(after)):
+        worst = max(worst, rotation_angle(Ra @ Rb.T) + float(np.linalg.norm(ta - tb)) / diameter)
+    return worst
+
+
+def alignment_error(T: RigidTransform, T_gt: RigidTransform, reference: PointCloud) -> float:
+    """Mean displacement between two poses over the reference (pipeline.py:89-93)."""
+    return float(np.linalg.norm(T.apply(reference.positions) - T_gt.apply(reference.positions),
+                                axis=1).mean())
+
+
+def log_likelihood(model_points, observation: PointCloud, config: GmmConfig,
+                   model_features=None) -> float:
+    """Exact mixture log-likelihood (pipeline.py:96-122); the kernel sums run
+    in the device brute-force transform."""
+    from .permutohedral import gaussian_transform_bruteforce
+    X = np.asarray(model_points, dtype=float)
+    fdim = observation.features.shape[1] if observation.features is not None else 0
+    widths = config.kernel_sigma(fdim)
+    q, src = [], []
+    if config.spatial_in_kernel():
+        q.append(X)
+        src.append(observation.positions)
+    if config.mode != "position":
+        q.append(np.asarray(model_features, dtype=float))
+        src.append(observation.features)
+    m0 = gaussian_transform_bruteforce(np.hstack(q), np.hstack(src),
+                                       np.ones((len(observation), 1)), widths)[:, 0]
+    norm = float(np.prod(1.0 / (np.sqrt(2.0 * np.pi) * widths)))
+    w = config.outlier_ratio
+    inlier = (1.0 - w) / len(observation) * m0 * norm
+    return float(np.sum(np.log(inlier + w / len(X))))
+
+
+def _rigid_m_step(path: RigidDevicePath, sums, R, t, s2, opts: MStepOptions):
+    """One M step of the rigid model from the pass statistics (mstep.py:421-459).
+
+    point_to_point: assembly, objectives of every halving candidate and extra
+    GN iterations in closed form from the sufficient statistics.
+    point_to_plane: candidates evaluated by the device objective pass."""
+    current = RigidModel(RigidTransform(R, t))
+    diag = MStepDiagnostics()
+    p2p = path.mode == 0
+    if p2p:
+        mom = RigidMoments.from_sums(sums)
+        c = path.centre(R, t)
+        value = mom.energy(s2)
+        H, g = mom.normal_equations(c, s2)
+    else:
+        value = 0.5 * float(sums[28])
+        H, g = unpack_upper6(sums[1:22]), np.asarray(sums[22:28], dtype=float)
+        if opts.max_gn_iters > 1:
+            raise NotImplementedError("point_to_plane with max_gn_iters > 1 is not in this build")
+    diag.objectives.append(value)
+    for _ in range(opts.max_gn_iters):
+        if not np.any(g):
+            break
+        stats: dict = {}
+        step = gn_solve(NormalEquations(6, b=g, A=H), opts.damping, opts.solve_method,
+                        _stats=stats)
+        diag.dampings.append(stats.get("damping", 0.0))
+        Rc, tc = current.pose.rotation, current.pose.translation
+        cands = []
+        scale = 1.0
+        for _h in range(opts.max_halvings + 1):
+            cands.append((current.updated(scale * step), scale))
+            scale *= 0.5
+        accepted = None
+        if p2p:
+            for h, (cand, sc) in enumerate(cands):
+                D = cand.pose.rotation @ Rc.T
+                delta = cand.pose.translation - D @ tc
+                cv = value + mom.delta_energy(D, delta, c, s2)
+                if _accepts(cv, value):
+                    accepted = (cand, cv, h, sc, D, delta)
+                    break
+        else:
+            first = path.candidate_objectives([(cands[0][0].pose.rotation,
+                                                cands[0][0].pose.translation)])
+            vals = list(first)
+            if not _accepts(vals[0], value) and len(cands) > 1:
+                rest = cands[1:]
+                for a in range(0, len(rest), 16):
+                    chunk = rest[a:a + 16]
+                    vals += list(path.candidate_objectives(
+                        [(cd.pose.rotation, cd.pose.translation) for cd, _ in chunk]))
+            for h, cv in enumerate(vals):
+                if _accepts(cv, value):
+                    accepted = (cands[h][0], cv, h, cands[h][1], None, None)
+                    break
+        if accepted is None:
+            break
+        cand, value, h, sc, D, delta = accepted
+        diag.objectives.append(value)
+        diag.halvings.append(h)
+        sn = float(np.linalg.norm(sc * step))
+        diag.step_norms.append(sn)
+        current = cand
+        if sn <= opts.step_tolerance:
+            break
+        if p2p:
+            mom = mom.moved(D, delta, c)
+            H, g = mom.normal_equations(c, s2)
+    return current, diag
+
+
+def register(reference: PointCloud, observation: PointCloud, initial_model,
+             config: RegistrationConfig | None = None,
+             timing: dict | None = None) -> RegistrationResult:
+    """Run EM until the update magnitude drops under the twist tolerance
+    (pipeline.py:125-181).  `timing` accumulates wall-clock seconds of the
+    fused E(+assembly) pass (`e_step_s`) and of the solve / halving phase
+    (`m_step_s`)."""
+    config = config if config is not None else RegistrationConfig()
+    if not isinstance(initial_model, RigidModel):
+        raise TypeError(f"unsupported kinematic model {type(initial_model).__name__} "
+                        "(this build registers RigidModel)")
+    if config.backend != "lattice" or config.gmm.mode != "position":
+        raise ValueError("the device EM path runs the lattice backend with position "
+                         "correspondences")
+    path = RigidDevicePath(reference, observation, config.gmm, config.residual_mode)
+    model = initial_model
+    diameter = reference.diameter()
+    sigma_current = path.sigma
+    result = RegistrationResult(kinematics=model, iterations=0,
+                                states=[] if config.record_states else None)
+    n_ref = len(reference)
+    for _ in range(config.max_em_iters):
+        result.iterations += 1
+        tick = time.perf_counter()
+        R, t = model.pose.rotation, model.pose.translation
+        sums = path.run_pass(R, t)
+        if timing is not None:
+            timing["e_step_s"] = timing.get("e_step_s", 0.0) + time.perf_counter() - tick
+        mass = float(sums[0])
+        result.inlier_masses.append(mass)
+        if mass < DEGENERATE_MASS_FRACTION * n_ref:
+            result.objectives.append(float("nan"))
+            result.twist_norms.append(float("nan"))
+            result.termination = "degenerate"
+            break
+        if config.gmm.update_sigma:
+            base = path.width - 2
+            num, den = float(sums[base]), float(sums[base + 1])
+            if den <= 0.0:
+                raise DegenerateCorrespondenceError("no correspondence mass left")
+            sigma_new = max(float(np.sqrt(max(num / (3.0 * den), 0.0))), config.gmm.sigma_floor)
+            if sigma_new != sigma_current[0]:
+                path.build(sigma_new)       # lattice rebuilt for the next E step
+                sigma_current = path.sigma
+            result.sigmas.append(sigma_new)
+        s2 = (1.0 / np.asarray(sigma_current, dtype=float)) ** 2
+        tick = time.perf_counter()
+        candidate, mdiag = _rigid_m_step(path, sums, R, t, s2, config.mstep)
+        if timing is not None:
+            timing["m_step_s"] = timing.get("m_step_s", 0.0) + time.perf_counter() - tick
+        norm = update_magnitude(model, candidate, diameter)
+        result.twist_norms.append(norm)
+        if norm < config.twist_tolerance:
+            result.objectives.append(mdiag.objectives[0])
+            result.termination = "converged"
+            break
+        model = candidate
+        result.objectives.append(mdiag.objectives[-1])
+        if result.states is not None:
+            result.states.append(model)
+    result.kinematics = model
+    if timing is not None:
+        timing["iterations"] = result.iterations
+    return result

@@ -1,0 +1,139 @@
+"""GPU registration parity (north-star bars: final rotation within 1e-4 rad,
+translation within 1e-5 x cloud extent) against the reference's golden EM
+traces and the CPU oracle; determinism; fused-pass statistics vs the oracle's
+per-point assembly."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import filterreg_oracle as O
+
+from .conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False)
+
+
+@pytest.fixture(scope="module")
+def fr():
+    import paper_1811_10136_b200 as fr
+    return fr
+
+
+def run_case(fr, g):
+    cfg = json.loads(str(g["config"]))
+    pl = "N" in g.files
+    reference = fr.PointCloud(g["X"], normals=None)
+    observation = fr.PointCloud(g["Y"], normals=g["N"] if pl else None)
+    config = fr.RegistrationConfig(
+        gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"],
+                         update_sigma=cfg.get("update_sigma", False)),
+        residual_mode="point_to_plane" if pl else "point_to_point",
+        max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"])
+    return fr.register(reference, observation, fr.RigidModel(), config)
+
+
+def assert_pose_parity(R, t, R_ref, t_ref, extent):
+    dR = O.rotation_angle(R @ R_ref.T)
+    dt = float(np.linalg.norm(t - t_ref))
+    assert dR <= 1e-4, f"rotation differs by {dR:.3e} rad"
+    assert dt <= 1e-5 * extent, f"translation differs by {dt:.3e} m (extent {extent:.3f})"
+    return dR, dt
+
+
+@pytest.mark.parametrize("case", ["pt2pt_seed0", "pt2pt_seed1", "pt2pt_seed2", "pt2pl_cuboid",
+                                  "pt2pt_update_sigma"])
+def test_golden_registration(fr, case):
+    g = load("register_" + case)
+    res = run_case(fr, g)
+    extent = O.bbox_diameter(g["X"])
+    assert_pose_parity(res.kinematics.pose.rotation, res.kinematics.pose.translation,
+                       g["R"], g["t"], extent)
+    assert res.termination == str(g["termination"])
+    assert abs(res.iterations - int(g["iterations"])) <= 1
+    n = min(len(res.objectives), len(g["objectives"])) - 1
+    np.testing.assert_allclose(res.objectives[:n], g["objectives"][:n], rtol=1e-5)
+    np.testing.assert_allclose(res.inlier_masses[:n], g["inlier_masses"][:n], rtol=1e-5)
+    if len(g["sigmas"]):
+        np.testing.assert_allclose(res.sigmas[:n], g["sigmas"][:n], rtol=1e-6)
+
+
+def test_bit_identical_reruns(fr):
+    g = load("register_pt2pt_seed0")
+    a = run_case(fr, g)
+    b = run_case(fr, g)
+    assert np.array_equal(a.kinematics.pose.matrix(), b.kinematics.pose.matrix())
+    assert a.objectives == b.objectives
+    assert a.twist_norms == b.twist_norms
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_c1_scale_against_oracle(fr, seed):
+    model, obs, _ = O.pebble_pair(10000, outlier_ratio=0.05, seed=seed)
+    X = model.astype(np.float32).astype(float)
+    Y = obs.astype(np.float32).astype(float)
+    sigma = 0.05 * O.bbox_diameter(X[:10000])
+    tr = O.register_rigid(X, Y, sigma=sigma, outlier_ratio=0.1, max_em_iters=250,
+                          twist_tolerance=2e-4)
+    cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=sigma, outlier_ratio=0.1),
+                                max_em_iters=250, twist_tolerance=2e-4)
+    res = fr.register(fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(), cfg)
+    assert_pose_parity(res.kinematics.pose.rotation, res.kinematics.pose.translation,
+                       tr["R"], tr["t"], O.bbox_diameter(X))
+    assert abs(res.iterations - tr["iterations"]) <= 1
+
+
+def test_fused_pass_statistics(fr):
+    """The device pass's normal equations equal the oracle's per-point assembly
+    on the oracle's own moments at the same pose (1e-4 moments bar)."""
+    from paper_1811_10136_b200._rigid import RigidDevicePath, RigidMoments, unpack_upper6
+    model, obs, _ = O.pebble_pair(20000, outlier_ratio=0.05, seed=5)
+    X = model.astype(np.float32).astype(float)
+    Y = obs.astype(np.float32).astype(float)
+    sigma = 0.05 * O.bbox_diameter(X[:20000])
+    R = O.rotation_about_axis([1.0, 0.2, -0.3], 0.3)
+    t = np.array([0.004, -0.002, 0.001])
+    gmm = fr.GmmConfig(sigma=sigma, outlier_ratio=0.1)
+    path = RigidDevicePath(fr.PointCloud(X), fr.PointCloud(Y), gmm, "point_to_point")
+    sums = path.run_pass(R, t)
+    eng = O.OracleMoments(Y, sigma, 0.1)
+    x = X @ R.T + t
+    mf = eng.moments(x)
+    assert float(sums[0]) == pytest.approx(mf["weight"].sum(), rel=1e-6)
+    mom = RigidMoments.from_sums(sums)
+    s2 = np.full(3, 1.0 / sigma ** 2)
+    H, g = mom.normal_equations(path.centre(R, t), s2)
+    spec = (mf["weight"], mf["target"], np.full(3, 1.0 / sigma), "point_to_point", None, None)
+    Ho, go = O.assemble_rigid(spec, x)
+    np.testing.assert_allclose(H, Ho, rtol=1e-6, atol=1e-6 * np.abs(Ho).max())
+    np.testing.assert_allclose(g, go, rtol=1e-5, atol=1e-5 * np.abs(go).max())
+    assert mom.energy(s2) == pytest.approx(O.rigid_objective(spec, x), rel=1e-6)
+
+
+def test_explicit_assembly_matches_oracle(fr):
+    rng = np.random.default_rng(2)
+    m = 500
+    w = rng.uniform(0.2, 1.0, m)
+    w[rng.random(m) < 0.2] = 0.0
+    tg = rng.uniform(-0.2, 0.2, (m, 3))
+    x = rng.uniform(-0.2, 0.2, (m, 3))
+    sinv = 1.0 / rng.uniform(0.02, 0.1, 3)
+    for mode in ("point_to_point", "point_to_plane"):
+        n = rng.standard_normal((m, 3))
+        n /= np.linalg.norm(n, axis=1, keepdims=True)
+        valid = rng.random(m) > 0.2
+        n[~valid] = 0.0
+        spec = fr.ResidualSpec(w, tg, sinv, mode, n if mode == "point_to_plane" else None,
+                               valid if mode == "point_to_plane" else None)
+        eq = fr.assemble_rigid(spec, x)
+        ospec = (w, tg, sinv, mode, n, valid)
+        Ho, go = O.assemble_rigid(ospec, x)
+        np.testing.assert_allclose(eq.A, Ho, rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(eq.b, go, rtol=1e-10, atol=1e-12)
+        assert fr.objective(spec, x) == pytest.approx(O.rigid_objective(ospec, x), rel=1e-12)
