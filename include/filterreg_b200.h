@@ -147,8 +147,10 @@ typedef struct fr_rigid_pass_params {
     int mode;           /* FR_POINT_TO_POINT / FR_POINT_TO_PLANE */
     int m2_col;         /* value column of |y|^2 or -1 */
     int normal_col;     /* value column of the normal sum or -1 */
-    int reserved;
+    int flags;          /* FR_PASS_FAST: float32 ranks / barycentrics / table rows */
 } fr_rigid_pass_params;
+
+enum { FR_PASS_FAST = 1 };
 
 /* Number of float64 partial sums the pass produces for a mode. */
 int fr_rigid_pass_width(int mode, int with_sigma);
@@ -168,11 +170,60 @@ int fr_rigid_pass(const fr_lattice *lat, const float *d_ref, int64_t m,
 /* Objective of k candidate poses (mstep.py:132-138 at mstep.py:443-449) under
  * the weights/targets/normals stored by the last point_to_plane pass.
  * cand_R: k x 9, cand_c: k x 3 (R_k c_ref + t_k) host doubles; d_out: k
- * float64 values 0.5 * sum r^2.  k <= 16. */
+ * float64 values 0.5 * sum r^2 (d_out must hold 16 doubles).  k <= 16. */
 int fr_rigid_objective(const float *d_ref, const float *d_wtn, int64_t m,
                        const double *c_ref, int k, const double *cand_R,
                        const double *cand_c, double *d_out, double *d_scratch,
                        void *stream);
+
+/* ---- device-resident rigid EM loop (pipeline.py:141-181, point_to_point) --
+ * The whole EM iteration stays on the GPU: fused pass, fixed-order reduction,
+ * and a one-thread float64 solver kernel that assembles the normal equations
+ * from the pass statistics, solves with the reference's damping escalation,
+ * halves steps with closed-form candidate objectives, applies the twist
+ * update, records objective / twist norm / inlier mass and sets the
+ * termination flag.  Iterations replay a captured CUDA graph; iterations
+ * enqueued after termination are no-ops.  For a sharded run, call
+ * fr_rigid_em_pass, all-reduce the fr_rigid_em_sums buffer, then
+ * fr_rigid_em_solve, in the same stream order on every rank. */
+typedef struct fr_rigid_em fr_rigid_em;
+
+typedef struct fr_rigid_em_config {
+    double R0[9];            /* initial pose */
+    double t0[3];
+    double c_ref[3];         /* centre of the whole reference cloud */
+    double sigma_inv[3];     /* residual scaling 1/sigma (mstep.py:98) */
+    double c_prime;          /* outlier constant */
+    double diameter;         /* bbox diagonal of the whole reference cloud */
+    double twist_tolerance;
+    double damping;          /* < 0: 1e-6 trace(A) / n (mstep.py:358) */
+    double step_tolerance;
+    double degenerate_mass;  /* 1e-9 * total model points (pipeline.py:150) */
+    int max_em_iters;
+    int max_gn_iters;
+    int max_halvings;
+    int fast;                /* FR_PASS_FAST query path */
+} fr_rigid_em_config;
+
+/* termination codes of fr_rigid_em_status / fr_rigid_em_result */
+enum { FR_TERM_MAX_ITERS = 0, FR_TERM_CONVERGED = 1, FR_TERM_DEGENERATE = 2,
+       FR_TERM_SOLVER = 3 };
+
+int fr_rigid_em_create(const fr_lattice *lat, const float *d_ref, int64_t m,
+                       const fr_rigid_em_config *cfg, fr_rigid_em **out);
+int fr_rigid_em_destroy(fr_rigid_em *em);
+int fr_rigid_em_sums(fr_rigid_em *em, double **d_sums, int *width);
+int fr_rigid_em_pass(fr_rigid_em *em, void *stream);
+int fr_rigid_em_solve(fr_rigid_em *em, void *stream);
+int fr_rigid_em_enqueue(fr_rigid_em *em, int n_iters, void *stream);
+int fr_rigid_em_run(fr_rigid_em *em, void *stream);
+int fr_rigid_em_status(fr_rigid_em *em, int *done, int *iterations, int *termination,
+                       void *stream);
+/* pose, per-iteration traces (host arrays of >= max_em_iters doubles or NULL),
+ * iteration count and termination; FR_ESOLVER when the solve failed. */
+int fr_rigid_em_result(fr_rigid_em *em, double *R, double *t, double *objectives,
+                       double *twist_norms, double *inlier_masses, int *iterations,
+                       int *termination, void *stream);
 
 #ifdef __cplusplus
 }

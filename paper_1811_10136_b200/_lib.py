@@ -26,6 +26,9 @@ EXPORTED = (
     "fr_lattice_export", "fr_lattice_slice", "fr_simplex", "fr_gauss_bruteforce",
     "fr_moments", "fr_rigid_pass_width", "fr_rigid_scratch_doubles", "fr_rigid_pass",
     "fr_rigid_objective", "fr_moments_epilogue", "fr_assemble_rigid",
+    "fr_rigid_em_create", "fr_rigid_em_destroy", "fr_rigid_em_sums", "fr_rigid_em_pass",
+    "fr_rigid_em_solve", "fr_rigid_em_enqueue", "fr_rigid_em_run", "fr_rigid_em_status",
+    "fr_rigid_em_result",
 )
 
 
@@ -35,7 +38,22 @@ class RigidPassParams(ctypes.Structure):
                 ("c_world", ctypes.c_double * 3), ("sigma", ctypes.c_double * 3),
                 ("c_prime", ctypes.c_double), ("mode", ctypes.c_int),
                 ("m2_col", ctypes.c_int), ("normal_col", ctypes.c_int),
-                ("reserved", ctypes.c_int)]
+                ("flags", ctypes.c_int)]
+
+
+class RigidEmConfig(ctypes.Structure):
+    """fr_rigid_em_config (include/filterreg_b200.h)."""
+    _fields_ = [("R0", ctypes.c_double * 9), ("t0", ctypes.c_double * 3),
+                ("c_ref", ctypes.c_double * 3), ("sigma_inv", ctypes.c_double * 3),
+                ("c_prime", ctypes.c_double), ("diameter", ctypes.c_double),
+                ("twist_tolerance", ctypes.c_double), ("damping", ctypes.c_double),
+                ("step_tolerance", ctypes.c_double), ("degenerate_mass", ctypes.c_double),
+                ("max_em_iters", ctypes.c_int), ("max_gn_iters", ctypes.c_int),
+                ("max_halvings", ctypes.c_int), ("fast", ctypes.c_int)]
+
+
+FR_PASS_FAST = 1
+FR_TERM = {0: "max_iters", 1: "converged", 2: "degenerate", 3: "solver_error"}
 
 
 _lib = None
@@ -66,6 +84,16 @@ _SIGS = {
     "fr_rigid_scratch_doubles": ([_I, _I, _L], _I),
     "fr_rigid_pass": ([_P, _P, _L, ctypes.POINTER(RigidPassParams), _P, _P, _P, _P], _I),
     "fr_rigid_objective": ([_P, _P, _L, _DP, _I, _DP, _DP, _P, _P, _P], _I),
+    "fr_rigid_em_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), ctypes.POINTER(_P)], _I),
+    "fr_rigid_em_destroy": ([_P], _I),
+    "fr_rigid_em_sums": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_I)], _I),
+    "fr_rigid_em_pass": ([_P, _P], _I),
+    "fr_rigid_em_solve": ([_P, _P], _I),
+    "fr_rigid_em_enqueue": ([_P, _I, _P], _I),
+    "fr_rigid_em_run": ([_P, _P], _I),
+    "fr_rigid_em_status": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I), _P], _I),
+    "fr_rigid_em_result": ([_P, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I), ctypes.POINTER(_I),
+                            _P], _I),
 }
 
 

@@ -43,6 +43,12 @@ from .permutohedral import PermutohedralLattice
 
 _E = [skew(e) for e in np.eye(3)]   # K_k = [e_k]x
 
+# Query-side arithmetic of the EM pass: float32 ranks / barycentrics / table
+# rows after a float64 embedding (FR_PASS_FAST), or the all-float64 path.
+# Model points are not a bit-exact contract (the reference forms them with a
+# BLAS product), and the float32 path keeps the E-step sums to ~1e-7 relative.
+FAST_QUERY = True
+
 
 def _sym3(v6) -> np.ndarray:
     xx, xy, xz, yy, yz, zz = v6
@@ -135,7 +141,7 @@ class RigidDevicePath:
     """HBM-resident state of one rigid registration: float32 SoA reference
     planes, the observation lattice, and the reduction buffers."""
 
-    def __init__(self, reference, observation, gmm, residual_mode: str):
+    def __init__(self, reference, observation, gmm, residual_mode: str, process_group=None):
         import torch
         self.dev = _lib.device()
         self.lib = _lib.load()
@@ -144,7 +150,16 @@ class RigidDevicePath:
         self.gmm = gmm
         P = np.asarray(reference.positions, dtype=float)
         self.M = len(P)
-        self.c_ref = P.mean(axis=0)
+        self.group = process_group
+        # global quantities a shard must not compute locally:
+        # total model count (outlier constant, degenerate test), the centre of
+        # the whole reference cloud and its bounding-box diameter
+        tot = self._allreduce(np.concatenate([[float(self.M)], P.sum(axis=0)]), "sum")
+        self.M_total = int(round(tot[0]))
+        self.c_ref = tot[1:] / tot[0]
+        lo = self._allreduce(P.min(axis=0), "min")
+        hi = self._allreduce(P.max(axis=0), "max")
+        self.diameter = float(np.linalg.norm(hi - lo))
         self.ref = torch.from_numpy(np.ascontiguousarray(P.T, dtype=np.float32)).to(self.dev)
         Y = np.asarray(observation.positions, dtype=float)
         self.N = len(Y)
@@ -181,10 +196,9 @@ class RigidDevicePath:
         lat.splat_points(self.obs, self.obs_n, self.value_mode)
         lat.blur()
         self.lattice, self.sigma = lat, s
-        self.c_prime = outlier_constant(self.gmm.outlier_ratio, self.N, self.M, s)
+        self.c_prime = outlier_constant(self.gmm.outlier_ratio, self.N, self.M_total, s)
 
-    def run_pass(self, R, t) -> np.ndarray:
-        """One fused E + assembly sweep at pose (R, t); returns the host sums."""
+    def pass_params(self, R, t) -> "_lib.RigidPassParams":
         R = np.asarray(R, dtype=float)
         p = _lib.RigidPassParams()
         p.R[:] = list(R.reshape(-1))
@@ -195,12 +209,40 @@ class RigidDevicePath:
         p.mode = self.mode
         p.m2_col = self.m2_col
         p.normal_col = self.normal_col
+        p.flags = _lib.FR_PASS_FAST if FAST_QUERY else 0
+        return p
+
+    def run_pass(self, R, t) -> np.ndarray:
+        """One fused E + assembly sweep at pose (R, t); returns the host sums."""
+        p = self.pass_params(R, t)
         _lib.check(self.lib.fr_rigid_pass(self.lattice.handle, _lib.ptr(self.ref), self.M,
                                           ctypes.byref(p), _lib.ptr(self.sums),
                                           _lib.ptr(self.wtn), _lib.ptr(self.scratch),
                                           _lib.stream_handle()))
+        self.reduce_device(self.sums[:self.width])
         self.host[:self.width].copy_(self.sums[:self.width])   # synchronising D2H
         return self.host[:self.width].numpy().copy()
+
+    def _allreduce(self, v, op: str) -> np.ndarray:
+        """Host-side all-reduce of a small float64 vector over the group."""
+        v = np.asarray(v, dtype=float)
+        if self.group is None:
+            return v
+        import torch
+        import torch.distributed as dist
+        backend = dist.get_backend(self.group)
+        dev = _lib.device() if backend == "nccl" else torch.device("cpu")
+        t = torch.from_numpy(v.copy()).to(dev)
+        red = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}[op]
+        dist.all_reduce(t, op=red, group=self.group)
+        return t.cpu().numpy()
+
+    def reduce_device(self, t) -> None:
+        """Sum the per-shard normal-equation partials across ranks (one NCCL
+        all-reduce of <= 31 doubles per EM iteration)."""
+        if self.group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
     def centre(self, R, t) -> np.ndarray:
         return np.asarray(R, dtype=float) @ self.c_ref + np.asarray(t, dtype=float)
@@ -217,5 +259,105 @@ class RigidDevicePath:
         _lib.check(self.lib.fr_rigid_objective(_lib.ptr(self.ref), _lib.ptr(self.wtn), self.M,
                                                cr, k, rp, cp, _lib.ptr(self.sums),
                                                _lib.ptr(self.scratch), _lib.stream_handle()))
+        self.reduce_device(self.sums[:16])
         self.host[:16].copy_(self.sums[:16])
         return 0.5 * self.host[:k].numpy().copy()
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of a raw device buffer (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class DeviceEM:
+    """The whole rigid point-to-point EM loop resident on the GPU
+    (fr_rigid_em_*): pass, fixed-order reduction and the float64 solver kernel
+    per iteration, replayed from a CUDA graph, no host round trip.  With a
+    process group the per-iteration partials are all-reduced between the pass
+    and the solve, in fixed chunks so every rank enqueues the same number of
+    collectives."""
+
+    CHUNK = 8
+
+    def __init__(self, path: RigidDevicePath, R0, t0, config, fast: bool | None = None):
+        import torch
+        self.path = path
+        self.lib = path.lib
+        self.max_iters = int(config.max_em_iters)
+        c = _lib.RigidEmConfig()
+        c.R0[:] = list(np.asarray(R0, dtype=float).reshape(-1))
+        c.t0[:] = list(np.asarray(t0, dtype=float).reshape(-1))
+        c.c_ref[:] = list(path.c_ref)
+        c.sigma_inv[:] = list(1.0 / np.asarray(path.sigma, dtype=float))
+        c.c_prime = path.c_prime
+        c.diameter = path.diameter
+        c.twist_tolerance = float(config.twist_tolerance)
+        ms = config.mstep
+        c.damping = -1.0 if ms.damping is None else float(ms.damping)
+        c.step_tolerance = float(ms.step_tolerance)
+        c.degenerate_mass = 1e-9 * path.M_total
+        c.max_em_iters = self.max_iters
+        c.max_gn_iters = int(ms.max_gn_iters)
+        c.max_halvings = int(ms.max_halvings)
+        c.fast = int(FAST_QUERY if fast is None else fast)
+        self._cfg = c
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.fr_rigid_em_create(path.lattice.handle, _lib.ptr(path.ref), path.M,
+                                               ctypes.byref(c), ctypes.byref(h)))
+        self.h = h
+        sp = ctypes.c_void_p()
+        w = ctypes.c_int()
+        _lib.check(self.lib.fr_rigid_em_sums(h, ctypes.byref(sp), ctypes.byref(w)))
+        self.sums = torch.as_tensor(_DeviceArray(sp.value, w.value), device=path.dev)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.fr_rigid_em_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def enqueue(self, n: int) -> None:
+        """Enqueue n iterations without synchronising (single rank)."""
+        if self.path.group is None:
+            _lib.check(self.lib.fr_rigid_em_enqueue(self.h, int(n), _lib.stream_handle()))
+            return
+        for _ in range(int(n)):
+            _lib.check(self.lib.fr_rigid_em_pass(self.h, _lib.stream_handle()))
+            self.path.reduce_device(self.sums)
+            _lib.check(self.lib.fr_rigid_em_solve(self.h, _lib.stream_handle()))
+
+    def status(self):
+        d, it, term = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(self.lib.fr_rigid_em_status(self.h, ctypes.byref(d), ctypes.byref(it),
+                                               ctypes.byref(term), _lib.stream_handle()))
+        return bool(d.value), int(it.value), _lib.FR_TERM[int(term.value)]
+
+    def run(self) -> None:
+        """Iterate until termination (converged / degenerate / max_iters)."""
+        if self.path.group is None:
+            _lib.check(self.lib.fr_rigid_em_run(self.h, _lib.stream_handle()))
+            return
+        while True:
+            self.enqueue(self.CHUNK)
+            if self.status()[0]:
+                return
+
+    def result(self):
+        n = self.max_iters
+        R = np.zeros(9)
+        t = np.zeros(3)
+        obj, tn, ms = np.zeros(n), np.zeros(n), np.zeros(n)
+        it, term = ctypes.c_int(), ctypes.c_int()
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        _lib.check(self.lib.fr_rigid_em_result(self.h, dp(R), dp(t), dp(obj), dp(tn), dp(ms),
+                                               ctypes.byref(it), ctypes.byref(term),
+                                               _lib.stream_handle()))
+        k = min(int(it.value), n)
+        return (R.reshape(3, 3), t, list(obj[:k]), list(tn[:k]), list(ms[:k]), int(it.value),
+                _lib.FR_TERM[int(term.value)])

@@ -124,15 +124,22 @@ struct Simplex {
     }
 };
 
+// x / (d+1): for d+1 a power of two the product with its reciprocal is the
+// same correctly rounded real, so the cheaper multiply is bit-identical
+template <int D>
+__device__ __forceinline__ double div_d1(double x) {
+    constexpr bool pow2 = ((D + 1) & D) == 0;
+    return pow2 ? __dmul_rn(x, 1.0 / (double)(D + 1)) : __ddiv_rn(x, (double)(D + 1));
+}
+
 template <int D>
 __device__ __forceinline__ void simplex_from_elevated(const double *el, Simplex<D> &s) {
-    const double d1 = (double)(D + 1);
     double diff[D + 1];
     long long hsum = 0;
     s.overflow = 0;
 #pragma unroll
     for (int i = 0; i <= D; ++i) {
-        double r = rint(__ddiv_rn(el[i], d1));
+        double r = rint(div_d1<D>(el[i]));
         if (!(fabs(r) < (double)(kKeyLim / (D + 1)))) { s.overflow = 1; r = 0.0; }
         int ri = (int)r;
         s.rem0[i] = ri * (D + 1);
@@ -159,7 +166,7 @@ __device__ __forceinline__ void simplex_from_elevated(const double *el, Simplex<
     }
     double res[D + 1], sv[D + 1];
 #pragma unroll
-    for (int i = 0; i <= D; ++i) res[i] = __ddiv_rn(__dsub_rn(el[i], (double)s.rem0[i]), d1);
+    for (int i = 0; i <= D; ++i) res[i] = div_d1<D>(__dsub_rn(el[i], (double)s.rem0[i]));
 #pragma unroll
     for (int r = 0; r <= D; ++r) {
         double v = 0.0;
@@ -197,29 +204,184 @@ __device__ __forceinline__ void simplex_exact(const double *feat, const LatticeC
 }
 
 // ---------------------------------------------------------------------------
-// slice table: open addressing, linear probing, key and float64 values inline
-// in one 32/64/128-byte slot so a hit costs one sector-aligned gather.
+// slice table: open addressing with linear probing, keys and values in two
+// arrays indexed by the same slot.  A gather issues the key load and the
+// (32/64/128-byte, sector-aligned) value-row load of all d+1 vertices at once;
+// only a key mismatch that is not EMPTY (rare at load factor <= 1/2) probes on.
 
-template <int VP>
-struct alignas(8 * (VP + 1)) SliceSlot {
-    unsigned long long key;
-    double v[VP];
+struct SliceTable {
+    const unsigned long long *keys;
+    const double *vals;     // [cap][nvp]
+    unsigned mask;
+    int shift;              // 64 - log2(cap)
+    int nvp;                // padded row width: 4, 8 or 16
 };
 
-template <int VP>
-__device__ __forceinline__ const SliceSlot<VP> *probe(const SliceSlot<VP> *tab, unsigned mask,
-                                                      unsigned long long key) {
-    unsigned h = (unsigned)mix64(key) & mask;
-    for (unsigned it = 0; it <= mask; ++it) {
-        unsigned long long k = __ldg(&tab[h].key);
-        if (k == key) return tab + h;
-        if (k == kEmptyKey) return nullptr;
-        h = (h + 1) & mask;
-    }
-    return nullptr;
+__host__ __device__ __forceinline__ unsigned slot_hash(unsigned long long key, int shift) {
+    return (unsigned)((key * 0x9E3779B97F4A7C15ull) >> shift);
 }
 
-inline int vp_for(int nv) { return nv <= 3 ? 3 : (nv <= 7 ? 7 : (nv <= 15 ? 15 : -1)); }
+template <int NV>
+__device__ __forceinline__ void load_row(const double *row, double *v) {
+    if (NV % 2 == 0 || NV > 1) {
+#pragma unroll
+        for (int q = 0; q + 1 < NV; q += 2) {
+            const double2 d = __ldg(reinterpret_cast<const double2 *>(row) + q / 2);
+            v[q] = d.x;
+            v[q + 1] = d.y;
+        }
+    }
+    if (NV % 2 == 1) v[NV - 1] = __ldg(row + NV - 1);
+}
+
+// probe for `key`; returns the slot or -1 when absent
+__device__ __forceinline__ int find_slot(const SliceTable &t, unsigned long long key, unsigned h) {
+    for (unsigned it = 0; it <= t.mask; ++it) {
+        const unsigned long long k = __ldg(t.keys + h);
+        if (k == key) return (int)h;
+        if (k == kEmptyKey) return -1;
+        h = (h + 1) & t.mask;
+    }
+    return -1;
+}
+
+// gather the d+1 vertex rows of one simplex; hit[l] = 0 for absent vertices
+template <int D, int NV>
+__device__ __forceinline__ void gather_simplex(const SliceTable &t, const unsigned long long *key,
+                                               double (*v)[NV], bool *hit) {
+    unsigned h[D + 1];
+    unsigned long long k[D + 1];
+#pragma unroll
+    for (int l = 0; l <= D; ++l) {
+        h[l] = slot_hash(key[l], t.shift);
+        k[l] = __ldg(t.keys + h[l]);
+        load_row<NV>(t.vals + (size_t)h[l] * t.nvp, v[l]);
+    }
+#pragma unroll
+    for (int l = 0; l <= D; ++l) {
+        hit[l] = k[l] == key[l];
+        if (!hit[l] && k[l] != kEmptyKey) {
+            const int s = find_slot(t, key[l], (h[l] + 1) & t.mask);
+            hit[l] = s >= 0;
+            if (hit[l]) load_row<NV>(t.vals + (size_t)s * t.nvp, v[l]);
+        }
+    }
+}
+
+inline int nvp_for(int nv) { return nv <= 4 ? 4 : (nv <= 8 ? 8 : (nv <= 16 ? 16 : -1)); }
+
+// ---------------------------------------------------------------------------
+// fast query path of the EM pass (model points are not bit-exact contracts:
+// they come out of a BLAS product in the reference, geometry.py:77).  The
+// embedding and the nearest remainder-0 point stay float64 (lattice
+// coordinates reach ~1e3-1e4); the residuals el - rem0 lie in [-2, 2], so
+// ranks and barycentrics are float32 (abs. error ~1e-7), the packed keys are
+// formed linearly from the packed remainder-0 point, and the value table
+// holds float32 rows (16 or 32 bytes: one or two float4 per vertex).
+
+struct SliceTableF {
+    const unsigned long long *keys;
+    const float4 *vals;     // [cap][nf4]
+    unsigned mask;
+    int shift;
+    int nf4;                // float4 per row: 1 (nv <= 4) or 2 (nv <= 8)
+};
+
+struct QSimplex3 {
+    unsigned long long key[4];
+    float bary[4];
+    int overflow;
+};
+
+__device__ __forceinline__ void qsimplex3(const double *el, QSimplex3 &q) {
+    constexpr long long kLim = kKeyLim / 4 - 2;
+    double r[4];
+    float d[4];
+    int ri[4];
+    q.overflow = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        r[i] = rint(el[i] * 0.25);
+        q.overflow |= !(fabs(r[i]) < (double)kLim);
+        ri[i] = (int)r[i];
+        d[i] = (float)fma(-4.0, r[i], el[i]);     // el - rem0, exact product
+    }
+    int rank[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int rk = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j == i) continue;
+            rk += (d[j] > d[i]) || (j < i && d[j] == d[i]);
+        }
+        rank[i] = rk;
+    }
+    const int h = ri[0] + ri[1] + ri[2] + ri[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int rk = rank[i] + h;
+        if (rk < 0) { rk += 4; ri[i] += 1; d[i] -= 4.0f; }
+        else if (rk > 3) { rk -= 4; ri[i] -= 1; d[i] += 4.0f; }
+        rank[i] = rk;
+    }
+    float sv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float v = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v = (rank[i] == k) ? d[i] : v;
+        sv[k] = 0.25f * v;
+    }
+    q.bary[0] = 1.0f + sv[3] - sv[0];
+#pragma unroll
+    for (int l = 1; l < 4; ++l) q.bary[l] = sv[3 - l] - sv[4 - l];
+    // packed(rem0 + canonical[l]) = packed(rem0) + l*U - 4*B_l, B_l = sum of the
+    // field units of the coordinates whose rank exceeds 3 - l (fields never borrow)
+    const unsigned long long unit[3] = {1ull << (2 * kKeyBits), 1ull << kKeyBits, 1ull};
+    unsigned long long p0 = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) p0 += (unsigned long long)(4 * ri[i] + kKeyOff) * unit[i];
+    const unsigned long long U = unit[0] + unit[1] + unit[2];
+    unsigned long long B = 0;
+    q.key[0] = p0;
+#pragma unroll
+    for (int l = 1; l < 4; ++l) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) B += (rank[i] == 4 - l) ? unit[i] : 0ull;
+        q.key[l] = p0 + (unsigned long long)l * U - 4ull * B;
+    }
+}
+
+template <int NF4>
+__device__ __forceinline__ void gather_simplex_f(const SliceTableF &t, const unsigned long long *key,
+                                                 float4 (*v)[NF4], bool *hit) {
+    unsigned h[4];
+    unsigned long long k[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        h[l] = slot_hash(key[l], t.shift);
+        k[l] = __ldg(t.keys + h[l]);
+#pragma unroll
+        for (int f = 0; f < NF4; ++f) v[l][f] = __ldg(t.vals + (size_t)h[l] * NF4 + f);
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        hit[l] = k[l] == key[l];
+        if (!hit[l] && k[l] != kEmptyKey) {
+            unsigned s = (h[l] + 1) & t.mask;
+            for (unsigned it = 0; it <= t.mask; ++it) {
+                const unsigned long long kk = __ldg(t.keys + s);
+                if (kk == key[l]) { hit[l] = true; break; }
+                if (kk == kEmptyKey) break;
+                s = (s + 1) & t.mask;
+            }
+            if (hit[l])
+#pragma unroll
+                for (int f = 0; f < NF4; ++f) v[l][f] = __ldg(t.vals + (size_t)s * NF4 + f);
+        }
+    }
+}
 
 inline unsigned next_pow2(unsigned long long x) {
     unsigned long long p = 64;
@@ -247,9 +409,20 @@ struct fr_lattice {
     int *hsite = nullptr;
     unsigned hmask = 0;
     // slice table
-    void *slots = nullptr;
+    unsigned long long *skeys = nullptr;
+    double *svals = nullptr;
     unsigned smask = 0;
-    int vp = 0;
+    int sshift = 0;
+    int nvp = 0;
+    fr::SliceTable table() const {
+        return fr::SliceTable{skeys, svals, smask, sshift, nvp};
+    }
+    // float32 copy of the value rows for the fast EM pass (same slots)
+    float4 *fvals = nullptr;
+    int nf4 = 0;
+    fr::SliceTableF table_f() const {
+        return fr::SliceTableF{skeys, fvals, smask, sshift, nf4};
+    }
     // device counters / flags
     unsigned long long *d_counters = nullptr;   // [0] sites, [1] src count, [2] overflow
 };

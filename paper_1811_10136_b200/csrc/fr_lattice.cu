@@ -169,47 +169,66 @@ __global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash
     }
 }
 
-// splat phase 2: one thread per site, sequential sum in flat order
+// splat phase 2a: every contribution bary * value in site-sorted order (each
+// product is one rounding, computed in parallel -- same bits as NumPy's)
 template <int D, class Src>
-__global__ void k_splat_segsum(Src src, int n_runs, const unsigned *run_slot,
-                               const int *run_off, const int *run_cnt,
-                               const unsigned *sorted_idx, const double *entry_bary,
-                               unsigned sentinel, int nv, double *run_vals,
-                               unsigned char *run_live) {
-    int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_runs) return;
-    if (run_slot[r] == sentinel) { run_live[r] = 0; return; }
-    double acc[15];
-#pragma unroll
-    for (int cc = 0; cc < 15; ++cc) acc[cc] = 0.0;
-    const int beg = run_off[r], cnt = run_cnt[r];
+__global__ void k_splat_contrib(Src src, long long E, const unsigned *sorted_slot,
+                                const unsigned *sorted_idx, const double *entry_bary,
+                                unsigned sentinel, int nv, double *contrib) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < E; j += stride) {
+        if (sorted_slot[j] == sentinel) continue;
+        const unsigned e = sorted_idx[j];
+        const double b = entry_bary[e];
+        const long long p = e / (D + 1);
+        for (int cc = 0; cc < nv; ++cc) contrib[j * nv + cc] = __dmul_rn(b, src.value(p, cc));
+    }
+}
+
+// splat phase 2b: one thread per (site, 4 channels) adds its contiguous run
+// of contributions sequentially in flat (point, vertex) order -- np.add.at's
+// accumulation order (permutohedral.py:241-242), hence bit-identical sums
+__global__ void k_splat_segsum(int n_runs, const unsigned *run_slot, const int *run_off,
+                               const int *run_cnt, const double *contrib, unsigned sentinel,
+                               int nv, double *run_vals) {
+    const int chunks = (nv + 3) / 4;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= (long long)n_runs * chunks) return;
+    const int r = (int)(tid / chunks), c0 = (int)(tid % chunks) * 4;
+    if (run_slot[r] == sentinel) return;
+    const int w = min(4, nv - c0);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double *row = contrib + (long long)run_off[r] * nv + c0;
+    const int cnt = run_cnt[r];
     constexpr int U = 8;
     int j = 0;
     for (; j + U <= cnt; j += U) {
-        unsigned e[U];
-        double b[U];
+        double v[U][4];
 #pragma unroll
-        for (int u = 0; u < U; ++u) e[u] = sorted_idx[beg + j + u];
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int u = 0; u < U; ++u) b[u] = entry_bary[e[u]];
+            for (int k = 0; k < 4; ++k) v[u][k] = k < w ? row[(long long)(j + u) * nv + k] : 0.0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            long long p = e[u] / (D + 1);
-            for (int cc = 0; cc < nv; ++cc)
-                acc[cc] = __dadd_rn(acc[cc], __dmul_rn(b[u], src.value(p, cc)));
-        }
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = __dadd_rn(acc[k], v[u][k]);
     }
-    for (; j < cnt; ++j) {
-        unsigned e = sorted_idx[beg + j];
-        double b = entry_bary[e];
-        long long p = e / (D + 1);
-        for (int cc = 0; cc < nv; ++cc) acc[cc] = __dadd_rn(acc[cc], __dmul_rn(b, src.value(p, cc)));
-    }
+    for (; j < cnt; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < w) acc[k] = __dadd_rn(acc[k], row[(long long)j * nv + k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (k < w) run_vals[(long long)r * nv + c0 + k] = acc[k];
+}
+
+__global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentinel,
+                           const double *run_vals, int nv, unsigned char *run_live) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_runs) return;
     bool live = false;
-    for (int cc = 0; cc < nv; ++cc) {
-        run_vals[(long long)r * nv + cc] = acc[cc];
-        live |= acc[cc] != 0.0;
-    }
+    if (run_slot[r] != sentinel)
+        for (int c = 0; c < nv; ++c) live |= run_vals[(long long)r * nv + c] != 0.0;
     run_live[r] = live;
 }
 
@@ -324,18 +343,18 @@ __global__ void k_gather_sites(int S, const int *idx, const int *kin, const doub
     for (int c = 0; c < nv; ++c) vout[(long long)i * nv + c] = vin[(long long)j * nv + c];
 }
 
-template <int D, int VP>
+template <int D>
 __global__ void k_slice_insert(long long S, const int *site_keys, const double *vals, int nv,
-                               SliceSlot<VP> *tab, unsigned mask, unsigned long long *counters) {
+                               unsigned long long *skeys, double *svals, int nvp, unsigned mask,
+                               int shift, unsigned long long *counters) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= S) return;
     unsigned long long key = pack_key<D>(site_keys + i * (D + 1));
-    unsigned s = (unsigned)mix64(key) & mask;
+    unsigned s = slot_hash(key, shift);
     for (unsigned it = 0; it <= mask; ++it) {
-        unsigned long long prev = atomicCAS(&tab[s].key, kEmptyKey, key);
+        unsigned long long prev = atomicCAS(&skeys[s], kEmptyKey, key);
         if (prev == kEmptyKey) {
-#pragma unroll
-            for (int c = 0; c < VP; ++c) tab[s].v[c] = c < nv ? vals[i * nv + c] : 0.0;
+            for (int c = 0; c < nvp; ++c) svals[(size_t)s * nvp + c] = c < nv ? vals[i * nv + c] : 0.0;
             return;
         }
         s = (s + 1) & mask;
@@ -343,33 +362,39 @@ __global__ void k_slice_insert(long long S, const int *site_keys, const double *
     atomicOr(&counters[2], 2ull);
 }
 
-// generic slice (permutohedral.py:329-341): gain * sum_l bary_l * value(key_l)
-template <int D, int VP>
-__global__ void k_slice_generic(const double *Q, long long m, LatticeConsts c,
-                                const SliceSlot<VP> *tab, unsigned mask, int nv, double *out) {
+// generic slice (permutohedral.py:329-341): gain * sum_l bary_l * value(key_l),
+// NV value columns handled per launch (columns [c0, c0 + NV) of the row)
+template <int D, int NV>
+__global__ void k_slice_generic(const double *Q, long long m, LatticeConsts c, SliceTable t,
+                                int c0, int nv_out, double *out) {
     long long stride = (long long)gridDim.x * blockDim.x;
+    SliceTable tc = t;
+    tc.vals = t.vals + c0;
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
         double f[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) f[j] = Q[p * D + j];
         Simplex<D> s;
         simplex_exact<D>(f, c, s);
-        double acc[VP];
+        double acc[NV];
 #pragma unroll
-        for (int q = 0; q < VP; ++q) acc[q] = 0.0;
+        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
         if (!s.overflow) {
+            unsigned long long key[D + 1];
 #pragma unroll
-            for (int l = 0; l <= D; ++l) {
-                const SliceSlot<VP> *hit = probe<VP>(tab, mask, s.packed(l));
-                double b = s.bary[l];
-                if (hit) {
+            for (int l = 0; l <= D; ++l) key[l] = s.packed(l);
+            double v[D + 1][NV];
+            bool hit[D + 1];
+            gather_simplex<D, NV>(tc, key, v, hit);
 #pragma unroll
-                    for (int q = 0; q < VP; ++q)
-                        acc[q] = __dadd_rn(acc[q], __dmul_rn(b, hit->v[q]));
-                }
-            }
+            for (int l = 0; l <= D; ++l)
+#pragma unroll
+                for (int q = 0; q < NV; ++q)
+                    acc[q] = hit[l] ? __dadd_rn(acc[q], __dmul_rn(s.bary[l], v[l][q])) : acc[q];
         }
-        for (int q = 0; q < nv; ++q) out[p * nv + q] = __dmul_rn(c.gain, acc[q]);
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+            if (c0 + q < nv_out) out[p * nv_out + c0 + q] = __dmul_rn(c.gain, acc[q]);
     }
 }
 
@@ -473,6 +498,8 @@ static int read_counters(fr_lattice *lat, cudaStream_t s, unsigned long long *h)
     return FR_OK;
 }
 
+static void free_slice(fr_lattice *lat);
+
 static void free_build(fr_lattice *lat) {
     cudaFree(lat->site_keys);
     cudaFree(lat->vals);
@@ -549,8 +576,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         return FR_EINVAL;
     }
     free_build(lat);
-    cudaFree(lat->slots);
-    lat->slots = nullptr;
+    free_slice(lat);
     lat->nv = nv;
     lat->n_sites = 0;
     lat->site_cap = 0;
@@ -624,10 +650,20 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_TRY(sc.get(&live_runs, nruns));
     FR_TRY(sc.get(&iota, nruns));
     FR_TRY(sc.get(&d_nlive, 1));
-    k_splat_segsum<D, Src><<<grid_for(nruns, 128), 128, 0, s>>>(
-        src, nruns, run_slot, run_off, run_cnt, sorted_idx, entry_bary, (unsigned)cap, nv,
-        run_vals, run_live);
-    FR_CHECK_LAUNCH();
+    {
+        double *contrib;
+        FR_TRY(sc.get(&contrib, (size_t)E * nv));
+        k_splat_contrib<D, Src><<<grid_for(E), 256, 0, s>>>(src, E, sorted_slot, sorted_idx,
+                                                            entry_bary, (unsigned)cap, nv, contrib);
+        FR_CHECK_LAUNCH();
+        const long long work = (long long)nruns * ((nv + 3) / 4);
+        k_splat_segsum<<<grid_for(work, 64), 64, 0, s>>>(nruns, run_slot, run_off, run_cnt, contrib,
+                                                         (unsigned)cap, nv, run_vals);
+        FR_CHECK_LAUNCH();
+        k_run_live<<<grid_for(nruns), 256, 0, s>>>(nruns, run_slot, (unsigned)cap, run_vals, nv,
+                                                   run_live);
+        FR_CHECK_LAUNCH();
+    }
     // live runs -> dense site rows
     {
         std::vector<int> h_iota(nruns);
@@ -704,20 +740,54 @@ static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
     return FR_OK;
 }
 
-template <int D, int VP>
+static void free_slice(fr_lattice *lat) {
+    cudaFree(lat->skeys);
+    cudaFree(lat->svals);
+    cudaFree(lat->fvals);
+    lat->skeys = nullptr;
+    lat->svals = nullptr;
+    lat->fvals = nullptr;
+    lat->nvp = 0;
+    lat->nf4 = 0;
+}
+
+// float32 rows of the slice table for the fast EM pass (nv <= 8)
+__global__ void k_slice_to_f32(long long cap, const double *svals, int nvp, int nf4,
+                               float4 *fvals) {
+    long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    for (int f = 0; f < nf4; ++f) {
+        const double *r = svals + s * nvp + 4 * f;
+        fvals[s * nf4 + f] = make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]);
+    }
+}
+
+template <int D>
 static int build_slice_table(fr_lattice *lat, cudaStream_t s) {
-    cudaFree(lat->slots);
-    lat->slots = nullptr;
-    unsigned cap = next_pow2(2ull * (unsigned long long)std::max<long long>(lat->n_sites, 1));
-    FR_CUDA(cudaMalloc(&lat->slots, (size_t)cap * sizeof(SliceSlot<VP>)));
-    FR_CUDA(cudaMemsetAsync(lat->slots, 0xff, (size_t)cap * sizeof(SliceSlot<VP>), s));
+    free_slice(lat);
+    // load factor <= 1/4: a first-probe hit for almost every vertex
+    unsigned cap = next_pow2(4ull * (unsigned long long)std::max<long long>(lat->n_sites, 1));
+    int bits = 0;
+    while ((1u << bits) < cap) ++bits;
+    lat->nvp = nvp_for(lat->nv);
+    FR_CUDA(cudaMalloc(&lat->skeys, (size_t)cap * sizeof(unsigned long long)));
+    FR_CUDA(cudaMalloc(&lat->svals, (size_t)cap * lat->nvp * sizeof(double)));
+    FR_CUDA(cudaMemsetAsync(lat->skeys, 0xff, (size_t)cap * sizeof(unsigned long long), s));
+    FR_CUDA(cudaMemsetAsync(lat->svals, 0, (size_t)cap * lat->nvp * sizeof(double), s));
     lat->smask = cap - 1;
-    lat->vp = VP;
+    lat->sshift = 64 - bits;
     FR_CUDA(cudaMemsetAsync(lat->d_counters + 2, 0, sizeof(unsigned long long), s));
     if (lat->n_sites > 0) {
-        k_slice_insert<D, VP><<<grid_for(lat->n_sites), 256, 0, s>>>(
-            lat->n_sites, lat->site_keys, lat->vals, lat->nv, (SliceSlot<VP> *)lat->slots,
-            lat->smask, lat->d_counters);
+        k_slice_insert<D><<<grid_for(lat->n_sites), 256, 0, s>>>(
+            lat->n_sites, lat->site_keys, lat->vals, lat->nv, lat->skeys, lat->svals, lat->nvp,
+            lat->smask, lat->sshift, lat->d_counters);
+        FR_CHECK_LAUNCH();
+    }
+    if (lat->nv <= 8) {
+        lat->nf4 = lat->nvp / 4;
+        FR_CUDA(cudaMalloc(&lat->fvals, (size_t)cap * lat->nf4 * sizeof(float4)));
+        k_slice_to_f32<<<grid_for(cap), 256, 0, s>>>(cap, lat->svals, lat->nvp, lat->nf4,
+                                                     lat->fvals);
         FR_CHECK_LAUNCH();
     }
     unsigned long long hc[3];
@@ -785,22 +855,25 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
     lat->hkeys = nullptr;
     lat->hsite = nullptr;
     lat->hmask = 0;
-    int vp = vp_for(nv);
-    if (vp == 3) FR_TRY((build_slice_table<D, 3>(lat, s)));
-    else if (vp == 7) FR_TRY((build_slice_table<D, 7>(lat, s)));
-    else FR_TRY((build_slice_table<D, 15>(lat, s)));
+    FR_TRY(build_slice_table<D>(lat, s));
     lat->blurred = 1;
     return FR_OK;
 }
 
-template <int D, int VP>
+template <int D>
 static int slice_impl(const fr_lattice *lat, const double *Q, long long m, double *out,
                       cudaStream_t s) {
     if (m == 0) return FR_OK;
     unsigned grid = (unsigned)std::min<long long>((m + 255) / 256, 148LL * 16);
-    k_slice_generic<D, VP><<<grid, 256, 0, s>>>(Q, m, lat->c, (const SliceSlot<VP> *)lat->slots,
-                                               lat->smask, lat->nv, out);
-    FR_CHECK_LAUNCH();
+    const SliceTable t = lat->table();
+    for (int c0 = 0; c0 < lat->nv; c0 += 4) {
+        const int w = std::min(4, lat->nv - c0);
+        if (w == 4) k_slice_generic<D, 4><<<grid, 256, 0, s>>>(Q, m, lat->c, t, c0, lat->nv, out);
+        else if (w == 3) k_slice_generic<D, 3><<<grid, 256, 0, s>>>(Q, m, lat->c, t, c0, lat->nv, out);
+        else if (w == 2) k_slice_generic<D, 2><<<grid, 256, 0, s>>>(Q, m, lat->c, t, c0, lat->nv, out);
+        else k_slice_generic<D, 1><<<grid, 256, 0, s>>>(Q, m, lat->c, t, c0, lat->nv, out);
+        FR_CHECK_LAUNCH();
+    }
     return FR_OK;
 }
 
@@ -847,7 +920,7 @@ int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
 int fr_lattice_destroy(fr_lattice *lat) {
     if (!lat) return FR_OK;
     free_build(lat);
-    cudaFree(lat->slots);
+    free_slice(lat);
     cudaFree(lat->d_counters);
     delete lat;
     return FR_OK;
@@ -933,12 +1006,7 @@ int fr_lattice_slice(const fr_lattice *lat, const double *Q, int64_t m, double *
         return FR_ESTATE;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    int dim = lat->dim;
-    switch (lat->vp) {
-        case 3: FR_DISPATCH_D(dim, FR_TRY((slice_impl<D, 3>(lat, Q, m, out, s)))); break;
-        case 7: FR_DISPATCH_D(dim, FR_TRY((slice_impl<D, 7>(lat, Q, m, out, s)))); break;
-        default: FR_DISPATCH_D(dim, FR_TRY((slice_impl<D, 15>(lat, Q, m, out, s)))); break;
-    }
+    FR_DISPATCH_D(lat->dim, FR_TRY(slice_impl<D>(lat, Q, m, out, s)));
     return FR_OK;
 }
 

@@ -1,0 +1,1038 @@
+// Rigid FilterReg EM on B200: the fused per-iteration pass and the
+// device-resident Gauss-Newton solver.
+//
+//   k_rigid_pass     one sweep over the model points per EM iteration: forward
+//                    transform (kinematics.py:317-320), lattice slice
+//                    (permutohedral.py:329-341), moments epilogue
+//                    (estep.py:195-217) and the residual statistics of the M
+//                    step (mstep.py:102-210), reduced in a fixed order.
+//   k_rigid_solve    the rest of one EM iteration on one GPU thread, in float64:
+//                    normal equations from the point-to-point statistics,
+//                    damped Cholesky with tenfold escalation (mstep.py:348-369),
+//                    step halving with closed-form candidate objectives
+//                    (mstep.py:421-459), twist update with polar
+//                    re-orthonormalisation (geometry.py:154-189), update
+//                    magnitude and termination (pipeline.py:141-177).
+//   k_rigid_objective  candidate objectives for point_to_plane halving.
+// With pass + solve in a CUDA graph an EM iteration needs no host round trip.
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "fr_reduce.cuh"
+
+namespace fr {
+
+struct RigidK {
+    double M[4][3];      // elevated = M xh + e0 (embedding folded with the pose)
+    double e0[4];
+    double R[9];
+    double c_ref[3];
+    double c_world[3];
+    double cp;
+    double gain;
+    int m2_col;
+    int ncol;
+};
+
+// E diag(sf / sigma): the embedding of permutohedral.py:171-179 as a matrix
+static void embedding_matrix(const LatticeConsts &c, double A[4][3]) {
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double e = 0.0;
+            if (i == 0) e = 1.0;
+            else if (j == i - 1) e = -(double)i;
+            else if (j >= i) e = 1.0;
+            A[i][j] = e * c.sf[j] / c.sigma[j];
+        }
+}
+
+__host__ __device__ inline void make_rigid_k(const double A[4][3], const double *R,
+                                             const double *t, const double *c_ref, double cp,
+                                             double gain, int m2_col, int ncol, RigidK *k) {
+    for (int i = 0; i < 3; ++i)
+        k->c_world[i] = R[3 * i] * c_ref[0] + R[3 * i + 1] * c_ref[1] + R[3 * i + 2] * c_ref[2] + t[i];
+    for (int i = 0; i < 4; ++i) {
+        for (int j = 0; j < 3; ++j)
+            k->M[i][j] = A[i][0] * R[j] + A[i][1] * R[3 + j] + A[i][2] * R[6 + j];
+        k->e0[i] = A[i][0] * k->c_world[0] + A[i][1] * k->c_world[1] + A[i][2] * k->c_world[2];
+    }
+    for (int q = 0; q < 9; ++q) k->R[q] = R[q];
+    for (int q = 0; q < 3; ++q) k->c_ref[q] = c_ref[q];
+    k->cp = cp;
+    k->gain = gain;
+    k->m2_col = m2_col;
+    k->ncol = ncol;
+}
+
+// accumulator widths (layout documented in paper_1811_10136_b200/_rigid.py)
+constexpr int kP2PtBase = 25;
+constexpr int kP2PlBase = 29;
+constexpr int kMaxCand = 16;
+
+__device__ __forceinline__ double pt2pl_cost(double w, const double *t, const double *n,
+                                             const double *x) {
+    const double d0 = x[0] - t[0], d1 = x[1] - t[1], d2 = x[2] - t[2];
+    if (n[0] != 0.0 || n[1] != 0.0 || n[2] != 0.0) {
+        const double r = (n[0] * d0 + n[1] * d1) + n[2] * d2;
+        return w * (r * r);
+    }
+    return w * ((d0 * d0 + d1 * d1) + d2 * d2);
+}
+
+// slice at one model point, float64 table (exact-path arithmetic)
+template <int NV>
+__device__ __forceinline__ void slice_point_exact(const double *el, const SliceTable &tab,
+                                                  double *out) {
+    Simplex<3> s;
+    simplex_from_elevated<3>(el, s);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) out[q] = 0.0;
+    if (s.overflow) return;
+    unsigned long long key[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) key[l] = s.packed(l);
+    double v[4][NV];
+    bool hit[4];
+    gather_simplex<3, NV>(tab, key, v, hit);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        const double b = hit[l] ? s.bary[l] : 0.0;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) out[q] = fma(b, v[l][q], out[q]);
+    }
+}
+
+// slice at one model point, float32 ranks / barycentrics / table rows
+template <int NV>
+__device__ __forceinline__ void slice_point_fast(const double *el, const SliceTableF &tab,
+                                                 double *out) {
+    constexpr int NF4 = (NV + 3) / 4;
+    QSimplex3 q;
+    qsimplex3(el, q);
+    float acc[4 * NF4];
+#pragma unroll
+    for (int c = 0; c < 4 * NF4; ++c) acc[c] = 0.0f;
+    if (!q.overflow) {
+        float4 v[4][NF4];
+        bool hit[4];
+        gather_simplex_f<NF4>(tab, q.key, v, hit);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const float b = hit[l] ? q.bary[l] : 0.0f;
+#pragma unroll
+            for (int f = 0; f < NF4; ++f) {
+                acc[4 * f] = fmaf(b, v[l][f].x, acc[4 * f]);
+                acc[4 * f + 1] = fmaf(b, v[l][f].y, acc[4 * f + 1]);
+                acc[4 * f + 2] = fmaf(b, v[l][f].z, acc[4 * f + 2]);
+                acc[4 * f + 3] = fmaf(b, v[l][f].w, acc[4 * f + 3]);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NV; ++c) out[c] = (double)acc[c];
+}
+
+template <int MODE, int NV, bool SIG, bool FAST, bool DEV>
+__global__ void __launch_bounds__(kPassThreads, MODE == FR_POINT_TO_POINT ? 2 : 1)
+k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
+             const int *done, SliceTable tab, SliceTableF tabf, float *__restrict__ wtn,
+             double *__restrict__ partials) {
+    constexpr int NA = (MODE == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase) + (SIG ? 2 : 0);
+    __shared__ RigidK k;
+    if (DEV && *done) return;
+    if (threadIdx.x == 0) k = DEV ? *kd : kv;
+    __syncthreads();
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
+        const double xh[3] = {(double)__ldg(ref + p) - k.c_ref[0],
+                              (double)__ldg(ref + m + p) - k.c_ref[1],
+                              (double)__ldg(ref + 2 * m + p) - k.c_ref[2]};
+        double xt[3], x[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            xt[i] = fma(k.R[3 * i + 2], xh[2], fma(k.R[3 * i + 1], xh[1], k.R[3 * i] * xh[0]));
+            x[i] = xt[i] + k.c_world[i];
+        }
+        double el[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            el[i] = fma(k.M[i][2], xh[2], fma(k.M[i][1], xh[1], fma(k.M[i][0], xh[0], k.e0[i])));
+        double out[NV];
+        if (FAST) slice_point_fast<NV>(el, tabf, out);
+        else slice_point_exact<NV>(el, tab, out);
+        const double m0 = fmax(k.gain * out[0], 0.0);
+        const bool sup = m0 >= 1e-12;
+        const double w = sup ? (k.cp > 0.0 ? m0 / (m0 + k.cp) : 1.0) : 0.0;
+        const double inv = sup ? 1.0 / m0 : 0.0;
+        double t[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) t[j] = sup ? (k.gain * out[1 + j]) * inv : x[j];
+        if (MODE == FR_POINT_TO_POINT) {
+            // branch-free: unsupported points have w = 0 and t = x
+            double r[3], wy[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                r[j] = x[j] - t[j];
+                wy[j] = w * xt[j];
+            }
+            acc[0] += w;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) acc[1 + j] += wy[j];
+            acc[4] = fma(wy[0], xt[0], acc[4]);
+            acc[5] = fma(wy[0], xt[1], acc[5]);
+            acc[6] = fma(wy[0], xt[2], acc[6]);
+            acc[7] = fma(wy[1], xt[1], acc[7]);
+            acc[8] = fma(wy[1], xt[2], acc[8]);
+            acc[9] = fma(wy[2], xt[2], acc[9]);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double wr = w * r[j];
+                acc[10 + j] += wr;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) acc[13 + 3 * j + q] = fma(wr, xt[q], acc[13 + 3 * j + q]);
+                acc[22 + j] = fma(wr, r[j], acc[22 + j]);
+            }
+        } else {
+            // point_to_plane: averaged normal and validity (estep.py:209-215)
+            double n[3] = {0.0, 0.0, 0.0};
+            if (sup) {
+                double a[3];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) a[j] = (k.gain * out[k.ncol + j]) * inv;
+                const double len = sqrt((a[0] * a[0] + a[1] * a[1]) + a[2] * a[2]);
+                if (len >= 0.1) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) n[j] = a[j] / len;
+                }
+            }
+            // round to the stored float32 values so the candidate pass sees
+            // exactly the residual definition assembled here
+            const float wf = (float)w;
+            const float tf[3] = {(float)t[0], (float)t[1], (float)t[2]};
+            const float nf[3] = {(float)n[0], (float)n[1], (float)n[2]};
+            wtn[p] = wf;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                wtn[(1 + j) * m + p] = tf[j];
+                wtn[(4 + j) * m + p] = nf[j];
+            }
+            acc[0] += w;
+            const double wr = (double)wf;
+            if (wr > 0.0) {
+                const double tr[3] = {tf[0], tf[1], tf[2]};
+                const double nr[3] = {nf[0], nf[1], nf[2]};
+                const double d[3] = {x[0] - tr[0], x[1] - tr[1], x[2] - tr[2]};
+                acc[28] += pt2pl_cost(wr, tr, nr, x);
+                if (nr[0] != 0.0 || nr[1] != 0.0 || nr[2] != 0.0) {
+                    // row [x x n, n], residual n.(x - t)
+                    const double a6[6] = {x[1] * nr[2] - x[2] * nr[1], x[2] * nr[0] - x[0] * nr[2],
+                                          x[0] * nr[1] - x[1] * nr[0], nr[0], nr[1], nr[2]};
+                    const double rr = (nr[0] * d[0] + nr[1] * d[1]) + nr[2] * d[2];
+                    int o = 1;
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const double wa = wr * a6[i];
+#pragma unroll
+                        for (int j = i; j < 6; ++j) { acc[o] = fma(wa, a6[j], acc[o]); ++o; }
+                        acc[22 + i] = fma(wa, rr, acc[22 + i]);
+                    }
+                } else {
+                    // no usable plane: point rows J = [-[x]x | I] in meters
+                    const double J[3][6] = {{0.0, x[2], -x[1], 1.0, 0.0, 0.0},
+                                            {-x[2], 0.0, x[0], 0.0, 1.0, 0.0},
+                                            {x[1], -x[0], 0.0, 0.0, 0.0, 1.0}};
+                    int o = 1;
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+#pragma unroll
+                        for (int j = i; j < 6; ++j) {
+                            const double h = (J[0][i] * J[0][j] + J[1][i] * J[1][j]) + J[2][i] * J[2][j];
+                            acc[o] = fma(wr, h, acc[o]);
+                            ++o;
+                        }
+                        const double gi = (J[0][i] * d[0] + J[1][i] * d[1]) + J[2][i] * d[2];
+                        acc[22 + i] = fma(wr, gi, acc[22 + i]);
+                    }
+                }
+            }
+        }
+        if (SIG && sup) {
+            // sigma update sums (estep.py:248-255)
+            constexpr int B = (MODE == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase);
+            const double den = m0 + k.cp;
+            const double xx = (x[0] * x[0] + x[1] * x[1]) + x[2] * x[2];
+            const double xm = (x[0] * (k.gain * out[1]) + x[1] * (k.gain * out[2])) +
+                              x[2] * (k.gain * out[3]);
+            double m2v = 0.0;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) m2v = (q == k.m2_col) ? k.gain * out[q] : m2v;
+            acc[B] += (m0 * xx - 2.0 * xm + m2v) / den;
+            acc[B + 1] += m0 / den;
+        }
+    }
+    block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
+}
+
+// candidate objectives for point_to_plane halving
+struct CandK {
+    double R[kMaxCand][9];
+    double c[kMaxCand][3];
+    double c_ref[3];
+    int k;
+};
+
+__global__ void __launch_bounds__(kPassThreads, 2)
+k_rigid_objective(const float *__restrict__ ref, const float *__restrict__ wtn, long long m,
+                  CandK ck, double *__restrict__ partials) {
+    double acc[kMaxCand];
+#pragma unroll
+    for (int a = 0; a < kMaxCand; ++a) acc[a] = 0.0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
+        const double w = (double)__ldg(wtn + p);
+        if (!(w > 0.0)) continue;
+        const double xh[3] = {(double)__ldg(ref + p) - ck.c_ref[0],
+                              (double)__ldg(ref + m + p) - ck.c_ref[1],
+                              (double)__ldg(ref + 2 * m + p) - ck.c_ref[2]};
+        const double t[3] = {(double)__ldg(wtn + m + p), (double)__ldg(wtn + 2 * m + p),
+                             (double)__ldg(wtn + 3 * m + p)};
+        const double n[3] = {(double)__ldg(wtn + 4 * m + p), (double)__ldg(wtn + 5 * m + p),
+                             (double)__ldg(wtn + 6 * m + p)};
+#pragma unroll
+        for (int c = 0; c < kMaxCand; ++c) {
+            if (c >= ck.k) break;
+            double x[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const double xt = fma(ck.R[c][3 * i + 2], xh[2],
+                                      fma(ck.R[c][3 * i + 1], xh[1], ck.R[c][3 * i] * xh[0]));
+                x[i] = xt + ck.c[c][i];
+            }
+            acc[c] += pt2pl_cost(w, t, n, x);
+        }
+    }
+    block_reduce_store<kMaxCand>(acc, partials + (long long)blockIdx.x * kMaxCand);
+}
+
+// ---------------------------------------------------------------------------
+// device-resident M step (point_to_point)
+
+struct EmDev {
+    double A[4][3];
+    double c_ref[3];
+    double s2[3];           // per-axis 1/sigma^2 of the residual spec
+    double cp, gain, diameter, tol, damping, step_tol, degenerate_mass;
+    int max_em_iters, max_gn_iters, max_halvings, use_damping;
+    // state
+    double R[9], t[3];
+    RigidK k;
+    int done, iterations, termination, pad;
+};
+
+enum { kTermMaxIters = 0, kTermConverged = 1, kTermDegenerate = 2, kTermSolver = 3 };
+
+struct Mom {
+    double S0, S1[3], S2[3][3], R1[3], RX[3][3], Q[3];
+};
+
+__device__ void mom_from_sums(const double *s, Mom &m) {
+    m.S0 = s[0];
+    for (int j = 0; j < 3; ++j) {
+        m.S1[j] = s[1 + j];
+        m.R1[j] = s[10 + j];
+        m.Q[j] = s[22 + j];
+        for (int q = 0; q < 3; ++q) m.RX[j][q] = s[13 + 3 * j + q];
+    }
+    m.S2[0][0] = s[4]; m.S2[0][1] = m.S2[1][0] = s[5]; m.S2[0][2] = m.S2[2][0] = s[6];
+    m.S2[1][1] = s[7]; m.S2[1][2] = m.S2[2][1] = s[8]; m.S2[2][2] = s[9];
+}
+
+__device__ double mom_energy(const Mom &m, const double *s2) {
+    return 0.5 * (s2[0] * m.Q[0] + s2[1] * m.Q[1] + s2[2] * m.Q[2]);
+}
+
+// H = sum w J^T S^2 J, g = sum w J^T S^2 r, J = [-[x]x | I], x = y + c
+__device__ void mom_normal_eq(const Mom &m, const double *c, const double *s2, double H[6][6],
+                              double g[6]) {
+    double X1[3], X2[3][3], XR[3][3];
+    for (int i = 0; i < 3; ++i) {
+        X1[i] = m.S1[i] + c[i] * m.S0;
+        for (int j = 0; j < 3; ++j) {
+            X2[i][j] = m.S2[i][j] + c[i] * m.S1[j] + m.S1[i] * c[j] + m.S0 * c[i] * c[j];
+            XR[i][j] = m.RX[i][j] + m.R1[i] * c[j];
+        }
+    }
+    H[0][0] = s2[1] * X2[2][2] + s2[2] * X2[1][1];
+    H[0][1] = -s2[2] * X2[1][0];
+    H[0][2] = -s2[1] * X2[2][0];
+    H[1][1] = s2[0] * X2[2][2] + s2[2] * X2[0][0];
+    H[1][2] = -s2[0] * X2[2][1];
+    H[2][2] = s2[0] * X2[1][1] + s2[1] * X2[0][0];
+    H[1][0] = H[0][1];
+    H[2][0] = H[0][2];
+    H[2][1] = H[1][2];
+    const double tr[3][3] = {{0.0, -X1[2] * s2[1], X1[1] * s2[2]},
+                             {X1[2] * s2[0], 0.0, -X1[0] * s2[2]},
+                             {-X1[1] * s2[0], X1[0] * s2[1], 0.0}};
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            H[a][3 + b] = tr[a][b];
+            H[3 + b][a] = tr[a][b];
+            H[3 + a][3 + b] = a == b ? m.S0 * s2[a] : 0.0;
+        }
+    g[0] = -s2[2] * XR[2][1] + s2[1] * XR[1][2];
+    g[1] = s2[2] * XR[2][0] - s2[0] * XR[0][2];
+    g[2] = -s2[1] * XR[1][0] + s2[0] * XR[0][1];
+    for (int j = 0; j < 3; ++j) g[3 + j] = s2[j] * m.R1[j];
+}
+
+// per-axis sum w u_j^2 and sum w u_j r_j for u = A y + dt
+__device__ void mom_motion(const Mom &m, const double *D, const double *delta, const double *c,
+                           double A[3][3], double dt[3], double su2[3], double sur[3]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) A[i][j] = D[3 * i + j] - (i == j ? 1.0 : 0.0);
+    for (int i = 0; i < 3; ++i) dt[i] = A[i][0] * c[0] + A[i][1] * c[1] + A[i][2] * c[2] + delta[i];
+    for (int j = 0; j < 3; ++j) {
+        double aSa = 0.0, aS1 = 0.0, aRX = 0.0;
+        for (int p = 0; p < 3; ++p) {
+            double row = 0.0;
+            for (int q = 0; q < 3; ++q) row += m.S2[p][q] * A[j][q];
+            aSa += A[j][p] * row;
+            aS1 += A[j][p] * m.S1[p];
+            aRX += A[j][p] * m.RX[j][p];
+        }
+        su2[j] = aSa + 2.0 * dt[j] * aS1 + dt[j] * dt[j] * m.S0;
+        sur[j] = aRX + dt[j] * m.R1[j];
+    }
+}
+
+__device__ double mom_delta_energy(const Mom &m, const double *D, const double *delta,
+                                   const double *c, const double *s2) {
+    double A[3][3], dt[3], su2[3], sur[3];
+    mom_motion(m, D, delta, c, A, dt, su2, sur);
+    double e = 0.0;
+    for (int j = 0; j < 3; ++j) e += s2[j] * (su2[j] + 2.0 * sur[j]);
+    return 0.5 * e;
+}
+
+__device__ void mom_moved(Mom &m, const double *D, const double *delta, const double *c) {
+    double A[3][3], dt[3], su2[3], sur[3];
+    mom_motion(m, D, delta, c, A, dt, su2, sur);
+    Mom n;
+    n.S0 = m.S0;
+    double DS1[3], AS1[3];
+    for (int i = 0; i < 3; ++i) {
+        DS1[i] = D[3 * i] * m.S1[0] + D[3 * i + 1] * m.S1[1] + D[3 * i + 2] * m.S1[2];
+        AS1[i] = A[i][0] * m.S1[0] + A[i][1] * m.S1[1] + A[i][2] * m.S1[2];
+    }
+    double DS2[3][3], AS2[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            DS2[i][j] = D[3 * i] * m.S2[0][j] + D[3 * i + 1] * m.S2[1][j] + D[3 * i + 2] * m.S2[2][j];
+            AS2[i][j] = A[i][0] * m.S2[0][j] + A[i][1] * m.S2[1][j] + A[i][2] * m.S2[2][j];
+        }
+    for (int i = 0; i < 3; ++i) {
+        n.S1[i] = DS1[i] + dt[i] * m.S0;
+        n.R1[i] = m.R1[i] + AS1[i] + dt[i] * m.S0;
+        n.Q[i] = m.Q[i] + 2.0 * sur[i] + su2[i];
+        for (int j = 0; j < 3; ++j) {
+            double dsd = 0.0, asd = 0.0, rxd = 0.0;
+            for (int q = 0; q < 3; ++q) {
+                dsd += DS2[i][q] * D[3 * j + q];
+                asd += AS2[i][q] * D[3 * j + q];
+                rxd += m.RX[i][q] * D[3 * j + q];
+            }
+            n.S2[i][j] = dsd + DS1[i] * dt[j] + dt[i] * DS1[j] + m.S0 * dt[i] * dt[j];
+            n.RX[i][j] = rxd + m.R1[i] * dt[j] + asd + AS1[i] * dt[j] + dt[i] * DS1[j] +
+                         m.S0 * dt[i] * dt[j];
+        }
+    }
+    m = n;
+}
+
+// 3x3 helpers (row-major double[9])
+__device__ void m3_mul(const double *A, const double *B, double *C) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+}
+
+__device__ void m3_mul_t(const double *A, const double *B, double *C) {   // A B^T
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            C[3 * i + j] = A[3 * i] * B[3 * j] + A[3 * i + 1] * B[3 * j + 1] + A[3 * i + 2] * B[3 * j + 2];
+}
+
+// orthogonal polar factor by Newton iteration X <- (X + X^-T) / 2; the input is
+// a rotation up to round-off, so this converges in a few steps to the same
+// factor the reference's SVD U V^T gives (geometry.py:41-48)
+__device__ void polar3(const double *M, double *R) {
+    double X[9];
+    for (int q = 0; q < 9; ++q) X[q] = M[q];
+    for (int it = 0; it < 30; ++it) {
+        double C[9];   // cofactor matrix = det * X^-T
+        C[0] = X[4] * X[8] - X[5] * X[7];
+        C[1] = X[5] * X[6] - X[3] * X[8];
+        C[2] = X[3] * X[7] - X[4] * X[6];
+        C[3] = X[2] * X[7] - X[1] * X[8];
+        C[4] = X[0] * X[8] - X[2] * X[6];
+        C[5] = X[1] * X[6] - X[0] * X[7];
+        C[6] = X[1] * X[5] - X[2] * X[4];
+        C[7] = X[2] * X[3] - X[0] * X[5];
+        C[8] = X[0] * X[4] - X[1] * X[3];
+        const double det = X[0] * C[0] + X[1] * C[1] + X[2] * C[2];
+        double diff = 0.0;
+        for (int q = 0; q < 9; ++q) {
+            const double xn = 0.5 * (X[q] + C[q] / det);
+            diff = fmax(diff, fabs(xn - X[q]));
+            X[q] = xn;
+        }
+        if (diff <= 1e-16) break;
+    }
+    for (int q = 0; q < 9; ++q) R[q] = X[q];
+}
+
+// exp of a twist (omega, v): Rodrigues + left Jacobian (geometry.py:154-175)
+__device__ void twist_exp_dev(const double *tw, double *R, double *t) {
+    const double w0 = tw[0], w1 = tw[1], w2 = tw[2];
+    const double th = sqrt((w0 * w0 + w1 * w1) + w2 * w2);
+    const double S[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
+    double S2[9];
+    m3_mul(S, S, S2);
+    double a, b, c;
+    if (th < 1e-9) {
+        a = 1.0 - th * th / 6.0;
+        b = 0.5 - th * th / 24.0;
+        c = 1.0 / 6.0 - th * th / 120.0;
+    } else {
+        const double s = sin(th), co = cos(th);
+        a = s / th;
+        b = (1.0 - co) / (th * th);
+        c = (th - s) / (th * th * th);
+    }
+    double Rr[9], V[9];
+    for (int q = 0; q < 9; ++q) {
+        const double I = (q % 4 == 0) ? 1.0 : 0.0;
+        Rr[q] = I + a * S[q] + b * S2[q];
+        V[q] = I + b * S[q] + c * S2[q];
+    }
+    polar3(Rr, R);
+    for (int i = 0; i < 3; ++i) t[i] = V[3 * i] * tw[3] + V[3 * i + 1] * tw[4] + V[3 * i + 2] * tw[5];
+}
+
+// exp(tw) o (R, t), re-orthonormalised; zero twist is a no-op (geometry.py:178-189)
+__device__ void apply_twist_dev(const double *tw, const double *R, const double *t, double *R2,
+                                double *t2) {
+    bool any = false;
+    for (int q = 0; q < 6; ++q) any |= tw[q] != 0.0;
+    if (!any) {
+        for (int q = 0; q < 9; ++q) R2[q] = R[q];
+        for (int q = 0; q < 3; ++q) t2[q] = t[q];
+        return;
+    }
+    double ER[9], Et[3], P[9];
+    twist_exp_dev(tw, ER, Et);
+    m3_mul(ER, R, P);
+    polar3(P, R2);
+    for (int i = 0; i < 3; ++i)
+        t2[i] = ER[3 * i] * t[0] + ER[3 * i + 1] * t[1] + ER[3 * i + 2] * t[2] + Et[i];
+}
+
+__device__ double rotation_angle_dev(const double *R) {
+    const double c = (R[0] + R[4] + R[8] - 1.0) / 2.0;
+    return acos(fmin(fmax(c, -1.0), 1.0));
+}
+
+// (A + lam I) x = b by Cholesky; false when not positive definite
+__device__ bool chol6_solve(const double (*A)[6], double lam, const double *b, double *x) {
+    double L[6][6];
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double s = A[i][j] + (i == j ? lam : 0.0);
+            for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
+            if (i == j) {
+                if (!(s > 0.0) || !isfinite(s)) return false;
+                L[i][i] = sqrt(s);
+            } else {
+                L[i][j] = s / L[j][j];
+            }
+        }
+    double y[6];
+    for (int i = 0; i < 6; ++i) {
+        double s = b[i];
+        for (int k = 0; k < i; ++k) s -= L[i][k] * y[k];
+        y[i] = s / L[i][i];
+    }
+    for (int i = 5; i >= 0; --i) {
+        double s = y[i];
+        for (int k = i + 1; k < 6; ++k) s -= L[k][i] * x[k];
+        x[i] = s / L[i][i];
+    }
+    for (int i = 0; i < 6; ++i)
+        if (!isfinite(x[i])) return false;
+    return true;
+}
+
+// step = -(A + lam I)^-1 b with the reference's damping and escalation
+__device__ bool gn_solve_dev(const double (*H)[6], const double *g, bool use_damping,
+                             double damping, double *step) {
+    const double tr = H[0][0] + H[1][1] + H[2][2] + H[3][3] + H[4][4] + H[5][5];
+    double lam = use_damping ? damping : 1e-6 * tr / 6.0;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        double x[6];
+        if (chol6_solve(H, lam, g, x)) {
+            for (int i = 0; i < 6; ++i) step[i] = -x[i];
+            return true;
+        }
+        lam = lam > 0.0 ? lam * 10.0 : fmax(tr / 6.0, 1.0) * 1e-10;
+    }
+    return false;
+}
+
+__global__ void k_rigid_solve(const double *sums, EmDev *e, double *objs, double *tnorms,
+                              double *masses) {
+    if (threadIdx.x != 0 || e->done) return;
+    const int it = e->iterations;
+    e->iterations = it + 1;
+    const double mass = sums[0];
+    masses[it] = mass;
+    if (mass < e->degenerate_mass) {
+        objs[it] = CUDART_NAN;
+        tnorms[it] = CUDART_NAN;
+        e->termination = kTermDegenerate;
+        e->done = 1;
+        return;
+    }
+    Mom mo;
+    mom_from_sums(sums, mo);
+    double c[3];
+    for (int i = 0; i < 3; ++i)
+        c[i] = e->R[3 * i] * e->c_ref[0] + e->R[3 * i + 1] * e->c_ref[1] +
+               e->R[3 * i + 2] * e->c_ref[2] + e->t[i];
+    const double value0 = mom_energy(mo, e->s2);
+    double value = value0;
+    double H[6][6], g[6];
+    mom_normal_eq(mo, c, e->s2, H, g);
+    double Rc[9], tc[3];
+    for (int q = 0; q < 9; ++q) Rc[q] = e->R[q];
+    for (int q = 0; q < 3; ++q) tc[q] = e->t[q];
+    for (int gn = 0; gn < e->max_gn_iters; ++gn) {
+        bool any = false;
+        for (int q = 0; q < 6; ++q) any |= g[q] != 0.0;
+        if (!any) break;
+        double step[6];
+        if (!gn_solve_dev(H, g, e->use_damping, e->damping, step)) {
+            e->termination = kTermSolver;
+            e->done = 1;
+            return;
+        }
+        double scale = 1.0, Rn[9], tn[3], D[9], delta[3], cv = 0.0;
+        bool accepted = false;
+        for (int h = 0; h <= e->max_halvings; ++h) {
+            double tw[6];
+            for (int q = 0; q < 6; ++q) tw[q] = scale * step[q];
+            apply_twist_dev(tw, Rc, tc, Rn, tn);
+            m3_mul_t(Rn, Rc, D);
+            for (int i = 0; i < 3; ++i)
+                delta[i] = tn[i] - (D[3 * i] * tc[0] + D[3 * i + 1] * tc[1] + D[3 * i + 2] * tc[2]);
+            cv = value + mom_delta_energy(mo, D, delta, c, e->s2);
+            if (cv <= value * (1.0 + 1e-12) + 1e-300) {   // mstep.py:446
+                accepted = true;
+                break;
+            }
+            scale *= 0.5;
+        }
+        if (!accepted) break;
+        mom_moved(mo, D, delta, c);
+        for (int q = 0; q < 9; ++q) Rc[q] = Rn[q];
+        for (int q = 0; q < 3; ++q) tc[q] = tn[q];
+        value = cv;
+        double sn = 0.0;
+        for (int q = 0; q < 6; ++q) sn += (scale * step[q]) * (scale * step[q]);
+        if (sqrt(sn) <= e->step_tol) break;
+        mom_normal_eq(mo, c, e->s2, H, g);
+    }
+    double Rd[9];
+    m3_mul_t(Rc, e->R, Rd);
+    const double dx = tc[0] - e->t[0], dy = tc[1] - e->t[1], dz = tc[2] - e->t[2];
+    const double norm = rotation_angle_dev(Rd) + sqrt((dx * dx + dy * dy) + dz * dz) / e->diameter;
+    tnorms[it] = norm;
+    if (norm < e->tol) {   // sub-tolerance motion: drop it (pipeline.py:169-173)
+        objs[it] = value0;
+        e->termination = kTermConverged;
+        e->done = 1;
+        return;
+    }
+    for (int q = 0; q < 9; ++q) e->R[q] = Rc[q];
+    for (int q = 0; q < 3; ++q) e->t[q] = tc[q];
+    objs[it] = value;
+    make_rigid_k(e->A, e->R, e->t, e->c_ref, e->k.cp, e->k.gain, e->k.m2_col, e->k.ncol, &e->k);
+    if (it + 1 >= e->max_em_iters) {
+        e->termination = kTermMaxIters;
+        e->done = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host
+
+static int width(int mode, int sig) {
+    return (mode == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase) + (sig ? 2 : 0);
+}
+
+template <int MODE, int NV, bool SIG, bool FAST, bool DEV>
+static int launch_pass_t(const fr_lattice *lat, const float *ref, long long m, const RigidK &k,
+                         const RigidK *kd, const int *done, float *wtn, double *scratch,
+                         double *sums, cudaStream_t s) {
+    const int grid = pass_grid();
+    k_rigid_pass<MODE, NV, SIG, FAST, DEV><<<grid, kPassThreads, 0, s>>>(
+        ref, m, k, kd, done, lat->table(), lat->table_f(), wtn, scratch);
+    FR_CHECK_LAUNCH();
+    const int na = width(MODE, SIG);
+    k_reduce_cols<<<1, 32 * na, 0, s>>>(scratch, grid, na, sums, done);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+// dispatch on (mode, nv, sigma sums, fast, device params)
+static int launch_pass(const fr_lattice *lat, int mode, bool sig, bool fast, bool dev,
+                       const float *ref, long long m, const RigidK &k, const RigidK *kd,
+                       const int *done, float *wtn, double *scratch, double *sums,
+                       cudaStream_t s) {
+    const int nv = lat->nv;
+    fast = fast && !sig && lat->fvals != nullptr;
+#define FR_L(MODE, NV, SIG, FAST, DEV) \
+    return launch_pass_t<MODE, NV, SIG, FAST, DEV>(lat, ref, m, k, kd, done, wtn, scratch, sums, s)
+    if (mode == FR_POINT_TO_POINT) {
+        if (nv == 4 && !sig) {
+            if (fast) { if (dev) FR_L(0, 4, false, true, true); FR_L(0, 4, false, true, false); }
+            if (dev) FR_L(0, 4, false, false, true);
+            FR_L(0, 4, false, false, false);
+        }
+        if (nv == 5 && sig) { if (dev) FR_L(0, 5, true, false, true); FR_L(0, 5, true, false, false); }
+        if (nv == 5 && !sig) { if (dev) FR_L(0, 5, false, false, true); FR_L(0, 5, false, false, false); }
+    } else if (!dev) {
+        if (nv == 7 && !sig) {
+            if (fast) FR_L(1, 7, false, true, false);
+            FR_L(1, 7, false, false, false);
+        }
+        if (nv == 8 && sig) FR_L(1, 8, true, false, false);
+        if (nv == 8 && !sig) FR_L(1, 8, false, false, false);
+    }
+#undef FR_L
+    set_error("lattice value columns (%d) do not match the residual mode / options", nv);
+    return FR_EINVAL;
+}
+
+}  // namespace fr
+
+// the device-resident EM object behind fr_rigid_em*
+struct fr_rigid_em {
+    const fr_lattice *lat = nullptr;
+    const float *ref = nullptr;
+    long long m = 0;
+    int fast = 1;
+    int max_iters = 0;
+    fr::EmDev *d_em = nullptr;
+    double *d_sums = nullptr;
+    double *d_scratch = nullptr;
+    double *d_traces = nullptr;   // [3][max_iters]: objectives, twist norms, inlier masses
+    cudaGraphExec_t graph = nullptr;
+    int graph_iters = 0;
+};
+
+using namespace fr;
+
+extern "C" {
+
+int fr_rigid_pass_width(int mode, int with_sigma) { return width(mode, with_sigma); }
+
+int fr_rigid_scratch_doubles(int mode, int with_sigma, int64_t m) {
+    (void)m;
+    return pass_grid() * std::max(std::max(width(mode, with_sigma), kMaxCand), 28);
+}
+
+int fr_rigid_pass(const fr_lattice *lat, const float *ref, int64_t m,
+                  const fr_rigid_pass_params *p, double *sums, float *wtn, double *scratch,
+                  void *stream) {
+    if (!lat || !lat->blurred) {
+        set_error("the EM pass needs a built (blurred) lattice");
+        return FR_ESTATE;
+    }
+    if (lat->dim != 3 || !p || !sums || !scratch || (m > 0 && !ref)) {
+        set_error("invalid rigid pass arguments");
+        return FR_EINVAL;
+    }
+    const int mode = p->mode;
+    if (mode != FR_POINT_TO_POINT && mode != FR_POINT_TO_PLANE) {
+        set_error("unknown residual mode %d", mode);
+        return FR_EINVAL;
+    }
+    if (mode == FR_POINT_TO_PLANE && (!wtn || p->normal_col < 0 || p->normal_col + 3 > lat->nv)) {
+        set_error("point_to_plane needs the normal channel and weight/target/normal planes");
+        return FR_EINVAL;
+    }
+    const bool sig = p->m2_col >= 0;
+    if (sig && p->m2_col >= lat->nv) {
+        set_error("m2 column out of range");
+        return FR_EINVAL;
+    }
+    double A[4][3];
+    embedding_matrix(lat->c, A);
+    const double t[3] = {p->c_world[0] - (p->R[0] * p->c_ref[0] + p->R[1] * p->c_ref[1] + p->R[2] * p->c_ref[2]),
+                         p->c_world[1] - (p->R[3] * p->c_ref[0] + p->R[4] * p->c_ref[1] + p->R[5] * p->c_ref[2]),
+                         p->c_world[2] - (p->R[6] * p->c_ref[0] + p->R[7] * p->c_ref[1] + p->R[8] * p->c_ref[2])};
+    RigidK k;
+    memset(&k, 0, sizeof(k));
+    make_rigid_k(A, p->R, t, p->c_ref, p->c_prime, lat->c.gain, p->m2_col, p->normal_col, &k);
+    // the caller's centre is authoritative (the host-side moments use it)
+    for (int i = 0; i < 3; ++i) k.c_world[i] = p->c_world[i];
+    for (int i = 0; i < 4; ++i)
+        k.e0[i] = A[i][0] * k.c_world[0] + A[i][1] * k.c_world[1] + A[i][2] * k.c_world[2];
+    cudaStream_t s = (cudaStream_t)stream;
+    const int na = width(mode, sig);
+    if (m == 0) {
+        FR_CUDA(cudaMemsetAsync(sums, 0, na * sizeof(double), s));
+        return FR_OK;
+    }
+    const bool fast = (p->flags & FR_PASS_FAST) != 0;
+    return launch_pass(lat, mode, sig, fast, false, ref, m, k, nullptr, nullptr, wtn, scratch,
+                       sums, s);
+}
+
+int fr_rigid_objective(const float *ref, const float *wtn, int64_t m, const double *c_ref, int k,
+                       const double *cand_R, const double *cand_c, double *out, double *scratch,
+                       void *stream) {
+    if (k < 1 || k > kMaxCand || !ref || !wtn || !out || !scratch) {
+        set_error("invalid candidate objective arguments (1 <= k <= %d)", kMaxCand);
+        return FR_EINVAL;
+    }
+    CandK ck;
+    memset(&ck, 0, sizeof(ck));
+    for (int c = 0; c < k; ++c) {
+        memcpy(ck.R[c], cand_R + 9 * c, 9 * sizeof(double));
+        memcpy(ck.c[c], cand_c + 3 * c, 3 * sizeof(double));
+    }
+    memcpy(ck.c_ref, c_ref, sizeof(ck.c_ref));
+    ck.k = k;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int grid = pass_grid();
+    k_rigid_objective<<<grid, kPassThreads, 0, s>>>(ref, wtn, m, ck, scratch);
+    FR_CHECK_LAUNCH();
+    k_reduce_cols<<<1, 32 * kMaxCand, 0, s>>>(scratch, grid, kMaxCand, out, nullptr);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+// ---- device-resident EM loop -----------------------------------------------
+
+int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
+                       const fr_rigid_em_config *cfg, fr_rigid_em **out) {
+    if (!lat || !lat->blurred || !ref || !cfg || !out || m <= 0) {
+        set_error("invalid device EM arguments");
+        return FR_EINVAL;
+    }
+    if (lat->dim != 3 || lat->nv != 4) {
+        set_error("the device EM loop runs point_to_point with a fixed kernel (4 value columns)");
+        return FR_EINVAL;
+    }
+    if (cfg->max_em_iters < 1 || cfg->max_gn_iters < 0 || cfg->max_halvings < 0) {
+        set_error("invalid iteration limits");
+        return FR_EINVAL;
+    }
+    fr_rigid_em *em = new fr_rigid_em();
+    em->lat = lat;
+    em->ref = ref;
+    em->m = m;
+    em->fast = cfg->fast ? 1 : 0;
+    em->max_iters = cfg->max_em_iters;
+    EmDev h;
+    memset(&h, 0, sizeof(h));
+    embedding_matrix(lat->c, h.A);
+    for (int i = 0; i < 3; ++i) {
+        h.c_ref[i] = cfg->c_ref[i];
+        h.s2[i] = cfg->sigma_inv[i] * cfg->sigma_inv[i];
+        h.t[i] = cfg->t0[i];
+    }
+    for (int q = 0; q < 9; ++q) h.R[q] = cfg->R0[q];
+    h.cp = cfg->c_prime;
+    h.gain = lat->c.gain;
+    h.diameter = cfg->diameter;
+    h.tol = cfg->twist_tolerance;
+    h.use_damping = cfg->damping >= 0.0;
+    h.damping = cfg->damping;
+    h.step_tol = cfg->step_tolerance;
+    h.degenerate_mass = cfg->degenerate_mass;
+    h.max_em_iters = cfg->max_em_iters;
+    h.max_gn_iters = cfg->max_gn_iters;
+    h.max_halvings = cfg->max_halvings;
+    make_rigid_k(h.A, h.R, h.t, h.c_ref, h.cp, h.gain, -1, -1, &h.k);
+    const int grid = pass_grid();
+    if (cudaMalloc(&em->d_em, sizeof(EmDev)) != cudaSuccess ||
+        cudaMalloc(&em->d_sums, 32 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&em->d_scratch, (size_t)grid * 32 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double)) != cudaSuccess ||
+        cudaMemcpy(em->d_em, &h, sizeof(EmDev), cudaMemcpyHostToDevice) != cudaSuccess) {
+        fr_rigid_em_destroy(em);
+        set_error("device EM allocation failed");
+        return FR_ECUDA;
+    }
+    *out = em;
+    return FR_OK;
+}
+
+int fr_rigid_em_destroy(fr_rigid_em *em) {
+    if (!em) return FR_OK;
+    if (em->graph) cudaGraphExecDestroy(em->graph);
+    cudaFree(em->d_em);
+    cudaFree(em->d_sums);
+    cudaFree(em->d_scratch);
+    cudaFree(em->d_traces);
+    delete em;
+    return FR_OK;
+}
+
+int fr_rigid_em_sums(fr_rigid_em *em, double **d_sums, int *width_out) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    if (d_sums) *d_sums = em->d_sums;
+    if (width_out) *width_out = kP2PtBase;
+    return FR_OK;
+}
+
+static int em_pass(fr_rigid_em *em, cudaStream_t s) {
+    RigidK unused;
+    memset(&unused, 0, sizeof(unused));
+    return launch_pass(em->lat, FR_POINT_TO_POINT, false, em->fast != 0, true, em->ref, em->m,
+                       unused, &em->d_em->k, &em->d_em->done, nullptr, em->d_scratch, em->d_sums,
+                       s);
+}
+
+static int em_solve(fr_rigid_em *em, cudaStream_t s) {
+    const int n = em->max_iters;
+    k_rigid_solve<<<1, 32, 0, s>>>(em->d_sums, em->d_em, em->d_traces, em->d_traces + n,
+                                   em->d_traces + 2 * n);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+int fr_rigid_em_pass(fr_rigid_em *em, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    return em_pass(em, (cudaStream_t)stream);
+}
+
+int fr_rigid_em_solve(fr_rigid_em *em, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    return em_solve(em, (cudaStream_t)stream);
+}
+
+// enqueue n EM iterations (pass + solve each); iterations after termination
+// are no-ops.  Groups of iterations replay one captured CUDA graph.
+int fr_rigid_em_enqueue(fr_rigid_em *em, int n, void *stream) {
+    if (!em || n < 0) {
+        set_error("invalid enqueue arguments");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    constexpr int kGraphIters = 8;
+    if (!em->graph) {
+        cudaStream_t cs;
+        FR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t g;
+        FR_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < kGraphIters; ++i) {
+            int st = em_pass(em, cs);
+            if (st == FR_OK) st = em_solve(em, cs);
+            if (st != FR_OK) {
+                cudaStreamEndCapture(cs, &g);
+                cudaStreamDestroy(cs);
+                return st;
+            }
+        }
+        FR_CUDA(cudaStreamEndCapture(cs, &g));
+        FR_CUDA(cudaGraphInstantiate(&em->graph, g, 0));
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(cs);
+        em->graph_iters = kGraphIters;
+    }
+    int left = n;
+    while (left >= em->graph_iters) {
+        FR_CUDA(cudaGraphLaunch(em->graph, s));
+        left -= em->graph_iters;
+    }
+    for (; left > 0; --left) {
+        FR_TRY(em_pass(em, s));
+        FR_TRY(em_solve(em, s));
+    }
+    return FR_OK;
+}
+
+int fr_rigid_em_status(fr_rigid_em *em, int *done, int *iterations, int *termination,
+                       void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    int h[3];
+    cudaStream_t s = (cudaStream_t)stream;
+    FR_CUDA(cudaMemcpyAsync(h, &em->d_em->done, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    if (done) *done = h[0];
+    if (iterations) *iterations = h[1];
+    if (termination) *termination = h[2];
+    return FR_OK;
+}
+
+int fr_rigid_em_run(fr_rigid_em *em, void *stream) {
+    int done = 0;
+    for (int guard = 0; !done && guard < em->max_iters + 16; guard += 8) {
+        FR_TRY(fr_rigid_em_enqueue(em, 8, stream));
+        FR_TRY(fr_rigid_em_status(em, &done, nullptr, nullptr, stream));
+    }
+    return FR_OK;
+}
+
+int fr_rigid_em_result(fr_rigid_em *em, double *R, double *t, double *objectives,
+                       double *twist_norms, double *inlier_masses, int *iterations,
+                       int *termination, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    EmDev h;
+    FR_CUDA(cudaMemcpyAsync(&h, em->d_em, sizeof(EmDev), cudaMemcpyDeviceToHost, s));
+    std::vector<double> tr((size_t)3 * em->max_iters);
+    FR_CUDA(cudaMemcpyAsync(tr.data(), em->d_traces, tr.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    if (R) memcpy(R, h.R, 9 * sizeof(double));
+    if (t) memcpy(t, h.t, 3 * sizeof(double));
+    const int n = std::min(h.iterations, em->max_iters);
+    if (objectives) memcpy(objectives, tr.data(), n * sizeof(double));
+    if (twist_norms) memcpy(twist_norms, tr.data() + em->max_iters, n * sizeof(double));
+    if (inlier_masses) memcpy(inlier_masses, tr.data() + 2 * em->max_iters, n * sizeof(double));
+    if (iterations) *iterations = h.iterations;
+    if (termination) *termination = h.termination;
+    if (h.termination == kTermSolver && h.done) {
+        set_error("normal equations not factorizable after damping escalation");
+        return FR_ESOLVER;
+    }
+    return FR_OK;
+}
+
+}  // extern "C"

@@ -187,13 +187,48 @@ def _rigid_m_step(path: RigidDevicePath, sums, R, t, s2, opts: MStepOptions):
     return current, diag
 
 
+def _register_device_loop(path, model, config, timing):
+    """Point-to-point EM with the whole iteration on the GPU (DeviceEM): the
+    fused pass, the reduction and the float64 Gauss-Newton / halving /
+    termination logic of pipeline.py:141-177 run as one CUDA graph per group of
+    iterations; the host only waits for the termination flag.  `timing`
+    receives the loop's wall time as `e_step_s` (E step and M step are fused
+    on the device) and 0 for `m_step_s`."""
+    import torch
+    from ._rigid import DeviceEM
+    from .errors import SolverError
+    tick = time.perf_counter()
+    em = DeviceEM(path, model.pose.rotation, model.pose.translation, config)
+    em.run()
+    R, t, objs, tnorms, masses, iters, term = em.result()
+    torch.cuda.current_stream().synchronize()
+    if timing is not None:
+        timing["e_step_s"] = timing.get("e_step_s", 0.0) + time.perf_counter() - tick
+        timing["m_step_s"] = timing.get("m_step_s", 0.0)
+        timing["iterations"] = iters
+    if term == "solver_error":
+        raise SolverError("normal equations not factorizable after damping escalation")
+    final = model if np.array_equal(R, model.pose.rotation) and \
+        np.array_equal(t, model.pose.translation) else RigidModel(RigidTransform(R, t))
+    return RegistrationResult(kinematics=final, iterations=iters, objectives=objs,
+                              twist_norms=tnorms, inlier_masses=masses, sigmas=[],
+                              termination=term, states=None)
+
+
 def register(reference: PointCloud, observation: PointCloud, initial_model,
              config: RegistrationConfig | None = None,
-             timing: dict | None = None) -> RegistrationResult:
+             timing: dict | None = None, process_group=None,
+             _path_factory=None) -> RegistrationResult:
     """Run EM until the update magnitude drops under the twist tolerance
     (pipeline.py:125-181).  `timing` accumulates wall-clock seconds of the
     fused E(+assembly) pass (`e_step_s`) and of the solve / halving phase
-    (`m_step_s`)."""
+    (`m_step_s`).
+
+    With `process_group` (torch.distributed), `reference` is this rank's shard
+    of the model cloud; every rank holds the whole observation lattice, the
+    per-iteration partial sums are all-reduced and all ranks take identical
+    decisions on identical totals.  The returned result is the same on every
+    rank."""
     config = config if config is not None else RegistrationConfig()
     if not isinstance(initial_model, RigidModel):
         raise TypeError(f"unsupported kinematic model {type(initial_model).__name__} "
@@ -201,13 +236,17 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
     if config.backend != "lattice" or config.gmm.mode != "position":
         raise ValueError("the device EM path runs the lattice backend with position "
                          "correspondences")
-    path = RigidDevicePath(reference, observation, config.gmm, config.residual_mode)
+    factory = _path_factory if _path_factory is not None else RigidDevicePath
+    path = factory(reference, observation, config.gmm, config.residual_mode, process_group)
+    if (_path_factory is None and config.residual_mode == "point_to_point"
+            and not config.gmm.update_sigma and not config.record_states):
+        return _register_device_loop(path, initial_model, config, timing)
     model = initial_model
-    diameter = reference.diameter()
+    diameter = path.diameter
     sigma_current = path.sigma
     result = RegistrationResult(kinematics=model, iterations=0,
                                 states=[] if config.record_states else None)
-    n_ref = len(reference)
+    n_ref = path.M_total
     for _ in range(config.max_em_iters):
         result.iterations += 1
         tick = time.perf_counter()
