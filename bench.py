@@ -2,20 +2,20 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--points P] [--impl b200|reference]
 
-Workload (BASELINE.json configs[4], "large-scale rigid sweep", at the 1M point
-of the metric "EM iters/sec & points/sec (100k/1M-pt rigid)"): the reference's
-pebble pair (synth.py:252-284 restated in oracle/filterreg_oracle.py) with
-P = 1,000,000 points per GPU plus 5% uniform outliers, 50 deg / 2% shift ground
-truth, sigma = 5% of the clean bbox diagonal, w = 0.1.  Weak scaling: the job's
-model cloud has N*P(1.05) points, sharded contiguously over the N ranks; every
-rank builds the lattice of the whole observation cloud (once, outside the
-timed region, reported as build_ms) and the per-iteration normal-equation
-partials are NCCL all-reduced.
+Workload (BASELINE.json configs[4], "large-scale rigid sweep 1M-16M observation
+points"): the reference's pebble pair (synth.py:252-284, restated in
+oracle/filterreg_oracle.py) with P = 16,000,000 clean points + 5% uniform
+outliers (16.8M) per GPU, 50 deg / 2% shift ground truth, sigma = 5% of the
+clean bbox diagonal, w = 0.1.  Weak scaling: every rank holds its own 16.8M-
+point model shard (see make_shard) and the whole observation lattice (built
+once, outside the timed region, reported as build_ms); the 25 per-iteration
+normal-equation partials are NCCL all-reduced.
 
-A step is ONE EM iteration over the whole job (fused E + assembly pass,
-all-reduce, host GN solve + step halving).  The tolerance is 1e-30 so every
-step does the full work.  Inputs are smaller than L2 at 1M points, so L2 is
-flushed (256 MiB write) before every timed step, outside its events.
+A step is ONE EM iteration over the whole job: fused E + assembly pass,
+fixed-order reduction, [all-reduce,] float64 solve / halving / termination --
+all on the device, replayed from a CUDA graph (DeviceEM).  The tolerance is
+1e-30 so every step does the full work.  The model planes (16.8M x 12 B =
+202 MB) are larger than L2, so no flush is needed between steps.
 
 value = model points x timed EM iterations / device time (max over ranks).
 """
@@ -26,7 +26,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -43,12 +42,14 @@ L2_BYTES = 126 * 1024 * 1024
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--points", type=int, default=1_000_000, help="clean points per GPU")
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--points", type=int, default=16_000_000, help="clean model points per GPU")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=262_144,
                     help="model points per CPU-baseline EM iteration")
+    ap.add_argument("--cpu-obs", type=int, default=1_048_576,
+                    help="observation points of the CPU-baseline lattice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -61,21 +62,24 @@ def dist_env():
     return world, rank, local
 
 
-def make_workload(points_per_gpu: int, world: int):
-    """fp32-rounded pebble pair of world * points clean points (+5% outliers)."""
+def make_shard(points: int, rank: int):
+    """This rank's model shard and the (replicated) observation cloud.
+
+    The observation cloud and rank 0's model shard are the reference's pebble
+    pair (synth.py:252-284; 50 deg / 2% shift ground truth, 5% outliers);
+    rank r > 0 holds an independent scattered re-sampling of the same surface
+    (seeded by r) with its own 5% outliers, so the per-GPU work is fixed as
+    the GPU count grows (weak scaling) and no rank materialises the job's
+    whole model cloud.  Everything is rounded to float32 once."""
     from oracle import filterreg_oracle as O
-    n = points_per_gpu * world
-    model, obs, gt = O.pebble_pair(n, rotation_degrees=50.0, translation_fraction=0.02,
-                                   outlier_ratio=0.05, seed=0)
+    model, obs, (Rg, tg) = O.pebble_pair(points, rotation_degrees=50.0,
+                                         translation_fraction=0.02, outlier_ratio=0.05, seed=0)
+    sigma = 0.05 * O.bbox_diameter(model[:points])
+    if rank > 0:
+        model = O.pebble_resample(points, seed=1000 + rank, outlier_ratio=0.05)
     X = model.astype(np.float32).astype(np.float64)
     Y = obs.astype(np.float32).astype(np.float64)
-    sigma = 0.05 * O.bbox_diameter(X[:n])
-    return X, Y, sigma, gt
-
-
-def shard(X, world, rank):
-    bounds = np.linspace(0, len(X), world + 1).astype(np.int64)
-    return X[bounds[rank]:bounds[rank + 1]]
+    return X, Y, sigma
 
 
 class ClockSampler:
@@ -152,15 +156,23 @@ def ncu_traffic(points: int):
     return None
 
 
-def cpu_baseline(X, Y, sigma, sample: int, iters: int):
-    """The oracle port (oracle/filterreg_oracle.py) on host cores: lattice built
-    on the full observation cloud (not timed), then `iters` EM iterations of the
-    same registration over a `sample`-point subset of the model cloud."""
-    from oracle import filterreg_oracle as O
+def cpu_sample(X, Y, sample: int, obs_sample: int):
+    """Bounded CPU sample of the workload: random subsets of the model and
+    observation clouds (the oracle port needs ~4 s per 1M-point lattice build
+    and ~1 s per 256k-point EM iteration)."""
     rng = np.random.default_rng(0)
-    idx = np.sort(rng.choice(len(X), min(sample, len(X)), replace=False))
-    Xs = X[idx]
-    eng = O.OracleMoments(Y, sigma, 0.1)
+    Xs = X[np.sort(rng.choice(len(X), min(sample, len(X)), replace=False))]
+    Ys = Y[np.sort(rng.choice(len(Y), min(obs_sample, len(Y)), replace=False))]
+    return Xs, Ys
+
+
+def cpu_baseline(X, Y, sigma, sample: int, obs_sample: int, iters: int):
+    """The oracle port (oracle/filterreg_oracle.py) on host cores: lattice built
+    on an observation subset (not timed), then `iters` EM iterations of the
+    same registration over a model subset."""
+    from oracle import filterreg_oracle as O
+    Xs, Ys = cpu_sample(X, Y, sample, obs_sample)
+    eng = O.OracleMoments(Ys, sigma, 0.1)
     R, t = np.eye(3), np.zeros(3)
     sinv = np.full(3, 1.0 / sigma)
     tick = time.perf_counter()
@@ -170,7 +182,7 @@ def cpu_baseline(X, Y, sigma, sample: int, iters: int):
         spec = (mom["weight"], mom["target"], sinv, "point_to_point", None, None)
         R, t, _ = O.rigid_m_step(spec, Xs, R, t)
     dt = time.perf_counter() - tick
-    return len(Xs) * iters / dt, dt, len(Xs)
+    return len(Xs) * iters / dt, dt, len(Xs), len(Ys)
 
 
 def run_reference(args):
@@ -179,13 +191,11 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    X, Y, sigma, _ = make_workload(args.points, world)
+    X, Y, sigma = make_shard(args.points, 0)
     from oracle import filterreg_oracle as O
-    rng = np.random.default_rng(0)
-    idx = np.sort(rng.choice(len(X), min(args.cpu_sample, len(X)), replace=False))
-    Xs = X[idx]
+    Xs, Ys = cpu_sample(X, Y, args.cpu_sample, args.cpu_obs)
     tick = time.perf_counter()
-    eng = O.OracleMoments(Y, sigma, 0.1)
+    eng = O.OracleMoments(Ys, sigma, 0.1)
     build_s = time.perf_counter() - tick
     R, t = np.eye(3), np.zeros(3)
     sinv = np.full(3, 1.0 / sigma)
@@ -202,7 +212,8 @@ def run_reference(args):
     value = len(Xs) * args.steps / total
     cores = 1
     sample = (f"{len(Xs)}-point random subset of the {len(X)}-point model cloud per EM "
-              f"iteration; lattice on all {len(Y)} observation points (build {build_s:.1f} s)")
+              f"iteration; lattice on a {len(Ys)}-point random subset of the {len(Y)}-point "
+              f"observation cloud (build {build_s:.1f} s, not timed)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -234,56 +245,59 @@ def run_b200(args):
     dev = torch.device("cuda", torch.cuda.current_device())
 
     import paper_1811_10136_b200 as fr
-    from paper_1811_10136_b200._rigid import RigidDevicePath
-    from paper_1811_10136_b200.pipeline import _rigid_m_step
+    from paper_1811_10136_b200 import _lib
+    from paper_1811_10136_b200._rigid import DeviceEM, RigidDevicePath
 
-    X, Y, sigma, _ = make_workload(args.points, world)
-    Xl = shard(X, world, rank)
-    M_local, M_total, N_obs = len(Xl), len(X), len(Y)
+    X, Y, sigma = make_shard(args.points, rank)
+    M_local, N_obs = len(X), len(Y)
     gmm = fr.GmmConfig(sigma=sigma, outlier_ratio=0.1)
 
+    # lattice build (splat + blur of the whole observation cloud), once per
+    # run; a warm-up build first so module loading is not timed
+    RigidDevicePath(fr.PointCloud(X[:1000]), fr.PointCloud(Y[:20000]), gmm, "point_to_point")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    path = RigidDevicePath(fr.PointCloud(Xl), fr.PointCloud(Y), gmm, "point_to_point", group)
+    path = RigidDevicePath(fr.PointCloud(X), fr.PointCloud(Y), gmm, "point_to_point", group)
     torch.cuda.synchronize()
     build_ms = 1e3 * (time.perf_counter() - t0)
+    M_total = path.M_total
     sites = path.lattice.num_sites
-
-    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
-    need_flush = 12 * M_local < 2 * L2_BYTES
-    s2 = np.full(3, 1.0 / sigma ** 2)
-    opts = fr.MStepOptions()
-    R, t = np.eye(3), np.zeros(3)
     stream = torch.cuda.current_stream()
+    l2_note = "inputs larger than L2" if 12 * M_local > L2_BYTES else "inputs smaller than L2"
 
-    def step(times=None):
-        nonlocal R, t
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record(stream)
-        sums_pass = _timed_pass(path, R, t, ev[1])
-        cand, _ = _rigid_m_step(path, sums_pass, R, t, s2, opts)
-        R, t = cand.pose.rotation, cand.pose.translation
-        ev[2].record(stream)
-        if times is not None:
-            times.append(ev)
+    # dominant kernel alone: the fused pass (+ its column reduction), R launches
+    cfg_k = fr.RegistrationConfig(gmm=gmm, max_em_iters=10 ** 6, twist_tolerance=1e-30)
+    em_k = DeviceEM(path, np.eye(3), np.zeros(3), cfg_k)
+    for _ in range(3):
+        _lib.check(path.lib.fr_rigid_em_pass(em_k.h, _lib.stream_handle()))
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        _lib.check(path.lib.fr_rigid_em_pass(em_k.h, _lib.stream_handle()))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pass_ms = e0.elapsed_time(e1) / reps
+    del em_k
 
-    for _ in range(args.warmup):
-        step()
+    # the timed EM: W warm-up iterations, then K timed iterations, all on the
+    # device (pass, reduction, [NCCL all-reduce], solver per iteration)
+    cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=args.warmup + args.steps,
+                                twist_tolerance=1e-30)
+    em = DeviceEM(path, np.eye(3), np.zeros(3), cfg)
+    em.enqueue(args.warmup)
     torch.cuda.synchronize()
     if group is not None:
         dist.barrier()
-    times = []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            if need_flush:
-                flush.zero_()
-            step(times)
+        ev[0].record(stream)
+        em.enqueue(args.steps)
+        ev[1].record(stream)
         torch.cuda.synchronize()
-    if group is not None:
-        dist.barrier()
-    step_ms = [a.elapsed_time(c) for a, _, c in times]
-    pass_ms = [a.elapsed_time(b) for a, b, _ in times]
-    total_ms = float(sum(step_ms))
+    total_ms = ev[0].elapsed_time(ev[1])
+    done, iters, term = em.status()
+    assert iters == args.warmup + args.steps, (iters, term)
     tot = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if group is not None:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -292,26 +306,22 @@ def run_b200(args):
 
     # roofline of the dominant kernel: the fused pass reads 12 B per model point
     # (float32 x, y, z); the lattice table (< L2) is not counted
-    pass_avg_ms = float(np.mean(pass_ms))
     alg_bytes = 12 * M_local
-    achieved = alg_bytes / (pass_avg_ms / 1e3) / 1e9
+    achieved = alg_bytes / (pass_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak()
     traffic = ncu_traffic(args.points)
 
     # end to end through the public API: register() from host arrays, H2D of
-    # both clouds, lattice build, K EM iterations, D2H of the pose
+    # both clouds, lattice build, K EM iterations, D2H of the result
     e2e = None
     if not args.no_e2e:
-        cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=args.steps, twist_tolerance=1e-30)
-        ref_host = fr.PointCloud(Xl)
-        obs_host = fr.PointCloud(Y)
-        fr.register(ref_host, obs_host, fr.RigidModel(), fr.RegistrationConfig(
-            gmm=gmm, max_em_iters=2, twist_tolerance=1e-30), process_group=group)
+        ecfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=args.steps, twist_tolerance=1e-30)
+        ref_host, obs_host = fr.PointCloud(X), fr.PointCloud(Y)
         torch.cuda.synchronize()
         if group is not None:
             dist.barrier()
         t0 = time.perf_counter()
-        res = fr.register(ref_host, obs_host, fr.RigidModel(), cfg, process_group=group)
+        res = fr.register(ref_host, obs_host, fr.RigidModel(), ecfg, process_group=group)
         _ = res.kinematics.pose.matrix()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
@@ -319,19 +329,20 @@ def run_b200(args):
         if group is not None:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_s = float(et.item())
-        h2d = (12 * M_local + 12 * N_obs) / args.steps
         e2e = {"value": M_total * res.iterations / e2e_s, "unit": "points/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * path.width,
+               "h2d_bytes_per_step": (12 * M_local + 12 * N_obs) / args.steps,
+               "d2h_bytes_per_step": (8 * 12 + 24 * args.steps) / args.steps,
                "em_iterations": res.iterations, "wall_s": e2e_s,
-               "includes": "H2D of model shard + observation cloud, lattice build, "
-                           "EM iterations, D2H of sums/pose"}
+               "includes": "H2D of the model shard + observation cloud, lattice build, "
+                           "EM iterations, D2H of pose and traces"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, ns = cpu_baseline(X, Y, sigma, args.cpu_sample, 4)
+        v, dt, ns, no = cpu_baseline(X, Y, sigma, args.cpu_sample, args.cpu_obs, 4)
         cpu = {"value": v, "unit": "points/s", "cores": 1, "kind": "port",
-               "sample": f"4 EM iterations over a {ns}-point subset of the model cloud, "
-                         f"lattice on all {N_obs} observation points ({dt:.1f} s)"}
+               "sample": f"4 EM iterations over a {ns}-point random subset of the model cloud "
+                         f"against a lattice on a {no}-point random subset of the observation "
+                         f"cloud ({dt:.1f} s timed; lattice build not timed)"}
 
     if rank == 0:
         line = {
@@ -339,53 +350,30 @@ def run_b200(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"C5 rigid pt2pt pebble, {args.points} clean pts/GPU + 5% "
-                                   "outliers (BASELINE configs[4])",
+            "config": {"workload": f"C5 rigid pt2pt pebble, {args.points} clean model pts/GPU "
+                                   "+ 5% outliers; observation {0} pts + 5% (BASELINE "
+                                   "configs[4])".format(args.points),
                        "points_per_gpu": M_local, "model_points_total": M_total,
                        "obs_points": N_obs, "sigma_frac": 0.05, "outlier_ratio": 0.1,
-                       "lattice_sites": sites, "build_ms": build_ms,
-                       "l2": "flushed before every timed step" if need_flush
-                       else "inputs larger than L2",
-                       "parallelism": f"dp{world} (model shards, replicated lattice)"},
+                       "lattice_sites": sites, "build_ms": build_ms, "l2": l2_note,
+                       "query_path": "float64 embedding, float32 ranks/barycentrics/table rows",
+                       "parallelism": f"dp{world} (model shards, replicated lattice, NCCL "
+                                      "all-reduce of 25 doubles per iteration)"},
             "em_iters_per_sec": args.steps / (total_ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_rigid_pass (+k_reduce_cols)",
-                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": pass_avg_ms,
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": pass_ms,
                          "peak_source": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if group is not None:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def _timed_pass(path, R, t, ev_after):
-    """run_pass with an event right after the pass kernels are enqueued (before
-    the all-reduce / D2H), so the pass duration is [step start, ev_after]."""
-    import ctypes
-    from paper_1811_10136_b200 import _lib
-    p = _lib.RigidPassParams()
-    p.R[:] = list(np.asarray(R, dtype=float).reshape(-1))
-    p.c_ref[:] = list(path.c_ref)
-    p.c_world[:] = list(path.centre(R, t))
-    p.sigma[:] = list(path.sigma)
-    p.c_prime = path.c_prime
-    p.mode = path.mode
-    p.m2_col = path.m2_col
-    p.normal_col = path.normal_col
-    _lib.check(path.lib.fr_rigid_pass(path.lattice.handle, _lib.ptr(path.ref), path.M,
-                                      ctypes.byref(p), _lib.ptr(path.sums), _lib.ptr(path.wtn),
-                                      _lib.ptr(path.scratch), _lib.stream_handle()))
-    import torch
-    ev_after.record(torch.cuda.current_stream())
-    path.reduce_device(path.sums[:path.width])
-    path.host[:path.width].copy_(path.sums[:path.width])
-    return path.host[:path.width].numpy().copy()
 
 
 def main():

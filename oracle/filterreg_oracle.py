@@ -632,6 +632,27 @@ def pebble(n, radius=0.0405):
                      r * np.cos(th)], axis=-1)
 
 
+def pebble_resample(n, seed, outlier_ratio=0.0, expansion=1.2, radius=0.0405):
+    """An independent scattered sampling of the pebble surface (same surface as
+    synth.py:69-89, sampling seed `seed`), with uniform outliers in its 1.2x
+    box -- the extra model shards of the weak-scaling benchmark."""
+    g = np.random.default_rng([_PEBBLE_SEED, seed])
+    u = g.uniform(np.cos(np.pi - 0.12), np.cos(0.12), n)
+    th = np.arccos(u)
+    ph = g.uniform(0.0, 2.0 * np.pi, n)
+    bump = (0.22 * np.sin(th) * np.cos(ph) + 0.16 * np.cos(2.0 * th) * np.sin(ph)
+            + 0.10 * np.sin(3.0 * th) * np.cos(2.0 * ph + 0.7))
+    r = radius * (1.0 + bump)
+    pts = np.stack([r * np.sin(th) * np.cos(ph), r * np.sin(th) * np.sin(ph),
+                    r * np.cos(th)], axis=-1)
+    if outlier_ratio > 0.0:
+        k = int(round(outlier_ratio * n))
+        lo, hi = pts.min(axis=0), pts.max(axis=0)
+        c, h = (lo + hi) / 2.0, (hi - lo) / 2.0 * expansion
+        pts = np.vstack([pts, c + g.uniform(-1.0, 1.0, (k, 3)) * h])
+    return pts
+
+
 def pebble_pair(n, rotation_degrees=50.0, translation_fraction=0.02,
                 outlier_ratio=0.0, seed=0, trial=0, expansion=1.2):
     """synthesize_pair for the pebble source, noise-free (synth.py:252-284)."""

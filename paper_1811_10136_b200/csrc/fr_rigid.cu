@@ -386,9 +386,10 @@ __device__ void mom_normal_eq(const Mom &m, const double *c, const double *s2, d
             H[3 + b][a] = tr[a][b];
             H[3 + a][3 + b] = a == b ? m.S0 * s2[a] : 0.0;
         }
-    g[0] = -s2[2] * XR[2][1] + s2[1] * XR[1][2];
-    g[1] = s2[2] * XR[2][0] - s2[0] * XR[0][2];
-    g[2] = -s2[1] * XR[1][0] + s2[0] * XR[0][1];
+    // sum_k e_k x (S^2 XR[:, k])
+    g[0] = s2[2] * XR[2][1] - s2[1] * XR[1][2];
+    g[1] = s2[0] * XR[0][2] - s2[2] * XR[2][0];
+    g[2] = s2[1] * XR[1][0] - s2[0] * XR[0][1];
     for (int j = 0; j < 3; ++j) g[3 + j] = s2[j] * m.R1[j];
 }
 

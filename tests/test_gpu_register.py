@@ -137,3 +137,57 @@ def test_explicit_assembly_matches_oracle(fr):
         np.testing.assert_allclose(eq.A, Ho, rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(eq.b, go, rtol=1e-10, atol=1e-12)
         assert fr.objective(spec, x) == pytest.approx(O.rigid_objective(ospec, x), rel=1e-12)
+
+
+@pytest.mark.parametrize("fast", [True, False])
+def test_device_loop_matches_host_loop(fr, fast):
+    """The device-resident EM (float64 solver kernel) reproduces the host-side
+    loop's decisions: same iterations/termination, poses to round-off."""
+    import paper_1811_10136_b200._rigid as rg
+    from paper_1811_10136_b200.pipeline import _register_device_loop
+    g = load("register_pt2pt_seed1")
+    cfg = json.loads(str(g["config"]))
+    config = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]),
+                                   max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"])
+    old = rg.FAST_QUERY
+    rg.FAST_QUERY = fast
+    try:
+        ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
+        dev = fr.register(ref, obs, fr.RigidModel(), config)            # device loop
+        host = fr.register(ref, obs, fr.RigidModel(), fr.RegistrationConfig(
+            gmm=config.gmm, max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"],
+            record_states=True))                                        # host loop
+    finally:
+        rg.FAST_QUERY = old
+    assert dev.iterations == host.iterations and dev.termination == host.termination
+    assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < 1e-9
+    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-9)
+    np.testing.assert_allclose(dev.twist_norms, host.twist_norms, rtol=1e-6, atol=1e-12)
+    assert_pose_parity(dev.kinematics.pose.rotation, dev.kinematics.pose.translation,
+                       g["R"], g["t"], O.bbox_diameter(g["X"]))
+
+
+def test_device_loop_mstep_options(fr):
+    """Extra GN iterations, explicit damping and the halving cap run through the
+    device solver with the same results as the host loop."""
+    g = load("register_pt2pt_seed2")
+    cfg = json.loads(str(g["config"]))
+    ms = fr.MStepOptions(max_gn_iters=3, damping=1e-4, max_halvings=4)
+    base = dict(gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]), max_em_iters=60,
+                twist_tolerance=cfg["tol"], mstep=ms)
+    ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
+    dev = fr.register(ref, obs, fr.RigidModel(), fr.RegistrationConfig(**base))
+    host = fr.register(ref, obs, fr.RigidModel(), fr.RegistrationConfig(**base, record_states=True))
+    assert dev.iterations == host.iterations
+    assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < 1e-9
+    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-9)
+
+
+def test_degenerate_termination(fr):
+    """Far-apart clouds: no correspondence mass -> 'degenerate' (pipeline.py:148-154)."""
+    X = np.random.default_rng(0).uniform(0, 0.1, (2000, 3))
+    Y = X + 10.0
+    res = fr.register(fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(),
+                      fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.005, outlier_ratio=0.1)))
+    assert res.termination == "degenerate" and res.iterations == 1
+    assert np.isnan(res.objectives[0]) and np.isnan(res.twist_norms[0])
