@@ -108,6 +108,14 @@ int fr_gauss_bruteforce(const double *d_q, int64_t m, const double *d_f, int64_t
                         const double *d_v, int nv, const double *sigma, double *d_out,
                         void *stream);
 
+/* Reorder a float32 SoA cloud (d_pos: `planes` planes of n, the first three
+ * x, y, z) in place along a 30-bit Morton curve of its bounding box, so that
+ * neighbouring threads of the EM pass query neighbouring simplices.  The
+ * permutation (new -> old index) is written to d_perm when not NULL.  Used
+ * once per registration on the model points: the EM sums are order-
+ * independent up to float64 round-off. */
+int fr_sort_points_morton(float *d_pos, int64_t n, int planes, int32_t *d_perm, void *stream);
+
 /* ---- E step (estep.py:186-217) ------------------------------------------ */
 
 /* MomentEngine.moments epilogue fused into the slice: d_x m x 3 float64

@@ -48,6 +48,8 @@ _E = [skew(e) for e in np.eye(3)]   # K_k = [e_k]x
 # Model points are not a bit-exact contract (the reference forms them with a
 # BLAS product), and the float32 path keeps the E-step sums to ~1e-7 relative.
 FAST_QUERY = True
+# Sort the model points along a Morton curve once per registration.
+SPATIAL_ORDER = True
 
 
 def _sym3(v6) -> np.ndarray:
@@ -161,6 +163,11 @@ class RigidDevicePath:
         hi = self._allreduce(P.max(axis=0), "max")
         self.diameter = float(np.linalg.norm(hi - lo))
         self.ref = torch.from_numpy(np.ascontiguousarray(P.T, dtype=np.float32)).to(self.dev)
+        if SPATIAL_ORDER and self.M > 1:
+            # Morton order of the model points: reduction sums are order-free up
+            # to float64 round-off, and neighbouring threads share table lines
+            _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self.ref), self.M, 3, None,
+                                                      _lib.stream_handle()))
         Y = np.asarray(observation.positions, dtype=float)
         self.N = len(Y)
         self.obs = torch.from_numpy(np.ascontiguousarray(Y.T, dtype=np.float32)).to(self.dev)

@@ -279,13 +279,19 @@ inline int nvp_for(int nv) { return nv <= 4 ? 4 : (nv <= 8 ? 8 : (nv <= 16 ? 16 
 // formed linearly from the packed remainder-0 point, and the value table
 // holds float32 rows (16 or 32 bytes: one or two float4 per vertex).
 
+// interleaved slot: packed key, then gain * value row as float32; 32 bytes
+// (one sector) for nv <= 4, 64 bytes for nv <= 8.  The hash is a 32-bit fold.
 struct SliceTableF {
-    const unsigned long long *keys;
-    const float4 *vals;     // [cap][nf4]
+    const float4 *slots;    // [cap][1 + nf4] float4; slot word 0 holds the key
     unsigned mask;
-    int shift;
-    int nf4;                // float4 per row: 1 (nv <= 4) or 2 (nv <= 8)
+    int shift32;            // 32 - log2(cap)
+    int nf4;                // value float4 per slot: 1 (nv <= 4) or 2 (nv <= 8)
 };
+
+__host__ __device__ __forceinline__ unsigned slot_hash32(unsigned long long key, int shift32) {
+    const unsigned k = (unsigned)key ^ (unsigned)(key >> 32) * 0x85EBCA6Bu;
+    return (k * 0x9E3779B1u) >> shift32;
+}
 
 struct QSimplex3 {
     unsigned long long key[4];
@@ -354,31 +360,43 @@ __device__ __forceinline__ void qsimplex3(const double *el, QSimplex3 &q) {
 }
 
 template <int NF4>
+__device__ __forceinline__ unsigned long long slot_key(const float4 *slot) {
+    return __ldg(reinterpret_cast<const unsigned long long *>(slot));
+}
+
+// gather the 4 vertex rows of one simplex; absent vertices get zero rows
+template <int NF4>
 __device__ __forceinline__ void gather_simplex_f(const SliceTableF &t, const unsigned long long *key,
-                                                 float4 (*v)[NF4], bool *hit) {
+                                                 float4 (*v)[NF4]) {
+    constexpr int W = 1 + NF4;   // float4 per slot (32 or 48 -> padded 64 bytes)
+    constexpr int S = (W == 2) ? 2 : 4;
     unsigned h[4];
     unsigned long long k[4];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-        h[l] = slot_hash(key[l], t.shift);
-        k[l] = __ldg(t.keys + h[l]);
+        h[l] = slot_hash32(key[l], t.shift32);
+        const float4 *slot = t.slots + (size_t)h[l] * S;
+        k[l] = slot_key<NF4>(slot);
 #pragma unroll
-        for (int f = 0; f < NF4; ++f) v[l][f] = __ldg(t.vals + (size_t)h[l] * NF4 + f);
+        for (int f = 0; f < NF4; ++f) v[l][f] = __ldg(slot + 1 + f);
     }
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-        hit[l] = k[l] == key[l];
-        if (!hit[l] && k[l] != kEmptyKey) {
-            unsigned s = (h[l] + 1) & t.mask;
-            for (unsigned it = 0; it <= t.mask; ++it) {
-                const unsigned long long kk = __ldg(t.keys + s);
-                if (kk == key[l]) { hit[l] = true; break; }
-                if (kk == kEmptyKey) break;
+        if (k[l] != key[l]) {
+            bool hit = false;
+            unsigned s = h[l];
+            if (k[l] != kEmptyKey) {
                 s = (s + 1) & t.mask;
+                for (unsigned it = 0; it <= t.mask; ++it) {
+                    const unsigned long long kk = slot_key<NF4>(t.slots + (size_t)s * S);
+                    if (kk == key[l]) { hit = true; break; }
+                    if (kk == kEmptyKey) break;
+                    s = (s + 1) & t.mask;
+                }
             }
-            if (hit[l])
 #pragma unroll
-                for (int f = 0; f < NF4; ++f) v[l][f] = __ldg(t.vals + (size_t)s * NF4 + f);
+            for (int f = 0; f < NF4; ++f)
+                v[l][f] = hit ? __ldg(t.slots + (size_t)s * S + 1 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
 }
@@ -417,11 +435,13 @@ struct fr_lattice {
     fr::SliceTable table() const {
         return fr::SliceTable{skeys, svals, smask, sshift, nvp};
     }
-    // float32 copy of the value rows for the fast EM pass (same slots)
-    float4 *fvals = nullptr;
+    // interleaved float32 slice table (gain folded in) for the fast EM pass
+    float4 *fslots = nullptr;
+    unsigned fmask = 0;
+    int fshift32 = 0;
     int nf4 = 0;
     fr::SliceTableF table_f() const {
-        return fr::SliceTableF{skeys, fvals, smask, sshift, nf4};
+        return fr::SliceTableF{fslots, fmask, fshift32, nf4};
     }
     // device counters / flags
     unsigned long long *d_counters = nullptr;   // [0] sites, [1] src count, [2] overflow

@@ -743,23 +743,37 @@ static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
 static void free_slice(fr_lattice *lat) {
     cudaFree(lat->skeys);
     cudaFree(lat->svals);
-    cudaFree(lat->fvals);
+    cudaFree(lat->fslots);
     lat->skeys = nullptr;
     lat->svals = nullptr;
-    lat->fvals = nullptr;
+    lat->fslots = nullptr;
     lat->nvp = 0;
     lat->nf4 = 0;
 }
 
-// float32 rows of the slice table for the fast EM pass (nv <= 8)
-__global__ void k_slice_to_f32(long long cap, const double *svals, int nvp, int nf4,
-                               float4 *fvals) {
-    long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= cap) return;
-    for (int f = 0; f < nf4; ++f) {
-        const double *r = svals + s * nvp + 4 * f;
-        fvals[s * nf4 + f] = make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]);
+// interleaved float32 slice table for the fast EM pass (nv <= 8): slot =
+// [packed key | pad][gain * values as float4 x nf4], 32 or 64 bytes
+template <int D>
+__global__ void k_fslice_insert(long long S, const int *site_keys, const double *vals, int nv,
+                                double gain, float4 *slots, int stride4, int nf4, unsigned mask,
+                                int shift32, unsigned long long *counters) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    const unsigned long long key = pack_key<D>(site_keys + i * (D + 1));
+    unsigned s = slot_hash32(key, shift32);
+    for (unsigned it = 0; it <= mask; ++it) {
+        unsigned long long *kw = reinterpret_cast<unsigned long long *>(slots + (size_t)s * stride4);
+        if (atomicCAS(kw, kEmptyKey, key) == kEmptyKey) {
+            float v[8];
+            for (int c = 0; c < 8; ++c) v[c] = c < nv ? (float)(gain * vals[i * nv + c]) : 0.0f;
+            for (int f = 0; f < nf4; ++f)
+                slots[(size_t)s * stride4 + 1 + f] =
+                    make_float4(v[4 * f], v[4 * f + 1], v[4 * f + 2], v[4 * f + 3]);
+            return;
+        }
+        s = (s + 1) & mask;
     }
+    atomicOr(&counters[2], 2ull);
 }
 
 template <int D>
@@ -784,11 +798,18 @@ static int build_slice_table(fr_lattice *lat, cudaStream_t s) {
         FR_CHECK_LAUNCH();
     }
     if (lat->nv <= 8) {
-        lat->nf4 = lat->nvp / 4;
-        FR_CUDA(cudaMalloc(&lat->fvals, (size_t)cap * lat->nf4 * sizeof(float4)));
-        k_slice_to_f32<<<grid_for(cap), 256, 0, s>>>(cap, lat->svals, lat->nvp, lat->nf4,
-                                                     lat->fvals);
-        FR_CHECK_LAUNCH();
+        lat->nf4 = lat->nv <= 4 ? 1 : 2;
+        const int stride4 = lat->nf4 == 1 ? 2 : 4;
+        FR_CUDA(cudaMalloc(&lat->fslots, (size_t)cap * stride4 * sizeof(float4)));
+        FR_CUDA(cudaMemsetAsync(lat->fslots, 0xff, (size_t)cap * stride4 * sizeof(float4), s));
+        lat->fmask = cap - 1;
+        lat->fshift32 = 32 - bits;
+        if (lat->n_sites > 0) {
+            k_fslice_insert<D><<<grid_for(lat->n_sites), 256, 0, s>>>(
+                lat->n_sites, lat->site_keys, lat->vals, lat->nv, lat->c.gain, lat->fslots,
+                stride4, lat->nf4, lat->fmask, lat->fshift32, lat->d_counters);
+            FR_CHECK_LAUNCH();
+        }
     }
     unsigned long long hc[3];
     FR_TRY(read_counters(lat, s, hc));
@@ -879,6 +900,42 @@ static int slice_impl(const fr_lattice *lat, const double *Q, long long m, doubl
 
 }  // namespace fr
 
+// ---------------------------------------------------------------------------
+// spatial (Morton) ordering of a point cloud: neighbouring threads then query
+// neighbouring simplices, so slice-table gathers hit L1 and coalesce
+
+__device__ __forceinline__ unsigned spread10(unsigned v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void k_morton(const float *pos, long long n, const float *lo, const float *hi,
+                         unsigned *codes, unsigned *idx) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned c = 0;
+    for (int a = 0; a < 3; ++a) {
+        const float span = fmaxf(hi[a] - lo[a], 1e-30f);
+        const float u = (pos[a * n + i] - lo[a]) / span;
+        const unsigned q = (unsigned)fminf(fmaxf(u * 1023.0f, 0.0f), 1023.0f);
+        c |= spread10(q) << (2 - a);
+    }
+    codes[i] = c;
+    idx[i] = (unsigned)i;
+}
+
+__global__ void k_gather_planes(const float *src, long long n, int planes, const unsigned *perm,
+                                float *dst) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned j = perm[i];
+    for (int a = 0; a < planes; ++a) dst[a * n + i] = src[a * n + j];
+}
+
 // ===========================================================================
 // C ABI
 
@@ -895,6 +952,50 @@ using namespace fr;
 extern "C" {
 
 int fr_abi_version(void) { return 1; }
+
+int fr_sort_points_morton(float *pos, int64_t n, int planes, int32_t *perm_out, void *stream) {
+    if (!pos || n < 0 || planes < 3) {
+        set_error("invalid Morton sort arguments");
+        return FR_EINVAL;
+    }
+    if (n < 2) return FR_OK;
+    if (n >= (1LL << 31)) {
+        set_error("too many points to sort");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch sc(s);
+    float *lohi, *tmp;
+    unsigned *codes, *codes2, *idx, *perm;
+    FR_TRY(sc.get(&lohi, 6));
+    FR_TRY(sc.get(&codes, n));
+    FR_TRY(sc.get(&codes2, n));
+    FR_TRY(sc.get(&idx, n));
+    FR_TRY(sc.get(&perm, n));
+    FR_TRY(sc.get(&tmp, (size_t)n * planes));
+    size_t tb = 0, t2 = 0;
+    FR_CUDA(cub::DeviceReduce::Min(nullptr, tb, pos, lohi, (int)n, s));
+    FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, codes, codes2, idx, perm, (int)n, 0, 30, s));
+    void *tmpb;
+    FR_TRY(sc.get((char **)&tmpb, std::max(tb, t2)));
+    for (int a = 0; a < 3; ++a) {
+        size_t tt = std::max(tb, t2);
+        FR_CUDA(cub::DeviceReduce::Min(tmpb, tt, pos + a * n, lohi + a, (int)n, s));
+        tt = std::max(tb, t2);
+        FR_CUDA(cub::DeviceReduce::Max(tmpb, tt, pos + a * n, lohi + 3 + a, (int)n, s));
+    }
+    k_morton<<<grid_for(n), 256, 0, s>>>(pos, n, lohi, lohi + 3, codes, idx);
+    FR_CHECK_LAUNCH();
+    size_t tt = std::max(tb, t2);
+    FR_CUDA(cub::DeviceRadixSort::SortPairs(tmpb, tt, codes, codes2, idx, perm, (int)n, 0, 30, s));
+    k_gather_planes<<<grid_for(n), 256, 0, s>>>(pos, n, planes, perm, tmp);
+    FR_CHECK_LAUNCH();
+    FR_CUDA(cudaMemcpyAsync(pos, tmp, (size_t)n * planes * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    if (perm_out)
+        FR_CUDA(cudaMemcpyAsync(perm_out, perm, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    return FR_OK;
+}
 
 const char *fr_last_error(void) { return fr::last_error(); }
 

@@ -105,34 +105,31 @@ __device__ __forceinline__ void slice_point_exact(const double *el, const SliceT
     }
 }
 
-// slice at one model point, float32 ranks / barycentrics / table rows
+// slice at one model point, float32 ranks / barycentrics / table rows; the
+// table rows already carry the gain, so out[] is the finished kernel sum
 template <int NV>
 __device__ __forceinline__ void slice_point_fast(const double *el, const SliceTableF &tab,
-                                                 double *out) {
+                                                 float *out) {
     constexpr int NF4 = (NV + 3) / 4;
     QSimplex3 q;
     qsimplex3(el, q);
-    float acc[4 * NF4];
 #pragma unroll
-    for (int c = 0; c < 4 * NF4; ++c) acc[c] = 0.0f;
+    for (int c = 0; c < 4 * NF4; ++c) out[c] = 0.0f;
     if (!q.overflow) {
         float4 v[4][NF4];
-        bool hit[4];
-        gather_simplex_f<NF4>(tab, q.key, v, hit);
+        gather_simplex_f<NF4>(tab, q.key, v);
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            const float b = hit[l] ? q.bary[l] : 0.0f;
+            const float b = q.bary[l];
 #pragma unroll
             for (int f = 0; f < NF4; ++f) {
-                acc[4 * f] = fmaf(b, v[l][f].x, acc[4 * f]);
-                acc[4 * f + 1] = fmaf(b, v[l][f].y, acc[4 * f + 1]);
-                acc[4 * f + 2] = fmaf(b, v[l][f].z, acc[4 * f + 2]);
-                acc[4 * f + 3] = fmaf(b, v[l][f].w, acc[4 * f + 3]);
+                out[4 * f] = fmaf(b, v[l][f].x, out[4 * f]);
+                out[4 * f + 1] = fmaf(b, v[l][f].y, out[4 * f + 1]);
+                out[4 * f + 2] = fmaf(b, v[l][f].z, out[4 * f + 2]);
+                out[4 * f + 3] = fmaf(b, v[l][f].w, out[4 * f + 3]);
             }
         }
     }
-#pragma unroll
-    for (int c = 0; c < NV; ++c) out[c] = (double)acc[c];
 }
 
 template <int MODE, int NV, bool SIG, bool FAST, bool DEV>
@@ -149,10 +146,24 @@ k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK
 #pragma unroll
     for (int a = 0; a < NA; ++a) acc[a] = 0.0;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
-        const double xh[3] = {(double)__ldg(ref + p) - k.c_ref[0],
-                              (double)__ldg(ref + m + p) - k.c_ref[1],
-                              (double)__ldg(ref + 2 * m + p) - k.c_ref[2]};
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // software prefetch of the next point's float32 position (hides the HBM
+    // latency behind this point's work)
+    float nx = 0.f, ny = 0.f, nz = 0.f;
+    if (p < m) {
+        nx = __ldg(ref + p);
+        ny = __ldg(ref + m + p);
+        nz = __ldg(ref + 2 * m + p);
+    }
+    for (; p < m; p += stride) {
+        const double xh[3] = {(double)nx - k.c_ref[0], (double)ny - k.c_ref[1],
+                              (double)nz - k.c_ref[2]};
+        const long long pn = p + stride;
+        if (pn < m) {
+            nx = __ldg(ref + pn);
+            ny = __ldg(ref + m + pn);
+            nz = __ldg(ref + 2 * m + pn);
+        }
         double xt[3], x[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -164,15 +175,34 @@ k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK
         for (int i = 0; i < 4; ++i)
             el[i] = fma(k.M[i][2], xh[2], fma(k.M[i][1], xh[1], fma(k.M[i][0], xh[0], k.e0[i])));
         double out[NV];
-        if (FAST) slice_point_fast<NV>(el, tabf, out);
-        else slice_point_exact<NV>(el, tab, out);
-        const double m0 = fmax(k.gain * out[0], 0.0);
-        const bool sup = m0 >= 1e-12;
-        const double w = sup ? (k.cp > 0.0 ? m0 / (m0 + k.cp) : 1.0) : 0.0;
-        const double inv = sup ? 1.0 / m0 : 0.0;
-        double t[3];
+        double m0, w, t[3];
+        bool sup;
+        if (FAST) {
+            // float32 epilogue (estep.py:195-205) on the float32 kernel sums
+            float o[4 * ((NV + 3) / 4)];
+            slice_point_fast<NV>(el, tabf, o);
+            const float m0f = fmaxf(o[0], 0.0f);
+            sup = m0f >= 1e-12f;
+            const float cpf = (float)k.cp;
+            const float wf = sup ? (cpf > 0.0f ? __fdividef(m0f, m0f + cpf) : 1.0f) : 0.0f;
+            const float invf = sup ? __frcp_rn(m0f) : 0.0f;
+            m0 = (double)m0f;
+            w = (double)wf;
 #pragma unroll
-        for (int j = 0; j < 3; ++j) t[j] = sup ? (k.gain * out[1 + j]) * inv : x[j];
+            for (int j = 0; j < 3; ++j) t[j] = sup ? (double)(o[1 + j] * invf) : x[j];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) out[q] = (double)o[q];
+        } else {
+            slice_point_exact<NV>(el, tab, out);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) out[q] *= k.gain;
+            m0 = fmax(out[0], 0.0);
+            sup = m0 >= 1e-12;
+            w = sup ? (k.cp > 0.0 ? m0 / (m0 + k.cp) : 1.0) : 0.0;
+            const double inv = sup ? 1.0 / m0 : 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) t[j] = sup ? out[1 + j] * inv : x[j];
+        }
         if (MODE == FR_POINT_TO_POINT) {
             // branch-free: unsupported points have w = 0 and t = x
             double r[3], wy[3];
@@ -202,9 +232,10 @@ k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK
             // point_to_plane: averaged normal and validity (estep.py:209-215)
             double n[3] = {0.0, 0.0, 0.0};
             if (sup) {
+                const double inv = 1.0 / m0;
                 double a[3];
 #pragma unroll
-                for (int j = 0; j < 3; ++j) a[j] = (k.gain * out[k.ncol + j]) * inv;
+                for (int j = 0; j < 3; ++j) a[j] = out[k.ncol + j] * inv;
                 const double len = sqrt((a[0] * a[0] + a[1] * a[1]) + a[2] * a[2]);
                 if (len >= 0.1) {
 #pragma unroll
@@ -267,11 +298,10 @@ k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK
             constexpr int B = (MODE == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase);
             const double den = m0 + k.cp;
             const double xx = (x[0] * x[0] + x[1] * x[1]) + x[2] * x[2];
-            const double xm = (x[0] * (k.gain * out[1]) + x[1] * (k.gain * out[2])) +
-                              x[2] * (k.gain * out[3]);
+            const double xm = (x[0] * out[1] + x[1] * out[2]) + x[2] * out[3];
             double m2v = 0.0;
 #pragma unroll
-            for (int q = 0; q < NV; ++q) m2v = (q == k.m2_col) ? k.gain * out[q] : m2v;
+            for (int q = 0; q < NV; ++q) m2v = (q == k.m2_col) ? out[q] : m2v;
             acc[B] += (m0 * xx - 2.0 * xm + m2v) / den;
             acc[B + 1] += m0 / den;
         }
@@ -707,7 +737,7 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, bool fast, boo
                        const int *done, float *wtn, double *scratch, double *sums,
                        cudaStream_t s) {
     const int nv = lat->nv;
-    fast = fast && !sig && lat->fvals != nullptr;
+    fast = fast && !sig && lat->fslots != nullptr;
 #define FR_L(MODE, NV, SIG, FAST, DEV) \
     return launch_pass_t<MODE, NV, SIG, FAST, DEV>(lat, ref, m, k, kd, done, wtn, scratch, sums, s)
     if (mode == FR_POINT_TO_POINT) {
