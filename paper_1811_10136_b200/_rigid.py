@@ -129,6 +129,17 @@ class RigidMoments:
         return RigidMoments(self.S0, S1n, S2n, R1n, RXn, Qn)
 
 
+def upload_soa(points, dev):
+    """(n, 3) host coordinates -> (3, n) float32 device planes: one float32
+    conversion on the host (12 B/point over PCIe), the transpose on the device."""
+    import torch
+    host = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float32))
+    aos = host.to(dev, non_blocking=False)
+    soa = torch.empty((3, aos.shape[0]), dtype=torch.float32, device=dev)
+    soa.copy_(aos.t())
+    return soa
+
+
 def unpack_upper6(v21) -> np.ndarray:
     H = np.zeros((6, 6))
     o = 0
@@ -150,33 +161,31 @@ class RigidDevicePath:
         self.mode = _lib.FR_POINT_TO_PLANE if residual_mode == "point_to_plane" \
             else _lib.FR_POINT_TO_POINT
         self.gmm = gmm
-        P = np.asarray(reference.positions, dtype=float)
-        self.M = len(P)
         self.group = process_group
+        self.ref = upload_soa(reference.positions, self.dev)
+        self.M = self.ref.shape[1]
         # global quantities a shard must not compute locally:
         # total model count (outlier constant, degenerate test), the centre of
         # the whole reference cloud and its bounding-box diameter
-        tot = self._allreduce(np.concatenate([[float(self.M)], P.sum(axis=0)]), "sum")
+        local_sum = self.ref.sum(dim=1, dtype=torch.float64).cpu().numpy()
+        tot = self._allreduce(np.concatenate([[float(self.M)], local_sum]), "sum")
         self.M_total = int(round(tot[0]))
         self.c_ref = tot[1:] / tot[0]
-        lo = self._allreduce(P.min(axis=0), "min")
-        hi = self._allreduce(P.max(axis=0), "max")
+        lo = self._allreduce(self.ref.amin(dim=1).double().cpu().numpy(), "min")
+        hi = self._allreduce(self.ref.amax(dim=1).double().cpu().numpy(), "max")
         self.diameter = float(np.linalg.norm(hi - lo))
-        self.ref = torch.from_numpy(np.ascontiguousarray(P.T, dtype=np.float32)).to(self.dev)
         if SPATIAL_ORDER and self.M > 1:
             # Morton order of the model points: reduction sums are order-free up
             # to float64 round-off, and neighbouring threads share table lines
             _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self.ref), self.M, 3, None,
                                                       _lib.stream_handle()))
-        Y = np.asarray(observation.positions, dtype=float)
-        self.N = len(Y)
-        self.obs = torch.from_numpy(np.ascontiguousarray(Y.T, dtype=np.float32)).to(self.dev)
+        self.obs = upload_soa(observation.positions, self.dev)
+        self.N = self.obs.shape[1]
         self.obs_n = None
         if self.mode == _lib.FR_POINT_TO_PLANE:
             if observation.normals is None:
                 raise ValueError("observation cloud has no normals")
-            self.obs_n = torch.from_numpy(
-                np.ascontiguousarray(observation.normals.T, dtype=np.float32)).to(self.dev)
+            self.obs_n = upload_soa(observation.normals, self.dev)
         self.with_sigma = bool(gmm.update_sigma)
         self.value_mode = (_lib.FR_VALUES_M2 if self.with_sigma else 0) | \
             (_lib.FR_VALUES_NORMALS if self.obs_n is not None else 0)

@@ -169,57 +169,49 @@ __global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash
     }
 }
 
-// splat phase 2a: every contribution bary * value in site-sorted order (each
-// product is one rounding, computed in parallel -- same bits as NumPy's)
-template <int D, class Src>
-__global__ void k_splat_contrib(Src src, long long E, const unsigned *sorted_slot,
-                                const unsigned *sorted_idx, const double *entry_bary,
-                                unsigned sentinel, int nv, double *contrib) {
-    long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < E; j += stride) {
-        if (sorted_slot[j] == sentinel) continue;
-        const unsigned e = sorted_idx[j];
-        const double b = entry_bary[e];
-        const long long p = e / (D + 1);
-        for (int cc = 0; cc < nv; ++cc) contrib[j * nv + cc] = __dmul_rn(b, src.value(p, cc));
-    }
-}
+// splat phase 2: one warp per site.  The lanes form 32 contributions
+// bary * value at a time (one rounding each, as NumPy's product) and stage
+// them in shared memory; lane 0 adds them in flat (point, vertex) order --
+// np.add.at's accumulation order (permutohedral.py:241-242), hence
+// bit-identical sums -- while the lanes already gather the next 32.
+constexpr int kSegWarps = 4;
 
-// splat phase 2b: one thread per (site, 4 channels) adds its contiguous run
-// of contributions sequentially in flat (point, vertex) order -- np.add.at's
-// accumulation order (permutohedral.py:241-242), hence bit-identical sums
-__global__ void k_splat_segsum(int n_runs, const unsigned *run_slot, const int *run_off,
-                               const int *run_cnt, const double *contrib, unsigned sentinel,
-                               int nv, double *run_vals) {
-    const int chunks = (nv + 3) / 4;
-    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= (long long)n_runs * chunks) return;
-    const int r = (int)(tid / chunks), c0 = (int)(tid % chunks) * 4;
-    if (run_slot[r] == sentinel) return;
-    const int w = min(4, nv - c0);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    const double *row = contrib + (long long)run_off[r] * nv + c0;
-    const int cnt = run_cnt[r];
-    constexpr int U = 8;
-    int j = 0;
-    for (; j + U <= cnt; j += U) {
-        double v[U][4];
+template <int D, class Src>
+__global__ void __launch_bounds__(32 * kSegWarps)
+k_splat_segsum(Src src, int n_runs, const unsigned *run_slot, const int *run_off,
+               const int *run_cnt, const unsigned *sorted_idx, const double *entry_bary,
+               unsigned sentinel, int nv, double *run_vals) {
+    __shared__ double buf[kSegWarps][2][32][16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * kSegWarps + warp;
+    if (r >= n_runs || run_slot[r] == sentinel) return;
+    const int beg = run_off[r], cnt = run_cnt[r];
+    double acc[16];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[u][k] = k < w ? row[(long long)(j + u) * nv + k] : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] = __dadd_rn(acc[k], v[u][k]);
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    const int chunks = (cnt + 31) / 32;
+    auto stage = [&](int ch, int slot) {
+        const int j = ch * 32 + lane;
+        if (j < cnt) {
+            const unsigned e = sorted_idx[beg + j];
+            const double b = entry_bary[e];
+            const long long p = e / (D + 1);
+            for (int c = 0; c < nv; ++c) buf[warp][slot][lane][c] = __dmul_rn(b, src.value(p, c));
+        }
+    };
+    stage(0, 0);
+    __syncwarp();
+    for (int ch = 0; ch < chunks; ++ch) {
+        if (ch + 1 < chunks) stage(ch + 1, (ch + 1) & 1);
+        if (lane == 0) {
+            const int n = min(32, cnt - ch * 32);
+            for (int i = 0; i < n; ++i)
+                for (int c = 0; c < nv; ++c) acc[c] = __dadd_rn(acc[c], buf[warp][ch & 1][i][c]);
+        }
+        __syncwarp();
     }
-    for (; j < cnt; ++j)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (k < w) acc[k] = __dadd_rn(acc[k], row[(long long)j * nv + k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (k < w) run_vals[(long long)r * nv + c0 + k] = acc[k];
+    if (lane == 0)
+        for (int c = 0; c < nv; ++c) run_vals[(long long)r * nv + c] = acc[c];
 }
 
 __global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentinel,
@@ -621,11 +613,13 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     size_t tmp_bytes = 0, t2 = 0;
     FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, entry_slot, sorted_slot,
                                             entry_idx, sorted_idx, (int)E, 0, end_bit, s));
+    // runs = distinct slots (+ the sentinel run): hc[0] counted the CAS winners
+    const long long max_runs = (long long)hc[0] + 2;
     unsigned *run_slot;
     int *run_cnt, *run_off, *d_nruns;
-    FR_TRY(sc.get(&run_slot, E));
-    FR_TRY(sc.get(&run_cnt, E));
-    FR_TRY(sc.get(&run_off, E));
+    FR_TRY(sc.get(&run_slot, max_runs));
+    FR_TRY(sc.get(&run_cnt, max_runs));
+    FR_TRY(sc.get(&run_off, max_runs));
     FR_TRY(sc.get(&d_nruns, 1));
     FR_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, sorted_slot, run_slot, run_cnt,
                                                d_nruns, (int)E, s));
@@ -651,14 +645,10 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_TRY(sc.get(&iota, nruns));
     FR_TRY(sc.get(&d_nlive, 1));
     {
-        double *contrib;
-        FR_TRY(sc.get(&contrib, (size_t)E * nv));
-        k_splat_contrib<D, Src><<<grid_for(E), 256, 0, s>>>(src, E, sorted_slot, sorted_idx,
-                                                            entry_bary, (unsigned)cap, nv, contrib);
-        FR_CHECK_LAUNCH();
-        const long long work = (long long)nruns * ((nv + 3) / 4);
-        k_splat_segsum<<<grid_for(work, 64), 64, 0, s>>>(nruns, run_slot, run_off, run_cnt, contrib,
-                                                         (unsigned)cap, nv, run_vals);
+        const unsigned blocks = (unsigned)((nruns + kSegWarps - 1) / kSegWarps);
+        k_splat_segsum<D, Src><<<std::max(blocks, 1u), 32 * kSegWarps, 0, s>>>(
+            src, nruns, run_slot, run_off, run_cnt, sorted_idx, entry_bary, (unsigned)cap, nv,
+            run_vals);
         FR_CHECK_LAUNCH();
         k_run_live<<<grid_for(nruns), 256, 0, s>>>(nruns, run_slot, (unsigned)cap, run_vals, nv,
                                                    run_live);
@@ -1006,6 +996,21 @@ int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
     }
     LatticeConsts c;
     FR_TRY(make_consts(dim, sigma, &c));
+    {
+        // keep the stream-ordered pool's pages mapped between builds (a splat
+        // at 16.8M points stages ~2 GB of sort scratch)
+        static bool pool_set = false;
+        if (!pool_set) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess &&
+                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                unsigned long long keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            pool_set = true;
+        }
+    }
     fr_lattice *lat = new fr_lattice();
     lat->c = c;
     lat->dim = dim;
