@@ -184,6 +184,32 @@ int fr_rigid_objective(const float *d_ref, const float *d_wtn, int64_t m,
                        const double *cand_c, double *d_out, double *d_scratch,
                        void *stream);
 
+/* ---- articulated trees (mstep.py:179-202, 213-229; kinematics.py:317-336) --
+ * Model points sorted by body; chunk i = points [chunk_beg[i], chunk_beg[i+1])
+ * of body chunk_body[i]; body b owns chunks [body_chunks[b], body_chunks[b+1]).
+ * One pass gives per-body statistics (fr_rigid_pass_width(mode, 0) doubles
+ * per body, same layout as the rigid pass, each about the body's own centre
+ * c_world = R_b c_ref_b + t_b); the host projects H_b, g_b through the
+ * spatial velocity Jacobians.  d_params: >= fr_body_params_doubles(n) doubles
+ * (n = n_bodies for the pass, n_bodies * k for the objective). */
+typedef struct fr_body_pose {
+    double R[9];
+    double c_ref[3];
+    double c_world[3];
+} fr_body_pose;
+
+int fr_body_params_doubles(int n);
+int fr_body_pass(const fr_lattice *lat, const float *d_ref, int64_t m, const fr_body_pose *poses,
+                 int n_bodies, const int32_t *d_chunk_body, const int64_t *d_chunk_beg,
+                 int n_chunks, const int32_t *d_body_chunks, int mode, double c_prime, int flags,
+                 double *d_params, double *d_sums, float *d_wtn, double *d_scratch,
+                 void *stream);
+/* point_to_plane halving candidates: cand[c * n_bodies + b]; d_out 16 doubles */
+int fr_body_objective(const float *d_ref, const float *d_wtn, int64_t m,
+                      const fr_body_pose *cand, int n_bodies, int k,
+                      const int32_t *d_chunk_body, const int64_t *d_chunk_beg, int n_chunks,
+                      double *d_params, double *d_out, double *d_scratch, void *stream);
+
 /* ---- device-resident rigid EM loop (pipeline.py:141-181, point_to_point) --
  * The whole EM iteration stays on the GPU: fused pass, fixed-order reduction,
  * and a one-thread float64 solver kernel that assembles the normal equations

@@ -132,38 +132,13 @@ __device__ __forceinline__ void slice_point_fast(const double *el, const SliceTa
     }
 }
 
-template <int MODE, int NV, bool SIG, bool FAST, bool DEV>
-__global__ void __launch_bounds__(kPassThreads, MODE == FR_POINT_TO_POINT ? 2 : 1)
-k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
-             const int *done, SliceTable tab, SliceTableF tabf, float *__restrict__ wtn,
-             double *__restrict__ partials) {
-    constexpr int NA = (MODE == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase) + (SIG ? 2 : 0);
-    __shared__ RigidK k;
-    if (DEV && *done) return;
-    if (threadIdx.x == 0) k = DEV ? *kd : kv;
-    __syncthreads();
-    double acc[NA];
-#pragma unroll
-    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    // software prefetch of the next point's float32 position (hides the HBM
-    // latency behind this point's work)
-    float nx = 0.f, ny = 0.f, nz = 0.f;
-    if (p < m) {
-        nx = __ldg(ref + p);
-        ny = __ldg(ref + m + p);
-        nz = __ldg(ref + 2 * m + p);
-    }
-    for (; p < m; p += stride) {
-        const double xh[3] = {(double)nx - k.c_ref[0], (double)ny - k.c_ref[1],
-                              (double)nz - k.c_ref[2]};
-        const long long pn = p + stride;
-        if (pn < m) {
-            nx = __ldg(ref + pn);
-            ny = __ldg(ref + m + pn);
-            nz = __ldg(ref + 2 * m + pn);
-        }
+// one model point of the EM pass: forward map, slice, epilogue, residual
+// statistics into acc (and, for point_to_plane, the stored w / t / n planes)
+template <int MODE, int NV, bool SIG, bool FAST, int NA>
+__device__ __forceinline__ void point_step(const RigidK &k, const SliceTable &tab,
+                                           const SliceTableF &tabf, const double *xh,
+                                           long long p, long long m, float *__restrict__ wtn,
+                                           double (&acc)[NA]) {
         double xt[3], x[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -305,8 +280,79 @@ k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK
             acc[B] += (m0 * xx - 2.0 * xm + m2v) / den;
             acc[B + 1] += m0 / den;
         }
+}
+
+template <int MODE, int NV, bool SIG, bool FAST, bool DEV>
+__global__ void __launch_bounds__(kPassThreads, MODE == FR_POINT_TO_POINT ? 2 : 1)
+k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
+             const int *done, SliceTable tab, SliceTableF tabf, float *__restrict__ wtn,
+             double *__restrict__ partials) {
+    constexpr int NA = (MODE == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase) + (SIG ? 2 : 0);
+    __shared__ RigidK k;
+    if (DEV && *done) return;
+    if (threadIdx.x == 0) k = DEV ? *kd : kv;
+    __syncthreads();
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // software prefetch of the next point's float32 position (hides the HBM
+    // latency behind this point's work)
+    float nx = 0.f, ny = 0.f, nz = 0.f;
+    if (p < m) {
+        nx = __ldg(ref + p);
+        ny = __ldg(ref + m + p);
+        nz = __ldg(ref + 2 * m + p);
+    }
+    for (; p < m; p += stride) {
+        const double xh[3] = {(double)nx - k.c_ref[0], (double)ny - k.c_ref[1],
+                              (double)nz - k.c_ref[2]};
+        const long long pn = p + stride;
+        if (pn < m) {
+            nx = __ldg(ref + pn);
+            ny = __ldg(ref + m + pn);
+            nz = __ldg(ref + 2 * m + pn);
+        }
+        point_step<MODE, NV, SIG, FAST, NA>(k, tab, tabf, xh, p, m, wtn, acc);
     }
     block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
+}
+
+// articulated pass (mstep.py:179-202, 213-229): model points sorted by body,
+// block b sweeps chunk b (one body) with that body's pose; partials per chunk
+template <int MODE, int NV, bool SIG, bool FAST>
+__global__ void __launch_bounds__(kPassThreads, MODE == FR_POINT_TO_POINT ? 2 : 1)
+k_body_pass(const float *__restrict__ ref, long long m, const RigidK *__restrict__ bodies,
+            const int *__restrict__ chunk_body, const long long *__restrict__ chunk_beg,
+            SliceTable tab, SliceTableF tabf, float *__restrict__ wtn,
+            double *__restrict__ partials) {
+    constexpr int NA = (MODE == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase) + (SIG ? 2 : 0);
+    __shared__ RigidK k;
+    const long long beg = chunk_beg[blockIdx.x], end = chunk_beg[blockIdx.x + 1];
+    if (threadIdx.x == 0) k = bodies[chunk_body[blockIdx.x]];
+    __syncthreads();
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+    for (long long p = beg + threadIdx.x; p < end; p += blockDim.x) {
+        const double xh[3] = {(double)__ldg(ref + p) - k.c_ref[0],
+                              (double)__ldg(ref + m + p) - k.c_ref[1],
+                              (double)__ldg(ref + 2 * m + p) - k.c_ref[2]};
+        point_step<MODE, NV, SIG, FAST, NA>(k, tab, tabf, xh, p, m, wtn, acc);
+    }
+    block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
+}
+
+// per-segment column sums: segment s = chunks [seg[s], seg[s+1]), fixed order
+__global__ void k_reduce_segments(const double *partials, const int *seg, int na, double *out) {
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31, s = blockIdx.x;
+    if (c >= na) return;
+    double v = 0.0;
+    for (int b = seg[s] + lane; b < seg[s + 1]; b += 32) v += partials[(long long)b * na + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) out[(long long)s * na + c] = v;
 }
 
 // candidate objectives for point_to_plane halving
@@ -344,6 +390,43 @@ k_rigid_objective(const float *__restrict__ ref, const float *__restrict__ wtn, 
                                       fma(ck.R[c][3 * i + 1], xh[1], ck.R[c][3 * i] * xh[0]));
                 x[i] = xt + ck.c[c][i];
             }
+            acc[c] += pt2pl_cost(w, t, n, x);
+        }
+    }
+    block_reduce_store<kMaxCand>(acc, partials + (long long)blockIdx.x * kMaxCand);
+}
+
+// point_to_plane halving candidates for articulated trees: candidate c moves
+// body b with cand[c * n_bodies + b] (R, c_world); one objective per candidate
+__global__ void __launch_bounds__(kPassThreads, 2)
+k_body_objective(const float *__restrict__ ref, const float *__restrict__ wtn, long long m,
+                 const RigidK *__restrict__ cand, int n_bodies, int ncand,
+                 const int *__restrict__ chunk_body, const long long *__restrict__ chunk_beg,
+                 double *__restrict__ partials) {
+    double acc[kMaxCand];
+#pragma unroll
+    for (int a = 0; a < kMaxCand; ++a) acc[a] = 0.0;
+    const int body = chunk_body[blockIdx.x];
+    const long long beg = chunk_beg[blockIdx.x], end = chunk_beg[blockIdx.x + 1];
+    for (long long p = beg + threadIdx.x; p < end; p += blockDim.x) {
+        const double w = (double)__ldg(wtn + p);
+        if (!(w > 0.0)) continue;
+        const double t[3] = {(double)__ldg(wtn + m + p), (double)__ldg(wtn + 2 * m + p),
+                             (double)__ldg(wtn + 3 * m + p)};
+        const double n[3] = {(double)__ldg(wtn + 4 * m + p), (double)__ldg(wtn + 5 * m + p),
+                             (double)__ldg(wtn + 6 * m + p)};
+        const float px = __ldg(ref + p), py = __ldg(ref + m + p), pz = __ldg(ref + 2 * m + p);
+#pragma unroll
+        for (int c = 0; c < kMaxCand; ++c) {
+            if (c >= ncand) break;
+            const RigidK &k = cand[c * n_bodies + body];
+            const double xh[3] = {(double)px - k.c_ref[0], (double)py - k.c_ref[1],
+                                  (double)pz - k.c_ref[2]};
+            double x[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                x[i] = fma(k.R[3 * i + 2], xh[2], fma(k.R[3 * i + 1], xh[1], k.R[3 * i] * xh[0])) +
+                       k.c_world[i];
             acc[c] += pt2pl_cost(w, t, n, x);
         }
     }
@@ -860,6 +943,101 @@ int fr_rigid_objective(const float *ref, const float *wtn, int64_t m, const doub
     FR_CHECK_LAUNCH();
     return FR_OK;
 }
+
+// ---- articulated trees (per-body statistics) --------------------------------
+
+static int body_params(const fr_lattice *lat, const fr_body_pose *poses, int n, double cp,
+                       int ncol, std::vector<RigidK> &out) {
+    double A[4][3];
+    embedding_matrix(lat->c, A);
+    out.resize(n);
+    for (int b = 0; b < n; ++b) {
+        const fr_body_pose &p = poses[b];
+        double t[3];
+        for (int i = 0; i < 3; ++i)
+            t[i] = p.c_world[i] -
+                   (p.R[3 * i] * p.c_ref[0] + p.R[3 * i + 1] * p.c_ref[1] + p.R[3 * i + 2] * p.c_ref[2]);
+        make_rigid_k(A, p.R, t, p.c_ref, cp, lat->c.gain, -1, ncol, &out[b]);
+        for (int i = 0; i < 3; ++i) out[b].c_world[i] = p.c_world[i];
+        for (int i = 0; i < 4; ++i)
+            out[b].e0[i] = A[i][0] * p.c_world[0] + A[i][1] * p.c_world[1] + A[i][2] * p.c_world[2];
+    }
+    return FR_OK;
+}
+
+int fr_body_pass(const fr_lattice *lat, const float *ref, int64_t m, const fr_body_pose *poses,
+                 int n_bodies, const int32_t *chunk_body, const int64_t *chunk_beg, int n_chunks,
+                 const int32_t *body_chunks, int mode, double c_prime, int flags,
+                 double *d_params, double *sums, float *wtn, double *scratch, void *stream) {
+    if (!lat || !lat->blurred || !ref || !poses || n_bodies < 1 || n_chunks < 1 || !chunk_body ||
+        !chunk_beg || !body_chunks || !sums || !scratch || !d_params) {
+        set_error("invalid articulated pass arguments");
+        return FR_EINVAL;
+    }
+    const bool pl = mode == FR_POINT_TO_PLANE;
+    const bool sig = pl ? lat->nv == 8 : lat->nv == 5;   // |y|^2 column splatted
+    if ((pl && (lat->nv < 7 || lat->nv > 8 || !wtn)) || (!pl && (lat->nv < 4 || lat->nv > 5))) {
+        set_error("lattice value columns (%d) do not match the residual mode", lat->nv);
+        return FR_EINVAL;
+    }
+    std::vector<RigidK> ks;
+    FR_TRY(body_params(lat, poses, n_bodies, c_prime, pl ? (sig ? 5 : 4) : -1, ks));
+    for (auto &k : ks) k.m2_col = sig ? 4 : -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    FR_CUDA(cudaMemcpyAsync(d_params, ks.data(), ks.size() * sizeof(RigidK), cudaMemcpyHostToDevice, s));
+    const RigidK *kd = reinterpret_cast<const RigidK *>(d_params);
+    const long long *cb = reinterpret_cast<const long long *>(chunk_beg);
+    const bool fast = (flags & FR_PASS_FAST) && lat->fslots && !sig;
+    const int na = (pl ? kP2PlBase : kP2PtBase) + (sig ? 2 : 0);
+    const SliceTable t = lat->table();
+    const SliceTableF tf = lat->table_f();
+#define FR_B(MODE, NV, SIG, FAST) \
+    k_body_pass<MODE, NV, SIG, FAST><<<n_chunks, kPassThreads, 0, s>>>(ref, m, kd, chunk_body, cb, t, tf, wtn, scratch)
+    if (!pl) {
+        if (sig) FR_B(0, 5, true, false);
+        else if (fast) FR_B(0, 4, false, true);
+        else FR_B(0, 4, false, false);
+    } else {
+        if (sig) FR_B(1, 8, true, false);
+        else if (fast) FR_B(1, 7, false, true);
+        else FR_B(1, 7, false, false);
+    }
+#undef FR_B
+    FR_CHECK_LAUNCH();
+    k_reduce_segments<<<n_bodies, 32 * na, 0, s>>>(scratch, body_chunks, na, sums);
+    FR_CHECK_LAUNCH();
+    // the host copy of the params must outlive the async copy
+    FR_CUDA(cudaStreamSynchronize(s));
+    return FR_OK;
+}
+
+int fr_body_objective(const float *ref, const float *wtn, int64_t m, const fr_body_pose *cand,
+                      int n_bodies, int ncand, const int32_t *chunk_body, const int64_t *chunk_beg,
+                      int n_chunks, double *d_params, double *out, double *scratch, void *stream) {
+    if (!ref || !wtn || !cand || ncand < 1 || ncand > kMaxCand || !out || !scratch || !d_params) {
+        set_error("invalid articulated objective arguments (1 <= k <= %d)", kMaxCand);
+        return FR_EINVAL;
+    }
+    std::vector<RigidK> ks((size_t)ncand * n_bodies);
+    memset(ks.data(), 0, ks.size() * sizeof(RigidK));
+    for (size_t i = 0; i < ks.size(); ++i) {
+        memcpy(ks[i].R, cand[i].R, sizeof(ks[i].R));
+        memcpy(ks[i].c_ref, cand[i].c_ref, sizeof(ks[i].c_ref));
+        memcpy(ks[i].c_world, cand[i].c_world, sizeof(ks[i].c_world));
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    FR_CUDA(cudaMemcpyAsync(d_params, ks.data(), ks.size() * sizeof(RigidK), cudaMemcpyHostToDevice, s));
+    k_body_objective<<<n_chunks, kPassThreads, 0, s>>>(
+        ref, wtn, m, reinterpret_cast<const RigidK *>(d_params), n_bodies, ncand, chunk_body,
+        reinterpret_cast<const long long *>(chunk_beg), scratch);
+    FR_CHECK_LAUNCH();
+    k_reduce_cols<<<1, 32 * kMaxCand, 0, s>>>(scratch, n_chunks, kMaxCand, out, nullptr);
+    FR_CHECK_LAUNCH();
+    FR_CUDA(cudaStreamSynchronize(s));
+    return FR_OK;
+}
+
+int fr_body_params_doubles(int n) { return (int)((n * sizeof(RigidK) + 7) / 8); }
 
 // ---- device-resident EM loop -----------------------------------------------
 
