@@ -28,7 +28,8 @@ EXPORTED = (
     "fr_rigid_objective", "fr_moments_epilogue", "fr_assemble_rigid",
     "fr_rigid_em_create", "fr_rigid_em_destroy", "fr_rigid_em_sums", "fr_rigid_em_pass",
     "fr_rigid_em_solve", "fr_rigid_em_enqueue", "fr_rigid_em_run", "fr_rigid_em_status",
-    "fr_rigid_em_result", "fr_sort_points_morton",
+    "fr_rigid_em_result", "fr_sort_points_morton", "fr_body_params_doubles", "fr_body_pass",
+    "fr_body_objective",
 )
 
 
@@ -85,6 +86,9 @@ _SIGS = {
     "fr_rigid_pass": ([_P, _P, _L, ctypes.POINTER(RigidPassParams), _P, _P, _P, _P], _I),
     "fr_rigid_objective": ([_P, _P, _L, _DP, _I, _DP, _DP, _P, _P, _P], _I),
     "fr_sort_points_morton": ([_P, _L, _I, _P, _P], _I),
+    "fr_body_params_doubles": ([_I], _I),
+    "fr_body_pass": ([_P, _P, _L, _P, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P, _P, _P], _I),
+    "fr_body_objective": ([_P, _P, _L, _P, _I, _I, _P, _P, _I, _P, _P, _P, _P], _I),
     "fr_rigid_em_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), ctypes.POINTER(_P)], _I),
     "fr_rigid_em_destroy": ([_P], _I),
     "fr_rigid_em_sums": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_I)], _I),

@@ -154,7 +154,8 @@ class RigidDevicePath:
     """HBM-resident state of one rigid registration: float32 SoA reference
     planes, the observation lattice, and the reduction buffers."""
 
-    def __init__(self, reference, observation, gmm, residual_mode: str, process_group=None):
+    def __init__(self, reference, observation, gmm, residual_mode: str, process_group=None,
+                 sort: bool = True):
         import torch
         self.dev = _lib.device()
         self.lib = _lib.load()
@@ -174,7 +175,7 @@ class RigidDevicePath:
         lo = self._allreduce(self.ref.amin(dim=1).double().cpu().numpy(), "min")
         hi = self._allreduce(self.ref.amax(dim=1).double().cpu().numpy(), "max")
         self.diameter = float(np.linalg.norm(hi - lo))
-        if SPATIAL_ORDER and self.M > 1:
+        if sort and SPATIAL_ORDER and self.M > 1:
             # Morton order of the model points: reduction sums are order-free up
             # to float64 round-off, and neighbouring threads share table lines
             _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self.ref), self.M, 3, None,

@@ -20,7 +20,7 @@ from ._rigid import RigidDevicePath, RigidMoments, unpack_upper6
 from .errors import DegenerateCorrespondenceError
 from .estep import GmmConfig, M0_FLOOR  # noqa: F401  (re-exported constants)
 from .geometry import PointCloud, RigidTransform, rotation_angle
-from .kinematics import RigidModel
+from .kinematics import ArticulatedTree, NodeGraph, RigidModel
 from .mstep import (RESIDUAL_MODES, MStepDiagnostics, MStepOptions, NormalEquations,
                     _accepts, gn_solve)
 
@@ -230,17 +230,26 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
     decisions on identical totals.  The returned result is the same on every
     rank."""
     config = config if config is not None else RegistrationConfig()
-    if not isinstance(initial_model, RigidModel):
-        raise TypeError(f"unsupported kinematic model {type(initial_model).__name__} "
-                        "(this build registers RigidModel)")
+    articulated = isinstance(initial_model, ArticulatedTree)
+    if isinstance(initial_model, NodeGraph):
+        from ._nodegraph import register_nodegraph
+        return register_nodegraph(reference, observation, initial_model, config, timing,
+                                  process_group)
+    if not (isinstance(initial_model, RigidModel) or articulated):
+        raise TypeError(f"unsupported kinematic model {type(initial_model).__name__}")
     if config.backend != "lattice" or config.gmm.mode != "position":
         raise ValueError("the device EM path runs the lattice backend with position "
                          "correspondences")
-    factory = _path_factory if _path_factory is not None else RigidDevicePath
-    path = factory(reference, observation, config.gmm, config.residual_mode, process_group)
-    if (_path_factory is None and config.residual_mode == "point_to_point"
-            and not config.gmm.update_sigma and not config.record_states):
-        return _register_device_loop(path, initial_model, config, timing)
+    if articulated:
+        from ._articulated import ArticulatedDevicePath, articulated_m_step
+        path = ArticulatedDevicePath(reference, observation, config.gmm, config.residual_mode,
+                                     initial_model, process_group)
+    else:
+        factory = _path_factory if _path_factory is not None else RigidDevicePath
+        path = factory(reference, observation, config.gmm, config.residual_mode, process_group)
+        if (_path_factory is None and config.residual_mode == "point_to_point"
+                and not config.gmm.update_sigma and not config.record_states):
+            return _register_device_loop(path, initial_model, config, timing)
     model = initial_model
     diameter = path.diameter
     sigma_current = path.sigma
@@ -250,8 +259,12 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
     for _ in range(config.max_em_iters):
         result.iterations += 1
         tick = time.perf_counter()
-        R, t = model.pose.rotation, model.pose.translation
-        sums = path.run_pass(R, t)
+        if articulated:
+            body_sums = path.run_body_pass(model)
+            sums = body_sums.sum(axis=0)          # mass and sigma sums are totals
+        else:
+            R, t = model.pose.rotation, model.pose.translation
+            sums = path.run_pass(R, t)
         if timing is not None:
             timing["e_step_s"] = timing.get("e_step_s", 0.0) + time.perf_counter() - tick
         mass = float(sums[0])
@@ -273,7 +286,10 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
             result.sigmas.append(sigma_new)
         s2 = (1.0 / np.asarray(sigma_current, dtype=float)) ** 2
         tick = time.perf_counter()
-        candidate, mdiag = _rigid_m_step(path, sums, R, t, s2, config.mstep)
+        if articulated:
+            candidate, mdiag = articulated_m_step(path, body_sums, model, s2, config.mstep)
+        else:
+            candidate, mdiag = _rigid_m_step(path, sums, R, t, s2, config.mstep)
         if timing is not None:
             timing["m_step_s"] = timing.get("m_step_s", 0.0) + time.perf_counter() - tick
         norm = update_magnitude(model, candidate, diameter)
