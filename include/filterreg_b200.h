@@ -210,6 +210,33 @@ int fr_body_objective(const float *d_ref, const float *d_wtn, int64_t m,
                       const int32_t *d_chunk_body, const int64_t *d_chunk_beg, int n_chunks,
                       double *d_params, double *d_out, double *d_scratch, void *stream);
 
+/* ---- node graphs (mstep.py:232-314, kinematics.py:254-346, geometry.py:342-368)
+ * d_sidx / d_swt: m x K skinning (int32 node index, -1 padding / float64
+ * weight); d_node_dq: n_nodes x 8 dual quaternions [real | dual].
+ * fr_graph_pass: DQB forward map, slice + moments (respec = 0) or the stored
+ * spec (respec = 1), per-point E^T E / E^T r into d_ete (m x 28), and
+ * d_sums = [data objective, inlier mass, sigma numerator, sigma mass].
+ * fr_graph_blocks: node diagonal blocks (n_nodes x 27: upper-21 H | g) and
+ * co-skinned pair blocks (n_pairs x 21, symmetric) from the (point, slot)
+ * lists d_dptr/d_dent (code p*K+slot, grouped by node) and d_pptr/d_pent
+ * (pairs of int32: point, slot_a | slot_c << 8), in list order.
+ * fr_graph_objective: data objectives of k <= 16 candidate node states
+ * (d_cand_dq: k x n_nodes x 8) under the stored spec; d_out 16 doubles.
+ * d_flag is set when a blend degenerates (DegenerateBlendError). */
+int fr_graph_pass(const fr_lattice *lat, const float *d_ref, int64_t m, const int32_t *d_sidx,
+                  const double *d_swt, int K, const double *d_node_dq, int mode,
+                  const double *sigma_inv, double c_prime, int respec, double *d_rec,
+                  double *d_ete, double *d_sums, double *d_scratch, int32_t *d_flag,
+                  void *stream);
+int fr_graph_blocks(const double *d_ete, const double *d_swt, int K, const int32_t *d_dptr,
+                    const int32_t *d_dent, int n_nodes, const int32_t *d_pptr,
+                    const int32_t *d_pent, int n_pairs, double *d_diag, double *d_off,
+                    void *stream);
+int fr_graph_objective(const float *d_ref, int64_t m, const int32_t *d_sidx,
+                       const double *d_swt, int K, const double *d_cand_dq, int n_nodes, int k,
+                       const double *d_rec, int mode, const double *sigma_inv, double *d_out,
+                       double *d_scratch, int32_t *d_flag, void *stream);
+
 /* ---- device-resident rigid EM loop (pipeline.py:141-181, point_to_point) --
  * The whole EM iteration stays on the GPU: fused pass, fixed-order reduction,
  * and a one-thread float64 solver kernel that assembles the normal equations

@@ -1,0 +1,296 @@
+"""Node-graph (deformable) FilterReg EM on the GPU (mstep.py:232-345,
+kinematics.py:254-346).
+
+Per EM iteration: `fr_graph_pass` (DQB forward map + slice + moments + each
+point's E^T E / E^T r) and `fr_graph_blocks` (block-sparse normal equations,
+one warp per node / co-skinned node pair over precomputed (point, slot) lists,
+fixed order).  The as-rigid-as-possible regulariser touches only node states
+(~10^3 edges) and is added on the host exactly as the reference forms it; the
+block-sparse system is factorised with the reference's damping / SuperLU rule
+(mstep.py:317-369).  Halving candidates are scored by `fr_graph_objective`
+under the stored residual spec.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _lib
+from ._rigid import RigidDevicePath, unpack_upper6
+from .errors import DegenerateBlendError, DegenerateCorrespondenceError
+from .geometry import point_twist_jacobian
+
+
+def _sym6_from21(v21):
+    return unpack_upper6(v21)
+
+
+class NodeGraphDevicePath(RigidDevicePath):
+    """Model planes in input order + skinning + gather lists + lattice."""
+
+    def __init__(self, reference, observation, gmm, residual_mode, graph, process_group=None):
+        import torch
+        super().__init__(reference, observation, gmm, residual_mode, process_group, sort=False)
+        sk = graph.skinning
+        if len(sk.indices) != self.M:
+            raise ValueError("skinning does not match the reference cloud")
+        K = sk.indices.shape[1]
+        self.K = K
+        self.n = graph.n_nodes
+        idx = np.asarray(sk.indices, dtype=np.int64)
+        wts = np.where(idx >= 0, np.asarray(sk.weights, dtype=float), 0.0)
+        live = (idx >= 0) & (wts > 0)
+        dev = self.dev
+        self.sidx = torch.from_numpy(idx.astype(np.int32)).to(dev)
+        self.swt = torch.from_numpy(np.ascontiguousarray(wts)).to(dev)
+        # node lists: (point, slot) codes grouped by node, point order inside
+        p_i, s_i = np.nonzero(live)
+        node = idx[p_i, s_i]
+        order = np.lexsort((p_i, node))
+        dcount = np.bincount(node, minlength=self.n)
+        self.dptr = torch.from_numpy(np.concatenate([[0], np.cumsum(dcount)]).astype(np.int32)).to(dev)
+        self.dent = torch.from_numpy((p_i * K + s_i)[order].astype(np.int32)).to(dev)
+        # co-skinned pairs (a < c slots, both live): canonical (lo, hi) order
+        pts, sa, sc, lo, hi = [], [], [], [], []
+        for a in range(K):
+            for c in range(a + 1, K):
+                m = live[:, a] & live[:, c]
+                pp = np.flatnonzero(m)
+                ia, ic = idx[pp, a], idx[pp, c]
+                pts.append(pp)
+                sa.append(np.full(len(pp), a))
+                sc.append(np.full(len(pp), c))
+                lo.append(np.minimum(ia, ic))
+                hi.append(np.maximum(ia, ic))
+        pts, sa, sc = map(np.concatenate, (pts, sa, sc))
+        codes = np.concatenate(lo) * self.n + np.concatenate(hi)
+        ucodes = np.unique(codes)
+        if self.group is not None:
+            import torch.distributed as dist
+            allc = [None] * dist.get_world_size(self.group)
+            dist.all_gather_object(allc, ucodes, group=self.group)
+            ucodes = np.unique(np.concatenate(allc))
+        self.pair_lo, self.pair_hi = ucodes // self.n, ucodes % self.n
+        pid = np.searchsorted(ucodes, codes)
+        order = np.lexsort((pts, pid))
+        pcount = np.bincount(pid, minlength=len(ucodes))
+        self.n_pairs = len(ucodes)
+        self.pptr = torch.from_numpy(np.concatenate([[0], np.cumsum(pcount)]).astype(np.int32)).to(dev)
+        pent = np.stack([pts[order], sa[order] | (sc[order] << 8)], axis=1).astype(np.int32)
+        self.pent = torch.from_numpy(np.ascontiguousarray(pent)).to(dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.rec = torch.empty((7, self.M), **f64)
+        self.ete = torch.empty((self.M, 28), **f64)
+        self.diag = torch.zeros((self.n, 27), **f64)
+        self.off = torch.zeros((max(self.n_pairs, 1), 21), **f64)
+        self.gsums = torch.empty(16, **f64)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.cand_dq = torch.empty((16, self.n, 8), **f64)
+
+    def _sinv(self, s2):
+        return np.sqrt(np.asarray(s2, dtype=float))
+
+    def run(self, graph, s2, respec=False):
+        """E step (or re-assembly under the stored spec) at `graph`'s nodes:
+        returns (data objective, mass, sigma num, sigma mass), diag, off."""
+        import torch
+        dq = torch.from_numpy(np.ascontiguousarray(graph.dual_quaternions)).to(self.dev)
+        si, _keep = _lib.dptr(self._sinv(s2))
+        self.flag.zero_()
+        _lib.check(self.lib.fr_graph_pass(
+            self.lattice.handle, _lib.ptr(self.ref), self.M, _lib.ptr(self.sidx),
+            _lib.ptr(self.swt), self.K, _lib.ptr(dq), self.mode, si, self.c_prime, int(respec),
+            _lib.ptr(self.rec), _lib.ptr(self.ete), _lib.ptr(self.gsums), _lib.ptr(self.scratch),
+            _lib.ptr(self.flag), _lib.stream_handle()))
+        _lib.check(self.lib.fr_graph_blocks(
+            _lib.ptr(self.ete), _lib.ptr(self.swt), self.K, _lib.ptr(self.dptr),
+            _lib.ptr(self.dent), self.n, _lib.ptr(self.pptr), _lib.ptr(self.pent), self.n_pairs,
+            _lib.ptr(self.diag), _lib.ptr(self.off), _lib.stream_handle()))
+        self.reduce_device(self.gsums[:4])
+        self.reduce_device(self.diag)
+        if self.n_pairs:
+            self.reduce_device(self.off)
+        if int(self.flag.item()):
+            raise DegenerateBlendError("blended real part vanished for some points")
+        return (self.gsums[:4].cpu().numpy().copy(), self.diag.cpu().numpy().copy(),
+                self.off[:self.n_pairs].cpu().numpy().copy())
+
+    def candidate_objectives(self, graphs, s2):
+        import torch
+        out = []
+        si, _keep = _lib.dptr(self._sinv(s2))
+        for a in range(0, len(graphs), 16):
+            chunk = graphs[a:a + 16]
+            self.cand_dq[:len(chunk)].copy_(torch.from_numpy(
+                np.stack([g.dual_quaternions for g in chunk])))
+            self.flag.zero_()
+            _lib.check(self.lib.fr_graph_objective(
+                _lib.ptr(self.ref), self.M, _lib.ptr(self.sidx), _lib.ptr(self.swt), self.K,
+                _lib.ptr(self.cand_dq), self.n, len(chunk), _lib.ptr(self.rec), self.mode, si,
+                _lib.ptr(self.gsums), _lib.ptr(self.scratch), _lib.ptr(self.flag),
+                _lib.stream_handle()))
+            self.reduce_device(self.gsums)
+            if int(self.flag.item()):
+                raise DegenerateBlendError("blended real part vanished for some points")
+            out += list(self.gsums[:len(chunk)].cpu().numpy())
+        return np.asarray(out)
+
+
+def regularizer_objective(graph, lambda_reg: float) -> float:
+    """0.5 lambda sum ||T_k p - T_l p||^2 over edges, both endpoints
+    (mstep.py:390-401)."""
+    if lambda_reg <= 0 or not len(graph.edges):
+        return 0.0
+    R = np.stack([T.rotation for T in graph.node_transforms])
+    t = np.stack([T.translation for T in graph.node_transforms])
+    k_ids, l_ids = graph.edges[:, 0], graph.edges[:, 1]
+    total = 0.0
+    for p in (graph.node_positions[l_ids], graph.node_positions[k_ids]):
+        xk = np.einsum("eij,ej->ei", R[k_ids], p) + t[k_ids]
+        xl = np.einsum("eij,ej->ei", R[l_ids], p) + t[l_ids]
+        total += 0.5 * lambda_reg * float(np.sum((xk - xl) ** 2))
+    return total
+
+
+def _grouped(values, ids, n):
+    out = np.zeros((n,) + values.shape[1:])
+    np.add.at(out, ids, values)
+    return out
+
+
+def normal_equations(graph, diag, off, path, lambda_reg):
+    """Block-sparse system: device data term + host ARAP term (mstep.py:290-314)."""
+    from .mstep import NormalEquations
+    n = graph.n_nodes
+    D = np.stack([_sym6_from21(diag[k, :21]) for k in range(n)])
+    b = diag[:, 21:27].copy()
+    blocks = {}
+    for i in range(path.n_pairs):
+        blocks[(int(path.pair_lo[i]), int(path.pair_hi[i]))] = _sym6_from21(off[i])
+    if lambda_reg > 0 and len(graph.edges):
+        R = np.stack([T.rotation for T in graph.node_transforms])
+        t = np.stack([T.translation for T in graph.node_transforms])
+        root = np.sqrt(lambda_reg)
+        k_ids, l_ids = graph.edges[:, 0], graph.edges[:, 1]
+        for p in (graph.node_positions[l_ids], graph.node_positions[k_ids]):
+            xk = np.einsum("eij,ej->ei", R[k_ids], p) + t[k_ids]
+            xl = np.einsum("eij,ej->ei", R[l_ids], p) + t[l_ids]
+            r = root * (xk - xl)
+            Jk = root * point_twist_jacobian(xk)
+            Jl = -root * point_twist_jacobian(xl)
+            D += _grouped(np.einsum("eri,erj->eij", Jk, Jk), k_ids, n)
+            D += _grouped(np.einsum("eri,erj->eij", Jl, Jl), l_ids, n)
+            b += _grouped(np.einsum("eri,er->ei", Jk, r), k_ids, n)
+            b += _grouped(np.einsum("eri,er->ei", Jl, r), l_ids, n)
+            cross = np.einsum("eri,erj->eij", Jk, Jl)
+            swap = k_ids > l_ids
+            cross[swap] = np.transpose(cross[swap], (0, 2, 1))
+            for e in range(len(k_ids)):
+                key = (int(min(k_ids[e], l_ids[e])), int(max(k_ids[e], l_ids[e])))
+                blocks[key] = blocks[key] + cross[e] if key in blocks else cross[e].copy()
+    for k in range(n):
+        blocks[(k, k)] = D[k]
+    return NormalEquations(6 * n, b=b.reshape(-1), blocks=blocks)
+
+
+def nodegraph_m_step(path, g4, diag, off, graph, s2, opts):
+    """mstep.py:421-459 for a NodeGraph."""
+    from .mstep import MStepDiagnostics, _accepts, gn_solve
+    current = graph
+    value = float(g4[0]) + regularizer_objective(current, opts.lambda_reg)
+    diagn = MStepDiagnostics(objectives=[value])
+    for it in range(opts.max_gn_iters):
+        if it > 0:
+            g4, diag, off = path.run(current, s2, respec=True)
+        eq = normal_equations(current, diag, off, path, opts.lambda_reg)
+        if not np.any(eq.b):
+            break
+        stats: dict = {}
+        step = gn_solve(eq, opts.damping, opts.solve_method, _stats=stats)
+        diagn.dampings.append(stats.get("damping", 0.0))
+        cands, scale = [], 1.0
+        for _h in range(opts.max_halvings + 1):
+            cands.append((current.updated(scale * step), scale))
+            scale *= 0.5
+        vals = list(path.candidate_objectives([cands[0][0]], s2))
+        if not _accepts(vals[0] + regularizer_objective(cands[0][0], opts.lambda_reg), value) \
+                and len(cands) > 1:
+            vals += list(path.candidate_objectives([c for c, _ in cands[1:]], s2))
+        accepted = None
+        for h, dv in enumerate(vals):
+            cv = dv + regularizer_objective(cands[h][0], opts.lambda_reg)
+            if _accepts(cv, value):
+                accepted = (cands[h][0], cv, h, cands[h][1])
+                break
+        if accepted is None:
+            break
+        current, value, h, sc = accepted
+        diagn.objectives.append(value)
+        diagn.halvings.append(h)
+        sn = float(np.linalg.norm(sc * step))
+        diagn.step_norms.append(sn)
+        if sn <= opts.step_tolerance:
+            break
+    return current, diagn
+
+
+def register_nodegraph(reference, observation, graph, config, timing=None, process_group=None):
+    """pipeline.py:125-181 for a NodeGraph model."""
+    from .pipeline import DEGENERATE_MASS_FRACTION, RegistrationResult, update_magnitude
+    if config.backend != "lattice" or config.gmm.mode != "position":
+        raise ValueError("the device EM path runs the lattice backend with position "
+                         "correspondences")
+    path = NodeGraphDevicePath(reference, observation, config.gmm, config.residual_mode, graph,
+                               process_group)
+    model = graph
+    sigma_current = path.sigma
+    result = RegistrationResult(kinematics=model, iterations=0,
+                                states=[] if config.record_states else None)
+    for _ in range(config.max_em_iters):
+        result.iterations += 1
+        tick = time.perf_counter()
+        s2 = (1.0 / np.asarray(sigma_current, dtype=float)) ** 2
+        g4, diag, off = path.run(model, s2)
+        if timing is not None:
+            timing["e_step_s"] = timing.get("e_step_s", 0.0) + time.perf_counter() - tick
+        mass = float(g4[1])
+        result.inlier_masses.append(mass)
+        if mass < DEGENERATE_MASS_FRACTION * path.M_total:
+            result.objectives.append(float("nan"))
+            result.twist_norms.append(float("nan"))
+            result.termination = "degenerate"
+            break
+        if config.gmm.update_sigma:
+            num, den = float(g4[2]), float(g4[3])
+            if den <= 0.0:
+                raise DegenerateCorrespondenceError("no correspondence mass left")
+            sigma_new = max(float(np.sqrt(max(num / (3.0 * den), 0.0))), config.gmm.sigma_floor)
+            if sigma_new != sigma_current[0]:
+                path.build(sigma_new)
+                sigma_current = path.sigma
+                s_new = (1.0 / np.asarray(sigma_current, dtype=float)) ** 2
+                if config.residual_mode == "point_to_point":
+                    # residual scaling follows the new width (pipeline.py:155-162)
+                    g4, diag, off = path.run(model, s_new, respec=True)
+                s2 = s_new
+            result.sigmas.append(sigma_new)
+        tick = time.perf_counter()
+        candidate, mdiag = nodegraph_m_step(path, g4, diag, off, model, s2, config.mstep)
+        if timing is not None:
+            timing["m_step_s"] = timing.get("m_step_s", 0.0) + time.perf_counter() - tick
+        norm = update_magnitude(model, candidate, path.diameter)
+        result.twist_norms.append(norm)
+        if norm < config.twist_tolerance:
+            result.objectives.append(mdiag.objectives[0])
+            result.termination = "converged"
+            break
+        model = candidate
+        result.objectives.append(mdiag.objectives[-1])
+        if result.states is not None:
+            result.states.append(model)
+    result.kinematics = model
+    if timing is not None:
+        timing["iterations"] = result.iterations
+    return result
