@@ -232,6 +232,12 @@ int fr_graph_blocks(const double *d_ete, const double *d_swt, int K, const int32
                     const int32_t *d_dent, int n_nodes, const int32_t *d_pptr,
                     const int32_t *d_pent, int n_pairs, double *d_diag, double *d_off,
                     void *stream);
+/* per-point [E^T E upper 21 | E^T r 6 | 0] (m x 28) of an explicit ResidualSpec
+ * at explicit positions (d_x, d_target, d_normal m x 3, d_weight m, d_valid m;
+ * the assemble_* API of mstep.py:179-314); feed fr_graph_blocks. */
+int fr_point_rows(const double *d_x, const double *d_weight, const double *d_target,
+                  const double *d_normal, const uint8_t *d_valid, int64_t m, int mode,
+                  const double *sigma_inv, double *d_ete, void *stream);
 int fr_graph_objective(const float *d_ref, int64_t m, const int32_t *d_sidx,
                        const double *d_swt, int K, const double *d_cand_dq, int n_nodes, int k,
                        const double *d_rec, int mode, const double *sigma_inv, double *d_out,

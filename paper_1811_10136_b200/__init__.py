@@ -19,8 +19,12 @@ from .errors import (BindingError, DegenerateBlendError, DegenerateCorrespondenc
 from .estep import GmmConfig, MomentEngine, MomentField, compute_moments, outlier_constant, \
     update_sigma
 from .geometry import PointCloud, RigidTransform, apply_twist, rotation_about_axis, twist_exp
-from .kinematics import RigidModel, forward_points
-from .mstep import MStepOptions, ResidualSpec, assemble_rigid, gn_solve, m_step, objective
+from .kinematics import (ArticulatedTree, Body, Joint, NodeGraph, RigidModel, Skinning,
+                         articulated_from_dict, bind_points_to_nodes, build_node_graph,
+                         forward_points, load_articulated_model)
+from .mstep import (MStepOptions, NormalEquations, ResidualSpec, assemble_articulated,
+                    assemble_nodegraph, assemble_rigid, gn_solve, m_step, objective,
+                    residuals_from_moments)
 from .permutohedral import (PermutohedralLattice, build_lattice, filter_augmented,
                             gaussian_transform_bruteforce, valid_lattice_key)
 from .pipeline import (RegistrationConfig, RegistrationResult, alignment_error, default_sigma,
@@ -29,12 +33,15 @@ from .pipeline import (RegistrationConfig, RegistrationResult, alignment_error, 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BindingError", "DegenerateBlendError", "DegenerateCorrespondenceError", "GmmConfig",
-    "MStepOptions", "MomentEngine", "MomentField", "ParseError", "PermutohedralLattice",
+    "ArticulatedTree", "BindingError", "Body", "DegenerateBlendError",
+    "DegenerateCorrespondenceError", "GmmConfig", "Joint", "MStepOptions", "MomentEngine",
+    "MomentField", "NodeGraph", "NormalEquations", "ParseError", "PermutohedralLattice",
     "PointCloud", "RegistrationConfig", "RegistrationResult", "ResidualSpec", "RigidModel",
-    "RigidTransform", "SolverError", "alignment_error", "apply_twist", "assemble_rigid",
-    "build_lattice", "compute_moments", "default_sigma", "filter_augmented", "forward_points",
-    "gaussian_transform_bruteforce", "gn_solve", "log_likelihood", "m_step", "objective",
-    "outlier_constant", "register", "rotation_about_axis", "twist_exp", "update_magnitude",
-    "update_sigma", "valid_lattice_key",
+    "RigidTransform", "Skinning", "SolverError", "alignment_error", "apply_twist",
+    "articulated_from_dict", "assemble_articulated", "assemble_nodegraph", "assemble_rigid",
+    "bind_points_to_nodes", "build_lattice", "build_node_graph", "compute_moments",
+    "default_sigma", "filter_augmented", "forward_points", "gaussian_transform_bruteforce",
+    "gn_solve", "load_articulated_model", "log_likelihood", "m_step", "objective",
+    "outlier_constant", "register", "residuals_from_moments", "rotation_about_axis",
+    "twist_exp", "update_magnitude", "update_sigma", "valid_lattice_key",
 ]

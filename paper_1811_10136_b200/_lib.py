@@ -30,6 +30,7 @@ EXPORTED = (
     "fr_rigid_em_solve", "fr_rigid_em_enqueue", "fr_rigid_em_run", "fr_rigid_em_status",
     "fr_rigid_em_result", "fr_sort_points_morton", "fr_body_params_doubles", "fr_body_pass",
     "fr_body_objective", "fr_graph_pass", "fr_graph_blocks", "fr_graph_objective",
+    "fr_point_rows",
 )
 
 
@@ -91,6 +92,7 @@ _SIGS = {
     "fr_body_objective": ([_P, _P, _L, _P, _I, _I, _P, _P, _I, _P, _P, _P, _P], _I),
     "fr_graph_pass": ([_P, _P, _L, _P, _P, _I, _P, _I, _DP, _D, _I, _P, _P, _P, _P, _P, _P], _I),
     "fr_graph_blocks": ([_P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P], _I),
+    "fr_point_rows": ([_P, _P, _P, _P, _P, _L, _I, _DP, _P, _P], _I),
     "fr_graph_objective": ([_P, _L, _P, _P, _I, _P, _I, _I, _P, _I, _DP, _P, _P, _P, _P], _I),
     "fr_rigid_em_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), ctypes.POINTER(_P)], _I),
     "fr_rigid_em_destroy": ([_P], _I),

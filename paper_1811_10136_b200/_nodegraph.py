@@ -27,6 +27,41 @@ def _sym6_from21(v21):
     return unpack_upper6(v21)
 
 
+def gather_lists(indices, weights, n_nodes, extra_codes=None):
+    """(point, slot) lists for fr_graph_blocks: node lists (code p*K + slot,
+    grouped by node, point order) and co-skinned pair lists (point, slot_a |
+    slot_c << 8) grouped by the canonical (lo, hi) pair, point order."""
+    idx = np.asarray(indices, dtype=np.int64)
+    K = idx.shape[1]
+    wts = np.where(idx >= 0, np.asarray(weights, dtype=float), 0.0)
+    live = (idx >= 0) & (wts > 0)
+    p_i, s_i = np.nonzero(live)
+    node = idx[p_i, s_i]
+    order = np.lexsort((p_i, node))
+    dcount = np.bincount(node, minlength=n_nodes)
+    pts, sa, sc, codes = [np.zeros(0, dtype=np.int64)], [np.zeros(0, dtype=np.int64)], \
+        [np.zeros(0, dtype=np.int64)], [np.zeros(0, dtype=np.int64)]
+    for a in range(K):
+        for c in range(a + 1, K):
+            pp = np.flatnonzero(live[:, a] & live[:, c])
+            ia, ic = idx[pp, a], idx[pp, c]
+            pts.append(pp)
+            sa.append(np.full(len(pp), a))
+            sc.append(np.full(len(pp), c))
+            codes.append(np.minimum(ia, ic) * n_nodes + np.maximum(ia, ic))
+    pts, sa, sc, codes = map(np.concatenate, (pts, sa, sc, codes))
+    ucodes = np.unique(codes) if extra_codes is None else np.asarray(extra_codes)
+    pid = np.searchsorted(ucodes, codes)
+    porder = np.lexsort((pts, pid))
+    pcount = np.bincount(pid, minlength=len(ucodes))
+    pent = np.stack([pts[porder], sa[porder] | (sc[porder] << 8)], axis=1).astype(np.int32)
+    return {"dptr": np.concatenate([[0], np.cumsum(dcount)]).astype(np.int32),
+            "dent": np.ascontiguousarray((p_i * K + s_i)[order].astype(np.int32)),
+            "pptr": np.concatenate([[0], np.cumsum(pcount)]).astype(np.int32),
+            "pent": np.ascontiguousarray(pent), "n_pairs": len(ucodes),
+            "pair_lo": ucodes // n_nodes, "pair_hi": ucodes % n_nodes, "codes": ucodes}
+
+
 class NodeGraphDevicePath(RigidDevicePath):
     """Model planes in input order + skinning + gather lists + lattice."""
 
@@ -41,45 +76,19 @@ class NodeGraphDevicePath(RigidDevicePath):
         self.n = graph.n_nodes
         idx = np.asarray(sk.indices, dtype=np.int64)
         wts = np.where(idx >= 0, np.asarray(sk.weights, dtype=float), 0.0)
-        live = (idx >= 0) & (wts > 0)
         dev = self.dev
         self.sidx = torch.from_numpy(idx.astype(np.int32)).to(dev)
         self.swt = torch.from_numpy(np.ascontiguousarray(wts)).to(dev)
-        # node lists: (point, slot) codes grouped by node, point order inside
-        p_i, s_i = np.nonzero(live)
-        node = idx[p_i, s_i]
-        order = np.lexsort((p_i, node))
-        dcount = np.bincount(node, minlength=self.n)
-        self.dptr = torch.from_numpy(np.concatenate([[0], np.cumsum(dcount)]).astype(np.int32)).to(dev)
-        self.dent = torch.from_numpy((p_i * K + s_i)[order].astype(np.int32)).to(dev)
-        # co-skinned pairs (a < c slots, both live): canonical (lo, hi) order
-        pts, sa, sc, lo, hi = [], [], [], [], []
-        for a in range(K):
-            for c in range(a + 1, K):
-                m = live[:, a] & live[:, c]
-                pp = np.flatnonzero(m)
-                ia, ic = idx[pp, a], idx[pp, c]
-                pts.append(pp)
-                sa.append(np.full(len(pp), a))
-                sc.append(np.full(len(pp), c))
-                lo.append(np.minimum(ia, ic))
-                hi.append(np.maximum(ia, ic))
-        pts, sa, sc = map(np.concatenate, (pts, sa, sc))
-        codes = np.concatenate(lo) * self.n + np.concatenate(hi)
-        ucodes = np.unique(codes)
+        L = gather_lists(idx, wts, self.n)
         if self.group is not None:
+            # the pair set (and its order) must be the union over all shards
             import torch.distributed as dist
             allc = [None] * dist.get_world_size(self.group)
-            dist.all_gather_object(allc, ucodes, group=self.group)
-            ucodes = np.unique(np.concatenate(allc))
-        self.pair_lo, self.pair_hi = ucodes // self.n, ucodes % self.n
-        pid = np.searchsorted(ucodes, codes)
-        order = np.lexsort((pts, pid))
-        pcount = np.bincount(pid, minlength=len(ucodes))
-        self.n_pairs = len(ucodes)
-        self.pptr = torch.from_numpy(np.concatenate([[0], np.cumsum(pcount)]).astype(np.int32)).to(dev)
-        pent = np.stack([pts[order], sa[order] | (sc[order] << 8)], axis=1).astype(np.int32)
-        self.pent = torch.from_numpy(np.ascontiguousarray(pent)).to(dev)
+            dist.all_gather_object(allc, L["codes"], group=self.group)
+            L = gather_lists(idx, wts, self.n, extra_codes=np.unique(np.concatenate(allc)))
+        self.pair_lo, self.pair_hi, self.n_pairs = L["pair_lo"], L["pair_hi"], L["n_pairs"]
+        self.dptr, self.dent, self.pptr, self.pent = (
+            torch.from_numpy(L[k]).to(dev) for k in ("dptr", "dent", "pptr", "pent"))
         f64 = dict(dtype=torch.float64, device=dev)
         self.rec = torch.empty((7, self.M), **f64)
         self.ete = torch.empty((self.M, 28), **f64)
@@ -162,13 +171,17 @@ def _grouped(values, ids, n):
 
 def normal_equations(graph, diag, off, path, lambda_reg):
     """Block-sparse system: device data term + host ARAP term (mstep.py:290-314)."""
+    return normal_equations_from(graph, diag, off, path.pair_lo, path.pair_hi, lambda_reg)
+
+
+def normal_equations_from(graph, diag, off, pair_lo, pair_hi, lambda_reg):
     from .mstep import NormalEquations
     n = graph.n_nodes
     D = np.stack([_sym6_from21(diag[k, :21]) for k in range(n)])
     b = diag[:, 21:27].copy()
     blocks = {}
-    for i in range(path.n_pairs):
-        blocks[(int(path.pair_lo[i]), int(path.pair_hi[i]))] = _sym6_from21(off[i])
+    for i in range(len(pair_lo)):
+        blocks[(int(pair_lo[i]), int(pair_hi[i]))] = _sym6_from21(off[i])
     if lambda_reg > 0 and len(graph.edges):
         R = np.stack([T.rotation for T in graph.node_transforms])
         t = np.stack([T.translation for T in graph.node_transforms])

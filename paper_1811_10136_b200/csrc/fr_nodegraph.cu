@@ -324,11 +324,46 @@ k_graph_objective(const float *__restrict__ ref, long long m, const int *__restr
     block_reduce_store<kGraphMaxCand>(acc, partials + (long long)blockIdx.x * kGraphMaxCand);
 }
 
+// per-point E^T E / E^T r of an explicit ResidualSpec at explicit positions
+// (assemble_articulated / assemble_nodegraph API, mstep.py:213-314)
+__global__ void k_point_rows(const double *__restrict__ X, const double *__restrict__ W,
+                             const double *__restrict__ T, const double *__restrict__ N,
+                             const unsigned char *__restrict__ valid, long long m, int mode,
+                             double s0, double s1, double s2, double *__restrict__ ete) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    const double sinv[3] = {s0, s1, s2};
+    const double x[3] = {X[3 * p], X[3 * p + 1], X[3 * p + 2]};
+    const double t[3] = {T[3 * p], T[3 * p + 1], T[3 * p + 2]};
+    double n[3] = {0.0, 0.0, 0.0};
+    if (mode == FR_POINT_TO_PLANE && valid[p])
+        for (int j = 0; j < 3; ++j) n[j] = N[3 * p + j];
+    double e[kGraphEte];
+    point_rows(mode, sinv, W[p], x, t, n, e);
+    for (int q = 0; q < kGraphEte; ++q) ete[p * kGraphEte + q] = e[q];
+}
+
 }  // namespace fr
 
 using namespace fr;
 
 extern "C" {
+
+int fr_point_rows(const double *X, const double *W, const double *T, const double *N,
+                  const uint8_t *valid, int64_t m, int mode, const double *sigma_inv,
+                  double *ete, void *stream) {
+    if (!X || !W || !T || !ete || !sigma_inv || (mode == FR_POINT_TO_PLANE && (!N || !valid))) {
+        set_error("invalid point-rows arguments");
+        return FR_EINVAL;
+    }
+    if (m == 0) return FR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    k_point_rows<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(X, W, T, N, valid, m, mode,
+                                                            sigma_inv[0], sigma_inv[1],
+                                                            sigma_inv[2], ete);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
 
 int fr_graph_pass(const fr_lattice *lat, const float *ref, int64_t m, const int32_t *sidx,
                   const double *swt, int K, const double *node_dq, int mode,

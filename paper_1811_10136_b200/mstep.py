@@ -274,6 +274,144 @@ def m_step(spec: ResidualSpec, reference: PointCloud, model, options: MStepOptio
     return current, diag
 
 
-__all__ = ["RESIDUAL_MODES", "ResidualSpec", "residuals_from_moments", "NormalEquations",
+def _device_point_rows(spec: ResidualSpec, x):
+    """fr_point_rows: per-point [E^T E | E^T r] (m x 28) on the device."""
+    import torch
+    from .permutohedral import _to_device
+    lib = _lib.load()
+    m = len(spec)
+    dev = _lib.device()
+    ete = torch.empty((m, 28), dtype=torch.float64, device=dev)
+    pl = spec.mode == "point_to_plane"
+    dX, dW, dT = _to_device(np.asarray(x, dtype=float)), _to_device(spec.weights), \
+        _to_device(spec.targets)
+    dN = _to_device(spec.normals) if pl else None
+    dV = _to_device(spec.normal_valid, np.uint8) if pl else None
+    si, _keep = _lib.dptr(spec.sigma_inv)
+    _lib.check(lib.fr_point_rows(_lib.ptr(dX), _lib.ptr(dW), _lib.ptr(dT), _lib.ptr(dN),
+                                 _lib.ptr(dV), m, int(pl), si, _lib.ptr(ete),
+                                 _lib.stream_handle()))
+    return ete
+
+
+def _device_blocks(ete, weights, indices, n_nodes, pair_codes=None):
+    """fr_graph_blocks over (point, slot) lists built from a skinning-like
+    (indices, weights) table: diag (n x 27) and pair blocks (p x 21)."""
+    import torch
+    from ._nodegraph import gather_lists
+    lib = _lib.load()
+    dev = ete.device
+    K = indices.shape[1]
+    L = gather_lists(indices, weights, n_nodes)
+    t = {k: torch.from_numpy(v).to(dev) for k, v in L.items() if isinstance(v, np.ndarray)}
+    swt = torch.from_numpy(np.ascontiguousarray(np.where(indices >= 0, weights, 0.0))).to(dev)
+    diag = torch.zeros((n_nodes, 27), dtype=torch.float64, device=dev)
+    off = torch.zeros((max(L["n_pairs"], 1), 21), dtype=torch.float64, device=dev)
+    _lib.check(lib.fr_graph_blocks(_lib.ptr(ete), _lib.ptr(swt), K, _lib.ptr(t["dptr"]),
+                                   _lib.ptr(t["dent"]), n_nodes, _lib.ptr(t["pptr"]),
+                                   _lib.ptr(t["pent"]), L["n_pairs"], _lib.ptr(diag),
+                                   _lib.ptr(off), _lib.stream_handle()))
+    return diag.cpu().numpy(), off[:L["n_pairs"]].cpu().numpy(), L
+
+
+def assemble_articulated(spec: ResidualSpec, current_positions, tree) -> NormalEquations:
+    """Two-phase assembly (mstep.py:213-229): per-body 6x6 blocks reduced on the
+    device (points grouped by body), projected through the spatial velocity
+    Jacobians on the host."""
+    from ._rigid import unpack_upper6
+    x = np.asarray(current_positions, dtype=float)
+    if len(x) != len(spec):
+        raise ValueError("residual count does not match point count")
+    if tree.point_bodies is None:
+        raise ValueError("articulated assembly needs the tree's point binding")
+    if len(tree.point_bodies) != len(spec):
+        raise ValueError("point binding does not match the residual count")
+    nb = tree.n_bodies
+    ete = _device_point_rows(spec, x)
+    idx = np.asarray(tree.point_bodies, dtype=np.int64)[:, None]
+    diag, _, _ = _device_blocks(ete, np.ones(idx.shape), idx, nb)
+    H = np.stack([unpack_upper6(diag[b, :21]) for b in range(nb)])
+    g = diag[:, 21:27]
+    live = np.flatnonzero(H.any(axis=(1, 2)) | g.any(axis=1))
+    S = tree.spatial_velocity_jacobians()[live]
+    A = np.einsum("bip,bij,bjq->pq", S, H[live], S, optimize=True)
+    b = np.einsum("bip,bi->p", S, g[live])
+    return NormalEquations(tree.n_params, b=b, A=A)
+
+
+def assemble_nodegraph(spec: ResidualSpec, current_positions, graph,
+                       lambda_reg: float = 0.0) -> NormalEquations:
+    """Block-sparse assembly (mstep.py:232-314): data blocks on the device,
+    ARAP regulariser on the host."""
+    from ._nodegraph import normal_equations_from
+    x = np.asarray(current_positions, dtype=float)
+    if len(x) != len(spec):
+        raise ValueError("residual count does not match point count")
+    if len(graph.skinning.indices) != len(spec):
+        raise ValueError("skinning does not match the residual count")
+    if lambda_reg < 0:
+        raise ValueError("lambda_reg must be nonnegative")
+    ete = _device_point_rows(spec, x)
+    diag, off, L = _device_blocks(ete, graph.skinning.weights, graph.skinning.indices,
+                                  graph.n_nodes)
+    return normal_equations_from(graph, diag, off, L["pair_lo"], L["pair_hi"], lambda_reg)
+
+
+def _assemble(spec, x, model, lambda_reg) -> NormalEquations:
+    from .kinematics import ArticulatedTree, NodeGraph
+    if isinstance(model, RigidModel):
+        return assemble_rigid(spec, x)
+    if isinstance(model, ArticulatedTree):
+        return assemble_articulated(spec, x, model)
+    if isinstance(model, NodeGraph):
+        return assemble_nodegraph(spec, x, model, lambda_reg)
+    raise TypeError(f"unsupported kinematic model {type(model).__name__}")
+
+
+def _total_objective(spec, reference, model, lambda_reg) -> float:
+    """mstep.py:404-408"""
+    from ._nodegraph import regularizer_objective
+    from .kinematics import NodeGraph
+    value = objective(spec, forward_points(reference, model).positions)
+    if isinstance(model, NodeGraph):
+        value += regularizer_objective(model, lambda_reg)
+    return value
+
+
+def m_step_general(spec, reference, model, opts):
+    """m_step for articulated trees and node graphs over an explicit spec."""
+    current = model
+    value = _total_objective(spec, reference, current, opts.lambda_reg)
+    diag = MStepDiagnostics(objectives=[value])
+    for _ in range(opts.max_gn_iters):
+        x = forward_points(reference, current).positions
+        eq = _assemble(spec, x, current, opts.lambda_reg)
+        if not np.any(eq.b):
+            break
+        stats: dict = {}
+        step = gn_solve(eq, opts.damping, opts.solve_method, _stats=stats)
+        diag.dampings.append(stats.get("damping", 0.0))
+        scale = 1.0
+        accepted = None
+        for halving in range(opts.max_halvings + 1):
+            cand = current.updated(scale * step)
+            cv = _total_objective(spec, reference, cand, opts.lambda_reg)
+            if _accepts(cv, value):
+                accepted = (cand, cv, halving)
+                break
+            scale *= 0.5
+        if accepted is None:
+            break
+        current, value, halvings = accepted
+        diag.objectives.append(value)
+        diag.halvings.append(halvings)
+        sn = float(np.linalg.norm(scale * step))
+        diag.step_norms.append(sn)
+        if sn <= opts.step_tolerance:
+            break
+    return current, diag
+
+
+__all__ = ["assemble_articulated", "assemble_nodegraph", "RESIDUAL_MODES", "ResidualSpec", "residuals_from_moments", "NormalEquations",
            "objective", "assemble_rigid", "gn_solve", "MStepOptions", "MStepDiagnostics",
            "m_step", "point_twist_jacobian"]
