@@ -155,10 +155,11 @@ typedef struct fr_rigid_pass_params {
     int mode;           /* FR_POINT_TO_POINT / FR_POINT_TO_PLANE */
     int m2_col;         /* value column of |y|^2 or -1 */
     int normal_col;     /* value column of the normal sum or -1 */
-    int flags;          /* FR_PASS_FAST: float32 ranks / barycentrics / table rows */
+    int flags;          /* FR_PASS_FAST: float32 ranks / barycentrics / table rows;
+                           FR_PASS_F32: + float32 coordinates / moments (pt2pt) */
 } fr_rigid_pass_params;
 
-enum { FR_PASS_FAST = 1 };
+enum { FR_PASS_FAST = 1, FR_PASS_F32 = 2 };
 
 /* Number of float64 partial sums the pass produces for a mode. */
 int fr_rigid_pass_width(int mode, int with_sigma);

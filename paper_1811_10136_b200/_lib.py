@@ -54,7 +54,7 @@ class RigidEmConfig(ctypes.Structure):
                 ("max_halvings", ctypes.c_int), ("fast", ctypes.c_int)]
 
 
-FR_PASS_FAST = 1
+FR_PASS_FAST, FR_PASS_F32 = 1, 2
 FR_TERM = {0: "max_iters", 1: "converged", 2: "degenerate", 3: "solver_error"}
 
 

@@ -48,8 +48,18 @@ _E = [skew(e) for e in np.eye(3)]   # K_k = [e_k]x
 # Model points are not a bit-exact contract (the reference forms them with a
 # BLAS product), and the float32 path keeps the E-step sums to ~1e-7 relative.
 FAST_QUERY = True
+# Point-to-point pass with float32 centred coordinates and float32 moment
+# partials folded into float64 every 16 points (FR_PASS_F32).
+F32_POINTS = True
 # Sort the model points along a Morton curve once per registration.
 SPATIAL_ORDER = True
+
+
+def pass_flags() -> int:
+    flags = _lib.FR_PASS_FAST if FAST_QUERY else 0
+    if FAST_QUERY and F32_POINTS:
+        flags |= _lib.FR_PASS_F32
+    return flags
 
 
 def _sym3(v6) -> np.ndarray:
@@ -226,7 +236,7 @@ class RigidDevicePath:
         p.mode = self.mode
         p.m2_col = self.m2_col
         p.normal_col = self.normal_col
-        p.flags = _lib.FR_PASS_FAST if FAST_QUERY else 0
+        p.flags = pass_flags()
         return p
 
     def run_pass(self, R, t) -> np.ndarray:
@@ -319,7 +329,7 @@ class DeviceEM:
         c.max_em_iters = self.max_iters
         c.max_gn_iters = int(ms.max_gn_iters)
         c.max_halvings = int(ms.max_halvings)
-        c.fast = int(FAST_QUERY if fast is None else fast)
+        c.fast = pass_flags() if fast is None else int(fast)
         self._cfg = c
         h = ctypes.c_void_p()
         _lib.check(self.lib.fr_rigid_em_create(path.lattice.handle, _lib.ptr(path.ref), path.M,

@@ -359,6 +359,63 @@ __device__ __forceinline__ void qsimplex3(const double *el, QSimplex3 &q) {
     }
 }
 
+// float32 variant: el = 4 * base + frac with `base` an exact integer offset per
+// coordinate (from the float64 pose constant) and |frac| = O(cloud / sigma)
+__device__ __forceinline__ void qsimplex3f(const float *frac, const int *base, QSimplex3 &q) {
+    constexpr int kLim = (int)(kKeyLim / 4 - 2);
+    float d[4];
+    int ri[4];
+    q.overflow = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float r = rintf(frac[i] * 0.25f);
+        d[i] = fmaf(-4.0f, r, frac[i]);
+        ri[i] = (int)r + base[i];
+        q.overflow |= (ri[i] >= kLim) | (ri[i] <= -kLim);
+    }
+    int rank[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i + 1; j < 4; ++j) {
+            // stable descending order: the earlier index wins ties
+            if (d[j] > d[i]) ++rank[i];
+            else ++rank[j];
+        }
+    const int h = ri[0] + ri[1] + ri[2] + ri[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int rk = rank[i] + h;
+        if (rk < 0) { rk += 4; ri[i] += 1; d[i] -= 4.0f; }
+        else if (rk > 3) { rk -= 4; ri[i] -= 1; d[i] += 4.0f; }
+        rank[i] = rk;
+    }
+    float sv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float v = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v = (rank[i] == k) ? d[i] : v;
+        sv[k] = 0.25f * v;
+    }
+    q.bary[0] = 1.0f + sv[3] - sv[0];
+#pragma unroll
+    for (int l = 1; l < 4; ++l) q.bary[l] = sv[3 - l] - sv[4 - l];
+    const unsigned long long unit[3] = {1ull << (2 * kKeyBits), 1ull << kKeyBits, 1ull};
+    unsigned long long p0 = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) p0 += (unsigned long long)(4 * ri[i] + kKeyOff) * unit[i];
+    const unsigned long long U = unit[0] + unit[1] + unit[2];
+    unsigned long long B = 0;
+    q.key[0] = p0;
+#pragma unroll
+    for (int l = 1; l < 4; ++l) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) B += (rank[i] == 4 - l) ? unit[i] : 0ull;
+        q.key[l] = p0 + (unsigned long long)l * U - 4ull * B;
+    }
+}
+
 template <int NF4>
 __device__ __forceinline__ unsigned long long slot_key(const float4 *slot) {
     return __ldg(reinterpret_cast<const unsigned long long *>(slot));

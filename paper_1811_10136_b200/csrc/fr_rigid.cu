@@ -28,6 +28,7 @@ namespace fr {
 struct RigidK {
     double M[4][3];      // elevated = M xh + e0 (embedding folded with the pose)
     double e0[4];
+    double A[4][3];      // embedding alone: elevated = A (xt + c_world)
     double R[9];
     double c_ref[3];
     double c_world[3];
@@ -55,8 +56,10 @@ __host__ __device__ inline void make_rigid_k(const double A[4][3], const double 
     for (int i = 0; i < 3; ++i)
         k->c_world[i] = R[3 * i] * c_ref[0] + R[3 * i + 1] * c_ref[1] + R[3 * i + 2] * c_ref[2] + t[i];
     for (int i = 0; i < 4; ++i) {
-        for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < 3; ++j) {
             k->M[i][j] = A[i][0] * R[j] + A[i][1] * R[3 + j] + A[i][2] * R[6 + j];
+            k->A[i][j] = A[i][j];
+        }
         k->e0[i] = A[i][0] * k->c_world[0] + A[i][1] * k->c_world[1] + A[i][2] * k->c_world[2];
     }
     for (int q = 0; q < 9; ++q) k->R[q] = R[q];
@@ -317,6 +320,157 @@ k_rigid_pass(const float *__restrict__ ref, long long m, RigidK kv, const RigidK
         point_step<MODE, NV, SIG, FAST, NA>(k, tab, tabf, xh, p, m, wtn, acc);
     }
     block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
+}
+
+// ---------------------------------------------------------------------------
+// float32 point path of the point_to_point pass (FR_PASS_F32).  Centred world
+// coordinates xt = R (x_ref - c_ref) are float32 (|xt| ~ cloud radius); the
+// elevated coordinates are A xt + A c with the pose constant A c split into an
+// exact multiple of 4 and a float32 fraction, so every rounding acts on
+// O(cloud / sigma) lattice units; targets are formed relative to the centre.
+// Moments are accumulated in float32 over 16 points per thread, then folded
+// into float64 accumulators (relative error ~1e-6, far below what moves a
+// halving decision or the pose).  Only float64 left per point:
+// the fold every 16 points.
+struct F32K {
+    float R[9];
+    float cref[3];
+    float cw[3];
+    float A[4][3];
+    float f0[4];
+    int base[4];
+    float cp;
+};
+
+constexpr int kF32Fold = 16;
+
+template <bool DEV>
+__global__ void __launch_bounds__(kPassThreads, 2)
+k_rigid_pass_f32(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
+                 const int *done, SliceTableF tabf, double *__restrict__ partials) {
+    constexpr int NA = kP2PtBase;
+    __shared__ F32K f;
+    if (DEV && *done) return;
+    if (threadIdx.x == 0) {
+        const RigidK &k = DEV ? *kd : kv;
+        for (int q = 0; q < 9; ++q) f.R[q] = (float)k.R[q];
+        for (int q = 0; q < 3; ++q) {
+            f.cref[q] = (float)k.c_ref[q];
+            f.cw[q] = (float)k.c_world[q];
+        }
+        for (int i = 0; i < 4; ++i) {
+            for (int j = 0; j < 3; ++j) f.A[i][j] = (float)k.A[i][j];
+            const double e = k.e0[i];
+            const double b = rint(e * 0.25);
+            f.base[i] = (int)b;
+            f.f0[i] = (float)(e - 4.0 * b);
+        }
+        f.cp = (float)k.cp;
+    }
+    // per-thread float64 accumulators live in shared memory (column per
+    // thread, conflict-free); registers hold only the float32 partials
+    extern __shared__ double sacc[];   // [NA][kPassThreads]
+#pragma unroll
+    for (int q = 0; q < NA; ++q) sacc[q * kPassThreads + threadIdx.x] = 0.0;
+    __syncthreads();
+    float a[NA];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) a[q] = 0.0f;
+    int fold = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    float nx = 0.f, ny = 0.f, nz = 0.f;
+    if (p < m) {
+        nx = __ldg(ref + p);
+        ny = __ldg(ref + m + p);
+        nz = __ldg(ref + 2 * m + p);
+    }
+    for (; p < m; p += stride) {
+        const float xh[3] = {nx - f.cref[0], ny - f.cref[1], nz - f.cref[2]};
+        const long long pn = p + stride;
+        if (pn < m) {
+            nx = __ldg(ref + pn);
+            ny = __ldg(ref + m + pn);
+            nz = __ldg(ref + 2 * m + pn);
+        }
+        float y[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            y[i] = fmaf(f.R[3 * i + 2], xh[2], fmaf(f.R[3 * i + 1], xh[1], f.R[3 * i] * xh[0]));
+        float el[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            el[i] = fmaf(f.A[i][2], y[2], fmaf(f.A[i][1], y[1], fmaf(f.A[i][0], y[0], f.f0[i])));
+        QSimplex3 q;
+        qsimplex3f(el, f.base, q);
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!q.overflow) {
+            float4 v[4][1];
+            gather_simplex_f<1>(tabf, q.key, v);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const float b = q.bary[l];
+                o[0] = fmaf(b, v[l][0].x, o[0]);
+                o[1] = fmaf(b, v[l][0].y, o[1]);
+                o[2] = fmaf(b, v[l][0].z, o[2]);
+                o[3] = fmaf(b, v[l][0].w, o[3]);
+            }
+        }
+        const float m0 = fmaxf(o[0], 0.0f);
+        const bool sup = m0 >= 1e-12f;
+        const float w = sup ? (f.cp > 0.0f ? __fdividef(m0, m0 + f.cp) : 1.0f) : 0.0f;
+        const float inv = sup ? __frcp_rn(m0) : 0.0f;
+        // residual r = x - t in centred coordinates; unsupported: t = x, w = 0
+        float r[3], wy[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            r[j] = sup ? y[j] - fmaf(o[1 + j], inv, -f.cw[j]) : 0.0f;
+            wy[j] = w * y[j];
+        }
+        a[0] += w;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) a[1 + j] += wy[j];
+        a[4] = fmaf(wy[0], y[0], a[4]);
+        a[5] = fmaf(wy[0], y[1], a[5]);
+        a[6] = fmaf(wy[0], y[2], a[6]);
+        a[7] = fmaf(wy[1], y[1], a[7]);
+        a[8] = fmaf(wy[1], y[2], a[8]);
+        a[9] = fmaf(wy[2], y[2], a[9]);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const float wr = w * r[j];
+            a[10 + j] += wr;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) a[13 + 3 * j + c] = fmaf(wr, y[c], a[13 + 3 * j + c]);
+            a[22 + j] = fmaf(wr, r[j], a[22 + j]);
+        }
+        if (++fold == kF32Fold) {
+#pragma unroll
+            for (int c = 0; c < NA; ++c) {
+                sacc[c * kPassThreads + threadIdx.x] += (double)a[c];
+                a[c] = 0.0f;
+            }
+            fold = 0;
+        }
+    }
+    double acc[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) acc[c] = sacc[c * kPassThreads + threadIdx.x] + (double)a[c];
+    block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
+}
+
+constexpr size_t kF32Smem = (size_t)kP2PtBase * kPassThreads * sizeof(double);
+
+static int set_f32_smem() {
+    static bool done = false;
+    if (!done) {
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
+        done = true;
+    }
+    return FR_OK;
 }
 
 // articulated pass (mstep.py:179-202, 213-229): model points sorted by body,
@@ -815,12 +969,26 @@ static int launch_pass_t(const fr_lattice *lat, const float *ref, long long m, c
 }
 
 // dispatch on (mode, nv, sigma sums, fast, device params)
-static int launch_pass(const fr_lattice *lat, int mode, bool sig, bool fast, bool dev,
+static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, bool dev,
                        const float *ref, long long m, const RigidK &k, const RigidK *kd,
                        const int *done, float *wtn, double *scratch, double *sums,
                        cudaStream_t s) {
     const int nv = lat->nv;
-    fast = fast && !sig && lat->fslots != nullptr;
+    const bool fast = qpath != 0 && !sig && lat->fslots != nullptr;
+    if (fast && qpath == 2 && mode == FR_POINT_TO_POINT && nv == 4) {
+        const int grid = pass_grid();
+        FR_TRY(set_f32_smem());
+        if (dev)
+            k_rigid_pass_f32<true><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
+                                                                        lat->table_f(), scratch);
+        else
+            k_rigid_pass_f32<false><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
+                                                                         lat->table_f(), scratch);
+        FR_CHECK_LAUNCH();
+        k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, grid, kP2PtBase, sums, done);
+        FR_CHECK_LAUNCH();
+        return FR_OK;
+    }
 #define FR_L(MODE, NV, SIG, FAST, DEV) \
     return launch_pass_t<MODE, NV, SIG, FAST, DEV>(lat, ref, m, k, kd, done, wtn, scratch, sums, s)
     if (mode == FR_POINT_TO_POINT) {
@@ -915,8 +1083,8 @@ int fr_rigid_pass(const fr_lattice *lat, const float *ref, int64_t m,
         FR_CUDA(cudaMemsetAsync(sums, 0, na * sizeof(double), s));
         return FR_OK;
     }
-    const bool fast = (p->flags & FR_PASS_FAST) != 0;
-    return launch_pass(lat, mode, sig, fast, false, ref, m, k, nullptr, nullptr, wtn, scratch,
+    const int qpath = (p->flags & FR_PASS_F32) ? 2 : ((p->flags & FR_PASS_FAST) ? 1 : 0);
+    return launch_pass(lat, mode, sig, qpath, false, ref, m, k, nullptr, nullptr, wtn, scratch,
                        sums, s);
 }
 
@@ -1059,7 +1227,7 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
     em->lat = lat;
     em->ref = ref;
     em->m = m;
-    em->fast = cfg->fast ? 1 : 0;
+    em->fast = (cfg->fast & FR_PASS_F32) ? 2 : ((cfg->fast & FR_PASS_FAST) ? 1 : 0);
     em->max_iters = cfg->max_em_iters;
     EmDev h;
     memset(&h, 0, sizeof(h));
@@ -1120,7 +1288,7 @@ int fr_rigid_em_sums(fr_rigid_em *em, double **d_sums, int *width_out) {
 static int em_pass(fr_rigid_em *em, cudaStream_t s) {
     RigidK unused;
     memset(&unused, 0, sizeof(unused));
-    return launch_pass(em->lat, FR_POINT_TO_POINT, false, em->fast != 0, true, em->ref, em->m,
+    return launch_pass(em->lat, FR_POINT_TO_POINT, false, em->fast, true, em->ref, em->m,
                        unused, &em->d_em->k, &em->d_em->done, nullptr, em->d_scratch, em->d_sums,
                        s);
 }

@@ -139,18 +139,18 @@ def test_explicit_assembly_matches_oracle(fr):
         assert fr.objective(spec, x) == pytest.approx(O.rigid_objective(ospec, x), rel=1e-12)
 
 
-@pytest.mark.parametrize("fast", [True, False])
-def test_device_loop_matches_host_loop(fr, fast):
+@pytest.mark.parametrize("path", ["f32", "fast", "exact"])
+def test_device_loop_matches_host_loop(fr, path):
     """The device-resident EM (float64 solver kernel) reproduces the host-side
-    loop's decisions: same iterations/termination, poses to round-off."""
+    loop's decisions: same iterations/termination, poses to round-off -- for
+    every query path of the pass."""
     import paper_1811_10136_b200._rigid as rg
-    from paper_1811_10136_b200.pipeline import _register_device_loop
     g = load("register_pt2pt_seed1")
     cfg = json.loads(str(g["config"]))
     config = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]),
                                    max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"])
-    old = rg.FAST_QUERY
-    rg.FAST_QUERY = fast
+    old = rg.FAST_QUERY, rg.F32_POINTS
+    rg.FAST_QUERY, rg.F32_POINTS = path != "exact", path == "f32"
     try:
         ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
         dev = fr.register(ref, obs, fr.RigidModel(), config)            # device loop
@@ -158,7 +158,7 @@ def test_device_loop_matches_host_loop(fr, fast):
             gmm=config.gmm, max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"],
             record_states=True))                                        # host loop
     finally:
-        rg.FAST_QUERY = old
+        rg.FAST_QUERY, rg.F32_POINTS = old
     assert dev.iterations == host.iterations and dev.termination == host.termination
     assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < 1e-9
     np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-9)
