@@ -140,10 +140,12 @@ class RigidMoments:
 
 
 def upload_soa(points, dev):
-    """(n, 3) host coordinates -> (3, n) float32 device planes: one float32
-    conversion on the host (12 B/point over PCIe), the transpose on the device."""
+    """(n, 3) host coordinates -> (3, n) float32 device planes.  The caller's
+    float64 array is copied as it is (no host-side conversion pass and no fresh
+    host allocation to fault in); the float32 rounding (numpy's astype
+    rounding: to nearest) and the transpose run on the device."""
     import torch
-    host = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float32))
+    host = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64))
     aos = host.to(dev, non_blocking=False)
     soa = torch.empty((3, aos.shape[0]), dtype=torch.float32, device=dev)
     soa.copy_(aos.t())

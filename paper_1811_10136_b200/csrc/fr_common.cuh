@@ -359,36 +359,38 @@ __device__ __forceinline__ void qsimplex3(const double *el, QSimplex3 &q) {
     }
 }
 
-// float32 variant: el = 4 * base + frac with `base` an exact integer offset per
-// coordinate (from the float64 pose constant) and |frac| = O(cloud / sigma)
-__device__ __forceinline__ void qsimplex3f(const float *frac, const int *base, QSimplex3 &q) {
-    constexpr int kLim = (int)(kKeyLim / 4 - 2);
+// float32 simplex core: el = 4 * base + frac with `base` an exact integer offset
+// per coordinate (from the float64 pose constant) and |frac| = O(cloud / sigma).
+// Outputs the remainder-0 point / 4 (ri, wrapped), the stable descending ranks
+// and the barycentric weights.  Vertex l has lattice coordinates
+// 4 * (ri_i - [rank_i > 3 - l]) + l (the canonical simplex of
+// permutohedral.py:140-160).
+__device__ __forceinline__ void simplex3f_core(const float *frac, const int *base, int *ri,
+                                               int *rank, float *bary) {
     float d[4];
-    int ri[4];
-    q.overflow = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const float r = rintf(frac[i] * 0.25f);
         d[i] = fmaf(-4.0f, r, frac[i]);
         ri[i] = (int)r + base[i];
-        q.overflow |= (ri[i] >= kLim) | (ri[i] <= -kLim);
+        rank[i] = 0;
     }
-    int rank[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = i + 1; j < 4; ++j) {
-            // stable descending order: the earlier index wins ties
             if (d[j] > d[i]) ++rank[i];
             else ++rank[j];
         }
     const int h = ri[0] + ri[1] + ri[2] + ri[3];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        int rk = rank[i] + h;
-        if (rk < 0) { rk += 4; ri[i] += 1; d[i] -= 4.0f; }
-        else if (rk > 3) { rk -= 4; ri[i] -= 1; d[i] += 4.0f; }
-        rank[i] = rk;
+        // single wrap into [0, 3] (select form: no divergent branches)
+        const int rk = rank[i] + h;
+        const bool lo = rk < 0, hi = rk > 3;
+        rank[i] = lo ? rk + 4 : (hi ? rk - 4 : rk);
+        ri[i] += lo ? 1 : (hi ? -1 : 0);
+        d[i] -= lo ? 4.0f : (hi ? -4.0f : 0.0f);
     }
     float sv[4];
 #pragma unroll
@@ -398,9 +400,57 @@ __device__ __forceinline__ void qsimplex3f(const float *frac, const int *base, Q
         for (int i = 0; i < 4; ++i) v = (rank[i] == k) ? d[i] : v;
         sv[k] = 0.25f * v;
     }
-    q.bary[0] = 1.0f + sv[3] - sv[0];
+    bary[0] = 1.0f + sv[3] - sv[0];
 #pragma unroll
-    for (int l = 1; l < 4; ++l) q.bary[l] = sv[3 - l] - sv[4 - l];
+    for (int l = 1; l < 4; ++l) bary[l] = sv[3 - l] - sv[4 - l];
+}
+
+// approximate float32 reciprocal (MUFU.RCP, ~1 ulp; no slow path)
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// dense float32 slice grid (d = 3, nv <= 4): one float4 (gain * value row) per
+// (cell q = floor(k / 4) over the first three lattice coordinates, remainder
+// class r = k mod 4); the fourth coordinate is implied by the zero sum.  The
+// grid spans the sites' q box padded by one cell on each side, so a point whose
+// remainder-0 cell ri lies in [a, b + 1] has all four vertices inside it and a
+// point outside that range has no site among its vertices (all-zero slice).
+struct DenseSliceF {
+    const float4 *cells;    // [n0][n1][n2][4]
+    int a[3];               // site q minimum per coordinate
+    unsigned span[3];       // b - a + 1
+    int s0, s1;             // cell strides of coordinates 0 and 1 (coordinate 2: 1)
+};
+
+// gather the 4 vertex rows of the simplex with remainder-0 cell ri and ranks
+__device__ __forceinline__ bool gather_dense(const DenseSliceF &t, const int *ri, const int *rank,
+                                             float4 *v) {
+    const bool in = ((unsigned)(ri[0] - t.a[0]) <= t.span[0]) &
+                    ((unsigned)(ri[1] - t.a[1]) <= t.span[1]) &
+                    ((unsigned)(ri[2] - t.a[2]) <= t.span[2]);
+    if (!in) return false;
+    // cell of ri relative to the padded origin a - 1
+    int c = (ri[0] - t.a[0] + 1) * t.s0 + (ri[1] - t.a[1] + 1) * t.s1 + (ri[2] - t.a[2] + 1);
+    v[0] = __ldg(t.cells + 4 * c);
+#pragma unroll
+    for (int l = 1; l < 4; ++l) {
+        c -= (rank[0] == 4 - l ? t.s0 : 0) + (rank[1] == 4 - l ? t.s1 : 0) + (rank[2] == 4 - l ? 1 : 0);
+        v[l] = __ldg(t.cells + 4 * c + l);
+    }
+    return true;
+}
+
+// float32 variant of qsimplex3 (packed keys for the hash-slot table)
+__device__ __forceinline__ void qsimplex3f(const float *frac, const int *base, QSimplex3 &q) {
+    constexpr int kLim = (int)(kKeyLim / 4 - 2);
+    int ri[4], rank[4];
+    simplex3f_core(frac, base, ri, rank, q.bary);
+    q.overflow = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q.overflow |= (ri[i] >= kLim) | (ri[i] <= -kLim);
     const unsigned long long unit[3] = {1ull << (2 * kKeyBits), 1ull << kKeyBits, 1ull};
     unsigned long long p0 = 0;
 #pragma unroll
@@ -500,6 +550,10 @@ struct fr_lattice {
     fr::SliceTableF table_f() const {
         return fr::SliceTableF{fslots, fmask, fshift32, nf4};
     }
+    // dense float32 slice grid (d = 3, nv <= 4, box small enough); null otherwise
+    float4 *dcells = nullptr;
+    fr::DenseSliceF dense{};
+    long long dense_cells = 0;
     // device counters / flags
     unsigned long long *d_counters = nullptr;   // [0] sites, [1] src count, [2] overflow
 };

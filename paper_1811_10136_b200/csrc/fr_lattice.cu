@@ -12,7 +12,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "fr_common.cuh"
@@ -734,11 +736,97 @@ static void free_slice(fr_lattice *lat) {
     cudaFree(lat->skeys);
     cudaFree(lat->svals);
     cudaFree(lat->fslots);
+    cudaFree(lat->dcells);
     lat->skeys = nullptr;
     lat->svals = nullptr;
     lat->fslots = nullptr;
+    lat->dcells = nullptr;
+    lat->dense = fr::DenseSliceF{};
+    lat->dense_cells = 0;
     lat->nvp = 0;
     lat->nf4 = 0;
+}
+
+// dense grid budget: the grid replaces hashing in the EM pass when the padded
+// site box needs at most this many cells (64 B each)
+static long long dense_cell_limit() {
+    const char *e = getenv("FR_DENSE_MAX_CELLS");
+    return e ? atoll(e) : (16ll << 20);    // 1 GiB
+}
+
+// q = floor(k / 4) box of the sites' first three coordinates
+__global__ void k_site_qbox(long long S, const int *site_keys, int *box) {
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S;
+         i += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int q = site_keys[i * 4 + c] >> 2;
+            lo[c] = min(lo[c], q);
+            hi[c] = max(hi[c], q);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[c] = min(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+            hi[c] = max(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(box + c, lo[c]);
+            atomicMax(box + 3 + c, hi[c]);
+        }
+    }
+}
+
+__global__ void k_dense_fill(long long S, const int *site_keys, const double *vals, int nv,
+                             double gain, fr::DenseSliceF t, float4 *cells) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    const int *k = site_keys + i * 4;
+    const int c = ((k[0] >> 2) - t.a[0] + 1) * t.s0 + ((k[1] >> 2) - t.a[1] + 1) * t.s1 +
+                  ((k[2] >> 2) - t.a[2] + 1);
+    float v[4];
+    for (int q = 0; q < 4; ++q) v[q] = q < nv ? (float)(gain * vals[i * nv + q]) : 0.0f;
+    cells[4 * (long long)c + (k[0] & 3)] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
+    if (lat->dim != 3 || lat->nv > 4 || lat->n_sites == 0) return FR_OK;
+    int *dbox = nullptr;
+    FR_CUDA(cudaMallocAsync(&dbox, 6 * sizeof(int), s));
+    const int init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
+    FR_CUDA(cudaMemcpyAsync(dbox, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    k_site_qbox<<<std::min<long long>(grid_for(lat->n_sites), 1184), 256, 0, s>>>(
+        lat->n_sites, lat->site_keys, dbox);
+    FR_CHECK_LAUNCH();
+    int box[6];
+    FR_CUDA(cudaMemcpyAsync(box, dbox, sizeof(box), cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    FR_CUDA(cudaFreeAsync(dbox, s));
+    long long n[3], cells = 1;
+    for (int c = 0; c < 3; ++c) {
+        n[c] = (long long)box[3 + c] - box[c] + 3;
+        cells *= n[c];
+        if (cells > dense_cell_limit()) return FR_OK;     // hash slots only
+    }
+    fr::DenseSliceF t{};
+    for (int c = 0; c < 3; ++c) {
+        t.a[c] = box[c];
+        t.span[c] = (unsigned)(box[3 + c] - box[c] + 1);
+    }
+    t.s1 = (int)n[2];
+    t.s0 = (int)(n[1] * n[2]);
+    FR_CUDA(cudaMalloc(&lat->dcells, (size_t)cells * 4 * sizeof(float4)));
+    FR_CUDA(cudaMemsetAsync(lat->dcells, 0, (size_t)cells * 4 * sizeof(float4), s));
+    k_dense_fill<<<grid_for(lat->n_sites), 256, 0, s>>>(lat->n_sites, lat->site_keys, lat->vals,
+                                                        lat->nv, lat->c.gain, t, lat->dcells);
+    FR_CHECK_LAUNCH();
+    t.cells = lat->dcells;
+    lat->dense = t;
+    lat->dense_cells = cells;
+    return FR_OK;
 }
 
 // interleaved float32 slice table for the fast EM pass (nv <= 8): slot =
@@ -801,6 +889,7 @@ static int build_slice_table(fr_lattice *lat, cudaStream_t s) {
             FR_CHECK_LAUNCH();
         }
     }
+    if (D == 3) FR_TRY(build_dense_grid(lat, s));
     unsigned long long hc[3];
     FR_TRY(read_counters(lat, s, hc));
     if (hc[2] & 2ull) {

@@ -344,10 +344,10 @@ struct F32K {
 
 constexpr int kF32Fold = 16;
 
-template <bool DEV>
+template <bool DEV, bool DENSE>
 __global__ void __launch_bounds__(kPassThreads, 2)
 k_rigid_pass_f32(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
-                 const int *done, SliceTableF tabf, double *__restrict__ partials) {
+                 const int *done, SliceTableF tabf, DenseSliceF dg, double *__restrict__ partials) {
     constexpr int NA = kP2PtBase;
     __shared__ F32K f;
     if (DEV && *done) return;
@@ -401,25 +401,41 @@ k_rigid_pass_f32(const float *__restrict__ ref, long long m, RigidK kv, const Ri
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             el[i] = fmaf(f.A[i][2], y[2], fmaf(f.A[i][1], y[1], fmaf(f.A[i][0], y[0], f.f0[i])));
-        QSimplex3 q;
-        qsimplex3f(el, f.base, q);
         float o[4] = {0.f, 0.f, 0.f, 0.f};
-        if (!q.overflow) {
-            float4 v[4][1];
-            gather_simplex_f<1>(tabf, q.key, v);
+        if (DENSE) {
+            int ri[4], rank[4];
+            float bary[4];
+            simplex3f_core(el, f.base, ri, rank, bary);
+            float4 v[4];
+            if (gather_dense(dg, ri, rank, v)) {
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const float b = q.bary[l];
-                o[0] = fmaf(b, v[l][0].x, o[0]);
-                o[1] = fmaf(b, v[l][0].y, o[1]);
-                o[2] = fmaf(b, v[l][0].z, o[2]);
-                o[3] = fmaf(b, v[l][0].w, o[3]);
+                for (int l = 0; l < 4; ++l) {
+                    o[0] = fmaf(bary[l], v[l].x, o[0]);
+                    o[1] = fmaf(bary[l], v[l].y, o[1]);
+                    o[2] = fmaf(bary[l], v[l].z, o[2]);
+                    o[3] = fmaf(bary[l], v[l].w, o[3]);
+                }
+            }
+        } else {
+            QSimplex3 q;
+            qsimplex3f(el, f.base, q);
+            if (!q.overflow) {
+                float4 v[4][1];
+                gather_simplex_f<1>(tabf, q.key, v);
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    const float b = q.bary[l];
+                    o[0] = fmaf(b, v[l][0].x, o[0]);
+                    o[1] = fmaf(b, v[l][0].y, o[1]);
+                    o[2] = fmaf(b, v[l][0].z, o[2]);
+                    o[3] = fmaf(b, v[l][0].w, o[3]);
+                }
             }
         }
         const float m0 = fmaxf(o[0], 0.0f);
         const bool sup = m0 >= 1e-12f;
-        const float w = sup ? (f.cp > 0.0f ? __fdividef(m0, m0 + f.cp) : 1.0f) : 0.0f;
-        const float inv = sup ? __frcp_rn(m0) : 0.0f;
+        const float w = sup ? (f.cp > 0.0f ? m0 * rcp_approx(m0 + f.cp) : 1.0f) : 0.0f;
+        const float inv = sup ? rcp_approx(m0) : 0.0f;
         // residual r = x - t in centred coordinates; unsupported: t = x, w = 0
         float r[3], wy[3];
 #pragma unroll
@@ -464,9 +480,13 @@ constexpr size_t kF32Smem = (size_t)kP2PtBase * kPassThreads * sizeof(double);
 static int set_f32_smem() {
     static bool done = false;
     if (!done) {
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
         done = true;
     }
@@ -978,12 +998,14 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
     if (fast && qpath == 2 && mode == FR_POINT_TO_POINT && nv == 4) {
         const int grid = pass_grid();
         FR_TRY(set_f32_smem());
-        if (dev)
-            k_rigid_pass_f32<true><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
-                                                                        lat->table_f(), scratch);
-        else
-            k_rigid_pass_f32<false><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
-                                                                         lat->table_f(), scratch);
+        const SliceTableF tf = lat->table_f();
+        const DenseSliceF dg = lat->dense;
+        const bool dense = lat->dcells != nullptr;
+#define FR_F32(DEV, DENSE) \
+    k_rigid_pass_f32<DEV, DENSE><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, tf, dg, scratch)
+        if (dev) { if (dense) FR_F32(true, true); else FR_F32(true, false); }
+        else { if (dense) FR_F32(false, true); else FR_F32(false, false); }
+#undef FR_F32
         FR_CHECK_LAUNCH();
         k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, grid, kP2PtBase, sums, done);
         FR_CHECK_LAUNCH();

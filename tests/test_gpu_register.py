@@ -139,18 +139,26 @@ def test_explicit_assembly_matches_oracle(fr):
         assert fr.objective(spec, x) == pytest.approx(O.rigid_objective(ospec, x), rel=1e-12)
 
 
-@pytest.mark.parametrize("path", ["f32", "fast", "exact"])
-def test_device_loop_matches_host_loop(fr, path):
+# device-vs-host loop agreement: float64 round-off, or float32 round-off on
+# the float32 point path
+LOOP_TOL = {"f32": 1e-6, "f32_hash": 1e-6, "fast": 1e-9, "exact": 1e-9}
+
+
+@pytest.mark.parametrize("path", ["f32", "f32_hash", "fast", "exact"])
+def test_device_loop_matches_host_loop(fr, path, monkeypatch):
     """The device-resident EM (float64 solver kernel) reproduces the host-side
     loop's decisions: same iterations/termination, poses to round-off -- for
-    every query path of the pass."""
+    every query path of the pass (f32 over the dense slice grid and over the
+    hash slots)."""
     import paper_1811_10136_b200._rigid as rg
+    if path == "f32_hash":
+        monkeypatch.setenv("FR_DENSE_MAX_CELLS", "0")
     g = load("register_pt2pt_seed1")
     cfg = json.loads(str(g["config"]))
     config = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]),
                                    max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"])
     old = rg.FAST_QUERY, rg.F32_POINTS
-    rg.FAST_QUERY, rg.F32_POINTS = path != "exact", path == "f32"
+    rg.FAST_QUERY, rg.F32_POINTS = path != "exact", path.startswith("f32")
     try:
         ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
         dev = fr.register(ref, obs, fr.RigidModel(), config)            # device loop
@@ -159,17 +167,25 @@ def test_device_loop_matches_host_loop(fr, path):
             record_states=True))                                        # host loop
     finally:
         rg.FAST_QUERY, rg.F32_POINTS = old
+    # the two loops derive the pose constants in different float64 orders
+    # (device FMAs vs NumPy); the float32 point path can turn that last-bit
+    # difference into a float32 ulp of a pass parameter
+    tol = LOOP_TOL[path]
     assert dev.iterations == host.iterations and dev.termination == host.termination
-    assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < 1e-9
-    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-9)
-    np.testing.assert_allclose(dev.twist_norms, host.twist_norms, rtol=1e-6, atol=1e-12)
+    assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < tol
+    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=tol)
+    np.testing.assert_allclose(dev.twist_norms, host.twist_norms, rtol=max(tol, 1e-6), atol=1e-12)
     assert_pose_parity(dev.kinematics.pose.rotation, dev.kinematics.pose.translation,
                        g["R"], g["t"], O.bbox_diameter(g["X"]))
 
 
-def test_device_loop_mstep_options(fr):
+@pytest.mark.parametrize("path", ["f32", "exact"])
+def test_device_loop_mstep_options(fr, path, monkeypatch):
     """Extra GN iterations, explicit damping and the halving cap run through the
     device solver with the same results as the host loop."""
+    import paper_1811_10136_b200._rigid as rg
+    monkeypatch.setattr(rg, "FAST_QUERY", path != "exact")
+    monkeypatch.setattr(rg, "F32_POINTS", path == "f32")
     g = load("register_pt2pt_seed2")
     cfg = json.loads(str(g["config"]))
     ms = fr.MStepOptions(max_gn_iters=3, damping=1e-4, max_halvings=4)
@@ -178,9 +194,10 @@ def test_device_loop_mstep_options(fr):
     ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
     dev = fr.register(ref, obs, fr.RigidModel(), fr.RegistrationConfig(**base))
     host = fr.register(ref, obs, fr.RigidModel(), fr.RegistrationConfig(**base, record_states=True))
+    tol = LOOP_TOL[path]
     assert dev.iterations == host.iterations
-    assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < 1e-9
-    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-9)
+    assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < tol
+    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=tol)
 
 
 def test_degenerate_termination(fr):
