@@ -355,14 +355,16 @@ def run_b200(args):
                                    "configs[4])".format(args.points),
                        "points_per_gpu": M_local, "model_points_total": M_total,
                        "obs_points": N_obs, "sigma_frac": 0.05, "outlier_ratio": 0.1,
-                       "lattice_sites": sites, "build_ms": build_ms, "l2": l2_note,
-                       "query_path": "float64 embedding, float32 ranks/barycentrics/table rows",
+                       "lattice_sites": sites, "dense_grid_cells": path.lattice.dense_cells,
+                       "build_ms": build_ms, "l2": l2_note,
+                       "query_path": "float32 points over the dense slice grid, float64 "
+                                     "accumulation every 32 points",
                        "parallelism": f"dp{world} (model shards, replicated lattice, NCCL "
                                       "all-reduce of 25 doubles per iteration)"},
             "em_iters_per_sec": args.steps / (total_ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_rigid_pass (+k_reduce_cols)",
+                         "kernel": "k_rigid_pass_grid (+k_reduce_cols)",
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": pass_ms,
                          "peak_source": peak_kind},
             "cpu_baseline": cpu,

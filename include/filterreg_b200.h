@@ -87,6 +87,12 @@ int fr_lattice_blur(fr_lattice *lat, void *stream);
 /* num_sites / value width / blurred flag (permutohedral.py:343-345). */
 int fr_lattice_info(const fr_lattice *lat, int64_t *num_sites, int *nv, int *blurred);
 
+/* Cells of the dense float32 slice grid the EM pass queries instead of the
+ * hash table (d = 3, 4 value columns, site box within FR_DENSE_MAX_CELLS,
+ * default 16M cells); 0 when the lattice has none.  Engine-internal
+ * acceleration structure -- no reference counterpart. */
+int fr_lattice_dense_cells(const fr_lattice *lat, int64_t *cells);
+
 /* Site table export (PermutohedralLattice.keys/.values): d_keys num_sites x
  * (dim+1) int32, d_values num_sites x nv float64.  Row order is unspecified;
  * callers sort lexicographically to get the reference order. */

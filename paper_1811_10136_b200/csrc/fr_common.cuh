@@ -412,36 +412,23 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
-// dense float32 slice grid (d = 3, nv <= 4): one float4 (gain * value row) per
-// (cell q = floor(k / 4) over the first three lattice coordinates, remainder
-// class r = k mod 4); the fourth coordinate is implied by the zero sum.  The
-// grid spans the sites' q box padded by one cell on each side, so a point whose
-// remainder-0 cell ri lies in [a, b + 1] has all four vertices inside it and a
-// point outside that range has no site among its vertices (all-zero slice).
+// dense float32 slice grid (d = 3, nv == 4): one float4 per (cell q =
+// floor(k / 4) over the first three lattice coordinates, remainder class
+// r = k mod 4); the fourth coordinate is implied by the zero sum.  A row holds
+// gain * (sum y0, sum y1, sum y2, mass) -- the value columns [1, y] of
+// estep.py:153-165 rotated so the pass forms float32 pairs without moves.
+// The grid spans the sites' q box [a, b] padded by kDensePad cells per side:
+// a query's pre-wrap remainder-0 cell ri and its final vertices differ by at
+// most 2 per coordinate, so every ri in [a - 1, b + 2] addresses inside the
+// grid, and a point outside that range has no site among its vertices.
+constexpr int kDensePad = 3;
+
 struct DenseSliceF {
     const float4 *cells;    // [n0][n1][n2][4]
     int a[3];               // site q minimum per coordinate
     unsigned span[3];       // b - a + 1
     int s0, s1;             // cell strides of coordinates 0 and 1 (coordinate 2: 1)
 };
-
-// gather the 4 vertex rows of the simplex with remainder-0 cell ri and ranks
-__device__ __forceinline__ bool gather_dense(const DenseSliceF &t, const int *ri, const int *rank,
-                                             float4 *v) {
-    const bool in = ((unsigned)(ri[0] - t.a[0]) <= t.span[0]) &
-                    ((unsigned)(ri[1] - t.a[1]) <= t.span[1]) &
-                    ((unsigned)(ri[2] - t.a[2]) <= t.span[2]);
-    if (!in) return false;
-    // cell of ri relative to the padded origin a - 1
-    int c = (ri[0] - t.a[0] + 1) * t.s0 + (ri[1] - t.a[1] + 1) * t.s1 + (ri[2] - t.a[2] + 1);
-    v[0] = __ldg(t.cells + 4 * c);
-#pragma unroll
-    for (int l = 1; l < 4; ++l) {
-        c -= (rank[0] == 4 - l ? t.s0 : 0) + (rank[1] == 4 - l ? t.s1 : 0) + (rank[2] == 4 - l ? 1 : 0);
-        v[l] = __ldg(t.cells + 4 * c + l);
-    }
-    return true;
-}
 
 // float32 variant of qsimplex3 (packed keys for the hash-slot table)
 __device__ __forceinline__ void qsimplex3f(const float *frac, const int *base, QSimplex3 &q) {

@@ -785,15 +785,18 @@ __global__ void k_dense_fill(long long S, const int *site_keys, const double *va
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= S) return;
     const int *k = site_keys + i * 4;
-    const int c = ((k[0] >> 2) - t.a[0] + 1) * t.s0 + ((k[1] >> 2) - t.a[1] + 1) * t.s1 +
-                  ((k[2] >> 2) - t.a[2] + 1);
-    float v[4];
-    for (int q = 0; q < 4; ++q) v[q] = q < nv ? (float)(gain * vals[i * nv + q]) : 0.0f;
-    cells[4 * (long long)c + (k[0] & 3)] = make_float4(v[0], v[1], v[2], v[3]);
+    constexpr int P = fr::kDensePad;
+    const int c = ((k[0] >> 2) - t.a[0] + P) * t.s0 + ((k[1] >> 2) - t.a[1] + P) * t.s1 +
+                  ((k[2] >> 2) - t.a[2] + P);
+    const double *v = vals + i * nv;
+    // [1, y0, y1, y2] -> (y0, y1, y2, 1) rows, times the gain
+    cells[4 * (long long)c + (k[0] & 3)] =
+        make_float4((float)(gain * v[1]), (float)(gain * v[2]), (float)(gain * v[3]),
+                    (float)(gain * v[0]));
 }
 
 static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
-    if (lat->dim != 3 || lat->nv > 4 || lat->n_sites == 0) return FR_OK;
+    if (lat->dim != 3 || lat->nv != 4 || lat->n_sites == 0) return FR_OK;
     int *dbox = nullptr;
     FR_CUDA(cudaMallocAsync(&dbox, 6 * sizeof(int), s));
     const int init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
@@ -807,7 +810,7 @@ static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
     FR_CUDA(cudaFreeAsync(dbox, s));
     long long n[3], cells = 1;
     for (int c = 0; c < 3; ++c) {
-        n[c] = (long long)box[3 + c] - box[c] + 3;
+        n[c] = (long long)box[3 + c] - box[c] + 1 + 2 * fr::kDensePad;
         cells *= n[c];
         if (cells > dense_cell_limit()) return FR_OK;     // hash slots only
     }
@@ -1170,6 +1173,15 @@ int fr_lattice_info(const fr_lattice *lat, int64_t *num_sites, int *nv, int *blu
     if (num_sites) *num_sites = lat->n_sites;
     if (nv) *nv = lat->nv;
     if (blurred) *blurred = lat->blurred;
+    return FR_OK;
+}
+
+int fr_lattice_dense_cells(const fr_lattice *lat, int64_t *cells) {
+    if (!lat || !cells) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    *cells = lat->dense_cells;
     return FR_OK;
 }
 

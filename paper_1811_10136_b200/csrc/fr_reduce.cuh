@@ -46,15 +46,21 @@ static __global__ void k_reduce_cols(const double *partials, int nblk, int na, d
 
 // one full wave of the point-sweep kernels (2 CTAs of 256 per SM); fixed per
 // device so the reduction order -- and the sums -- are reproducible
-static inline int pass_grid() {
-    static int grid = 0;
-    if (!grid) {
-        int dev = 0, sms = 148;
+static inline int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = 2 * sms;
     }
-    return grid;
+    return sms;
 }
+
+// persistent pass grids: 2 blocks per SM, 3 for the dense-grid pass
+static inline int pass_grid() { return 2 * sm_count(); }
+static inline int pass_grid_dense() { return 3 * sm_count(); }
+// scratch rows every pass grid fits in
+static inline int pass_grid_max() { return 3 * sm_count(); }
 
 }  // namespace fr

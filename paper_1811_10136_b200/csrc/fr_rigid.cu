@@ -344,10 +344,10 @@ struct F32K {
 
 constexpr int kF32Fold = 16;
 
-template <bool DEV, bool DENSE>
+template <bool DEV>
 __global__ void __launch_bounds__(kPassThreads, 2)
 k_rigid_pass_f32(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
-                 const int *done, SliceTableF tabf, DenseSliceF dg, double *__restrict__ partials) {
+                 const int *done, SliceTableF tabf, double *__restrict__ partials) {
     constexpr int NA = kP2PtBase;
     __shared__ F32K f;
     if (DEV && *done) return;
@@ -402,34 +402,18 @@ k_rigid_pass_f32(const float *__restrict__ ref, long long m, RigidK kv, const Ri
         for (int i = 0; i < 4; ++i)
             el[i] = fmaf(f.A[i][2], y[2], fmaf(f.A[i][1], y[1], fmaf(f.A[i][0], y[0], f.f0[i])));
         float o[4] = {0.f, 0.f, 0.f, 0.f};
-        if (DENSE) {
-            int ri[4], rank[4];
-            float bary[4];
-            simplex3f_core(el, f.base, ri, rank, bary);
-            float4 v[4];
-            if (gather_dense(dg, ri, rank, v)) {
+        QSimplex3 q;
+        qsimplex3f(el, f.base, q);
+        if (!q.overflow) {
+            float4 v[4][1];
+            gather_simplex_f<1>(tabf, q.key, v);
 #pragma unroll
-                for (int l = 0; l < 4; ++l) {
-                    o[0] = fmaf(bary[l], v[l].x, o[0]);
-                    o[1] = fmaf(bary[l], v[l].y, o[1]);
-                    o[2] = fmaf(bary[l], v[l].z, o[2]);
-                    o[3] = fmaf(bary[l], v[l].w, o[3]);
-                }
-            }
-        } else {
-            QSimplex3 q;
-            qsimplex3f(el, f.base, q);
-            if (!q.overflow) {
-                float4 v[4][1];
-                gather_simplex_f<1>(tabf, q.key, v);
-#pragma unroll
-                for (int l = 0; l < 4; ++l) {
-                    const float b = q.bary[l];
-                    o[0] = fmaf(b, v[l][0].x, o[0]);
-                    o[1] = fmaf(b, v[l][0].y, o[1]);
-                    o[2] = fmaf(b, v[l][0].z, o[2]);
-                    o[3] = fmaf(b, v[l][0].w, o[3]);
-                }
+            for (int l = 0; l < 4; ++l) {
+                const float b = q.bary[l];
+                o[0] = fmaf(b, v[l][0].x, o[0]);
+                o[1] = fmaf(b, v[l][0].y, o[1]);
+                o[2] = fmaf(b, v[l][0].z, o[2]);
+                o[3] = fmaf(b, v[l][0].w, o[3]);
             }
         }
         const float m0 = fmaxf(o[0], 0.0f);
@@ -477,16 +461,326 @@ k_rigid_pass_f32(const float *__restrict__ ref, long long m, RigidK kv, const Ri
 
 constexpr size_t kF32Smem = (size_t)kP2PtBase * kPassThreads * sizeof(double);
 
+// ---------------------------------------------------------------------------
+// dense-grid point path (FR_PASS_F32 when the lattice has a dense grid; the
+// EM hot loop of SURVEY.md 8(a)).  Same float32 geometry as k_rigid_pass_f32,
+// restructured for issue throughput (the kernel is instruction-bound, not
+// HBM-bound, at 12 B per point):
+//   * rounding by the 1.5 * 2^23 magic constant (FFMA + FADD, no XU ops);
+//     the integer cell comes from the float's bits;
+//   * no per-point rank wrap: the six pairwise comparison bits and h (the
+//     sum of the rounded coordinates, |h| <= 2) index a 320-entry table of the
+//     four vertex slot offsets with the wrap and the rotation of the
+//     barycentrics by h folded in (the cyclic gaps of the sorted residuals
+//     are wrap-invariant, permutohedral.py:198-212);
+//   * barycentrics from a 5-comparator sorting network;
+//   * float32 pairs (FFMA2) for the transform, the slice and the moments.
+struct GridK {
+    float2 Rc[3];           // (R0k, R1k): rows 0-1 of column k
+    float2 R2[3];           // (R2k, 0)
+    float2 A01[3], A23[3];  // (A0k, A1k), (A2k, A3k)
+    float2 f01, f23;        // fractional pose constants (e0 - 4 base)
+    float2 cw01, cw2;       // (cw0, cw1), (cw2, 0)
+    float cref[3];
+    float cp;
+    int C[3];               // ri - (a - 1) = bits(t) + C
+    unsigned lim[3];        // span + 2
+    int s0, s1;
+    unsigned K;             // cell of ri = bits0 * s0 + bits1 * s1 + bits2 + K
+    unsigned H;             // h = sum bits + H
+};
+
+constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
+constexpr int kGridTab = 64 * 5;
+constexpr int kGridFold = 32;
+constexpr int kGridStages = 4;
+
+__device__ __forceinline__ void cp_async4(float *smem, const float *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// stage one point's three coordinates (the thread's own slot)
+__device__ __forceinline__ void ring_issue(float (*slot)[kPassThreads], const float *ref,
+                                           long long m, long long q, long long end) {
+    if (q < end) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async4(&slot[c][threadIdx.x], ref + c * m + q);
+    }
+    cp_async_commit();
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// table entry e = code * 5 + (h + 2): pre-wrap ranks from the comparison bits
+// (pair order (0,1) (0,2) (0,3) (1,2) (1,3) (2,3); bit set: d[j] > d[i]; the
+// earlier index wins ties, as the stable argsort of permutohedral.py:193-197),
+// the +-4 wrap (:198-203), vertex l's cell ri_final - [rank_final >= 4 - l]
+// (:214), and pre-wrap barycentric k -> vertex (k - h) mod 4
+__device__ __forceinline__ int4 grid_entry(int e, int s0, int s1) {
+    const int code = e / 5, h = e % 5 - 2;
+    int rank[4] = {0, 0, 0, 0};
+    int p = 0;
+    for (int i = 0; i < 4; ++i)
+        for (int j = i + 1; j < 4; ++j, ++p) {
+            if ((code >> p) & 1) ++rank[i];
+            else ++rank[j];
+        }
+    int rf[4], dri[4];
+    for (int i = 0; i < 4; ++i) {
+        const int rk = rank[i] + h;
+        const int adj = rk < 0 ? -1 : (rk > 3 ? 1 : 0);
+        rf[i] = rk - 4 * adj;
+        dri[i] = -adj;
+    }
+    const int st[3] = {s0, s1, 1};
+    int off[4];
+    for (int l = 0; l < 4; ++l) {
+        int c = 0;
+        for (int i = 0; i < 3; ++i) c += (dri[i] - (rf[i] >= 4 - l ? 1 : 0)) * st[i];
+        off[l] = 4 * c + l;
+    }
+    int rot[4];
+    for (int k = 0; k < 4; ++k) {
+        const int l = (k - h + 8) & 3;
+        rot[k] = l == 0 ? off[0] : (l == 1 ? off[1] : (l == 2 ? off[2] : off[3]));
+    }
+    return make_int4(rot[0], rot[1], rot[2], rot[3]);
+}
+
+__device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
+
+// float32 pair accumulators -> the 25 float64 columns (layout of _rigid.py)
+struct GridAcc {
+    float2 s1_01, s1_2_s0, s2_00_01, s2_02_12, rx01[3], rx2_r1[3], q01;
+    float s2_11, s2_22, q2;
+    __device__ __forceinline__ void zero() {
+        s1_01 = s1_2_s0 = s2_00_01 = s2_02_12 = q01 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) rx01[j] = rx2_r1[j] = make_float2(0.f, 0.f);
+        s2_11 = s2_22 = q2 = 0.f;
+    }
+    __device__ __forceinline__ float col(int c) const {
+        switch (c) {
+            case 0: return s1_2_s0.y;
+            case 1: return s1_01.x;
+            case 2: return s1_01.y;
+            case 3: return s1_2_s0.x;
+            case 4: return s2_00_01.x;
+            case 5: return s2_00_01.y;
+            case 6: return s2_02_12.x;
+            case 7: return s2_11;
+            case 8: return s2_02_12.y;
+            case 9: return s2_22;
+            case 22: return q01.x;
+            case 23: return q01.y;
+            case 24: return q2;
+            default: break;
+        }
+        if (c < 13) return rx2_r1[c - 10].y;
+        const int j = (c - 13) / 3, k = (c - 13) % 3;
+        return k == 0 ? rx01[j].x : (k == 1 ? rx01[j].y : rx2_r1[j].x);
+    }
+};
+
+template <bool DEV>
+__global__ void __launch_bounds__(kPassThreads, 3)
+k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
+                  const int *done, DenseSliceF dg, double *__restrict__ partials) {
+    constexpr int NA = kP2PtBase;
+    __shared__ GridK g;
+    __shared__ int4 tab[kGridTab];
+    __shared__ float ring[kGridStages][3][kPassThreads];
+    if (DEV && *done) return;
+    if (threadIdx.x == 0) {
+        const RigidK &k = DEV ? *kd : kv;
+        for (int c = 0; c < 3; ++c) {
+            g.Rc[c] = make_float2((float)k.R[c], (float)k.R[3 + c]);
+            g.R2[c] = make_float2((float)k.R[6 + c], 0.0f);
+            g.A01[c] = make_float2((float)k.A[0][c], (float)k.A[1][c]);
+            g.A23[c] = make_float2((float)k.A[2][c], (float)k.A[3][c]);
+            g.cref[c] = (float)k.c_ref[c];
+        }
+        int base[4];
+        float fr0[4];
+        for (int i = 0; i < 4; ++i) {
+            const double b = rint(k.e0[i] * 0.25);
+            base[i] = (int)b;
+            fr0[i] = (float)(k.e0[i] - 4.0 * b);
+        }
+        g.f01 = make_float2(fr0[0], fr0[1]);
+        g.f23 = make_float2(fr0[2], fr0[3]);
+        g.cw01 = make_float2((float)k.c_world[0], (float)k.c_world[1]);
+        g.cw2 = make_float2((float)k.c_world[2], 0.0f);
+        g.cp = (float)k.cp;
+        const int st[3] = {dg.s0, dg.s1, 1};
+        unsigned K = 0, H = 0;
+        for (int i = 0; i < 4; ++i) H += (unsigned)(base[i] - kMagicBits);
+        for (int i = 0; i < 3; ++i) {
+            g.C[i] = base[i] - kMagicBits - (dg.a[i] - 1);
+            g.lim[i] = dg.span[i] + 2u;
+            K += (unsigned)(base[i] - kMagicBits - (dg.a[i] - kDensePad)) * (unsigned)st[i];
+        }
+        g.s0 = dg.s0;
+        g.s1 = dg.s1;
+        g.K = K;
+        g.H = H;
+    }
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, dg.s0, dg.s1);
+    extern __shared__ double sacc[];   // [NA][kPassThreads]
+#pragma unroll
+    for (int q = 0; q < NA; ++q) sacc[q * kPassThreads + threadIdx.x] = 0.0;
+    __syncthreads();
+    GridAcc a;
+    a.zero();
+    int fold = 0;
+    // contiguous chunk per block (Morton-sorted points: the block's gathers
+    // stay in a compact region of the grid, so they hit L1), streamed through
+    // a kGridStages-deep cp.async ring; each thread reads back only its own
+    // slots, so the ring needs no block barrier
+    const long long chunk = ((m + gridDim.x - 1) / gridDim.x + 31) & ~31ll;
+    const long long beg = (long long)blockIdx.x * chunk;
+    const long long end = min(beg + chunk, m);
+#pragma unroll
+    for (int st = 0; st < kGridStages - 1; ++st)
+        ring_issue(ring[st], ref, m, beg + (long long)st * kPassThreads + threadIdx.x, end);
+    int stage = 0;
+    for (long long base = beg; base < end; base += kPassThreads) {
+        ring_issue(ring[stage == 0 ? kGridStages - 1 : stage - 1], ref, m,
+                   base + (long long)(kGridStages - 1) * kPassThreads + threadIdx.x, end);
+        cp_async_wait<kGridStages - 1>();
+        const long long p = base + threadIdx.x;
+        const float nx = ring[stage][0][threadIdx.x];
+        const float ny = ring[stage][1][threadIdx.x];
+        const float nz = ring[stage][2][threadIdx.x];
+        stage = stage + 1 == kGridStages ? 0 : stage + 1;
+        if (p >= end) continue;
+        const float x0 = nx - g.cref[0], x1 = ny - g.cref[1], x2 = nz - g.cref[2];
+        // y = R xh as (y0, y1) and (y2, 1)
+        float2 y01 = __fmul2_rn(g.Rc[0], bc(x0));
+        y01 = __ffma2_rn(g.Rc[1], bc(x1), y01);
+        y01 = __ffma2_rn(g.Rc[2], bc(x2), y01);
+        float2 y2v = __ffma2_rn(g.R2[0], bc(x0), make_float2(0.0f, 1.0f));
+        y2v = __ffma2_rn(g.R2[1], bc(x1), y2v);
+        y2v = __ffma2_rn(g.R2[2], bc(x2), y2v);
+        // elevated coordinates minus 4 * base
+        float2 e01 = __ffma2_rn(g.A01[0], bc(y01.x), g.f01);
+        e01 = __ffma2_rn(g.A01[1], bc(y01.y), e01);
+        e01 = __ffma2_rn(g.A01[2], bc(y2v.x), e01);
+        float2 e23 = __ffma2_rn(g.A23[0], bc(y01.x), g.f23);
+        e23 = __ffma2_rn(g.A23[1], bc(y01.y), e23);
+        e23 = __ffma2_rn(g.A23[2], bc(y2v.x), e23);
+        const float el[4] = {e01.x, e01.y, e23.x, e23.y};
+        float d[4];
+        int tb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float t = fmaf(el[i], 0.25f, kMagic);   // rint(el / 4) + magic
+            tb[i] = __float_as_int(t);
+            d[i] = fmaf(-4.0f, t - kMagic, el[i]);
+        }
+        unsigned code = 0;
+        {
+            int q = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = i + 1; j < 4; ++j, ++q) code |= (d[j] > d[i] ? 1u : 0u) << q;
+        }
+        // descending sorting network -> pre-wrap barycentrics
+        float s0 = fmaxf(d[0], d[1]), s1 = fminf(d[0], d[1]);
+        float s2 = fmaxf(d[2], d[3]), s3 = fminf(d[2], d[3]);
+        {
+            const float hi = fmaxf(s0, s2), lo = fminf(s0, s2);
+            s0 = hi;
+            s2 = lo;
+            const float hi2 = fmaxf(s1, s3), lo2 = fminf(s1, s3);
+            s1 = hi2;
+            s3 = lo2;
+            const float hi3 = fmaxf(s1, s2), lo3 = fminf(s1, s2);
+            s1 = hi3;
+            s2 = lo3;
+        }
+        const float b0 = fmaf(0.25f, s3 - s0, 1.0f);
+        const float b1 = 0.25f * (s2 - s3);
+        const float b2 = 0.25f * (s1 - s2);
+        const float b3 = 0.25f * (s0 - s1);
+        const int h = (int)((unsigned)tb[0] + (unsigned)tb[1] + (unsigned)tb[2] + (unsigned)tb[3] + g.H);
+        const int hi = min(max(h + 2, 0), 4);
+        const int4 T = tab[code * 5 + hi];
+        const bool in = ((unsigned)(tb[0] + g.C[0]) <= g.lim[0]) &
+                        ((unsigned)(tb[1] + g.C[1]) <= g.lim[1]) &
+                        ((unsigned)(tb[2] + g.C[2]) <= g.lim[2]);
+        float2 o01 = make_float2(0.f, 0.f), o23 = make_float2(0.f, 0.f);
+        if (in) {
+            const unsigned c4 = 4u * ((unsigned)tb[0] * (unsigned)g.s0 +
+                                      (unsigned)tb[1] * (unsigned)g.s1 + (unsigned)tb[2] + g.K);
+            const float4 v0 = __ldg(dg.cells + (int)(c4 + (unsigned)T.x));
+            const float4 v1 = __ldg(dg.cells + (int)(c4 + (unsigned)T.y));
+            const float4 v2 = __ldg(dg.cells + (int)(c4 + (unsigned)T.z));
+            const float4 v3 = __ldg(dg.cells + (int)(c4 + (unsigned)T.w));
+            o01 = __fmul2_rn(bc(b0), make_float2(v0.x, v0.y));
+            o23 = __fmul2_rn(bc(b0), make_float2(v0.z, v0.w));
+            o01 = __ffma2_rn(bc(b1), make_float2(v1.x, v1.y), o01);
+            o23 = __ffma2_rn(bc(b1), make_float2(v1.z, v1.w), o23);
+            o01 = __ffma2_rn(bc(b2), make_float2(v2.x, v2.y), o01);
+            o23 = __ffma2_rn(bc(b2), make_float2(v2.z, v2.w), o23);
+            o01 = __ffma2_rn(bc(b3), make_float2(v3.x, v3.y), o01);
+            o23 = __ffma2_rn(bc(b3), make_float2(v3.z, v3.w), o23);
+        }
+        // o01 = (sum y0, sum y1), o23 = (sum y2, mass)
+        const float m0 = fmaxf(o23.y, 0.0f);
+        const bool sup = m0 >= 1e-12f;
+        const float w = sup ? (g.cp > 0.0f ? m0 * rcp_approx(m0 + g.cp) : 1.0f) : 0.0f;
+        const float ninv = sup ? -rcp_approx(m0) : 0.0f;
+        // residual r = x - t (centred); w = 0 zeroes every term of an
+        // unsupported point, whatever r holds
+        const float2 r01 = __fadd2_rn(y01, __ffma2_rn(o01, bc(ninv), g.cw01));
+        const float r2 = y2v.x + fmaf(o23.x, ninv, g.cw2.x);
+        const float2 wy01 = __fmul2_rn(bc(w), y01);
+        const float2 wy2v = __fmul2_rn(bc(w), y2v);          // (w y2, w)
+        const float2 wr01 = __fmul2_rn(bc(w), r01);
+        const float wr2 = w * r2;
+        a.s1_01 = __fadd2_rn(a.s1_01, wy01);
+        a.s1_2_s0 = __fadd2_rn(a.s1_2_s0, wy2v);
+        a.s2_00_01 = __ffma2_rn(bc(wy01.x), y01, a.s2_00_01);
+        a.s2_02_12 = __ffma2_rn(bc(y2v.x), wy01, a.s2_02_12);
+        a.s2_11 = fmaf(wy01.y, y01.y, a.s2_11);
+        a.s2_22 = fmaf(wy2v.x, y2v.x, a.s2_22);
+        a.rx01[0] = __ffma2_rn(bc(wr01.x), y01, a.rx01[0]);
+        a.rx2_r1[0] = __ffma2_rn(bc(wr01.x), y2v, a.rx2_r1[0]);
+        a.rx01[1] = __ffma2_rn(bc(wr01.y), y01, a.rx01[1]);
+        a.rx2_r1[1] = __ffma2_rn(bc(wr01.y), y2v, a.rx2_r1[1]);
+        a.rx01[2] = __ffma2_rn(bc(wr2), y01, a.rx01[2]);
+        a.rx2_r1[2] = __ffma2_rn(bc(wr2), y2v, a.rx2_r1[2]);
+        a.q01 = __ffma2_rn(wr01, r01, a.q01);
+        a.q2 = fmaf(wr2, r2, a.q2);
+        if (++fold == kGridFold) {
+#pragma unroll
+            for (int c = 0; c < NA; ++c) sacc[c * kPassThreads + threadIdx.x] += (double)a.col(c);
+            a.zero();
+            fold = 0;
+        }
+    }
+    double acc[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) acc[c] = sacc[c * kPassThreads + threadIdx.x] + (double)a.col(c);
+    block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
+}
+
 static int set_f32_smem() {
     static bool done = false;
     if (!done) {
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true, true>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false, true>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true, false>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false, false>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
         done = true;
     }
@@ -1000,12 +1294,18 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         FR_TRY(set_f32_smem());
         const SliceTableF tf = lat->table_f();
         const DenseSliceF dg = lat->dense;
-        const bool dense = lat->dcells != nullptr;
-#define FR_F32(DEV, DENSE) \
-    k_rigid_pass_f32<DEV, DENSE><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, tf, dg, scratch)
-        if (dev) { if (dense) FR_F32(true, true); else FR_F32(true, false); }
-        else { if (dense) FR_F32(false, true); else FR_F32(false, false); }
-#undef FR_F32
+        if (lat->dcells != nullptr) {
+            const int g3 = pass_grid_dense();
+            if (dev) k_rigid_pass_grid<true><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, dg, scratch);
+            else k_rigid_pass_grid<false><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, dg, scratch);
+            FR_CHECK_LAUNCH();
+            k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g3, kP2PtBase, sums, done);
+            FR_CHECK_LAUNCH();
+            return FR_OK;
+        } else {
+            if (dev) k_rigid_pass_f32<true><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, tf, scratch);
+            else k_rigid_pass_f32<false><<<grid, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, tf, scratch);
+        }
         FR_CHECK_LAUNCH();
         k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, grid, kP2PtBase, sums, done);
         FR_CHECK_LAUNCH();
@@ -1059,7 +1359,7 @@ int fr_rigid_pass_width(int mode, int with_sigma) { return width(mode, with_sigm
 
 int fr_rigid_scratch_doubles(int mode, int with_sigma, int64_t m) {
     (void)m;
-    return pass_grid() * std::max(std::max(width(mode, with_sigma), kMaxCand), 28);
+    return pass_grid_max() * std::max(std::max(width(mode, with_sigma), kMaxCand), 28);
 }
 
 int fr_rigid_pass(const fr_lattice *lat, const float *ref, int64_t m,
@@ -1272,7 +1572,7 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
     h.max_gn_iters = cfg->max_gn_iters;
     h.max_halvings = cfg->max_halvings;
     make_rigid_k(h.A, h.R, h.t, h.c_ref, h.cp, h.gain, -1, -1, &h.k);
-    const int grid = pass_grid();
+    const int grid = pass_grid_max();
     if (cudaMalloc(&em->d_em, sizeof(EmDev)) != cudaSuccess ||
         cudaMalloc(&em->d_sums, 32 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&em->d_scratch, (size_t)grid * 32 * sizeof(double)) != cudaSuccess ||

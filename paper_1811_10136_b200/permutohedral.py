@@ -215,6 +215,13 @@ class PermutohedralLattice:
         return max(self._info()[1], 1)
 
     @property
+    def dense_cells(self) -> int:
+        """Cells of the dense float32 slice grid (0: the EM pass hashes)."""
+        c = ctypes.c_int64()
+        _lib.check(self._lib.fr_lattice_dense_cells(self._h, ctypes.byref(c)))
+        return int(c.value)
+
+    @property
     def num_sites(self) -> int:
         return self._info()[0]
 

@@ -208,3 +208,40 @@ def test_degenerate_termination(fr):
                       fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.005, outlier_ratio=0.1)))
     assert res.termination == "degenerate" and res.iterations == 1
     assert np.isnan(res.objectives[0]) and np.isnan(res.twist_norms[0])
+
+
+@pytest.mark.parametrize("dense", [True, False])
+def test_float32_pass_matches_exact(fr, dense, monkeypatch):
+    """The float32 point paths (dense slice grid / hash slots) give the exact
+    float64 pass's 25 sufficient statistics to float32 accuracy, including
+    points far outside the lattice box (no site among their vertices) and a
+    pose that moves part of the cloud across the box boundary."""
+    import paper_1811_10136_b200._rigid as rg
+    if not dense:
+        monkeypatch.setenv("FR_DENSE_MAX_CELLS", "0")
+    model, obs, _ = O.pebble_pair(30000, outlier_ratio=0.05, seed=11)
+    X = model.astype(np.float32).astype(float)
+    Y = obs.astype(np.float32).astype(float)
+    far = np.random.default_rng(3).uniform(-5.0, 5.0, (2000, 3))   # well outside the cloud
+    X = np.vstack([X, far])
+    sigma = 0.05 * O.bbox_diameter(X[:30000])
+    gmm = fr.GmmConfig(sigma=sigma, outlier_ratio=0.1)
+    path = rg.RigidDevicePath(fr.PointCloud(X), fr.PointCloud(Y), gmm, "point_to_point")
+    assert (path.lattice.dense_cells > 0) == dense
+    L = float(np.sqrt(((X[:30000] - X[:30000].mean(axis=0)) ** 2).sum(axis=1).mean()))
+    # length dimension of each of the 25 columns (layout of _rigid.py)
+    k = np.array([0, 1, 1, 1, 2, 2, 2, 2, 2, 2, 1, 1, 1] + [2] * 9 + [2, 2, 2])
+    c = X[:30000].mean(axis=0)
+    Rb = O.rotation_about_axis([1.0, 1.0, 0.0], 2.5)          # about the cloud centre,
+    tb = c - Rb @ c + np.array([0.6, 0.0, 0.3]) * L           # half the cloud leaves the box
+    for R, t in [(np.eye(3), np.zeros(3)),
+                 (O.rotation_about_axis([0.3, -1.0, 0.5], 0.4), np.array([0.03, -0.05, 0.02])),
+                 (Rb, tb)]:
+        monkeypatch.setattr(rg, "FAST_QUERY", False)
+        monkeypatch.setattr(rg, "F32_POINTS", False)
+        ex = path.run_pass(R, t).copy()
+        monkeypatch.setattr(rg, "FAST_QUERY", True)
+        monkeypatch.setattr(rg, "F32_POINTS", True)
+        f32 = path.run_pass(R, t).copy()
+        assert ex[0] > 50.0
+        np.testing.assert_array_less(np.abs(f32 - ex) / (ex[0] * L ** k), 1e-5)
