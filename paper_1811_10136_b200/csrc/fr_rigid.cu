@@ -18,6 +18,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -1069,13 +1070,16 @@ __device__ void polar3(const double *M, double *R) {
         C[7] = X[2] * X[3] - X[0] * X[5];
         C[8] = X[0] * X[4] - X[1] * X[3];
         const double det = X[0] * C[0] + X[1] * C[1] + X[2] * C[2];
+        const double inv = 1.0 / det;
         double diff = 0.0;
         for (int q = 0; q < 9; ++q) {
-            const double xn = 0.5 * (X[q] + C[q] / det);
+            const double xn = 0.5 * (X[q] + C[q] * inv);
             diff = fmax(diff, fabs(xn - X[q]));
             X[q] = xn;
         }
-        if (diff <= 1e-16) break;
+        // quadratic convergence: once a step is at round-off level (a few ulp
+        // of the unit-scale entries) the next one only reshuffles last bits
+        if (diff <= 1e-15) break;
     }
     for (int q = 0; q < 9; ++q) R[q] = X[q];
 }
@@ -1177,9 +1181,8 @@ __device__ bool gn_solve_dev(const double (*H)[6], const double *g, bool use_dam
     return false;
 }
 
-__global__ void k_rigid_solve(const double *sums, EmDev *e, double *objs, double *tnorms,
-                              double *masses) {
-    if (threadIdx.x != 0 || e->done) return;
+__device__ void rigid_solve_body(const double *sums, EmDev *e, double *objs, double *tnorms,
+                                 double *masses) {
     const int it = e->iterations;
     e->iterations = it + 1;
     const double mass = sums[0];
@@ -1261,6 +1264,26 @@ __global__ void k_rigid_solve(const double *sums, EmDev *e, double *objs, double
     }
 }
 
+// EmDev staged through shared memory: the serial float64 solve touches the
+// state hundreds of times, so it works on an on-chip copy
+__device__ __forceinline__ void em_copy(EmDev *dst, const EmDev *src, int lane, int nlanes) {
+    static_assert(sizeof(EmDev) % 8 == 0, "EmDev is copied as 8-byte words");
+    const unsigned long long *a = reinterpret_cast<const unsigned long long *>(src);
+    unsigned long long *b = reinterpret_cast<unsigned long long *>(dst);
+    for (int w = lane; w < (int)(sizeof(EmDev) / 8); w += nlanes) b[w] = a[w];
+}
+
+__global__ void k_rigid_solve(const double *sums, EmDev *e, double *objs, double *tnorms,
+                              double *masses) {
+    __shared__ EmDev se;
+    if (e->done) return;
+    em_copy(&se, e, threadIdx.x, blockDim.x);
+    __syncthreads();
+    if (threadIdx.x == 0) rigid_solve_body(sums, &se, objs, tnorms, masses);
+    __syncthreads();
+    em_copy(e, &se, threadIdx.x, blockDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // host
 
@@ -1296,8 +1319,12 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         const DenseSliceF dg = lat->dense;
         if (lat->dcells != nullptr) {
             const int g3 = pass_grid_dense();
-            if (dev) k_rigid_pass_grid<true><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, dg, scratch);
-            else k_rigid_pass_grid<false><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, dg, scratch);
+            if (dev)
+                k_rigid_pass_grid<true><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
+                                                                           dg, scratch);
+            else
+                k_rigid_pass_grid<false><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
+                                                                            dg, scratch);
             FR_CHECK_LAUNCH();
             k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g3, kP2PtBase, sums, done);
             FR_CHECK_LAUNCH();
@@ -1577,6 +1604,7 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
         cudaMalloc(&em->d_sums, 32 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&em->d_scratch, (size_t)grid * 32 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double)) != cudaSuccess ||
+
         cudaMemcpy(em->d_em, &h, sizeof(EmDev), cudaMemcpyHostToDevice) != cudaSuccess) {
         fr_rigid_em_destroy(em);
         set_error("device EM allocation failed");
@@ -1623,6 +1651,11 @@ static int em_solve(fr_rigid_em *em, cudaStream_t s) {
     return FR_OK;
 }
 
+static int em_iteration(fr_rigid_em *em, cudaStream_t s) {
+    FR_TRY(em_pass(em, s));
+    return em_solve(em, s);
+}
+
 int fr_rigid_em_pass(fr_rigid_em *em, void *stream) {
     if (!em) {
         set_error("null EM object");
@@ -1654,8 +1687,7 @@ int fr_rigid_em_enqueue(fr_rigid_em *em, int n, void *stream) {
         cudaGraph_t g;
         FR_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         for (int i = 0; i < kGraphIters; ++i) {
-            int st = em_pass(em, cs);
-            if (st == FR_OK) st = em_solve(em, cs);
+            int st = em_iteration(em, cs);
             if (st != FR_OK) {
                 cudaStreamEndCapture(cs, &g);
                 cudaStreamDestroy(cs);
@@ -1673,10 +1705,7 @@ int fr_rigid_em_enqueue(fr_rigid_em *em, int n, void *stream) {
         FR_CUDA(cudaGraphLaunch(em->graph, s));
         left -= em->graph_iters;
     }
-    for (; left > 0; --left) {
-        FR_TRY(em_pass(em, s));
-        FR_TRY(em_solve(em, s));
-    }
+    for (; left > 0; --left) FR_TRY(em_iteration(em, s));
     return FR_OK;
 }
 

@@ -245,3 +245,4 @@ def test_float32_pass_matches_exact(fr, dense, monkeypatch):
         f32 = path.run_pass(R, t).copy()
         assert ex[0] > 50.0
         np.testing.assert_array_less(np.abs(f32 - ex) / (ex[0] * L ** k), 1e-5)
+
