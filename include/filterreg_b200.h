@@ -80,6 +80,14 @@ int fr_lattice_splat(fr_lattice *lat, const double *d_features, const double *d_
 int fr_lattice_splat_points(fr_lattice *lat, const float *d_pos, const float *d_normals,
                             int64_t n, int value_mode, void *stream);
 
+/* (n, 3) float64 host rows (pageable) -> (3, n) float32 device planes, the
+ * boundary conversion of PointCloud.positions / normals (geometry.py:109-139,
+ * "convert once to fp32 SoA device tensors").  Rounds to
+ * nearest like numpy.astype(float32).  Host helper: worker threads convert
+ * sub-chunks into pinned staging slots and enqueue the copies on `stream`; the
+ * host rows may be reused once the call returns. */
+int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa, void *stream);
+
 /* PermutohedralLattice.blur() (permutohedral.py:291-327), incl. frontier growth
  * with the reference's site cap and the final drop of all-zero rows. */
 int fr_lattice_blur(fr_lattice *lat, void *stream);

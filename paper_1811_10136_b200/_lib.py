@@ -30,7 +30,7 @@ EXPORTED = (
     "fr_rigid_em_solve", "fr_rigid_em_enqueue", "fr_rigid_em_run", "fr_rigid_em_status",
     "fr_rigid_em_result", "fr_sort_points_morton", "fr_body_params_doubles", "fr_body_pass",
     "fr_body_objective", "fr_graph_pass", "fr_graph_blocks", "fr_graph_objective",
-    "fr_point_rows",
+    "fr_point_rows", "fr_upload_points",
 )
 
 
@@ -76,6 +76,7 @@ _SIGS = {
     "fr_lattice_blur": ([_P, _P], _I),
     "fr_lattice_info": ([_P, ctypes.POINTER(_L), ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "fr_lattice_dense_cells": ([_P, ctypes.POINTER(_L)], _I),
+    "fr_upload_points": ([_P, _L, _P, _P], _I),
     "fr_lattice_export": ([_P, _P, _P, _P], _I),
     "fr_lattice_slice": ([_P, _P, _L, _P, _P], _I),
     "fr_simplex": ([_I, _DP, _P, _L, _P, _P, _P], _I),

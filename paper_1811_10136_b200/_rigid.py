@@ -140,16 +140,39 @@ class RigidMoments:
 
 
 def upload_soa(points, dev):
-    """(n, 3) host coordinates -> (3, n) float32 device planes.  The caller's
-    float64 array is copied as it is (no host-side conversion pass and no fresh
-    host allocation to fault in); the float32 rounding (numpy's astype
-    rounding: to nearest) and the transpose run on the device."""
+    """(n, 3) host coordinates -> (3, n) float32 device planes through the
+    native staged upload (fr_upload_points: threaded float32 conversion into
+    pinned slots, DMA on the current stream)."""
     import torch
-    host = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64))
-    aos = host.to(dev, non_blocking=False)
-    soa = torch.empty((3, aos.shape[0]), dtype=torch.float32, device=dev)
-    soa.copy_(aos.t())
+    P = np.ascontiguousarray(points, dtype=np.float64)
+    soa = torch.empty((3, P.shape[0]), dtype=torch.float32, device=dev)
+    _lib.check(_lib.load().fr_upload_points(P.ctypes.data_as(ctypes.c_void_p), P.shape[0],
+                                            _lib.ptr(soa), _lib.stream_handle()))
     return soa
+
+
+class _SetupClock:
+    """Per-phase wall times of the device-path setup when FR_PROFILE_SETUP=1
+    (synchronising between phases); a no-op otherwise."""
+
+    def __init__(self):
+        import os
+        self.on = os.environ.get("FR_PROFILE_SETUP") == "1"
+        self.phases = {}
+        if self.on:
+            import time
+            import torch
+            torch.cuda.synchronize()
+            self._t = time.perf_counter()
+
+    def __call__(self, name: str) -> None:
+        if self.on:
+            import time
+            import torch
+            torch.cuda.synchronize()
+            now = time.perf_counter()
+            self.phases[name] = now - self._t
+            self._t = now
 
 
 def unpack_upper6(v21) -> np.ndarray:
@@ -175,8 +198,10 @@ class RigidDevicePath:
             else _lib.FR_POINT_TO_POINT
         self.gmm = gmm
         self.group = process_group
+        lap = _SetupClock()
         self.ref = upload_soa(reference.positions, self.dev)
         self.M = self.ref.shape[1]
+        lap("upload_ref")
         # global quantities a shard must not compute locally:
         # total model count (outlier constant, degenerate test), the centre of
         # the whole reference cloud and its bounding-box diameter
@@ -187,13 +212,16 @@ class RigidDevicePath:
         lo = self._allreduce(self.ref.amin(dim=1).double().cpu().numpy(), "min")
         hi = self._allreduce(self.ref.amax(dim=1).double().cpu().numpy(), "max")
         self.diameter = float(np.linalg.norm(hi - lo))
+        lap("global_stats")
         if sort and SPATIAL_ORDER and self.M > 1:
             # Morton order of the model points: reduction sums are order-free up
             # to float64 round-off, and neighbouring threads share table lines
             _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self.ref), self.M, 3, None,
                                                       _lib.stream_handle()))
+        lap("morton_sort")
         self.obs = upload_soa(observation.positions, self.dev)
         self.N = self.obs.shape[1]
+        lap("upload_obs")
         self.obs_n = None
         if self.mode == _lib.FR_POINT_TO_PLANE:
             if observation.normals is None:
@@ -214,7 +242,10 @@ class RigidDevicePath:
             if self.mode == _lib.FR_POINT_TO_PLANE else None
         self.lattice = None
         self.sigma = None
+        lap("buffers")
         self.build(gmm.sigma)
+        lap("lattice_build")
+        self.setup_s = lap.phases
 
     def build(self, sigma) -> None:
         """(Re)build the observation lattice at kernel width sigma."""

@@ -543,4 +543,5 @@ struct fr_lattice {
     long long dense_cells = 0;
     // device counters / flags
     unsigned long long *d_counters = nullptr;   // [0] sites, [1] src count, [2] overflow
+    cudaStream_t stream = nullptr;              // stream of the last build call (pool ordering)
 };

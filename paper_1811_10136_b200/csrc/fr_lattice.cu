@@ -494,12 +494,23 @@ static int read_counters(fr_lattice *lat, cudaStream_t s, unsigned long long *h)
 
 static void free_slice(fr_lattice *lat);
 
+// every lattice buffer comes from the device's stream-ordered pool (release
+// threshold: never), on the stream of the call that builds the lattice: a
+// rebuild reuses mapped pages instead of cudaMalloc / cudaFree mapping and
+// unmapping ~100 MB-GB per build (seconds-long outliers at C5 sizes)
+static cudaError_t pool_alloc(fr_lattice *lat, void **p, size_t bytes) {
+    return cudaMallocAsync(p, std::max<size_t>(bytes, 1), lat->stream);
+}
+static void pool_free(fr_lattice *lat, void *p) {
+    if (p) cudaFreeAsync(p, lat->stream);
+}
+
 static void free_build(fr_lattice *lat) {
-    cudaFree(lat->site_keys);
-    cudaFree(lat->vals);
-    cudaFree(lat->vals_alt);
-    cudaFree(lat->hkeys);
-    cudaFree(lat->hsite);
+    pool_free(lat, lat->site_keys);
+    pool_free(lat, lat->vals);
+    pool_free(lat, lat->vals_alt);
+    pool_free(lat, lat->hkeys);
+    pool_free(lat, lat->hsite);
     lat->site_keys = nullptr;
     lat->vals = lat->vals_alt = nullptr;
     lat->hkeys = nullptr;
@@ -508,12 +519,12 @@ static void free_build(fr_lattice *lat) {
 }
 
 static int alloc_hash(fr_lattice *lat, unsigned cap, cudaStream_t s) {
-    cudaFree(lat->hkeys);
-    cudaFree(lat->hsite);
+    pool_free(lat, lat->hkeys);
+    pool_free(lat, lat->hsite);
     lat->hkeys = nullptr;
     lat->hsite = nullptr;
-    FR_CUDA(cudaMalloc(&lat->hkeys, (size_t)cap * sizeof(unsigned long long)));
-    FR_CUDA(cudaMalloc(&lat->hsite, (size_t)cap * sizeof(int)));
+    FR_CUDA(pool_alloc(lat, (void **)&lat->hkeys, (size_t)cap * sizeof(unsigned long long)));
+    FR_CUDA(pool_alloc(lat, (void **)&lat->hsite, (size_t)cap * sizeof(int)));
     FR_CUDA(cudaMemsetAsync(lat->hkeys, 0xff, (size_t)cap * sizeof(unsigned long long), s));
     FR_CUDA(cudaMemsetAsync(lat->hsite, 0xff, (size_t)cap * sizeof(int), s));
     lat->hmask = cap - 1;
@@ -540,9 +551,9 @@ static int reserve_sites(fr_lattice *lat, long long need, cudaStream_t s) {
     const int D1 = lat->dim + 1, nv = lat->nv;
     int *nk = nullptr;
     double *nvals = nullptr, *nalt = nullptr;
-    FR_CUDA(cudaMalloc(&nk, (size_t)cap * D1 * sizeof(int)));
-    FR_CUDA(cudaMalloc(&nvals, (size_t)cap * nv * sizeof(double)));
-    FR_CUDA(cudaMalloc(&nalt, (size_t)cap * nv * sizeof(double)));
+    FR_CUDA(pool_alloc(lat, (void **)&nk, (size_t)cap * D1 * sizeof(int)));
+    FR_CUDA(pool_alloc(lat, (void **)&nvals, (size_t)cap * nv * sizeof(double)));
+    FR_CUDA(pool_alloc(lat, (void **)&nalt, (size_t)cap * nv * sizeof(double)));
     if (lat->n_sites > 0) {
         FR_CUDA(cudaMemcpyAsync(nk, lat->site_keys, (size_t)lat->n_sites * D1 * sizeof(int),
                                 cudaMemcpyDeviceToDevice, s));
@@ -550,9 +561,9 @@ static int reserve_sites(fr_lattice *lat, long long need, cudaStream_t s) {
                                 cudaMemcpyDeviceToDevice, s));
     }
     FR_CUDA(cudaStreamSynchronize(s));
-    cudaFree(lat->site_keys);
-    cudaFree(lat->vals);
-    cudaFree(lat->vals_alt);
+    pool_free(lat, lat->site_keys);
+    pool_free(lat, lat->vals);
+    pool_free(lat, lat->vals_alt);
     lat->site_keys = nk;
     lat->vals = nvals;
     lat->vals_alt = nalt;
@@ -681,7 +692,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
             FR_CHECK_LAUNCH();
         }
         FR_CUDA(cudaStreamSynchronize(s));
-        cudaFree(old_keys);
+        pool_free(lat, old_keys);
         lat->n_sites = S;
     }
     FR_TRY(rehash_sites<D>(lat, next_pow2(2ull * (unsigned long long)lat->n_sites), s));
@@ -733,10 +744,10 @@ static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
 }
 
 static void free_slice(fr_lattice *lat) {
-    cudaFree(lat->skeys);
-    cudaFree(lat->svals);
-    cudaFree(lat->fslots);
-    cudaFree(lat->dcells);
+    pool_free(lat, lat->skeys);
+    pool_free(lat, lat->svals);
+    pool_free(lat, lat->fslots);
+    pool_free(lat, lat->dcells);
     lat->skeys = nullptr;
     lat->svals = nullptr;
     lat->fslots = nullptr;
@@ -821,7 +832,7 @@ static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
     }
     t.s1 = (int)n[2];
     t.s0 = (int)(n[1] * n[2]);
-    FR_CUDA(cudaMalloc(&lat->dcells, (size_t)cells * 4 * sizeof(float4)));
+    FR_CUDA(pool_alloc(lat, (void **)&lat->dcells, (size_t)cells * 4 * sizeof(float4)));
     FR_CUDA(cudaMemsetAsync(lat->dcells, 0, (size_t)cells * 4 * sizeof(float4), s));
     k_dense_fill<<<grid_for(lat->n_sites), 256, 0, s>>>(lat->n_sites, lat->site_keys, lat->vals,
                                                         lat->nv, lat->c.gain, t, lat->dcells);
@@ -865,8 +876,8 @@ static int build_slice_table(fr_lattice *lat, cudaStream_t s) {
     int bits = 0;
     while ((1u << bits) < cap) ++bits;
     lat->nvp = nvp_for(lat->nv);
-    FR_CUDA(cudaMalloc(&lat->skeys, (size_t)cap * sizeof(unsigned long long)));
-    FR_CUDA(cudaMalloc(&lat->svals, (size_t)cap * lat->nvp * sizeof(double)));
+    FR_CUDA(pool_alloc(lat, (void **)&lat->skeys, (size_t)cap * sizeof(unsigned long long)));
+    FR_CUDA(pool_alloc(lat, (void **)&lat->svals, (size_t)cap * lat->nvp * sizeof(double)));
     FR_CUDA(cudaMemsetAsync(lat->skeys, 0xff, (size_t)cap * sizeof(unsigned long long), s));
     FR_CUDA(cudaMemsetAsync(lat->svals, 0, (size_t)cap * lat->nvp * sizeof(double), s));
     lat->smask = cap - 1;
@@ -881,7 +892,7 @@ static int build_slice_table(fr_lattice *lat, cudaStream_t s) {
     if (lat->nv <= 8) {
         lat->nf4 = lat->nv <= 4 ? 1 : 2;
         const int stride4 = lat->nf4 == 1 ? 2 : 4;
-        FR_CUDA(cudaMalloc(&lat->fslots, (size_t)cap * stride4 * sizeof(float4)));
+        FR_CUDA(pool_alloc(lat, (void **)&lat->fslots, (size_t)cap * stride4 * sizeof(float4)));
         FR_CUDA(cudaMemsetAsync(lat->fslots, 0xff, (size_t)cap * stride4 * sizeof(float4), s));
         lat->fmask = cap - 1;
         lat->fshift32 = 32 - bits;
@@ -953,8 +964,8 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
         }
     }
     FR_TRY(compact_nonzero<D>(lat, s));
-    cudaFree(lat->hkeys);
-    cudaFree(lat->hsite);
+    pool_free(lat, lat->hkeys);
+    pool_free(lat, lat->hsite);
     lat->hkeys = nullptr;
     lat->hsite = nullptr;
     lat->hmask = 0;
@@ -1106,9 +1117,10 @@ int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
     fr_lattice *lat = new fr_lattice();
     lat->c = c;
     lat->dim = dim;
-    if (cudaMalloc(&lat->d_counters, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    if (pool_alloc(lat, (void **)&lat->d_counters, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaStreamSynchronize(lat->stream) != cudaSuccess) {
         delete lat;
-        set_error("cudaMalloc failed for lattice counters");
+        set_error("device allocation failed for lattice counters");
         return FR_ECUDA;
     }
     *out = lat;
@@ -1117,9 +1129,12 @@ int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
 
 int fr_lattice_destroy(fr_lattice *lat) {
     if (!lat) return FR_OK;
+    // a blurred lattice may have been sliced from any stream: finish all work
+    // before its buffers return to the pool (cudaFree's implicit guarantee)
+    cudaDeviceSynchronize();
     free_build(lat);
     free_slice(lat);
-    cudaFree(lat->d_counters);
+    pool_free(lat, lat->d_counters);
     delete lat;
     return FR_OK;
 }
@@ -1131,6 +1146,7 @@ int fr_lattice_splat(fr_lattice *lat, const double *F, const double *V, int64_t 
         return FR_EINVAL;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    lat->stream = s;
     GenericSrc src{F, V, nv};
     FR_DISPATCH_D(lat->dim, FR_TRY((splat_impl<D, GenericSrc>(lat, src, n, nv, s))));
     return FR_OK;
@@ -1150,6 +1166,7 @@ int fr_lattice_splat_points(fr_lattice *lat, const float *pos, const float *nrm,
         set_error("observation cloud has no normals");
         return FR_EINVAL;
     }
+    lat->stream = (cudaStream_t)stream;
     int m2 = (value_mode & FR_VALUES_M2) ? 1 : 0;
     int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
     PointSrc src{pos, nrm, n, m2, nv};
@@ -1161,6 +1178,7 @@ int fr_lattice_blur(fr_lattice *lat, void *stream) {
         set_error("null lattice");
         return FR_EINVAL;
     }
+    lat->stream = (cudaStream_t)stream;
     FR_DISPATCH_D(lat->dim, FR_TRY(blur_impl<D>(lat, (cudaStream_t)stream)));
     return FR_OK;
 }

@@ -1600,10 +1600,14 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
     h.max_halvings = cfg->max_halvings;
     make_rigid_k(h.A, h.R, h.t, h.c_ref, h.cp, h.gain, -1, -1, &h.k);
     const int grid = pass_grid_max();
-    if (cudaMalloc(&em->d_em, sizeof(EmDev)) != cudaSuccess ||
-        cudaMalloc(&em->d_sums, 32 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&em->d_scratch, (size_t)grid * 32 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double)) != cudaSuccess ||
+    // stream-ordered pool (see fr_lattice.cu pool_alloc): no cudaMalloc /
+    // cudaFree mapping work per registration
+    if (cudaMallocAsync((void **)&em->d_em, sizeof(EmDev), 0) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_sums, 32 * sizeof(double), 0) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_scratch, (size_t)grid * 32 * sizeof(double), 0) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double), 0) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(0) != cudaSuccess ||
 
         cudaMemcpy(em->d_em, &h, sizeof(EmDev), cudaMemcpyHostToDevice) != cudaSuccess) {
         fr_rigid_em_destroy(em);
@@ -1617,10 +1621,10 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
 int fr_rigid_em_destroy(fr_rigid_em *em) {
     if (!em) return FR_OK;
     if (em->graph) cudaGraphExecDestroy(em->graph);
-    cudaFree(em->d_em);
-    cudaFree(em->d_sums);
-    cudaFree(em->d_scratch);
-    cudaFree(em->d_traces);
+    cudaDeviceSynchronize();   // the loop may still run on the caller's stream
+    for (void *p : {(void *)em->d_em, (void *)em->d_sums, (void *)em->d_scratch,
+                    (void *)em->d_traces})
+        if (p) cudaFreeAsync(p, 0);
     delete em;
     return FR_OK;
 }

@@ -1,0 +1,127 @@
+// Host -> device upload of a point cloud: (n, 3) float64 rows in pageable
+// host memory -> (3, n) float32 planes in HBM (the layout every pass reads).
+//
+// The reference keeps clouds as float64 NumPy arrays (geometry.py:109-139) and
+// the engine converts them once at the boundary.  A plain
+// pageable copy of the float64 rows runs at ~10 GB/s and the NumPy float32
+// conversion is single-threaded, so at C5 sizes the upload dominated the
+// end-to-end call.  Here worker threads each own a slice of the rows and two
+// pinned staging slots from a process-wide pool: a worker converts a sub-chunk
+// (float32 rounding to nearest, as numpy.astype) into one slot as three
+// planes while the DMA of its other slot is in flight, then enqueues one 2-D
+// copy into the three device planes on the caller's stream.  The workers are
+// joined before return; the copies stay stream-ordered.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "fr_common.cuh"
+
+namespace fr {
+
+namespace {
+
+constexpr long long kSubChunk = 1 << 17;   // points per staging slot (1.5 MB)
+constexpr int kMaxWorkers = 16;
+
+struct StagePool {
+    std::mutex mu;
+    int workers = 0;
+    float *base = nullptr;                 // one pinned block, carved into slots
+    float *slots[kMaxWorkers][2] = {};
+    cudaEvent_t done[kMaxWorkers][2] = {};
+
+    // all kMaxWorkers x 2 slots (48 MB pinned) on first use, so the one-time
+    // allocation lands in whatever call comes first (e.g. a warm-up)
+    int init() {
+        if (workers) return FR_OK;
+        const size_t slot = (size_t)kSubChunk * 3;
+        FR_CUDA(cudaHostAlloc(&base, slot * 2 * kMaxWorkers * sizeof(float), cudaHostAllocDefault));
+        for (int i = 0; i < kMaxWorkers; ++i)
+            for (int j = 0; j < 2; ++j) {
+                slots[i][j] = base + slot * (2 * i + j);
+                FR_CUDA(cudaEventCreateWithFlags(&done[i][j], cudaEventDisableTiming));
+            }
+        workers = kMaxWorkers;
+        return FR_OK;
+    }
+};
+
+StagePool &pool() {
+    static StagePool p;
+    return p;
+}
+
+struct WorkerResult {
+    int status = FR_OK;
+    char msg[256] = {0};
+};
+
+void worker(int id, const double *src, long long n, long long a, long long b, float *dst,
+            cudaStream_t s, WorkerResult *res) {
+    StagePool &p = pool();
+    int slot = 0;
+    for (long long c = a; c < b; c += kSubChunk) {
+        const long long len = std::min(kSubChunk, b - c);
+        float *buf = p.slots[id][slot];
+        cudaError_t e = cudaEventSynchronize(p.done[id][slot]);   // slot's previous DMA
+        if (e == cudaSuccess) {
+            const double *r = src + 3 * c;
+            float *x = buf, *y = buf + kSubChunk, *z = buf + 2 * kSubChunk;
+            for (long long i = 0; i < len; ++i) {
+                x[i] = (float)r[3 * i];
+                y[i] = (float)r[3 * i + 1];
+                z[i] = (float)r[3 * i + 2];
+            }
+            e = cudaMemcpy2DAsync(dst + c, (size_t)n * sizeof(float), buf,
+                                  (size_t)kSubChunk * sizeof(float), (size_t)len * sizeof(float),
+                                  3, cudaMemcpyHostToDevice, s);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(p.done[id][slot], s);
+        if (e != cudaSuccess) {
+            res->status = FR_ECUDA;
+            snprintf(res->msg, sizeof(res->msg), "point upload: %s", cudaGetErrorString(e));
+            return;
+        }
+        slot ^= 1;
+    }
+}
+
+}  // namespace
+}  // namespace fr
+
+using namespace fr;
+
+extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa, void *stream) {
+    if (n < 0 || (n > 0 && (!host_xyz || !d_soa))) {
+        set_error("fr_upload_points: invalid arguments");
+        return FR_EINVAL;
+    }
+    if (n == 0) return FR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int w = (int)std::max<long long>(
+        1, std::min<long long>({(long long)kMaxWorkers, (long long)hw, (n + kSubChunk - 1) / kSubChunk}));
+    StagePool &p = pool();
+    std::lock_guard<std::mutex> lock(p.mu);   // one upload at a time owns the slots
+    FR_TRY(p.init());
+    const long long per = (n + w - 1) / w;
+    std::vector<WorkerResult> res(w);
+    std::vector<std::thread> th;
+    th.reserve(w);
+    for (int i = 0; i < w; ++i) {
+        const long long a = std::min<long long>(n, (long long)i * per);
+        const long long b = std::min<long long>(n, a + per);
+        th.emplace_back(worker, i, host_xyz, (long long)n, a, b, d_soa, s, &res[i]);
+    }
+    for (auto &t : th) t.join();
+    for (const auto &r : res)
+        if (r.status != FR_OK) {
+            set_error("%s", r.msg);
+            return r.status;
+        }
+    return FR_OK;
+}
