@@ -171,49 +171,59 @@ __global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash
     }
 }
 
-// splat phase 2: one warp per site.  The lanes form 32 contributions
-// bary * value at a time (one rounding each, as NumPy's product) and stage
-// them in shared memory; lane 0 adds them in flat (point, vertex) order --
-// np.add.at's accumulation order (permutohedral.py:241-242), hence
-// bit-identical sums -- while the lanes already gather the next 32.
-constexpr int kSegWarps = 4;
+// splat phase 2: one block per site.  All threads form 256 contributions
+// bary * value at a time (one rounding each, as NumPy's product) into a
+// kSegStages-deep shared-memory ring; lane c of warp 0 adds column c in flat
+// (point, vertex) order -- np.add.at's accumulation order
+// (permutohedral.py:241-242), hence bit-identical sums -- while the other
+// threads already gather the following chunks.  A heavy site (10^5-10^6
+// entries at C5 sizes) is then bound by its one float64 add chain per column,
+// not by the latency of its random gathers.
+constexpr int kSegBlock = 256;
+constexpr int kSegStages = 3;
 
 template <int D, class Src>
-__global__ void __launch_bounds__(32 * kSegWarps)
-k_splat_segsum(Src src, int n_runs, const unsigned *run_slot, const int *run_off,
-               const int *run_cnt, const unsigned *sorted_idx, const double *entry_bary,
-               unsigned sentinel, int nv, double *run_vals) {
-    __shared__ double buf[kSegWarps][2][32][16];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = blockIdx.x * kSegWarps + warp;
-    if (r >= n_runs || run_slot[r] == sentinel) return;
+__global__ void __launch_bounds__(kSegBlock)
+k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int *run_cnt,
+               const unsigned *sorted_idx, const double *entry_bary, unsigned sentinel, int nv,
+               double *run_vals) {
+    extern __shared__ double ring[];   // [kSegStages][kSegBlock][nv]
+    const int r = blockIdx.x;
+    if (run_slot[r] == sentinel) return;
     const int beg = run_off[r], cnt = run_cnt[r];
-    double acc[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
-    const int chunks = (cnt + 31) / 32;
-    auto stage = [&](int ch, int slot) {
-        const int j = ch * 32 + lane;
+    const int chunks = (cnt + kSegBlock - 1) / kSegBlock;
+    const int t = threadIdx.x;
+    auto stage = [&](int ch) {
+        const int j = ch * kSegBlock + t;
         if (j < cnt) {
             const unsigned e = sorted_idx[beg + j];
             const double b = entry_bary[e];
             const long long p = e / (D + 1);
-            for (int c = 0; c < nv; ++c) buf[warp][slot][lane][c] = __dmul_rn(b, src.value(p, c));
+            double *row = ring + ((size_t)(ch % kSegStages) * kSegBlock + t) * nv;
+            for (int c = 0; c < nv; ++c) row[c] = __dmul_rn(b, src.value(p, c));
         }
     };
-    stage(0, 0);
-    __syncwarp();
+    for (int st = 0; st < kSegStages - 1 && st < chunks; ++st) stage(st);
+    __syncthreads();
+    double acc = 0.0;
     for (int ch = 0; ch < chunks; ++ch) {
-        if (ch + 1 < chunks) stage(ch + 1, (ch + 1) & 1);
-        if (lane == 0) {
-            const int n = min(32, cnt - ch * 32);
-            for (int i = 0; i < n; ++i)
-                for (int c = 0; c < nv; ++c) acc[c] = __dadd_rn(acc[c], buf[warp][ch & 1][i][c]);
+        if (ch + kSegStages - 1 < chunks) stage(ch + kSegStages - 1);
+        if (t < nv) {
+            const double *col = ring + (size_t)(ch % kSegStages) * kSegBlock * nv + t;
+            const int n = min(kSegBlock, cnt - ch * kSegBlock);
+            int i = 0;
+            for (; i + 8 <= n; i += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = col[(i + u) * nv];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+            }
+            for (; i < n; ++i) acc = __dadd_rn(acc, col[i * nv]);
         }
-        __syncwarp();
+        __syncthreads();
     }
-    if (lane == 0)
-        for (int c = 0; c < nv; ++c) run_vals[(long long)r * nv + c] = acc[c];
+    if (t < nv) run_vals[(long long)r * nv + t] = acc;
 }
 
 __global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentinel,
@@ -658,11 +668,15 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_TRY(sc.get(&iota, nruns));
     FR_TRY(sc.get(&d_nlive, 1));
     {
-        const unsigned blocks = (unsigned)((nruns + kSegWarps - 1) / kSegWarps);
-        k_splat_segsum<D, Src><<<std::max(blocks, 1u), 32 * kSegWarps, 0, s>>>(
-            src, nruns, run_slot, run_off, run_cnt, sorted_idx, entry_bary, (unsigned)cap, nv,
-            run_vals);
-        FR_CHECK_LAUNCH();
+        const size_t smem = (size_t)kSegStages * kSegBlock * nv * sizeof(double);
+        FR_CUDA(cudaFuncSetAttribute(k_splat_segsum<D, Src>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (nruns > 0) {
+            k_splat_segsum<D, Src><<<nruns, kSegBlock, smem, s>>>(
+                src, run_slot, run_off, run_cnt, sorted_idx, entry_bary, (unsigned)cap, nv,
+                run_vals);
+            FR_CHECK_LAUNCH();
+        }
         k_run_live<<<grid_for(nruns), 256, 0, s>>>(nruns, run_slot, (unsigned)cap, run_vals, nv,
                                                    run_live);
         FR_CHECK_LAUNCH();
