@@ -502,12 +502,16 @@ __device__ __forceinline__ void cp_async4(float *smem, const float *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// stage one point's three coordinates (the thread's own slot)
-__device__ __forceinline__ void ring_issue(float (*slot)[kPassThreads], const float *ref,
-                                           long long m, long long q, long long end) {
-    if (q < end) {
+template <int PTS>
+__device__ __forceinline__ void ring_issue_pts(float (*slot)[3][kPassThreads], const float *ref,
+                                               long long m, long long base, long long end) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async4(&slot[c][threadIdx.x], ref + c * m + q);
+    for (int k = 0; k < PTS; ++k) {
+        const long long q = base + (long long)k * kPassThreads + threadIdx.x;
+        if (q < end) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) cp_async4(&slot[k][c][threadIdx.x], ref + c * m + q);
+        }
     }
     cp_async_commit();
 }
@@ -587,14 +591,122 @@ struct GridAcc {
     }
 };
 
-template <bool DEV>
-__global__ void __launch_bounds__(kPassThreads, 3)
+// one model point of the dense-grid pass (valid = 0: the point contributes
+// nothing; branch-free so the points of a thread interleave)
+__device__ __forceinline__ void grid_point(float nx, float ny, float nz, bool valid,
+                                           const GridK &g, const int4 *tab,
+                                           const DenseSliceF &dg, GridAcc &a) {
+    const float x0 = nx - g.cref[0], x1 = ny - g.cref[1], x2 = nz - g.cref[2];
+    // y = R xh as (y0, y1) and (y2, 1)
+    float2 y01 = __fmul2_rn(g.Rc[0], bc(x0));
+    y01 = __ffma2_rn(g.Rc[1], bc(x1), y01);
+    y01 = __ffma2_rn(g.Rc[2], bc(x2), y01);
+    float2 y2v = __ffma2_rn(g.R2[0], bc(x0), make_float2(0.0f, 1.0f));
+    y2v = __ffma2_rn(g.R2[1], bc(x1), y2v);
+    y2v = __ffma2_rn(g.R2[2], bc(x2), y2v);
+    // elevated coordinates minus 4 * base
+    float2 e01 = __ffma2_rn(g.A01[0], bc(y01.x), g.f01);
+    e01 = __ffma2_rn(g.A01[1], bc(y01.y), e01);
+    e01 = __ffma2_rn(g.A01[2], bc(y2v.x), e01);
+    float2 e23 = __ffma2_rn(g.A23[0], bc(y01.x), g.f23);
+    e23 = __ffma2_rn(g.A23[1], bc(y01.y), e23);
+    e23 = __ffma2_rn(g.A23[2], bc(y2v.x), e23);
+    const float el[4] = {e01.x, e01.y, e23.x, e23.y};
+    float d[4];
+    int tb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float t = fmaf(el[i], 0.25f, kMagic);   // rint(el / 4) + magic
+        tb[i] = __float_as_int(t);
+        d[i] = fmaf(-4.0f, t - kMagic, el[i]);
+    }
+    unsigned code = 0;
+    {
+        int q = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i + 1; j < 4; ++j, ++q) code |= (d[j] > d[i] ? 1u : 0u) << q;
+    }
+    // descending sorting network -> pre-wrap barycentrics
+    float s0 = fmaxf(d[0], d[1]), s1 = fminf(d[0], d[1]);
+    float s2 = fmaxf(d[2], d[3]), s3 = fminf(d[2], d[3]);
+    {
+        const float hi = fmaxf(s0, s2), lo = fminf(s0, s2);
+        s0 = hi;
+        s2 = lo;
+        const float hi2 = fmaxf(s1, s3), lo2 = fminf(s1, s3);
+        s1 = hi2;
+        s3 = lo2;
+        const float hi3 = fmaxf(s1, s2), lo3 = fminf(s1, s2);
+        s1 = hi3;
+        s2 = lo3;
+    }
+    const float b0 = fmaf(0.25f, s3 - s0, 1.0f);
+    const float b1 = 0.25f * (s2 - s3);
+    const float b2 = 0.25f * (s1 - s2);
+    const float b3 = 0.25f * (s0 - s1);
+    const int h = (int)((unsigned)tb[0] + (unsigned)tb[1] + (unsigned)tb[2] + (unsigned)tb[3] + g.H);
+    const int hi = min(max(h + 2, 0), 4);
+    const int4 T = tab[code * 5 + hi];
+    const bool in = ((unsigned)(tb[0] + g.C[0]) <= g.lim[0]) &
+                    ((unsigned)(tb[1] + g.C[1]) <= g.lim[1]) &
+                    ((unsigned)(tb[2] + g.C[2]) <= g.lim[2]);
+    float2 o01 = make_float2(0.f, 0.f), o23 = make_float2(0.f, 0.f);
+    if (in) {
+        const unsigned c4 = 4u * ((unsigned)tb[0] * (unsigned)g.s0 +
+                                  (unsigned)tb[1] * (unsigned)g.s1 + (unsigned)tb[2] + g.K);
+        const float4 v0 = __ldg(dg.cells + (int)(c4 + (unsigned)T.x));
+        const float4 v1 = __ldg(dg.cells + (int)(c4 + (unsigned)T.y));
+        const float4 v2 = __ldg(dg.cells + (int)(c4 + (unsigned)T.z));
+        const float4 v3 = __ldg(dg.cells + (int)(c4 + (unsigned)T.w));
+        o01 = __fmul2_rn(bc(b0), make_float2(v0.x, v0.y));
+        o23 = __fmul2_rn(bc(b0), make_float2(v0.z, v0.w));
+        o01 = __ffma2_rn(bc(b1), make_float2(v1.x, v1.y), o01);
+        o23 = __ffma2_rn(bc(b1), make_float2(v1.z, v1.w), o23);
+        o01 = __ffma2_rn(bc(b2), make_float2(v2.x, v2.y), o01);
+        o23 = __ffma2_rn(bc(b2), make_float2(v2.z, v2.w), o23);
+        o01 = __ffma2_rn(bc(b3), make_float2(v3.x, v3.y), o01);
+        o23 = __ffma2_rn(bc(b3), make_float2(v3.z, v3.w), o23);
+    }
+    // o01 = (sum y0, sum y1), o23 = (sum y2, mass)
+    const float m0 = fmaxf(o23.y, 0.0f);
+    const bool sup = m0 >= 1e-12f;
+    const float w = (sup && valid) ? (g.cp > 0.0f ? m0 * rcp_approx(m0 + g.cp) : 1.0f) : 0.0f;
+    const float ninv = sup ? -rcp_approx(m0) : 0.0f;
+    // residual r = x - t (centred); w = 0 zeroes every term of an
+    // unsupported point, whatever r holds
+    const float2 r01 = __fadd2_rn(y01, __ffma2_rn(o01, bc(ninv), g.cw01));
+    const float r2 = y2v.x + fmaf(o23.x, ninv, g.cw2.x);
+    const float2 wy01 = __fmul2_rn(bc(w), y01);
+    const float2 wy2v = __fmul2_rn(bc(w), y2v);          // (w y2, w)
+    const float2 wr01 = __fmul2_rn(bc(w), r01);
+    const float wr2 = w * r2;
+    a.s1_01 = __fadd2_rn(a.s1_01, wy01);
+    a.s1_2_s0 = __fadd2_rn(a.s1_2_s0, wy2v);
+    a.s2_00_01 = __ffma2_rn(bc(wy01.x), y01, a.s2_00_01);
+    a.s2_02_12 = __ffma2_rn(bc(y2v.x), wy01, a.s2_02_12);
+    a.s2_11 = fmaf(wy01.y, y01.y, a.s2_11);
+    a.s2_22 = fmaf(wy2v.x, y2v.x, a.s2_22);
+    a.rx01[0] = __ffma2_rn(bc(wr01.x), y01, a.rx01[0]);
+    a.rx2_r1[0] = __ffma2_rn(bc(wr01.x), y2v, a.rx2_r1[0]);
+    a.rx01[1] = __ffma2_rn(bc(wr01.y), y01, a.rx01[1]);
+    a.rx2_r1[1] = __ffma2_rn(bc(wr01.y), y2v, a.rx2_r1[1]);
+    a.rx01[2] = __ffma2_rn(bc(wr2), y01, a.rx01[2]);
+    a.rx2_r1[2] = __ffma2_rn(bc(wr2), y2v, a.rx2_r1[2]);
+    a.q01 = __ffma2_rn(wr01, r01, a.q01);
+    a.q2 = fmaf(wr2, r2, a.q2);
+}
+
+// PTS model points per thread per ring stage (1: 3 CTAs/SM; 2: 2 CTAs/SM)
+template <bool DEV, int PTS>
+__global__ void __launch_bounds__(kPassThreads, PTS == 1 ? 3 : 2)
 k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
                   const int *done, DenseSliceF dg, double *__restrict__ partials) {
     constexpr int NA = kP2PtBase;
     __shared__ GridK g;
     __shared__ int4 tab[kGridTab];
-    __shared__ float ring[kGridStages][3][kPassThreads];
+    __shared__ float ring[kGridStages][PTS][3][kPassThreads];
     if (DEV && *done) return;
     if (threadIdx.x == 0) {
         const RigidK &k = DEV ? *kd : kv;
@@ -645,121 +757,31 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
     const long long chunk = ((m + gridDim.x - 1) / gridDim.x + 31) & ~31ll;
     const long long beg = (long long)blockIdx.x * chunk;
     const long long end = min(beg + chunk, m);
+    constexpr long long SP = (long long)PTS * kPassThreads;   // points per ring stage
 #pragma unroll
     for (int st = 0; st < kGridStages - 1; ++st)
-        ring_issue(ring[st], ref, m, beg + (long long)st * kPassThreads + threadIdx.x, end);
+        ring_issue_pts<PTS>(ring[st], ref, m, beg + st * SP, end);
     int stage = 0;
-    for (long long base = beg; base < end; base += kPassThreads) {
-        ring_issue(ring[stage == 0 ? kGridStages - 1 : stage - 1], ref, m,
-                   base + (long long)(kGridStages - 1) * kPassThreads + threadIdx.x, end);
+    for (long long base = beg; base < end; base += SP) {
+        ring_issue_pts<PTS>(ring[stage == 0 ? kGridStages - 1 : stage - 1], ref, m,
+                            base + (kGridStages - 1) * SP, end);
         cp_async_wait<kGridStages - 1>();
-        const long long p = base + threadIdx.x;
-        const float nx = ring[stage][0][threadIdx.x];
-        const float ny = ring[stage][1][threadIdx.x];
-        const float nz = ring[stage][2][threadIdx.x];
+        float px[PTS], py[PTS], pz[PTS];
+        bool ok[PTS];
+#pragma unroll
+        for (int k = 0; k < PTS; ++k) {
+            // a slot past the chunk end holds stale shared memory (maybe NaN,
+            // which w = 0 would not cancel): feed it finite coordinates
+            ok[k] = base + k * kPassThreads + threadIdx.x < end;
+            px[k] = ok[k] ? ring[stage][k][0][threadIdx.x] : 0.0f;
+            py[k] = ok[k] ? ring[stage][k][1][threadIdx.x] : 0.0f;
+            pz[k] = ok[k] ? ring[stage][k][2][threadIdx.x] : 0.0f;
+        }
         stage = stage + 1 == kGridStages ? 0 : stage + 1;
-        if (p >= end) continue;
-        const float x0 = nx - g.cref[0], x1 = ny - g.cref[1], x2 = nz - g.cref[2];
-        // y = R xh as (y0, y1) and (y2, 1)
-        float2 y01 = __fmul2_rn(g.Rc[0], bc(x0));
-        y01 = __ffma2_rn(g.Rc[1], bc(x1), y01);
-        y01 = __ffma2_rn(g.Rc[2], bc(x2), y01);
-        float2 y2v = __ffma2_rn(g.R2[0], bc(x0), make_float2(0.0f, 1.0f));
-        y2v = __ffma2_rn(g.R2[1], bc(x1), y2v);
-        y2v = __ffma2_rn(g.R2[2], bc(x2), y2v);
-        // elevated coordinates minus 4 * base
-        float2 e01 = __ffma2_rn(g.A01[0], bc(y01.x), g.f01);
-        e01 = __ffma2_rn(g.A01[1], bc(y01.y), e01);
-        e01 = __ffma2_rn(g.A01[2], bc(y2v.x), e01);
-        float2 e23 = __ffma2_rn(g.A23[0], bc(y01.x), g.f23);
-        e23 = __ffma2_rn(g.A23[1], bc(y01.y), e23);
-        e23 = __ffma2_rn(g.A23[2], bc(y2v.x), e23);
-        const float el[4] = {e01.x, e01.y, e23.x, e23.y};
-        float d[4];
-        int tb[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float t = fmaf(el[i], 0.25f, kMagic);   // rint(el / 4) + magic
-            tb[i] = __float_as_int(t);
-            d[i] = fmaf(-4.0f, t - kMagic, el[i]);
-        }
-        unsigned code = 0;
-        {
-            int q = 0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = i + 1; j < 4; ++j, ++q) code |= (d[j] > d[i] ? 1u : 0u) << q;
-        }
-        // descending sorting network -> pre-wrap barycentrics
-        float s0 = fmaxf(d[0], d[1]), s1 = fminf(d[0], d[1]);
-        float s2 = fmaxf(d[2], d[3]), s3 = fminf(d[2], d[3]);
-        {
-            const float hi = fmaxf(s0, s2), lo = fminf(s0, s2);
-            s0 = hi;
-            s2 = lo;
-            const float hi2 = fmaxf(s1, s3), lo2 = fminf(s1, s3);
-            s1 = hi2;
-            s3 = lo2;
-            const float hi3 = fmaxf(s1, s2), lo3 = fminf(s1, s2);
-            s1 = hi3;
-            s2 = lo3;
-        }
-        const float b0 = fmaf(0.25f, s3 - s0, 1.0f);
-        const float b1 = 0.25f * (s2 - s3);
-        const float b2 = 0.25f * (s1 - s2);
-        const float b3 = 0.25f * (s0 - s1);
-        const int h = (int)((unsigned)tb[0] + (unsigned)tb[1] + (unsigned)tb[2] + (unsigned)tb[3] + g.H);
-        const int hi = min(max(h + 2, 0), 4);
-        const int4 T = tab[code * 5 + hi];
-        const bool in = ((unsigned)(tb[0] + g.C[0]) <= g.lim[0]) &
-                        ((unsigned)(tb[1] + g.C[1]) <= g.lim[1]) &
-                        ((unsigned)(tb[2] + g.C[2]) <= g.lim[2]);
-        float2 o01 = make_float2(0.f, 0.f), o23 = make_float2(0.f, 0.f);
-        if (in) {
-            const unsigned c4 = 4u * ((unsigned)tb[0] * (unsigned)g.s0 +
-                                      (unsigned)tb[1] * (unsigned)g.s1 + (unsigned)tb[2] + g.K);
-            const float4 v0 = __ldg(dg.cells + (int)(c4 + (unsigned)T.x));
-            const float4 v1 = __ldg(dg.cells + (int)(c4 + (unsigned)T.y));
-            const float4 v2 = __ldg(dg.cells + (int)(c4 + (unsigned)T.z));
-            const float4 v3 = __ldg(dg.cells + (int)(c4 + (unsigned)T.w));
-            o01 = __fmul2_rn(bc(b0), make_float2(v0.x, v0.y));
-            o23 = __fmul2_rn(bc(b0), make_float2(v0.z, v0.w));
-            o01 = __ffma2_rn(bc(b1), make_float2(v1.x, v1.y), o01);
-            o23 = __ffma2_rn(bc(b1), make_float2(v1.z, v1.w), o23);
-            o01 = __ffma2_rn(bc(b2), make_float2(v2.x, v2.y), o01);
-            o23 = __ffma2_rn(bc(b2), make_float2(v2.z, v2.w), o23);
-            o01 = __ffma2_rn(bc(b3), make_float2(v3.x, v3.y), o01);
-            o23 = __ffma2_rn(bc(b3), make_float2(v3.z, v3.w), o23);
-        }
-        // o01 = (sum y0, sum y1), o23 = (sum y2, mass)
-        const float m0 = fmaxf(o23.y, 0.0f);
-        const bool sup = m0 >= 1e-12f;
-        const float w = sup ? (g.cp > 0.0f ? m0 * rcp_approx(m0 + g.cp) : 1.0f) : 0.0f;
-        const float ninv = sup ? -rcp_approx(m0) : 0.0f;
-        // residual r = x - t (centred); w = 0 zeroes every term of an
-        // unsupported point, whatever r holds
-        const float2 r01 = __fadd2_rn(y01, __ffma2_rn(o01, bc(ninv), g.cw01));
-        const float r2 = y2v.x + fmaf(o23.x, ninv, g.cw2.x);
-        const float2 wy01 = __fmul2_rn(bc(w), y01);
-        const float2 wy2v = __fmul2_rn(bc(w), y2v);          // (w y2, w)
-        const float2 wr01 = __fmul2_rn(bc(w), r01);
-        const float wr2 = w * r2;
-        a.s1_01 = __fadd2_rn(a.s1_01, wy01);
-        a.s1_2_s0 = __fadd2_rn(a.s1_2_s0, wy2v);
-        a.s2_00_01 = __ffma2_rn(bc(wy01.x), y01, a.s2_00_01);
-        a.s2_02_12 = __ffma2_rn(bc(y2v.x), wy01, a.s2_02_12);
-        a.s2_11 = fmaf(wy01.y, y01.y, a.s2_11);
-        a.s2_22 = fmaf(wy2v.x, y2v.x, a.s2_22);
-        a.rx01[0] = __ffma2_rn(bc(wr01.x), y01, a.rx01[0]);
-        a.rx2_r1[0] = __ffma2_rn(bc(wr01.x), y2v, a.rx2_r1[0]);
-        a.rx01[1] = __ffma2_rn(bc(wr01.y), y01, a.rx01[1]);
-        a.rx2_r1[1] = __ffma2_rn(bc(wr01.y), y2v, a.rx2_r1[1]);
-        a.rx01[2] = __ffma2_rn(bc(wr2), y01, a.rx01[2]);
-        a.rx2_r1[2] = __ffma2_rn(bc(wr2), y2v, a.rx2_r1[2]);
-        a.q01 = __ffma2_rn(wr01, r01, a.q01);
-        a.q2 = fmaf(wr2, r2, a.q2);
-        if (++fold == kGridFold) {
+        for (int k = 0; k < PTS; ++k) grid_point(px[k], py[k], pz[k], ok[k], g, tab, dg, a);
+        fold += PTS;
+        if (fold >= kGridFold) {
 #pragma unroll
             for (int c = 0; c < NA; ++c) sacc[c * kPassThreads + threadIdx.x] += (double)a.col(c);
             a.zero();
@@ -772,6 +794,18 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
     block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
 }
 
+// points per thread per ring stage of the dense-grid pass: 2 (two
+// independent chains per thread, shared parameter loads; 8 % faster than 1 at
+// 16.8M points, 2 CTAs/SM); FR_GRID_PTS=1 selects the 3-CTA single-point form
+static int grid_pts() {
+    static int pts = 0;
+    if (!pts) {
+        const char *e = getenv("FR_GRID_PTS");
+        pts = (e && e[0] == '1') ? 1 : 2;
+    }
+    return pts;
+}
+
 static int set_f32_smem() {
     static bool done = false;
     if (!done) {
@@ -779,9 +813,13 @@ static int set_f32_smem() {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
         FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<true>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<true, 1>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<false>,
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<false, 1>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<true, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
+        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<false, 2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
         done = true;
     }
@@ -1318,13 +1356,13 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         const SliceTableF tf = lat->table_f();
         const DenseSliceF dg = lat->dense;
         if (lat->dcells != nullptr) {
-            const int g3 = pass_grid_dense();
-            if (dev)
-                k_rigid_pass_grid<true><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
-                                                                           dg, scratch);
-            else
-                k_rigid_pass_grid<false><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done,
-                                                                            dg, scratch);
+            const int pts = grid_pts();
+            const int g3 = pts == 2 ? pass_grid() : pass_grid_dense();
+#define FR_GRID(DEV, P) \
+    k_rigid_pass_grid<DEV, P><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, dg, scratch)
+            if (pts == 2) { if (dev) FR_GRID(true, 2); else FR_GRID(false, 2); }
+            else { if (dev) FR_GRID(true, 1); else FR_GRID(false, 1); }
+#undef FR_GRID
             FR_CHECK_LAUNCH();
             k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g3, kP2PtBase, sums, done);
             FR_CHECK_LAUNCH();
