@@ -140,10 +140,14 @@ def embed_simplex(features, sigma):
 # sorted site table with mixed-radix codes (permutohedral.py:96-137, 253-270)
 
 class _Codes:
-    """Lexicographic int64 codes of the first d key columns over fixed bounds."""
+    """Sortable codes of the first d key columns (_RowCodec,
+    permutohedral.py:96-131): mixed-radix int64 over the rows' bounds when the
+    span product is below 2**62, else the raw bytes of the little-endian int64
+    rows (numpy void view: memcmp order, no range test)."""
 
     def __init__(self, rows):
         rows = np.asarray(rows, dtype=np.int64)
+        self.cols = rows.shape[1]
         if len(rows):
             self.lo = rows.min(axis=0)
             self.hi = rows.max(axis=0)
@@ -154,14 +158,17 @@ class _Codes:
         total = 1
         for s in span:
             total *= s
-        if total >= 2 ** 62:
-            raise OverflowError("key span too wide for the oracle's int64 codes")
+        self.arithmetic = total < 2 ** 62
         self.mult = np.ones(len(span), dtype=np.int64)
-        for c in range(len(span) - 2, -1, -1):
-            self.mult[c] = self.mult[c + 1] * span[c + 1]
+        if self.arithmetic:
+            for c in range(len(span) - 2, -1, -1):
+                self.mult[c] = self.mult[c + 1] * span[c + 1]
 
     def __call__(self, rows):
-        rows = np.asarray(rows, dtype=np.int64)
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        if not self.arithmetic:
+            codes = rows.view(np.dtype((np.void, 8 * self.cols))).reshape(-1)
+            return codes, np.ones(len(rows), dtype=bool)
         ok = np.all((rows >= self.lo) & (rows <= self.hi), axis=1)
         return (np.clip(rows, self.lo, self.hi) - self.lo) @ self.mult, ok
 

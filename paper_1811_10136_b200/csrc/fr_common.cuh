@@ -140,7 +140,9 @@ __device__ __forceinline__ void simplex_from_elevated(const double *el, Simplex<
 #pragma unroll
     for (int i = 0; i <= D; ++i) {
         double r = rint(div_d1<D>(el[i]));
-        if (!(fabs(r) < (double)(kKeyLim / (D + 1)))) { s.overflow = 1; r = 0.0; }
+        // d <= 3: the 21-bit packed key range; d >= 4: int32 keys
+        constexpr double kLim = D <= 3 ? (double)(kKeyLim / (D + 1)) : (double)((1 << 28) / (D + 1));
+        if (!(fabs(r) < kLim)) { s.overflow = 1; r = 0.0; }
         int ri = (int)r;
         s.rem0[i] = ri * (D + 1);
         hsum += ri;
@@ -281,6 +283,17 @@ inline int nvp_for(int nv) { return nv <= 4 ? 4 : (nv <= 8 ? 8 : (nv <= 16 ? 16 
 
 // interleaved slot: packed key, then gain * value row as float32; 32 bytes
 // (one sector) for nv <= 4, 64 bytes for nv <= 8.  The hash is a 32-bit fold.
+// 128-bit key codec of the d >= 4 lattice (fr_lattice_wide.cuh): coordinate i
+// of the first d occupies `bits[i]` bits at `shift[i]` (coordinate 0 highest),
+// stored as k[i] - lo[i]
+struct WideCodec {
+    int d;
+    int lo[kMaxDim];
+    int bits[kMaxDim];
+    int shift[kMaxDim];
+    int total;
+};
+
 struct SliceTableF {
     const float4 *slots;    // [cap][1 + nf4] float4; slot word 0 holds the key
     unsigned mask;
@@ -541,6 +554,9 @@ struct fr_lattice {
     float4 *dcells = nullptr;
     fr::DenseSliceF dense{};
     long long dense_cells = 0;
+    // d >= 4: sorted 128-bit site keys (hi / lo words) and their codec
+    unsigned long long *wkh = nullptr, *wkl = nullptr;
+    fr::WideCodec wc{};
     // device counters / flags
     unsigned long long *d_counters = nullptr;   // [0] sites, [1] src count, [2] overflow
     cudaStream_t stream = nullptr;              // stream of the last build call (pool ordering)

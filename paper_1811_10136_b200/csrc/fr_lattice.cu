@@ -41,8 +41,8 @@ static const double kGain[13] = {0,
                                  7167.31894204168,   16021.44046866235,  36206.979459505295};
 
 int make_consts(int dim, const double *sigma, LatticeConsts *out) {
-    if (dim < 1 || dim > 3) {
-        set_error("feature dimension %d not compiled in this build (supported: 1..3)", dim);
+    if (dim < 1 || dim > kMaxDim) {
+        set_error("lattice dimension %d outside 1..12", dim);   // permutohedral.py:148-149
         return FR_EINVAL;
     }
     memset(out, 0, sizeof(*out));
@@ -189,7 +189,7 @@ k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int 
                double *run_vals) {
     extern __shared__ double ring[];   // [kSegStages][kSegBlock][nv]
     const int r = blockIdx.x;
-    if (run_slot[r] == sentinel) return;
+    if (run_slot && run_slot[r] == sentinel) return;   // (null: no sentinel runs)
     const int beg = run_off[r], cnt = run_cnt[r];
     const int chunks = (cnt + kSegBlock - 1) / kSegBlock;
     const int t = threadIdx.x;
@@ -231,7 +231,7 @@ __global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentin
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_runs) return;
     bool live = false;
-    if (run_slot[r] != sentinel)
+    if (!run_slot || run_slot[r] != sentinel)
         for (int c = 0; c < nv; ++c) live |= run_vals[(long long)r * nv + c] != 0.0;
     run_live[r] = live;
 }
@@ -516,6 +516,9 @@ static void pool_free(fr_lattice *lat, void *p) {
 }
 
 static void free_build(fr_lattice *lat) {
+    pool_free(lat, lat->wkh);
+    pool_free(lat, lat->wkl);
+    lat->wkh = lat->wkl = nullptr;
     pool_free(lat, lat->site_keys);
     pool_free(lat, lat->vals);
     pool_free(lat, lat->vals_alt);
@@ -1043,6 +1046,8 @@ __global__ void k_gather_planes(const float *src, long long n, int planes, const
     for (int a = 0; a < planes; ++a) dst[a * n + i] = src[a * n + j];
 }
 
+#include "fr_lattice_wide.cuh"
+
 // ===========================================================================
 // C ABI
 
@@ -1053,6 +1058,21 @@ using namespace fr;
         case 1: { constexpr int D = 1; CALL; } break;                          \
         case 2: { constexpr int D = 2; CALL; } break;                          \
         case 3: { constexpr int D = 3; CALL; } break;                          \
+        default: set_error("dimension %d not compiled", dim); return FR_EINVAL; \
+    }
+
+// d = 4..12: the sorted 128-bit-key lattice (fr_lattice_wide.cuh)
+#define FR_DISPATCH_WIDE(dim, CALL)                                            \
+    switch (dim) {                                                             \
+        case 4: { constexpr int D = 4; CALL; } break;                          \
+        case 5: { constexpr int D = 5; CALL; } break;                          \
+        case 6: { constexpr int D = 6; CALL; } break;                          \
+        case 7: { constexpr int D = 7; CALL; } break;                          \
+        case 8: { constexpr int D = 8; CALL; } break;                          \
+        case 9: { constexpr int D = 9; CALL; } break;                          \
+        case 10: { constexpr int D = 10; CALL; } break;                        \
+        case 11: { constexpr int D = 11; CALL; } break;                        \
+        case 12: { constexpr int D = 12; CALL; } break;                        \
         default: set_error("dimension %d not compiled", dim); return FR_EINVAL; \
     }
 
@@ -1162,6 +1182,10 @@ int fr_lattice_splat(fr_lattice *lat, const double *F, const double *V, int64_t 
     cudaStream_t s = (cudaStream_t)stream;
     lat->stream = s;
     GenericSrc src{F, V, nv};
+    if (lat->dim >= 4) {
+        FR_DISPATCH_WIDE(lat->dim, FR_TRY((wide_splat<D, GenericSrc>(lat, src, n, nv, s))));
+        return FR_OK;
+    }
     FR_DISPATCH_D(lat->dim, FR_TRY((splat_impl<D, GenericSrc>(lat, src, n, nv, s))));
     return FR_OK;
 }
@@ -1193,6 +1217,10 @@ int fr_lattice_blur(fr_lattice *lat, void *stream) {
         return FR_EINVAL;
     }
     lat->stream = (cudaStream_t)stream;
+    if (lat->dim >= 4) {
+        FR_DISPATCH_WIDE(lat->dim, FR_TRY(wide_blur<D>(lat, (cudaStream_t)stream)));
+        return FR_OK;
+    }
     FR_DISPATCH_D(lat->dim, FR_TRY(blur_impl<D>(lat, (cudaStream_t)stream)));
     return FR_OK;
 }
@@ -1245,6 +1273,10 @@ int fr_lattice_slice(const fr_lattice *lat, const double *Q, int64_t m, double *
         return FR_ESTATE;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    if (lat->dim >= 4) {
+        FR_DISPATCH_WIDE(lat->dim, FR_TRY(wide_slice<D>(lat, Q, m, out, s)));
+        return FR_OK;
+    }
     FR_DISPATCH_D(lat->dim, FR_TRY(slice_impl<D>(lat, Q, m, out, s)));
     return FR_OK;
 }
@@ -1258,7 +1290,11 @@ int fr_simplex(int dim, const double *sigma, const double *F, int64_t n, int32_t
     unsigned long long *flag = nullptr;
     FR_CUDA(cudaMallocAsync(&flag, sizeof(unsigned long long), s));
     FR_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned long long), s));
-    FR_DISPATCH_D(dim, (k_simplex<D><<<grid_for(n), 256, 0, s>>>(F, n, c, keys, bary, flag)));
+    if (dim >= 4) {
+        FR_DISPATCH_WIDE(dim, (k_simplex<D><<<grid_for(n), 256, 0, s>>>(F, n, c, keys, bary, flag)));
+    } else {
+        FR_DISPATCH_D(dim, (k_simplex<D><<<grid_for(n), 256, 0, s>>>(F, n, c, keys, bary, flag)));
+    }
     unsigned long long h = 0;
     FR_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, s));
     FR_CUDA(cudaFreeAsync(flag, s));

@@ -19,7 +19,7 @@ import numpy as np
 from . import _lib
 
 _MAX_DIM = 12
-COMPILED_DIMS = (1, 2, 3)
+COMPILED_DIMS = tuple(range(1, 13))   # d <= 3: hashed 63-bit keys; 4..12: sorted 128-bit keys
 MAX_VALUE_COLUMNS = 15
 
 
@@ -80,6 +80,22 @@ def gaussian_transform_bruteforce(query_features, input_features, input_values,
                                            _lib.stream_handle()))
         out[:, c0:c1] = part
     return out.cpu().numpy()
+
+
+def _reference_row_order(rows: np.ndarray) -> np.ndarray:
+    """Row order of the reference's site table (_RowCodec + _index,
+    permutohedral.py:96-131, 253-260): numeric lexicographic when the product of
+    the column spans is below 2**62 (mixed-radix int64 codes), else the order of
+    the rows' raw little-endian int64 bytes (the codec's void-view fallback)."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    spans = (rows.max(axis=0) - rows.min(axis=0) + 1).astype(object)
+    total = 1
+    for sp in spans:
+        total *= int(sp)
+    if total < 2 ** 62:
+        return np.lexsort(rows.T[::-1])
+    return np.argsort(rows.view(np.dtype((np.void, 8 * rows.shape[1]))).reshape(-1),
+                      kind="stable")
 
 
 class PermutohedralLattice:
@@ -237,8 +253,7 @@ class PermutohedralLattice:
                                                        _lib.stream_handle()))
             k = keys.cpu().numpy().astype(np.int64)
             v = vals.cpu().numpy()
-            # reference order: lexicographic in the first d columns
-            order = np.lexsort(k[:, :self.dim].T[::-1]) if S else np.zeros(0, dtype=np.int64)
+            order = _reference_row_order(k[:, :self.dim]) if S else np.zeros(0, dtype=np.int64)
             self._export = (k[order], v[order])
         return self._export
 

@@ -215,6 +215,66 @@ def _register_device_loop(path, model, config, timing):
                               termination=term, states=None)
 
 
+def _register_generic(reference: PointCloud, observation: PointCloud, initial_model,
+                      config: RegistrationConfig, timing: dict | None) -> RegistrationResult:
+    """The reference loop over the moment-field API (pipeline.py:125-181
+    line for line): `MomentEngine.moments` on the device (generic lattice
+    slice for feature / concatenated kernels up to d = 12, or the exact
+    transform for backend="bruteforce") + the device epilogue, then `m_step`
+    with device assembly.  Used where the fused point-to-point pass does not
+    apply: feature and concatenated correspondences
+    and the brute-force backend."""
+    from .estep import MomentEngine, update_sigma
+    from .kinematics import forward_points
+    from .mstep import m_step, residuals_from_moments
+    engine = MomentEngine(observation, config.gmm, config.backend,
+                          include_normals=config.residual_mode == "point_to_plane")
+    model = initial_model
+    diameter = reference.diameter()
+    sigma_current = engine.config.sigma
+    result = RegistrationResult(kinematics=model, iterations=0,
+                                states=[] if config.record_states else None)
+    for _ in range(config.max_em_iters):
+        result.iterations += 1
+        tick = time.perf_counter()
+        moved = forward_points(reference, model)
+        moments = engine.moments(moved.positions, reference.features)
+        if timing is not None:
+            timing["e_step_s"] = timing.get("e_step_s", 0.0) + time.perf_counter() - tick
+        mass = moments.inlier_mass()
+        result.inlier_masses.append(mass)
+        if mass < DEGENERATE_MASS_FRACTION * len(reference):
+            result.objectives.append(float("nan"))
+            result.twist_norms.append(float("nan"))
+            result.termination = "degenerate"
+            break
+        if config.gmm.update_sigma:
+            sigma_new = update_sigma(moved.positions, moments, floor=config.gmm.sigma_floor)
+            if sigma_new != sigma_current[0]:
+                engine = engine.with_sigma(sigma_new)
+                sigma_current = engine.config.sigma
+            result.sigmas.append(sigma_new)
+        spec = residuals_from_moments(moments, sigma_current, config.residual_mode)
+        tick = time.perf_counter()
+        candidate, mdiag = m_step(spec, reference, model, config.mstep)
+        if timing is not None:
+            timing["m_step_s"] = timing.get("m_step_s", 0.0) + time.perf_counter() - tick
+        norm = update_magnitude(model, candidate, diameter)
+        result.twist_norms.append(norm)
+        if norm < config.twist_tolerance:
+            result.objectives.append(mdiag.objectives[0])
+            result.termination = "converged"
+            break
+        model = candidate
+        result.objectives.append(mdiag.objectives[-1])
+        if result.states is not None:
+            result.states.append(model)
+    result.kinematics = model
+    if timing is not None:
+        timing["iterations"] = result.iterations
+    return result
+
+
 def register(reference: PointCloud, observation: PointCloud, initial_model,
              config: RegistrationConfig | None = None,
              timing: dict | None = None, process_group=None,
@@ -230,6 +290,11 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
     decisions on identical totals.  The returned result is the same on every
     rank."""
     config = config if config is not None else RegistrationConfig()
+    if config.backend != "lattice" or config.gmm.mode != "position":
+        if process_group is not None:
+            raise ValueError("feature / concatenated correspondences and the brute-force "
+                             "backend run on one GPU (no process_group)")
+        return _register_generic(reference, observation, initial_model, config, timing)
     articulated = isinstance(initial_model, ArticulatedTree)
     if isinstance(initial_model, NodeGraph):
         from ._nodegraph import register_nodegraph
@@ -237,9 +302,6 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
                                   process_group)
     if not (isinstance(initial_model, RigidModel) or articulated):
         raise TypeError(f"unsupported kinematic model {type(initial_model).__name__}")
-    if config.backend != "lattice" or config.gmm.mode != "position":
-        raise ValueError("the device EM path runs the lattice backend with position "
-                         "correspondences")
     if articulated:
         from ._articulated import ArticulatedDevicePath, articulated_m_step
         path = ArticulatedDevicePath(reference, observation, config.gmm, config.residual_mode,
