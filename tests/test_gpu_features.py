@@ -92,3 +92,21 @@ def test_feature_registration_golden(fr, case):
     n = min(len(res.objectives), len(g["objectives"])) - 1
     np.testing.assert_allclose(res.objectives[:n], g["objectives"][:n], rtol=1e-5)
     np.testing.assert_allclose(res.inlier_masses[:n], g["inlier_masses"][:n], rtol=1e-5)
+
+
+def test_bruteforce_backend_registration(fr):
+    """backend="bruteforce" (exact Gaussian transform, permutohedral.py:64-86)
+    through register(): same trace as the oracle's exact-transform loop."""
+    model, obs, _ = O.pebble_pair(1200, outlier_ratio=0.05, seed=9)
+    X = model.astype(np.float32).astype(float)
+    Y = obs.astype(np.float32).astype(float)
+    sigma = 0.05 * O.bbox_diameter(X[:1200])
+    tr = O.register_rigid(X, Y, sigma=sigma, outlier_ratio=0.1, max_em_iters=60,
+                          twist_tolerance=1e-4, backend="bruteforce")
+    cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=sigma, outlier_ratio=0.1),
+                                backend="bruteforce", max_em_iters=60, twist_tolerance=1e-4)
+    res = fr.register(fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(), cfg)
+    assert O.rotation_angle(res.kinematics.pose.rotation @ tr["R"].T) <= 1e-4
+    assert np.linalg.norm(res.kinematics.pose.translation - tr["t"]) <= 1e-5 * O.bbox_diameter(X)
+    assert res.termination == tr["termination"]
+    assert abs(res.iterations - tr["iterations"]) <= 1
