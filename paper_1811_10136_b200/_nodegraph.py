@@ -27,6 +27,18 @@ def _sym6_from21(v21):
     return unpack_upper6(v21)
 
 
+_IU6 = np.triu_indices(6)
+
+
+def _sym6_stack(v21) -> np.ndarray:
+    """(n, 21) upper-triangular rows -> (n, 6, 6) symmetric blocks."""
+    v21 = np.asarray(v21, dtype=float).reshape(-1, 21)
+    out = np.zeros((len(v21), 6, 6))
+    out[:, _IU6[0], _IU6[1]] = v21
+    out[:, _IU6[1], _IU6[0]] = v21
+    return out
+
+
 def gather_lists(indices, weights, n_nodes, extra_codes=None):
     """(point, slot) lists for fr_graph_blocks: node lists (code p*K + slot,
     grouped by node, point order) and co-skinned pair lists (point, slot_a |
@@ -177,11 +189,10 @@ def normal_equations(graph, diag, off, path, lambda_reg):
 def normal_equations_from(graph, diag, off, pair_lo, pair_hi, lambda_reg):
     from .mstep import NormalEquations
     n = graph.n_nodes
-    D = np.stack([_sym6_from21(diag[k, :21]) for k in range(n)])
+    D = _sym6_stack(diag[:, :21])
     b = diag[:, 21:27].copy()
-    blocks = {}
-    for i in range(len(pair_lo)):
-        blocks[(int(pair_lo[i]), int(pair_hi[i]))] = _sym6_from21(off[i])
+    offb = _sym6_stack(off[:len(pair_lo), :21]) if len(pair_lo) else np.zeros((0, 6, 6))
+    blocks = {(int(a), int(c)): offb[i] for i, (a, c) in enumerate(zip(pair_lo, pair_hi))}
     if lambda_reg > 0 and len(graph.edges):
         R = np.stack([T.rotation for T in graph.node_transforms])
         t = np.stack([T.translation for T in graph.node_transforms])

@@ -26,6 +26,11 @@ from .kinematics import RigidModel, forward_points
 
 RESIDUAL_MODES = ("point_to_point", "point_to_plane")
 _DENSE_SOLVE_MAX = 360
+# block-sparse systems up to this size are factored densely on the GPU
+# (cuSOLVER Cholesky through torch) instead of SuperLU on the host: the damped
+# normal equations are symmetric positive definite, so the solution agrees to
+# round-off and the escalation path is the same (factorization failure)
+_GPU_DENSE_MAX = 8192
 
 
 @dataclass(frozen=True)
@@ -154,8 +159,37 @@ def assemble_rigid(spec: ResidualSpec, current_positions) -> NormalEquations:
     return NormalEquations(6, b=s[21:27].copy(), A=unpack_upper6(s[:21]))
 
 
+def _dense_blocks(eq: NormalEquations) -> np.ndarray:
+    """Dense A of a 6x6-block system (both triangles), one scatter per block."""
+    P = eq.n_params
+    full = np.zeros((P // 6, 6, P // 6, 6))
+    for (k, l), blk in eq.blocks.items():
+        full[k, :, l, :] += blk
+        if k != l:
+            full[l, :, k, :] += blk.T
+    return full.reshape(P, P)
+
+
+def _gpu_cholesky_solve(A: np.ndarray, lam: float, b: np.ndarray) -> np.ndarray:
+    import torch
+    dev = _lib.device()
+    At = torch.from_numpy(A).to(dev)
+    At.diagonal().add_(lam)
+    L, info = torch.linalg.cholesky_ex(At)
+    if int(info.item()) != 0:
+        raise scipy.linalg.LinAlgError("normal equations not positive definite")
+    x = torch.cholesky_solve(torch.from_numpy(np.ascontiguousarray(b)).to(dev)[:, None], L)
+    sol = x[:, 0].cpu().numpy()
+    if not np.all(np.isfinite(sol)):
+        raise scipy.linalg.LinAlgError("factorization produced non-finite values")
+    return sol
+
+
 def _factor_solve(eq: NormalEquations, lam: float, method: str) -> np.ndarray:
     """mstep.py:317-345"""
+    if (method == "auto" and eq.A is None and eq.blocks is not None
+            and _DENSE_SOLVE_MAX < eq.n_params <= _GPU_DENSE_MAX):
+        return _gpu_cholesky_solve(_dense_blocks(eq), lam, eq.b)
     sparse = method == "sparse" or (method == "auto" and eq.A is None
                                     and eq.n_params > _DENSE_SOLVE_MAX)
     if sparse and eq.blocks is not None:
