@@ -164,8 +164,7 @@ def regularizer_objective(graph, lambda_reg: float) -> float:
     (mstep.py:390-401)."""
     if lambda_reg <= 0 or not len(graph.edges):
         return 0.0
-    R = np.stack([T.rotation for T in graph.node_transforms])
-    t = np.stack([T.translation for T in graph.node_transforms])
+    R, t = graph.node_rotations, graph.node_translations
     k_ids, l_ids = graph.edges[:, 0], graph.edges[:, 1]
     total = 0.0
     for p in (graph.node_positions[l_ids], graph.node_positions[k_ids]):
@@ -194,8 +193,7 @@ def normal_equations_from(graph, diag, off, pair_lo, pair_hi, lambda_reg):
     offb = _sym6_stack(off[:len(pair_lo), :21]) if len(pair_lo) else np.zeros((0, 6, 6))
     blocks = {(int(a), int(c)): offb[i] for i, (a, c) in enumerate(zip(pair_lo, pair_hi))}
     if lambda_reg > 0 and len(graph.edges):
-        R = np.stack([T.rotation for T in graph.node_transforms])
-        t = np.stack([T.translation for T in graph.node_transforms])
+        R, t = graph.node_rotations, graph.node_translations
         root = np.sqrt(lambda_reg)
         k_ids, l_ids = graph.edges[:, 0], graph.edges[:, 1]
         for p in (graph.node_positions[l_ids], graph.node_positions[k_ids]):

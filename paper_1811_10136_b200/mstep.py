@@ -160,14 +160,15 @@ def assemble_rigid(spec: ResidualSpec, current_positions) -> NormalEquations:
 
 
 def _dense_blocks(eq: NormalEquations) -> np.ndarray:
-    """Dense A of a 6x6-block system (both triangles), one scatter per block."""
-    P = eq.n_params
-    full = np.zeros((P // 6, 6, P // 6, 6))
-    for (k, l), blk in eq.blocks.items():
-        full[k, :, l, :] += blk
-        if k != l:
-            full[l, :, k, :] += blk.T
-    return full.reshape(P, P)
+    """Dense A of a 6x6-block system (both triangles), one scatter."""
+    P, nb = eq.n_params, eq.n_params // 6
+    keys = np.array(list(eq.blocks.keys()), dtype=np.int64).reshape(-1, 2)
+    vals = np.stack(list(eq.blocks.values())) if len(keys) else np.zeros((0, 6, 6))
+    F = np.zeros((nb, nb, 6, 6))
+    np.add.at(F, (keys[:, 0], keys[:, 1]), vals)
+    off = keys[:, 0] != keys[:, 1]
+    np.add.at(F, (keys[off, 1], keys[off, 0]), np.transpose(vals[off], (0, 2, 1)))
+    return F.transpose(0, 2, 1, 3).reshape(P, P)
 
 
 def _gpu_cholesky_solve(A: np.ndarray, lam: float, b: np.ndarray) -> np.ndarray:
