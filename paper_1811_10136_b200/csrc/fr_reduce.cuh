@@ -61,6 +61,6 @@ static inline int sm_count() {
 static inline int pass_grid() { return 2 * sm_count(); }
 static inline int pass_grid_dense() { return 3 * sm_count(); }
 // scratch rows every pass grid fits in
-static inline int pass_grid_max() { return 3 * sm_count(); }
+static inline int pass_grid_max() { return 4 * sm_count(); }
 
 }  // namespace fr

@@ -698,9 +698,32 @@ __device__ __forceinline__ void grid_point(float nx, float ny, float nz, bool va
     a.q2 = fmaf(wr2, r2, a.q2);
 }
 
-// PTS model points per thread per ring stage (1: 3 CTAs/SM; 2: 2 CTAs/SM)
-template <bool DEV, int PTS>
-__global__ void __launch_bounds__(kPassThreads, PTS == 1 ? 3 : 2)
+// the warp's float32 partials folded into its float64 accumulators: a
+// butterfly reduce-scatter (5 shuffle rounds, 31 adds per lane) leaves lane c
+// holding the warp sum of statistic c, which it adds into wacc[c].  Fixed
+// order, hence deterministic; shared memory is 25 doubles per warp instead of
+// per thread, so it no longer caps the CTAs per SM.
+__device__ __forceinline__ void grid_warp_fold(const GridAcc &a, double *wacc) {
+    const int lane = threadIdx.x & 31;
+    float v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = c < kP2PtBase ? a.col(c) : 0.0f;
+#pragma unroll
+    for (int n = 32, off = 16; off >= 1; n >>= 1, off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const float send = upper ? v[i] : v[i + n / 2];
+            const float keep = upper ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    if (lane < kP2PtBase) wacc[lane] += (double)v[0];
+}
+
+// PTS model points per thread per ring stage, MINB CTAs per SM
+template <bool DEV, int PTS, int MINB>
+__global__ void __launch_bounds__(kPassThreads, MINB)
 k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
                   const int *done, DenseSliceF dg, double *__restrict__ partials) {
     constexpr int NA = kP2PtBase;
@@ -743,10 +766,10 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
         g.H = H;
     }
     for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, dg.s0, dg.s1);
-    extern __shared__ double sacc[];   // [NA][kPassThreads]
-#pragma unroll
-    for (int q = 0; q < NA; ++q) sacc[q * kPassThreads + threadIdx.x] = 0.0;
+    __shared__ double wacc[kPassThreads / 32][NA];   // per-warp float64 accumulators
+    if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
     __syncthreads();
+    double *my_wacc = wacc[threadIdx.x >> 5];
     GridAcc a;
     a.zero();
     int fold = 0;
@@ -781,22 +804,25 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
 #pragma unroll
         for (int k = 0; k < PTS; ++k) grid_point(px[k], py[k], pz[k], ok[k], g, tab, dg, a);
         fold += PTS;
-        if (fold >= kGridFold) {
-#pragma unroll
-            for (int c = 0; c < NA; ++c) sacc[c * kPassThreads + threadIdx.x] += (double)a.col(c);
+        if (fold >= kGridFold) {       // warp-uniform: every lane runs the same loop
+            grid_warp_fold(a, my_wacc);
             a.zero();
             fold = 0;
         }
     }
-    double acc[NA];
+    grid_warp_fold(a, my_wacc);
+    __syncthreads();
+    if (threadIdx.x < NA) {
+        double v = 0.0;
 #pragma unroll
-    for (int c = 0; c < NA; ++c) acc[c] = sacc[c * kPassThreads + threadIdx.x] + (double)a.col(c);
-    block_reduce_store<NA>(acc, partials + (long long)blockIdx.x * NA);
+        for (int w = 0; w < kPassThreads / 32; ++w) v += wacc[w][threadIdx.x];
+        partials[(long long)blockIdx.x * NA + threadIdx.x] = v;
+    }
 }
 
 // points per thread per ring stage of the dense-grid pass: 2 (two
-// independent chains per thread, shared parameter loads; 8 % faster than 1 at
-// 16.8M points, 2 CTAs/SM); FR_GRID_PTS=1 selects the 3-CTA single-point form
+// independent chains per thread, shared parameter loads); FR_GRID_PTS=1
+// selects the single-point form (4 CTAs/SM)
 static int grid_pts() {
     static int pts = 0;
     if (!pts) {
@@ -806,20 +832,25 @@ static int grid_pts() {
     return pts;
 }
 
+// CTAs per SM of the two-point dense-grid pass (FR_GRID_MINB=2|3).  2 (96
+// registers, no spills) measured 142.5 us at 16.8M points; 3 caps registers at
+// 80 and spills 144 B per thread inside the loop (177.5 us); the one-point
+// form at 4 CTAs (64 registers) 148 us
+static int grid_minb() {
+    static int b = 0;
+    if (!b) {
+        const char *e = getenv("FR_GRID_MINB");
+        b = (e && e[0] == '3') ? 3 : 2;
+    }
+    return b;
+}
+
 static int set_f32_smem() {
     static bool done = false;
     if (!done) {
         FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
         FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_f32<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<true, 1>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<false, 1>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<true, 2>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
-        FR_CUDA(cudaFuncSetAttribute(k_rigid_pass_grid<false, 2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem));
         done = true;
     }
@@ -1357,11 +1388,12 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         const DenseSliceF dg = lat->dense;
         if (lat->dcells != nullptr) {
             const int pts = grid_pts();
-            const int g3 = pts == 2 ? pass_grid() : pass_grid_dense();
-#define FR_GRID(DEV, P) \
-    k_rigid_pass_grid<DEV, P><<<g3, kPassThreads, kF32Smem, s>>>(ref, m, k, kd, done, dg, scratch)
-            if (pts == 2) { if (dev) FR_GRID(true, 2); else FR_GRID(false, 2); }
-            else { if (dev) FR_GRID(true, 1); else FR_GRID(false, 1); }
+            const int g3 = pts == 1 ? 4 * sm_count() : grid_minb() * sm_count();
+#define FR_GRID(DEV, P, B) \
+    k_rigid_pass_grid<DEV, P, B><<<g3, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch)
+            if (pts == 1) { if (dev) FR_GRID(true, 1, 4); else FR_GRID(false, 1, 4); }
+            else if (grid_minb() == 3) { if (dev) FR_GRID(true, 2, 3); else FR_GRID(false, 2, 3); }
+            else { if (dev) FR_GRID(true, 2, 2); else FR_GRID(false, 2, 2); }
 #undef FR_GRID
             FR_CHECK_LAUNCH();
             k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g3, kP2PtBase, sums, done);
