@@ -820,14 +820,15 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
     }
 }
 
-// points per thread per ring stage of the dense-grid pass: 2 (two
-// independent chains per thread, shared parameter loads); FR_GRID_PTS=1
-// selects the single-point form (4 CTAs/SM)
+// points per thread per ring stage of the dense-grid pass (FR_GRID_PTS):
+// 3 (default: three independent chains per thread sharing the parameter
+// loads, 118 registers, 2 CTAs/SM: 139.6 us at 16.8M points), 2 (96
+// registers: 142.5 us) or 1 (4 CTAs/SM: 148 us)
 static int grid_pts() {
     static int pts = 0;
     if (!pts) {
         const char *e = getenv("FR_GRID_PTS");
-        pts = (e && e[0] == '1') ? 1 : 2;
+        pts = (e && e[0] == '1') ? 1 : ((e && e[0] == '2') ? 2 : 3);
     }
     return pts;
 }
@@ -1388,11 +1389,12 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         const DenseSliceF dg = lat->dense;
         if (lat->dcells != nullptr) {
             const int pts = grid_pts();
-            const int g3 = pts == 1 ? 4 * sm_count() : grid_minb() * sm_count();
+            const int g3 = pts == 1 ? 4 * sm_count() : (pts == 3 ? 2 : grid_minb()) * sm_count();
 #define FR_GRID(DEV, P, B) \
     k_rigid_pass_grid<DEV, P, B><<<g3, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch)
             if (pts == 1) { if (dev) FR_GRID(true, 1, 4); else FR_GRID(false, 1, 4); }
             else if (grid_minb() == 3) { if (dev) FR_GRID(true, 2, 3); else FR_GRID(false, 2, 3); }
+            else if (pts == 3) { if (dev) FR_GRID(true, 3, 2); else FR_GRID(false, 3, 2); }
             else { if (dev) FR_GRID(true, 2, 2); else FR_GRID(false, 2, 2); }
 #undef FR_GRID
             FR_CHECK_LAUNCH();
