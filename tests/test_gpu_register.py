@@ -246,3 +246,30 @@ def test_float32_pass_matches_exact(fr, dense, monkeypatch):
         assert ex[0] > 50.0
         np.testing.assert_array_less(np.abs(f32 - ex) / (ex[0] * L ** k), 1e-5)
 
+
+
+@pytest.mark.parametrize("m", [1, 7, 255, 256, 769, 3001, 70001])
+def test_grid_pass_odd_sizes(fr, m, monkeypatch):
+    """Chunk / ring-stage boundaries of the dense-grid pass: any model size
+    gives the exact pass's statistics (float32 accuracy), and a point count
+    smaller than one stage per block leaves most blocks empty."""
+    import paper_1811_10136_b200._rigid as rg
+    model, obs, _ = O.pebble_pair(max(m, 2000), outlier_ratio=0.05, seed=21)
+    X = model[:m].astype(np.float32).astype(float)
+    Y = obs.astype(np.float32).astype(float)
+    sigma = 0.05 * O.bbox_diameter(model[:2000])
+    path = rg.RigidDevicePath(fr.PointCloud(X), fr.PointCloud(Y),
+                              fr.GmmConfig(sigma=sigma, outlier_ratio=0.1), "point_to_point")
+    assert path.lattice.dense_cells > 0
+    R = O.rotation_about_axis([0.2, 1.0, -0.4], 0.1)
+    t = np.array([0.002, -0.001, 0.003])
+    monkeypatch.setattr(rg, "FAST_QUERY", False)
+    monkeypatch.setattr(rg, "F32_POINTS", False)
+    ex = path.run_pass(R, t).copy()
+    monkeypatch.setattr(rg, "FAST_QUERY", True)
+    monkeypatch.setattr(rg, "F32_POINTS", True)
+    f32 = path.run_pass(R, t).copy()
+    L = float(np.sqrt(((X - X.mean(axis=0)) ** 2).sum(axis=1).mean())) + 1e-3
+    k = np.array([0, 1, 1, 1, 2, 2, 2, 2, 2, 2, 1, 1, 1] + [2] * 9 + [2, 2, 2])
+    scale = max(ex[0], 1.0) * L ** k
+    np.testing.assert_array_less(np.abs(f32 - ex) / scale, 2e-5)
