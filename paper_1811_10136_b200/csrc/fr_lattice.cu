@@ -141,7 +141,7 @@ struct PointSrc {
 template <int D, class Src>
 __global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash h,
                                 unsigned sentinel, unsigned *entry_slot, unsigned *entry_idx,
-                                double *entry_bary, unsigned long long *counters) {
+                                double *entry_bary, double *contrib, unsigned long long *counters) {
     long long stride = (long long)gridDim.x * blockDim.x;
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
         double f[D];
@@ -167,6 +167,11 @@ __global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash
             entry_slot[e] = slot;
             entry_idx[e] = (unsigned)e;
             entry_bary[e] = s.bary[l];
+            // the entry's products bary * value (NumPy's single rounding), laid
+            // out as one row so the site sums gather one row per entry
+            if (contrib && slot != sentinel)
+                for (int cc = 0; cc < src.nv; ++cc)
+                    contrib[e * src.nv + cc] = __dmul_rn(s.bary[l], src.value(p, cc));
         }
     }
 }
@@ -180,13 +185,22 @@ __global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash
 // entries at C5 sizes) is then bound by its one float64 add chain per column,
 // not by the latency of its random gathers.
 constexpr int kSegBlock = 256;
+
+// the per-entry product rows take E * nv doubles of pool memory: formed in the
+// entries kernel when that stays within 8 GiB, else in the site-sum kernel
+static inline bool contrib_fits(long long E, int nv) {
+    return (unsigned long long)E * (unsigned long long)nv * 8ull <= (8ull << 30);
+}
 constexpr int kSegStages = 3;
 
+// contrib != null: the entries' products were formed by the entries kernel
+// (point-coalesced) and are gathered as rows; else formed here from the
+// point values (random gathers of bary and coordinates)
 template <int D, class Src>
 __global__ void __launch_bounds__(kSegBlock)
 k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int *run_cnt,
-               const unsigned *sorted_idx, const double *entry_bary, unsigned sentinel, int nv,
-               double *run_vals) {
+               const unsigned *sorted_idx, const double *entry_bary, const double *contrib,
+               unsigned sentinel, int nv, double *run_vals) {
     extern __shared__ double ring[];   // [kSegStages][kSegBlock][nv]
     const int r = blockIdx.x;
     if (run_slot && run_slot[r] == sentinel) return;   // (null: no sentinel runs)
@@ -197,10 +211,15 @@ k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int 
         const int j = ch * kSegBlock + t;
         if (j < cnt) {
             const unsigned e = sorted_idx[beg + j];
-            const double b = entry_bary[e];
-            const long long p = e / (D + 1);
             double *row = ring + ((size_t)(ch % kSegStages) * kSegBlock + t) * nv;
-            for (int c = 0; c < nv; ++c) row[c] = __dmul_rn(b, src.value(p, c));
+            if (contrib) {
+                const double *cr = contrib + (size_t)e * nv;
+                for (int c = 0; c < nv; ++c) row[c] = __ldg(cr + c);
+            } else {
+                const double b = entry_bary[e];
+                const long long p = e / (D + 1);
+                for (int c = 0; c < nv; ++c) row[c] = __dmul_rn(b, src.value(p, c));
+            }
         }
     };
     for (int st = 0; st < kSegStages - 1 && st < chunks; ++st) stage(st);
@@ -608,12 +627,13 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     }
     Scratch sc(s);
     unsigned *entry_slot, *entry_idx, *sorted_slot, *sorted_idx;
-    double *entry_bary;
+    double *entry_bary, *contrib = nullptr;
     FR_TRY(sc.get(&entry_slot, E));
     FR_TRY(sc.get(&entry_idx, E));
     FR_TRY(sc.get(&sorted_slot, E));
     FR_TRY(sc.get(&sorted_idx, E));
     FR_TRY(sc.get(&entry_bary, E));
+    if (contrib_fits(E, nv)) FR_TRY(sc.get(&contrib, (size_t)E * nv));
     // hash sized for the unique-key count; grown x4 on overflow
     unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
     unsigned long long hc[3];
@@ -623,7 +643,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
         k_splat_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, n, lat->c, h, (unsigned)cap,
                                                             entry_slot, entry_idx, entry_bary,
-                                                            lat->d_counters);
+                                                            contrib, lat->d_counters);
         FR_CHECK_LAUNCH();
         FR_TRY(read_counters(lat, s, hc));
         bool full = (hc[2] & 2ull) || hc[0] * 2 > cap;
@@ -676,8 +696,8 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (nruns > 0) {
             k_splat_segsum<D, Src><<<nruns, kSegBlock, smem, s>>>(
-                src, run_slot, run_off, run_cnt, sorted_idx, entry_bary, (unsigned)cap, nv,
-                run_vals);
+                src, run_slot, run_off, run_cnt, sorted_idx, entry_bary, contrib, (unsigned)cap,
+                nv, run_vals);
             FR_CHECK_LAUNCH();
         }
         k_run_live<<<grid_for(nruns), 256, 0, s>>>(nruns, run_slot, (unsigned)cap, run_vals, nv,

@@ -111,7 +111,7 @@ __global__ void k_wide_range(Src src, long long n, LatticeConsts c, int *mn, int
 template <int D, class Src>
 __global__ void k_wide_entries(Src src, long long n, LatticeConsts c, WideCodec w,
                                unsigned long long *kh, unsigned long long *kl, unsigned *idx,
-                               double *bary, unsigned long long *flag) {
+                               double *bary, double *contrib, unsigned long long *flag) {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     double f[D];
@@ -136,6 +136,9 @@ __global__ void k_wide_entries(Src src, long long n, LatticeConsts c, WideCodec 
         kl[e] = lw;
         idx[e] = (unsigned)e;
         bary[e] = s.bary[l];
+        if (contrib && h != kWideSentinel)
+            for (int cc = 0; cc < src.nv; ++cc)
+                contrib[e * src.nv + cc] = __dmul_rn(s.bary[l], src.value(p, cc));
     }
 }
 
@@ -333,8 +336,10 @@ static int wide_splat(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_TRY(sc.get(&kl, E));
     FR_TRY(sc.get(&eidx, E));
     FR_TRY(sc.get(&ebary, E));
+    double *contrib = nullptr;
+    if (contrib_fits(E, nv)) FR_TRY(sc.get(&contrib, (size_t)E * nv));
     k_wide_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, n, lat->c, w, kh, kl, eidx, ebary,
-                                                        flag);
+                                                        contrib, flag);
     FR_CHECK_LAUNCH();
     unsigned long long *skh, *skl;
     unsigned *perm;
@@ -377,7 +382,7 @@ static int wide_splat(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_CUDA(cudaFuncSetAttribute(k_splat_segsum<D, Src>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_splat_segsum<D, Src><<<R, kSegBlock, smem, s>>>(src, nullptr, run_off, run_cnt, perm, ebary,
-                                                      0u, nv, run_vals);
+                                                      contrib, 0u, nv, run_vals);
     FR_CHECK_LAUNCH();
     // live runs (any non-zero value) -> the sorted site table
     unsigned char *live;
