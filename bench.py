@@ -432,7 +432,7 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
             "data": "synthetic",
             "config": {"workload": f"C5 rigid pt2pt pebble, {args.points} clean model pts/GPU "
                                    "+ 5% outliers; observation {0} pts + 5% (BASELINE "

@@ -502,15 +502,18 @@ __device__ __forceinline__ void cp_async4(float *smem, const float *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// stage this thread's PTS points of one ring stage: 32-bit offsets j from the
+// chunk's three plane pointers (a block's chunk is < 2^31 points)
 template <int PTS>
-__device__ __forceinline__ void ring_issue_pts(float (*slot)[3][kPassThreads], const float *ref,
-                                               long long m, long long base, long long end) {
+__device__ __forceinline__ void ring_issue_pts(float (*slot)[3][kPassThreads], const float *p0,
+                                               const float *p1, const float *p2, int j, int cnt) {
 #pragma unroll
     for (int k = 0; k < PTS; ++k) {
-        const long long q = base + (long long)k * kPassThreads + threadIdx.x;
-        if (q < end) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) cp_async4(&slot[k][c][threadIdx.x], ref + c * m + q);
+        const int q = j + k * kPassThreads + (int)threadIdx.x;
+        if (q < cnt) {
+            cp_async4(&slot[k][0][threadIdx.x], p0 + q);
+            cp_async4(&slot[k][1][threadIdx.x], p1 + q);
+            cp_async4(&slot[k][2][threadIdx.x], p2 + q);
         }
     }
     cp_async_commit();
@@ -779,15 +782,15 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
     // slots, so the ring needs no block barrier
     const long long chunk = ((m + gridDim.x - 1) / gridDim.x + 31) & ~31ll;
     const long long beg = (long long)blockIdx.x * chunk;
-    const long long end = min(beg + chunk, m);
-    constexpr long long SP = (long long)PTS * kPassThreads;   // points per ring stage
+    const int cnt = (int)max(0ll, min(beg + chunk, m) - beg);
+    const float *p0 = ref + min(beg, m), *p1 = p0 + m, *p2 = p1 + m;
+    constexpr int SP = PTS * kPassThreads;   // points per ring stage
 #pragma unroll
-    for (int st = 0; st < kGridStages - 1; ++st)
-        ring_issue_pts<PTS>(ring[st], ref, m, beg + st * SP, end);
+    for (int st = 0; st < kGridStages - 1; ++st) ring_issue_pts<PTS>(ring[st], p0, p1, p2, st * SP, cnt);
     int stage = 0;
-    for (long long base = beg; base < end; base += SP) {
-        ring_issue_pts<PTS>(ring[stage == 0 ? kGridStages - 1 : stage - 1], ref, m,
-                            base + (kGridStages - 1) * SP, end);
+    for (int j = 0; j < cnt; j += SP) {
+        ring_issue_pts<PTS>(ring[stage == 0 ? kGridStages - 1 : stage - 1], p0, p1, p2,
+                            j + (kGridStages - 1) * SP, cnt);
         cp_async_wait<kGridStages - 1>();
         float px[PTS], py[PTS], pz[PTS];
         bool ok[PTS];
@@ -795,7 +798,7 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
         for (int k = 0; k < PTS; ++k) {
             // a slot past the chunk end holds stale shared memory (maybe NaN,
             // which w = 0 would not cancel): feed it finite coordinates
-            ok[k] = base + k * kPassThreads + threadIdx.x < end;
+            ok[k] = j + k * kPassThreads + (int)threadIdx.x < cnt;
             px[k] = ok[k] ? ring[stage][k][0][threadIdx.x] : 0.0f;
             py[k] = ok[k] ? ring[stage][k][1][threadIdx.x] : 0.0f;
             pz[k] = ok[k] ? ring[stage][k][2][threadIdx.x] : 0.0f;
