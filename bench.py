@@ -52,10 +52,11 @@ def parse():
                     help="observation points of the CPU-baseline lattice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--mode", default="fixed", choices=["fixed", "sigma"],
+    ap.add_argument("--mode", default="fixed", choices=["fixed", "sigma", "batch"],
                     help="fixed: the headline fixed-sigma EM (default); sigma: the "
                          "sigma-re-estimating EM, lattice rebuilt every iteration "
-                         "(SURVEY.md 8(f) rank 1; single GPU)")
+                         "(SURVEY.md 8(f) rank 1; single GPU); batch: the reference's "
+                         "30-trial C1 protocol through register_batch (8(f) rank 4)")
     return ap.parse_args()
 
 
@@ -507,12 +508,57 @@ def run_sigma(args):
     }), flush=True)
 
 
+def run_batch(args):
+    """--mode batch: the reference's C1 bench protocol (bench.py:92-130 there:
+    30 seeded trials of a 10k-point pebble + 5 % outliers, sigma 5 % of the
+    clean diagonal, <= 250 iterations, tolerance 2e-4) -- sequential register()
+    calls vs one register_batch() call with concurrent streams."""
+    import torch
+
+    import paper_1811_10136_b200 as fr
+    from oracle import filterreg_oracle as O
+    torch.cuda.set_device(0)
+    problems = []
+    for trial in range(30):
+        model, obs, _ = O.pebble_pair(10000, outlier_ratio=0.05, seed=trial)
+        X = model.astype(np.float32).astype(float)
+        Y = obs.astype(np.float32).astype(float)
+        sigma = 0.05 * O.bbox_diameter(X[:10000])
+        cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=sigma, outlier_ratio=0.1),
+                                    max_em_iters=250, twist_tolerance=2e-4)
+        problems.append((fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(), cfg))
+    fr.register_batch(problems[:8], max_concurrent=8)      # warm-up (pools, graphs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    seq = [fr.register(*p) for p in problems]
+    torch.cuda.synchronize()
+    t_seq = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    bat = fr.register_batch(problems, max_concurrent=8)
+    torch.cuda.synchronize()
+    t_bat = time.perf_counter() - t0
+    same = all(np.array_equal(a.kinematics.pose.matrix(), b.kinematics.pose.matrix())
+               for a, b in zip(seq, bat))
+    iters = sum(r.iterations for r in bat)
+    print(json.dumps({
+        "metric": "registrations/s (C1 bench protocol, 30 trials)", "value": 30 / t_bat,
+        "unit": "registrations/s", "n_gpus": 1, "higher_is_better": True, "mode": "batch",
+        "data": "synthetic", "dtype": "f32+f64",
+        "config": {"workload": "C1 rigid pt2pt pebble 10k + 5% outliers, 30 seeded trials, "
+                               "<= 250 iterations, tol 2e-4", "max_concurrent": 8},
+        "batched_s": t_bat, "sequential_s": t_seq, "speedup_vs_sequential": t_seq / t_bat,
+        "em_iterations_total": iters, "identical_to_sequential": bool(same),
+    }), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
     elif args.mode == "sigma":
         run_sigma(args)
+    elif args.mode == "batch":
+        run_batch(args)
     else:
         run_b200(args)
 

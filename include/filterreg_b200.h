@@ -62,8 +62,11 @@ const char *fr_last_error(void);
 /* ---- permutohedral lattice (permutohedral.py:140-345) ------------------- */
 
 /* PermutohedralLattice(dim, sigma) (permutohedral.py:147-167); sigma has dim
- * host doubles.  Only dim == 3 (position correspondences) is compiled in this
- * build; other dims return FR_EINVAL. */
+ * host doubles, dim in 1..12 (d <= 3: hashed 63-bit keys; 4..12: sorted
+ * 128-bit keys).  Destroy is stream-ordered: the buffers return to the device
+ * pool behind the work enqueued on the stream of the last build call
+ * (splat / blur); callers that slice from other streams synchronise those
+ * streams before destroying. */
 int fr_lattice_create(int dim, const double *sigma, fr_lattice **out);
 int fr_lattice_destroy(fr_lattice *lat);
 

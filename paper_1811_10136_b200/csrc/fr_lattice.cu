@@ -1183,9 +1183,9 @@ int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
 
 int fr_lattice_destroy(fr_lattice *lat) {
     if (!lat) return FR_OK;
-    // a blurred lattice may have been sliced from any stream: finish all work
-    // before its buffers return to the pool (cudaFree's implicit guarantee)
-    cudaDeviceSynchronize();
+    // stream-ordered: the buffers return to the pool behind the work already
+    // enqueued on the lattice's build stream (callers that read the lattice
+    // from other streams synchronise those first -- include/filterreg_b200.h)
     free_build(lat);
     free_slice(lat);
     pool_free(lat, lat->d_counters);

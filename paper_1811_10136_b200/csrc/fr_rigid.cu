@@ -1451,6 +1451,7 @@ struct fr_rigid_em {
     double *d_traces = nullptr;   // [3][max_iters]: objectives, twist norms, inlier masses
     cudaGraphExec_t graph = nullptr;
     int graph_iters = 0;
+    cudaStream_t stream = nullptr;   // stream of the last call (destroy orders behind it)
 };
 
 using namespace fr;
@@ -1695,11 +1696,13 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
 
 int fr_rigid_em_destroy(fr_rigid_em *em) {
     if (!em) return FR_OK;
+    // the loop may still run on the caller's stream: wait for that stream only
+    // (other streams' independent registrations keep running)
+    cudaStreamSynchronize(em->stream);
     if (em->graph) cudaGraphExecDestroy(em->graph);
-    cudaDeviceSynchronize();   // the loop may still run on the caller's stream
     for (void *p : {(void *)em->d_em, (void *)em->d_sums, (void *)em->d_scratch,
                     (void *)em->d_traces})
-        if (p) cudaFreeAsync(p, 0);
+        if (p) cudaFreeAsync(p, em->stream);
     delete em;
     return FR_OK;
 }
@@ -1740,6 +1743,7 @@ int fr_rigid_em_pass(fr_rigid_em *em, void *stream) {
         set_error("null EM object");
         return FR_EINVAL;
     }
+    em->stream = (cudaStream_t)stream;
     return em_pass(em, (cudaStream_t)stream);
 }
 
@@ -1748,6 +1752,7 @@ int fr_rigid_em_solve(fr_rigid_em *em, void *stream) {
         set_error("null EM object");
         return FR_EINVAL;
     }
+    em->stream = (cudaStream_t)stream;
     return em_solve(em, (cudaStream_t)stream);
 }
 
@@ -1758,6 +1763,7 @@ int fr_rigid_em_enqueue(fr_rigid_em *em, int n, void *stream) {
         set_error("invalid enqueue arguments");
         return FR_EINVAL;
     }
+    em->stream = (cudaStream_t)stream;
     cudaStream_t s = (cudaStream_t)stream;
     constexpr int kGraphIters = 8;
     if (!em->graph) {

@@ -368,3 +368,59 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
     if timing is not None:
         timing["iterations"] = result.iterations
     return result
+
+
+def register_batch(problems, config: RegistrationConfig | None = None,
+                   max_concurrent: int = 8) -> list:
+    """Independent registrations run concurrently on one GPU (the batched
+    multi-problem driver of SURVEY.md 8(f) rank 4; the reference runs bench
+    trials one after another, bench.py:132-159).
+
+    `problems` holds (reference, observation, initial_model) triples, or
+    (reference, observation, initial_model, config) to override `config`.
+    Up to `max_concurrent` worker threads each own a CUDA stream and run
+    `register` on it; the native calls release the GIL, so one problem's
+    kernels overlap another's host work and kernels.  Problems are replicas:
+    no collectives, no shared device state.  Results come back in input order
+    and are identical to running each problem alone (every registration is
+    deterministic)."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+    problems = list(problems)
+    if not problems:
+        return []
+    workers = max(1, min(int(max_concurrent), len(problems)))
+    streams = _batch_streams(workers)
+    slot = threading.local()
+    counter = iter(range(workers))
+    lock = threading.Lock()
+
+    def run(item):
+        ref, obs, model = item[:3]
+        cfg = item[3] if len(item) > 3 else config
+        if getattr(slot, "stream", None) is None:
+            with lock:
+                slot.stream = streams[next(counter)]
+        with torch.cuda.stream(slot.stream):
+            res = register(ref, obs, model, cfg)
+            slot.stream.synchronize()
+        return res
+
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        return list(pool.map(run, problems))
+
+
+_STREAMS: dict = {}
+
+
+def _batch_streams(n: int):
+    """Worker streams kept for the process: torch's caching allocator pools
+    blocks per stream, so reusing the streams keeps later batches warm."""
+    import torch
+    dev = torch.cuda.current_device()
+    pool = _STREAMS.setdefault(dev, [])
+    while len(pool) < n:
+        pool.append(torch.cuda.Stream())
+    return pool[:n]
