@@ -70,6 +70,12 @@ const char *fr_last_error(void);
 int fr_lattice_create(int dim, const double *sigma, fr_lattice **out);
 int fr_lattice_destroy(fr_lattice *lat);
 
+/* Re-bind the stream the lattice's stream-ordered frees (destroy, rebuild) go
+ * behind -- for a lattice built on a side stream and then used on another
+ * (the build must be complete, e.g. that stream synchronised).  Engine-
+ * internal lifetime control; no reference counterpart. */
+int fr_lattice_set_stream(fr_lattice *lat, void *stream);
+
 /* PermutohedralLattice.splat(features, values) (permutohedral.py:219-251):
  * d_features n x dim row-major float64, d_values n x nv row-major float64.
  * Deterministic: per-site sums run in flat (point, vertex) order, bit-identical

@@ -151,6 +151,22 @@ def upload_soa(points, dev):
     return soa
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream():
+    """The observation-side setup stream of this thread / device, kept for the
+    process (torch's caching allocator pools blocks per stream)."""
+    import threading
+
+    import torch
+    key = (torch.cuda.current_device(), threading.get_ident())
+    st = _SIDE_STREAMS.get(key)
+    if st is None:
+        st = _SIDE_STREAMS[key] = torch.cuda.Stream()
+    return st
+
+
 class _SetupClock:
     """Per-phase wall times of the device-path setup when FR_PROFILE_SETUP=1
     (synchronising between phases); a no-op otherwise."""
@@ -199,6 +215,24 @@ class RigidDevicePath:
         self.gmm = gmm
         self.group = process_group
         lap = _SetupClock()
+        if observation.normals is None and residual_mode == "point_to_plane":
+            raise ValueError("observation cloud has no normals")
+        # the observation side (upload, splat, blur: host round trips) runs in
+        # a worker thread on its own stream while this thread uploads, reduces
+        # and Morton-sorts the model cloud
+        from concurrent.futures import ThreadPoolExecutor
+        normals = residual_mode == "point_to_plane"
+        self.with_sigma = bool(gmm.update_sigma)
+        self.value_mode = (_lib.FR_VALUES_M2 if self.with_sigma else 0) | \
+            (_lib.FR_VALUES_NORMALS if normals else 0)
+        self.m2_col = 4 if self.with_sigma else -1
+        self.normal_col = (5 if self.with_sigma else 4) if normals else -1
+        self.lattice = None
+        self.sigma = None
+        main_stream = torch.cuda.current_stream()
+        side = _side_stream()
+        pool = ThreadPoolExecutor(max_workers=1)
+        obs_job = pool.submit(self._build_observation, observation, gmm, residual_mode, side)
         self.ref = upload_soa(reference.positions, self.dev)
         self.M = self.ref.shape[1]
         lap("upload_ref")
@@ -219,19 +253,6 @@ class RigidDevicePath:
             _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self.ref), self.M, 3, None,
                                                       _lib.stream_handle()))
         lap("morton_sort")
-        self.obs = upload_soa(observation.positions, self.dev)
-        self.N = self.obs.shape[1]
-        lap("upload_obs")
-        self.obs_n = None
-        if self.mode == _lib.FR_POINT_TO_PLANE:
-            if observation.normals is None:
-                raise ValueError("observation cloud has no normals")
-            self.obs_n = upload_soa(observation.normals, self.dev)
-        self.with_sigma = bool(gmm.update_sigma)
-        self.value_mode = (_lib.FR_VALUES_M2 if self.with_sigma else 0) | \
-            (_lib.FR_VALUES_NORMALS if self.obs_n is not None else 0)
-        self.m2_col = 4 if self.with_sigma else -1
-        self.normal_col = (5 if self.with_sigma else 4) if self.obs_n is not None else -1
         self.width = self.lib.fr_rigid_pass_width(self.mode, int(self.with_sigma))
         f64 = dict(dtype=torch.float64, device=self.dev)
         self.sums = torch.empty(max(self.width, 16), **f64)
@@ -240,12 +261,35 @@ class RigidDevicePath:
         self.host = torch.empty(max(self.width, 16), dtype=torch.float64, pin_memory=True)
         self.wtn = torch.empty((7, self.M), dtype=torch.float32, device=self.dev) \
             if self.mode == _lib.FR_POINT_TO_PLANE else None
-        self.lattice = None
-        self.sigma = None
         lap("buffers")
-        self.build(gmm.sigma)
-        lap("lattice_build")
+        try:
+            obs_job.result()          # the side stream is synchronised inside
+        finally:
+            pool.shutdown(wait=True)
+        # later work (passes, rebuilds, frees) is ordered on the caller's stream
+        self.obs.record_stream(main_stream)
+        if self.obs_n is not None:
+            self.obs_n.record_stream(main_stream)
+        self.lattice.bind_stream(main_stream)
+        lap("observation_side")
         self.setup_s = lap.phases
+
+    @property
+    def c_prime(self) -> float:
+        """Outlier constant over the global model count (estep.py:97-112,
+        SURVEY.md 8(e)) at the current kernel width."""
+        return outlier_constant(self.gmm.outlier_ratio, self.N, self.M_total, self.sigma)
+
+    def _build_observation(self, observation, gmm, residual_mode, stream) -> None:
+        import torch
+        with torch.cuda.stream(stream):
+            self.obs = upload_soa(observation.positions, self.dev)
+            self.N = self.obs.shape[1]
+            self.obs_n = None
+            if residual_mode == "point_to_plane":
+                self.obs_n = upload_soa(observation.normals, self.dev)
+            self.build(gmm.sigma)
+            stream.synchronize()
 
     def build(self, sigma) -> None:
         """(Re)build the observation lattice at kernel width sigma."""
@@ -256,7 +300,6 @@ class RigidDevicePath:
         lat.splat_points(self.obs, self.obs_n, self.value_mode)
         lat.blur()
         self.lattice, self.sigma = lat, s
-        self.c_prime = outlier_constant(self.gmm.outlier_ratio, self.N, self.M_total, s)
 
     def pass_params(self, R, t) -> "_lib.RigidPassParams":
         R = np.asarray(R, dtype=float)

@@ -1256,6 +1256,15 @@ int fr_lattice_info(const fr_lattice *lat, int64_t *num_sites, int *nv, int *blu
     return FR_OK;
 }
 
+int fr_lattice_set_stream(fr_lattice *lat, void *stream) {
+    if (!lat) {
+        set_error("null lattice");
+        return FR_EINVAL;
+    }
+    lat->stream = (cudaStream_t)stream;
+    return FR_OK;
+}
+
 int fr_lattice_dense_cells(const fr_lattice *lat, int64_t *cells) {
     if (!lat || !cells) {
         set_error("null argument");

@@ -187,6 +187,11 @@ class PermutohedralLattice:
         self._splatted = True
         self._export = None
 
+    def bind_stream(self, stream) -> None:
+        """Stream the lattice's stream-ordered frees go behind (after a side-
+        stream build has completed)."""
+        _lib.check(self._lib.fr_lattice_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)))
+
     def blur(self) -> None:
         """permutohedral.py:291-327"""
         if self.blurred:

@@ -273,3 +273,20 @@ def test_grid_pass_odd_sizes(fr, m, monkeypatch):
     k = np.array([0, 1, 1, 1, 2, 2, 2, 2, 2, 2, 1, 1, 1] + [2] * 9 + [2, 2, 2])
     scale = max(ex[0], 1.0) * L ** k
     np.testing.assert_array_less(np.abs(f32 - ex) / scale, 2e-5)
+
+
+def test_setup_overlap_small_model_large_observation(fr):
+    """The observation side (upload, splat, blur) builds on a worker thread
+    while the model side is set up: a tiny model against a large observation
+    finishes the model side first and must still see the finished lattice."""
+    model, obs, _ = O.pebble_pair(2_000_000, outlier_ratio=0.05, seed=4)
+    X = model[:1000].astype(np.float32).astype(float)
+    Y = obs.astype(np.float32).astype(float)
+    sigma = 0.05 * O.bbox_diameter(model[:2_000_000])
+    cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=sigma, outlier_ratio=0.1),
+                                max_em_iters=40, twist_tolerance=1e-4)
+    a = fr.register(fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(), cfg)
+    b = fr.register(fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(), cfg)
+    assert a.iterations >= 1 and np.isfinite(a.objectives[0])
+    assert np.array_equal(a.kinematics.pose.matrix(), b.kinematics.pose.matrix())
+    assert a.objectives == b.objectives
