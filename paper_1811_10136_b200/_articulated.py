@@ -17,7 +17,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._rigid import FAST_QUERY, RigidDevicePath, RigidMoments, unpack_upper6
+from ._rigid import FAST_QUERY, RigidDevicePath, unpack_upper6
 
 
 class BodyPose(ctypes.Structure):
@@ -119,6 +119,96 @@ class ArticulatedDevicePath(RigidDevicePath):
         return np.asarray(out)
 
 
+class BodyMoments:
+    """RigidMoments (_rigid.py) of all nb bodies at once: the same closed forms
+    (normal equations, energy change and moved statistics of x' = D x + delta)
+    as batched array expressions, one per M-step quantity instead of one per
+    body."""
+
+    _E = np.stack([np.array([[0.0, 0.0, 0.0], [0.0, 0.0, -1.0], [0.0, 1.0, 0.0]]),
+                   np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 0.0], [-1.0, 0.0, 0.0]]),
+                   np.array([[0.0, -1.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.0, 0.0]])])
+
+    def __init__(self, S0, S1, S2, R1, RX, Q):
+        self.S0, self.S1, self.S2, self.R1, self.RX, self.Q = S0, S1, S2, R1, RX, Q
+
+    @classmethod
+    def from_sums(cls, sums) -> "BodyMoments":
+        s = np.asarray(sums, dtype=float)
+        S2 = np.empty((len(s), 3, 3))
+        iu = [(0, 0, 4), (0, 1, 5), (0, 2, 6), (1, 1, 7), (1, 2, 8), (2, 2, 9)]
+        for i, j, c in iu:
+            S2[:, i, j] = S2[:, j, i] = s[:, c]
+        return cls(s[:, 0].copy(), s[:, 1:4].copy(), S2, s[:, 10:13].copy(),
+                   s[:, 13:22].reshape(-1, 3, 3).copy(), s[:, 22:25].copy())
+
+    def energy(self, s2) -> float:
+        return float(0.5 * np.sum(self.Q @ s2))
+
+    def normal_equations(self, c, s2):
+        """(nb, 6, 6) H and (nb, 6) g about centres c (nb, 3)."""
+        E = self._E
+        S0 = self.S0[:, None]
+        X1 = self.S1 + c * S0
+        X2 = (self.S2 + c[:, :, None] * self.S1[:, None, :] + self.S1[:, :, None] * c[:, None, :]
+              + S0[:, :, None] * c[:, :, None] * c[:, None, :])
+        XR = self.RX + self.R1[:, :, None] * c[:, None, :]
+        Ssq = np.diag(s2)
+        T = np.einsum("kji,jm,lmn->klin", E, Ssq, E)          # E_k^T Ssq E_l
+        nb = len(self.S0)
+        H = np.zeros((nb, 6, 6))
+        H[:, :3, :3] = np.einsum("bkl,klin->bin", X2, T)
+        K1 = np.zeros((nb, 3, 3))
+        K1[:, 0, 1], K1[:, 0, 2] = -X1[:, 2], X1[:, 1]
+        K1[:, 1, 0], K1[:, 1, 2] = X1[:, 2], -X1[:, 0]
+        K1[:, 2, 0], K1[:, 2, 1] = -X1[:, 1], X1[:, 0]
+        H[:, :3, 3:] = K1 @ Ssq
+        H[:, 3:, :3] = np.transpose(H[:, :3, 3:], (0, 2, 1))
+        H[:, 3:, 3:] = self.S0[:, None, None] * Ssq
+        g = np.zeros((nb, 6))
+        g[:, :3] = np.einsum("kij,bjk->bi", E, s2[None, :, None] * XR)
+        g[:, 3:] = self.R1 * s2
+        return H, g
+
+    def _motion(self, D, delta, c):
+        A = D - np.eye(3)
+        dt = np.einsum("bij,bj->bi", A, c) + delta
+        su2 = (np.einsum("bji,bik,bjk->bj", A, self.S2, A)
+               + 2.0 * dt * np.einsum("bji,bi->bj", A, self.S1) + dt ** 2 * self.S0[:, None])
+        sur = np.einsum("bji,bji->bj", A, self.RX) + dt * self.R1
+        return A, dt, su2, sur
+
+    def delta_energy(self, D, delta, c, s2) -> float:
+        _, _, su2, sur = self._motion(D, delta, c)
+        return float(0.5 * np.sum((su2 + 2.0 * sur) @ s2))
+
+    def moved(self, D, delta, c) -> "BodyMoments":
+        A, dt, su2, sur = self._motion(D, delta, c)
+        S0 = self.S0[:, None]
+        DS1 = np.einsum("bij,bj->bi", D, self.S1)
+        S1n = DS1 + dt * S0
+        outer = np.einsum
+        S2n = (D @ self.S2 @ np.transpose(D, (0, 2, 1)) + outer("bi,bj->bij", DS1, dt)
+               + outer("bi,bj->bij", dt, DS1) + S0[:, :, None] * outer("bi,bj->bij", dt, dt))
+        AS1 = np.einsum("bij,bj->bi", A, self.S1)
+        R1n = self.R1 + AS1 + dt * S0
+        U = (A @ self.S2 @ np.transpose(D, (0, 2, 1)) + outer("bi,bj->bij", AS1, dt)
+             + outer("bi,bj->bij", dt, DS1) + S0[:, :, None] * outer("bi,bj->bij", dt, dt))
+        RXn = self.RX @ np.transpose(D, (0, 2, 1)) + outer("bi,bj->bij", self.R1, dt) + U
+        Qn = self.Q + 2.0 * sur + su2
+        return BodyMoments(self.S0, S1n, S2n, R1n, RXn, Qn)
+
+
+def _body_motion(cur, cand):
+    """Per-body (D, delta) taking the current body poses to the candidate's."""
+    Rb = np.stack([cur.body_pose(b).rotation for b in range(cur.n_bodies)])
+    tb = np.stack([cur.body_pose(b).translation for b in range(cur.n_bodies)])
+    Rc = np.stack([cand.body_pose(b).rotation for b in range(cand.n_bodies)])
+    tc = np.stack([cand.body_pose(b).translation for b in range(cand.n_bodies)])
+    D = Rc @ np.transpose(Rb, (0, 2, 1))
+    return D, tc - np.einsum("bij,bj->bi", D, tb)
+
+
 def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
     """One M step of an articulated tree from per-body pass statistics
     (mstep.py:421-459 with assemble_articulated, mstep.py:213-229)."""
@@ -128,9 +218,9 @@ def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
     nb = path.nb
     current = tree
     if p2p:
-        moms = [RigidMoments.from_sums(sums[b]) for b in range(nb)]
-        cents = path.centres(tree)
-        value = float(sum(m.energy(s2) for m in moms))
+        moms = BodyMoments.from_sums(sums[:nb])
+        cents = np.asarray(path.centres(tree), dtype=float)
+        value = moms.energy(s2)
     else:
         value = 0.5 * float(sums[:, 28].sum())
         Hb = np.stack([unpack_upper6(sums[b, 1:22]) for b in range(nb)])
@@ -142,9 +232,7 @@ def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
     def system(tr):
         S = tr.spatial_velocity_jacobians()
         if p2p:
-            HG = [m.normal_equations(c, s2) for m, c in zip(moms, cents)]
-            H = np.stack([h for h, _ in HG])
-            g = np.stack([gg for _, gg in HG])
+            H, g = moms.normal_equations(cents, s2)
         else:
             H, g = Hb, gb
         live = np.flatnonzero(H.any(axis=(1, 2)) | g.any(axis=1))
@@ -159,26 +247,24 @@ def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
         stats: dict = {}
         step = gn_solve(eq, opts.damping, opts.solve_method, _stats=stats)
         diag.dampings.append(stats.get("damping", 0.0))
-        cands, scale = [], 1.0
-        for _h in range(opts.max_halvings + 1):
-            cands.append((current.updated(scale * step), scale))
-            scale *= 0.5
         accepted = None
         if p2p:
-            for h, (cand, sc) in enumerate(cands):
-                dE = 0.0
-                motions = []
-                for b in range(nb):
-                    Tb, Tc = current.body_pose(b), cand.body_pose(b)
-                    D = Tc.rotation @ Tb.rotation.T
-                    delta = Tc.translation - D @ Tb.translation
-                    motions.append((D, delta))
-                    dE += moms[b].delta_energy(D, delta, cents[b], s2)
-                cv = value + dE
+            # candidates built one halving at a time (each is a forward
+            # kinematics pass); the first acceptable one stops the search
+            scale = 1.0
+            for h in range(opts.max_halvings + 1):
+                cand = current.updated(scale * step)
+                D, delta = _body_motion(current, cand)
+                cv = value + moms.delta_energy(D, delta, cents, s2)
                 if _accepts(cv, value):
-                    accepted = (cand, cv, h, sc, motions)
+                    accepted = (cand, cv, h, scale, (D, delta))
                     break
+                scale *= 0.5
         else:
+            cands, scale = [], 1.0
+            for _h in range(opts.max_halvings + 1):
+                cands.append((current.updated(scale * step), scale))
+                scale *= 0.5
             vals = list(path.candidate_objectives_trees([cands[0][0]]))
             if not _accepts(vals[0], value) and len(cands) > 1:
                 vals += list(path.candidate_objectives_trees([c for c, _ in cands[1:]]))
@@ -188,7 +274,7 @@ def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
                     break
         if accepted is None:
             break
-        cand, value, h, sc, motions = accepted
+        cand, value, h, sc, motion = accepted
         diag.objectives.append(value)
         diag.halvings.append(h)
         sn = float(np.linalg.norm(sc * step))
@@ -197,6 +283,6 @@ def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
         if sn <= opts.step_tolerance:
             break
         if p2p:
-            moms = [m.moved(D, delta, c) for m, (D, delta), c in zip(moms, motions, cents)]
+            moms = moms.moved(motion[0], motion[1], cents)
             eq = system(current)
     return current, diag
