@@ -49,7 +49,9 @@ def gather_lists(indices, weights, n_nodes, extra_codes=None):
     live = (idx >= 0) & (wts > 0)
     p_i, s_i = np.nonzero(live)
     node = idx[p_i, s_i]
-    order = np.lexsort((p_i, node))
+    npts = len(idx)
+    # (node, point) order via one combined integer key (cheaper than lexsort)
+    order = np.argsort(node * npts + p_i, kind="stable")
     dcount = np.bincount(node, minlength=n_nodes)
     pts, sa, sc, codes = [np.zeros(0, dtype=np.int64)], [np.zeros(0, dtype=np.int64)], \
         [np.zeros(0, dtype=np.int64)], [np.zeros(0, dtype=np.int64)]
@@ -62,9 +64,15 @@ def gather_lists(indices, weights, n_nodes, extra_codes=None):
             sc.append(np.full(len(pp), c))
             codes.append(np.minimum(ia, ic) * n_nodes + np.maximum(ia, ic))
     pts, sa, sc, codes = map(np.concatenate, (pts, sa, sc, codes))
-    ucodes = np.unique(codes) if extra_codes is None else np.asarray(extra_codes)
-    pid = np.searchsorted(ucodes, codes)
-    porder = np.lexsort((pts, pid))
+    if extra_codes is None and n_nodes * n_nodes <= (1 << 24):
+        # codes < n_nodes^2: unique codes and their ranks by counting
+        present = np.bincount(codes, minlength=n_nodes * n_nodes) > 0
+        ucodes = np.flatnonzero(present)
+        pid = (np.cumsum(present) - 1)[codes]
+    else:
+        ucodes = np.unique(codes) if extra_codes is None else np.asarray(extra_codes)
+        pid = np.searchsorted(ucodes, codes)
+    porder = np.argsort(pid * npts + pts, kind="stable")
     pcount = np.bincount(pid, minlength=len(ucodes))
     pent = np.stack([pts[porder], sa[porder] | (sc[porder] << 8)], axis=1).astype(np.int32)
     return {"dptr": np.concatenate([[0], np.cumsum(dcount)]).astype(np.int32),
@@ -72,6 +80,42 @@ def gather_lists(indices, weights, n_nodes, extra_codes=None):
             "pptr": np.concatenate([[0], np.cumsum(pcount)]).astype(np.int32),
             "pent": np.ascontiguousarray(pent), "n_pairs": len(ucodes),
             "pair_lo": ucodes // n_nodes, "pair_hi": ucodes % n_nodes, "codes": ucodes}
+
+
+def gather_lists_device(sidx, swt, n_nodes):
+    """gather_lists on the device (torch's stable GPU sorts), for one GPU:
+    the same lists and order, built where they are used."""
+    import torch
+    npts, K = sidx.shape
+    idx = sidx.long()
+    live = (idx >= 0) & (swt > 0)
+    p_i, s_i = torch.nonzero(live, as_tuple=True)
+    node = idx[p_i, s_i]
+    _, order = torch.sort(node * npts + p_i, stable=True)
+    dcount = torch.bincount(node, minlength=n_nodes)
+    pts, sa, sc, codes = [], [], [], []
+    for a in range(K):
+        for c in range(a + 1, K):
+            pp = torch.nonzero(live[:, a] & live[:, c], as_tuple=True)[0]
+            ia, ic = idx[pp, a], idx[pp, c]
+            pts.append(pp)
+            sa.append(torch.full_like(pp, a))
+            sc.append(torch.full_like(pp, c))
+            codes.append(torch.minimum(ia, ic) * n_nodes + torch.maximum(ia, ic))
+    z = torch.zeros(0, dtype=torch.int64, device=sidx.device)
+    pts, sa, sc, codes = (torch.cat(v) if v else z for v in (pts, sa, sc, codes))
+    present = torch.bincount(codes, minlength=n_nodes * n_nodes) > 0
+    ucodes = torch.nonzero(present, as_tuple=True)[0]
+    pid = (torch.cumsum(present.long(), 0) - 1)[codes]
+    _, porder = torch.sort(pid * npts + pts, stable=True)
+    pcount = torch.bincount(pid, minlength=len(ucodes))
+    zero = torch.zeros(1, dtype=torch.int64, device=sidx.device)
+    uc = ucodes.cpu().numpy()
+    return {"dptr": torch.cat([zero, torch.cumsum(dcount, 0)]).int(),
+            "dent": (p_i * K + s_i)[order].int().contiguous(),
+            "pptr": torch.cat([zero, torch.cumsum(pcount, 0)]).int(),
+            "pent": torch.stack([pts[porder], sa[porder] | (sc[porder] << 8)], 1).int().contiguous(),
+            "n_pairs": len(uc), "pair_lo": uc // n_nodes, "pair_hi": uc % n_nodes, "codes": uc}
 
 
 class NodeGraphDevicePath(RigidDevicePath):
@@ -91,16 +135,20 @@ class NodeGraphDevicePath(RigidDevicePath):
         dev = self.dev
         self.sidx = torch.from_numpy(idx.astype(np.int32)).to(dev)
         self.swt = torch.from_numpy(np.ascontiguousarray(wts)).to(dev)
-        L = gather_lists(idx, wts, self.n)
-        if self.group is not None:
-            # the pair set (and its order) must be the union over all shards
-            import torch.distributed as dist
-            allc = [None] * dist.get_world_size(self.group)
-            dist.all_gather_object(allc, L["codes"], group=self.group)
-            L = gather_lists(idx, wts, self.n, extra_codes=np.unique(np.concatenate(allc)))
+        if self.group is None and self.n * self.n <= (1 << 24):
+            L = gather_lists_device(self.sidx, self.swt, self.n)
+        else:
+            L = gather_lists(idx, wts, self.n)
+            if self.group is not None:
+                # the pair set (and its order) must be the union over all shards
+                import torch.distributed as dist
+                allc = [None] * dist.get_world_size(self.group)
+                dist.all_gather_object(allc, L["codes"], group=self.group)
+                L = gather_lists(idx, wts, self.n, extra_codes=np.unique(np.concatenate(allc)))
+            L = {k: (torch.from_numpy(v).to(dev) if k in ("dptr", "dent", "pptr", "pent") else v)
+                 for k, v in L.items()}
         self.pair_lo, self.pair_hi, self.n_pairs = L["pair_lo"], L["pair_hi"], L["n_pairs"]
-        self.dptr, self.dent, self.pptr, self.pent = (
-            torch.from_numpy(L[k]).to(dev) for k in ("dptr", "dent", "pptr", "pent"))
+        self.dptr, self.dent, self.pptr, self.pent = (L[k] for k in ("dptr", "dent", "pptr", "pent"))
         f64 = dict(dtype=torch.float64, device=dev)
         self.rec = torch.empty((7, self.M), **f64)
         self.ete = torch.empty((self.M, 28), **f64)
@@ -186,16 +234,20 @@ def normal_equations(graph, diag, off, path, lambda_reg):
 
 
 def normal_equations_from(graph, diag, off, pair_lo, pair_hi, lambda_reg):
+    """6x6-block system as block arrays (keys (m, 2) with k <= l, values
+    (m, 6, 6); repeated keys add up): device data term + host ARAP term."""
     from .mstep import NormalEquations
     n = graph.n_nodes
     D = _sym6_stack(diag[:, :21])
     b = diag[:, 21:27].copy()
-    offb = _sym6_stack(off[:len(pair_lo), :21]) if len(pair_lo) else np.zeros((0, 6, 6))
-    blocks = {(int(a), int(c)): offb[i] for i, (a, c) in enumerate(zip(pair_lo, pair_hi))}
+    keys = [np.stack([np.asarray(pair_lo), np.asarray(pair_hi)], axis=1).reshape(-1, 2)]
+    vals = [_sym6_stack(off[:len(pair_lo), :21]) if len(pair_lo) else np.zeros((0, 6, 6))]
     if lambda_reg > 0 and len(graph.edges):
         R, t = graph.node_rotations, graph.node_translations
         root = np.sqrt(lambda_reg)
         k_ids, l_ids = graph.edges[:, 0], graph.edges[:, 1]
+        lo, hi = np.minimum(k_ids, l_ids), np.maximum(k_ids, l_ids)
+        swap = k_ids > l_ids
         for p in (graph.node_positions[l_ids], graph.node_positions[k_ids]):
             xk = np.einsum("eij,ej->ei", R[k_ids], p) + t[k_ids]
             xl = np.einsum("eij,ej->ei", R[l_ids], p) + t[l_ids]
@@ -207,14 +259,14 @@ def normal_equations_from(graph, diag, off, pair_lo, pair_hi, lambda_reg):
             b += _grouped(np.einsum("eri,er->ei", Jk, r), k_ids, n)
             b += _grouped(np.einsum("eri,er->ei", Jl, r), l_ids, n)
             cross = np.einsum("eri,erj->eij", Jk, Jl)
-            swap = k_ids > l_ids
             cross[swap] = np.transpose(cross[swap], (0, 2, 1))
-            for e in range(len(k_ids)):
-                key = (int(min(k_ids[e], l_ids[e])), int(max(k_ids[e], l_ids[e])))
-                blocks[key] = blocks[key] + cross[e] if key in blocks else cross[e].copy()
-    for k in range(n):
-        blocks[(k, k)] = D[k]
-    return NormalEquations(6 * n, b=b.reshape(-1), blocks=blocks)
+            keys.append(np.stack([lo, hi], axis=1))
+            vals.append(cross)
+    keys.append(np.stack([np.arange(n), np.arange(n)], axis=1))
+    vals.append(D)
+    return NormalEquations(6 * n, b=b.reshape(-1),
+                           block_arrays=(np.concatenate(keys).astype(np.int64),
+                                         np.concatenate(vals)))
 
 
 def nodegraph_m_step(path, g4, diag, off, graph, s2, opts):
@@ -232,20 +284,21 @@ def nodegraph_m_step(path, g4, diag, off, graph, s2, opts):
         stats: dict = {}
         step = gn_solve(eq, opts.damping, opts.solve_method, _stats=stats)
         diagn.dampings.append(stats.get("damping", 0.0))
-        cands, scale = [], 1.0
-        for _h in range(opts.max_halvings + 1):
-            cands.append((current.updated(scale * step), scale))
-            scale *= 0.5
-        vals = list(path.candidate_objectives([cands[0][0]], s2))
-        if not _accepts(vals[0] + regularizer_objective(cands[0][0], opts.lambda_reg), value) \
-                and len(cands) > 1:
-            vals += list(path.candidate_objectives([c for c, _ in cands[1:]], s2))
-        accepted = None
-        for h, dv in enumerate(vals):
-            cv = dv + regularizer_objective(cands[h][0], opts.lambda_reg)
-            if _accepts(cv, value):
-                accepted = (cands[h][0], cv, h, cands[h][1])
-                break
+        # the full step first; the halvings (built only when it is rejected)
+        # are evaluated together in one device pass
+        first = current.updated(step)
+        cv0 = float(path.candidate_objectives([first], s2)[0]) + \
+            regularizer_objective(first, opts.lambda_reg)
+        accepted = (first, cv0, 0, 1.0) if _accepts(cv0, value) else None
+        if accepted is None and opts.max_halvings > 0:
+            scales = [0.5 ** h for h in range(1, opts.max_halvings + 1)]
+            cands = [current.updated(sc * step) for sc in scales]
+            vals = path.candidate_objectives(cands, s2)
+            for h, (cand, dv) in enumerate(zip(cands, vals), start=1):
+                cv = float(dv) + regularizer_objective(cand, opts.lambda_reg)
+                if _accepts(cv, value):
+                    accepted = (cand, cv, h, scales[h - 1])
+                    break
         if accepted is None:
             break
         current, value, h, sc = accepted

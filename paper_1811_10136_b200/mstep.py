@@ -96,27 +96,40 @@ def residuals_from_moments(moments, sigma, mode: str = "point_to_point") -> Resi
 
 @dataclass
 class NormalEquations:
-    """Dense or 6x6-block-sparse A and b (mstep.py:154-176)."""
+    """Dense or 6x6-block-sparse A and b (mstep.py:154-176).  A block system
+    is a dict {(k, l): block} (k <= l) or, as the device assemblies produce
+    it, `block_arrays` = (keys (m, 2) with k <= l, values (m, 6, 6)), repeated
+    keys adding up."""
 
     n_params: int
     b: np.ndarray
     A: np.ndarray | None = None
     blocks: dict | None = None
+    block_arrays: tuple | None = None
+
+    @property
+    def is_block(self) -> bool:
+        return self.A is None and (self.blocks is not None or self.block_arrays is not None)
+
+    def arrays(self):
+        """(keys, values) of the block system."""
+        if self.block_arrays is not None:
+            return self.block_arrays
+        keys = np.array(list(self.blocks.keys()), dtype=np.int64).reshape(-1, 2)
+        vals = np.stack(list(self.blocks.values())) if len(keys) else np.zeros((0, 6, 6))
+        return keys, vals
 
     def to_dense(self) -> np.ndarray:
         if self.A is not None:
             return self.A
-        full = np.zeros((self.n_params, self.n_params))
-        for (k, l), blk in self.blocks.items():
-            full[6 * k:6 * k + 6, 6 * l:6 * l + 6] += blk
-            if k != l:
-                full[6 * l:6 * l + 6, 6 * k:6 * k + 6] += blk.T
-        return full
+        return _dense_blocks(self)
 
     def trace(self) -> float:
         if self.A is not None:
             return float(np.trace(self.A))
-        return float(sum(np.trace(b) for (k, l), b in self.blocks.items() if k == l))
+        keys, vals = self.arrays()
+        d = keys[:, 0] == keys[:, 1]
+        return float(np.trace(vals[d], axis1=1, axis2=2).sum())
 
 
 def _device_rigid_sums(spec: ResidualSpec, x) -> np.ndarray:
@@ -162,8 +175,7 @@ def assemble_rigid(spec: ResidualSpec, current_positions) -> NormalEquations:
 def _dense_blocks(eq: NormalEquations) -> np.ndarray:
     """Dense A of a 6x6-block system (both triangles), one scatter."""
     P, nb = eq.n_params, eq.n_params // 6
-    keys = np.array(list(eq.blocks.keys()), dtype=np.int64).reshape(-1, 2)
-    vals = np.stack(list(eq.blocks.values())) if len(keys) else np.zeros((0, 6, 6))
+    keys, vals = eq.arrays()
     F = np.zeros((nb, nb, 6, 6))
     np.add.at(F, (keys[:, 0], keys[:, 1]), vals)
     off = keys[:, 0] != keys[:, 1]
@@ -171,15 +183,26 @@ def _dense_blocks(eq: NormalEquations) -> np.ndarray:
     return F.transpose(0, 2, 1, 3).reshape(P, P)
 
 
-def _gpu_cholesky_solve(A: np.ndarray, lam: float, b: np.ndarray) -> np.ndarray:
+def _gpu_block_cholesky_solve(eq: NormalEquations, lam: float) -> np.ndarray:
+    """(A + lam I) x = b for a 6x6-block system: the blocks (not the dense
+    matrix) go to the device, which scatters them into the dense A and factors
+    it (cuSOLVER Cholesky through torch)."""
     import torch
     dev = _lib.device()
-    At = torch.from_numpy(A).to(dev)
-    At.diagonal().add_(lam)
-    L, info = torch.linalg.cholesky_ex(At)
+    P, nb = eq.n_params, eq.n_params // 6
+    keys, vals = eq.arrays()
+    k = torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
+    v = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64)).to(dev)
+    F = torch.zeros((nb, nb, 6, 6), dtype=torch.float64, device=dev)
+    F.index_put_((k[:, 0], k[:, 1]), v, accumulate=True)
+    off = k[:, 0] != k[:, 1]
+    F.index_put_((k[off, 1], k[off, 0]), v[off].transpose(1, 2), accumulate=True)
+    A = F.permute(0, 2, 1, 3).reshape(P, P)
+    A.diagonal().add_(lam)
+    L, info = torch.linalg.cholesky_ex(A)
     if int(info.item()) != 0:
         raise scipy.linalg.LinAlgError("normal equations not positive definite")
-    x = torch.cholesky_solve(torch.from_numpy(np.ascontiguousarray(b)).to(dev)[:, None], L)
+    x = torch.cholesky_solve(torch.from_numpy(np.ascontiguousarray(eq.b)).to(dev)[:, None], L)
     sol = x[:, 0].cpu().numpy()
     if not np.all(np.isfinite(sol)):
         raise scipy.linalg.LinAlgError("factorization produced non-finite values")
@@ -188,28 +211,23 @@ def _gpu_cholesky_solve(A: np.ndarray, lam: float, b: np.ndarray) -> np.ndarray:
 
 def _factor_solve(eq: NormalEquations, lam: float, method: str) -> np.ndarray:
     """mstep.py:317-345"""
-    if (method == "auto" and eq.A is None and eq.blocks is not None
-            and _DENSE_SOLVE_MAX < eq.n_params <= _GPU_DENSE_MAX):
-        return _gpu_cholesky_solve(_dense_blocks(eq), lam, eq.b)
+    if method == "auto" and eq.is_block and _DENSE_SOLVE_MAX < eq.n_params <= _GPU_DENSE_MAX:
+        return _gpu_block_cholesky_solve(eq, lam)
     sparse = method == "sparse" or (method == "auto" and eq.A is None
                                     and eq.n_params > _DENSE_SOLVE_MAX)
-    if sparse and eq.blocks is not None:
-        rows, cols, vals = [], [], []
+    if sparse and eq.is_block:
+        keys, vals = eq.arrays()
         rr, cc = np.meshgrid(np.arange(6), np.arange(6), indexing="ij")
-        for (k, l), blk in eq.blocks.items():
-            rows.append((6 * k + rr).ravel())
-            cols.append((6 * l + cc).ravel())
-            vals.append(blk.ravel())
-            if k != l:
-                rows.append((6 * l + rr).ravel())
-                cols.append((6 * k + cc).ravel())
-                vals.append(blk.T.ravel())
-        rows.append(np.arange(eq.n_params))
-        cols.append(np.arange(eq.n_params))
-        vals.append(np.full(eq.n_params, lam))
-        A = scipy.sparse.csc_matrix((np.concatenate(vals), (np.concatenate(rows),
-                                                           np.concatenate(cols))),
-                                    shape=(eq.n_params, eq.n_params))
+        off = keys[:, 0] != keys[:, 1]
+        rows = np.concatenate([(6 * keys[:, 0, None, None] + rr).ravel(),
+                               (6 * keys[off, 1, None, None] + rr).ravel(),
+                               np.arange(eq.n_params)])
+        cols = np.concatenate([(6 * keys[:, 1, None, None] + cc).ravel(),
+                               (6 * keys[off, 0, None, None] + cc).ravel(),
+                               np.arange(eq.n_params)])
+        data = np.concatenate([vals.ravel(), np.transpose(vals[off], (0, 2, 1)).ravel(),
+                               np.full(eq.n_params, lam)])
+        A = scipy.sparse.csc_matrix((data, (rows, cols)), shape=(eq.n_params, eq.n_params))
         sol = scipy.sparse.linalg.splu(A).solve(eq.b)
         if not np.all(np.isfinite(sol)):
             raise scipy.linalg.LinAlgError("sparse factorization produced non-finite values")

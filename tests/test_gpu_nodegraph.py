@@ -96,3 +96,21 @@ def test_nodegraph_assembly_matches_dense_oracle(fr):
     # the device forward map (DQB) reproduces the host blend
     ob = 0.5 * float(np.sum(w * ((x - tg) ** 2 @ s2)))
     assert float(g4[0]) == pytest.approx(ob, rel=1e-9)
+
+
+def test_gather_lists_device_equals_host():
+    """The device-built gather lists equal the host builder's, entry for entry."""
+    import torch
+    from paper_1811_10136_b200._nodegraph import gather_lists, gather_lists_device
+    g = np.load(os.path.join(GOLDEN, "nodegraph_strip6k_pt2pl.npz"))
+    idx = np.asarray(g["skin_idx"], dtype=np.int64)
+    wts = np.where(idx >= 0, np.asarray(g["skin_w"], dtype=float), 0.0)
+    n = len(g["nodes"])
+    host = gather_lists(idx, wts, n)
+    dev = gather_lists_device(torch.from_numpy(idx.astype(np.int32)).cuda(),
+                              torch.from_numpy(wts).cuda(), n)
+    for k in ("dptr", "dent", "pptr", "pent"):
+        assert np.array_equal(dev[k].cpu().numpy(), host[k]), k
+    for k in ("pair_lo", "pair_hi", "codes"):
+        assert np.array_equal(dev[k], host[k]), k
+    assert dev["n_pairs"] == host["n_pairs"]

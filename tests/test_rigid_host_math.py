@@ -81,3 +81,36 @@ def test_moved_statistics_equal_recomputed(problem):
     for name in ("S1", "S2", "R1", "RX", "Q"):
         np.testing.assert_allclose(getattr(moved, name), getattr(direct, name),
                                    rtol=1e-9, atol=1e-15)
+
+
+def test_block_system_dict_and_arrays_agree():
+    """NormalEquations block systems: the dict form and the block-array form
+    (repeated keys add up) give the same dense A, trace and sparse solution."""
+    import paper_1811_10136_b200.mstep as M
+    rng = np.random.default_rng(3)
+    nb = 9
+    blocks = {}
+    keys, vals = [], []
+    for k in range(nb):
+        G = rng.standard_normal((6, 6))
+        blk = G @ G.T + 6 * np.eye(6)
+        blocks[(k, k)] = blk
+        half = 0.5 * blk
+        keys += [(k, k), (k, k)]
+        vals += [half, blk - half]
+    for _ in range(12):
+        k, l = sorted(rng.choice(nb, 2, replace=False))
+        blk = 0.1 * rng.standard_normal((6, 6))
+        blocks[(k, l)] = blocks.get((k, l), 0) + blk
+        keys.append((k, l))
+        vals.append(blk)
+    b = rng.standard_normal(6 * nb)
+    eq_d = M.NormalEquations(6 * nb, b=b, blocks=blocks)
+    eq_a = M.NormalEquations(6 * nb, b=b, block_arrays=(np.array(keys), np.array(vals)))
+    np.testing.assert_allclose(eq_d.to_dense(), eq_a.to_dense(), rtol=0, atol=1e-12)
+    assert eq_d.trace() == pytest.approx(eq_a.trace(), rel=1e-14)
+    x_d = M.gn_solve(eq_d, damping=1e-3, method="sparse")
+    x_a = M.gn_solve(eq_a, damping=1e-3, method="sparse")
+    x_dense = M.gn_solve(eq_a, damping=1e-3, method="dense")
+    np.testing.assert_allclose(x_d, x_a, rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(x_a, x_dense, rtol=1e-9, atol=1e-12)
