@@ -24,7 +24,6 @@
 namespace fr {
 
 constexpr int kMaxK = 8;
-constexpr int kGraphRec = 7;    // w, t[3], n[3]
 constexpr int kGraphEte = 28;   // E^T E upper 21 | E^T r 6 | pad
 
 struct GraphK {
