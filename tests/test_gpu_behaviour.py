@@ -22,6 +22,16 @@ def surface(n, seed):
     return O.pebble_resample(n, seed=seed)
 
 
+def ring_sphere(n_rings=16, n_per_ring=36, radius=0.075, cap=0.4):
+    """A capless sphere on a regular (theta, phi) grid: symmetric under the
+    2 pi / n_per_ring spin and the z-mirror, so the cloud's kernel pulls on
+    itself cancel (the shape of test_pipeline.py's self-registration test)."""
+    th, ph = np.meshgrid(np.linspace(cap, np.pi - cap, n_rings),
+                         np.arange(n_per_ring) * (2.0 * np.pi / n_per_ring), indexing="ij")
+    return radius * np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)],
+                             axis=-1).reshape(-1, 3)
+
+
 # --- lattice (test_permutohedral.py) ---------------------------------------
 
 def test_keys_valid_after_blur_and_mass_bounded(fr):
@@ -109,8 +119,8 @@ def test_identical_clouds_stay_put(fr):
     """Identical clouds with the exact transform: converged within 2
     iterations at the identity (test_pipeline.py:161-173, brute force as
     there; the lattice's approximation moves a self-registration slightly)."""
-    P = surface(3000, 6)
-    cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.002, outlier_ratio=0.1),
+    P = ring_sphere()
+    cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.0075, outlier_ratio=0.1),
                                 backend="bruteforce")
     res = fr.register(fr.PointCloud(P), fr.PointCloud(P.copy()), fr.RigidModel(), cfg)
     assert res.termination == "converged" and res.iterations <= 2
