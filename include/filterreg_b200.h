@@ -308,6 +308,20 @@ int fr_rigid_em_pass(fr_rigid_em *em, void *stream);
 int fr_rigid_em_solve(fr_rigid_em *em, void *stream);
 int fr_rigid_em_enqueue(fr_rigid_em *em, int n_iters, void *stream);
 int fr_rigid_em_run(fr_rigid_em *em, void *stream);
+
+/* 1 when fr_rigid_em_run takes the persistent path: the dense-grid float32
+ * point pass and at most FR_PERSIST_MAX model points (default 32768).  There
+ * one CTA runs the whole EM loop (pass, fixed-order reduction, float64 solve)
+ * with no launches or host polls between iterations. */
+int fr_rigid_em_persistent(const fr_rigid_em *em);
+
+/* Independent registrations (replicas, no collectives) in ONE launch: CTA i
+ * runs ems[i]'s EM loop to termination (the batched multi-problem driver,
+ * bench.py:132-159 of the reference runs trials one after another).  Every
+ * em must run the dense-grid float32 pass (FR_EINVAL otherwise); a problem's
+ * result equals fr_rigid_em_run's when fr_rigid_em_persistent(em) is 1.
+ * Synchronises `stream`. */
+int fr_rigid_em_run_batch(fr_rigid_em **ems, int n, void *stream);
 int fr_rigid_em_status(fr_rigid_em *em, int *done, int *iterations, int *termination,
                        void *stream);
 /* pose, per-iteration traces (host arrays of >= max_em_iters doubles or NULL),

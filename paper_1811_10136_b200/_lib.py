@@ -30,7 +30,7 @@ EXPORTED = (
     "fr_rigid_em_solve", "fr_rigid_em_enqueue", "fr_rigid_em_run", "fr_rigid_em_status",
     "fr_rigid_em_result", "fr_sort_points_morton", "fr_body_params_doubles", "fr_body_pass",
     "fr_body_objective", "fr_graph_pass", "fr_graph_blocks", "fr_graph_objective",
-    "fr_point_rows", "fr_upload_points",
+    "fr_point_rows", "fr_upload_points", "fr_rigid_em_persistent", "fr_rigid_em_run_batch",
 )
 
 
@@ -104,6 +104,8 @@ _SIGS = {
     "fr_rigid_em_solve": ([_P, _P], _I),
     "fr_rigid_em_enqueue": ([_P, _I, _P], _I),
     "fr_rigid_em_run": ([_P, _P], _I),
+    "fr_rigid_em_persistent": ([_P], _I),
+    "fr_rigid_em_run_batch": ([ctypes.POINTER(_P), _I, _P], _I),
     "fr_rigid_em_status": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I), _P], _I),
     "fr_rigid_em_result": ([_P, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I), ctypes.POINTER(_I),
                             _P], _I),

@@ -594,6 +594,41 @@ struct GridAcc {
     }
 };
 
+// float32 pass constants of pose k over the dense grid dg (one thread)
+__device__ __forceinline__ void grid_params(const RigidK &k, const DenseSliceF &dg, GridK &g) {
+    for (int c = 0; c < 3; ++c) {
+        g.Rc[c] = make_float2((float)k.R[c], (float)k.R[3 + c]);
+        g.R2[c] = make_float2((float)k.R[6 + c], 0.0f);
+        g.A01[c] = make_float2((float)k.A[0][c], (float)k.A[1][c]);
+        g.A23[c] = make_float2((float)k.A[2][c], (float)k.A[3][c]);
+        g.cref[c] = (float)k.c_ref[c];
+    }
+    int base[4];
+    float fr0[4];
+    for (int i = 0; i < 4; ++i) {
+        const double b = rint(k.e0[i] * 0.25);
+        base[i] = (int)b;
+        fr0[i] = (float)(k.e0[i] - 4.0 * b);
+    }
+    g.f01 = make_float2(fr0[0], fr0[1]);
+    g.f23 = make_float2(fr0[2], fr0[3]);
+    g.cw01 = make_float2((float)k.c_world[0], (float)k.c_world[1]);
+    g.cw2 = make_float2((float)k.c_world[2], 0.0f);
+    g.cp = (float)k.cp;
+    const int st[3] = {dg.s0, dg.s1, 1};
+    unsigned K = 0, H = 0;
+    for (int i = 0; i < 4; ++i) H += (unsigned)(base[i] - kMagicBits);
+    for (int i = 0; i < 3; ++i) {
+        g.C[i] = base[i] - kMagicBits - (dg.a[i] - 1);
+        g.lim[i] = dg.span[i] + 2u;
+        K += (unsigned)(base[i] - kMagicBits - (dg.a[i] - kDensePad)) * (unsigned)st[i];
+    }
+    g.s0 = dg.s0;
+    g.s1 = dg.s1;
+    g.K = K;
+    g.H = H;
+}
+
 // one model point of the dense-grid pass (valid = 0: the point contributes
 // nothing; branch-free so the points of a thread interleave)
 __device__ __forceinline__ void grid_point(float nx, float ny, float nz, bool valid,
@@ -734,40 +769,7 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
     __shared__ int4 tab[kGridTab];
     __shared__ float ring[kGridStages][PTS][3][kPassThreads];
     if (DEV && *done) return;
-    if (threadIdx.x == 0) {
-        const RigidK &k = DEV ? *kd : kv;
-        for (int c = 0; c < 3; ++c) {
-            g.Rc[c] = make_float2((float)k.R[c], (float)k.R[3 + c]);
-            g.R2[c] = make_float2((float)k.R[6 + c], 0.0f);
-            g.A01[c] = make_float2((float)k.A[0][c], (float)k.A[1][c]);
-            g.A23[c] = make_float2((float)k.A[2][c], (float)k.A[3][c]);
-            g.cref[c] = (float)k.c_ref[c];
-        }
-        int base[4];
-        float fr0[4];
-        for (int i = 0; i < 4; ++i) {
-            const double b = rint(k.e0[i] * 0.25);
-            base[i] = (int)b;
-            fr0[i] = (float)(k.e0[i] - 4.0 * b);
-        }
-        g.f01 = make_float2(fr0[0], fr0[1]);
-        g.f23 = make_float2(fr0[2], fr0[3]);
-        g.cw01 = make_float2((float)k.c_world[0], (float)k.c_world[1]);
-        g.cw2 = make_float2((float)k.c_world[2], 0.0f);
-        g.cp = (float)k.cp;
-        const int st[3] = {dg.s0, dg.s1, 1};
-        unsigned K = 0, H = 0;
-        for (int i = 0; i < 4; ++i) H += (unsigned)(base[i] - kMagicBits);
-        for (int i = 0; i < 3; ++i) {
-            g.C[i] = base[i] - kMagicBits - (dg.a[i] - 1);
-            g.lim[i] = dg.span[i] + 2u;
-            K += (unsigned)(base[i] - kMagicBits - (dg.a[i] - kDensePad)) * (unsigned)st[i];
-        }
-        g.s0 = dg.s0;
-        g.s1 = dg.s1;
-        g.K = K;
-        g.H = H;
-    }
+    if (threadIdx.x == 0) grid_params(DEV ? *kd : kv, dg, g);
     for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, dg.s0, dg.s1);
     __shared__ double wacc[kPassThreads / 32][NA];   // per-warp float64 accumulators
     if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
@@ -1358,6 +1360,86 @@ __global__ void k_rigid_solve(const double *sums, EmDev *e, double *objs, double
 }
 
 // ---------------------------------------------------------------------------
+// persistent EM for small problems: one CTA runs a whole registration -- the
+// dense-grid pass over its points, the warp folds and a fixed-order block
+// reduction, the float64 solve (thread 0) and the next pose's pass constants
+// -- with no kernel launches or host polls between iterations.  A launch with
+// P CTAs runs P independent problems (the batched driver, SURVEY.md 8(f)
+// rank 4).  The per-CTA reduction order is fixed, so a problem's result does
+// not depend on what else shares the launch.
+struct PersistProblem {
+    const float *ref;       // SoA planes of m points (Morton order)
+    long long m;
+    EmDev *em;
+    double *sums;           // last iteration's 25 sums (fr_rigid_em_sums)
+    double *objs, *tnorms, *masses;
+    DenseSliceF dg;
+};
+
+constexpr int kPersistThreads = 256;
+
+__global__ void __launch_bounds__(kPersistThreads, 1)
+k_em_persistent(const PersistProblem *probs) {
+    constexpr int NA = kP2PtBase;
+    const PersistProblem P = probs[blockIdx.x];
+    __shared__ EmDev se;
+    __shared__ GridK g;
+    __shared__ int4 tab[kGridTab];
+    __shared__ double wacc[kPersistThreads / 32][NA];
+    __shared__ double tsum[NA];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    em_copy(&se, P.em, threadIdx.x, blockDim.x);
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, P.dg.s0, P.dg.s1);
+    __syncthreads();
+    if (threadIdx.x == 0 && !se.done) grid_params(se.k, P.dg, g);
+    __syncthreads();
+    while (!se.done) {                  // block-uniform: read after a barrier
+        if (lane < NA) wacc[warp][lane] = 0.0;
+        GridAcc a;
+        a.zero();
+        int fold = 0;
+        // three independent points per thread per trip (warp-uniform trips)
+        constexpr int PP = 3;
+        for (long long base = 0; base < P.m; base += PP * kPersistThreads) {
+            float x[PP], y[PP], z[PP];
+            bool ok[PP];
+#pragma unroll
+            for (int k = 0; k < PP; ++k) {
+                const long long p = base + k * kPersistThreads + threadIdx.x;
+                ok[k] = p < P.m;
+                x[k] = ok[k] ? __ldg(P.ref + p) : 0.0f;
+                y[k] = ok[k] ? __ldg(P.ref + P.m + p) : 0.0f;
+                z[k] = ok[k] ? __ldg(P.ref + 2 * P.m + p) : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < PP; ++k) grid_point(x[k], y[k], z[k], ok[k], g, tab, P.dg, a);
+            fold += PP;
+            if (fold >= kGridFold) {
+                grid_warp_fold(a, wacc[warp]);
+                a.zero();
+                fold = 0;
+            }
+        }
+        grid_warp_fold(a, wacc[warp]);
+        __syncthreads();
+        if (threadIdx.x < NA) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < kPersistThreads / 32; ++w) v += wacc[w][threadIdx.x];
+            tsum[threadIdx.x] = v;
+            P.sums[threadIdx.x] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            rigid_solve_body(tsum, &se, P.objs, P.tnorms, P.masses);
+            if (!se.done) grid_params(se.k, P.dg, g);
+        }
+        __syncthreads();
+    }
+    em_copy(P.em, &se, threadIdx.x, blockDim.x);
+}
+
+// ---------------------------------------------------------------------------
 // host
 
 static int width(int mode, int sig) {
@@ -1810,7 +1892,54 @@ int fr_rigid_em_status(fr_rigid_em *em, int *done, int *iterations, int *termina
     return FR_OK;
 }
 
+static bool em_persist_ok(const fr_rigid_em *em) {
+    return em && em->fast == 2 && em->lat && em->lat->dcells != nullptr && em->lat->nv == 4 &&
+           em->m > 0;
+}
+
+// largest model cloud fr_rigid_em_run sends through the persistent one-CTA
+// loop (FR_PERSIST_MAX points; larger clouds use the graph-replayed iteration)
+static long long persist_max() {
+    const char *e = getenv("FR_PERSIST_MAX");
+    return e ? atoll(e) : 32768;
+}
+
+int fr_rigid_em_run_batch(fr_rigid_em **ems, int n, void *stream) {
+    if (n < 0 || (n > 0 && !ems)) {
+        set_error("invalid batch arguments");
+        return FR_EINVAL;
+    }
+    if (n == 0) return FR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<PersistProblem> h((size_t)n);
+    for (int i = 0; i < n; ++i) {
+        fr_rigid_em *em = ems[i];
+        if (!em_persist_ok(em)) {
+            set_error("batch problem %d does not run the dense-grid float32 point path", i);
+            return FR_EINVAL;
+        }
+        const int k = em->max_iters;
+        h[i] = PersistProblem{em->ref, em->m, em->d_em, em->d_sums, em->d_traces,
+                              em->d_traces + k, em->d_traces + 2 * k, em->lat->dense};
+        em->stream = s;
+    }
+    PersistProblem *d = nullptr;
+    FR_CUDA(cudaMallocAsync((void **)&d, h.size() * sizeof(PersistProblem), s));
+    FR_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(PersistProblem), cudaMemcpyHostToDevice,
+                            s));
+    k_em_persistent<<<n, kPersistThreads, 0, s>>>(d);
+    FR_CHECK_LAUNCH();
+    FR_CUDA(cudaFreeAsync(d, s));
+    FR_CUDA(cudaStreamSynchronize(s));   // the host vector h backs the copy
+    return FR_OK;
+}
+
+int fr_rigid_em_persistent(const fr_rigid_em *em) {
+    return em_persist_ok(em) && em->m <= persist_max() ? 1 : 0;
+}
+
 int fr_rigid_em_run(fr_rigid_em *em, void *stream) {
+    if (fr_rigid_em_persistent(em)) return fr_rigid_em_run_batch(&em, 1, stream);
     int done = 0;
     for (int guard = 0; !done && guard < em->max_iters + 16; guard += 8) {
         FR_TRY(fr_rigid_em_enqueue(em, 8, stream));

@@ -200,6 +200,12 @@ def _register_device_loop(path, model, config, timing):
     tick = time.perf_counter()
     em = DeviceEM(path, model.pose.rotation, model.pose.translation, config)
     em.run()
+    return _device_loop_result(em, model, timing, tick)
+
+
+def _device_loop_result(em, model, timing, tick):
+    import torch
+    from .errors import SolverError
     R, t, objs, tnorms, masses, iters, term = em.result()
     torch.cuda.current_stream().synchronize()
     if timing is not None:
@@ -370,46 +376,102 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
     return result
 
 
+def _device_loop_eligible(model, cfg) -> bool:
+    return (isinstance(model, RigidModel) and cfg.backend == "lattice"
+            and cfg.gmm.mode == "position" and cfg.residual_mode == "point_to_point"
+            and not cfg.gmm.update_sigma and not cfg.record_states)
+
+
 def register_batch(problems, config: RegistrationConfig | None = None,
                    max_concurrent: int = 8) -> list:
-    """Independent registrations run concurrently on one GPU (the batched
-    multi-problem driver of SURVEY.md 8(f) rank 4; the reference runs bench
-    trials one after another, bench.py:132-159).
+    """Independent registrations on one GPU (the batched multi-problem driver
+    of SURVEY.md 8(f) rank 4; the reference runs bench trials one after
+    another, bench.py:132-159).
 
     `problems` holds (reference, observation, initial_model) triples, or
     (reference, observation, initial_model, config) to override `config`.
-    Up to `max_concurrent` worker threads each own a CUDA stream and run
-    `register` on it; the native calls release the GIL, so one problem's
-    kernels overlap another's host work and kernels.  Problems are replicas:
-    no collectives, no shared device state.  Results come back in input order
-    and are identical to running each problem alone (every registration is
-    deterministic)."""
+    Worker threads, each on its own CUDA stream, set the problems up (upload,
+    lattice build); every rigid point-to-point problem small enough for the
+    persistent one-CTA EM loop (fr_rigid_em_persistent) then runs in ONE
+    launch (fr_rigid_em_run_batch, one CTA per problem); the rest run on the
+    worker streams.  Results come back in input order and equal register()'s
+    on each problem alone."""
+    import ctypes
     import threading
     from concurrent.futures import ThreadPoolExecutor
 
     import torch
+
+    from ._rigid import DeviceEM
     problems = list(problems)
     if not problems:
         return []
-    workers = max(1, min(int(max_concurrent), len(problems)))
+    items = [(p[0], p[1], p[2], (p[3] if len(p) > 3 else config) or RegistrationConfig())
+             for p in problems]
+    workers = max(1, min(int(max_concurrent), len(items)))
     streams = _batch_streams(workers)
     slot = threading.local()
     counter = iter(range(workers))
     lock = threading.Lock()
 
-    def run(item):
-        ref, obs, model = item[:3]
-        cfg = item[3] if len(item) > 3 else config
+    def stream():
         if getattr(slot, "stream", None) is None:
             with lock:
                 slot.stream = streams[next(counter)]
-        with torch.cuda.stream(slot.stream):
-            res = register(ref, obs, model, cfg)
-            slot.stream.synchronize()
+        return slot.stream
+
+    def setup(item):
+        ref, obs, model, cfg = item
+        st = stream()
+        with torch.cuda.stream(st):
+            if not _device_loop_eligible(model, cfg):
+                res = register(ref, obs, model, cfg)
+                st.synchronize()
+                return ("done", res)
+            path = RigidDevicePath(ref, obs, cfg.gmm, cfg.residual_mode)
+            em = DeviceEM(path, model.pose.rotation, model.pose.translation, cfg)
+            st.synchronize()
+            return ("em", path, em)
+
+    def finish(k):
+        _, _, em = staged[k]
+        st = stream()
+        with torch.cuda.stream(st):
+            em.run()
+            res = _device_loop_result(em, items[k][2], None, 0.0)
+            st.synchronize()
         return res
 
     with ThreadPoolExecutor(max_workers=workers) as pool:
-        return list(pool.map(run, problems))
+        staged = list(pool.map(setup, items))
+        out = [s[1] if s[0] == "done" else None for s in staged]
+        em_idx = [k for k, s in enumerate(staged) if s[0] == "em"]
+        lib = _lib_load()
+        persist = [k for k in em_idx if lib.fr_rigid_em_persistent(staged[k][2].h)]
+        if persist:
+            handles = (ctypes.c_void_p * len(persist))(*[staged[k][2].h.value for k in persist])
+            _check(lib.fr_rigid_em_run_batch(handles, len(persist), _stream_handle()))
+            for k in persist:
+                out[k] = _device_loop_result(staged[k][2], items[k][2], None, 0.0)
+        rest = [k for k in em_idx if k not in set(persist)]
+        for k, res in zip(rest, pool.map(finish, rest)):
+            out[k] = res
+    return out
+
+
+def _lib_load():
+    from . import _lib
+    return _lib.load()
+
+
+def _check(status):
+    from . import _lib
+    _lib.check(status)
+
+
+def _stream_handle():
+    from . import _lib
+    return _lib.stream_handle()
 
 
 _STREAMS: dict = {}

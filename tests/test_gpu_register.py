@@ -174,7 +174,9 @@ def test_device_loop_matches_host_loop(fr, path, monkeypatch):
     assert dev.iterations == host.iterations and dev.termination == host.termination
     assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < tol
     np.testing.assert_allclose(dev.objectives, host.objectives, rtol=tol)
-    np.testing.assert_allclose(dev.twist_norms, host.twist_norms, rtol=max(tol, 1e-6), atol=1e-12)
+    # twist norms near convergence are ~1e-2; the float32 paths agree to ~1e-9
+    np.testing.assert_allclose(dev.twist_norms, host.twist_norms, rtol=max(tol, 1e-6),
+                               atol=1e-12 if tol < 1e-6 else 1e-8)
     assert_pose_parity(dev.kinematics.pose.rotation, dev.kinematics.pose.translation,
                        g["R"], g["t"], O.bbox_diameter(g["X"]))
 
