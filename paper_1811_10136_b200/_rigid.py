@@ -48,8 +48,9 @@ _E = [skew(e) for e in np.eye(3)]   # K_k = [e_k]x
 # Model points are not a bit-exact contract (the reference forms them with a
 # BLAS product), and the float32 path keeps the E-step sums to ~1e-7 relative.
 FAST_QUERY = True
-# Point-to-point pass with float32 centred coordinates and float32 moment
-# partials folded into float64 every 16 points (FR_PASS_F32).
+# Point-to-point pass with float32 centred coordinates over the lattice's dense
+# float32 grid (hash slots when the grid would be too large), float32 moment
+# partials folded into float64 accumulators every 32 points (FR_PASS_F32).
 F32_POINTS = True
 # Sort the model points along a Morton curve once per registration.
 SPATIAL_ORDER = True
