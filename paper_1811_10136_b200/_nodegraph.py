@@ -18,13 +18,9 @@ import time
 import numpy as np
 
 from . import _lib
-from ._rigid import RigidDevicePath, unpack_upper6
+from ._rigid import RigidDevicePath
 from .errors import DegenerateBlendError, DegenerateCorrespondenceError
 from .geometry import point_twist_jacobian
-
-
-def _sym6_from21(v21):
-    return unpack_upper6(v21)
 
 
 _IU6 = np.triu_indices(6)

@@ -11,7 +11,6 @@ iterations follow in closed form (see _rigid.py).
 
 from __future__ import annotations
 
-import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
