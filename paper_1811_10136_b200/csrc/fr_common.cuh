@@ -432,9 +432,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // estep.py:153-165 rotated so the pass forms float32 pairs without moves.
 // The grid spans the sites' q box [a, b] padded by kDensePad cells per side:
 // a query's pre-wrap remainder-0 cell ri and its final vertices differ by at
-// most 2 per coordinate, so every ri in [a - 1, b + 2] addresses inside the
-// grid, and a point outside that range has no site among its vertices.
-constexpr int kDensePad = 3;
+// most 2 per coordinate (vertex cells ri - 2 .. ri + 1), so every ri in
+// [a - 1, b + 2] addresses inside the grid, and a point outside that range has
+// no site among its vertices.  The fourth pad cell lets the pass clamp ri into
+// [a - 2, b + 3] instead of branching: a clamped cell's vertices are all
+// padding (zero rows), exactly as an out-of-range point has no site.
+constexpr int kDensePad = 4;
 
 struct DenseSliceF {
     const float4 *cells;    // [n0][n1][n2][4]

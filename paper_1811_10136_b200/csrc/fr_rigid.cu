@@ -489,6 +489,12 @@ struct GridK {
     int s0, s1;
     unsigned K;             // cell of ri = bits0 * s0 + bits1 * s1 + bits2 + K
     unsigned H;             // h = sum bits + H
+    // quarter-scale / clamped form (k_rigid_pass_grid4): el / 4 directly
+    float2 Q01[3], Q23[3];  // A / 4
+    float2 q01, q23;        // (e0 - 4 base) / 4
+    unsigned Cq[3];         // v = bits(t) + Cq = ri - (a - 2), clamped to limq
+    unsigned limq[3];       // span + 4
+    unsigned Kq;            // cell of ri = v0 * s0 + v1 * s1 + v2 + Kq
 };
 
 constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23
@@ -627,6 +633,17 @@ __device__ __forceinline__ void grid_params(const RigidK &k, const DenseSliceF &
     g.s1 = dg.s1;
     g.K = K;
     g.H = H;
+    // x 0.25 is exact: the quarter-scale path's t, d / 4 and barycentrics
+    // are bit-identical to the unscaled ones
+    for (int c = 0; c < 3; ++c) {
+        g.Q01[c] = make_float2(0.25f * g.A01[c].x, 0.25f * g.A01[c].y);
+        g.Q23[c] = make_float2(0.25f * g.A23[c].x, 0.25f * g.A23[c].y);
+        g.Cq[c] = (unsigned)(base[c] - kMagicBits - (dg.a[c] - 2));
+        g.limq[c] = dg.span[c] + 4u;
+    }
+    g.q01 = make_float2(0.25f * fr0[0], 0.25f * fr0[1]);
+    g.q23 = make_float2(0.25f * fr0[2], 0.25f * fr0[3]);
+    g.Kq = (unsigned)(kDensePad - 2) * (unsigned)(dg.s0 + dg.s1 + 1);
 }
 
 // one model point of the dense-grid pass (valid = 0: the point contributes
@@ -736,6 +753,119 @@ __device__ __forceinline__ void grid_point(float nx, float ny, float nz, bool va
     a.q2 = fmaf(wr2, r2, a.q2);
 }
 
+// base + 16 i as one IMAD.WIDE (keeps ptxas from re-associating the cell and
+// vertex offsets into a 32-bit add plus a sign-extending 64-bit add per gather)
+__device__ __forceinline__ const float4 *wide_ptr16(const float4 *base, unsigned i) {
+    const float4 *r;
+    asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(r) : "r"(i), "l"(base));
+    return r;
+}
+__device__ __forceinline__ const float4 *wide_ptr16s(const float4 *base, int i) {
+    const float4 *r;
+    asm("mad.wide.s32 %0, %1, 16, %2;" : "=l"(r) : "r"(i), "l"(base));
+    return r;
+}
+
+// one model point of the quarter-scale dense-grid pass: as grid_point, with
+// the embedding pre-scaled by 1/4 (t = el/4 + magic, d/4 = el/4 - round(el/4),
+// barycentrics = gaps of the sorted d/4 -- bit-identical, three multiplies
+// fewer), the remainder-0 cell clamped into the zero-padded box instead of a
+// range branch (an outside point reads padding rows: no mass, as the
+// reference's absent sites), and the four gathers addressed from one cell
+// pointer
+__device__ __forceinline__ void grid_point_q(float nx, float ny, float nz, bool valid,
+                                             const GridK &g, const int4 *tab,
+                                             const float4 *__restrict__ cells, GridAcc &a) {
+    const float x0 = nx - g.cref[0], x1 = ny - g.cref[1], x2 = nz - g.cref[2];
+    float2 y01 = __fmul2_rn(g.Rc[0], bc(x0));
+    y01 = __ffma2_rn(g.Rc[1], bc(x1), y01);
+    y01 = __ffma2_rn(g.Rc[2], bc(x2), y01);
+    float2 y2v = __ffma2_rn(g.R2[0], bc(x0), make_float2(0.0f, 1.0f));
+    y2v = __ffma2_rn(g.R2[1], bc(x1), y2v);
+    y2v = __ffma2_rn(g.R2[2], bc(x2), y2v);
+    float2 e01 = __ffma2_rn(g.Q01[0], bc(y01.x), g.q01);
+    e01 = __ffma2_rn(g.Q01[1], bc(y01.y), e01);
+    e01 = __ffma2_rn(g.Q01[2], bc(y2v.x), e01);
+    float2 e23 = __ffma2_rn(g.Q23[0], bc(y01.x), g.q23);
+    e23 = __ffma2_rn(g.Q23[1], bc(y01.y), e23);
+    e23 = __ffma2_rn(g.Q23[2], bc(y2v.x), e23);
+    const float2 t01 = __fadd2_rn(e01, bc(kMagic)), t23 = __fadd2_rn(e23, bc(kMagic));
+    // round(el / 4) = t - magic exactly; d / 4 = el / 4 - round(el / 4) exactly
+    const float2 d01 = __ffma2_rn(__fadd2_rn(t01, bc(-kMagic)), bc(-1.0f), e01);
+    const float2 d23 = __ffma2_rn(__fadd2_rn(t23, bc(-kMagic)), bc(-1.0f), e23);
+    const float d[4] = {d01.x, d01.y, d23.x, d23.y};
+    const int tb[4] = {__float_as_int(t01.x), __float_as_int(t01.y), __float_as_int(t23.x),
+                       __float_as_int(t23.y)};
+    unsigned code = 0;
+    {
+        int q = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i + 1; j < 4; ++j, ++q) code |= (d[j] > d[i] ? 1u : 0u) << q;
+    }
+    float s0 = fmaxf(d[0], d[1]), s1 = fminf(d[0], d[1]);
+    float s2 = fmaxf(d[2], d[3]), s3 = fminf(d[2], d[3]);
+    {
+        const float hi = fmaxf(s0, s2), lo = fminf(s0, s2);
+        s0 = hi;
+        s2 = lo;
+        const float hi2 = fmaxf(s1, s3), lo2 = fminf(s1, s3);
+        s1 = hi2;
+        s3 = lo2;
+        const float hi3 = fmaxf(s1, s2), lo3 = fminf(s1, s2);
+        s1 = hi3;
+        s2 = lo3;
+    }
+    const float b0 = 1.0f + (s3 - s0);
+    const float b1 = s2 - s3, b2 = s1 - s2, b3 = s0 - s1;
+    const int h = (int)((unsigned)tb[0] + (unsigned)tb[1] + (unsigned)tb[2] + (unsigned)tb[3] + g.H);
+    const int hi = min(max(h + 2, 0), 4);
+    const int4 T = tab[code * 5 + hi];
+    const unsigned v0 = min((unsigned)tb[0] + g.Cq[0], g.limq[0]);
+    const unsigned v1 = min((unsigned)tb[1] + g.Cq[1], g.limq[1]);
+    const unsigned v2 = min((unsigned)tb[2] + g.Cq[2], g.limq[2]);
+    const float4 *cb = wide_ptr16(cells, 4u * (v0 * (unsigned)g.s0 + v1 * (unsigned)g.s1 + v2 + g.Kq));
+    const float4 q0 = __ldg(wide_ptr16s(cb, T.x)), q1 = __ldg(wide_ptr16s(cb, T.y));
+    const float4 q2 = __ldg(wide_ptr16s(cb, T.z)), q3 = __ldg(wide_ptr16s(cb, T.w));
+    float2 o01 = __fmul2_rn(bc(b0), make_float2(q0.x, q0.y));
+    float2 o23 = __fmul2_rn(bc(b0), make_float2(q0.z, q0.w));
+    o01 = __ffma2_rn(bc(b1), make_float2(q1.x, q1.y), o01);
+    o23 = __ffma2_rn(bc(b1), make_float2(q1.z, q1.w), o23);
+    o01 = __ffma2_rn(bc(b2), make_float2(q2.x, q2.y), o01);
+    o23 = __ffma2_rn(bc(b2), make_float2(q2.z, q2.w), o23);
+    o01 = __ffma2_rn(bc(b3), make_float2(q3.x, q3.y), o01);
+    o23 = __ffma2_rn(bc(b3), make_float2(q3.z, q3.w), o23);
+    const float m0 = fmaxf(o23.y, 0.0f);
+    const bool sup = m0 >= 1e-12f;
+    // branch-free: both reciprocals unconditionally, then selects (the
+    // c' > 0 test is block-uniform)
+    const float wc = g.cp > 0.0f ? m0 * rcp_approx(m0 + g.cp) : 1.0f;
+    const float w = (sup && valid) ? wc : 0.0f;
+    const float rm = rcp_approx(m0);
+    const float ninv = sup ? -rm : 0.0f;
+    const float2 r01 = __fadd2_rn(y01, __ffma2_rn(o01, bc(ninv), g.cw01));
+    const float r2 = y2v.x + fmaf(o23.x, ninv, g.cw2.x);
+    const float2 wy01 = __fmul2_rn(bc(w), y01);
+    const float2 wy2v = __fmul2_rn(bc(w), y2v);
+    const float2 wr01 = __fmul2_rn(bc(w), r01);
+    const float wr2 = w * r2;
+    a.s1_01 = __fadd2_rn(a.s1_01, wy01);
+    a.s1_2_s0 = __fadd2_rn(a.s1_2_s0, wy2v);
+    a.s2_00_01 = __ffma2_rn(bc(wy01.x), y01, a.s2_00_01);
+    a.s2_02_12 = __ffma2_rn(bc(y2v.x), wy01, a.s2_02_12);
+    a.s2_11 = fmaf(wy01.y, y01.y, a.s2_11);
+    a.s2_22 = fmaf(wy2v.x, y2v.x, a.s2_22);
+    a.rx01[0] = __ffma2_rn(bc(wr01.x), y01, a.rx01[0]);
+    a.rx2_r1[0] = __ffma2_rn(bc(wr01.x), y2v, a.rx2_r1[0]);
+    a.rx01[1] = __ffma2_rn(bc(wr01.y), y01, a.rx01[1]);
+    a.rx2_r1[1] = __ffma2_rn(bc(wr01.y), y2v, a.rx2_r1[1]);
+    a.rx01[2] = __ffma2_rn(bc(wr2), y01, a.rx01[2]);
+    a.rx2_r1[2] = __ffma2_rn(bc(wr2), y2v, a.rx2_r1[2]);
+    a.q01 = __ffma2_rn(wr01, r01, a.q01);
+    a.q2 = fmaf(wr2, r2, a.q2);
+}
+
 // the warp's float32 partials folded into its float64 accumulators: a
 // butterfly reduce-scatter (5 shuffle rounds, 31 adds per lane) leaves lane c
 // holding the warp sum of statistic c, which it adds into wacc[c].  Fixed
@@ -823,6 +953,111 @@ k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const R
         for (int w = 0; w < kPassThreads / 32; ++w) v += wacc[w][threadIdx.x];
         partials[(long long)blockIdx.x * NA + threadIdx.x] = v;
     }
+}
+
+// streaming 16-byte load that leaves L1 to the grid gathers
+__device__ __forceinline__ float4 ld_stream4(const float *p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+// the four consecutive points j .. j + 3 of a chunk (zero past cnt); VEC: the
+// three planes are 16-byte aligned (m % 4 == 0, chunk starts at multiples of 4)
+template <bool VEC>
+__device__ __forceinline__ void load_quad(const float *p0, const float *p1, const float *p2,
+                                          int j, int cnt, float4 &x, float4 &y, float4 &z) {
+    if (VEC && j + 3 < cnt) {
+        x = ld_stream4(p0 + j);
+        y = ld_stream4(p1 + j);
+        z = ld_stream4(p2 + j);
+        return;
+    }
+    float t[3][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool ok = j + k < cnt;
+        t[0][k] = ok ? __ldcs(p0 + j + k) : 0.0f;
+        t[1][k] = ok ? __ldcs(p1 + j + k) : 0.0f;
+        t[2][k] = ok ? __ldcs(p2 + j + k) : 0.0f;
+    }
+    x = make_float4(t[0][0], t[0][1], t[0][2], t[0][3]);
+    y = make_float4(t[1][0], t[1][1], t[1][2], t[1][3]);
+    z = make_float4(t[2][0], t[2][1], t[2][2], t[2][3]);
+}
+
+// dense-grid pass, four consecutive points per thread per trip: 16-byte
+// streaming loads of each plane (one trip ahead in registers, no shared-memory
+// staging), the quarter-scale clamped point (grid_point_q), warp fold every
+// kGridFold points per thread.  Per-block contiguous chunks (multiples of
+// 1024 points) keep a block's gathers in a compact grid region (Morton order).
+constexpr int kQuadPts = 4 * kPassThreads;
+template <bool DEV, bool VEC>
+__global__ void __launch_bounds__(kPassThreads, 2)
+k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
+                   const int *done, DenseSliceF dg, double *__restrict__ partials) {
+    constexpr int NA = kP2PtBase;
+    __shared__ GridK g;
+    __shared__ int4 tab[kGridTab];
+    __shared__ double wacc[kPassThreads / 32][NA];
+    if (DEV && *done) return;
+    if (threadIdx.x == 0) grid_params(DEV ? *kd : kv, dg, g);
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, dg.s0, dg.s1);
+    if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
+    __syncthreads();
+    double *my_wacc = wacc[threadIdx.x >> 5];
+    GridAcc a;
+    a.zero();
+    const long long chunk = ((m + gridDim.x - 1) / gridDim.x + kQuadPts - 1) / kQuadPts * kQuadPts;
+    const long long beg = (long long)blockIdx.x * chunk;
+    const int cnt = (int)max(0ll, min(beg + chunk, m) - beg);
+    const float *p0 = ref + min(beg, m), *p1 = p0 + m, *p2 = p1 + m;
+    const int me = 4 * (int)threadIdx.x;
+    // two register buffers alternate (trip t computes one while the other
+    // receives trip t + 1): no buffer moves
+    float4 ax, ay, az, bx, by, bz;
+    load_quad<VEC>(p0, p1, p2, me, cnt, ax, ay, az);
+    int fold = 0;
+    auto quad = [&](int j, const float4 &cx, const float4 &cy, const float4 &cz) {
+        const int q = j + me;
+        grid_point_q(cx.x, cy.x, cz.x, q < cnt, g, tab, dg.cells, a);
+        grid_point_q(cx.y, cy.y, cz.y, q + 1 < cnt, g, tab, dg.cells, a);
+        grid_point_q(cx.z, cy.z, cz.z, q + 2 < cnt, g, tab, dg.cells, a);
+        grid_point_q(cx.w, cy.w, cz.w, q + 3 < cnt, g, tab, dg.cells, a);
+        fold += 4;
+        if (fold >= kGridFold) {       // warp-uniform trips
+            grid_warp_fold(a, my_wacc);
+            a.zero();
+            fold = 0;
+        }
+    };
+    for (int j = 0; j < cnt; j += 2 * kQuadPts) {
+        if (j + kQuadPts < cnt) load_quad<VEC>(p0, p1, p2, j + kQuadPts + me, cnt, bx, by, bz);
+        quad(j, ax, ay, az);
+        if (j + kQuadPts >= cnt) break;
+        if (j + 2 * kQuadPts < cnt) load_quad<VEC>(p0, p1, p2, j + 2 * kQuadPts + me, cnt, ax, ay, az);
+        quad(j + kQuadPts, bx, by, bz);
+    }
+    grid_warp_fold(a, my_wacc);
+    __syncthreads();
+    if (threadIdx.x < NA) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kPassThreads / 32; ++w) v += wacc[w][threadIdx.x];
+        partials[(long long)blockIdx.x * NA + threadIdx.x] = v;
+    }
+}
+
+// dense-grid pass variant (FR_GRID_KERNEL): 4 = k_rigid_pass_grid4 (default),
+// 3 = the cp.async-ring k_rigid_pass_grid
+static int grid_kernel() {
+    static int v = 0;
+    if (!v) {
+        const char *e = getenv("FR_GRID_KERNEL");
+        v = (e && e[0] == '3') ? 3 : 4;
+    }
+    return v;
 }
 
 // points per thread per ring stage of the dense-grid pass (FR_GRID_PTS):
@@ -1473,6 +1708,19 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         const SliceTableF tf = lat->table_f();
         const DenseSliceF dg = lat->dense;
         if (lat->dcells != nullptr) {
+            if (grid_kernel() == 4) {
+                const int g4 = 2 * sm_count();
+                const bool vec = (m & 3) == 0;
+#define FR_GRID4(DEV, VEC) \
+    k_rigid_pass_grid4<DEV, VEC><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch)
+                if (vec) { if (dev) FR_GRID4(true, true); else FR_GRID4(false, true); }
+                else { if (dev) FR_GRID4(true, false); else FR_GRID4(false, false); }
+#undef FR_GRID4
+                FR_CHECK_LAUNCH();
+                k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g4, kP2PtBase, sums, done);
+                FR_CHECK_LAUNCH();
+                return FR_OK;
+            }
             const int pts = grid_pts();
             const int g3 = pts == 1 ? 4 * sm_count() : (pts == 3 ? 2 : grid_minb()) * sm_count();
 #define FR_GRID(DEV, P, B) \
