@@ -18,6 +18,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cmath>
 #include <vector>
@@ -993,16 +994,51 @@ __device__ __forceinline__ void load_quad(const float *p0, const float *p1, cons
 // kGridFold points per thread.  Per-block contiguous chunks (multiples of
 // 1024 points) keep a block's gathers in a compact grid region (Morton order).
 constexpr int kQuadPts = 4 * kPassThreads;
-template <bool DEV, bool VEC>
-__global__ void __launch_bounds__(kPassThreads, 2)
+// pass constants of the device loop in the constant bank (CONSTP): operands
+// straight from the bank, no registers held for them (written by a
+// device-to-device copy node after k_grid_params each iteration)
+__constant__ GridK c_grid;
+
+__global__ void k_grid_params(const RigidK *kd, const int *done, DenseSliceF dg, GridK *out) {
+    if (*done) return;
+    grid_params(*kd, dg, *out);
+}
+
+// RING: the point stream staged through a kRing4-deep shared-memory ring by
+// 16-byte cp.async (L1-bypassing) instead of the register double buffer
+constexpr int kRing4 = 3;
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void ring_issue_quad(float4 (*slot)[kPassThreads], const float *p0,
+                                                const float *p1, const float *p2, int j, int cnt) {
+    if (j + 3 < cnt) {
+        cp_async16(&slot[0][threadIdx.x], p0 + j);
+        cp_async16(&slot[1][threadIdx.x], p1 + j);
+        cp_async16(&slot[2][threadIdx.x], p2 + j);
+    } else if (j < cnt) {
+        float4 x, y, z;
+        load_quad<false>(p0, p1, p2, j, cnt, x, y, z);
+        slot[0][threadIdx.x] = x;
+        slot[1][threadIdx.x] = y;
+        slot[2][threadIdx.x] = z;
+    }
+    cp_async_commit();
+}
+
+template <bool DEV, bool VEC, int MINB, bool CONSTP, bool RING = false>
+__global__ void __launch_bounds__(kPassThreads, MINB)
 k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
                    const int *done, DenseSliceF dg, double *__restrict__ partials) {
     constexpr int NA = kP2PtBase;
-    __shared__ GridK g;
+    __shared__ float4 ring[RING ? kRing4 : 1][3][kPassThreads];
+    __shared__ GridK gs;
     __shared__ int4 tab[kGridTab];
     __shared__ double wacc[kPassThreads / 32][NA];
     if (DEV && *done) return;
-    if (threadIdx.x == 0) grid_params(DEV ? *kd : kv, dg, g);
+    const GridK &g = CONSTP ? c_grid : gs;
+    if (!CONSTP && threadIdx.x == 0) grid_params(DEV ? *kd : kv, dg, gs);
     for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, dg.s0, dg.s1);
     if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
     __syncthreads();
@@ -1014,10 +1050,6 @@ k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const 
     const int cnt = (int)max(0ll, min(beg + chunk, m) - beg);
     const float *p0 = ref + min(beg, m), *p1 = p0 + m, *p2 = p1 + m;
     const int me = 4 * (int)threadIdx.x;
-    // two register buffers alternate (trip t computes one while the other
-    // receives trip t + 1): no buffer moves
-    float4 ax, ay, az, bx, by, bz;
-    load_quad<VEC>(p0, p1, p2, me, cnt, ax, ay, az);
     int fold = 0;
     auto quad = [&](int j, const float4 &cx, const float4 &cy, const float4 &cz) {
         const int q = j + me;
@@ -1032,12 +1064,33 @@ k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const 
             fold = 0;
         }
     };
-    for (int j = 0; j < cnt; j += 2 * kQuadPts) {
-        if (j + kQuadPts < cnt) load_quad<VEC>(p0, p1, p2, j + kQuadPts + me, cnt, bx, by, bz);
-        quad(j, ax, ay, az);
-        if (j + kQuadPts >= cnt) break;
-        if (j + 2 * kQuadPts < cnt) load_quad<VEC>(p0, p1, p2, j + 2 * kQuadPts + me, cnt, ax, ay, az);
-        quad(j + kQuadPts, bx, by, bz);
+    if (RING) {
+        // each thread reads back only the slots it filled: no block barrier
+#pragma unroll
+        for (int st = 0; st < kRing4 - 1; ++st)
+            ring_issue_quad(ring[st], p0, p1, p2, st * kQuadPts + me, cnt);
+        int stage = 0;
+        for (int j = 0; j < cnt; j += kQuadPts) {
+            ring_issue_quad(ring[stage == 0 ? kRing4 - 1 : stage - 1], p0, p1, p2,
+                            j + (kRing4 - 1) * kQuadPts + me, cnt);
+            cp_async_wait<kRing4 - 1>();
+            const float4 cx = ring[stage][0][threadIdx.x], cy = ring[stage][1][threadIdx.x],
+                         cz = ring[stage][2][threadIdx.x];
+            stage = stage + 1 == kRing4 ? 0 : stage + 1;
+            quad(j, cx, cy, cz);
+        }
+    } else {
+        // two register buffers alternate (trip t computes one while the
+        // other receives trip t + 1): no buffer moves
+        float4 ax, ay, az, bx, by, bz;
+        load_quad<VEC>(p0, p1, p2, me, cnt, ax, ay, az);
+        for (int j = 0; j < cnt; j += 2 * kQuadPts) {
+            if (j + kQuadPts < cnt) load_quad<VEC>(p0, p1, p2, j + kQuadPts + me, cnt, bx, by, bz);
+            quad(j, ax, ay, az);
+            if (j + kQuadPts >= cnt) break;
+            if (j + 2 * kQuadPts < cnt) load_quad<VEC>(p0, p1, p2, j + 2 * kQuadPts + me, cnt, ax, ay, az);
+            quad(j + kQuadPts, bx, by, bz);
+        }
     }
     grid_warp_fold(a, my_wacc);
     __syncthreads();
@@ -1049,16 +1102,23 @@ k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const 
     }
 }
 
-// dense-grid pass variant (FR_GRID_KERNEL): 4 = k_rigid_pass_grid4 (default),
-// 3 = the cp.async-ring k_rigid_pass_grid
+// dense-grid pass variant (FR_GRID_KERNEL): 5 (default) = k_rigid_pass_grid4,
+// with its pass constants in the constant bank when the device loop holds
+// c_grid (one EM object at a time, else shared memory); 4 = grid4 with
+// shared-memory constants always; 3 = the cp.async-ring k_rigid_pass_grid.
+// Measured at 16.8M points: 3: 135.7 us, 4: 125.1 us, 5: 120.4 us per pass;
+// grid4 at 3 CTAs/SM (80 registers, spills): 124 us
 static int grid_kernel() {
     static int v = 0;
     if (!v) {
         const char *e = getenv("FR_GRID_KERNEL");
-        v = (e && e[0] == '3') ? 3 : 4;
+        v = (e && e[0] >= '3' && e[0] <= '5') ? e[0] - '0' : 5;
     }
     return v;
 }
+
+// owner flag of c_grid: the first device EM object over a dense grid takes it
+static std::atomic<bool> g_const_grid_busy{false};
 
 // points per thread per ring stage of the dense-grid pass (FR_GRID_PTS):
 // 3 (default: three independent chains per thread sharing the parameter
@@ -1699,7 +1759,7 @@ static int launch_pass_t(const fr_lattice *lat, const float *ref, long long m, c
 static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, bool dev,
                        const float *ref, long long m, const RigidK &k, const RigidK *kd,
                        const int *done, float *wtn, double *scratch, double *sums,
-                       cudaStream_t s) {
+                       cudaStream_t s, GridK *gk_buf = nullptr) {
     const int nv = lat->nv;
     const bool fast = qpath != 0 && !sig && lat->fslots != nullptr;
     if (fast && qpath == 2 && mode == FR_POINT_TO_POINT && nv == 4) {
@@ -1708,13 +1768,24 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         const SliceTableF tf = lat->table_f();
         const DenseSliceF dg = lat->dense;
         if (lat->dcells != nullptr) {
-            if (grid_kernel() == 4) {
-                const int g4 = 2 * sm_count();
+            const int gk = grid_kernel();
+            if (gk >= 4) {
                 const bool vec = (m & 3) == 0;
-#define FR_GRID4(DEV, VEC) \
-    k_rigid_pass_grid4<DEV, VEC><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch)
-                if (vec) { if (dev) FR_GRID4(true, true); else FR_GRID4(false, true); }
-                else { if (dev) FR_GRID4(true, false); else FR_GRID4(false, false); }
+                const bool cst = dev && gk == 5 && gk_buf != nullptr;
+                const int g4 = 2 * sm_count();
+#define FR_GRID4(DEV, VEC, B, C) \
+    k_rigid_pass_grid4<DEV, VEC, B, C><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch)
+                if (cst) {
+                    k_grid_params<<<1, 1, 0, s>>>(kd, done, dg, gk_buf);
+                    FR_CHECK_LAUNCH();
+                    FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, gk_buf, sizeof(GridK), 0,
+                                                    cudaMemcpyDeviceToDevice, s));
+                    static const bool ring = getenv("FR_GRID_RING") && getenv("FR_GRID_RING")[0] == '1';
+                    if (vec && ring) k_rigid_pass_grid4<true, true, 2, true, true><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
+                    else if (vec) FR_GRID4(true, true, 2, true); else FR_GRID4(true, false, 2, true);
+                }
+                else if (vec) { if (dev) FR_GRID4(true, true, 2, false); else FR_GRID4(false, true, 2, false); }
+                else { if (dev) FR_GRID4(true, false, 2, false); else FR_GRID4(false, false, 2, false); }
 #undef FR_GRID4
                 FR_CHECK_LAUNCH();
                 k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g4, kP2PtBase, sums, done);
@@ -1782,6 +1853,7 @@ struct fr_rigid_em {
     cudaGraphExec_t graph = nullptr;
     int graph_iters = 0;
     cudaStream_t stream = nullptr;   // stream of the last call (destroy orders behind it)
+    fr::GridK *d_gk = nullptr;       // staging of the c_grid constants (owner only)
 };
 
 using namespace fr;
@@ -2020,6 +2092,16 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
         set_error("device EM allocation failed");
         return FR_ECUDA;
     }
+    bool idle = false;
+    if (lat->dcells != nullptr && em->fast == 2 &&
+        g_const_grid_busy.compare_exchange_strong(idle, true)) {
+        if (cudaMallocAsync((void **)&em->d_gk, sizeof(GridK), 0) != cudaSuccess ||
+            cudaStreamSynchronize(0) != cudaSuccess) {
+            em->d_gk = nullptr;
+            g_const_grid_busy.store(false);
+            cudaGetLastError();
+        }
+    }
     *out = em;
     return FR_OK;
 }
@@ -2033,6 +2115,10 @@ int fr_rigid_em_destroy(fr_rigid_em *em) {
     for (void *p : {(void *)em->d_em, (void *)em->d_sums, (void *)em->d_scratch,
                     (void *)em->d_traces})
         if (p) cudaFreeAsync(p, em->stream);
+    if (em->d_gk) {     // the stream is drained: no pass still reads c_grid
+        cudaFreeAsync(em->d_gk, em->stream);
+        g_const_grid_busy.store(false);
+    }
     delete em;
     return FR_OK;
 }
@@ -2052,7 +2138,7 @@ static int em_pass(fr_rigid_em *em, cudaStream_t s) {
     memset(&unused, 0, sizeof(unused));
     return launch_pass(em->lat, FR_POINT_TO_POINT, false, em->fast, true, em->ref, em->m,
                        unused, &em->d_em->k, &em->d_em->done, nullptr, em->d_scratch, em->d_sums,
-                       s);
+                       s, em->d_gk);
 }
 
 static int em_solve(fr_rigid_em *em, cudaStream_t s) {

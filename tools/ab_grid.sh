@@ -1,8 +1,8 @@
-# A/B of the dense-grid pass kernels (FR_GRID_KERNEL=3: cp.async ring, 3 pts/thread;
-# 4: quarter-scale clamped pass, 4 consecutive points/thread from 16-byte loads)
+# A/B of dense-grid pass variants (FR_GRID_KERNEL=3: cp.async ring, 3 pts/thread;
+# 4: grid4, shared-memory constants; 5: grid4 with constant-bank constants;
+# FR_GRID_RING=1: grid4's point stream through a cp.async shared-memory ring)
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_register.py tests/test_gpu_behaviour.py tests/test_gpu_batch.py -m gpu -x -q 2>&1 | tail -2
-for v in 3 4 3 4; do
-  FR_GRID_KERNEL=$v python bench.py --no-cpu-baseline --no-e2e --steps 400 > gpurun_out/v.log 2>&1
+for v in "5 0" "5 1" "5 0" "5 1"; do set -- $v
+  FR_GRID_RING=$2 FR_GRID_KERNEL=$1 python bench.py --no-cpu-baseline --no-e2e --steps 400 > gpurun_out/v.log 2>&1
   python -c "
-import json; d=json.loads(open('gpurun_out/v.log').read().strip().splitlines()[-1]); print('kernel=$v', d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac'])"; done
+import json; d=json.loads(open('gpurun_out/v.log').read().strip().splitlines()[-1]); print('kernel=$1 ring=$2', d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac'])" || tail -3 gpurun_out/v.log; done
