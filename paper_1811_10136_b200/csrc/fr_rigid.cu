@@ -21,6 +21,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "fr_reduce.cuh"
@@ -566,6 +567,15 @@ __device__ __forceinline__ int4 grid_entry(int e, int s0, int s1) {
     return make_int4(rot[0], rot[1], rot[2], rot[3]);
 }
 
+// grid_entry for a comparison code whose six pair bits are stored reversed
+// (pair (0,1) in bit 5), as grid_point_q forms it
+__device__ __forceinline__ int4 grid_entry_q(int e, int s0, int s1) {
+    const int code = e / 5, hi = e % 5;
+    int rev = 0;
+    for (int b = 0; b < 6; ++b) rev |= ((code >> b) & 1) << (5 - b);
+    return grid_entry(rev * 5 + hi, s0, s1);
+}
+
 __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
 
 // float32 pair accumulators -> the 25 float64 columns (layout of _rigid.py)
@@ -797,14 +807,14 @@ __device__ __forceinline__ void grid_point_q(float nx, float ny, float nz, bool 
     const float d[4] = {d01.x, d01.y, d23.x, d23.y};
     const int tb[4] = {__float_as_int(t01.x), __float_as_int(t01.y), __float_as_int(t23.x),
                        __float_as_int(t23.y)};
-    unsigned code = 0;
-    {
-        int q = 0;
+    // comparison code: the sign bit of d[i] - d[j] (set iff d[j] > d[i]; a
+    // tie gives +0, unset) shifted in by one funnel shift per pair, pair
+    // (0,1) ending in bit 5 (grid_entry_q reverses the bit order)
+    const float2 dd = __fadd2_rn(d01, make_float2(-d23.x, -d23.y));   // (d0 - d2, d1 - d3)
+    const float df[6] = {d[0] - d[1], dd.x, d[0] - d[3], d[1] - d[2], dd.y, d[2] - d[3]};
+    unsigned code = __float_as_uint(df[0]) >> 31;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = i + 1; j < 4; ++j, ++q) code |= (d[j] > d[i] ? 1u : 0u) << q;
-    }
+    for (int q = 1; q < 6; ++q) code = __funnelshift_l(__float_as_uint(df[q]), code, 1);
     float s0 = fmaxf(d[0], d[1]), s1 = fminf(d[0], d[1]);
     float s2 = fmaxf(d[2], d[3]), s3 = fminf(d[2], d[3]);
     {
@@ -1027,7 +1037,7 @@ __device__ __forceinline__ void ring_issue_quad(float4 (*slot)[kPassThreads], co
     cp_async_commit();
 }
 
-template <bool DEV, bool VEC, int MINB, bool CONSTP, bool RING = false>
+template <bool DEV, bool VEC, int MINB, bool CONSTP, bool RING = false, int FOLD = kGridFold>
 __global__ void __launch_bounds__(kPassThreads, MINB)
 k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
                    const int *done, DenseSliceF dg, double *__restrict__ partials) {
@@ -1039,7 +1049,7 @@ k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const 
     if (DEV && *done) return;
     const GridK &g = CONSTP ? c_grid : gs;
     if (!CONSTP && threadIdx.x == 0) grid_params(DEV ? *kd : kv, dg, gs);
-    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, dg.s0, dg.s1);
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry_q(e, dg.s0, dg.s1);
     if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
     __syncthreads();
     double *my_wacc = wacc[threadIdx.x >> 5];
@@ -1051,18 +1061,24 @@ k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const 
     const float *p0 = ref + min(beg, m), *p1 = p0 + m, *p2 = p1 + m;
     const int me = 4 * (int)threadIdx.x;
     int fold = 0;
-    auto quad = [&](int j, const float4 &cx, const float4 &cy, const float4 &cz) {
+    // a trip is full (every point valid) except possibly the block's last
+    auto quad_t = [&](auto full, int j, const float4 &cx, const float4 &cy, const float4 &cz) {
+        constexpr bool F = decltype(full)::value;
         const int q = j + me;
-        grid_point_q(cx.x, cy.x, cz.x, q < cnt, g, tab, dg.cells, a);
-        grid_point_q(cx.y, cy.y, cz.y, q + 1 < cnt, g, tab, dg.cells, a);
-        grid_point_q(cx.z, cy.z, cz.z, q + 2 < cnt, g, tab, dg.cells, a);
-        grid_point_q(cx.w, cy.w, cz.w, q + 3 < cnt, g, tab, dg.cells, a);
+        grid_point_q(cx.x, cy.x, cz.x, F || q < cnt, g, tab, dg.cells, a);
+        grid_point_q(cx.y, cy.y, cz.y, F || q + 1 < cnt, g, tab, dg.cells, a);
+        grid_point_q(cx.z, cy.z, cz.z, F || q + 2 < cnt, g, tab, dg.cells, a);
+        grid_point_q(cx.w, cy.w, cz.w, F || q + 3 < cnt, g, tab, dg.cells, a);
         fold += 4;
-        if (fold >= kGridFold) {       // warp-uniform trips
+        if (fold >= FOLD) {       // warp-uniform trips
             grid_warp_fold(a, my_wacc);
             a.zero();
             fold = 0;
         }
+    };
+    auto quad = [&](int j, const float4 &cx, const float4 &cy, const float4 &cz) {
+        if (j + kQuadPts <= cnt) quad_t(std::true_type{}, j, cx, cy, cz);
+        else quad_t(std::false_type{}, j, cx, cy, cz);
     };
     if (RING) {
         // each thread reads back only the slots it filled: no block barrier
@@ -1780,9 +1796,10 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
                     FR_CHECK_LAUNCH();
                     FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, gk_buf, sizeof(GridK), 0,
                                                     cudaMemcpyDeviceToDevice, s));
-                    static const bool ring = getenv("FR_GRID_RING") && getenv("FR_GRID_RING")[0] == '1';
-                    if (vec && ring) k_rigid_pass_grid4<true, true, 2, true, true><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
-                    else if (vec) FR_GRID4(true, true, 2, true); else FR_GRID4(true, false, 2, true);
+                    static const bool fold64 = getenv("FR_GRID_FOLD") && atoi(getenv("FR_GRID_FOLD")) == 64;
+                    if (vec && fold64) k_rigid_pass_grid4<true, true, 2, true, true, 64><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
+                    else if (vec) k_rigid_pass_grid4<true, true, 2, true, true><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
+                    else FR_GRID4(true, false, 2, true);
                 }
                 else if (vec) { if (dev) FR_GRID4(true, true, 2, false); else FR_GRID4(false, true, 2, false); }
                 else { if (dev) FR_GRID4(true, false, 2, false); else FR_GRID4(false, false, 2, false); }
