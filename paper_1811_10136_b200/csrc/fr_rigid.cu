@@ -784,10 +784,14 @@ __device__ __forceinline__ const float4 *wide_ptr16s(const float4 *base, int i) 
 // range branch (an outside point reads padding rows: no mass, as the
 // reference's absent sites), and the four gathers addressed from one cell
 // pointer
+template <bool CENTRED = false>
 __device__ __forceinline__ void grid_point_q(float nx, float ny, float nz, bool valid,
                                              const GridK &g, const int4 *tab,
                                              const float4 *__restrict__ cells, GridAcc &a) {
-    const float x0 = nx - g.cref[0], x1 = ny - g.cref[1], x2 = nz - g.cref[2];
+    // CENTRED: the caller's coordinates are already x - (float)c_ref
+    const float x0 = CENTRED ? nx : nx - g.cref[0];
+    const float x1 = CENTRED ? ny : ny - g.cref[1];
+    const float x2 = CENTRED ? nz : nz - g.cref[2];
     float2 y01 = __fmul2_rn(g.Rc[0], bc(x0));
     y01 = __ffma2_rn(g.Rc[1], bc(x1), y01);
     y01 = __ffma2_rn(g.Rc[2], bc(x2), y01);
@@ -1107,6 +1111,110 @@ k_rigid_pass_grid4(const float *__restrict__ ref, long long m, RigidK kv, const 
             if (j + 2 * kQuadPts < cnt) load_quad<VEC>(p0, p1, p2, j + 2 * kQuadPts + me, cnt, ax, ay, az);
             quad(j + kQuadPts, bx, by, bz);
         }
+    }
+    grid_warp_fold(a, my_wacc);
+    __syncthreads();
+    if (threadIdx.x < NA) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kPassThreads / 32; ++w) v += wacc[w][threadIdx.x];
+        partials[(long long)blockIdx.x * NA + threadIdx.x] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tiled dense-grid pass of the device loop: the EM object's model points,
+// centred once (x - (float)c_ref: the same float32 subtraction the point
+// kernels make per pass) and laid out as tiles of 1024 points, each tile
+// [3][256] float4 (thread t's four consecutive points per plane).  One tile is
+// one trip of the block: three 16-byte cp.async at immediate offsets from a
+// pointer that advances 12 KB per trip (no per-trip 64-bit plane arithmetic),
+// no centring adds in the point chain.
+constexpr int kTileF4 = 3 * kPassThreads;   // float4 per tile
+
+__global__ void k_tile_points(const float *__restrict__ ref, long long m, float c0, float c1,
+                              float c2, float4 *__restrict__ tiles, long long ntiles) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // quad index
+    if (i >= ntiles * kPassThreads) return;
+    const long long t = i / kPassThreads, lane = i % kPassThreads, p = 4 * i;
+    const float c[3] = {c0, c1, c2};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = p + k < m ? ref[d * m + p + k] - c[d] : 0.0f;
+        tiles[t * kTileF4 + d * kPassThreads + lane] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+template <int FOLD = kGridFold>
+__global__ void __launch_bounds__(kPassThreads, 2)
+k_rigid_pass_tiles(const float4 *__restrict__ tiles, long long m, const int *done, DenseSliceF dg,
+                   double *__restrict__ partials) {
+    constexpr int NA = kP2PtBase;
+    __shared__ float4 ring[kRing4][3][kPassThreads];
+    __shared__ int4 tab[kGridTab];
+    __shared__ double wacc[kPassThreads / 32][NA];
+    if (*done) return;
+    const GridK &g = c_grid;
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry_q(e, dg.s0, dg.s1);
+    if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
+    __syncthreads();
+    double *my_wacc = wacc[threadIdx.x >> 5];
+    GridAcc a;
+    a.zero();
+    const long long ntiles = (m + kQuadPts - 1) / kQuadPts;
+    const long long tpb = (ntiles + gridDim.x - 1) / gridDim.x;
+    const long long t0 = (long long)blockIdx.x * tpb;
+    const int nt = (int)max(0ll, min(t0 + tpb, ntiles) - t0);
+    // points of this block's tiles that exist: the last tile of the cloud may
+    // be partial (its padding is zeros, which are real coordinates: masked)
+    const long long first = t0 * kQuadPts;
+    const int cnt = (int)max(0ll, min((long long)nt * kQuadPts, m - first));
+    const float4 *src = tiles + t0 * kTileF4 + threadIdx.x;
+    const int me = 4 * (int)threadIdx.x;
+    int fold = 0;
+    auto quad_t = [&](auto full, int j, const float4 &cx, const float4 &cy, const float4 &cz) {
+        constexpr bool F = decltype(full)::value;
+        const int q = j + me;
+        grid_point_q<true>(cx.x, cy.x, cz.x, F || q < cnt, g, tab, dg.cells, a);
+        grid_point_q<true>(cx.y, cy.y, cz.y, F || q + 1 < cnt, g, tab, dg.cells, a);
+        grid_point_q<true>(cx.z, cy.z, cz.z, F || q + 2 < cnt, g, tab, dg.cells, a);
+        grid_point_q<true>(cx.w, cy.w, cz.w, F || q + 3 < cnt, g, tab, dg.cells, a);
+        fold += 4;
+        if (fold >= FOLD) {       // warp-uniform trips
+            grid_warp_fold(a, my_wacc);
+            a.zero();
+            fold = 0;
+        }
+    };
+#pragma unroll
+    for (int st = 0; st < kRing4 - 1; ++st) {
+        if (st < nt) {
+            cp_async16(&ring[st][0][threadIdx.x], src + st * kTileF4);
+            cp_async16(&ring[st][1][threadIdx.x], src + st * kTileF4 + kPassThreads);
+            cp_async16(&ring[st][2][threadIdx.x], src + st * kTileF4 + 2 * kPassThreads);
+        }
+        cp_async_commit();
+    }
+    const float4 *nxt = src + (kRing4 - 1) * kTileF4;
+    int stage = 0;
+    for (int t = 0; t < nt; ++t) {
+        const int ws = stage == 0 ? kRing4 - 1 : stage - 1;
+        if (t + kRing4 - 1 < nt) {
+            cp_async16(&ring[ws][0][threadIdx.x], nxt);
+            cp_async16(&ring[ws][1][threadIdx.x], nxt + kPassThreads);
+            cp_async16(&ring[ws][2][threadIdx.x], nxt + 2 * kPassThreads);
+        }
+        cp_async_commit();
+        nxt += kTileF4;
+        cp_async_wait<kRing4 - 1>();
+        const float4 cx = ring[stage][0][threadIdx.x], cy = ring[stage][1][threadIdx.x],
+                     cz = ring[stage][2][threadIdx.x];
+        stage = stage + 1 == kRing4 ? 0 : stage + 1;
+        const int j = t * kQuadPts;
+        if (j + kQuadPts <= cnt) quad_t(std::true_type{}, j, cx, cy, cz);
+        else quad_t(std::false_type{}, j, cx, cy, cz);
     }
     grid_warp_fold(a, my_wacc);
     __syncthreads();
@@ -1775,7 +1883,8 @@ static int launch_pass_t(const fr_lattice *lat, const float *ref, long long m, c
 static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, bool dev,
                        const float *ref, long long m, const RigidK &k, const RigidK *kd,
                        const int *done, float *wtn, double *scratch, double *sums,
-                       cudaStream_t s, GridK *gk_buf = nullptr) {
+                       cudaStream_t s, GridK *gk_buf = nullptr,
+                       const float4 *tiles = nullptr) {
     const int nv = lat->nv;
     const bool fast = qpath != 0 && !sig && lat->fslots != nullptr;
     if (fast && qpath == 2 && mode == FR_POINT_TO_POINT && nv == 4) {
@@ -1797,7 +1906,8 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
                     FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, gk_buf, sizeof(GridK), 0,
                                                     cudaMemcpyDeviceToDevice, s));
                     static const bool fold64 = getenv("FR_GRID_FOLD") && atoi(getenv("FR_GRID_FOLD")) == 64;
-                    if (vec && fold64) k_rigid_pass_grid4<true, true, 2, true, true, 64><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
+                    if (tiles) k_rigid_pass_tiles<><<<g4, kPassThreads, 0, s>>>(tiles, m, done, dg, scratch);
+                    else if (vec && fold64) k_rigid_pass_grid4<true, true, 2, true, true, 64><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
                     else if (vec) k_rigid_pass_grid4<true, true, 2, true, true><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
                     else FR_GRID4(true, false, 2, true);
                 }
@@ -1871,6 +1981,7 @@ struct fr_rigid_em {
     int graph_iters = 0;
     cudaStream_t stream = nullptr;   // stream of the last call (destroy orders behind it)
     fr::GridK *d_gk = nullptr;       // staging of the c_grid constants (owner only)
+    float4 *d_tiles = nullptr;       // centred tiled model points (owner only)
 };
 
 using namespace fr;
@@ -2112,12 +2223,25 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
     bool idle = false;
     if (lat->dcells != nullptr && em->fast == 2 &&
         g_const_grid_busy.compare_exchange_strong(idle, true)) {
+        const long long ntiles = (m + kQuadPts - 1) / kQuadPts;
+        const bool tiled = !(getenv("FR_GRID_TILES") && getenv("FR_GRID_TILES")[0] == '0');
         if (cudaMallocAsync((void **)&em->d_gk, sizeof(GridK), 0) != cudaSuccess ||
-            cudaStreamSynchronize(0) != cudaSuccess) {
+            (tiled && cudaMallocAsync((void **)&em->d_tiles, (size_t)ntiles * kTileF4 * sizeof(float4),
+                                      0) != cudaSuccess)) {
+            cudaStreamSynchronize(0);
+            if (em->d_gk) cudaFreeAsync(em->d_gk, 0);
+            if (em->d_tiles) cudaFreeAsync(em->d_tiles, 0);
             em->d_gk = nullptr;
+            em->d_tiles = nullptr;
             g_const_grid_busy.store(false);
             cudaGetLastError();
+        } else if (tiled) {
+            const long long quads = ntiles * kPassThreads;
+            k_tile_points<<<(unsigned)((quads + 255) / 256), 256, 0, 0>>>(
+                ref, m, (float)cfg->c_ref[0], (float)cfg->c_ref[1], (float)cfg->c_ref[2],
+                em->d_tiles, ntiles);
         }
+        cudaStreamSynchronize(0);
     }
     *out = em;
     return FR_OK;
@@ -2132,6 +2256,7 @@ int fr_rigid_em_destroy(fr_rigid_em *em) {
     for (void *p : {(void *)em->d_em, (void *)em->d_sums, (void *)em->d_scratch,
                     (void *)em->d_traces})
         if (p) cudaFreeAsync(p, em->stream);
+    if (em->d_tiles) cudaFreeAsync(em->d_tiles, em->stream);
     if (em->d_gk) {     // the stream is drained: no pass still reads c_grid
         cudaFreeAsync(em->d_gk, em->stream);
         g_const_grid_busy.store(false);
@@ -2155,7 +2280,7 @@ static int em_pass(fr_rigid_em *em, cudaStream_t s) {
     memset(&unused, 0, sizeof(unused));
     return launch_pass(em->lat, FR_POINT_TO_POINT, false, em->fast, true, em->ref, em->m,
                        unused, &em->d_em->k, &em->d_em->done, nullptr, em->d_scratch, em->d_sums,
-                       s, em->d_gk);
+                       s, em->d_gk, em->d_tiles);
 }
 
 static int em_solve(fr_rigid_em *em, cudaStream_t s) {
