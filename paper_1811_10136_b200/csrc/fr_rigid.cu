@@ -1147,10 +1147,25 @@ __global__ void k_tile_points(const float *__restrict__ ref, long long m, float 
     }
 }
 
-template <int FOLD = kGridFold>
-__global__ void __launch_bounds__(kPassThreads, 2)
+// the tiled pass's fused tail: the last block to finish reduces the block
+// partials (the fixed order of k_reduce_cols) into sums and, with SOLVE, runs
+// the iteration's float64 solve and writes the next pose's pass constants --
+// one kernel per EM iteration instead of pass + reduction + solver
+struct EmDev;
+struct TailArgs {
+    unsigned *counter;      // zero between launches (the last block resets it)
+    double *sums;
+    EmDev *em;              // SOLVE only
+    double *objs, *tnorms, *masses;
+    GridK *gk_out;          // next iteration's pass constants (SOLVE only)
+};
+template <bool SOLVE>
+__device__ void pass_tail(const double *partials, DenseSliceF dg, const TailArgs &ta);
+
+template <int FOLD = kGridFold, int MINB = 2, bool SOLVE = false>
+__global__ void __launch_bounds__(kPassThreads, MINB)
 k_rigid_pass_tiles(const float4 *__restrict__ tiles, long long m, const int *done, DenseSliceF dg,
-                   double *__restrict__ partials) {
+                   double *__restrict__ partials, TailArgs ta) {
     constexpr int NA = kP2PtBase;
     __shared__ float4 ring[kRing4][3][kPassThreads];
     __shared__ int4 tab[kGridTab];
@@ -1224,6 +1239,7 @@ k_rigid_pass_tiles(const float4 *__restrict__ tiles, long long m, const int *don
         for (int w = 0; w < kPassThreads / 32; ++w) v += wacc[w][threadIdx.x];
         partials[(long long)blockIdx.x * NA + threadIdx.x] = v;
     }
+    pass_tail<SOLVE>(partials, dg, ta);
 }
 
 // dense-grid pass variant (FR_GRID_KERNEL): 5 (default) = k_rigid_pass_grid4,
@@ -1768,14 +1784,72 @@ __device__ __forceinline__ void em_copy(EmDev *dst, const EmDev *src, int lane, 
 }
 
 __global__ void k_rigid_solve(const double *sums, EmDev *e, double *objs, double *tnorms,
-                              double *masses) {
+                              double *masses, DenseSliceF dg = DenseSliceF{},
+                              GridK *gk_out = nullptr) {
     __shared__ EmDev se;
     if (e->done) return;
     em_copy(&se, e, threadIdx.x, blockDim.x);
     __syncthreads();
-    if (threadIdx.x == 0) rigid_solve_body(sums, &se, objs, tnorms, masses);
+    if (threadIdx.x == 0) {
+        rigid_solve_body(sums, &se, objs, tnorms, masses);
+        if (gk_out && !se.done) grid_params(se.k, dg, *gk_out);
+    }
     __syncthreads();
     em_copy(e, &se, threadIdx.x, blockDim.x);
+}
+
+template <bool SOLVE>
+__device__ void pass_tail(const double *partials, DenseSliceF dg, const TailArgs &ta) {
+    constexpr int NA = kP2PtBase;
+    __shared__ bool last;
+    __shared__ double tsum[NA];
+    __threadfence();            // this block's partials before its arrival
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ta.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // thread (c, k) of kSeg per column sums rows k, k + kSeg, ... with its
+    // loads issued together (a latency chain of a few L2 trips, not one per
+    // row), then the kSeg segment sums in order: fixed order, deterministic
+    constexpr int kSeg = 10, kRows = 32;
+    __shared__ double seg[NA][kSeg];
+    const int nb = (int)gridDim.x;
+    if (threadIdx.x < NA * kSeg) {
+        const int c = threadIdx.x / kSeg, k = threadIdx.x % kSeg;
+        double r[kRows];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const int b = k + i * kSeg;
+            r[i] = b < nb ? __ldcg(partials + (long long)b * NA + c) : 0.0;
+        }
+        double v = 0.0;
+        for (int b = k + kRows * kSeg; b < nb; b += kSeg) v += __ldcg(partials + (long long)b * NA + c);
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) v += r[i];
+        seg[c][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NA) {
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < kSeg; ++k) v += seg[threadIdx.x][k];
+        tsum[threadIdx.x] = v;
+        ta.sums[threadIdx.x] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ta.counter = 0u;
+    if (SOLVE) {
+        __shared__ EmDev se;
+        em_copy(&se, ta.em, threadIdx.x, blockDim.x);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            rigid_solve_body(tsum, &se, ta.objs, ta.tnorms, ta.masses);
+            if (!se.done) grid_params(se.k, dg, *ta.gk_out);
+        }
+        __syncthreads();
+        em_copy(ta.em, &se, threadIdx.x, blockDim.x);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1883,8 +1957,7 @@ static int launch_pass_t(const fr_lattice *lat, const float *ref, long long m, c
 static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, bool dev,
                        const float *ref, long long m, const RigidK &k, const RigidK *kd,
                        const int *done, float *wtn, double *scratch, double *sums,
-                       cudaStream_t s, GridK *gk_buf = nullptr,
-                       const float4 *tiles = nullptr) {
+                       cudaStream_t s, GridK *gk_buf = nullptr) {
     const int nv = lat->nv;
     const bool fast = qpath != 0 && !sig && lat->fslots != nullptr;
     if (fast && qpath == 2 && mode == FR_POINT_TO_POINT && nv == 4) {
@@ -1906,8 +1979,7 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
                     FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, gk_buf, sizeof(GridK), 0,
                                                     cudaMemcpyDeviceToDevice, s));
                     static const bool fold64 = getenv("FR_GRID_FOLD") && atoi(getenv("FR_GRID_FOLD")) == 64;
-                    if (tiles) k_rigid_pass_tiles<><<<g4, kPassThreads, 0, s>>>(tiles, m, done, dg, scratch);
-                    else if (vec && fold64) k_rigid_pass_grid4<true, true, 2, true, true, 64><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
+                    if (vec && fold64) k_rigid_pass_grid4<true, true, 2, true, true, 64><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
                     else if (vec) k_rigid_pass_grid4<true, true, 2, true, true><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
                     else FR_GRID4(true, false, 2, true);
                 }
@@ -1982,6 +2054,7 @@ struct fr_rigid_em {
     cudaStream_t stream = nullptr;   // stream of the last call (destroy orders behind it)
     fr::GridK *d_gk = nullptr;       // staging of the c_grid constants (owner only)
     float4 *d_tiles = nullptr;       // centred tiled model points (owner only)
+    unsigned *d_counter = nullptr;   // arrival counter of the tiled pass's fused tail
 };
 
 using namespace fr;
@@ -2226,13 +2299,15 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
         const long long ntiles = (m + kQuadPts - 1) / kQuadPts;
         const bool tiled = !(getenv("FR_GRID_TILES") && getenv("FR_GRID_TILES")[0] == '0');
         if (cudaMallocAsync((void **)&em->d_gk, sizeof(GridK), 0) != cudaSuccess ||
-            (tiled && cudaMallocAsync((void **)&em->d_tiles, (size_t)ntiles * kTileF4 * sizeof(float4),
-                                      0) != cudaSuccess)) {
+            (tiled && (cudaMallocAsync((void **)&em->d_tiles,
+                                       (size_t)ntiles * kTileF4 * sizeof(float4), 0) != cudaSuccess ||
+                       cudaMallocAsync((void **)&em->d_counter, sizeof(unsigned), 0) != cudaSuccess))) {
             cudaStreamSynchronize(0);
-            if (em->d_gk) cudaFreeAsync(em->d_gk, 0);
-            if (em->d_tiles) cudaFreeAsync(em->d_tiles, 0);
+            for (void *p : {(void *)em->d_gk, (void *)em->d_tiles, (void *)em->d_counter})
+                if (p) cudaFreeAsync(p, 0);
             em->d_gk = nullptr;
             em->d_tiles = nullptr;
+            em->d_counter = nullptr;
             g_const_grid_busy.store(false);
             cudaGetLastError();
         } else if (tiled) {
@@ -2240,6 +2315,9 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
             k_tile_points<<<(unsigned)((quads + 255) / 256), 256, 0, 0>>>(
                 ref, m, (float)cfg->c_ref[0], (float)cfg->c_ref[1], (float)cfg->c_ref[2],
                 em->d_tiles, ntiles);
+            cudaMemsetAsync(em->d_counter, 0, sizeof(unsigned), 0);
+            // the tiled pass reads d_gk (via c_grid) as maintained by the solver
+            k_grid_params<<<1, 1, 0, 0>>>(&em->d_em->k, &em->d_em->done, lat->dense, em->d_gk);
         }
         cudaStreamSynchronize(0);
     }
@@ -2257,6 +2335,7 @@ int fr_rigid_em_destroy(fr_rigid_em *em) {
                     (void *)em->d_traces})
         if (p) cudaFreeAsync(p, em->stream);
     if (em->d_tiles) cudaFreeAsync(em->d_tiles, em->stream);
+    if (em->d_counter) cudaFreeAsync(em->d_counter, em->stream);
     if (em->d_gk) {     // the stream is drained: no pass still reads c_grid
         cudaFreeAsync(em->d_gk, em->stream);
         g_const_grid_busy.store(false);
@@ -2275,23 +2354,50 @@ int fr_rigid_em_sums(fr_rigid_em *em, double **d_sums, int *width_out) {
     return FR_OK;
 }
 
+// the tiled pass of the device loop (EM objects holding c_grid): the pass
+// constants of the current pose (d_gk, kept by the solver) copied into the
+// constant bank, then one kernel; SOLVE fuses the iteration's solve
+static int em_tiles_pass(fr_rigid_em *em, cudaStream_t s, bool solve) {
+    FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, em->d_gk, sizeof(GridK), 0, cudaMemcpyDeviceToDevice, s));
+    const int n = em->max_iters;
+    const TailArgs ta{em->d_counter, em->d_sums, solve ? em->d_em : nullptr, em->d_traces,
+                      em->d_traces + n, em->d_traces + 2 * n, solve ? em->d_gk : nullptr};
+    if (solve)
+        k_rigid_pass_tiles<kGridFold, 2, true><<<2 * sm_count(), kPassThreads, 0, s>>>(
+            em->d_tiles, em->m, &em->d_em->done, em->lat->dense, em->d_scratch, ta);
+    else
+        k_rigid_pass_tiles<kGridFold, 2, false><<<2 * sm_count(), kPassThreads, 0, s>>>(
+            em->d_tiles, em->m, &em->d_em->done, em->lat->dense, em->d_scratch, ta);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
 static int em_pass(fr_rigid_em *em, cudaStream_t s) {
+    if (em->d_tiles) return em_tiles_pass(em, s, false);
     RigidK unused;
     memset(&unused, 0, sizeof(unused));
     return launch_pass(em->lat, FR_POINT_TO_POINT, false, em->fast, true, em->ref, em->m,
                        unused, &em->d_em->k, &em->d_em->done, nullptr, em->d_scratch, em->d_sums,
-                       s, em->d_gk, em->d_tiles);
+                       s, em->d_gk);
 }
 
 static int em_solve(fr_rigid_em *em, cudaStream_t s) {
     const int n = em->max_iters;
     k_rigid_solve<<<1, 32, 0, s>>>(em->d_sums, em->d_em, em->d_traces, em->d_traces + n,
-                                   em->d_traces + 2 * n);
+                                   em->d_traces + 2 * n, em->lat->dense,
+                                   em->d_tiles ? em->d_gk : nullptr);
     FR_CHECK_LAUNCH();
     return FR_OK;
 }
 
+// FR_EM_FUSED=0: pass and solver as separate kernels in the tiled loop
+static bool em_fused() {
+    static const bool f = !(getenv("FR_EM_FUSED") && getenv("FR_EM_FUSED")[0] == '0');
+    return f;
+}
+
 static int em_iteration(fr_rigid_em *em, cudaStream_t s) {
+    if (em->d_tiles && em_fused()) return em_tiles_pass(em, s, true);
     FR_TRY(em_pass(em, s));
     return em_solve(em, s);
 }
