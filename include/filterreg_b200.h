@@ -302,6 +302,11 @@ enum { FR_TERM_MAX_ITERS = 0, FR_TERM_CONVERGED = 1, FR_TERM_DEGENERATE = 2,
 
 int fr_rigid_em_create(const fr_lattice *lat, const float *d_ref, int64_t m,
                        const fr_rigid_em_config *cfg, fr_rigid_em **out);
+/* as fr_rigid_em_create, with the setup (allocations, the centred tiled copy
+ * of d_ref for clouds above FR_PERSIST_MAX points, the first pass constants)
+ * ordered on `stream` -- the stream that produced d_ref */
+int fr_rigid_em_create_on(const fr_lattice *lat, const float *d_ref, int64_t m,
+                          const fr_rigid_em_config *cfg, void *stream, fr_rigid_em **out);
 int fr_rigid_em_destroy(fr_rigid_em *em);
 int fr_rigid_em_sums(fr_rigid_em *em, double **d_sums, int *width);
 int fr_rigid_em_pass(fr_rigid_em *em, void *stream);

@@ -409,8 +409,9 @@ class DeviceEM:
         c.fast = pass_flags() if fast is None else int(fast)
         self._cfg = c
         h = ctypes.c_void_p()
-        _lib.check(self.lib.fr_rigid_em_create(path.lattice.handle, _lib.ptr(path.ref), path.M,
-                                               ctypes.byref(c), ctypes.byref(h)))
+        _lib.check(self.lib.fr_rigid_em_create_on(path.lattice.handle, _lib.ptr(path.ref), path.M,
+                                                  ctypes.byref(c), _lib.stream_handle(),
+                                                  ctypes.byref(h)))
         self.h = h
         sp = ctypes.c_void_p()
         w = ctypes.c_int()

@@ -1259,6 +1259,12 @@ static int grid_kernel() {
 
 // owner flag of c_grid: the first device EM object over a dense grid takes it
 static std::atomic<bool> g_const_grid_busy{false};
+// largest model cloud fr_rigid_em_run sends through the persistent one-CTA
+// loop (FR_PERSIST_MAX points; larger clouds use the graph-replayed iteration)
+static long long persist_max() {
+    const char *e = getenv("FR_PERSIST_MAX");
+    return e ? atoll(e) : 32768;
+}
 
 // points per thread per ring stage of the dense-grid pass (FR_GRID_PTS):
 // 3 (default: three independent chains per thread sharing the parameter
@@ -1882,7 +1888,7 @@ k_em_persistent(const PersistProblem *probs) {
     __shared__ double tsum[NA];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     em_copy(&se, P.em, threadIdx.x, blockDim.x);
-    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, P.dg.s0, P.dg.s1);
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry_q(e, P.dg.s0, P.dg.s1);
     __syncthreads();
     if (threadIdx.x == 0 && !se.done) grid_params(se.k, P.dg, g);
     __syncthreads();
@@ -1905,7 +1911,7 @@ k_em_persistent(const PersistProblem *probs) {
                 z[k] = ok[k] ? __ldg(P.ref + 2 * P.m + p) : 0.0f;
             }
 #pragma unroll
-            for (int k = 0; k < PP; ++k) grid_point(x[k], y[k], z[k], ok[k], g, tab, P.dg, a);
+            for (int k = 0; k < PP; ++k) grid_point_q(x[k], y[k], z[k], ok[k], g, tab, P.dg.cells, a);
             fold += PP;
             if (fold >= kGridFold) {
                 grid_warp_fold(a, wacc[warp]);
@@ -2239,6 +2245,14 @@ int fr_body_params_doubles(int n) { return (int)((n * sizeof(RigidK) + 7) / 8); 
 
 int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
                        const fr_rigid_em_config *cfg, fr_rigid_em **out) {
+    return fr_rigid_em_create_on(lat, ref, m, cfg, nullptr, out);
+}
+
+// every allocation, copy and kernel of the setup is ordered on the caller's
+// stream (which also orders it after the caller's upload / sort of ref)
+int fr_rigid_em_create_on(const fr_lattice *lat, const float *ref, int64_t m,
+                          const fr_rigid_em_config *cfg, void *stream, fr_rigid_em **out) {
+    cudaStream_t s = (cudaStream_t)stream;
     if (!lat || !lat->blurred || !ref || !cfg || !out || m <= 0) {
         set_error("invalid device EM arguments");
         return FR_EINVAL;
@@ -2252,6 +2266,7 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
         return FR_EINVAL;
     }
     fr_rigid_em *em = new fr_rigid_em();
+    em->stream = s;
     em->lat = lat;
     em->ref = ref;
     em->m = m;
@@ -2281,30 +2296,31 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
     const int grid = pass_grid_max();
     // stream-ordered pool (see fr_lattice.cu pool_alloc): no cudaMalloc /
     // cudaFree mapping work per registration
-    if (cudaMallocAsync((void **)&em->d_em, sizeof(EmDev), 0) != cudaSuccess ||
-        cudaMallocAsync((void **)&em->d_sums, 32 * sizeof(double), 0) != cudaSuccess ||
-        cudaMallocAsync((void **)&em->d_scratch, (size_t)grid * 32 * sizeof(double), 0) != cudaSuccess ||
-        cudaMallocAsync((void **)&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double), 0) !=
+    if (cudaMallocAsync((void **)&em->d_em, sizeof(EmDev), s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_sums, 32 * sizeof(double), s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_scratch, (size_t)grid * 32 * sizeof(double), s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double), s) !=
             cudaSuccess ||
-        cudaStreamSynchronize(0) != cudaSuccess ||
-
-        cudaMemcpy(em->d_em, &h, sizeof(EmDev), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpyAsync(em->d_em, &h, sizeof(EmDev), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
         fr_rigid_em_destroy(em);
         set_error("device EM allocation failed");
         return FR_ECUDA;
     }
+    // the constant-bank tiled loop for clouds fr_rigid_em_run does not send
+    // through the persistent one-CTA kernel
     bool idle = false;
-    if (lat->dcells != nullptr && em->fast == 2 &&
+    if (lat->dcells != nullptr && em->fast == 2 && m > persist_max() &&
         g_const_grid_busy.compare_exchange_strong(idle, true)) {
         const long long ntiles = (m + kQuadPts - 1) / kQuadPts;
         const bool tiled = !(getenv("FR_GRID_TILES") && getenv("FR_GRID_TILES")[0] == '0');
-        if (cudaMallocAsync((void **)&em->d_gk, sizeof(GridK), 0) != cudaSuccess ||
+        if (cudaMallocAsync((void **)&em->d_gk, sizeof(GridK), s) != cudaSuccess ||
             (tiled && (cudaMallocAsync((void **)&em->d_tiles,
-                                       (size_t)ntiles * kTileF4 * sizeof(float4), 0) != cudaSuccess ||
-                       cudaMallocAsync((void **)&em->d_counter, sizeof(unsigned), 0) != cudaSuccess))) {
-            cudaStreamSynchronize(0);
+                                       (size_t)ntiles * kTileF4 * sizeof(float4), s) != cudaSuccess ||
+                       cudaMallocAsync((void **)&em->d_counter, sizeof(unsigned), s) != cudaSuccess))) {
+            cudaStreamSynchronize(s);
             for (void *p : {(void *)em->d_gk, (void *)em->d_tiles, (void *)em->d_counter})
-                if (p) cudaFreeAsync(p, 0);
+                if (p) cudaFreeAsync(p, s);
             em->d_gk = nullptr;
             em->d_tiles = nullptr;
             em->d_counter = nullptr;
@@ -2312,14 +2328,14 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *ref, int64_t m,
             cudaGetLastError();
         } else if (tiled) {
             const long long quads = ntiles * kPassThreads;
-            k_tile_points<<<(unsigned)((quads + 255) / 256), 256, 0, 0>>>(
+            k_tile_points<<<(unsigned)((quads + 255) / 256), 256, 0, s>>>(
                 ref, m, (float)cfg->c_ref[0], (float)cfg->c_ref[1], (float)cfg->c_ref[2],
                 em->d_tiles, ntiles);
-            cudaMemsetAsync(em->d_counter, 0, sizeof(unsigned), 0);
+            cudaMemsetAsync(em->d_counter, 0, sizeof(unsigned), s);
             // the tiled pass reads d_gk (via c_grid) as maintained by the solver
-            k_grid_params<<<1, 1, 0, 0>>>(&em->d_em->k, &em->d_em->done, lat->dense, em->d_gk);
+            k_grid_params<<<1, 1, 0, s>>>(&em->d_em->k, &em->d_em->done, lat->dense, em->d_gk);
         }
-        cudaStreamSynchronize(0);
+        cudaStreamSynchronize(s);
     }
     *out = em;
     return FR_OK;
@@ -2479,12 +2495,6 @@ static bool em_persist_ok(const fr_rigid_em *em) {
            em->m > 0;
 }
 
-// largest model cloud fr_rigid_em_run sends through the persistent one-CTA
-// loop (FR_PERSIST_MAX points; larger clouds use the graph-replayed iteration)
-static long long persist_max() {
-    const char *e = getenv("FR_PERSIST_MAX");
-    return e ? atoll(e) : 32768;
-}
 
 int fr_rigid_em_run_batch(fr_rigid_em **ems, int n, void *stream) {
     if (n < 0 || (n > 0 && !ems)) {

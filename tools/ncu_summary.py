@@ -17,7 +17,18 @@ WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Cache Throug
         "Warp Cycles Per Issued Instruction", "Executed Instructions", "No Eligible",
         "Block Size", "Grid Size"]
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-       "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread"]
+       "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+       "smsp__issue_active.avg.pct_of_peak_sustained_active",
+       "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+       "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct",
+       "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio"]
 
 
 def launches(path):
