@@ -308,8 +308,15 @@ int fr_rigid_em_create(const fr_lattice *lat, const float *d_ref, int64_t m,
 int fr_rigid_em_create_on(const fr_lattice *lat, const float *d_ref, int64_t m,
                           const fr_rigid_em_config *cfg, void *stream, fr_rigid_em **out);
 int fr_rigid_em_destroy(fr_rigid_em *em);
+/* kernels one fr_rigid_em_enqueue'd iteration launches (1: the tiled pass with
+ * its fused reduction and solve) -- for launch accounting */
+int fr_rigid_em_kernels_per_iter(const fr_rigid_em *em);
 int fr_rigid_em_sums(fr_rigid_em *em, double **d_sums, int *width);
 int fr_rigid_em_pass(fr_rigid_em *em, void *stream);
+/* the tiled pass kernel alone, reusing the pass constants the last
+ * fr_rigid_em_pass copied into the constant bank (kernel timing: the pose
+ * must not have changed since) */
+int fr_rigid_em_pass_kernel(fr_rigid_em *em, void *stream);
 int fr_rigid_em_solve(fr_rigid_em *em, void *stream);
 int fr_rigid_em_enqueue(fr_rigid_em *em, int n_iters, void *stream);
 int fr_rigid_em_run(fr_rigid_em *em, void *stream);

@@ -26,7 +26,8 @@ EXPORTED = (
     "fr_lattice_export", "fr_lattice_slice", "fr_simplex", "fr_gauss_bruteforce",
     "fr_moments", "fr_rigid_pass_width", "fr_rigid_scratch_doubles", "fr_rigid_pass",
     "fr_rigid_objective", "fr_moments_epilogue", "fr_assemble_rigid",
-    "fr_rigid_em_create", "fr_rigid_em_create_on", "fr_rigid_em_destroy", "fr_rigid_em_sums",
+    "fr_rigid_em_create", "fr_rigid_em_create_on", "fr_rigid_em_destroy",
+    "fr_rigid_em_kernels_per_iter", "fr_rigid_em_pass_kernel", "fr_rigid_em_sums",
     "fr_rigid_em_pass",
     "fr_rigid_em_solve", "fr_rigid_em_enqueue", "fr_rigid_em_run", "fr_rigid_em_status",
     "fr_rigid_em_result", "fr_sort_points_morton", "fr_body_params_doubles", "fr_body_pass",
@@ -99,6 +100,8 @@ _SIGS = {
     "fr_point_rows": ([_P, _P, _P, _P, _P, _L, _I, _DP, _P, _P], _I),
     "fr_graph_objective": ([_P, _L, _P, _P, _I, _P, _I, _I, _P, _I, _DP, _P, _P, _P, _P], _I),
     "fr_rigid_em_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), ctypes.POINTER(_P)], _I),
+    "fr_rigid_em_kernels_per_iter": ([_P], _I),
+    "fr_rigid_em_pass_kernel": ([_P, _P], _I),
     "fr_rigid_em_create_on": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)],
                               _I),
     "fr_rigid_em_destroy": ([_P], _I),

@@ -2373,8 +2373,10 @@ int fr_rigid_em_sums(fr_rigid_em *em, double **d_sums, int *width_out) {
 // the tiled pass of the device loop (EM objects holding c_grid): the pass
 // constants of the current pose (d_gk, kept by the solver) copied into the
 // constant bank, then one kernel; SOLVE fuses the iteration's solve
-static int em_tiles_pass(fr_rigid_em *em, cudaStream_t s, bool solve) {
-    FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, em->d_gk, sizeof(GridK), 0, cudaMemcpyDeviceToDevice, s));
+static int em_tiles_pass(fr_rigid_em *em, cudaStream_t s, bool solve, bool copy = true) {
+    if (copy)
+        FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, em->d_gk, sizeof(GridK), 0,
+                                        cudaMemcpyDeviceToDevice, s));
     const int n = em->max_iters;
     const TailArgs ta{em->d_counter, em->d_sums, solve ? em->d_em : nullptr, em->d_traces,
                       em->d_traces + n, em->d_traces + 2 * n, solve ? em->d_gk : nullptr};
@@ -2416,6 +2418,22 @@ static int em_iteration(fr_rigid_em *em, cudaStream_t s) {
     if (em->d_tiles && em_fused()) return em_tiles_pass(em, s, true);
     FR_TRY(em_pass(em, s));
     return em_solve(em, s);
+}
+
+int fr_rigid_em_pass_kernel(fr_rigid_em *em, void *stream) {
+    if (!em || !em->d_tiles) {
+        set_error("fr_rigid_em_pass_kernel needs an EM object on the tiled loop");
+        return FR_EINVAL;
+    }
+    em->stream = (cudaStream_t)stream;
+    return em_tiles_pass(em, (cudaStream_t)stream, false, false);
+}
+
+int fr_rigid_em_kernels_per_iter(const fr_rigid_em *em) {
+    if (!em) return 0;
+    if (em->d_tiles) return em_fused() ? 1 : 2;    // tiled pass (+ solver kernel)
+    if (em->d_gk) return 4;                          // params, grid pass, reduction, solver
+    return 3;                                        // pass, reduction, solver
 }
 
 int fr_rigid_em_pass(fr_rigid_em *em, void *stream) {

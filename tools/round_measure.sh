@@ -9,6 +9,8 @@ python bench.py --mode batch --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > g
 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_rigid_pass_tiles -s 5 -c 1 \
+    -o gpurun_out/pass_only_full python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full0.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_rigid_pass_tiles -s 25 -c 1 \
     -o gpurun_out/pass_full python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_splat_segsum -s 1 -c 1 \
