@@ -12,9 +12,12 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "fr_common.cuh"
@@ -487,6 +490,27 @@ static inline unsigned grid_for(long long n, int block = 256) {
     return (unsigned)std::max<long long>(1, std::min<long long>(g, 1LL << 30));
 }
 
+// FR_SPLAT_TIMING=1: host wall-clock of the splat's phases (device-synchronised)
+struct PhaseClock {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0;
+    explicit PhaseClock(cudaStream_t st) : on(getenv("FR_SPLAT_TIMING") != nullptr), s(st) {
+        if (on) {
+            cudaStreamSynchronize(s);
+            t0 = std::chrono::steady_clock::now();
+        }
+    }
+    void lap(const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[splat] %-14s %8.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
+
 struct Scratch {
     cudaStream_t s;
     std::vector<void *> bufs;
@@ -508,6 +532,74 @@ struct Scratch {
         return FR_OK;
     }
 };
+
+// grow-only per-device workspace for a splat's entry-sized buffers (~64 B per
+// entry: 4.3 GB at 16.8M points): a rebuild reuses one mapped block instead of
+// asking the pool for GB-sized blocks that, fragmented, get freshly mapped
+// (75-130 ms outliers in the sigma-re-estimating loop).  One lease at a time;
+// a concurrent splat (register_batch threads) falls back to the pool.  The
+// next lessee's stream waits on the previous lessee's release event.
+struct Workspace {
+    std::mutex mu;
+    char *p = nullptr;
+    size_t cap = 0;
+    bool busy = false;
+    cudaEvent_t ev = nullptr;
+};
+static Workspace g_ws[16];
+
+struct WsLease {
+    Workspace *w = nullptr;
+    cudaStream_t s = nullptr;
+    size_t off = 0;
+    ~WsLease() { release(); }
+    // 1: leased `need` bytes; 0: busy or unavailable (use the pool)
+    int acquire(size_t need, cudaStream_t st) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        Workspace &ws = g_ws[dev & 15];
+        {
+            std::lock_guard<std::mutex> g(ws.mu);
+            if (ws.busy) return 0;
+            ws.busy = true;
+        }
+        w = &ws;
+        s = st;
+        if (ws.ev) cudaStreamWaitEvent(s, ws.ev, 0);
+        else cudaEventCreateWithFlags(&ws.ev, cudaEventDisableTiming);
+        if (ws.cap < need) {
+            if (ws.p) cudaFreeAsync(ws.p, s);
+            ws.p = nullptr;
+            ws.cap = 0;
+            const size_t grow = need + need / 4;
+            if (cudaMallocAsync((void **)&ws.p, grow, s) != cudaSuccess) {
+                cudaGetLastError();
+                ws.p = nullptr;
+                release();
+                return 0;
+            }
+            ws.cap = grow;
+        }
+        return 1;
+    }
+    template <class T>
+    T *carve(size_t count) {
+        const size_t bytes = (std::max<size_t>(count, 1) * sizeof(T) + 255) & ~(size_t)255;
+        T *r = (T *)(w->p + off);
+        off += bytes;
+        return r;
+    }
+    void release() {
+        if (!w) return;
+        cudaEventRecord(w->ev, s);
+        std::lock_guard<std::mutex> g(w->mu);
+        w->busy = false;
+        w = nullptr;
+    }
+};
+static inline size_t ws_bytes(size_t count, size_t elem) {
+    return (std::max<size_t>(count, 1) * elem + 255) & ~(size_t)255;
+}
 
 static int read_counters(fr_lattice *lat, cudaStream_t s, unsigned long long *h) {
     FR_CUDA(cudaMemcpyAsync(h, lat->d_counters, 3 * sizeof(unsigned long long),
@@ -612,6 +704,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         set_error("value width %d unsupported (1..15 columns per lattice)", nv);
         return FR_EINVAL;
     }
+    PhaseClock pc(s);
     free_build(lat);
     free_slice(lat);
     lat->nv = nv;
@@ -628,12 +721,33 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     Scratch sc(s);
     unsigned *entry_slot, *entry_idx, *sorted_slot, *sorted_idx;
     double *entry_bary, *contrib = nullptr;
-    FR_TRY(sc.get(&entry_slot, E));
-    FR_TRY(sc.get(&entry_idx, E));
-    FR_TRY(sc.get(&sorted_slot, E));
-    FR_TRY(sc.get(&sorted_idx, E));
-    FR_TRY(sc.get(&entry_bary, E));
-    if (contrib_fits(E, nv)) FR_TRY(sc.get(&contrib, (size_t)E * nv));
+    const bool with_contrib = contrib_fits(E, nv);
+    // the entry-sized buffers and an upper bound of the sort's temporary
+    size_t sort_bound = 0;
+    FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bound, (unsigned *)nullptr,
+                                            (unsigned *)nullptr, (unsigned *)nullptr,
+                                            (unsigned *)nullptr, (int)E, 0, 32, s));
+    const size_t need = 4 * ws_bytes(E, 4) + ws_bytes(E, 8) +
+                        (with_contrib ? ws_bytes((size_t)E * nv, 8) : 0) + ws_bytes(sort_bound, 1);
+    WsLease lease;
+    char *sort_tmp = nullptr;
+    if (lease.acquire(need, s)) {
+        entry_slot = lease.carve<unsigned>(E);
+        entry_idx = lease.carve<unsigned>(E);
+        sorted_slot = lease.carve<unsigned>(E);
+        sorted_idx = lease.carve<unsigned>(E);
+        entry_bary = lease.carve<double>(E);
+        if (with_contrib) contrib = lease.carve<double>((size_t)E * nv);
+        sort_tmp = lease.carve<char>(sort_bound);
+    } else {
+        FR_TRY(sc.get(&entry_slot, E));
+        FR_TRY(sc.get(&entry_idx, E));
+        FR_TRY(sc.get(&sorted_slot, E));
+        FR_TRY(sc.get(&sorted_idx, E));
+        FR_TRY(sc.get(&entry_bary, E));
+        if (with_contrib) FR_TRY(sc.get(&contrib, (size_t)E * nv));
+    }
+    pc.lap("alloc");
     // hash sized for the unique-key count; grown x4 on overflow
     unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
     unsigned long long hc[3];
@@ -654,6 +768,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         }
         cap *= 4;
     }
+    pc.lap("entries");
     const int end_bit = 1 + (int)std::log2((double)cap);
     // stable radix sort of entries by slot: per-site groups in flat order
     size_t tmp_bytes = 0, t2 = 0;
@@ -672,8 +787,8 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     tmp_bytes = std::max(tmp_bytes, t2);
     FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_cnt, run_off, (int)E, s));
     tmp_bytes = std::max(tmp_bytes, t2);
-    void *tmp;
-    FR_TRY(sc.get((char **)&tmp, tmp_bytes));
+    void *tmp = sort_tmp;
+    if (!tmp || tmp_bytes > sort_bound) FR_TRY(sc.get((char **)&tmp, tmp_bytes));
     FR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, entry_slot, sorted_slot, entry_idx,
                                             sorted_idx, (int)E, 0, end_bit, s));
     FR_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tmp_bytes, sorted_slot, run_slot, run_cnt,
@@ -682,6 +797,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_CUDA(cudaMemcpyAsync(&nruns, d_nruns, sizeof(int), cudaMemcpyDeviceToHost, s));
     FR_CUDA(cudaStreamSynchronize(s));
     FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, run_cnt, run_off, nruns, s));
+    pc.lap("sort+runs");
     double *run_vals;
     unsigned char *run_live;
     int *live_runs, *iota, *d_nlive;
@@ -704,6 +820,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
                                                    run_live);
         FR_CHECK_LAUNCH();
     }
+    pc.lap("segsum");
     // live runs -> dense site rows
     {
         std::vector<int> h_iota(nruns);
@@ -732,8 +849,10 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         pool_free(lat, old_keys);
         lat->n_sites = S;
     }
+    pc.lap("sites");
     FR_TRY(rehash_sites<D>(lat, next_pow2(2ull * (unsigned long long)lat->n_sites), s));
     FR_TRY(read_counters(lat, s, hc));
+    pc.lap("rehash");
     return FR_OK;
 }
 
