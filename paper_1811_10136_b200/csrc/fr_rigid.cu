@@ -2410,8 +2410,8 @@ static int em_solve(fr_rigid_em *em, cudaStream_t s) {
 
 // FR_EM_FUSED=0: pass and solver as separate kernels in the tiled loop
 static bool em_fused() {
-    static const bool f = !(getenv("FR_EM_FUSED") && getenv("FR_EM_FUSED")[0] == '0');
-    return f;
+    const char *e = getenv("FR_EM_FUSED");
+    return !(e && e[0] == '0');
 }
 
 static int em_iteration(fr_rigid_em *em, cudaStream_t s) {
