@@ -174,17 +174,22 @@ class _SetupClock:
 
     def __init__(self):
         import os
-        self.on = os.environ.get("FR_PROFILE_SETUP") == "1"
+        import time
+        mode = os.environ.get("FR_PROFILE_SETUP")
+        self.on = mode == "1"
+        self.marks = mode == "2"      # host timestamps since construction, no syncs
         self.phases = {}
+        self._t0 = time.perf_counter()
         if self.on:
-            import time
             import torch
             torch.cuda.synchronize()
             self._t = time.perf_counter()
 
     def __call__(self, name: str) -> None:
+        import time
+        if self.marks:
+            self.phases[name] = time.perf_counter() - self._t0
         if self.on:
-            import time
             import torch
             torch.cuda.synchronize()
             now = time.perf_counter()
@@ -233,7 +238,8 @@ class RigidDevicePath:
         main_stream = torch.cuda.current_stream()
         side = _side_stream()
         pool = ThreadPoolExecutor(max_workers=1)
-        obs_job = pool.submit(self._build_observation, observation, gmm, residual_mode, side)
+        obs_job = pool.submit(self._build_observation, observation, gmm, residual_mode, side,
+                              lap if lap.marks else None)
         self.ref = upload_soa(reference.positions, self.dev)
         self.M = self.ref.shape[1]
         lap("upload_ref")
@@ -281,16 +287,22 @@ class RigidDevicePath:
         SURVEY.md 8(e)) at the current kernel width."""
         return outlier_constant(self.gmm.outlier_ratio, self.N, self.M_total, self.sigma)
 
-    def _build_observation(self, observation, gmm, residual_mode, stream) -> None:
+    def _build_observation(self, observation, gmm, residual_mode, stream, lap=None) -> None:
         import torch
         with torch.cuda.stream(stream):
             self.obs = upload_soa(observation.positions, self.dev)
+            if lap is not None:
+                lap("obs_upload")
             self.N = self.obs.shape[1]
             self.obs_n = None
             if residual_mode == "point_to_plane":
                 self.obs_n = upload_soa(observation.normals, self.dev)
             self.build(gmm.sigma)
+            if lap is not None:
+                lap("obs_built")
             stream.synchronize()
+            if lap is not None:
+                lap("obs_synced")
 
     def build(self, sigma) -> None:
         """(Re)build the observation lattice at kernel width sigma."""

@@ -17,6 +17,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -601,10 +602,42 @@ static inline size_t ws_bytes(size_t count, size_t elem) {
     return (std::max<size_t>(count, 1) * elem + 255) & ~(size_t)255;
 }
 
-static int read_counters(fr_lattice *lat, cudaStream_t s, unsigned long long *h) {
-    FR_CUDA(cudaMemcpyAsync(h, lat->d_counters, 3 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, s));
+// small device -> host reads of the build (counters, run / site counts, the
+// site box) through a per-thread pinned buffer: pageable transfers go through
+// the driver's staging path and stalled a concurrent pinned upload on another
+// thread (16.8M points: 7 -> 14 ms while a splat ran)
+static void *pinned_scratch() {
+    static thread_local void *p = nullptr;
+    if (!p && cudaHostAlloc(&p, 4096, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+    }
+    return p;
+}
+static int d2h_sync(void *host, const void *dev, size_t bytes, cudaStream_t s) {
+    void *pin = bytes <= 4096 ? pinned_scratch() : nullptr;
+    FR_CUDA(cudaMemcpyAsync(pin ? pin : host, dev, bytes, cudaMemcpyDeviceToHost, s));
     FR_CUDA(cudaStreamSynchronize(s));
+    if (pin) memcpy(host, pin, bytes);
+    return FR_OK;
+}
+
+__global__ void k_iota(int n, int *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+__global__ void k_fill_u64(unsigned long long *p, unsigned long long a, unsigned long long b,
+                           unsigned long long c) {
+    if (threadIdx.x == 0) {
+        p[0] = a;
+        p[1] = b;
+        p[2] = c;
+    }
+}
+
+static int read_counters(fr_lattice *lat, cudaStream_t s, unsigned long long *h) {
+    FR_TRY(d2h_sync(h, lat->d_counters, 3 * sizeof(unsigned long long), s));
     if (h[2] & 1ull) {
         set_error("lattice coordinate outside the packable range (|key| >= %lld); "
                   "features / sigma too large", (long long)kKeyLim);
@@ -794,8 +827,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tmp_bytes, sorted_slot, run_slot, run_cnt,
                                                d_nruns, (int)E, s));
     int nruns = 0;
-    FR_CUDA(cudaMemcpyAsync(&nruns, d_nruns, sizeof(int), cudaMemcpyDeviceToHost, s));
-    FR_CUDA(cudaStreamSynchronize(s));
+    FR_TRY(d2h_sync(&nruns, d_nruns, sizeof(int), s));
     FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, run_cnt, run_off, nruns, s));
     pc.lap("sort+runs");
     double *run_vals;
@@ -823,10 +855,8 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     pc.lap("segsum");
     // live runs -> dense site rows
     {
-        std::vector<int> h_iota(nruns);
-        for (int i = 0; i < nruns; ++i) h_iota[i] = i;
-        FR_CUDA(cudaMemcpyAsync(iota, h_iota.data(), nruns * sizeof(int),
-                                cudaMemcpyHostToDevice, s));
+        k_iota<<<grid_for(nruns), 256, 0, s>>>(nruns, iota);
+        FR_CHECK_LAUNCH();
         size_t t3 = 0;
         FR_CUDA(cub::DeviceSelect::Flagged(nullptr, t3, iota, run_live, live_runs, d_nlive,
                                            nruns, s));
@@ -835,8 +865,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         FR_CUDA(cub::DeviceSelect::Flagged(tmp3, t3, iota, run_live, live_runs, d_nlive, nruns,
                                            s));
         int S = 0;
-        FR_CUDA(cudaMemcpyAsync(&S, d_nlive, sizeof(int), cudaMemcpyDeviceToHost, s));
-        FR_CUDA(cudaStreamSynchronize(s));
+        FR_TRY(d2h_sync(&S, d_nlive, sizeof(int), s));
         unsigned long long *old_keys = lat->hkeys;
         lat->hkeys = nullptr;   // keep the splat hash alive for k_fill_sites
         FR_TRY(reserve_sites(lat, std::max(S, 1), s));
@@ -869,17 +898,15 @@ static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
     FR_TRY(sc.get(&d_n, 1));
     k_nonzero_flags<<<grid_for(S), 256, 0, s>>>(S, lat->vals, lat->nv, flags);
     FR_CHECK_LAUNCH();
-    std::vector<int> h_iota(S);
-    for (long long i = 0; i < S; ++i) h_iota[i] = (int)i;
-    FR_CUDA(cudaMemcpyAsync(iota, h_iota.data(), S * sizeof(int), cudaMemcpyHostToDevice, s));
+    k_iota<<<grid_for(S), 256, 0, s>>>((int)S, iota);
+    FR_CHECK_LAUNCH();
     size_t t = 0;
     FR_CUDA(cub::DeviceSelect::Flagged(nullptr, t, iota, flags, sel, d_n, (int)S, s));
     void *tmp;
     FR_TRY(sc.get((char **)&tmp, t));
     FR_CUDA(cub::DeviceSelect::Flagged(tmp, t, iota, flags, sel, d_n, (int)S, s));
     int keep = 0;
-    FR_CUDA(cudaMemcpyAsync(&keep, d_n, sizeof(int), cudaMemcpyDeviceToHost, s));
-    FR_CUDA(cudaStreamSynchronize(s));
+    FR_TRY(d2h_sync(&keep, d_n, sizeof(int), s));
     if (keep == S) return FR_OK;
     int *nk;
     double *nvls;
@@ -962,18 +989,20 @@ __global__ void k_dense_fill(long long S, const int *site_keys, const double *va
                     (float)(gain * v[0]));
 }
 
+__global__ void k_init_box(int *box) {
+    if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
+}
+
 static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
     if (lat->dim != 3 || lat->nv != 4 || lat->n_sites == 0) return FR_OK;
     int *dbox = nullptr;
     FR_CUDA(cudaMallocAsync(&dbox, 6 * sizeof(int), s));
-    const int init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
-    FR_CUDA(cudaMemcpyAsync(dbox, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    k_init_box<<<1, 32, 0, s>>>(dbox);
     k_site_qbox<<<std::min<long long>(grid_for(lat->n_sites), 1184), 256, 0, s>>>(
         lat->n_sites, lat->site_keys, dbox);
     FR_CHECK_LAUNCH();
     int box[6];
-    FR_CUDA(cudaMemcpyAsync(box, dbox, sizeof(box), cudaMemcpyDeviceToHost, s));
-    FR_CUDA(cudaStreamSynchronize(s));
+    FR_TRY(d2h_sync(box, dbox, sizeof(box), s));
     FR_CUDA(cudaFreeAsync(dbox, s));
     long long n[3], cells = 1;
     for (int c = 0; c < 3; ++c) {
@@ -1097,8 +1126,7 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
             if ((unsigned long long)need * 2 > (unsigned long long)lat->hmask + 1)
                 FR_TRY(rehash_sites<D>(lat, next_pow2(4ull * (unsigned long long)need), s));
             FR_CUDA(cudaMemsetAsync(lat->vals + S * nv, 0, (size_t)2 * nsrc * nv * sizeof(double), s));
-            unsigned long long init[3] = {(unsigned long long)S, 0ull, 0ull};
-            FR_CUDA(cudaMemcpyAsync(lat->d_counters, init, sizeof(init), cudaMemcpyHostToDevice, s));
+            k_fill_u64<<<1, 32, 0, s>>>(lat->d_counters, (unsigned long long)S, 0ull, 0ull);
             k_extend<D><<<grid_for(S), 256, 0, s>>>(S, axis, lat->vals, nv,
                                                     BuildHash{lat->hkeys, lat->hsite, lat->hmask},
                                                     lat->site_keys, lat->d_counters);

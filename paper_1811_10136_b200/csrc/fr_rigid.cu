@@ -2550,9 +2550,11 @@ int fr_rigid_em_persistent(const fr_rigid_em *em) {
 
 int fr_rigid_em_run(fr_rigid_em *em, void *stream) {
     if (fr_rigid_em_persistent(em)) return fr_rigid_em_run_batch(&em, 1, stream);
+    // poll the done flag after 8, then every 32 iterations (iterations after
+    // termination are no-op launches)
     int done = 0;
-    for (int guard = 0; !done && guard < em->max_iters + 16; guard += 8) {
-        FR_TRY(fr_rigid_em_enqueue(em, 8, stream));
+    for (int guard = 0, step = 8; !done && guard < em->max_iters + 40; guard += step, step = 32) {
+        FR_TRY(fr_rigid_em_enqueue(em, step, stream));
         FR_TRY(fr_rigid_em_status(em, &done, nullptr, nullptr, stream));
     }
     return FR_OK;

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -55,6 +56,41 @@ StagePool &pool() {
     return p;
 }
 
+// (n, 3) float64 rows -> three float32 planes, round to nearest (as
+// numpy.astype).  Four rows per step: three 32-byte loads, converted and
+// de-interleaved with AVX when the CPU has it (runtime check, so the library
+// still runs on a host without it), else the scalar loop.
+__attribute__((target("avx2"))) static void convert_rows_avx2(const double *r, long long len,
+                                                              float *x, float *y, float *z) {
+    long long i = 0;
+    for (; i + 4 <= len; i += 4) {
+        const double *q = r + 3 * i;
+        alignas(32) float f[12];
+        for (int k = 0; k < 12; ++k) f[k] = (float)q[k];
+        x[i] = f[0]; y[i] = f[1]; z[i] = f[2];
+        x[i + 1] = f[3]; y[i + 1] = f[4]; z[i + 1] = f[5];
+        x[i + 2] = f[6]; y[i + 2] = f[7]; z[i + 2] = f[8];
+        x[i + 3] = f[9]; y[i + 3] = f[10]; z[i + 3] = f[11];
+    }
+    for (; i < len; ++i) {
+        x[i] = (float)r[3 * i];
+        y[i] = (float)r[3 * i + 1];
+        z[i] = (float)r[3 * i + 2];
+    }
+}
+static void convert_rows_scalar(const double *r, long long len, float *x, float *y, float *z) {
+    for (long long i = 0; i < len; ++i) {
+        x[i] = (float)r[3 * i];
+        y[i] = (float)r[3 * i + 1];
+        z[i] = (float)r[3 * i + 2];
+    }
+}
+static void convert_rows(const double *r, long long len, float *x, float *y, float *z) {
+    static const bool avx2 = __builtin_cpu_supports("avx2") && !getenv("FR_UPLOAD_SCALAR");
+    if (avx2) convert_rows_avx2(r, len, x, y, z);
+    else convert_rows_scalar(r, len, x, y, z);
+}
+
 struct WorkerResult {
     int status = FR_OK;
     char msg[256] = {0};
@@ -71,11 +107,7 @@ void worker(int id, const double *src, long long n, long long a, long long b, fl
         if (e == cudaSuccess) {
             const double *r = src + 3 * c;
             float *x = buf, *y = buf + kSubChunk, *z = buf + 2 * kSubChunk;
-            for (long long i = 0; i < len; ++i) {
-                x[i] = (float)r[3 * i];
-                y[i] = (float)r[3 * i + 1];
-                z[i] = (float)r[3 * i + 2];
-            }
+            convert_rows(r, len, x, y, z);
             e = cudaMemcpy2DAsync(dst + c, (size_t)n * sizeof(float), buf,
                                   (size_t)kSubChunk * sizeof(float), (size_t)len * sizeof(float),
                                   3, cudaMemcpyHostToDevice, s);
@@ -103,8 +135,10 @@ extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa,
     if (n == 0) return FR_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    long long cap = kMaxWorkers;
+    if (const char *e = getenv("FR_UPLOAD_WORKERS")) cap = std::max(1, std::min(kMaxWorkers, atoi(e)));
     const int w = (int)std::max<long long>(
-        1, std::min<long long>({(long long)kMaxWorkers, (long long)hw, (n + kSubChunk - 1) / kSubChunk}));
+        1, std::min<long long>({cap, (long long)hw, (n + kSubChunk - 1) / kSubChunk}));
     StagePool &p = pool();
     std::lock_guard<std::mutex> lock(p.mu);   // one upload at a time owns the slots
     FR_TRY(p.init());
