@@ -218,10 +218,22 @@ def regularizer_objective(graph, lambda_reg: float) -> float:
     return total
 
 
+_INCIDENCE: dict = {}
+
+
 def _grouped(values, ids, n):
-    out = np.zeros((n,) + values.shape[1:])
-    np.add.at(out, ids, values)
-    return out
+    """Per-node sums of per-edge values (np.add.at semantics) as one sparse
+    incidence product; the incidence matrix of an edge list is cached."""
+    import scipy.sparse as sp
+    key = (n, len(ids), hash(np.ascontiguousarray(ids).tobytes()))
+    A = _INCIDENCE.get(key)
+    if A is None:
+        A = sp.csr_matrix((np.ones(len(ids)), (ids, np.arange(len(ids)))), shape=(n, len(ids)))
+        if len(_INCIDENCE) > 64:
+            _INCIDENCE.clear()
+        _INCIDENCE[key] = A
+    flat = values.reshape(len(ids), -1)
+    return np.asarray(A @ flat).reshape((n,) + values.shape[1:])
 
 
 def normal_equations(graph, diag, off, path, lambda_reg):

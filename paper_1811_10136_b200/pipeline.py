@@ -79,7 +79,14 @@ def _poses(model):
 
 
 def update_magnitude(before, after, diameter: float) -> float:
-    """Largest per-body angle + shift / diameter (pipeline.py:79-86)."""
+    """Largest per-body angle + shift / diameter (pipeline.py:79-86).  Node
+    graphs (hundreds of poses) take the batched form of the same formula."""
+    if hasattr(before, "_R") and hasattr(after, "_R") and len(before._R) > 32:
+        Rb, tb = np.asarray(before._R, dtype=float), np.asarray(before._t, dtype=float)
+        Ra, ta = np.asarray(after._R, dtype=float), np.asarray(after._t, dtype=float)
+        c = (np.trace(Ra @ np.transpose(Rb, (0, 2, 1)), axis1=1, axis2=2) - 1.0) / 2.0
+        per = np.arccos(np.clip(c, -1.0, 1.0)) + np.linalg.norm(ta - tb, axis=1) / diameter
+        return max(0.0, float(per.max()))
     worst = 0.0
     for (Rb, tb), (Ra, ta) in zip(_poses(before), _poses(after)):
         worst = max(worst, rotation_angle(Ra @ Rb.T) + float(np.linalg.norm(ta - tb)) / diameter)
