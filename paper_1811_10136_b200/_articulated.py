@@ -75,20 +75,23 @@ class ArticulatedDevicePath(RigidDevicePath):
         self.bhost = torch.empty((nb, w), dtype=torch.float64, pin_memory=True)
 
     def _poses(self, tree, n_cand=1, trees=None):
+        """BodyPose records (R, c_ref, c_world) of every body of every tree,
+        filled through a float64 view of the ctypes array."""
         trees = trees if trees is not None else [tree]
         arr = (BodyPose * (len(trees) * self.nb))()
+        view = np.ctypeslib.as_array(ctypes.cast(arr, ctypes.POINTER(ctypes.c_double)),
+                                     shape=(len(trees), self.nb, 15))
+        cb = np.asarray(self.c_body, dtype=float)
         for c, tr in enumerate(trees):
-            for b in range(self.nb):
-                T = tr.body_pose(b)
-                p = arr[c * self.nb + b]
-                p.R[:] = list(T.rotation.reshape(-1))
-                p.c_ref[:] = list(self.c_body[b])
-                p.c_world[:] = list(T.rotation @ self.c_body[b] + T.translation)
+            R, t = tr.world_arrays()
+            view[c, :, :9] = R.reshape(self.nb, 9)
+            view[c, :, 9:12] = cb
+            view[c, :, 12:15] = np.einsum("bij,bj->bi", R, cb) + t
         return arr
 
     def centres(self, tree) -> np.ndarray:
-        return np.stack([tree.body_pose(b).rotation @ self.c_body[b]
-                         + tree.body_pose(b).translation for b in range(self.nb)])
+        R, t = tree.world_arrays()
+        return np.einsum("bij,bj->bi", R, np.asarray(self.c_body, dtype=float)) + t
 
     def run_body_pass(self, tree) -> np.ndarray:
         poses = self._poses(tree)
@@ -201,10 +204,8 @@ class BodyMoments:
 
 def _body_motion(cur, cand):
     """Per-body (D, delta) taking the current body poses to the candidate's."""
-    Rb = np.stack([cur.body_pose(b).rotation for b in range(cur.n_bodies)])
-    tb = np.stack([cur.body_pose(b).translation for b in range(cur.n_bodies)])
-    Rc = np.stack([cand.body_pose(b).rotation for b in range(cand.n_bodies)])
-    tc = np.stack([cand.body_pose(b).translation for b in range(cand.n_bodies)])
+    Rb, tb = cur.world_arrays()
+    Rc, tc = cand.world_arrays()
     D = Rc @ np.transpose(Rb, (0, 2, 1))
     return D, tc - np.einsum("bij,bj->bi", D, tb)
 

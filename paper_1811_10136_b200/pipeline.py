@@ -80,8 +80,8 @@ def _poses(model):
 
 def update_magnitude(before, after, diameter: float) -> float:
     """Largest per-body angle + shift / diameter (pipeline.py:79-86).  Node
-    graphs (hundreds of poses) take the batched form of the same formula."""
-    if hasattr(before, "_R") and hasattr(after, "_R") and len(before._R) > 32:
+    graphs and articulated trees take the batched form of the same formula."""
+    if hasattr(before, "_R") and hasattr(after, "_R") and len(before._R) > 1:
         Rb, tb = np.asarray(before._R, dtype=float), np.asarray(before._t, dtype=float)
         Ra, ta = np.asarray(after._R, dtype=float), np.asarray(after._t, dtype=float)
         c = (np.trace(Ra @ np.transpose(Rb, (0, 2, 1)), axis1=1, axis2=2) - 1.0) / 2.0
