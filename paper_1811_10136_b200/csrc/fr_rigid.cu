@@ -14,7 +14,14 @@
 //                    re-orthonormalisation (geometry.py:154-189), update
 //                    magnitude and termination (pipeline.py:141-177).
 //   k_rigid_objective  candidate objectives for point_to_plane halving.
-// With pass + solve in a CUDA graph an EM iteration needs no host round trip.
+//   k_rigid_pass_grid4 the point-to-point pass over the dense float32 slice
+//                    grid (quarter-scale embedding, clamped cells, four
+//                    consecutive points per thread).
+//   k_rigid_pass_tiles the device loop's pass over centred 1024-point tiles,
+//                    pass constants in the constant bank; its last block
+//                    reduces the partials and (in the EM loop) runs the
+//                    solve: one kernel per EM iteration.
+// With the iterations in a CUDA graph an EM iteration needs no host round trip.
 #include <math_constants.h>
 
 #include <algorithm>
@@ -481,18 +488,13 @@ constexpr size_t kF32Smem = (size_t)kP2PtBase * kPassThreads * sizeof(double);
 struct GridK {
     float2 Rc[3];           // (R0k, R1k): rows 0-1 of column k
     float2 R2[3];           // (R2k, 0)
-    float2 A01[3], A23[3];  // (A0k, A1k), (A2k, A3k)
-    float2 f01, f23;        // fractional pose constants (e0 - 4 base)
     float2 cw01, cw2;       // (cw0, cw1), (cw2, 0)
     float cref[3];
     float cp;
-    int C[3];               // ri - (a - 1) = bits(t) + C
-    unsigned lim[3];        // span + 2
-    int s0, s1;
-    unsigned K;             // cell of ri = bits0 * s0 + bits1 * s1 + bits2 + K
+    int s0, s1;             // cell strides of coordinates 0 and 1
     unsigned H;             // h = sum bits + H
-    // quarter-scale / clamped form (k_rigid_pass_grid4): el / 4 directly
-    float2 Q01[3], Q23[3];  // A / 4
+    // quarter-scale embedding: el / 4 directly
+    float2 Q01[3], Q23[3];  // (A0k, A1k) / 4, (A2k, A3k) / 4
     float2 q01, q23;        // (e0 - 4 base) / 4
     unsigned Cq[3];         // v = bits(t) + Cq = ri - (a - 2), clamped to limq
     unsigned limq[3];       // span + 4
@@ -503,29 +505,8 @@ constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23
 constexpr int kMagicBits = 0x4B400000;
 constexpr int kGridTab = 64 * 5;
 constexpr int kGridFold = 32;
-constexpr int kGridStages = 4;
 
-__device__ __forceinline__ void cp_async4(float *smem, const float *gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// stage this thread's PTS points of one ring stage: 32-bit offsets j from the
-// chunk's three plane pointers (a block's chunk is < 2^31 points)
-template <int PTS>
-__device__ __forceinline__ void ring_issue_pts(float (*slot)[3][kPassThreads], const float *p0,
-                                               const float *p1, const float *p2, int j, int cnt) {
-#pragma unroll
-    for (int k = 0; k < PTS; ++k) {
-        const int q = j + k * kPassThreads + (int)threadIdx.x;
-        if (q < cnt) {
-            cp_async4(&slot[k][0][threadIdx.x], p0 + q);
-            cp_async4(&slot[k][1][threadIdx.x], p1 + q);
-            cp_async4(&slot[k][2][threadIdx.x], p2 + q);
-        }
-    }
-    cp_async_commit();
-}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -611,13 +592,17 @@ struct GridAcc {
     }
 };
 
-// float32 pass constants of pose k over the dense grid dg (one thread)
+// float32 pass constants of pose k over the dense grid dg (one thread).  The
+// embedding is pre-scaled by 1/4 (exact: t = el/4 + magic, d/4 and the
+// barycentrics are bit-identical to the unscaled forms); the integer part of
+// the float64 pose constant e0 is split off exactly, so every float32
+// rounding acts on O(cloud / sigma) lattice units.
 __device__ __forceinline__ void grid_params(const RigidK &k, const DenseSliceF &dg, GridK &g) {
     for (int c = 0; c < 3; ++c) {
         g.Rc[c] = make_float2((float)k.R[c], (float)k.R[3 + c]);
         g.R2[c] = make_float2((float)k.R[6 + c], 0.0f);
-        g.A01[c] = make_float2((float)k.A[0][c], (float)k.A[1][c]);
-        g.A23[c] = make_float2((float)k.A[2][c], (float)k.A[3][c]);
+        g.Q01[c] = make_float2(0.25f * (float)k.A[0][c], 0.25f * (float)k.A[1][c]);
+        g.Q23[c] = make_float2(0.25f * (float)k.A[2][c], 0.25f * (float)k.A[3][c]);
         g.cref[c] = (float)k.c_ref[c];
     }
     int base[4];
@@ -627,141 +612,21 @@ __device__ __forceinline__ void grid_params(const RigidK &k, const DenseSliceF &
         base[i] = (int)b;
         fr0[i] = (float)(k.e0[i] - 4.0 * b);
     }
-    g.f01 = make_float2(fr0[0], fr0[1]);
-    g.f23 = make_float2(fr0[2], fr0[3]);
+    g.q01 = make_float2(0.25f * fr0[0], 0.25f * fr0[1]);
+    g.q23 = make_float2(0.25f * fr0[2], 0.25f * fr0[3]);
     g.cw01 = make_float2((float)k.c_world[0], (float)k.c_world[1]);
     g.cw2 = make_float2((float)k.c_world[2], 0.0f);
     g.cp = (float)k.cp;
-    const int st[3] = {dg.s0, dg.s1, 1};
-    unsigned K = 0, H = 0;
+    unsigned H = 0;
     for (int i = 0; i < 4; ++i) H += (unsigned)(base[i] - kMagicBits);
-    for (int i = 0; i < 3; ++i) {
-        g.C[i] = base[i] - kMagicBits - (dg.a[i] - 1);
-        g.lim[i] = dg.span[i] + 2u;
-        K += (unsigned)(base[i] - kMagicBits - (dg.a[i] - kDensePad)) * (unsigned)st[i];
-    }
-    g.s0 = dg.s0;
-    g.s1 = dg.s1;
-    g.K = K;
-    g.H = H;
-    // x 0.25 is exact: the quarter-scale path's t, d / 4 and barycentrics
-    // are bit-identical to the unscaled ones
     for (int c = 0; c < 3; ++c) {
-        g.Q01[c] = make_float2(0.25f * g.A01[c].x, 0.25f * g.A01[c].y);
-        g.Q23[c] = make_float2(0.25f * g.A23[c].x, 0.25f * g.A23[c].y);
         g.Cq[c] = (unsigned)(base[c] - kMagicBits - (dg.a[c] - 2));
         g.limq[c] = dg.span[c] + 4u;
     }
-    g.q01 = make_float2(0.25f * fr0[0], 0.25f * fr0[1]);
-    g.q23 = make_float2(0.25f * fr0[2], 0.25f * fr0[3]);
+    g.s0 = dg.s0;
+    g.s1 = dg.s1;
+    g.H = H;
     g.Kq = (unsigned)(kDensePad - 2) * (unsigned)(dg.s0 + dg.s1 + 1);
-}
-
-// one model point of the dense-grid pass (valid = 0: the point contributes
-// nothing; branch-free so the points of a thread interleave)
-__device__ __forceinline__ void grid_point(float nx, float ny, float nz, bool valid,
-                                           const GridK &g, const int4 *tab,
-                                           const DenseSliceF &dg, GridAcc &a) {
-    const float x0 = nx - g.cref[0], x1 = ny - g.cref[1], x2 = nz - g.cref[2];
-    // y = R xh as (y0, y1) and (y2, 1)
-    float2 y01 = __fmul2_rn(g.Rc[0], bc(x0));
-    y01 = __ffma2_rn(g.Rc[1], bc(x1), y01);
-    y01 = __ffma2_rn(g.Rc[2], bc(x2), y01);
-    float2 y2v = __ffma2_rn(g.R2[0], bc(x0), make_float2(0.0f, 1.0f));
-    y2v = __ffma2_rn(g.R2[1], bc(x1), y2v);
-    y2v = __ffma2_rn(g.R2[2], bc(x2), y2v);
-    // elevated coordinates minus 4 * base
-    float2 e01 = __ffma2_rn(g.A01[0], bc(y01.x), g.f01);
-    e01 = __ffma2_rn(g.A01[1], bc(y01.y), e01);
-    e01 = __ffma2_rn(g.A01[2], bc(y2v.x), e01);
-    float2 e23 = __ffma2_rn(g.A23[0], bc(y01.x), g.f23);
-    e23 = __ffma2_rn(g.A23[1], bc(y01.y), e23);
-    e23 = __ffma2_rn(g.A23[2], bc(y2v.x), e23);
-    const float el[4] = {e01.x, e01.y, e23.x, e23.y};
-    float d[4];
-    int tb[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float t = fmaf(el[i], 0.25f, kMagic);   // rint(el / 4) + magic
-        tb[i] = __float_as_int(t);
-        d[i] = fmaf(-4.0f, t - kMagic, el[i]);
-    }
-    unsigned code = 0;
-    {
-        int q = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = i + 1; j < 4; ++j, ++q) code |= (d[j] > d[i] ? 1u : 0u) << q;
-    }
-    // descending sorting network -> pre-wrap barycentrics
-    float s0 = fmaxf(d[0], d[1]), s1 = fminf(d[0], d[1]);
-    float s2 = fmaxf(d[2], d[3]), s3 = fminf(d[2], d[3]);
-    {
-        const float hi = fmaxf(s0, s2), lo = fminf(s0, s2);
-        s0 = hi;
-        s2 = lo;
-        const float hi2 = fmaxf(s1, s3), lo2 = fminf(s1, s3);
-        s1 = hi2;
-        s3 = lo2;
-        const float hi3 = fmaxf(s1, s2), lo3 = fminf(s1, s2);
-        s1 = hi3;
-        s2 = lo3;
-    }
-    const float b0 = fmaf(0.25f, s3 - s0, 1.0f);
-    const float b1 = 0.25f * (s2 - s3);
-    const float b2 = 0.25f * (s1 - s2);
-    const float b3 = 0.25f * (s0 - s1);
-    const int h = (int)((unsigned)tb[0] + (unsigned)tb[1] + (unsigned)tb[2] + (unsigned)tb[3] + g.H);
-    const int hi = min(max(h + 2, 0), 4);
-    const int4 T = tab[code * 5 + hi];
-    const bool in = ((unsigned)(tb[0] + g.C[0]) <= g.lim[0]) &
-                    ((unsigned)(tb[1] + g.C[1]) <= g.lim[1]) &
-                    ((unsigned)(tb[2] + g.C[2]) <= g.lim[2]);
-    float2 o01 = make_float2(0.f, 0.f), o23 = make_float2(0.f, 0.f);
-    if (in) {
-        const unsigned c4 = 4u * ((unsigned)tb[0] * (unsigned)g.s0 +
-                                  (unsigned)tb[1] * (unsigned)g.s1 + (unsigned)tb[2] + g.K);
-        const float4 v0 = __ldg(dg.cells + (int)(c4 + (unsigned)T.x));
-        const float4 v1 = __ldg(dg.cells + (int)(c4 + (unsigned)T.y));
-        const float4 v2 = __ldg(dg.cells + (int)(c4 + (unsigned)T.z));
-        const float4 v3 = __ldg(dg.cells + (int)(c4 + (unsigned)T.w));
-        o01 = __fmul2_rn(bc(b0), make_float2(v0.x, v0.y));
-        o23 = __fmul2_rn(bc(b0), make_float2(v0.z, v0.w));
-        o01 = __ffma2_rn(bc(b1), make_float2(v1.x, v1.y), o01);
-        o23 = __ffma2_rn(bc(b1), make_float2(v1.z, v1.w), o23);
-        o01 = __ffma2_rn(bc(b2), make_float2(v2.x, v2.y), o01);
-        o23 = __ffma2_rn(bc(b2), make_float2(v2.z, v2.w), o23);
-        o01 = __ffma2_rn(bc(b3), make_float2(v3.x, v3.y), o01);
-        o23 = __ffma2_rn(bc(b3), make_float2(v3.z, v3.w), o23);
-    }
-    // o01 = (sum y0, sum y1), o23 = (sum y2, mass)
-    const float m0 = fmaxf(o23.y, 0.0f);
-    const bool sup = m0 >= 1e-12f;
-    const float w = (sup && valid) ? (g.cp > 0.0f ? m0 * rcp_approx(m0 + g.cp) : 1.0f) : 0.0f;
-    const float ninv = sup ? -rcp_approx(m0) : 0.0f;
-    // residual r = x - t (centred); w = 0 zeroes every term of an
-    // unsupported point, whatever r holds
-    const float2 r01 = __fadd2_rn(y01, __ffma2_rn(o01, bc(ninv), g.cw01));
-    const float r2 = y2v.x + fmaf(o23.x, ninv, g.cw2.x);
-    const float2 wy01 = __fmul2_rn(bc(w), y01);
-    const float2 wy2v = __fmul2_rn(bc(w), y2v);          // (w y2, w)
-    const float2 wr01 = __fmul2_rn(bc(w), r01);
-    const float wr2 = w * r2;
-    a.s1_01 = __fadd2_rn(a.s1_01, wy01);
-    a.s1_2_s0 = __fadd2_rn(a.s1_2_s0, wy2v);
-    a.s2_00_01 = __ffma2_rn(bc(wy01.x), y01, a.s2_00_01);
-    a.s2_02_12 = __ffma2_rn(bc(y2v.x), wy01, a.s2_02_12);
-    a.s2_11 = fmaf(wy01.y, y01.y, a.s2_11);
-    a.s2_22 = fmaf(wy2v.x, y2v.x, a.s2_22);
-    a.rx01[0] = __ffma2_rn(bc(wr01.x), y01, a.rx01[0]);
-    a.rx2_r1[0] = __ffma2_rn(bc(wr01.x), y2v, a.rx2_r1[0]);
-    a.rx01[1] = __ffma2_rn(bc(wr01.y), y01, a.rx01[1]);
-    a.rx2_r1[1] = __ffma2_rn(bc(wr01.y), y2v, a.rx2_r1[1]);
-    a.rx01[2] = __ffma2_rn(bc(wr2), y01, a.rx01[2]);
-    a.rx2_r1[2] = __ffma2_rn(bc(wr2), y2v, a.rx2_r1[2]);
-    a.q01 = __ffma2_rn(wr01, r01, a.q01);
-    a.q2 = fmaf(wr2, r2, a.q2);
 }
 
 // base + 16 i as one IMAD.WIDE (keeps ptxas from re-associating the cell and
@@ -902,72 +767,6 @@ __device__ __forceinline__ void grid_warp_fold(const GridAcc &a, double *wacc) {
         }
     }
     if (lane < kP2PtBase) wacc[lane] += (double)v[0];
-}
-
-// PTS model points per thread per ring stage, MINB CTAs per SM
-template <bool DEV, int PTS, int MINB>
-__global__ void __launch_bounds__(kPassThreads, MINB)
-k_rigid_pass_grid(const float *__restrict__ ref, long long m, RigidK kv, const RigidK *kd,
-                  const int *done, DenseSliceF dg, double *__restrict__ partials) {
-    constexpr int NA = kP2PtBase;
-    __shared__ GridK g;
-    __shared__ int4 tab[kGridTab];
-    __shared__ float ring[kGridStages][PTS][3][kPassThreads];
-    if (DEV && *done) return;
-    if (threadIdx.x == 0) grid_params(DEV ? *kd : kv, dg, g);
-    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry(e, dg.s0, dg.s1);
-    __shared__ double wacc[kPassThreads / 32][NA];   // per-warp float64 accumulators
-    if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
-    __syncthreads();
-    double *my_wacc = wacc[threadIdx.x >> 5];
-    GridAcc a;
-    a.zero();
-    int fold = 0;
-    // contiguous chunk per block (Morton-sorted points: the block's gathers
-    // stay in a compact region of the grid, so they hit L1), streamed through
-    // a kGridStages-deep cp.async ring; each thread reads back only its own
-    // slots, so the ring needs no block barrier
-    const long long chunk = ((m + gridDim.x - 1) / gridDim.x + 31) & ~31ll;
-    const long long beg = (long long)blockIdx.x * chunk;
-    const int cnt = (int)max(0ll, min(beg + chunk, m) - beg);
-    const float *p0 = ref + min(beg, m), *p1 = p0 + m, *p2 = p1 + m;
-    constexpr int SP = PTS * kPassThreads;   // points per ring stage
-#pragma unroll
-    for (int st = 0; st < kGridStages - 1; ++st) ring_issue_pts<PTS>(ring[st], p0, p1, p2, st * SP, cnt);
-    int stage = 0;
-    for (int j = 0; j < cnt; j += SP) {
-        ring_issue_pts<PTS>(ring[stage == 0 ? kGridStages - 1 : stage - 1], p0, p1, p2,
-                            j + (kGridStages - 1) * SP, cnt);
-        cp_async_wait<kGridStages - 1>();
-        float px[PTS], py[PTS], pz[PTS];
-        bool ok[PTS];
-#pragma unroll
-        for (int k = 0; k < PTS; ++k) {
-            // a slot past the chunk end holds stale shared memory (maybe NaN,
-            // which w = 0 would not cancel): feed it finite coordinates
-            ok[k] = j + k * kPassThreads + (int)threadIdx.x < cnt;
-            px[k] = ok[k] ? ring[stage][k][0][threadIdx.x] : 0.0f;
-            py[k] = ok[k] ? ring[stage][k][1][threadIdx.x] : 0.0f;
-            pz[k] = ok[k] ? ring[stage][k][2][threadIdx.x] : 0.0f;
-        }
-        stage = stage + 1 == kGridStages ? 0 : stage + 1;
-#pragma unroll
-        for (int k = 0; k < PTS; ++k) grid_point(px[k], py[k], pz[k], ok[k], g, tab, dg, a);
-        fold += PTS;
-        if (fold >= kGridFold) {       // warp-uniform: every lane runs the same loop
-            grid_warp_fold(a, my_wacc);
-            a.zero();
-            fold = 0;
-        }
-    }
-    grid_warp_fold(a, my_wacc);
-    __syncthreads();
-    if (threadIdx.x < NA) {
-        double v = 0.0;
-#pragma unroll
-        for (int w = 0; w < kPassThreads / 32; ++w) v += wacc[w][threadIdx.x];
-        partials[(long long)blockIdx.x * NA + threadIdx.x] = v;
-    }
 }
 
 // streaming 16-byte load that leaves L1 to the grid gathers
@@ -1242,21 +1041,6 @@ k_rigid_pass_tiles(const float4 *__restrict__ tiles, long long m, const int *don
     pass_tail<SOLVE>(partials, dg, ta);
 }
 
-// dense-grid pass variant (FR_GRID_KERNEL): 5 (default) = k_rigid_pass_grid4,
-// with its pass constants in the constant bank when the device loop holds
-// c_grid (one EM object at a time, else shared memory); 4 = grid4 with
-// shared-memory constants always; 3 = the cp.async-ring k_rigid_pass_grid.
-// Measured at 16.8M points: 3: 135.7 us, 4: 125.1 us, 5: 120.4 us per pass;
-// grid4 at 3 CTAs/SM (80 registers, spills): 124 us
-static int grid_kernel() {
-    static int v = 0;
-    if (!v) {
-        const char *e = getenv("FR_GRID_KERNEL");
-        v = (e && e[0] >= '3' && e[0] <= '5') ? e[0] - '0' : 5;
-    }
-    return v;
-}
-
 // owner flag of c_grid: the first device EM object over a dense grid takes it
 static std::atomic<bool> g_const_grid_busy{false};
 // largest model cloud fr_rigid_em_run sends through the persistent one-CTA
@@ -1264,32 +1048,6 @@ static std::atomic<bool> g_const_grid_busy{false};
 static long long persist_max() {
     const char *e = getenv("FR_PERSIST_MAX");
     return e ? atoll(e) : 32768;
-}
-
-// points per thread per ring stage of the dense-grid pass (FR_GRID_PTS):
-// 3 (default: three independent chains per thread sharing the parameter
-// loads, 118 registers, 2 CTAs/SM: 139.6 us at 16.8M points), 2 (96
-// registers: 142.5 us) or 1 (4 CTAs/SM: 148 us)
-static int grid_pts() {
-    static int pts = 0;
-    if (!pts) {
-        const char *e = getenv("FR_GRID_PTS");
-        pts = (e && e[0] == '1') ? 1 : ((e && e[0] == '2') ? 2 : 3);
-    }
-    return pts;
-}
-
-// CTAs per SM of the two-point dense-grid pass (FR_GRID_MINB=2|3).  2 (96
-// registers, no spills) measured 142.5 us at 16.8M points; 3 caps registers at
-// 80 and spills 144 B per thread inside the loop (177.5 us); the one-point
-// form at 4 CTAs (64 registers) 148 us
-static int grid_minb() {
-    static int b = 0;
-    if (!b) {
-        const char *e = getenv("FR_GRID_MINB");
-        b = (e && e[0] == '3') ? 3 : 2;
-    }
-    return b;
 }
 
 static int set_f32_smem() {
@@ -1972,42 +1730,26 @@ static int launch_pass(const fr_lattice *lat, int mode, bool sig, int qpath, boo
         const SliceTableF tf = lat->table_f();
         const DenseSliceF dg = lat->dense;
         if (lat->dcells != nullptr) {
-            const int gk = grid_kernel();
-            if (gk >= 4) {
-                const bool vec = (m & 3) == 0;
-                const bool cst = dev && gk == 5 && gk_buf != nullptr;
-                const int g4 = 2 * sm_count();
+            const bool vec = (m & 3) == 0;
+            const int g4 = 2 * sm_count();
 #define FR_GRID4(DEV, VEC, B, C) \
     k_rigid_pass_grid4<DEV, VEC, B, C><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch)
-                if (cst) {
-                    k_grid_params<<<1, 1, 0, s>>>(kd, done, dg, gk_buf);
-                    FR_CHECK_LAUNCH();
-                    FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, gk_buf, sizeof(GridK), 0,
-                                                    cudaMemcpyDeviceToDevice, s));
-                    static const bool fold64 = getenv("FR_GRID_FOLD") && atoi(getenv("FR_GRID_FOLD")) == 64;
-                    if (vec && fold64) k_rigid_pass_grid4<true, true, 2, true, true, 64><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
-                    else if (vec) k_rigid_pass_grid4<true, true, 2, true, true><<<g4, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch);
-                    else FR_GRID4(true, false, 2, true);
-                }
-                else if (vec) { if (dev) FR_GRID4(true, true, 2, false); else FR_GRID4(false, true, 2, false); }
-                else { if (dev) FR_GRID4(true, false, 2, false); else FR_GRID4(false, false, 2, false); }
-#undef FR_GRID4
+            if (dev && gk_buf) {
+                // the owner of c_grid without the tiled copy (FR_GRID_TILES=0)
+                k_grid_params<<<1, 1, 0, s>>>(kd, done, dg, gk_buf);
                 FR_CHECK_LAUNCH();
-                k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g4, kP2PtBase, sums, done);
-                FR_CHECK_LAUNCH();
-                return FR_OK;
+                FR_CUDA(cudaMemcpyToSymbolAsync(c_grid, gk_buf, sizeof(GridK), 0,
+                                                cudaMemcpyDeviceToDevice, s));
+                if (vec)
+                    k_rigid_pass_grid4<true, true, 2, true, true><<<g4, kPassThreads, 0, s>>>(
+                        ref, m, k, kd, done, dg, scratch);
+                else FR_GRID4(true, false, 2, true);
             }
-            const int pts = grid_pts();
-            const int g3 = pts == 1 ? 4 * sm_count() : (pts == 3 ? 2 : grid_minb()) * sm_count();
-#define FR_GRID(DEV, P, B) \
-    k_rigid_pass_grid<DEV, P, B><<<g3, kPassThreads, 0, s>>>(ref, m, k, kd, done, dg, scratch)
-            if (pts == 1) { if (dev) FR_GRID(true, 1, 4); else FR_GRID(false, 1, 4); }
-            else if (grid_minb() == 3) { if (dev) FR_GRID(true, 2, 3); else FR_GRID(false, 2, 3); }
-            else if (pts == 3) { if (dev) FR_GRID(true, 3, 2); else FR_GRID(false, 3, 2); }
-            else { if (dev) FR_GRID(true, 2, 2); else FR_GRID(false, 2, 2); }
-#undef FR_GRID
+            else if (vec) { if (dev) FR_GRID4(true, true, 2, false); else FR_GRID4(false, true, 2, false); }
+            else { if (dev) FR_GRID4(true, false, 2, false); else FR_GRID4(false, false, 2, false); }
+#undef FR_GRID4
             FR_CHECK_LAUNCH();
-            k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g3, kP2PtBase, sums, done);
+            k_reduce_cols<<<1, 32 * kP2PtBase, 0, s>>>(scratch, g4, kP2PtBase, sums, done);
             FR_CHECK_LAUNCH();
             return FR_OK;
         } else {
