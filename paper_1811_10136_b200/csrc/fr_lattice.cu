@@ -155,17 +155,33 @@ __global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash
         if (s.overflow) atomicOr(&counters[2], 1ull);
         bool any_value = false;
         for (int cc = 0; cc < src.nv; ++cc) any_value |= (src.value(p, cc) != 0.0);
+        // the vertices' home slots probed together (their keys are mostly
+        // present already: one L2 round trip for the four, not four in a
+        // row); a miss takes the full insert
+        unsigned long long key[D + 1], home[D + 1];
+        unsigned hs[D + 1];
+#pragma unroll
+        for (int l = 0; l <= D; ++l) {
+            key[l] = s.packed(l);
+            hs[l] = (unsigned)mix64(key[l]) & h.mask;
+        }
+#pragma unroll
+        for (int l = 0; l <= D; ++l) home[l] = __ldcg(h.keys + hs[l]);
 #pragma unroll
         for (int l = 0; l <= D; ++l) {
             long long e = p * (D + 1) + l;
             unsigned slot = sentinel;
             if (s.bary[l] != 0.0 && any_value && !s.overflow) {
-                int created;
-                int sl = hash_insert(h, s.packed(l), &created);
-                if (sl < 0) atomicOr(&counters[2], 2ull);
-                else {
-                    slot = (unsigned)sl;
-                    if (created) atomicAdd(&counters[0], 1ull);
+                if (home[l] == key[l]) {
+                    slot = hs[l];
+                } else {
+                    int created;
+                    int sl = hash_insert(h, key[l], &created);
+                    if (sl < 0) atomicOr(&counters[2], 2ull);
+                    else {
+                        slot = (unsigned)sl;
+                        if (created) atomicAdd(&counters[0], 1ull);
+                    }
                 }
             }
             entry_slot[e] = slot;
