@@ -88,6 +88,15 @@ int fr_lattice_splat(fr_lattice *lat, const double *d_features, const double *d_
  * [1, y, (|y|^2 if FR_VALUES_M2), (n if FR_VALUES_NORMALS)] (estep.py:153-165). */
 int fr_lattice_splat_points(fr_lattice *lat, const float *d_pos, const float *d_normals,
                             int64_t n, int value_mode, void *stream);
+/* fr_upload_points + fr_lattice_splat_points (positions only, value columns
+ * [1, y] or [1, y, |y|^2]) in one call: each staged chunk's splat entries run
+ * as soon as its copy lands, overlapping the rest of the upload.  d_soa
+ * receives the (3, n) float32 planes as from fr_upload_points.  `uploaded`
+ * (nullable) is called with `ctx` on the calling thread once the host-side
+ * staging is done (the staged-upload slots are free for another upload)
+ * while the rest of the splat is still being enqueued. */
+int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
+                            float *d_soa, void *stream, void (*uploaded)(void *), void *ctx);
 
 /* (n, 3) float64 host rows (pageable) -> (3, n) float32 device planes, the
  * boundary conversion of PointCloud.positions / normals (geometry.py:109-139,

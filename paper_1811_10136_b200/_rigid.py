@@ -54,6 +54,9 @@ FAST_QUERY = True
 F32_POINTS = True
 # Sort the model points along a Morton curve once per registration.
 SPATIAL_ORDER = True
+# point-to-point setup: observation upload and splat in one pipelined call
+# (fr_lattice_splat_upload); False: upload, then splat
+PIPELINED_SPLAT = True
 
 
 def pass_flags() -> int:
@@ -238,8 +241,14 @@ class RigidDevicePath:
         main_stream = torch.cuda.current_stream()
         side = _side_stream()
         pool = ThreadPoolExecutor(max_workers=1)
+        import threading
+        self._obs_uploaded = threading.Event()
         obs_job = pool.submit(self._build_observation, observation, gmm, residual_mode, side,
                               lap if lap.marks else None)
+        # the observation upload (the critical path: its splat follows) takes
+        # the host memory bandwidth first; the model upload overlaps the splat
+        if residual_mode == "point_to_point" and PIPELINED_SPLAT:
+            self._obs_uploaded.wait(timeout=120.0)
         self.ref = upload_soa(reference.positions, self.dev)
         self.M = self.ref.shape[1]
         lap("upload_ref")
@@ -288,16 +297,37 @@ class RigidDevicePath:
         return outlier_constant(self.gmm.outlier_ratio, self.N, self.M_total, self.sigma)
 
     def _build_observation(self, observation, gmm, residual_mode, stream, lap=None) -> None:
+        try:
+            self._build_observation_on(observation, gmm, residual_mode, stream, lap)
+        finally:
+            self._obs_uploaded.set()      # never leave the model side waiting
+
+    def _build_observation_on(self, observation, gmm, residual_mode, stream, lap) -> None:
         import torch
         with torch.cuda.stream(stream):
-            self.obs = upload_soa(observation.positions, self.dev)
-            if lap is not None:
-                lap("obs_upload")
-            self.N = self.obs.shape[1]
-            self.obs_n = None
-            if residual_mode == "point_to_plane":
-                self.obs_n = upload_soa(observation.normals, self.dev)
-            self.build(gmm.sigma)
+            if residual_mode == "point_to_point" and PIPELINED_SPLAT:
+                # upload and splat in one call: the splat entries of each
+                # staged chunk overlap the rest of the upload
+                P = np.ascontiguousarray(observation.positions, dtype=np.float64)
+                self.obs = torch.empty((3, len(P)), dtype=torch.float32, device=self.dev)
+                self.N, self.obs_n = len(P), None
+                s = np.atleast_1d(np.asarray(gmm.sigma, dtype=float))
+                s = np.full(3, s[0]) if s.size == 1 else s
+                lat = PermutohedralLattice(3, s)
+                lat.splat_upload(P, self.obs, self.value_mode, uploaded=self._obs_uploaded.set)
+                if lap is not None:
+                    lap("obs_upload")
+                lat.blur()
+                self.lattice, self.sigma = lat, s
+            else:
+                self.obs = upload_soa(observation.positions, self.dev)
+                if lap is not None:
+                    lap("obs_upload")
+                self.N = self.obs.shape[1]
+                self.obs_n = None
+                if residual_mode == "point_to_plane":
+                    self.obs_n = upload_soa(observation.normals, self.dev)
+                self.build(gmm.sigma)
             if lap is not None:
                 lap("obs_built")
             stream.synchronize()

@@ -9,9 +9,18 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <functional>
+
 #include "../../include/filterreg_b200.h"
 
 namespace fr {
+
+// staged host -> device point upload (fr_upload.cu); the hook runs on the
+// worker threads after each sub-chunk's copy is enqueued, with the event that
+// marks the chunk [a, a + len) landed on the device
+using ChunkHook = std::function<void(long long, long long, cudaEvent_t)>;
+int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cudaStream_t s,
+                         const ChunkHook &hook);
 
 // ---------------------------------------------------------------------------
 // errors

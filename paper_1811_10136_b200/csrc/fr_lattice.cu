@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -143,11 +144,11 @@ struct PointSrc {
 
 // splat phase 1: embed, insert keys, record (slot, bary) per (point, vertex)
 template <int D, class Src>
-__global__ void k_splat_entries(Src src, long long n, LatticeConsts c, BuildHash h,
+__global__ void k_splat_entries(Src src, long long p0, long long p1, LatticeConsts c, BuildHash h,
                                 unsigned sentinel, unsigned *entry_slot, unsigned *entry_idx,
                                 double *entry_bary, double *contrib, unsigned long long *counters) {
     long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    for (long long p = p0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += stride) {
         double f[D];
         src.template feat<D>(p, f);
         Simplex<D> s;
@@ -744,8 +745,14 @@ static int reserve_sites(fr_lattice *lat, long long need, cudaStream_t s) {
     return FR_OK;
 }
 
+// a caller-run entries pass: given launch(a, b, stream) for the point range
+// [a, b), it enqueues every range and orders the splat's stream after them
+using EntriesLaunch = std::function<void(long long, long long, cudaStream_t)>;
+using EntriesHook = std::function<int(const EntriesLaunch &)>;
+
 template <int D, class Src>
-static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cudaStream_t s) {
+static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cudaStream_t s,
+                      const EntriesHook *first = nullptr) {
     if (lat->blurred || lat->splatted) {
         // the reference allows re-splatting an unblurred lattice (it replaces the table)
     }
@@ -800,13 +807,24 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     // hash sized for the unique-key count; grown x4 on overflow
     unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
     unsigned long long hc[3];
-    for (;;) {
+    for (int attempt = 0;; ++attempt) {
         FR_TRY(alloc_hash(lat, (unsigned)cap, s));
         FR_CUDA(cudaMemsetAsync(lat->d_counters, 0, 3 * sizeof(unsigned long long), s));
         BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
-        k_splat_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, n, lat->c, h, (unsigned)cap,
-                                                            entry_slot, entry_idx, entry_bary,
-                                                            contrib, lat->d_counters);
+        if (attempt == 0 && first) {
+            // the caller runs the entries pass itself (range by range as the
+            // points land) and leaves s ordered after it
+            const auto launch = [&](long long a, long long b, cudaStream_t st) {
+                k_splat_entries<D, Src><<<grid_for(b - a), 256, 0, st>>>(
+                    src, a, b, lat->c, h, (unsigned)cap, entry_slot, entry_idx, entry_bary,
+                    contrib, lat->d_counters);
+            };
+            FR_TRY((*first)(launch));
+        } else {
+            k_splat_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, 0, n, lat->c, h, (unsigned)cap,
+                                                                entry_slot, entry_idx, entry_bary,
+                                                                contrib, lat->d_counters);
+        }
         FR_CHECK_LAUNCH();
         FR_TRY(read_counters(lat, s, hc));
         bool full = (hc[2] & 2ull) || hc[0] * 2 > cap;
@@ -1392,6 +1410,49 @@ int fr_lattice_splat_points(fr_lattice *lat, const float *pos, const float *nrm,
     int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
     PointSrc src{pos, nrm, n, m2, nv};
     return splat_impl<3, PointSrc>(lat, src, n, nv, (cudaStream_t)stream);
+}
+
+int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
+                            float *d_soa, void *stream, void (*uploaded)(void *), void *ctx) {
+    if (!lat || (n > 0 && (!host_xyz || !d_soa))) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    if (lat->dim != 3) {
+        set_error("point splat needs a 3-D lattice");
+        return FR_EINVAL;
+    }
+    if (value_mode & FR_VALUES_NORMALS) {
+        set_error("fr_lattice_splat_upload takes positions only (normals: fr_lattice_splat_points)");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    lat->stream = s;
+    const int m2 = (value_mode & FR_VALUES_M2) ? 1 : 0;
+    const int nv = 4 + m2;
+    PointSrc src{d_soa, nullptr, n, m2, nv};
+    // the entries of each staged chunk run on a side stream as soon as the
+    // chunk's copy has landed, overlapping the rest of the upload
+    const EntriesHook hook = [&](const EntriesLaunch &launch) -> int {
+        cudaStream_t side;
+        FR_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        std::mutex mu;
+        const int st = upload_points_hooked(host_xyz, n, d_soa, s,
+                                            [&](long long a, long long len, cudaEvent_t landed) {
+            std::lock_guard<std::mutex> g(mu);
+            cudaStreamWaitEvent(side, landed, 0);
+            launch(a, a + len, side);
+        });
+        if (uploaded) uploaded(ctx);     // host staging done: the pinned slots are free
+        cudaEvent_t done;
+        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        cudaEventRecord(done, side);
+        cudaStreamWaitEvent(s, done, 0);
+        cudaEventDestroy(done);
+        cudaStreamDestroy(side);
+        return st;
+    };
+    return splat_impl<3, PointSrc>(lat, src, n, nv, s, &hook);
 }
 
 int fr_lattice_blur(fr_lattice *lat, void *stream) {

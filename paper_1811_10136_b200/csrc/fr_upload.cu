@@ -97,7 +97,7 @@ struct WorkerResult {
 };
 
 void worker(int id, const double *src, long long n, long long a, long long b, float *dst,
-            cudaStream_t s, WorkerResult *res) {
+            cudaStream_t s, WorkerResult *res, const ChunkHook *hook) {
     StagePool &p = pool();
     int slot = 0;
     for (long long c = a; c < b; c += kSubChunk) {
@@ -113,6 +113,7 @@ void worker(int id, const double *src, long long n, long long a, long long b, fl
                                   3, cudaMemcpyHostToDevice, s);
         }
         if (e == cudaSuccess) e = cudaEventRecord(p.done[id][slot], s);
+        if (e == cudaSuccess && hook && *hook) (*hook)(c, len, p.done[id][slot]);
         if (e != cudaSuccess) {
             res->status = FR_ECUDA;
             snprintf(res->msg, sizeof(res->msg), "point upload: %s", cudaGetErrorString(e));
@@ -127,13 +128,17 @@ void worker(int id, const double *src, long long n, long long a, long long b, fl
 
 using namespace fr;
 
-extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa, void *stream) {
+namespace fr {
+
+// the staged upload; `hook` (may be empty) is called from the worker threads
+// after each sub-chunk's copy was enqueued, with the event that marks it landed
+int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cudaStream_t s,
+                         const ChunkHook &hook) {
     if (n < 0 || (n > 0 && (!host_xyz || !d_soa))) {
         set_error("fr_upload_points: invalid arguments");
         return FR_EINVAL;
     }
     if (n == 0) return FR_OK;
-    cudaStream_t s = (cudaStream_t)stream;
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     long long cap = kMaxWorkers;
     if (const char *e = getenv("FR_UPLOAD_WORKERS")) cap = std::max(1, std::min(kMaxWorkers, atoi(e)));
@@ -149,7 +154,7 @@ extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa,
     for (int i = 0; i < w; ++i) {
         const long long a = std::min<long long>(n, (long long)i * per);
         const long long b = std::min<long long>(n, a + per);
-        th.emplace_back(worker, i, host_xyz, (long long)n, a, b, d_soa, s, &res[i]);
+        th.emplace_back(worker, i, host_xyz, (long long)n, a, b, d_soa, s, &res[i], &hook);
     }
     for (auto &t : th) t.join();
     for (const auto &r : res)
@@ -158,4 +163,10 @@ extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa,
             return r.status;
         }
     return FR_OK;
+}
+
+}  // namespace fr
+
+extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa, void *stream) {
+    return fr::upload_points_hooked(host_xyz, n, d_soa, (cudaStream_t)stream, fr::ChunkHook());
 }

@@ -98,6 +98,9 @@ def _reference_row_order(rows: np.ndarray) -> np.ndarray:
                       kind="stable")
 
 
+_UPLOADED_CB = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
+
+
 class PermutohedralLattice:
     """Splat/blur/slice Gaussian filter over an A*_d lattice, table in HBM
     (permutohedral.py:140-345)."""
@@ -183,6 +186,20 @@ class PermutohedralLattice:
         _lib.check(self._lib.fr_lattice_splat_points(
             self._h, _lib.ptr(positions_soa), _lib.ptr(normals_soa), n, value_mode,
             _lib.stream_handle()))
+        self.blurred = False
+        self._splatted = True
+        self._export = None
+
+    def splat_upload(self, host_positions, out_soa, value_mode: int = 0, uploaded=None) -> None:
+        """Upload (n, 3) float64 host positions into the float32 planes
+        `out_soa` (3, n) and splat [1, y, (|y|^2)] from them, each staged
+        chunk's splat entries overlapping the rest of the upload.  `uploaded()`
+        runs once the host-side staging is done."""
+        P = np.ascontiguousarray(host_positions, dtype=np.float64)
+        cb = _UPLOADED_CB((lambda _ctx: uploaded()) if uploaded is not None else (lambda _ctx: None))
+        _lib.check(self._lib.fr_lattice_splat_upload(
+            self._h, P.ctypes.data_as(ctypes.c_void_p), len(P), value_mode, _lib.ptr(out_soa),
+            _lib.stream_handle(), ctypes.cast(cb, ctypes.c_void_p), None))
         self.blurred = False
         self._splatted = True
         self._export = None

@@ -5,6 +5,8 @@ around the staging sub-chunk and worker split boundaries."""
 import numpy as np
 import pytest
 
+from oracle import filterreg_oracle as O
+
 pytestmark = pytest.mark.gpu
 
 
@@ -33,3 +35,31 @@ def test_upload_reuses_slots_across_calls():
     torch.cuda.synchronize()
     for c, o in zip(clouds, outs):
         assert np.array_equal(o.cpu().numpy(), c.astype(np.float32).T)
+
+
+@pytest.mark.parametrize("value_mode", [0, 1])
+def test_pipelined_upload_splat_matches_two_step(value_mode):
+    """fr_lattice_splat_upload (entries of each staged chunk overlapping the
+    upload) == fr_upload_points + fr_lattice_splat_points: planes bit-exact to
+    numpy astype(float32), pre- and post-blur site tables bit-exact."""
+    import torch
+    import paper_1811_10136_b200 as fr
+    from paper_1811_10136_b200.permutohedral import PermutohedralLattice
+    from paper_1811_10136_b200._rigid import upload_soa
+    model, obs, _ = O.pebble_pair(700_000, outlier_ratio=0.05, seed=2)
+    Y = obs.astype(np.float32).astype(float)
+    sigma = np.full(3, 0.03 * O.bbox_diameter(Y))
+    dev = torch.device("cuda", 0)
+    planes = torch.empty((3, len(Y)), dtype=torch.float32, device=dev)
+    a = PermutohedralLattice(3, sigma)
+    a.splat_upload(Y, planes, value_mode)
+    assert np.array_equal(planes.cpu().numpy(), Y.T.astype(np.float32))
+    b = PermutohedralLattice(3, sigma)
+    b.splat_points(upload_soa(Y, dev), None, value_mode)
+    for stage in ("splat", "blur"):
+        if stage == "blur":
+            a.blur()
+            b.blur()
+        assert a.num_sites == b.num_sites
+        assert np.array_equal(a.keys, b.keys)
+        assert np.array_equal(a.values, b.values)
