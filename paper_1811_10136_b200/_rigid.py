@@ -57,6 +57,9 @@ SPATIAL_ORDER = True
 # point-to-point setup: observation upload and splat in one pipelined call
 # (fr_lattice_splat_upload); False: upload, then splat
 PIPELINED_SPLAT = True
+# sigma re-estimation rebuilds splat a Morton-ordered copy of the observation
+# points (same sites; sums in that order)
+SORTED_REBUILD = True
 
 
 def pass_flags() -> int:
@@ -335,12 +338,24 @@ class RigidDevicePath:
                 lap("obs_synced")
 
     def build(self, sigma) -> None:
-        """(Re)build the observation lattice at kernel width sigma."""
+        """(Re)build the observation lattice at kernel width sigma.  The first
+        build splats the points in the caller's order (site sums bit-exact to
+        the reference); sigma re-estimation rebuilds (estep.py:232-259) splat
+        a Morton-ordered copy: the keys and occupied sites are the same, the
+        site sums add in that order (round-off apart, SURVEY 8(a) M0/M1
+        contract) and their row gathers become near-sequential."""
         s = np.atleast_1d(np.asarray(sigma, dtype=float))
         if s.size == 1:
             s = np.full(3, s[0])
+        pos = self.obs
+        if self.lattice is not None and SORTED_REBUILD and self.obs_n is None:
+            if getattr(self, "_obs_sorted", None) is None:
+                self._obs_sorted = self.obs.clone()
+                _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self._obs_sorted), self.N, 3,
+                                                          None, _lib.stream_handle()))
+            pos = self._obs_sorted
         lat = PermutohedralLattice(3, s)
-        lat.splat_points(self.obs, self.obs_n, self.value_mode)
+        lat.splat_points(pos, self.obs_n, self.value_mode)
         lat.blur()
         self.lattice, self.sigma = lat, s
 

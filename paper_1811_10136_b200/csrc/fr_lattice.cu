@@ -144,7 +144,8 @@ struct PointSrc {
 
 // splat phase 1: embed, insert keys, record (slot, bary) per (point, vertex)
 template <int D, class Src>
-__global__ void k_splat_entries(Src src, long long p0, long long p1, LatticeConsts c, BuildHash h,
+__global__ void k_splat_entries(Src src, long long p0, long long p1, long long n_all,
+                                LatticeConsts c, BuildHash h,
                                 unsigned sentinel, unsigned *entry_slot, unsigned *entry_idx,
                                 double *entry_bary, double *contrib, unsigned long long *counters) {
     long long stride = (long long)gridDim.x * blockDim.x;
@@ -188,11 +189,14 @@ __global__ void k_splat_entries(Src src, long long p0, long long p1, LatticeCons
             entry_slot[e] = slot;
             entry_idx[e] = (unsigned)e;
             entry_bary[e] = s.bary[l];
-            // the entry's products bary * value (NumPy's single rounding), laid
-            // out as one row so the site sums gather one row per entry
+            // the entry's products bary * value (NumPy's single rounding), one
+            // row per entry, vertex-major ([l][p] rows): a site's entries share
+            // their vertex index l, so for spatially ordered points its rows
+            // are near-contiguous for the site sums' gathers
             if (contrib && slot != sentinel)
                 for (int cc = 0; cc < src.nv; ++cc)
-                    contrib[e * src.nv + cc] = __dmul_rn(s.bary[l], src.value(p, cc));
+                    contrib[((size_t)l * n_all + p) * src.nv + cc] =
+                        __dmul_rn(s.bary[l], src.value(p, cc));
         }
     }
 }
@@ -221,7 +225,7 @@ template <int D, class Src>
 __global__ void __launch_bounds__(kSegBlock)
 k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int *run_cnt,
                const unsigned *sorted_idx, const double *entry_bary, const double *contrib,
-               unsigned sentinel, int nv, double *run_vals) {
+               unsigned sentinel, int nv, double *run_vals, long long lmajor_n = 0) {
     extern __shared__ double ring[];   // [kSegStages][kSegBlock][nv]
     const int r = blockIdx.x;
     if (run_slot && run_slot[r] == sentinel) return;   // (null: no sentinel runs)
@@ -234,7 +238,9 @@ k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int 
             const unsigned e = sorted_idx[beg + j];
             double *row = ring + ((size_t)(ch % kSegStages) * kSegBlock + t) * nv;
             if (contrib) {
-                const double *cr = contrib + (size_t)e * nv;
+                // rows [l][p] (lmajor_n = point count) or [p][l] (0)
+                const size_t rix = lmajor_n ? (size_t)(e % (D + 1)) * lmajor_n + e / (D + 1) : e;
+                const double *cr = contrib + rix * nv;
                 for (int c = 0; c < nv; ++c) row[c] = __ldg(cr + c);
             } else {
                 const double b = entry_bary[e];
@@ -816,12 +822,12 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
             // points land) and leaves s ordered after it
             const auto launch = [&](long long a, long long b, cudaStream_t st) {
                 k_splat_entries<D, Src><<<grid_for(b - a), 256, 0, st>>>(
-                    src, a, b, lat->c, h, (unsigned)cap, entry_slot, entry_idx, entry_bary,
+                    src, a, b, n, lat->c, h, (unsigned)cap, entry_slot, entry_idx, entry_bary,
                     contrib, lat->d_counters);
             };
             FR_TRY((*first)(launch));
         } else {
-            k_splat_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, 0, n, lat->c, h, (unsigned)cap,
+            k_splat_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, 0, n, n, lat->c, h, (unsigned)cap,
                                                                 entry_slot, entry_idx, entry_bary,
                                                                 contrib, lat->d_counters);
         }
@@ -879,7 +885,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         if (nruns > 0) {
             k_splat_segsum<D, Src><<<nruns, kSegBlock, smem, s>>>(
                 src, run_slot, run_off, run_cnt, sorted_idx, entry_bary, contrib, (unsigned)cap,
-                nv, run_vals);
+                nv, run_vals, n);
             FR_CHECK_LAUNCH();
         }
         k_run_live<<<grid_for(nruns), 256, 0, s>>>(nruns, run_slot, (unsigned)cap, run_vals, nv,
