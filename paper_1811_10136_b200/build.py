@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfilterreg_b200.so")
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-              "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-shared", "-Xptxas", "-warn-spills"]
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-Xptxas", "-warn-spills"]
 
 
 def sources():
@@ -31,13 +31,32 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    """Each translation unit compiled in parallel (no device code crosses
+    files), then one shared-library link."""
     if not force and not stale():
         return OUT
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", OUT + ".tmp", *sources()]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+    with tempfile.TemporaryDirectory(prefix="fr_build_") as tmp:
+        objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in sources()]
+        cmds = [[nvcc, *NVCC_FLAGS, "-c", "-o", obj, src] for src, obj in zip(sources(), objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), flush=True)
+        with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+            results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True),
+                                  cmds))
+        for c, r in zip(cmds, results):
+            if verbose and (r.stdout or r.stderr):
+                print(r.stdout + r.stderr, end="", flush=True)
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, c, r.stdout, r.stderr)
+        link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                "-Xcompiler", "-pthread", "-o", OUT + ".tmp", *objs]
+        if verbose:
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 
