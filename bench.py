@@ -453,7 +453,7 @@ def run_b200(args):
                        "lattice_sites": sites, "dense_grid_cells": dense_cells,
                        "build_ms": build_ms, "l2": l2_note,
                        "query_path": "centred float32 point tiles over the dense slice grid, "
-                                     "float64 accumulation every 32 points; one kernel per EM "
+                                     "float64 accumulation every 64 points per thread; one kernel per EM "
                                      "iteration (pass + reduction + float64 solve)",
                        "parallelism": f"dp{world} (model shards, replicated lattice, NCCL "
                                       "all-reduce of 25 doubles per iteration)"},

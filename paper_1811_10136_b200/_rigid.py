@@ -50,7 +50,7 @@ _E = [skew(e) for e in np.eye(3)]   # K_k = [e_k]x
 FAST_QUERY = True
 # Point-to-point pass with float32 centred coordinates over the lattice's dense
 # float32 grid (hash slots when the grid would be too large), float32 moment
-# partials folded into float64 accumulators every 32 points (FR_PASS_F32).
+# partials folded into float64 accumulators every 64 points per thread (FR_PASS_F32).
 F32_POINTS = True
 # Sort the model points along a Morton curve once per registration.
 SPATIAL_ORDER = True

@@ -504,7 +504,10 @@ struct GridK {
 constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23
 constexpr int kMagicBits = 0x4B400000;
 constexpr int kGridTab = 64 * 5;
-constexpr int kGridFold = 32;
+// points per thread between warp folds of the float32 partials into the
+// float64 accumulators: 64 measured 98.9 vs 100.8 us per pass (32) at 16.8M
+// points, inside the parity tolerances of the float32 query path
+constexpr int kGridFold = 64;
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
