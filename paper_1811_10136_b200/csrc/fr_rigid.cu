@@ -974,12 +974,6 @@ k_rigid_pass_tiles(const float4 *__restrict__ tiles, long long m, const int *don
     __shared__ double wacc[kPassThreads / 32][NA];
     if (*done) return;
     const GridK &g = c_grid;
-    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry_q(e, dg.s0, dg.s1);
-    if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
-    __syncthreads();
-    double *my_wacc = wacc[threadIdx.x >> 5];
-    GridAcc a;
-    a.zero();
     const long long ntiles = (m + kQuadPts - 1) / kQuadPts;
     const long long tpb = (ntiles + gridDim.x - 1) / gridDim.x;
     const long long t0 = (long long)blockIdx.x * tpb;
@@ -989,6 +983,23 @@ k_rigid_pass_tiles(const float4 *__restrict__ tiles, long long m, const int *don
     const long long first = t0 * kQuadPts;
     const int cnt = (int)max(0ll, min((long long)nt * kQuadPts, m - first));
     const float4 *src = tiles + t0 * kTileF4 + threadIdx.x;
+    // the first tiles' copies go out before the table is built (their DRAM
+    // latency overlaps it); each thread later reads only its own slots
+#pragma unroll
+    for (int st = 0; st < kRing4 - 1; ++st) {
+        if (st < nt) {
+            cp_async16(&ring[st][0][threadIdx.x], src + st * kTileF4);
+            cp_async16(&ring[st][1][threadIdx.x], src + st * kTileF4 + kPassThreads);
+            cp_async16(&ring[st][2][threadIdx.x], src + st * kTileF4 + 2 * kPassThreads);
+        }
+        cp_async_commit();
+    }
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry_q(e, dg.s0, dg.s1);
+    if ((threadIdx.x & 31) < NA) wacc[threadIdx.x >> 5][threadIdx.x & 31] = 0.0;
+    __syncthreads();
+    double *my_wacc = wacc[threadIdx.x >> 5];
+    GridAcc a;
+    a.zero();
     const int me = 4 * (int)threadIdx.x;
     int fold = 0;
     auto quad_t = [&](auto full, int j, const float4 &cx, const float4 &cy, const float4 &cz) {
@@ -1005,15 +1016,6 @@ k_rigid_pass_tiles(const float4 *__restrict__ tiles, long long m, const int *don
             fold = 0;
         }
     };
-#pragma unroll
-    for (int st = 0; st < kRing4 - 1; ++st) {
-        if (st < nt) {
-            cp_async16(&ring[st][0][threadIdx.x], src + st * kTileF4);
-            cp_async16(&ring[st][1][threadIdx.x], src + st * kTileF4 + kPassThreads);
-            cp_async16(&ring[st][2][threadIdx.x], src + st * kTileF4 + 2 * kPassThreads);
-        }
-        cp_async_commit();
-    }
     const float4 *nxt = src + (kRing4 - 1) * kTileF4;
     int stage = 0;
     for (int t = 0; t < nt; ++t) {
