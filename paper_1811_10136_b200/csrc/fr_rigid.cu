@@ -2297,13 +2297,36 @@ int fr_rigid_em_persistent(const fr_rigid_em *em) {
 
 int fr_rigid_em_run(fr_rigid_em *em, void *stream) {
     if (fr_rigid_em_persistent(em)) return fr_rigid_em_run_batch(&em, 1, stream);
-    // poll the done flag after 8, then every 32 iterations (iterations after
-    // termination are no-op launches)
-    int done = 0;
-    for (int guard = 0, step = 8; !done && guard < em->max_iters + 40; guard += step, step = 32) {
-        FR_TRY(fr_rigid_em_enqueue(em, step, stream));
-        FR_TRY(fr_rigid_em_status(em, &done, nullptr, nullptr, stream));
+    // one chunk of iterations always in flight: chunk k + 1 is enqueued before
+    // the host waits for chunk k's done flag (copied into pinned memory behind
+    // it), so the GPU never drains for a poll; iterations after termination
+    // are no-op launches (8 first, then chunks of 32)
+    cudaStream_t s = (cudaStream_t)stream;
+    static thread_local int *flags = nullptr;      // [2][4] pinned
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (!flags) {
+        FR_CUDA(cudaHostAlloc((void **)&flags, 8 * sizeof(int), cudaHostAllocDefault));
+        for (int i = 0; i < 2; ++i) FR_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     }
+    int issued = 0, k = 0;
+    auto chunk = [&](int n) -> int {
+        FR_TRY(fr_rigid_em_enqueue(em, n, stream));
+        FR_CUDA(cudaMemcpyAsync(flags + 4 * (k & 1), &em->d_em->done, 3 * sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+        FR_CUDA(cudaEventRecord(ev[k & 1], s));
+        issued += n;
+        ++k;
+        return FR_OK;
+    };
+    FR_TRY(chunk(8));
+    while (true) {
+        const bool more = issued < em->max_iters + 40;
+        if (more) FR_TRY(chunk(32));
+        const int prev = (k - (more ? 2 : 1)) & 1;
+        FR_CUDA(cudaEventSynchronize(ev[prev]));
+        if (flags[4 * prev] || !more) break;
+    }
+    FR_CUDA(cudaStreamSynchronize(s));
     return FR_OK;
 }
 
