@@ -22,6 +22,7 @@
 //                    reduces the partials and (in the EM loop) runs the
 //                    solve: one kernel per EM iteration.
 // With the iterations in a CUDA graph an EM iteration needs no host round trip.
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include <algorithm>
@@ -1702,6 +1703,105 @@ k_em_persistent(const PersistProblem *probs) {
 }
 
 // ---------------------------------------------------------------------------
+// cluster-cooperative EM for small problems: a thread-block cluster of
+// kEmCluster CTAs (one per SM) runs one registration's whole EM loop.  Each
+// CTA sweeps 1/kEmCluster of the points; the leader (rank 0) sums the CTAs'
+// 25 partial sums over distributed shared memory in rank order, runs the
+// float64 solve and publishes the next pass constants and the done flag in
+// its shared memory, which the other CTAs read over DSMEM after the cluster
+// barrier.  Two cluster barriers per iteration, no global memory round trip
+// and no kernel launch between iterations.  A launch with P clusters runs P
+// problems; the reduction order is fixed (warps, then ranks), so a problem's
+// result does not depend on what else shares the launch.
+constexpr int kEmCluster = 8;
+
+__global__ void __cluster_dims__(kEmCluster, 1, 1) __launch_bounds__(kPersistThreads, 1)
+k_em_cluster(const PersistProblem *probs) {
+    namespace cg = cooperative_groups;
+    constexpr int NA = kP2PtBase;
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    const PersistProblem P = probs[blockIdx.x / kEmCluster];
+    __shared__ EmDev se;               // leader only
+    __shared__ GridK g;                // this CTA's copy of the pass constants
+    __shared__ GridK g_next;           // leader: constants of the next iteration
+    __shared__ int done_flag;          // leader: loop state
+    __shared__ int4 tab[kGridTab];
+    __shared__ double wacc[kPersistThreads / 32][NA];
+    __shared__ double bsum[NA];        // this CTA's partial sums
+    __shared__ double tsum[NA];        // leader: cluster sums
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long beg = P.m * rank / kEmCluster, end = P.m * (rank + 1) / kEmCluster;
+    if (rank == 0) em_copy(&se, P.em, threadIdx.x, blockDim.x);
+    for (int e = threadIdx.x; e < kGridTab; e += blockDim.x) tab[e] = grid_entry_q(e, P.dg.s0, P.dg.s1);
+    __syncthreads();
+    if (rank == 0 && threadIdx.x == 0) {
+        done_flag = se.done;
+        if (!se.done) grid_params(se.k, P.dg, g_next);
+    }
+    cl.sync();
+    const volatile int *ldone = cl.map_shared_rank(&done_flag, 0);
+    const unsigned *lg = reinterpret_cast<const unsigned *>(cl.map_shared_rank(&g_next, 0));
+    while (!*ldone) {                  // cluster-uniform: read after a cluster barrier
+        static_assert(sizeof(GridK) % 4 == 0, "GridK copied as words");
+        for (int w = threadIdx.x; w < (int)(sizeof(GridK) / 4); w += blockDim.x)
+            reinterpret_cast<unsigned *>(&g)[w] = lg[w];
+        if (lane < NA) wacc[warp][lane] = 0.0;
+        __syncthreads();
+        GridAcc a;
+        a.zero();
+        int fold = 0;
+        constexpr int PP = 3;
+        for (long long base = beg; base < end; base += PP * kPersistThreads) {
+            float x[PP], y[PP], z[PP];
+            bool ok[PP];
+#pragma unroll
+            for (int k = 0; k < PP; ++k) {
+                const long long p = base + k * kPersistThreads + threadIdx.x;
+                ok[k] = p < end;
+                x[k] = ok[k] ? __ldg(P.ref + p) : 0.0f;
+                y[k] = ok[k] ? __ldg(P.ref + P.m + p) : 0.0f;
+                z[k] = ok[k] ? __ldg(P.ref + 2 * P.m + p) : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < PP; ++k) grid_point_q(x[k], y[k], z[k], ok[k], g, tab, P.dg.cells, a);
+            fold += PP;
+            if (fold >= kGridFold) {
+                grid_warp_fold(a, wacc[warp]);
+                a.zero();
+                fold = 0;
+            }
+        }
+        grid_warp_fold(a, wacc[warp]);
+        __syncthreads();
+        if (threadIdx.x < NA) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < kPersistThreads / 32; ++w) v += wacc[w][threadIdx.x];
+            bsum[threadIdx.x] = v;
+        }
+        cl.sync();                     // every CTA's partials are final
+        if (rank == 0) {
+            if (threadIdx.x < NA) {
+                double v = 0.0;
+                for (int r = 0; r < kEmCluster; ++r) v += cl.map_shared_rank(bsum, r)[threadIdx.x];
+                tsum[threadIdx.x] = v;
+                P.sums[threadIdx.x] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                rigid_solve_body(tsum, &se, P.objs, P.tnorms, P.masses);
+                if (!se.done) grid_params(se.k, P.dg, g_next);
+                done_flag = se.done;
+            }
+        }
+        cl.sync();                     // the leader's flag and constants are published
+    }
+    if (rank == 0) em_copy(P.em, &se, threadIdx.x, blockDim.x);
+    cl.sync();                         // no CTA leaves while its DSMEM may still be read
+}
+
+// ---------------------------------------------------------------------------
 // host
 
 static int width(int mode, int sig) {
@@ -2261,6 +2361,13 @@ static bool em_persist_ok(const fr_rigid_em *em) {
 }
 
 
+// FR_EM_CLUSTER=0: one CTA per small problem (k_em_persistent) instead of a
+// cluster of kEmCluster CTAs (k_em_cluster)
+static bool em_cluster() {
+    const char *e = getenv("FR_EM_CLUSTER");
+    return !(e && e[0] == '0');
+}
+
 int fr_rigid_em_run_batch(fr_rigid_em **ems, int n, void *stream) {
     if (n < 0 || (n > 0 && !ems)) {
         set_error("invalid batch arguments");
@@ -2284,7 +2391,8 @@ int fr_rigid_em_run_batch(fr_rigid_em **ems, int n, void *stream) {
     FR_CUDA(cudaMallocAsync((void **)&d, h.size() * sizeof(PersistProblem), s));
     FR_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(PersistProblem), cudaMemcpyHostToDevice,
                             s));
-    k_em_persistent<<<n, kPersistThreads, 0, s>>>(d);
+    if (em_cluster()) k_em_cluster<<<n * kEmCluster, kPersistThreads, 0, s>>>(d);
+    else k_em_persistent<<<n, kPersistThreads, 0, s>>>(d);
     FR_CHECK_LAUNCH();
     FR_CUDA(cudaFreeAsync(d, s));
     FR_CUDA(cudaStreamSynchronize(s));   // the host vector h backs the copy
