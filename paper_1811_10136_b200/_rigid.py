@@ -160,6 +160,32 @@ def upload_soa(points, dev):
 
 _SIDE_STREAMS: dict = {}
 
+# model + observation points below which the setup runs on the calling thread
+SETUP_OVERLAP_MIN = 400_000
+
+
+class _InlineExecutor:
+    """ThreadPoolExecutor stand-in that runs the job on submit."""
+
+    class _Done:
+        def __init__(self, fn, args):
+            self._exc, self._val = None, None
+            try:
+                self._val = fn(*args)
+            except BaseException as e:      # re-raised by result(), as a Future would
+                self._exc = e
+
+        def result(self):
+            if self._exc is not None:
+                raise self._exc
+            return self._val
+
+    def submit(self, fn, *args):
+        return self._Done(fn, args)
+
+    def shutdown(self, wait=True):
+        pass
+
 
 def _side_stream():
     """The observation-side setup stream of this thread / device, kept for the
@@ -243,14 +269,17 @@ class RigidDevicePath:
         self.sigma = None
         main_stream = torch.cuda.current_stream()
         side = _side_stream()
-        pool = ThreadPoolExecutor(max_workers=1)
+        # small clouds: the worker thread's handoff costs more than the
+        # overlap saves (and serialises on the GIL in register_batch)
+        small = len(reference.positions) + len(observation.positions) < SETUP_OVERLAP_MIN
+        pool = _InlineExecutor() if small else ThreadPoolExecutor(max_workers=1)
         import threading
         self._obs_uploaded = threading.Event()
         obs_job = pool.submit(self._build_observation, observation, gmm, residual_mode, side,
                               lap if lap.marks else None)
         # the observation upload (the critical path: its splat follows) takes
         # the host memory bandwidth first; the model upload overlaps the splat
-        if residual_mode == "point_to_point" and PIPELINED_SPLAT:
+        if residual_mode == "point_to_point" and PIPELINED_SPLAT and not small:
             self._obs_uploaded.wait(timeout=120.0)
         self.ref = upload_soa(reference.positions, self.dev)
         self.M = self.ref.shape[1]
