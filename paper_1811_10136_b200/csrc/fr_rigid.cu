@@ -1377,7 +1377,8 @@ __device__ void twist_exp_dev(const double *tw, double *R, double *t) {
         b = 0.5 - th * th / 24.0;
         c = 1.0 / 6.0 - th * th / 120.0;
     } else {
-        const double s = sin(th), co = cos(th);
+        double s, co;
+        sincos(th, &s, &co);            // one range reduction for both
         a = s / th;
         b = (1.0 - co) / (th * th);
         c = (th - s) / (th * th * th);
@@ -1417,7 +1418,9 @@ __device__ double rotation_angle_dev(const double *R) {
 
 // (A + lam I) x = b by Cholesky; false when not positive definite
 __device__ bool chol6_solve(const double (*A)[6], double lam, const double *b, double *x) {
-    double L[6][6];
+    // one reciprocal per pivot instead of a float64 division per entry (the
+    // serial solve sits on every EM iteration's critical path)
+    double L[6][6], r[6];
     for (int i = 0; i < 6; ++i)
         for (int j = 0; j <= i; ++j) {
             double s = A[i][j] + (i == j ? lam : 0.0);
@@ -1425,20 +1428,21 @@ __device__ bool chol6_solve(const double (*A)[6], double lam, const double *b, d
             if (i == j) {
                 if (!(s > 0.0) || !isfinite(s)) return false;
                 L[i][i] = sqrt(s);
+                r[i] = 1.0 / L[i][i];
             } else {
-                L[i][j] = s / L[j][j];
+                L[i][j] = s * r[j];
             }
         }
     double y[6];
     for (int i = 0; i < 6; ++i) {
         double s = b[i];
         for (int k = 0; k < i; ++k) s -= L[i][k] * y[k];
-        y[i] = s / L[i][i];
+        y[i] = s * r[i];
     }
     for (int i = 5; i >= 0; --i) {
         double s = y[i];
         for (int k = i + 1; k < 6; ++k) s -= L[k][i] * x[k];
-        x[i] = s / L[i][i];
+        x[i] = s * r[i];
     }
     for (int i = 0; i < 6; ++i)
         if (!isfinite(x[i])) return false;

@@ -196,7 +196,10 @@ def test_device_loop_mstep_options(fr, path, monkeypatch):
     ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
     dev = fr.register(ref, obs, fr.RigidModel(), fr.RegistrationConfig(**base))
     host = fr.register(ref, obs, fr.RigidModel(), fr.RegistrationConfig(**base, record_states=True))
-    tol = LOOP_TOL[path]
+    # the device Cholesky multiplies by pivot reciprocals (LAPACK divides):
+    # with three GN iterations per EM step over 60 iterations those last-bit
+    # differences grow to ~2e-8 rad (the reference contract is 1e-4 rad)
+    tol = max(LOOP_TOL[path], 1e-7)
     assert dev.iterations == host.iterations
     assert O.rotation_angle(dev.kinematics.pose.rotation @ host.kinematics.pose.rotation.T) < tol
     np.testing.assert_allclose(dev.objectives, host.objectives, rtol=tol)
