@@ -351,6 +351,47 @@ int fr_rigid_em_result(fr_rigid_em *em, double *R, double *t, double *objectives
                        double *twist_norms, double *inlier_masses, int *iterations,
                        int *termination, void *stream);
 
+/* ---- float64 device-resident rigid EM loop (pipeline.py:125-181 with the
+ * reference's float64 arithmetic; point_to_point, fixed kernel width) ------
+ * Model points are float64 SoA planes (d_ref: 3 planes of m, the caller's
+ * values, Morton-ordered by fr_sort_points_morton64).  Every query-side
+ * operation (forward map kinematics.py:317-320, elevation and simplex
+ * permutohedral.py:171-215, slice permutohedral.py:329-341 over the
+ * lattice's dense float64 grid, moments epilogue estep.py:195-205, the
+ * point-to-point statistics of mstep.py:102-210) runs in float64; the solve
+ * is the same float64 device solve as fr_rigid_em.  fr_em64_run runs up to
+ * n_iters iterations (<= 0: max_em_iters) in ONE cooperative grid-resident
+ * launch: pass, fixed-order reduction by the last CTA to arrive, solve, and a
+ * release of the next pose to the spinning CTAs, per iteration.  Sharded
+ * runs call fr_em64_pass, all-reduce fr_em64_sums, then fr_em64_solve. */
+typedef struct fr_em64 fr_em64;
+
+int fr_em64_create(const fr_lattice *lat, const double *d_ref, int64_t m,
+                   const fr_rigid_em_config *cfg, void *stream, fr_em64 **out);
+int fr_em64_destroy(fr_em64 *em);
+int fr_em64_run(fr_em64 *em, int n_iters, void *stream);
+/* one pass + fixed-order reduction at the current pose into the sums buffer
+ * (no solve): kernel timing and the sharded loop */
+int fr_em64_pass(fr_em64 *em, void *stream);
+int fr_em64_solve(fr_em64 *em, void *stream);
+int fr_em64_sums(fr_em64 *em, double **d_sums, int *width);
+/* CTAs and threads per CTA of the grid-resident kernel (launch accounting) */
+int fr_em64_launch_info(const fr_em64 *em, int *grid, int *block);
+int fr_em64_status(fr_em64 *em, int *done, int *iterations, int *termination, void *stream);
+int fr_em64_result(fr_em64 *em, double *R, double *t, double *objectives, double *twist_norms,
+                   double *inlier_masses, int *iterations, int *termination, void *stream);
+
+/* float64 counterparts of the point helpers above: (n, 3) host rows ->
+ * (3, n) float64 device planes (a transpose, no rounding); splat of
+ * [1, y, (|y|^2), (n)] from float64 planes; Morton reorder of float64 planes */
+int fr_upload_points64(const double *host_xyz, int64_t n, double *d_soa, void *stream);
+int fr_lattice_splat_points64(fr_lattice *lat, const double *d_pos, const double *d_normals,
+                              int64_t n, int value_mode, void *stream);
+int fr_sort_points_morton64(double *d_pos, int64_t n, int planes, int32_t *d_perm, void *stream);
+/* Cells of the dense float64 slice grid fr_em64 slices (0: none -- the site
+ * box exceeds FR_DENSE64_MAX_CELLS, default 8M cells of 128 B). */
+int fr_lattice_dense_cells64(const fr_lattice *lat, int64_t *cells);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,6 +32,7 @@ weight/target/normal planes the pass stored.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -60,6 +61,14 @@ PIPELINED_SPLAT = True
 # sigma re-estimation rebuilds splat a Morton-ordered copy of the observation
 # points (same sites; sums in that order)
 SORTED_REBUILD = True
+
+
+# Arithmetic of the point-to-point device EM loop: "f64" (default) -- the
+# reference's float64 everywhere: float64 point planes (the caller's values bit
+# for bit), float64 forward map / simplex / slice over the dense float64 grid /
+# epilogue / statistics in one grid-resident kernel (fr_em64_*); "f32" -- the
+# float32 point path above (FR_PASS_F32).  FR_PRECISION overrides.
+PRECISION = os.environ.get("FR_PRECISION", "f64")
 
 
 def pass_flags() -> int:
@@ -158,6 +167,17 @@ def upload_soa(points, dev):
     return soa
 
 
+def upload_soa64(points, dev):
+    """(n, 3) host coordinates -> (3, n) float64 device planes (a transpose
+    through the native staged upload, fr_upload_points64; no rounding)."""
+    import torch
+    P = np.ascontiguousarray(points, dtype=np.float64)
+    soa = torch.empty((3, P.shape[0]), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().fr_upload_points64(P.ctypes.data_as(ctypes.c_void_p), P.shape[0],
+                                              _lib.ptr(soa), _lib.stream_handle()))
+    return soa
+
+
 _SIDE_STREAMS: dict = {}
 
 # model + observation points below which the setup runs on the calling thread
@@ -244,10 +264,15 @@ class RigidDevicePath:
     planes, the observation lattice, and the reduction buffers."""
 
     def __init__(self, reference, observation, gmm, residual_mode: str, process_group=None,
-                 sort: bool = True):
+                 sort: bool = True, precision: str = "f32"):
         import torch
         self.dev = _lib.device()
         self.lib = _lib.load()
+        if precision not in ("f32", "f64"):
+            raise ValueError(f"unknown precision {precision!r}")
+        # float64 planes for the float64 device loop (point_to_point, fixed sigma)
+        self.f64 = precision == "f64" and residual_mode == "point_to_point" \
+            and not gmm.update_sigma
         self.mode = _lib.FR_POINT_TO_PLANE if residual_mode == "point_to_plane" \
             else _lib.FR_POINT_TO_POINT
         self.gmm = gmm
@@ -279,9 +304,10 @@ class RigidDevicePath:
                               lap if lap.marks else None)
         # the observation upload (the critical path: its splat follows) takes
         # the host memory bandwidth first; the model upload overlaps the splat
-        if residual_mode == "point_to_point" and PIPELINED_SPLAT and not small:
+        if residual_mode == "point_to_point" and PIPELINED_SPLAT and not small and not self.f64:
             self._obs_uploaded.wait(timeout=120.0)
-        self.ref = upload_soa(reference.positions, self.dev)
+        self.ref = upload_soa64(reference.positions, self.dev) if self.f64 \
+            else upload_soa(reference.positions, self.dev)
         self.M = self.ref.shape[1]
         lap("upload_ref")
         # global quantities a shard must not compute locally:
@@ -298,8 +324,8 @@ class RigidDevicePath:
         if sort and SPATIAL_ORDER and self.M > 1:
             # Morton order of the model points: reduction sums are order-free up
             # to float64 round-off, and neighbouring threads share table lines
-            _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self.ref), self.M, 3, None,
-                                                      _lib.stream_handle()))
+            fn = self.lib.fr_sort_points_morton64 if self.f64 else self.lib.fr_sort_points_morton
+            _lib.check(fn(_lib.ptr(self.ref), self.M, 3, None, _lib.stream_handle()))
         lap("morton_sort")
         self.width = self.lib.fr_rigid_pass_width(self.mode, int(self.with_sigma))
         f64 = dict(dtype=torch.float64, device=self.dev)
@@ -322,6 +348,13 @@ class RigidDevicePath:
         lap("observation_side")
         self.setup_s = lap.phases
 
+    def demote_f32(self) -> None:
+        """Float32 copies of the float64 planes (for the float32-plane pass
+        kernels; the caller's values round to nearest)."""
+        if self.ref.dtype != np.float32 and str(self.ref.dtype) != "torch.float32":
+            self.ref = self.ref.float()
+        self.f64 = False
+
     @property
     def c_prime(self) -> float:
         """Outlier constant over the global model count (estep.py:97-112,
@@ -337,7 +370,15 @@ class RigidDevicePath:
     def _build_observation_on(self, observation, gmm, residual_mode, stream, lap) -> None:
         import torch
         with torch.cuda.stream(stream):
-            if residual_mode == "point_to_point" and PIPELINED_SPLAT:
+            if self.f64:
+                # float64 planes, splat from them (keys bit-exact for any input)
+                self.obs = upload_soa64(observation.positions, self.dev)
+                self.N, self.obs_n = self.obs.shape[1], None
+                self._obs_uploaded.set()
+                if lap is not None:
+                    lap("obs_upload")
+                self.build(gmm.sigma)
+            elif residual_mode == "point_to_point" and PIPELINED_SPLAT:
                 # upload and splat in one call: the splat entries of each
                 # staged chunk overlap the rest of the upload
                 P = np.ascontiguousarray(observation.positions, dtype=np.float64)
@@ -373,6 +414,7 @@ class RigidDevicePath:
         a Morton-ordered copy: the keys and occupied sites are the same, the
         site sums add in that order (round-off apart, SURVEY 8(a) M0/M1
         contract) and their row gathers become near-sequential."""
+        import torch
         s = np.atleast_1d(np.asarray(sigma, dtype=float))
         if s.size == 1:
             s = np.full(3, s[0])
@@ -380,8 +422,9 @@ class RigidDevicePath:
         if self.lattice is not None and SORTED_REBUILD and self.obs_n is None:
             if getattr(self, "_obs_sorted", None) is None:
                 self._obs_sorted = self.obs.clone()
-                _lib.check(self.lib.fr_sort_points_morton(_lib.ptr(self._obs_sorted), self.N, 3,
-                                                          None, _lib.stream_handle()))
+                fn = self.lib.fr_sort_points_morton64 if self.obs.dtype == torch.float64 \
+                    else self.lib.fr_sort_points_morton
+                _lib.check(fn(_lib.ptr(self._obs_sorted), self.N, 3, None, _lib.stream_handle()))
             pos = self._obs_sorted
         lat = PermutohedralLattice(3, s)
         lat.splat_points(pos, self.obs_n, self.value_mode)
@@ -552,3 +595,116 @@ class DeviceEM:
         k = min(int(it.value), n)
         return (R.reshape(3, 3), t, list(obj[:k]), list(tn[:k]), list(ms[:k]), int(it.value),
                 _lib.FR_TERM[int(term.value)])
+
+
+class DeviceEM64:
+    """The float64 rigid point-to-point EM loop (fr_em64_*): one cooperative
+    grid-resident kernel runs pass, fixed-order reduction and the float64
+    solve of every iteration to termination.  With a process group each
+    iteration is pass -> all-reduce of the 25 sums -> solve, and the
+    termination flag is polled in chunks of iterations (every rank issues the
+    same number of collectives)."""
+
+    CHUNK = 8
+
+    def __init__(self, path: RigidDevicePath, R0, t0, config):
+        import torch
+        self.path = path
+        self.lib = path.lib
+        self.max_iters = int(config.max_em_iters)
+        c = _lib.RigidEmConfig()
+        c.R0[:] = list(np.asarray(R0, dtype=float).reshape(-1))
+        c.t0[:] = list(np.asarray(t0, dtype=float).reshape(-1))
+        c.c_ref[:] = list(path.c_ref)
+        c.sigma_inv[:] = list(1.0 / np.asarray(path.sigma, dtype=float))
+        c.c_prime = path.c_prime
+        c.diameter = path.diameter
+        c.twist_tolerance = float(config.twist_tolerance)
+        ms = config.mstep
+        c.damping = -1.0 if ms.damping is None else float(ms.damping)
+        c.step_tolerance = float(ms.step_tolerance)
+        c.degenerate_mass = 1e-9 * path.M_total
+        c.max_em_iters = self.max_iters
+        c.max_gn_iters = int(ms.max_gn_iters)
+        c.max_halvings = int(ms.max_halvings)
+        c.fast = 0
+        self._cfg = c
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.fr_em64_create(path.lattice.handle, _lib.ptr(path.ref), path.M,
+                                           ctypes.byref(c), _lib.stream_handle(),
+                                           ctypes.byref(h)))
+        self.h = h
+        sp = ctypes.c_void_p()
+        w = ctypes.c_int()
+        _lib.check(self.lib.fr_em64_sums(h, ctypes.byref(sp), ctypes.byref(w)))
+        self.sums = torch.as_tensor(_DeviceArray(sp.value, w.value), device=path.dev)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.fr_em64_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def launch_info(self):
+        g, b = ctypes.c_int(), ctypes.c_int()
+        _lib.check(self.lib.fr_em64_launch_info(self.h, ctypes.byref(g), ctypes.byref(b)))
+        return int(g.value), int(b.value)
+
+    def enqueue(self, n: int) -> None:
+        """Enqueue up to n more iterations without synchronising."""
+        if self.path.group is None:
+            _lib.check(self.lib.fr_em64_run(self.h, int(n), _lib.stream_handle()))
+            return
+        for _ in range(int(n)):
+            _lib.check(self.lib.fr_em64_pass(self.h, _lib.stream_handle()))
+            self.path.reduce_device(self.sums)
+            _lib.check(self.lib.fr_em64_solve(self.h, _lib.stream_handle()))
+
+    def pass_only(self) -> None:
+        """One pass + reduction at the current pose (no solve)."""
+        _lib.check(self.lib.fr_em64_pass(self.h, _lib.stream_handle()))
+
+    def status(self):
+        d, it, term = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(self.lib.fr_em64_status(self.h, ctypes.byref(d), ctypes.byref(it),
+                                           ctypes.byref(term), _lib.stream_handle()))
+        return bool(d.value), int(it.value), _lib.FR_TERM[int(term.value)]
+
+    def run(self) -> None:
+        if self.path.group is None:
+            _lib.check(self.lib.fr_em64_run(self.h, 0, _lib.stream_handle()))
+            return
+        while True:
+            self.enqueue(self.CHUNK)
+            if self.status()[0]:
+                return
+
+    def result(self):
+        n = self.max_iters
+        R = np.zeros(9)
+        t = np.zeros(3)
+        obj, tn, ms = np.zeros(n), np.zeros(n), np.zeros(n)
+        it, term = ctypes.c_int(), ctypes.c_int()
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        _lib.check(self.lib.fr_em64_result(self.h, dp(R), dp(t), dp(obj), dp(tn), dp(ms),
+                                           ctypes.byref(it), ctypes.byref(term),
+                                           _lib.stream_handle()))
+        k = min(int(it.value), n)
+        return (R.reshape(3, 3), t, list(obj[:k]), list(tn[:k]), list(ms[:k]), int(it.value),
+                _lib.FR_TERM[int(term.value)])
+
+
+def device_em(path: RigidDevicePath, R0, t0, config):
+    """The device EM loop of a path: float64 (DeviceEM64) on float64 planes
+    with a dense float64 grid, else the float32-point loop (DeviceEM; a
+    lattice whose site box exceeds the float64 grid budget runs DeviceEM's
+    all-float64 hash-table pass over float32 copies of the planes)."""
+    if path.f64:
+        if path.lattice.dense64:
+            return DeviceEM64(path, R0, t0, config)
+        path.demote_f32()
+        return DeviceEM(path, R0, t0, config, fast=0)
+    return DeviceEM(path, R0, t0, config)

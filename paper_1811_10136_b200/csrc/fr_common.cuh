@@ -18,7 +18,7 @@ namespace fr {
 // staged host -> device point upload (fr_upload.cu); the hook runs on the
 // worker threads after each sub-chunk's copy is enqueued, with the event that
 // marks the chunk [a, a + len) landed on the device
-using ChunkHook = std::function<void(long long, long long, cudaEvent_t)>;
+using ChunkHook = std::function<int(long long, long long, cudaEvent_t)>;
 int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cudaStream_t s,
                          const ChunkHook &hook);
 
@@ -26,6 +26,7 @@ int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cuda
 // errors
 
 void set_error(const char *fmt, ...);
+const char *last_error();
 
 #define FR_CUDA(expr)                                                          \
     do {                                                                       \
@@ -455,6 +456,16 @@ struct DenseSliceF {
     int s0, s1;             // cell strides of coordinates 0 and 1 (coordinate 2: 1)
 };
 
+// dense float64 slice grid, the float64 query path's table (same cells and
+// padding as DenseSliceF): per (cell, remainder class) one 32-byte row
+// gain * (sum y0, sum y1 | sum y2, mass) as two double2
+struct DenseSliceD {
+    const double2 *cells;   // [n0][n1][n2][4][2]
+    int a[3];               // site q minimum per coordinate
+    int n[3];               // padded extents (span + 2 * kDensePad)
+    int s0, s1;             // cell strides of coordinates 0 and 1
+};
+
 // float32 variant of qsimplex3 (packed keys for the hash-slot table)
 __device__ __forceinline__ void qsimplex3f(const float *frac, const int *base, QSimplex3 &q) {
     constexpr int kLim = (int)(kKeyLim / 4 - 2);
@@ -566,6 +577,9 @@ struct fr_lattice {
     float4 *dcells = nullptr;
     fr::DenseSliceF dense{};
     long long dense_cells = 0;
+    // dense float64 slice grid (same box; FR_DENSE64_MAX_CELLS) for the float64 EM loop
+    double2 *dcells64 = nullptr;
+    fr::DenseSliceD dense64{};
     // d >= 4: sorted 128-bit site keys (hi / lo words) and their codec
     unsigned long long *wkh = nullptr, *wkl = nullptr;
     fr::WideCodec wc{};

@@ -1,0 +1,820 @@
+// The float64 rigid point-to-point EM loop on B200 (the reference's arithmetic:
+// every operation on the query path is float64, as twistreg's NumPy code).
+//
+// One cooperative, grid-resident kernel runs a whole registration:
+//
+//   per EM iteration (pipeline.py:141-177)
+//     every CTA   sweeps its contiguous slice of the Morton-ordered model
+//                 points (float64 SoA planes, the caller's values bit for
+//                 bit): forward map x = R (x_ref - c_ref) + c_world
+//                 (kinematics.py:317-320), elevation and enclosing simplex
+//                 (permutohedral.py:171-215: remainder-0 point, stable
+//                 descending ranks, single wrap, barycentrics), slice over the
+//                 dense float64 grid (permutohedral.py:329-341: four 32-byte
+//                 rows, index arithmetic instead of hashing), the moments
+//                 epilogue (estep.py:195-205: m0 clamp, w = m0 / (m0 + c'),
+//                 target = m1 / m0) and the 25 point-to-point sufficient
+//                 statistics of the M step (mstep.py:102-210), accumulated in
+//                 float64 registers;
+//     block       warp reduce-scatter (31 shuffles for 25 columns) + a fixed-
+//                 order sum over the 8 warps -> one row of partials;
+//     grid        arrival counter; the LAST CTA to arrive sums the rows in a
+//                 fixed order, runs the float64 solve (fr_solve.cuh: normal
+//                 equations, damped Cholesky with tenfold escalation, step
+//                 halving with closed-form candidate objectives, twist update,
+//                 update magnitude, termination) and publishes the next pose
+//                 with a release increment of a generation word the other CTAs
+//                 spin on (acquire).
+//
+// No launches, host polls or graph replays between iterations; all sums are
+// formed in a fixed order, so reruns are bit-identical.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "fr_common.cuh"
+#include "fr_reduce.cuh"
+#include "fr_solve.cuh"
+
+namespace fr {
+
+constexpr int kE64Threads = 256;
+constexpr int kE64Stats = 25;        // point-to-point sufficient statistics (_rigid.py)
+constexpr int kE64Row = 32;          // partials row stride (doubles)
+constexpr int kE64MaxSms = 160;      // grid <= MINB x this (the column sums' row registers)
+
+struct Em64Args {
+    const double *tiles; // [n_tiles][3][T] centred model points (Morton order), T = threads
+    long long m;
+    int tiles_per_cta;   // contiguous tiles per CTA
+    DenseSliceD g;
+    EmDev *em;           // state; em->k holds the current pass constants
+    double *partials;    // [gridDim.x][kE64Row]
+    double *sums;        // [kE64Row] the last pass's reduced statistics
+    double *traces;      // [3][max_iters]
+    unsigned *counter;   // arrivals of the current iteration
+    unsigned *gen;       // release generation
+    int n_iters;         // iterations of this launch (or fewer: termination)
+    int solve;           // 0: pass + reduction only
+    unsigned long long *prof;   // optional phase timestamps [n_iters][8] (FR_EM64_PROFILE)
+    // pose-independent constants (kernel parameters: constant-bank operands)
+    double sc[3];        // sf_j / sigma_j: f = x * sc (permutohedral.py:172)
+    double cp;           // outlier constant c' (estep.py:99-112)
+};
+
+// pose constants of one iteration, held in registers by every thread
+struct Pose64 {
+    double R[9];
+    double cw[3];        // R c_ref + t
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_add(unsigned *p) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+// 1 / x to ~1 ulp without a slow path: MUFU seed, one cubic and one Newton
+// step (x > 0 finite; x = 0 gives inf, masked by the caller)
+__device__ __forceinline__ double rcp64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(fma(e, e, e), r, r);
+    e = fma(-x, r, 1.0);
+    return fma(e, r, r);
+}
+
+constexpr double kRoundMagic = 6755399441055744.0;     // 1.5 * 2^52
+
+// p ? a : b as a predicated select (no branch)
+__device__ __forceinline__ double sel64(bool p, double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+        : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)p));
+    return r;
+}
+
+// one model point: forward map, simplex, slice, epilogue, statistics
+// (h0, h1, h2) = x_ref - c_ref (the centred tile); valid = 0 for the padding
+// of the last tile (computed, contributes nothing: no branch)
+__device__ __forceinline__ void e64_point(const Em64Args &a, const Pose64 &k, double cp,
+                                          double h0, double h1, double h2, bool valid,
+                                          double (&acc)[kE64Stats]) {
+    const DenseSliceD &g = a.g;
+    double xt[3], X[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        xt[i] = fma(k.R[3 * i + 2], h2, fma(k.R[3 * i + 1], h1, k.R[3 * i] * h0));
+        X[i] = xt[i] + k.cw[i];                          // x = R x_ref + t
+    }
+    // elevation E (x / sigma * sf) (permutohedral.py:171-179): row 0 = 1s,
+    // row j: -j at column j-1, 1 at columns >= j
+    const double f0 = X[0] * a.sc[0], f1 = X[1] * a.sc[1], f2 = X[2] * a.sc[2];
+    const double u = f1 + f2;
+    double el[4];
+    el[0] = f0 + u;
+    el[1] = u - f0;
+    el[2] = fma(-2.0, f1, f2);
+    el[3] = -3.0 * f2;
+    // rint(el / 4) (round half to even, as np.rint) by the 1.5 * 2^52 magic
+    // add: the integer sits in the low word; el - rem0 with one rounding
+    // (permutohedral.py:191-193).  Points beyond 2^40 lattice units get no
+    // support.
+    const bool in_range = (fabs(f0) + fabs(f1)) + fabs(f2) < 1e12;
+    int ri[4];
+    double d[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double t = fma(el[i], 0.25, kRoundMagic);
+        ri[i] = __double2loint(t);
+        d[i] = fma(-4.0, t - kRoundMagic, el[i]);
+    }
+    const int h = (ri[0] + ri[1]) + (ri[2] + ri[3]);
+    // stable descending ranks (:194-197): rank_i = #{j: d_j > d_i} + #{j < i: d_j == d_i}
+    const bool c01 = d[1] > d[0], c02 = d[2] > d[0], c03 = d[3] > d[0];
+    const bool c12 = d[2] > d[1], c13 = d[3] > d[1], c23 = d[3] > d[2];
+    int rank[4];
+    rank[0] = (int)c01 + (int)c02 + (int)c03;
+    rank[1] = (int)!c01 + (int)c12 + (int)c13;
+    rank[2] = (int)!c02 + (int)!c12 + (int)c23;
+    rank[3] = (int)!c03 + (int)!c13 + (int)!c23;
+    // vertex cells from the unwrapped ranks: vertex l (remainder class l) of
+    // the wrapped simplex (:198-203, 214) has cell coordinates
+    // q_c = ri_c - floor((rank_c + h + l) / 4); the remainder-0 cell is
+    // clamped into [2, n - 2]: a point clamped there has every vertex in the
+    // zero padding, as a point whose vertices have no site
+    int t[3], base = 0;
+    {
+        const int cq0 = min(max(ri[0] - g.a[0] + kDensePad, 2), g.n[0] - 2);
+        const int cq1 = min(max(ri[1] - g.a[1] + kDensePad, 2), g.n[1] - 2);
+        const int cq2 = min(max(ri[2] - g.a[2] + kDensePad, 2), g.n[2] - 2);
+        base = cq0 * g.s0 + cq1 * g.s1 + cq2;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) t[c] = rank[c] + h;
+    // single +-(d+1) wrap of the ranks and res = (el - rem0') / (d+1) (:206)
+    double res[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rk = rank[i] + h;
+        const int adj = (rk > 3) - (rk < 0);             // rem0' = rem0 - 4 adj
+        rank[i] = rk - 4 * adj;
+        res[i] = fma(d[i], 0.25, (double)adj);
+    }
+    double sv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        sv[r] = sel64(rank[0] == r, res[0], sel64(rank[1] == r, res[1],
+                                                  sel64(rank[2] == r, res[2], res[3])));
+    double bary[4];
+    bary[0] = (1.0 + sv[3]) - sv[0];                       // (:211-212)
+#pragma unroll
+    for (int l = 1; l < 4; ++l) bary[l] = sv[3 - l] - sv[4 - l];
+    double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        const int cell = base - ((t[0] + l) >> 2) * g.s0 - ((t[1] + l) >> 2) * g.s1 -
+                         ((t[2] + l) >> 2);
+        const double2 *row = g.cells + 2 * (4 * cell + l);
+        const double2 ra = __ldg(row), rb = __ldg(row + 1);
+        o0 = fma(bary[l], ra.x, o0);
+        o1 = fma(bary[l], ra.y, o1);
+        o2 = fma(bary[l], rb.x, o2);
+        o3 = fma(bary[l], rb.y, o3);
+    }
+    // moments epilogue (estep.py:195-205): m0 = max(out0, 0), supported iff
+    // m0 >= 1e-12, w = m0 / (m0 + c'), target = m1 / m0; unsupported points
+    // get w = 0 and target = x (zero residual).  One reciprocal:
+    // q = 1 / (m0 (m0 + c')), 1 / m0 = (m0 + c') q, w = m0^2 q.
+    const double m0 = o3 > 0.0 ? o3 : 0.0;
+    const bool sup = m0 >= 1e-12 && in_range && valid;
+    const double den = m0 + cp;
+    const double q = rcp64(m0 * den);
+    const double inv = den * q;
+    const double w = sup ? (cp > 0.0 ? (m0 * m0) * q : 1.0) : 0.0;
+    double r[3];
+    r[0] = sup ? fma(-o0, inv, X[0]) : 0.0;
+    r[1] = sup ? fma(-o1, inv, X[1]) : 0.0;
+    r[2] = sup ? fma(-o2, inv, X[2]) : 0.0;
+    // sufficient statistics about c_world (layout: _rigid.py)
+    double wy[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) wy[j] = w * xt[j];
+    acc[0] += w;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) acc[1 + j] += wy[j];
+    acc[4] = fma(wy[0], xt[0], acc[4]);
+    acc[5] = fma(wy[0], xt[1], acc[5]);
+    acc[6] = fma(wy[0], xt[2], acc[6]);
+    acc[7] = fma(wy[1], xt[1], acc[7]);
+    acc[8] = fma(wy[1], xt[2], acc[8]);
+    acc[9] = fma(wy[2], xt[2], acc[9]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const double wr = w * r[j];
+        acc[10 + j] += wr;
+#pragma unroll
+        for (int q2 = 0; q2 < 3; ++q2) acc[13 + 3 * j + q2] = fma(wr, xt[q2], acc[13 + 3 * j + q2]);
+        acc[22 + j] = fma(wr, r[j], acc[22 + j]);
+    }
+}
+
+// warp reduce-scatter of N <= 32 columns, in place: after the five butterfly
+// steps lane L holds the warp's sum of column L (0 for L >= N).  31 shuffles
+// instead of the 5 N of a per-column tree.  Fixed order (deterministic).
+template <int N>
+__device__ __forceinline__ double warp_reduce_scatter(double (&v)[N]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+        const bool upper = lane & k;
+#pragma unroll
+        for (int i = 0; i < k; ++i) {
+            if (i >= N) break;
+            const double lo = v[i];
+            const double hi = (i + k < N) ? v[i + k] : 0.0;
+            const double send = upper ? lo : hi;
+            const double keep = upper ? hi : lo;
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+        }
+    }
+    return v[0];
+}
+
+// L2-coherent copy (the last CTA of the previous iteration wrote it from
+// another SM; L1 may hold the old lines)
+template <class T>
+__device__ __forceinline__ void copy_cg(T *dst, const T *src, int lane, int nlanes) {
+    static_assert(sizeof(T) % 8 == 0, "copied as 8-byte words");
+    const unsigned long long *a = reinterpret_cast<const unsigned long long *>(src);
+    unsigned long long *b = reinterpret_cast<unsigned long long *>(dst);
+    for (int w = lane; w < (int)(sizeof(T) / 8); w += nlanes) b[w] = __ldcg(a + w);
+}
+
+// One CTA of the grid-resident loop.  Every CTA keeps the EM state (EmDev)
+// in shared memory and runs the SAME fixed-order reduction and float64 solve
+// on the same partial rows, so all CTAs hold bit-identical poses without a
+// broadcast: an iteration costs one arrival barrier (monotone counter,
+// release/acquire) and one read of the partial rows -- no release hop, no
+// state round trip through global memory.  Partial rows are double-buffered
+// by iteration parity (a CTA can only reuse a buffer after every CTA passed
+// the next barrier, i.e. finished reading it).
+// TMA bulk copies into a shared-memory ring (cp.async.bulk + mbarrier
+// transaction counts): one elected thread keeps S tiles in flight -- the
+// point stream needs ~40 KB in flight per SM to cover the HBM latency, far
+// more than one register prefetch per thread holds
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes,
+                                          unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// One CTA of the grid-resident loop.  Every CTA keeps the EM state (EmDev)
+// in shared memory and runs the SAME fixed-order reduction and float64 solve
+// on the same partial rows, so all CTAs hold bit-identical poses without a
+// broadcast: an iteration costs one arrival barrier (monotone counter,
+// release/acquire) and one read of the partial rows -- no release hop, no
+// state round trip through global memory.  Partial rows are double-buffered
+// by iteration parity (a CTA can only reuse a buffer after every CTA passed
+// the next barrier, i.e. finished reading it).  The CTA's tiles stream
+// through an S-stage TMA ring that runs ahead across iteration boundaries
+// (the points do not depend on the pose), so the next iteration's first
+// tiles land during the barrier and the solve.
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int THREADS, int MINB, int S>
+__global__ void __launch_bounds__(THREADS + (S ? 32 : 0), MINB) k_em64(Em64Args a) {
+    // S > 0: warp W produces tiles into an S-stage TMA ring; S == 0: every
+    // thread prefetches its next point into registers (plain loads)
+    constexpr int W = THREADS / 32;          // consumer warps
+    constexpr int NT = THREADS + (S ? 32 : 0);
+    constexpr int SS = S ? S : 1;
+    constexpr unsigned kTileBytes = 3u * THREADS * sizeof(double);
+    extern __shared__ __align__(128) double ring[];          // [S][3][THREADS]
+    __shared__ double red[W][32];
+    __shared__ double tsum[kE64Row];
+    __shared__ EmDev se;
+    __shared__ __align__(8) unsigned long long full[SS], empty[SS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = S && warp == W;
+    const int nb = (int)gridDim.x;
+    const long long t0 = (long long)blockIdx.x * a.tiles_per_cta;
+    const long long n_tiles_all = (a.m + THREADS - 1) / THREADS;
+    const int nt = (int)max(0LL, min((long long)a.tiles_per_cta, n_tiles_all - t0));
+    const double cp = a.cp;
+    copy_cg(&se, a.em, tid, NT);
+    if (S && tid == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], W);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // tile sequence k = 0, 1, ... walks this CTA's tiles cyclically (iteration
+    // k / nt, tile k % nt) through stage k % S; the producer keeps S tiles in
+    // flight, across iteration boundaries (the points do not depend on the pose)
+    const unsigned n_total = (unsigned)nt * (unsigned)a.n_iters;
+    unsigned issued = 0;                     // producer lane 0 only
+    auto produce_until = [&](unsigned upto) {
+        for (; issued < upto && issued < n_total; ++issued) {
+            const unsigned st = issued % SS;
+            if (issued >= (unsigned)SS) mbar_wait(&empty[st], ((issued / SS) + 1) & 1);
+            bulk_load(ring + st * 3 * THREADS, a.tiles + (t0 + issued % nt) * 3 * THREADS,
+                      kTileBytes, &full[st]);
+        }
+    };
+    if (producer && lane == 0) produce_until(SS);
+    unsigned n = 0;                          // consumed tiles (uniform)
+    int it = 0;
+    for (; it < a.n_iters; ++it) {
+        if (a.solve && se.done) break;          // identical in every CTA
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 0] = gtime();
+        double acc[kE64Stats];
+#pragma unroll
+        for (int q = 0; q < kE64Stats; ++q) acc[q] = 0.0;
+        if (producer) {
+            if (lane == 0) produce_until(n + nt + SS);
+            n += nt;
+        } else {
+            Pose64 pose;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) pose.R[q] = se.k.R[q];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) pose.cw[q] = se.k.c_world[q];
+            // contiguous tiles per CTA (Morton order: the CTA's grid rows stay
+            // in L1), one point per consumer thread and tile
+            const double *src = a.tiles + t0 * 3 * THREADS + tid;
+            long long pidx = t0 * THREADS + tid;
+            if (S) {
+                // a warp frees a stage as soon as its 32 lanes read it
+                for (int tt = 0; tt < nt; ++tt, ++n, pidx += THREADS) {
+                    const unsigned st = n % SS;
+                    mbar_wait(&full[st], (n / SS) & 1);
+                    const double *tile = ring + st * 3 * THREADS;
+                    const double h0 = tile[tid], h1 = tile[THREADS + tid], h2 = tile[2 * THREADS + tid];
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[st]);
+                    e64_point(a, pose, cp, h0, h1, h2, pidx < a.m, acc);
+                }
+            } else {
+                double nx = 0.0, ny = 0.0, nz = 0.0;
+                if (nt > 0) {
+                    nx = __ldg(src);
+                    ny = __ldg(src + THREADS);
+                    nz = __ldg(src + 2 * THREADS);
+                }
+                for (int tt = 0; tt < nt; ++tt, pidx += THREADS) {
+                    const double h0 = nx, h1 = ny, h2 = nz;
+                    if (tt + 1 < nt) {
+                        src += 3 * THREADS;
+                        nx = __ldg(src);
+                        ny = __ldg(src + THREADS);
+                        nz = __ldg(src + 2 * THREADS);
+                    }
+                    e64_point(a, pose, cp, h0, h1, h2, pidx < a.m, acc);
+                }
+                n += nt;
+            }
+        }
+        if (!producer) red[warp][lane] = warp_reduce_scatter(acc);
+        __syncthreads();
+        double *rows = a.partials + (long long)(it & 1) * nb * kE64Row;
+        if (tid < kE64Stats) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) s += red[w][tid];
+            rows[(long long)blockIdx.x * kE64Row + tid] = s;
+            __threadfence();             // the row before this CTA's arrival
+        }
+        __syncthreads();
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 1] = gtime();
+        if (tid == 0) {
+            const unsigned target = (unsigned)nb * (unsigned)(it + 1);
+            atomicAdd(a.counter, 1u);
+            while (ld_acquire(a.counter) < target) __nanosleep(20);
+        }
+        __syncthreads();
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 2] = gtime();
+        if (!a.solve && blockIdx.x != 0) continue;
+        // fixed-order column sums: thread (g, c) adds the rows g, g + W, ...
+        // of column c with every load issued up front (one L2 round trip),
+        // then the W group sums in order -- the same order in every CTA
+        {
+            const int c = lane, grp = warp;
+            double s = 0.0;
+            if (!producer && c < kE64Stats) {
+                constexpr int kMaxRows = (kE64MaxSms * MINB + W - 1) / W;
+                double r[kMaxRows];
+#pragma unroll
+                for (int u = 0; u < kMaxRows; ++u) {
+                    const int b = grp + W * u;
+                    r[u] = b < nb ? __ldcg(rows + (long long)b * kE64Row + c) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kMaxRows; ++u) s += r[u];
+            }
+            __syncthreads();             // red[] reuse
+            if (!producer) red[grp][c] = s;
+        }
+        __syncthreads();
+        if (tid < kE64Stats) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < W; ++j) s += red[j][tid];
+            tsum[tid] = s;
+            if (blockIdx.x == 0) a.sums[tid] = s;
+        }
+        __syncthreads();
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 3] = gtime();
+        if (a.solve) {
+            if (tid == 0) {
+                const int n = se.max_em_iters;
+                if (MINB == 1 && THREADS <= 256)   // 255 registers: the solve inlined
+                    rigid_solve_impl(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
+                                     blockIdx.x == 0);
+                else
+                    rigid_solve_body(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
+                                     blockIdx.x == 0);
+            }
+            __syncthreads();
+        }
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 4] = gtime();
+    }
+    // no bulk copy may still target this CTA's shared memory when it exits
+    if (producer && lane == 0)
+        for (; n < issued; ++n) mbar_wait(&full[n % SS], (n / SS) & 1);
+    // the state after the last iteration (status / result / a later launch)
+    if (blockIdx.x == 0 && a.solve) {
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&se);
+        for (int q = tid; q < (int)(sizeof(EmDev) / 8); q += NT)
+            reinterpret_cast<unsigned long long *>(a.em)[q] = src[q];
+    }
+}
+
+// the solve alone (sharded runs: after the all-reduce of the pass sums)
+__global__ void k_em64_solve(const double *sums, EmDev *e, double *traces) {
+    __shared__ EmDev se;
+    __shared__ double ts[kE64Row];
+    if (e->done) return;
+    copy_cg(&se, e, threadIdx.x, blockDim.x);
+    if (threadIdx.x < kE64Stats) ts[threadIdx.x] = sums[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int n = se.max_em_iters;
+        rigid_solve_body(ts, &se, traces, traces + n, traces + 2 * n, true);
+    }
+    __syncthreads();
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&se);
+    for (int q = threadIdx.x; q < (int)(sizeof(EmDev) / 8); q += blockDim.x)
+        reinterpret_cast<unsigned long long *>(e)[q] = src[q];
+}
+
+// launch variants (FR_EM64_VARIANT): threads x CTAs/SM, tile ring stages
+// (0: per-thread register prefetch; > 0: TMA ring with a producer warp)
+using E64Kernel = void (*)(Em64Args);
+struct E64Variant {
+    E64Kernel fn;
+    int threads, minb, stages;
+    int block() const { return threads + (stages ? 32 : 0); }
+    size_t smem() const { return (size_t)stages * 3 * threads * sizeof(double); }
+};
+
+static E64Variant e64_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("FR_EM64_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    switch (v) {
+        case 1: return {k_em64<384, 1, 8>, 384, 1, 8};
+        case 2: return {k_em64<384, 1, 0>, 384, 1, 0};
+        case 3: return {k_em64<256, 2, 4>, 256, 2, 4};
+        default: return {k_em64<512, 1, 0>, 512, 1, 0};
+    }
+}
+
+static int e64_grid(const E64Variant &k) {
+    cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem());
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k.fn, k.block(), k.smem()) !=
+            cudaSuccess || per < 1)
+        per = 1;
+    return std::min(per, k.minb) * std::min(sm_count(), kE64MaxSms);
+}
+
+// centred point tiles: tiles[t][c][j] = ref[c][t T + j] - c_ref[c] (zero past m)
+__global__ void k_em64_tiles(const double *ref, long long m, double c0, double c1, double c2,
+                             int T, long long n_tiles, double *tiles) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_tiles * T) return;
+    const long long t = i / T;
+    const int j = (int)(i % T);
+    const double c[3] = {c0, c1, c2};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) tiles[(t * 3 + q) * T + j] = i < m ? ref[q * m + i] - c[q] : 0.0;
+}
+
+}  // namespace fr
+
+// the float64 device EM object behind fr_em64*
+struct fr_em64 {
+    const fr_lattice *lat = nullptr;
+    long long m = 0;
+    int max_iters = 0;
+    int grid = 0;
+    int threads = 0;
+    int block = 0;
+    size_t smem = 0;
+    long long n_tiles = 0;
+    double *d_tiles = nullptr;       // centred [n_tiles][3][threads] copy of the model points
+    fr::E64Kernel fn = nullptr;
+    fr::EmDev *d_em = nullptr;
+    double *d_sums = nullptr;
+    double *d_partials = nullptr;
+    double *d_traces = nullptr;
+    unsigned *d_sync = nullptr;      // [0] counter, [1] generation
+    cudaStream_t stream = nullptr;
+    unsigned long long *d_prof = nullptr;   // FR_EM64_PROFILE=1: phase timestamps
+    double cp = 0.0;
+};
+
+using namespace fr;
+
+static int e64_launch(fr_em64 *em, int n_iters, int solve, cudaStream_t s) {
+    Em64Args a;
+    a.tiles = em->d_tiles;
+    a.m = em->m;
+    a.tiles_per_cta = (int)((em->n_tiles + em->grid - 1) / em->grid);
+    a.g = em->lat->dense64;
+    a.em = em->d_em;
+    a.partials = em->d_partials;
+    a.sums = em->d_sums;
+    a.traces = em->d_traces;
+    a.counter = em->d_sync;
+    a.gen = em->d_sync + 1;
+    a.n_iters = n_iters;
+    a.solve = solve;
+    a.prof = em->d_prof;
+    for (int j = 0; j < 3; ++j) a.sc[j] = em->lat->c.sf[j] / em->lat->c.sigma[j];
+    a.cp = em->cp;
+    FR_CUDA(cudaMemsetAsync(em->d_sync, 0, 2 * sizeof(unsigned), s));
+    void *args[] = {&a};
+    FR_CUDA(cudaLaunchCooperativeKernel((const void *)em->fn, dim3(em->grid), dim3(em->block),
+                                        args, em->smem, s));
+    return FR_OK;
+}
+
+extern "C" {
+
+int fr_em64_create(const fr_lattice *lat, const double *ref, int64_t m,
+                   const fr_rigid_em_config *cfg, void *stream, fr_em64 **out) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!lat || !lat->blurred || !ref || !cfg || !out || m <= 0) {
+        set_error("invalid float64 EM arguments");
+        return FR_EINVAL;
+    }
+    if (lat->dim != 3 || lat->nv != 4) {
+        set_error("the float64 EM loop runs point_to_point with a fixed kernel (4 value columns)");
+        return FR_EINVAL;
+    }
+    if (!lat->dcells64) {
+        set_error("lattice has no dense float64 slice grid (site box above FR_DENSE64_MAX_CELLS)");
+        return FR_ECAPACITY;
+    }
+    if (cfg->max_em_iters < 1 || cfg->max_gn_iters < 0 || cfg->max_halvings < 0) {
+        set_error("invalid iteration limits");
+        return FR_EINVAL;
+    }
+    fr_em64 *em = new fr_em64();
+    em->stream = s;
+    em->lat = lat;
+    em->m = m;
+    em->max_iters = cfg->max_em_iters;
+    em->cp = cfg->c_prime;
+    const E64Variant kv = e64_variant();
+    em->fn = kv.fn;
+    em->threads = kv.threads;
+    em->block = kv.block();
+    em->smem = kv.smem();
+    em->grid = e64_grid(kv);
+    em->n_tiles = (m + kv.threads - 1) / kv.threads;
+    EmDev h;
+    memset(&h, 0, sizeof(h));
+    embedding_matrix(lat->c, h.A);
+    for (int i = 0; i < 3; ++i) {
+        h.c_ref[i] = cfg->c_ref[i];
+        h.s2[i] = cfg->sigma_inv[i] * cfg->sigma_inv[i];
+        h.t[i] = cfg->t0[i];
+    }
+    for (int q = 0; q < 9; ++q) h.R[q] = cfg->R0[q];
+    h.cp = cfg->c_prime;
+    h.gain = lat->c.gain;
+    h.diameter = cfg->diameter;
+    h.tol = cfg->twist_tolerance;
+    h.use_damping = cfg->damping >= 0.0;
+    h.damping = cfg->damping;
+    h.step_tol = cfg->step_tolerance;
+    h.degenerate_mass = cfg->degenerate_mass;
+    h.max_em_iters = cfg->max_em_iters;
+    h.max_gn_iters = cfg->max_gn_iters;
+    h.max_halvings = cfg->max_halvings;
+    make_rigid_k(h.A, h.R, h.t, h.c_ref, h.cp, h.gain, -1, -1, &h.k);
+    if (cudaMallocAsync((void **)&em->d_em, sizeof(EmDev), s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_sums, kE64Row * sizeof(double), s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_partials, (size_t)2 * em->grid * kE64Row * sizeof(double),
+                        s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double), s) !=
+            cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_sync, 2 * sizeof(unsigned), s) != cudaSuccess ||
+        cudaMemcpyAsync(em->d_em, &h, sizeof(EmDev), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemsetAsync(em->d_sync, 0, 2 * sizeof(unsigned), s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_tiles, (size_t)em->n_tiles * 3 * em->threads * sizeof(double),
+                        s) != cudaSuccess ||
+        cudaMemsetAsync(em->d_sums, 0, kE64Row * sizeof(double), s) != cudaSuccess ||
+        (getenv("FR_EM64_PROFILE") && getenv("FR_EM64_PROFILE")[0] == '1' &&
+         (cudaMallocAsync((void **)&em->d_prof, (size_t)8 * cfg->max_em_iters * 8, s) != cudaSuccess ||
+          cudaMemsetAsync(em->d_prof, 0, (size_t)8 * cfg->max_em_iters * 8, s) != cudaSuccess)) ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        fr_em64_destroy(em);
+        set_error("float64 EM allocation failed");
+        return FR_ECUDA;
+    }
+    {
+        const long long tot = em->n_tiles * em->threads;
+        k_em64_tiles<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(
+            ref, m, cfg->c_ref[0], cfg->c_ref[1], cfg->c_ref[2], em->threads, em->n_tiles,
+            em->d_tiles);
+        if (cudaGetLastError() != cudaSuccess) {
+            fr_em64_destroy(em);
+            set_error("float64 EM tile copy failed");
+            return FR_ECUDA;
+        }
+    }
+    *out = em;
+    return FR_OK;
+}
+
+int fr_em64_destroy(fr_em64 *em) {
+    if (!em) return FR_OK;
+    cudaStreamSynchronize(em->stream);
+    for (void *p : {(void *)em->d_em, (void *)em->d_sums, (void *)em->d_partials,
+                    (void *)em->d_traces, (void *)em->d_sync, (void *)em->d_prof,
+                    (void *)em->d_tiles})
+        if (p) cudaFreeAsync(p, em->stream);
+    delete em;
+    return FR_OK;
+}
+
+int fr_em64_launch_info(const fr_em64 *em, int *grid, int *block) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    if (grid) *grid = em->grid;
+    if (block) *block = em->block;
+    return FR_OK;
+}
+
+int fr_em64_run(fr_em64 *em, int n_iters, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    em->stream = (cudaStream_t)stream;
+    const int n = n_iters > 0 ? n_iters : em->max_iters;
+    return e64_launch(em, n, 1, (cudaStream_t)stream);
+}
+
+int fr_em64_pass(fr_em64 *em, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    em->stream = (cudaStream_t)stream;
+    return e64_launch(em, 1, 0, (cudaStream_t)stream);
+}
+
+int fr_em64_solve(fr_em64 *em, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    em->stream = (cudaStream_t)stream;
+    k_em64_solve<<<1, 32, 0, (cudaStream_t)stream>>>(em->d_sums, em->d_em, em->d_traces);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+// FR_EM64_PROFILE=1 diagnostics: the phase timestamps of the last launch's
+// iterations ([n][8] ns: CTA 0 pass start / end, last CTA tail start / after
+// the reduction / after the solve, CTA 0 release seen); not part of the C ABI
+int fr_em64_profile(fr_em64 *em, unsigned long long *host, int n, void *stream) {
+    if (!em || !em->d_prof) {
+        set_error("profiling is off (FR_EM64_PROFILE=1 at create)");
+        return FR_ESTATE;
+    }
+    n = std::min(n, em->max_iters);
+    FR_CUDA(cudaMemcpyAsync(host, em->d_prof, (size_t)8 * n * 8, cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+    FR_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return FR_OK;
+}
+
+int fr_em64_sums(fr_em64 *em, double **d_sums, int *width) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    if (d_sums) *d_sums = em->d_sums;
+    if (width) *width = kE64Stats;
+    return FR_OK;
+}
+
+int fr_em64_status(fr_em64 *em, int *done, int *iterations, int *termination, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    int h[3];
+    cudaStream_t s = (cudaStream_t)stream;
+    FR_CUDA(cudaMemcpyAsync(h, &em->d_em->done, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    if (done) *done = h[0];
+    if (iterations) *iterations = h[1];
+    if (termination) *termination = h[2];
+    return FR_OK;
+}
+
+int fr_em64_result(fr_em64 *em, double *R, double *t, double *objectives, double *twist_norms,
+                   double *inlier_masses, int *iterations, int *termination, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    EmDev h;
+    FR_CUDA(cudaMemcpyAsync(&h, em->d_em, sizeof(EmDev), cudaMemcpyDeviceToHost, s));
+    std::vector<double> tr((size_t)3 * em->max_iters);
+    FR_CUDA(cudaMemcpyAsync(tr.data(), em->d_traces, tr.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    if (R) memcpy(R, h.R, 9 * sizeof(double));
+    if (t) memcpy(t, h.t, 3 * sizeof(double));
+    const int n = std::min(h.iterations, em->max_iters);
+    if (objectives) memcpy(objectives, tr.data(), n * sizeof(double));
+    if (twist_norms) memcpy(twist_norms, tr.data() + em->max_iters, n * sizeof(double));
+    if (inlier_masses) memcpy(inlier_masses, tr.data() + 2 * em->max_iters, n * sizeof(double));
+    if (iterations) *iterations = h.iterations;
+    if (termination) *termination = h.termination;
+    if (h.termination == kTermSolver && h.done) {
+        set_error("normal equations not factorizable after damping escalation");
+        return FR_ESOLVER;
+    }
+    return FR_OK;
+}
+
+}  // extern "C"

@@ -117,10 +117,11 @@ struct GenericSrc {
     __device__ __forceinline__ double value(long long p, int c) const { return V[p * nv + c]; }
 };
 
-// [1, y, (|y|^2), (n)] from float32 SoA planes (estep.py:153-165)
-struct PointSrc {
-    const float *pos;   // 3 planes of n
-    const float *nrm;   // 3 planes of n or null
+// [1, y, (|y|^2), (n)] from float32 or float64 SoA planes (estep.py:153-165)
+template <class T>
+struct PointSrcT {
+    const T *pos;       // 3 planes of n
+    const T *nrm;       // 3 planes of n or null
     long long n;
     int m2;             // 1 when the |y|^2 column is present
     int nv;
@@ -141,6 +142,8 @@ struct PointSrc {
         return (double)nrm[k * n + p];
     }
 };
+using PointSrc = PointSrcT<float>;
+using PointSrc64 = PointSrcT<double>;
 
 // splat phase 1: embed, insert keys, record (slot, bary) per (point, vertex)
 template <int D, class Src>
@@ -753,7 +756,7 @@ static int reserve_sites(fr_lattice *lat, long long need, cudaStream_t s) {
 
 // a caller-run entries pass: given launch(a, b, stream) for the point range
 // [a, b), it enqueues every range and orders the splat's stream after them
-using EntriesLaunch = std::function<void(long long, long long, cudaStream_t)>;
+using EntriesLaunch = std::function<int(long long, long long, cudaStream_t)>;
 using EntriesHook = std::function<int(const EntriesLaunch &)>;
 
 template <int D, class Src>
@@ -820,10 +823,12 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         if (attempt == 0 && first) {
             // the caller runs the entries pass itself (range by range as the
             // points land) and leaves s ordered after it
-            const auto launch = [&](long long a, long long b, cudaStream_t st) {
+            const auto launch = [&](long long a, long long b, cudaStream_t st) -> int {
                 k_splat_entries<D, Src><<<grid_for(b - a), 256, 0, st>>>(
                     src, a, b, n, lat->c, h, (unsigned)cap, entry_slot, entry_idx, entry_bary,
                     contrib, lat->d_counters);
+                FR_CHECK_LAUNCH();     // on the launching (worker) thread
+                return FR_OK;
             };
             FR_TRY((*first)(launch));
         } else {
@@ -971,11 +976,14 @@ static void free_slice(fr_lattice *lat) {
     pool_free(lat, lat->svals);
     pool_free(lat, lat->fslots);
     pool_free(lat, lat->dcells);
+    pool_free(lat, lat->dcells64);
     lat->skeys = nullptr;
     lat->svals = nullptr;
     lat->fslots = nullptr;
     lat->dcells = nullptr;
+    lat->dcells64 = nullptr;
     lat->dense = fr::DenseSliceF{};
+    lat->dense64 = fr::DenseSliceD{};
     lat->dense_cells = 0;
     lat->nvp = 0;
     lat->nf4 = 0;
@@ -1029,6 +1037,26 @@ __global__ void k_dense_fill(long long S, const int *site_keys, const double *va
                     (float)(gain * v[0]));
 }
 
+// float64 rows: gain * (y0, y1 | y2, 1) sums of the value columns [1, y]
+__global__ void k_dense_fill64(long long S, const int *site_keys, const double *vals, int nv,
+                               double gain, fr::DenseSliceD t, double2 *cells) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    const int *k = site_keys + i * 4;
+    constexpr int P = fr::kDensePad;
+    const long long c = ((long long)((k[0] >> 2) - t.a[0] + P) * t.s0 +
+                         (long long)((k[1] >> 2) - t.a[1] + P) * t.s1 + ((k[2] >> 2) - t.a[2] + P));
+    const double *v = vals + i * nv;
+    double2 *row = cells + 2 * (4 * c + (k[0] & 3));
+    row[0] = make_double2(gain * v[1], gain * v[2]);
+    row[1] = make_double2(gain * v[3], gain * v[0]);
+}
+
+static long long dense64_cell_limit() {
+    const char *e = getenv("FR_DENSE64_MAX_CELLS");
+    return e ? atoll(e) : (8ll << 20);     // 1 GiB
+}
+
 __global__ void k_init_box(int *box) {
     if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
 }
@@ -1065,6 +1093,24 @@ static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
     t.cells = lat->dcells;
     lat->dense = t;
     lat->dense_cells = cells;
+    if (cells <= dense64_cell_limit()) {
+        fr::DenseSliceD d{};
+        for (int c = 0; c < 3; ++c) {
+            d.a[c] = box[c];
+            d.n[c] = (int)n[c];
+        }
+        d.s1 = (int)n[2];
+        d.s0 = (int)(n[1] * n[2]);
+        const size_t bytes = (size_t)cells * 4 * 2 * sizeof(double2);
+        FR_CUDA(pool_alloc(lat, (void **)&lat->dcells64, bytes));
+        FR_CUDA(cudaMemsetAsync(lat->dcells64, 0, bytes, s));
+        k_dense_fill64<<<grid_for(lat->n_sites), 256, 0, s>>>(lat->n_sites, lat->site_keys,
+                                                              lat->vals, lat->nv, lat->c.gain, d,
+                                                              lat->dcells64);
+        FR_CHECK_LAUNCH();
+        d.cells = lat->dcells64;
+        lat->dense64 = d;
+    }
     return FR_OK;
 }
 
@@ -1230,14 +1276,15 @@ __device__ __forceinline__ unsigned spread10(unsigned v) {
     return v;
 }
 
-__global__ void k_morton(const float *pos, long long n, const float *lo, const float *hi,
+template <class T>
+__global__ void k_morton(const T *pos, long long n, const T *lo, const T *hi,
                          unsigned *codes, unsigned *idx) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     unsigned c = 0;
     for (int a = 0; a < 3; ++a) {
-        const float span = fmaxf(hi[a] - lo[a], 1e-30f);
-        const float u = (pos[a * n + i] - lo[a]) / span;
+        const float span = fmaxf((float)(hi[a] - lo[a]), 1e-30f);
+        const float u = (float)(pos[a * n + i] - lo[a]) / span;
         const unsigned q = (unsigned)fminf(fmaxf(u * 1023.0f, 0.0f), 1023.0f);
         c |= spread10(q) << (2 - a);
     }
@@ -1245,8 +1292,9 @@ __global__ void k_morton(const float *pos, long long n, const float *lo, const f
     idx[i] = (unsigned)i;
 }
 
-__global__ void k_gather_planes(const float *src, long long n, int planes, const unsigned *perm,
-                                float *dst) {
+template <class T>
+__global__ void k_gather_planes(const T *src, long long n, int planes, const unsigned *perm,
+                                T *dst) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned j = perm[i];
@@ -1287,7 +1335,10 @@ extern "C" {
 
 int fr_abi_version(void) { return 1; }
 
-int fr_sort_points_morton(float *pos, int64_t n, int planes, int32_t *perm_out, void *stream) {
+}  // extern "C"
+
+template <class T>
+static int sort_morton_impl(T *pos, int64_t n, int planes, int32_t *perm_out, void *stream) {
     if (!pos || n < 0 || planes < 3) {
         set_error("invalid Morton sort arguments");
         return FR_EINVAL;
@@ -1299,7 +1350,7 @@ int fr_sort_points_morton(float *pos, int64_t n, int planes, int32_t *perm_out, 
     }
     cudaStream_t s = (cudaStream_t)stream;
     Scratch sc(s);
-    float *lohi, *tmp;
+    T *lohi, *tmp;
     unsigned *codes, *codes2, *idx, *perm;
     FR_TRY(sc.get(&lohi, 6));
     FR_TRY(sc.get(&codes, n));
@@ -1324,11 +1375,21 @@ int fr_sort_points_morton(float *pos, int64_t n, int planes, int32_t *perm_out, 
     FR_CUDA(cub::DeviceRadixSort::SortPairs(tmpb, tt, codes, codes2, idx, perm, (int)n, 0, 30, s));
     k_gather_planes<<<grid_for(n), 256, 0, s>>>(pos, n, planes, perm, tmp);
     FR_CHECK_LAUNCH();
-    FR_CUDA(cudaMemcpyAsync(pos, tmp, (size_t)n * planes * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    FR_CUDA(cudaMemcpyAsync(pos, tmp, (size_t)n * planes * sizeof(T), cudaMemcpyDeviceToDevice, s));
     if (perm_out)
         FR_CUDA(cudaMemcpyAsync(perm_out, perm, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     FR_CUDA(cudaStreamSynchronize(s));
     return FR_OK;
+}
+
+extern "C" {
+
+int fr_sort_points_morton(float *pos, int64_t n, int planes, int32_t *perm_out, void *stream) {
+    return sort_morton_impl<float>(pos, n, planes, perm_out, stream);
+}
+
+int fr_sort_points_morton64(double *pos, int64_t n, int planes, int32_t *perm_out, void *stream) {
+    return sort_morton_impl<double>(pos, n, planes, perm_out, stream);
 }
 
 const char *fr_last_error(void) { return fr::last_error(); }
@@ -1418,6 +1479,27 @@ int fr_lattice_splat_points(fr_lattice *lat, const float *pos, const float *nrm,
     return splat_impl<3, PointSrc>(lat, src, n, nv, (cudaStream_t)stream);
 }
 
+int fr_lattice_splat_points64(fr_lattice *lat, const double *pos, const double *nrm, int64_t n,
+                              int value_mode, void *stream) {
+    if (!lat || (n > 0 && !pos)) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    if (lat->dim != 3) {
+        set_error("point splat needs a 3-D lattice");
+        return FR_EINVAL;
+    }
+    if ((value_mode & FR_VALUES_NORMALS) && !nrm) {
+        set_error("observation cloud has no normals");
+        return FR_EINVAL;
+    }
+    lat->stream = (cudaStream_t)stream;
+    int m2 = (value_mode & FR_VALUES_M2) ? 1 : 0;
+    int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
+    PointSrc64 src{pos, nrm, n, m2, nv};
+    return splat_impl<3, PointSrc64>(lat, src, n, nv, (cudaStream_t)stream);
+}
+
 int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
                             float *d_soa, void *stream, void (*uploaded)(void *), void *ctx) {
     if (!lat || (n > 0 && (!host_xyz || !d_soa))) {
@@ -1444,10 +1526,10 @@ int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, 
         FR_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         std::mutex mu;
         const int st = upload_points_hooked(host_xyz, n, d_soa, s,
-                                            [&](long long a, long long len, cudaEvent_t landed) {
+                                            [&](long long a, long long len, cudaEvent_t landed) -> int {
             std::lock_guard<std::mutex> g(mu);
-            cudaStreamWaitEvent(side, landed, 0);
-            launch(a, a + len, side);
+            FR_CUDA(cudaStreamWaitEvent(side, landed, 0));
+            return launch(a, a + len, side);
         });
         if (uploaded) uploaded(ctx);     // host staging done: the pinned slots are free
         cudaEvent_t done;
@@ -1501,6 +1583,15 @@ int fr_lattice_dense_cells(const fr_lattice *lat, int64_t *cells) {
         return FR_EINVAL;
     }
     *cells = lat->dense_cells;
+    return FR_OK;
+}
+
+int fr_lattice_dense_cells64(const fr_lattice *lat, int64_t *cells) {
+    if (!lat || !cells) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    *cells = lat->dcells64 ? lat->dense_cells : 0;
     return FR_OK;
 }
 

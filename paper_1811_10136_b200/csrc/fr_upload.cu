@@ -32,7 +32,7 @@ struct StagePool {
     std::mutex mu;
     int workers = 0;
     float *base = nullptr;                 // one pinned block, carved into slots
-    float *slots[kMaxWorkers][2] = {};
+    float *slots[kMaxWorkers][2] = {};     // kSubChunk float32 rows, or kSubChunk / 2 float64
     cudaEvent_t done[kMaxWorkers][2] = {};
 
     // all kMaxWorkers x 2 slots (48 MB pinned) on first use, so the one-time
@@ -90,36 +90,56 @@ static void convert_rows(const double *r, long long len, float *x, float *y, flo
     if (avx2) convert_rows_avx2(r, len, x, y, z);
     else convert_rows_scalar(r, len, x, y, z);
 }
+// float64 planes: a transpose, no rounding (the float64 query path keeps the
+// caller's values bit for bit)
+static void convert_rows(const double *r, long long len, double *x, double *y, double *z) {
+    for (long long i = 0; i < len; ++i) {
+        x[i] = r[3 * i];
+        y[i] = r[3 * i + 1];
+        z[i] = r[3 * i + 2];
+    }
+}
 
 struct WorkerResult {
     int status = FR_OK;
     char msg[256] = {0};
 };
 
-void worker(int id, const double *src, long long n, long long a, long long b, float *dst,
+// worker threads run on the caller's device: CUDA's current device is per
+// host thread, and a fresh std::thread starts on device 0 (a launch or copy
+// from it would target another GPU's context for any caller on device k > 0)
+template <class T>
+void worker(int dev, int id, const double *src, long long n, long long a, long long b, T *dst,
             cudaStream_t s, WorkerResult *res, const ChunkHook *hook) {
     StagePool &p = pool();
+    constexpr long long kSub = kSubChunk * (long long)sizeof(float) / (long long)sizeof(T);
     int slot = 0;
-    for (long long c = a; c < b; c += kSubChunk) {
-        const long long len = std::min(kSubChunk, b - c);
-        float *buf = p.slots[id][slot];
-        cudaError_t e = cudaEventSynchronize(p.done[id][slot]);   // slot's previous DMA
+    cudaError_t e = cudaSetDevice(dev);
+    for (long long c = a; c < b && e == cudaSuccess; c += kSub) {
+        const long long len = std::min(kSub, b - c);
+        T *buf = reinterpret_cast<T *>(p.slots[id][slot]);
+        e = cudaEventSynchronize(p.done[id][slot]);   // slot's previous DMA
         if (e == cudaSuccess) {
             const double *r = src + 3 * c;
-            float *x = buf, *y = buf + kSubChunk, *z = buf + 2 * kSubChunk;
+            T *x = buf, *y = buf + kSub, *z = buf + 2 * kSub;
             convert_rows(r, len, x, y, z);
-            e = cudaMemcpy2DAsync(dst + c, (size_t)n * sizeof(float), buf,
-                                  (size_t)kSubChunk * sizeof(float), (size_t)len * sizeof(float),
-                                  3, cudaMemcpyHostToDevice, s);
+            e = cudaMemcpy2DAsync(dst + c, (size_t)n * sizeof(T), buf, (size_t)kSub * sizeof(T),
+                                  (size_t)len * sizeof(T), 3, cudaMemcpyHostToDevice, s);
         }
         if (e == cudaSuccess) e = cudaEventRecord(p.done[id][slot], s);
-        if (e == cudaSuccess && hook && *hook) (*hook)(c, len, p.done[id][slot]);
-        if (e != cudaSuccess) {
-            res->status = FR_ECUDA;
-            snprintf(res->msg, sizeof(res->msg), "point upload: %s", cudaGetErrorString(e));
-            return;
+        if (e == cudaSuccess && hook && *hook) {
+            const int st = (*hook)(c, len, p.done[id][slot]);
+            if (st != FR_OK) {
+                res->status = st;
+                snprintf(res->msg, sizeof(res->msg), "point upload hook: %s", last_error());
+                return;
+            }
         }
         slot ^= 1;
+    }
+    if (e != cudaSuccess) {
+        res->status = FR_ECUDA;
+        snprintf(res->msg, sizeof(res->msg), "point upload: %s", cudaGetErrorString(e));
     }
 }
 
@@ -131,9 +151,11 @@ using namespace fr;
 namespace fr {
 
 // the staged upload; `hook` (may be empty) is called from the worker threads
-// after each sub-chunk's copy was enqueued, with the event that marks it landed
-int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cudaStream_t s,
-                         const ChunkHook &hook) {
+// (current device = the caller's) after each sub-chunk's copy was enqueued,
+// with the event that marks it landed; a hook's failure status is returned
+template <class T>
+static int upload_impl(const double *host_xyz, long long n, T *d_soa, cudaStream_t s,
+                       const ChunkHook &hook) {
     if (n < 0 || (n > 0 && (!host_xyz || !d_soa))) {
         set_error("fr_upload_points: invalid arguments");
         return FR_EINVAL;
@@ -144,6 +166,8 @@ int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cuda
     if (const char *e = getenv("FR_UPLOAD_WORKERS")) cap = std::max(1, std::min(kMaxWorkers, atoi(e)));
     const int w = (int)std::max<long long>(
         1, std::min<long long>({cap, (long long)hw, (n + kSubChunk - 1) / kSubChunk}));
+    int dev = 0;
+    FR_CUDA(cudaGetDevice(&dev));
     StagePool &p = pool();
     std::lock_guard<std::mutex> lock(p.mu);   // one upload at a time owns the slots
     FR_TRY(p.init());
@@ -154,7 +178,7 @@ int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cuda
     for (int i = 0; i < w; ++i) {
         const long long a = std::min<long long>(n, (long long)i * per);
         const long long b = std::min<long long>(n, a + per);
-        th.emplace_back(worker, i, host_xyz, (long long)n, a, b, d_soa, s, &res[i], &hook);
+        th.emplace_back(worker<T>, dev, i, host_xyz, (long long)n, a, b, d_soa, s, &res[i], &hook);
     }
     for (auto &t : th) t.join();
     for (const auto &r : res)
@@ -165,8 +189,17 @@ int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cuda
     return FR_OK;
 }
 
+int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cudaStream_t s,
+                         const ChunkHook &hook) {
+    return upload_impl<float>(host_xyz, n, d_soa, s, hook);
+}
+
 }  // namespace fr
 
 extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa, void *stream) {
     return fr::upload_points_hooked(host_xyz, n, d_soa, (cudaStream_t)stream, fr::ChunkHook());
+}
+
+extern "C" int fr_upload_points64(const double *host_xyz, int64_t n, double *d_soa, void *stream) {
+    return fr::upload_impl<double>(host_xyz, n, d_soa, (cudaStream_t)stream, fr::ChunkHook());
 }

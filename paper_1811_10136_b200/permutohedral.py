@@ -180,12 +180,14 @@ class PermutohedralLattice:
         self._export = None
 
     def splat_points(self, positions_soa, normals_soa=None, value_mode: int = 0) -> None:
-        """Splat [1, y, (|y|^2), (n)] generated on device from float32 SoA planes
-        (the MomentEngine value columns, estep.py:153-165)."""
+        """Splat [1, y, (|y|^2), (n)] generated on device from float32 or
+        float64 SoA planes (the MomentEngine value columns, estep.py:153-165)."""
+        import torch
         n = positions_soa.shape[1]
-        _lib.check(self._lib.fr_lattice_splat_points(
-            self._h, _lib.ptr(positions_soa), _lib.ptr(normals_soa), n, value_mode,
-            _lib.stream_handle()))
+        fn = self._lib.fr_lattice_splat_points64 if positions_soa.dtype == torch.float64 \
+            else self._lib.fr_lattice_splat_points
+        _lib.check(fn(self._h, _lib.ptr(positions_soa), _lib.ptr(normals_soa), n, value_mode,
+                      _lib.stream_handle()))
         self.blurred = False
         self._splatted = True
         self._export = None
@@ -258,6 +260,14 @@ class PermutohedralLattice:
         c = ctypes.c_int64()
         _lib.check(self._lib.fr_lattice_dense_cells(self._h, ctypes.byref(c)))
         return int(c.value)
+
+    @property
+    def dense64(self) -> bool:
+        """True when the lattice carries the dense float64 slice grid of the
+        float64 EM loop (site box within FR_DENSE64_MAX_CELLS)."""
+        c = ctypes.c_int64()
+        _lib.check(self._lib.fr_lattice_dense_cells64(self._h, ctypes.byref(c)))
+        return c.value > 0
 
     @property
     def num_sites(self) -> int:

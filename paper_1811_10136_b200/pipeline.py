@@ -201,11 +201,9 @@ def _register_device_loop(path, model, config, timing):
     iterations; the host only waits for the termination flag.  `timing`
     receives the loop's wall time as `e_step_s` (E step and M step are fused
     on the device) and 0 for `m_step_s`."""
-    import torch
-    from ._rigid import DeviceEM
-    from .errors import SolverError
+    from ._rigid import device_em
     tick = time.perf_counter()
-    em = DeviceEM(path, model.pose.rotation, model.pose.translation, config)
+    em = device_em(path, model.pose.rotation, model.pose.translation, config)
     em.run()
     return _device_loop_result(em, model, timing, tick)
 
@@ -320,10 +318,17 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
         path = ArticulatedDevicePath(reference, observation, config.gmm, config.residual_mode,
                                      initial_model, process_group)
     else:
-        factory = _path_factory if _path_factory is not None else RigidDevicePath
-        path = factory(reference, observation, config.gmm, config.residual_mode, process_group)
-        if (_path_factory is None and config.residual_mode == "point_to_point"
-                and not config.gmm.update_sigma and not config.record_states):
+        loop = (_path_factory is None and config.residual_mode == "point_to_point"
+                and not config.gmm.update_sigma and not config.record_states)
+        if _path_factory is not None:
+            path = _path_factory(reference, observation, config.gmm, config.residual_mode,
+                                 process_group)
+        else:
+            from . import _rigid
+            path = RigidDevicePath(reference, observation, config.gmm, config.residual_mode,
+                                   process_group,
+                                   precision=_rigid.PRECISION if loop else "f32")
+        if loop:
             return _register_device_loop(path, initial_model, config, timing)
     model = initial_model
     diameter = path.diameter

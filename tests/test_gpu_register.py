@@ -141,16 +141,18 @@ def test_explicit_assembly_matches_oracle(fr):
 
 # device-vs-host loop agreement: float64 round-off, or float32 round-off on
 # the float32 point path
-LOOP_TOL = {"f32": 1e-6, "f32_hash": 1e-6, "fast": 1e-9, "exact": 1e-9}
+LOOP_TOL = {"f32": 1e-6, "f32_hash": 1e-6, "fast": 1e-9, "exact": 1e-9, "f64": 1e-9}
 
 
-@pytest.mark.parametrize("path", ["f32", "f32_hash", "fast", "exact"])
+@pytest.mark.parametrize("path", ["f64", "f32", "f32_hash", "fast", "exact"])
 def test_device_loop_matches_host_loop(fr, path, monkeypatch):
     """The device-resident EM (float64 solver kernel) reproduces the host-side
     loop's decisions: same iterations/termination, poses to round-off -- for
     every query path of the pass (f32 over the dense slice grid and over the
-    hash slots)."""
+    hash slots; f64: the grid-resident float64 loop vs the host loop over the
+    all-float64 hash pass)."""
     import paper_1811_10136_b200._rigid as rg
+    monkeypatch.setattr(rg, "PRECISION", "f64" if path == "f64" else "f32")
     if path == "f32_hash":
         monkeypatch.setenv("FR_DENSE_MAX_CELLS", "0")
     g = load("register_pt2pt_seed1")
@@ -158,7 +160,7 @@ def test_device_loop_matches_host_loop(fr, path, monkeypatch):
     config = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]),
                                    max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"])
     old = rg.FAST_QUERY, rg.F32_POINTS
-    rg.FAST_QUERY, rg.F32_POINTS = path != "exact", path.startswith("f32")
+    rg.FAST_QUERY, rg.F32_POINTS = path not in ("exact", "f64"), path.startswith("f32")
     try:
         ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
         dev = fr.register(ref, obs, fr.RigidModel(), config)            # device loop
@@ -181,12 +183,13 @@ def test_device_loop_matches_host_loop(fr, path, monkeypatch):
                        g["R"], g["t"], O.bbox_diameter(g["X"]))
 
 
-@pytest.mark.parametrize("path", ["f32", "exact"])
+@pytest.mark.parametrize("path", ["f64", "f32", "exact"])
 def test_device_loop_mstep_options(fr, path, monkeypatch):
     """Extra GN iterations, explicit damping and the halving cap run through the
     device solver with the same results as the host loop."""
     import paper_1811_10136_b200._rigid as rg
-    monkeypatch.setattr(rg, "FAST_QUERY", path != "exact")
+    monkeypatch.setattr(rg, "PRECISION", "f64" if path == "f64" else "f32")
+    monkeypatch.setattr(rg, "FAST_QUERY", path not in ("exact", "f64"))
     monkeypatch.setattr(rg, "F32_POINTS", path == "f32")
     g = load("register_pt2pt_seed2")
     cfg = json.loads(str(g["config"]))
