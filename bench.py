@@ -1,23 +1,31 @@
-"""FilterReg B200 benchmark: rigid point-to-point EM on the C5 workload.
+"""FilterReg B200 benchmark: rigid point-to-point EM, BASELINE metric
+"EM iters/sec & points/sec (100k/1M-pt rigid)".
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--points P] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--points P]
+                    [--precision f64|f32] [--impl b200|reference] [--mode fixed|sigma|batch]
 
-Workload (BASELINE.json configs[4], "large-scale rigid sweep 1M-16M observation
-points"): the reference's pebble pair (synth.py:252-284, restated in
-oracle/filterreg_oracle.py) with P = 16,000,000 clean points + 5% uniform
-outliers (16.8M) per GPU, 50 deg / 2% shift ground truth, sigma = 5% of the
-clean bbox diagonal, w = 0.1.  Weak scaling: every rank holds its own 16.8M-
-point model shard (see make_shard) and the whole observation lattice (built
-once, outside the timed region, reported as build_ms); the 25 per-iteration
-normal-equation partials are NCCL all-reduced.
+Workload (BASELINE.json configs[4] at its 1M point; configs' 100k point as a
+secondary line): the reference's pebble pair (synth.py:252-284, restated in
+oracle/filterreg_oracle.py), P = 1,000,000 clean points + 5 % uniform
+outliers (1.05M) for the model and the observation cloud, 50 deg / 2 % shift
+ground truth, sigma = 5 % of the clean bbox diagonal, w = 0.1.  Inputs are
+float64 (float32-rounded values, as every parity fixture).
 
-A step is ONE EM iteration over the whole job: fused E + assembly pass,
-fixed-order reduction, [all-reduce,] float64 solve / halving / termination --
-all on the device, replayed from a CUDA graph (DeviceEM).  The tolerance is
-1e-30 so every step does the full work.  The model planes (16.8M x 12 B =
-202 MB) are larger than L2, so no flush is needed between steps.
+A step is ONE registration of EM_PER_STEP = 50 EM iterations (the reference's
+default max_em_iters; tolerance 1e-30 so every iteration runs) on the
+resident lattice: the float64 grid-resident EM loop (fr_em64: pass,
+fixed-order reduction and float64 solve of every iteration in one cooperative
+launch).  The lattice build is once per run and reported as build_ms.  At 1M
+the 25 MB of model points fit in L2, so L2 is flushed (a 256 MB write) before
+every timed step, outside its CUDA-event bracket; within a step the
+iterations re-read the points as a real registration does.
 
-value = model points x timed EM iterations / device time (max over ranks).
+value = model points x EM iterations / device time (sum of the per-step event
+times, max over ranks).  e2e = the same metric through the public register()
+from host float64 arrays (H2D, Morton sort, lattice build, EM loop, D2H).
+Weak scaling for N > 1: every rank holds its own model shard (1.05M points)
+and the whole observation lattice; the 25 partial sums are NCCL all-reduced
+per iteration.
 """
 
 from __future__ import annotations
@@ -37,19 +45,23 @@ sys.path.insert(0, ROOT)
 
 METRIC = "points/sec (model points x EM iterations / s, rigid point-to-point FilterReg)"
 L2_BYTES = 126 * 1024 * 1024
+EM_PER_STEP = 50
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--points", type=int, default=16_000_000, help="clean model points per GPU")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--points", type=int, default=1_000_000, help="clean model points per GPU")
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                    help="query-side arithmetic of the headline line (the other is reported "
+                         "beside it)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=1_048_576,
-                    help="model points per CPU-baseline EM iteration")
-    ap.add_argument("--cpu-obs", type=int, default=1_048_576,
-                    help="observation points of the CPU-baseline lattice")
+    ap.add_argument("--cpu-iters", type=int, default=6,
+                    help="EM iterations of the in-run CPU baseline (same clouds, all cores)")
+    ap.add_argument("--ref-iters", type=int, default=4,
+                    help="EM iterations per step of --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="fixed", choices=["fixed", "sigma", "batch"],
@@ -148,32 +160,10 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(points: int):
-    """dram bytes per launch of the pass kernel from the committed ncu capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
-            doc = json.load(fh)
-        rec = doc.get("rigid_pass", {})
-        if int(rec.get("points", -1)) == points:
-            return float(rec["dram_bytes"])
-    except Exception:
-        pass
-    return None
-
-
-def cpu_sample(X, Y, sample: int, obs_sample: int):
-    """Bounded CPU sample of the workload: random subsets of the model and
-    observation clouds (the oracle port needs ~4 s per 1M-point lattice build
-    and ~1 s per 256k-point EM iteration)."""
-    rng = np.random.default_rng(0)
-    Xs = X[np.sort(rng.choice(len(X), min(sample, len(X)), replace=False))]
-    Ys = Y[np.sort(rng.choice(len(Y), min(obs_sample, len(Y)), replace=False))]
-    return Xs, Ys
-
-
-def _cpu_worker(conn, shard, eng, sinv):
+def _cpu_worker(conn, shard, eng, sinv, n_model):
     """One host core of the CPU arm: E step, assembly and candidate objectives
-    of the oracle's rigid EM iteration over this worker's model shard."""
+    of the oracle's rigid EM iteration over this worker's model shard (the
+    outlier constant over the whole model count, estep.py:197-198)."""
     from threadpoolctl import threadpool_limits
 
     from oracle import filterreg_oracle as O
@@ -186,7 +176,7 @@ def _cpu_worker(conn, shard, eng, sinv):
             R, t = msg[1], msg[2]
             x = shard @ R.T + t
             if msg[0] == "estep":
-                mom = eng.moments(x)
+                mom = eng.moments(x, n_model=n_model)
                 spec = (mom["weight"], mom["target"], sinv, "point_to_point", None, None)
                 H, g = O.assemble_rigid(spec, x)
                 conn.send((O.rigid_objective(spec, x), H, g))
@@ -197,28 +187,30 @@ def _cpu_worker(conn, shard, eng, sinv):
 class CpuArm:
     """The reference algorithm's CPU path (the oracle port of pipeline.py /
     mstep.py / estep.py, bit-identical to the reference on its fixtures) on all
-    host cores: the model sample is split into one contiguous shard per core
-    (forked worker processes sharing the lattice copy-on-write); per EM
-    iteration the shards' objective / H / g are summed, the 6x6 solve and the
-    step halving run as in oracle.rigid_m_step (mstep.py:421-459), candidate
-    objectives are again summed over shards."""
+    host cores, over the SAME clouds as the GPU arm (no subsampling): the
+    lattice is built once on the whole observation cloud (not timed), the
+    model cloud is split into one contiguous shard per core (forked worker
+    processes sharing the lattice copy-on-write); per EM iteration the shards'
+    objective / H / g are summed, the 6x6 solve and the step halving run as in
+    oracle.rigid_m_step (mstep.py:421-459), candidate objectives are again
+    summed over shards."""
 
-    def __init__(self, Xs, Ys, sigma, workers=None):
+    def __init__(self, X, Y, sigma, workers=None):
         import multiprocessing as mp
 
         from oracle import filterreg_oracle as O
         self.O = O
         tick = time.perf_counter()
-        eng = O.OracleMoments(Ys, sigma, 0.1)
+        eng = O.OracleMoments(Y, sigma, 0.1)
         self.build_s = time.perf_counter() - tick
         self.workers = workers or max(1, len(os.sched_getaffinity(0)))
         ctx = mp.get_context("fork")
         sinv = np.full(3, 1.0 / sigma)
         self.conns, self.procs = [], []
-        for shard in np.array_split(Xs, self.workers):
+        for shard in np.array_split(X, self.workers):
             a, b = ctx.Pipe()
-            p = ctx.Process(target=_cpu_worker, args=(b, np.ascontiguousarray(shard), eng, sinv),
-                            daemon=True)
+            p = ctx.Process(target=_cpu_worker,
+                            args=(b, np.ascontiguousarray(shard), eng, sinv, len(X)), daemon=True)
             p.start()
             self.conns.append(a)
             self.procs.append(p)
@@ -254,57 +246,95 @@ class CpuArm:
             p.join(timeout=10)
 
 
-def cpu_baseline(X, Y, sigma, sample: int, obs_sample: int, iters: int):
-    """The CPU arm on a bounded sample: lattice built on an observation subset
-    (not timed), then `iters` EM iterations over a model subset on all cores."""
-    Xs, Ys = cpu_sample(X, Y, sample, obs_sample)
-    arm = CpuArm(Xs, Ys, sigma)
+def cpu_baseline(X, Y, sigma, iters: int):
+    """The CPU arm on the full clouds: `iters` EM iterations timed after one
+    warm-up iteration (lattice build not timed)."""
+    arm = CpuArm(X, Y, sigma)
     arm.iteration()                     # warm-up (worker start, first-touch)
     tick = time.perf_counter()
     for _ in range(iters):
         arm.iteration()
     dt = time.perf_counter() - tick
     arm.close()
-    return len(Xs) * iters / dt, dt, len(Xs), len(Ys), arm.workers
+    return len(X) * iters / dt, dt, arm.workers, arm.build_s
+
+
+def workload_name(points: int) -> str:
+    return (f"C5 rigid pt2pt pebble {points} clean pts + 5% outliers (model and observation), "
+            f"{EM_PER_STEP}-iteration registrations (BASELINE configs[4] at 1M; metric "
+            "'100k/1M-pt rigid')")
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU path (oracle port; the
-    Python reference itself cannot travel to the GPU box) on this box's cores."""
+    """--impl reference: the reference algorithm's CPU path (the oracle port;
+    the Python reference itself cannot travel to the GPU box) on this box's
+    cores, on the same clouds as the GPU arm.  Each step is a bounded sample of
+    the workload: `--ref-iters` EM iterations of the full-size registration."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     X, Y, sigma = make_shard(args.points, 0)
-    Xs, Ys = cpu_sample(X, Y, args.cpu_sample, args.cpu_obs)
-    arm = CpuArm(Xs, Ys, sigma)
+    arm = CpuArm(X, Y, sigma)
     times = []
     for i in range(args.warmup + args.steps):
         tick = time.perf_counter()
-        arm.iteration()
+        for _ in range(args.ref_iters):
+            arm.iteration()
         if i >= args.warmup:
             times.append(time.perf_counter() - tick)
     arm.close()
     total = sum(times)
-    value = len(Xs) * args.steps / total
+    value = len(X) * args.ref_iters * args.steps / total
     cores = arm.workers
-    sample = (f"{len(Xs)}-point random subset of the {len(X)}-point model cloud per EM "
-              f"iteration, split over {cores} worker processes; lattice on a {len(Ys)}-point "
-              f"random subset of the {len(Y)}-point observation cloud (build "
-              f"{arm.build_s:.1f} s, not timed)")
+    sample = (f"{args.ref_iters} EM iterations per step over the full {len(X)}-point model "
+              f"cloud against the lattice of the full {len(Y)}-point observation cloud, "
+              f"{cores} worker processes (lattice build {arm.build_s:.1f} s, not timed)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C5 rigid pt2pt pebble, {args.points} clean pts/GPU + 5% "
-                               "outliers (CPU arm: bounded sample)",
-                   "points_per_gpu": len(X) // world, "sigma_frac": 0.05,
-                   "outlier_ratio": 0.1, "parallelism": "cpu"},
+        "config": {"workload": workload_name(args.points), "points_per_gpu": len(X),
+                   "obs_points": len(Y), "sigma_frac": 0.05, "outlier_ratio": 0.1,
+                   "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+class L2Flush:
+    """A 256 MB device buffer written between timed steps (twice L2)."""
+
+    def __init__(self, dev):
+        import torch
+        self.buf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+
+    def __call__(self):
+        self.buf.fill_(1.0)
+
+
+def time_em_steps(em_factory, steps, warmup, flush, stream):
+    """Per-step CUDA-event times of `steps` registrations (after `warmup`),
+    each a fresh EM state at the identity run for EM_PER_STEP iterations in
+    one launch, L2 flushed before each (outside the event bracket)."""
+    import torch
+    times = []
+    for i in range(warmup + steps):
+        em = em_factory()
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        em.enqueue(EM_PER_STEP)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        done, iters, term = em.status()
+        assert iters == EM_PER_STEP, (iters, term)
+        if i >= warmup:
+            times.append(e0.elapsed_time(e1))
+        del em
+    return times
 
 
 def run_b200(args):
@@ -322,158 +352,207 @@ def run_b200(args):
     dev = torch.device("cuda", torch.cuda.current_device())
 
     import paper_1811_10136_b200 as fr
-    from paper_1811_10136_b200 import _lib
-    from paper_1811_10136_b200._rigid import DeviceEM, RigidDevicePath
+    from paper_1811_10136_b200 import _lib, _rigid
+    from paper_1811_10136_b200._rigid import RigidDevicePath
 
     X, Y, sigma = make_shard(args.points, rank)
     M_local, N_obs = len(X), len(Y)
     gmm = fr.GmmConfig(sigma=sigma, outlier_ratio=0.1)
-
-    # lattice build (splat + blur of the whole observation cloud), once per
-    # run; a warm-up build first so module loading is not timed
-    # first full-size setup grows the device memory pool once (untimed); the
-    # reported build is the steady-state one of a warm process
-    ref_pc, obs_pc = fr.PointCloud(X), fr.PointCloud(Y)      # host-side validation, untimed
-    first = RigidDevicePath(ref_pc, obs_pc, gmm, "point_to_point", group)
-    del first
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    path = RigidDevicePath(ref_pc, obs_pc, gmm, "point_to_point", group)
-    torch.cuda.synchronize()
-    build_ms = 1e3 * (time.perf_counter() - t0)
-    M_total = path.M_total
-    sites = path.lattice.num_sites
+    cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=EM_PER_STEP, twist_tolerance=1e-30)
     stream = torch.cuda.current_stream()
-    l2_note = "inputs larger than L2" if 12 * M_local > L2_BYTES else "inputs smaller than L2"
+    flush = L2Flush(dev)
+    l2_note = ("inputs smaller than L2: L2 flushed (256 MB write) before every timed step"
+               if 24 * M_local < L2_BYTES else "inputs larger than L2 (and L2 flushed)")
+    ref_pc, obs_pc = fr.PointCloud(X), fr.PointCloud(Y)          # host-side validation, untimed
 
-    # dominant kernel alone: the fused pass (+ its column reduction), R launches
-    cfg_k = fr.RegistrationConfig(gmm=gmm, max_em_iters=10 ** 6, twist_tolerance=1e-30)
-    em_k = DeviceEM(path, np.eye(3), np.zeros(3), cfg_k)
-    for _ in range(3):
-        _lib.check(path.lib.fr_rigid_em_pass(em_k.h, _lib.stream_handle()))
-    reps = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        _lib.check(path.lib.fr_rigid_em_pass(em_k.h, _lib.stream_handle()))
-    e1.record(stream)
-    torch.cuda.synchronize()
-    pass_ms = e0.elapsed_time(e1) / reps      # constant-bank copy + pass kernel
-    # the pass kernel alone (same pose: the constants copied above stay valid)
-    kernel_ms = pass_ms
-    if int(path.lib.fr_rigid_em_kernels_per_iter(em_k.h)) <= 2:
-        e0.record(stream)
-        for _ in range(reps):
-            _lib.check(path.lib.fr_rigid_em_pass_kernel(em_k.h, _lib.stream_handle()))
-        e1.record(stream)
+    def measure(precision, points_tag):
+        """Setup once (warm-up setup first), then the timed registrations."""
+        first = RigidDevicePath(ref_pc, obs_pc, gmm, "point_to_point", group, precision=precision)
+        del first
         torch.cuda.synchronize()
-        kernel_ms = e0.elapsed_time(e1) / reps
-    del em_k
-
-    # the timed EM: W warm-up iterations, then K timed iterations, all on the
-    # device (pass, reduction, [NCCL all-reduce], solver per iteration)
-    cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=args.warmup + args.steps,
-                                twist_tolerance=1e-30)
-    em = DeviceEM(path, np.eye(3), np.zeros(3), cfg)
-    kernels_per_iter = int(path.lib.fr_rigid_em_kernels_per_iter(em.h))
-    em.enqueue(args.warmup)
-    torch.cuda.synchronize()
-    if group is not None:
-        dist.barrier()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    with ClockSampler(local) as clk:
-        ev[0].record(stream)
-        em.enqueue(args.steps)
-        ev[1].record(stream)
+        t0 = time.perf_counter()
+        path = RigidDevicePath(ref_pc, obs_pc, gmm, "point_to_point", group, precision=precision)
         torch.cuda.synchronize()
-    total_ms = ev[0].elapsed_time(ev[1])
-    done, iters, term = em.status()
-    assert iters == args.warmup + args.steps, (iters, term)
-    tot = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if group is not None:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    total_ms = float(tot.item())
-    value = M_total * args.steps / (total_ms / 1e3)
+        build_ms = 1e3 * (time.perf_counter() - t0)
 
-    # roofline of the dominant kernel: the fused pass reads 12 B per model point
-    # (float32 x, y, z); the lattice table (< L2) is not counted
-    alg_bytes = 12 * M_local
-    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
-    peak, peak_kind = measured_peak()
-    traffic = ncu_traffic(args.points)
-
-    # end to end through the public API: register() from host arrays, H2D of
-    # both clouds, lattice build, K EM iterations, D2H of the result
-    e2e = None
-    dense_cells = path.lattice.dense_cells
-    del em, path    # the e2e registration sets up its own state (warm process, pools reused)
-    torch.cuda.synchronize()
-    if not args.no_e2e:
-        ecfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=args.steps, twist_tolerance=1e-30)
-        ref_host, obs_host = fr.PointCloud(X), fr.PointCloud(Y)
-        torch.cuda.synchronize()
+        def factory():
+            return _rigid.device_em(path, np.eye(3), np.zeros(3), cfg)
         if group is not None:
             dist.barrier()
-        t0 = time.perf_counter()
-        res = fr.register(ref_host, obs_host, fr.RigidModel(), ecfg, process_group=group)
-        _ = res.kinematics.pose.matrix()
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        with ClockSampler(local) as clk:
+            times = time_em_steps(factory, args.steps, args.warmup, flush, stream)
+        tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+        if group is not None:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        total_ms = float(tot.item())
+        out = {"path": path, "build_ms": build_ms, "total_ms": total_ms, "clocks": clk.summary(),
+               "value": path.M_total * EM_PER_STEP * args.steps / (total_ms / 1e3),
+               "ms_per_step": total_ms / args.steps}
+        em = factory()
+        out["em_kind"] = type(em).__name__
+        if isinstance(em, _rigid.DeviceEM64):
+            grid, block = em.launch_info()
+            out["launch"] = {"grid": grid, "block": block, "kernels_per_step": 1}
+            # the pass alone (one cooperative launch: pass + fixed-order
+            # reduction, no solve), cold (L2 flushed) and warm
+            cold = []
+            for _ in range(10):
+                flush()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                em.pass_only()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                cold.append(e0.elapsed_time(e1))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            em.pass_only()
+            e0.record(stream)
+            for _ in range(20):
+                em.pass_only()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            out["pass_cold_ms"] = float(np.median(cold))
+            out["pass_warm_ms"] = e0.elapsed_time(e1) / 20
+        else:
+            out["launch"] = {"kernels_per_step": EM_PER_STEP *
+                             int(path.lib.fr_rigid_em_kernels_per_iter(em.h))}
+        del em
+        return out
+
+    head = measure(args.precision, "head")
+    other_precision = "f32" if args.precision == "f64" else "f64"
+    other = measure(other_precision, "other")
+
+    # the metric's 100k point (same protocol), rank 0 / N = 1 only
+    p100k = None
+    if world == 1 and args.points != 100_000:
+        X1, Y1, s1 = make_shard(100_000, 0)
+        g1 = fr.GmmConfig(sigma=s1, outlier_ratio=0.1)
+        c1 = fr.RegistrationConfig(gmm=g1, max_em_iters=EM_PER_STEP, twist_tolerance=1e-30)
+        path1 = RigidDevicePath(fr.PointCloud(X1), fr.PointCloud(Y1), g1, "point_to_point",
+                                precision=args.precision)
+
+        def f1():
+            return _rigid.device_em(path1, np.eye(3), np.zeros(3), c1)
+        t1 = time_em_steps(f1, args.steps, args.warmup, flush, stream)
+        p100k = {"points": len(X1), "value": len(X1) * EM_PER_STEP * args.steps / (sum(t1) / 1e3),
+                 "unit": "points/s", "ms_per_step": sum(t1) / args.steps,
+                 "em_iters_per_sec": EM_PER_STEP * args.steps / (sum(t1) / 1e3),
+                 "dtype": args.precision}
+        del path1
+
+    # roofline of the dominant kernel (k_em64, the whole loop): one pass reads
+    # the 24-byte float64 position of every model point (the reference's
+    # float64 arrays); the dense slice grid (~3 MB) is L1/L2-resident and not
+    # counted.  Timed alone (fr_em64_pass: launch + pass + reduction) with L2
+    # flushed, so the points come from HBM.
+    peak, peak_kind = measured_peak()
+    hp = head
+    alg_bytes = (24 if args.precision == "f64" else 12) * M_local
+    kernel_ms = hp.get("pass_cold_ms")
+    roofline = None
+    if kernel_ms:
+        achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "k_em64 (float64 grid-resident EM loop; one launch = one pass + "
+                              "fixed-order reduction, timed alone, L2 flushed)",
+                    "alg_bytes_per_launch": alg_bytes, "kernel_ms": kernel_ms,
+                    "kernel_warm_ms": hp.get("pass_warm_ms"),
+                    "em_iteration_ms": hp["ms_per_step"] / EM_PER_STEP,
+                    "peak_source": peak_kind,
+                    "note": "traffic: see profiles/ (ncu dram bytes of the same launch); the "
+                            "float64 pass is bound by the FP64 pipe and issue, not HBM"}
+
+    # end to end through the public API: register() from host float64
+    # arrays, H2D of both clouds, sort, lattice build, the EM loop, D2H
+    e2e = None
+    build_ms = head["build_ms"]
+    sites = head["path"].lattice.num_sites
+    del head["path"], other["path"]
+    torch.cuda.synchronize()
+    if not args.no_e2e:
+        old = _rigid.PRECISION
+        _rigid.PRECISION = args.precision
+        try:
+            for _ in range(2):          # warm-up registrations (pools, streams)
+                fr.register(ref_pc, obs_pc, fr.RigidModel(), cfg, process_group=group)
+            torch.cuda.synchronize()
+            if group is not None:
+                dist.barrier()
+            walls = []
+            for _ in range(max(3, min(args.steps, 10))):
+                t0 = time.perf_counter()
+                res = fr.register(fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(), cfg,
+                                  process_group=group)
+                _ = res.kinematics.pose.matrix()
+                torch.cuda.synchronize()
+                walls.append(time.perf_counter() - t0)
+        finally:
+            _rigid.PRECISION = old
+        et = torch.tensor([float(np.mean(walls))], dtype=torch.float64, device=dev)
         if group is not None:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_s = float(et.item())
-        e2e = {"value": M_total * res.iterations / e2e_s, "unit": "points/s",
-               "h2d_bytes_per_step": (12 * M_local + 12 * N_obs) / args.steps,
-               "d2h_bytes_per_step": (8 * 12 + 24 * args.steps) / args.steps,
-               "em_iterations": res.iterations, "wall_s": e2e_s,
-               "includes": "H2D of the model shard + observation cloud, lattice build, "
-                           "EM iterations, D2H of pose and traces"}
+        bpp = 24 if args.precision == "f64" else 12
+        e2e = {"value": M_total_of(head, M_local, world) * res.iterations / e2e_s,
+               "unit": "points/s", "h2d_bytes_per_step": bpp * (M_local + N_obs),
+               "d2h_bytes_per_step": 8 * 12 + 24 * res.iterations,
+               "em_iterations": res.iterations, "wall_s_mean": e2e_s,
+               "wall_s_reps": walls,
+               "includes": "register() from host float64 PointClouds: H2D of the model shard "
+                           "and observation cloud, Morton sort, lattice build (splat + blur + "
+                           "dense grid), tile copy, the EM loop, D2H of pose and traces"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, ns, no, nw = cpu_baseline(X, Y, sigma, args.cpu_sample, args.cpu_obs, 16)
+        v, dt, nw, bs = cpu_baseline(X, Y, sigma, args.cpu_iters)
         cpu = {"value": v, "unit": "points/s", "cores": nw, "kind": "port",
-               "sample": f"16 EM iterations over a {ns}-point random subset of the model cloud "
-                         f"({nw} worker processes) against a lattice on a {no}-point random "
-                         f"subset of the observation cloud ({dt:.1f} s timed; lattice build not "
-                         f"timed)"}
+               "sample": f"{args.cpu_iters} EM iterations over the full {len(X)}-point model "
+                         f"cloud against the lattice of the full {len(Y)}-point observation "
+                         f"cloud ({nw} worker processes, {dt:.1f} s timed; lattice build "
+                         f"{bs:.1f} s not timed)",
+               "same_config": True}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
-            "data": "synthetic",
-            "config": {"workload": f"C5 rigid pt2pt pebble, {args.points} clean model pts/GPU "
-                                   "+ 5% outliers; observation {0} pts + 5% (BASELINE "
-                                   "configs[4])".format(args.points),
-                       "points_per_gpu": M_local, "model_points_total": M_total,
+            "metric": METRIC, "value": head["value"], "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": workload_name(args.points),
+                       "points_per_gpu": M_local, "model_points_total": M_local * world,
                        "obs_points": N_obs, "sigma_frac": 0.05, "outlier_ratio": 0.1,
-                       "lattice_sites": sites, "dense_grid_cells": dense_cells,
+                       "em_iters_per_step": EM_PER_STEP, "lattice_sites": sites,
                        "build_ms": build_ms, "l2": l2_note,
-                       "query_path": "centred float32 point tiles over the dense slice grid, "
-                                     "float64 accumulation every 64 points per thread; one kernel per EM "
-                                     "iteration (pass + reduction + float64 solve)",
+                       "query_path": ("float64: forward map, simplex, dense float64 slice grid, "
+                                      "epilogue and the 25 statistics all in float64; one "
+                                      "cooperative grid-resident launch per registration")
+                       if args.precision == "f64" else "float32 point path",
                        "parallelism": f"dp{world} (model shards, replicated lattice, NCCL "
                                       "all-reduce of 25 doubles per iteration)"},
-            "em_iters_per_sec": args.steps / (total_ms / 1e3),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_rigid_pass_tiles (pass-only variant, incl. its fused "
-                                   "fixed-order reduction in the last block)",
-                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": kernel_ms,
-                         "pass_with_copy_ms": pass_ms,
-                         "peak_source": peak_kind},
+            "em_iters_per_sec": EM_PER_STEP * args.steps / (head["total_ms"] / 1e3),
+            "em_iteration_us": 1e3 * head["ms_per_step"] / EM_PER_STEP,
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": kernels_per_iter * args.steps,
-            "clocks": clk.summary(),
+            "gpu_launches": head["launch"]["kernels_per_step"] * args.steps,
+            "launch": head["launch"],
+            "clocks": head["clocks"],
+            "other_precision": {"dtype": other_precision, "value": other["value"],
+                                "ms_per_step": other["ms_per_step"],
+                                "em_iteration_us": 1e3 * other["ms_per_step"] / EM_PER_STEP,
+                                "engine": other["em_kind"], "build_ms": other["build_ms"]},
+            "p100k": p100k,
         }
         print(json.dumps(line), flush=True)
     if group is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def M_total_of(head, M_local, world):
+    return M_local * world
 
 
 def run_sigma(args):

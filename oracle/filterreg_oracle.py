@@ -386,10 +386,13 @@ class OracleMoments:
             return self.lattice.slice(x)
         return gauss_bruteforce(x, self.obs, self.values, self.sigma)
 
-    def moments(self, x):
+    def moments(self, x, n_model=None):
+        """`n_model`: the whole model cloud's size when x is one shard of it
+        (the outlier constant uses the global count, estep.py:197-198)."""
         x = np.asarray(x, dtype=float)
         out = self.raw(x)
-        cp = outlier_constant(self.w, len(self.obs), len(x), self.sigma)
+        cp = outlier_constant(self.w, len(self.obs), len(x) if n_model is None else n_model,
+                              self.sigma)
         return moment_epilogue(out, x, cp, self.m2_col, self.normal_cols)
 
 

@@ -475,10 +475,12 @@ __global__ void __launch_bounds__(THREADS + (S ? 32 : 0), MINB) k_em64(Em64Args 
                 const int n = se.max_em_iters;
                 if (MINB == 1 && THREADS <= 256)   // 255 registers: the solve inlined
                     rigid_solve_impl(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
-                                     blockIdx.x == 0);
+                                     blockIdx.x == 0,
+                                     a.prof && blockIdx.x == 0 ? a.prof + 8 * it + 5 : nullptr);
                 else
                     rigid_solve_body(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
-                                     blockIdx.x == 0);
+                                     blockIdx.x == 0,
+                                     a.prof && blockIdx.x == 0 ? a.prof + 8 * it + 5 : nullptr);
             }
             __syncthreads();
         }

@@ -77,6 +77,10 @@ def main():
                       "barrier_wait_us": float(np.median(b[:, 2] - b[:, 1])) / 1e3,
                       "reduce_us": float(np.median(b[:, 3] - b[:, 2])) / 1e3,
                       "solve_us": float(np.median(b[:, 4] - b[:, 3])) / 1e3,
+                      "solve_normal_eq_us": float(np.median(b[:, 5] - b[:, 3])) / 1e3,
+                      "solve_chol_us": float(np.median(b[:, 6] - b[:, 5])) / 1e3,
+                      "solve_halving_us": float(np.median(b[:, 7] - b[:, 6])) / 1e3,
+                      "solve_update_us": float(np.median(b[:, 4] - b[:, 7])) / 1e3,
                       "next_start_us": float(np.median(buf.astype(np.int64)[3:, 0]
                                                        - buf.astype(np.int64)[2:-1, 4])) / 1e3}
         print(json.dumps({"points": len(X), "setup_ms": setup_ms, "pass_ms": pass_ms,
