@@ -641,16 +641,19 @@ def run_batch(args):
     t_seq, t_bat = float(np.median(seqs)), float(np.median(bats))
     same = all(np.array_equal(a.kinematics.pose.matrix(), b.kinematics.pose.matrix())
                for a, b in zip(seq, bat))
+    dev = max(O.rotation_angle(a.kinematics.pose.rotation @ b.kinematics.pose.rotation.T)
+              for a, b in zip(seq, bat))
     iters = sum(r.iterations for r in bat)
     print(json.dumps({
         "metric": "registrations/s (C1 bench protocol, 30 trials)", "value": 30 / t_bat,
         "unit": "registrations/s", "n_gpus": 1, "higher_is_better": True, "mode": "batch",
-        "data": "synthetic", "dtype": "f32+f64",
+        "data": "synthetic", "dtype": fr._rigid.PRECISION,
         "config": {"workload": "C1 rigid pt2pt pebble 10k + 5% outliers, 30 seeded trials, "
                                "<= 250 iterations, tol 2e-4", "max_concurrent": 8},
         "batched_s": t_bat, "sequential_s": t_seq, "speedup_vs_sequential": t_seq / t_bat,
         "batched_s_reps": bats, "sequential_s_reps": seqs,
         "em_iterations_total": iters, "identical_to_sequential": bool(same),
+        "max_rotation_deviation_vs_sequential_rad": dev,
     }), flush=True)
 
 

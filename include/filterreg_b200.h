@@ -372,6 +372,11 @@ int fr_em64_destroy(fr_em64 *em);
 int fr_em64_run(fr_em64 *em, int n_iters, void *stream);
 /* one pass + fixed-order reduction at the current pose into the sums buffer
  * (no solve): kernel timing and the sharded loop */
+/* independent registrations (replicas, no collectives) in ONE cooperative
+ * launch, problem i on its own CTAs (the batched multi-problem driver; the
+ * reference runs bench trials one after another, bench.py:132-159).
+ * Synchronises `stream`. */
+int fr_em64_run_batch(fr_em64 **ems, int n, void *stream);
 int fr_em64_pass(fr_em64 *em, void *stream);
 int fr_em64_solve(fr_em64 *em, void *stream);
 int fr_em64_sums(fr_em64 *em, double **d_sums, int *width);

@@ -34,7 +34,8 @@ EXPORTED = (
     "fr_rigid_em_result", "fr_sort_points_morton", "fr_body_params_doubles", "fr_body_pass",
     "fr_body_objective", "fr_graph_pass", "fr_graph_blocks", "fr_graph_objective",
     "fr_point_rows", "fr_upload_points", "fr_rigid_em_persistent", "fr_rigid_em_run_batch",
-    "fr_em64_create", "fr_em64_destroy", "fr_em64_run", "fr_em64_pass", "fr_em64_solve",
+    "fr_em64_create", "fr_em64_destroy", "fr_em64_run", "fr_em64_run_batch", "fr_em64_pass",
+    "fr_em64_solve",
     "fr_em64_sums", "fr_em64_launch_info", "fr_em64_status", "fr_em64_result",
     "fr_upload_points64", "fr_lattice_splat_points64", "fr_sort_points_morton64",
     "fr_lattice_dense_cells64",
@@ -125,6 +126,7 @@ _SIGS = {
     "fr_em64_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),
     "fr_em64_destroy": ([_P], _I),
     "fr_em64_run": ([_P, _I, _P], _I),
+    "fr_em64_run_batch": ([ctypes.POINTER(_P), _I, _P], _I),
     "fr_em64_pass": ([_P, _P], _I),
     "fr_em64_solve": ([_P, _P], _I),
     "fr_em64_sums": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_I)], _I),

@@ -326,7 +326,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
 }
 
 template <int THREADS, int MINB, int S>
-__global__ void __launch_bounds__(THREADS + (S ? 32 : 0), MINB) k_em64(Em64Args a) {
+__device__ __forceinline__ void em64_cta(const Em64Args &a) {
     // S > 0: warp W produces tiles into an S-stage TMA ring; S == 0: every
     // thread prefetches its next point into registers (plain loads)
     constexpr int W = THREADS / 32;          // consumer warps
@@ -497,6 +497,20 @@ __global__ void __launch_bounds__(THREADS + (S ? 32 : 0), MINB) k_em64(Em64Args 
     }
 }
 
+// the kernel: one problem (parameters by value: constant-bank operands), or a
+// batch of independent problems, blockIdx.y = problem (replicas, no
+// collectives; every problem has its own state, partial rows and counter)
+template <int THREADS, int MINB, int S, bool BATCH>
+__global__ void __launch_bounds__(THREADS + (S ? 32 : 0), MINB)
+k_em64(Em64Args a0, const Em64Args *__restrict__ batch) {
+    if constexpr (BATCH) {
+        const Em64Args a = batch[blockIdx.y];
+        em64_cta<THREADS, MINB, S>(a);
+    } else {
+        em64_cta<THREADS, MINB, S>(a0);
+    }
+}
+
 // the solve alone (sharded runs: after the all-reduce of the pass sums)
 __global__ void k_em64_solve(const double *sums, EmDev *e, double *traces) {
     __shared__ EmDev se;
@@ -515,11 +529,13 @@ __global__ void k_em64_solve(const double *sums, EmDev *e, double *traces) {
         reinterpret_cast<unsigned long long *>(e)[q] = src[q];
 }
 
-// launch variants (FR_EM64_VARIANT): threads x CTAs/SM, tile ring stages
-// (0: per-thread register prefetch; > 0: TMA ring with a producer warp)
-using E64Kernel = void (*)(Em64Args);
+// launch variants (FR_EM64_VARIANT): 0 (default) = 512 consumer threads x 1
+// CTA/SM with a per-thread register prefetch of the next point; 1 = 384 x 1
+// with an 8-stage TMA bulk-copy ring fed by a producer warp (measured slower:
+// the pass is issue / FP64-latency bound, not stream bound)
+using E64Kernel = void (*)(Em64Args, const Em64Args *);
 struct E64Variant {
-    E64Kernel fn;
+    E64Kernel fn, batch;
     int threads, minb, stages;
     int block() const { return threads + (stages ? 32 : 0); }
     size_t smem() const { return (size_t)stages * 3 * threads * sizeof(double); }
@@ -531,16 +547,13 @@ static E64Variant e64_variant() {
         const char *e = getenv("FR_EM64_VARIANT");
         v = e ? atoi(e) : 0;
     }
-    switch (v) {
-        case 1: return {k_em64<384, 1, 8>, 384, 1, 8};
-        case 2: return {k_em64<384, 1, 0>, 384, 1, 0};
-        case 3: return {k_em64<256, 2, 4>, 256, 2, 4};
-        default: return {k_em64<512, 1, 0>, 512, 1, 0};
-    }
+    if (v == 1) return {k_em64<384, 1, 8, false>, k_em64<384, 1, 8, true>, 384, 1, 8};
+    return {k_em64<512, 1, 0, false>, k_em64<512, 1, 0, true>, 512, 1, 0};
 }
 
 static int e64_grid(const E64Variant &k) {
     cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem());
+    cudaFuncSetAttribute(k.batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem());
     int per = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k.fn, k.block(), k.smem()) !=
             cudaSuccess || per < 1)
@@ -573,7 +586,7 @@ struct fr_em64 {
     size_t smem = 0;
     long long n_tiles = 0;
     double *d_tiles = nullptr;       // centred [n_tiles][3][threads] copy of the model points
-    fr::E64Kernel fn = nullptr;
+    fr::E64Kernel fn = nullptr, batch_fn = nullptr;
     fr::EmDev *d_em = nullptr;
     double *d_sums = nullptr;
     double *d_partials = nullptr;
@@ -586,11 +599,11 @@ struct fr_em64 {
 
 using namespace fr;
 
-static int e64_launch(fr_em64 *em, int n_iters, int solve, cudaStream_t s) {
+static Em64Args e64_args(fr_em64 *em, int n_iters, int solve, int grid) {
     Em64Args a;
     a.tiles = em->d_tiles;
     a.m = em->m;
-    a.tiles_per_cta = (int)((em->n_tiles + em->grid - 1) / em->grid);
+    a.tiles_per_cta = (int)((em->n_tiles + grid - 1) / grid);
     a.g = em->lat->dense64;
     a.em = em->d_em;
     a.partials = em->d_partials;
@@ -603,8 +616,14 @@ static int e64_launch(fr_em64 *em, int n_iters, int solve, cudaStream_t s) {
     a.prof = em->d_prof;
     for (int j = 0; j < 3; ++j) a.sc[j] = em->lat->c.sf[j] / em->lat->c.sigma[j];
     a.cp = em->cp;
+    return a;
+}
+
+static int e64_launch(fr_em64 *em, int n_iters, int solve, cudaStream_t s) {
+    Em64Args a = e64_args(em, n_iters, solve, em->grid);
+    const Em64Args *none = nullptr;
     FR_CUDA(cudaMemsetAsync(em->d_sync, 0, 2 * sizeof(unsigned), s));
-    void *args[] = {&a};
+    void *args[] = {&a, &none};
     FR_CUDA(cudaLaunchCooperativeKernel((const void *)em->fn, dim3(em->grid), dim3(em->block),
                                         args, em->smem, s));
     return FR_OK;
@@ -639,11 +658,14 @@ int fr_em64_create(const fr_lattice *lat, const double *ref, int64_t m,
     em->cp = cfg->c_prime;
     const E64Variant kv = e64_variant();
     em->fn = kv.fn;
+    em->batch_fn = kv.batch;
     em->threads = kv.threads;
     em->block = kv.block();
     em->smem = kv.smem();
-    em->grid = e64_grid(kv);
     em->n_tiles = (m + kv.threads - 1) / kv.threads;
+    // small clouds: no more CTAs than tiles (fewer arrivals per barrier, and
+    // the SMs stay free for other problems)
+    em->grid = (int)std::min<long long>(e64_grid(kv), em->n_tiles);
     EmDev h;
     memset(&h, 0, sizeof(h));
     embedding_matrix(lat->c, h.A);
@@ -667,8 +689,9 @@ int fr_em64_create(const fr_lattice *lat, const double *ref, int64_t m,
     make_rigid_k(h.A, h.R, h.t, h.c_ref, h.cp, h.gain, -1, -1, &h.k);
     if (cudaMallocAsync((void **)&em->d_em, sizeof(EmDev), s) != cudaSuccess ||
         cudaMallocAsync((void **)&em->d_sums, kE64Row * sizeof(double), s) != cudaSuccess ||
-        cudaMallocAsync((void **)&em->d_partials, (size_t)2 * em->grid * kE64Row * sizeof(double),
-                        s) != cudaSuccess ||
+        cudaMallocAsync((void **)&em->d_partials,
+                        (size_t)2 * kE64MaxSms * kv.minb * kE64Row * sizeof(double), s) !=
+            cudaSuccess ||
         cudaMallocAsync((void **)&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double), s) !=
             cudaSuccess ||
         cudaMallocAsync((void **)&em->d_sync, 2 * sizeof(unsigned), s) != cudaSuccess ||
@@ -729,6 +752,49 @@ int fr_em64_run(fr_em64 *em, int n_iters, void *stream) {
     em->stream = (cudaStream_t)stream;
     const int n = n_iters > 0 ? n_iters : em->max_iters;
     return e64_launch(em, n, 1, (cudaStream_t)stream);
+}
+
+// independent float64 registrations in one cooperative launch: problem i
+// runs on its own G CTAs (blockIdx.y = i), G = SMs / n (at least 1; waves of
+// at most SMs problems).  Every problem's result equals fr_em64_run's on the
+// same grid size.  Synchronises `stream`.
+int fr_em64_run_batch(fr_em64 **ems, int n, void *stream) {
+    if (n < 0 || (n > 0 && !ems)) {
+        set_error("invalid batch arguments");
+        return FR_EINVAL;
+    }
+    if (n == 0) return FR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int i = 0; i < n; ++i)
+        if (!ems[i] || ems[i]->fn != ems[0]->fn) {
+            set_error("batch problem %d is null or was created under another launch variant", i);
+            return FR_EINVAL;
+        }
+    const int sms = std::min(sm_count(), kE64MaxSms);
+    for (int w0 = 0; w0 < n; w0 += sms) {
+        const int nw = std::min(n - w0, sms);
+        int g = std::max(1, sms / nw);
+        long long max_tiles = 0;
+        for (int i = w0; i < w0 + nw; ++i) max_tiles = std::max(max_tiles, ems[i]->n_tiles);
+        g = (int)std::min<long long>(g, max_tiles);
+        std::vector<Em64Args> h((size_t)nw);
+        for (int i = 0; i < nw; ++i) {
+            fr_em64 *em = ems[w0 + i];
+            em->stream = s;
+            h[i] = e64_args(em, em->max_iters, 1, g);
+            FR_CUDA(cudaMemsetAsync(em->d_sync, 0, 2 * sizeof(unsigned), s));
+        }
+        Em64Args *d = nullptr;
+        FR_CUDA(cudaMallocAsync((void **)&d, h.size() * sizeof(Em64Args), s));
+        FR_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(Em64Args), cudaMemcpyHostToDevice, s));
+        Em64Args unused = h[0];
+        void *args[] = {&unused, &d};
+        FR_CUDA(cudaLaunchCooperativeKernel((const void *)ems[0]->batch_fn, dim3(g, nw),
+                                            dim3(ems[0]->block), args, ems[0]->smem, s));
+        FR_CUDA(cudaFreeAsync(d, s));
+        FR_CUDA(cudaStreamSynchronize(s));       // the host vector backs the copy
+    }
+    return FR_OK;
 }
 
 int fr_em64_pass(fr_em64 *em, void *stream) {

@@ -414,7 +414,6 @@ def register_batch(problems, config: RegistrationConfig | None = None,
 
     import torch
 
-    from ._rigid import DeviceEM
     problems = list(problems)
     if not problems:
         return []
@@ -432,6 +431,9 @@ def register_batch(problems, config: RegistrationConfig | None = None,
                 slot.stream = streams[next(counter)]
         return slot.stream
 
+    from . import _rigid
+    precision = _rigid.PRECISION
+
     def setup(item):
         ref, obs, model, cfg = item
         st = stream()
@@ -440,8 +442,8 @@ def register_batch(problems, config: RegistrationConfig | None = None,
                 res = register(ref, obs, model, cfg)
                 st.synchronize()
                 return ("done", res)
-            path = RigidDevicePath(ref, obs, cfg.gmm, cfg.residual_mode)
-            em = DeviceEM(path, model.pose.rotation, model.pose.translation, cfg)
+            path = RigidDevicePath(ref, obs, cfg.gmm, cfg.residual_mode, precision=precision)
+            em = _rigid.device_em(path, model.pose.rotation, model.pose.translation, cfg)
             st.synchronize()
             return ("em", path, em)
 
@@ -459,13 +461,22 @@ def register_batch(problems, config: RegistrationConfig | None = None,
         out = [s[1] if s[0] == "done" else None for s in staged]
         em_idx = [k for k, s in enumerate(staged) if s[0] == "em"]
         lib = _lib_load()
-        persist = [k for k in em_idx if lib.fr_rigid_em_persistent(staged[k][2].h)]
+        # float64 loops: every problem in one cooperative launch (own CTAs each)
+        f64 = [k for k in em_idx if isinstance(staged[k][2], _rigid.DeviceEM64)]
+        if f64:
+            handles = (ctypes.c_void_p * len(f64))(*[staged[k][2].h.value for k in f64])
+            _check(lib.fr_em64_run_batch(handles, len(f64), _stream_handle()))
+            for k in f64:
+                out[k] = _device_loop_result(staged[k][2], items[k][2], None, 0.0)
+        # float32 loops small enough for the cluster kernel: one launch too
+        persist = [k for k in em_idx if k not in set(f64)
+                   and lib.fr_rigid_em_persistent(staged[k][2].h)]
         if persist:
             handles = (ctypes.c_void_p * len(persist))(*[staged[k][2].h.value for k in persist])
             _check(lib.fr_rigid_em_run_batch(handles, len(persist), _stream_handle()))
             for k in persist:
                 out[k] = _device_loop_result(staged[k][2], items[k][2], None, 0.0)
-        rest = [k for k in em_idx if k not in set(persist)]
+        rest = [k for k in em_idx if k not in set(persist) and k not in set(f64)]
         for k, res in zip(rest, pool.map(finish, rest)):
             out[k] = res
     return out
