@@ -386,6 +386,31 @@ int fr_em64_status(fr_em64 *em, int *done, int *iterations, int *termination, vo
 int fr_em64_result(fr_em64 *em, double *R, double *t, double *objectives, double *twist_norms,
                    double *inlier_masses, int *iterations, int *termination, void *stream);
 
+/* ---- float64 device-resident rigid point-to-plane EM loop (pipeline.py:
+ * 125-181, residual_mode "point_to_plane"; mstep.py:39-98, 179-210, 421-459)
+ * d_ref: float64 planes of m model points (Morton order); the lattice holds
+ * the [1, y, n] columns (7; fr_lattice_splat_points64 with FR_VALUES_NORMALS)
+ * and its dense float64 grid.  One cooperative launch per fr_em64pl_run: per
+ * iteration the E pass (moments, averaged normals, the residual spec stored
+ * per point, H and g), the damped 6x6 Cholesky with tenfold escalation, step
+ * halving with candidate objectives evaluated over the stored spec (batches
+ * of candidate poses built in parallel), max_gn_iters > 1 re-assembly at the
+ * accepted pose, update magnitude and termination -- no host round trip.
+ * Same result conventions as fr_em64 (cfg->sigma_inv is unused: plane rows
+ * and the point rows of invalid normals are unscaled, mstep.py:86-98). */
+typedef struct fr_em64pl fr_em64pl;
+
+int fr_em64pl_create(const fr_lattice *lat, const double *d_ref, int64_t m,
+                     const fr_rigid_em_config *cfg, void *stream, fr_em64pl **out);
+int fr_em64pl_destroy(fr_em64pl *em);
+int fr_em64pl_run(fr_em64pl *em, int n_iters, void *stream);
+int fr_em64pl_sums(fr_em64pl *em, double **d_sums, int *width);
+int fr_em64pl_launch_info(const fr_em64pl *em, int *grid, int *block);
+int fr_em64pl_status(fr_em64pl *em, int *done, int *iterations, int *termination, void *stream);
+int fr_em64pl_result(fr_em64pl *em, double *R, double *t, double *objectives,
+                     double *twist_norms, double *inlier_masses, int *iterations,
+                     int *termination, void *stream);
+
 /* float64 counterparts of the point helpers above: (n, 3) host rows ->
  * (3, n) float64 device planes (a transpose, no rounding); splat of
  * [1, y, (|y|^2), (n)] from float64 planes; Morton reorder of float64 planes */

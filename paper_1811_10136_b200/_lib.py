@@ -39,6 +39,8 @@ EXPORTED = (
     "fr_em64_sums", "fr_em64_launch_info", "fr_em64_status", "fr_em64_result",
     "fr_upload_points64", "fr_lattice_splat_points64", "fr_sort_points_morton64",
     "fr_lattice_dense_cells64",
+    "fr_em64pl_create", "fr_em64pl_destroy", "fr_em64pl_run", "fr_em64pl_sums",
+    "fr_em64pl_launch_info", "fr_em64pl_status", "fr_em64pl_result",
 )
 
 
@@ -135,6 +137,15 @@ _SIGS = {
     "fr_em64_result": ([_P, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I), ctypes.POINTER(_I), _P],
                        _I),
     "fr_upload_points64": ([_P, _L, _P, _P], _I),
+    "fr_em64pl_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),
+    "fr_em64pl_destroy": ([_P], _I),
+    "fr_em64pl_run": ([_P, _I, _P], _I),
+    "fr_em64pl_sums": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_I)], _I),
+    "fr_em64pl_launch_info": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "fr_em64pl_status": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I), _P],
+                         _I),
+    "fr_em64pl_result": ([_P, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I), ctypes.POINTER(_I),
+                          _P], _I),
     "fr_lattice_splat_points64": ([_P, _P, _P, _L, _I, _P], _I),
     "fr_sort_points_morton64": ([_P, _L, _I, _P, _P], _I),
 }

@@ -271,8 +271,7 @@ class RigidDevicePath:
         if precision not in ("f32", "f64"):
             raise ValueError(f"unknown precision {precision!r}")
         # float64 planes for the float64 device loop (point_to_point, fixed sigma)
-        self.f64 = precision == "f64" and residual_mode == "point_to_point" \
-            and not gmm.update_sigma
+        self.f64 = precision == "f64" and not gmm.update_sigma
         self.mode = _lib.FR_POINT_TO_PLANE if residual_mode == "point_to_plane" \
             else _lib.FR_POINT_TO_POINT
         self.gmm = gmm
@@ -334,7 +333,7 @@ class RigidDevicePath:
             self.lib.fr_rigid_scratch_doubles(self.mode, int(self.with_sigma), self.M), **f64)
         self.host = torch.empty(max(self.width, 16), dtype=torch.float64, pin_memory=True)
         self.wtn = torch.empty((7, self.M), dtype=torch.float32, device=self.dev) \
-            if self.mode == _lib.FR_POINT_TO_PLANE else None
+            if self.mode == _lib.FR_POINT_TO_PLANE and not self.f64 else None
         lap("buffers")
         try:
             obs_job.result()          # the side stream is synchronised inside
@@ -351,8 +350,11 @@ class RigidDevicePath:
     def demote_f32(self) -> None:
         """Float32 copies of the float64 planes (for the float32-plane pass
         kernels; the caller's values round to nearest)."""
-        if self.ref.dtype != np.float32 and str(self.ref.dtype) != "torch.float32":
+        import torch
+        if self.ref.dtype != torch.float32:
             self.ref = self.ref.float()
+        if self.mode == _lib.FR_POINT_TO_PLANE and self.wtn is None:
+            self.wtn = torch.empty((7, self.M), dtype=torch.float32, device=self.dev)
         self.f64 = False
 
     @property
@@ -374,6 +376,8 @@ class RigidDevicePath:
                 # float64 planes, splat from them (keys bit-exact for any input)
                 self.obs = upload_soa64(observation.positions, self.dev)
                 self.N, self.obs_n = self.obs.shape[1], None
+                if residual_mode == "point_to_plane":
+                    self.obs_n = upload_soa64(observation.normals, self.dev)
                 self._obs_uploaded.set()
                 if lap is not None:
                     lap("obs_upload")
@@ -479,6 +483,29 @@ class RigidDevicePath:
 
     def centre(self, R, t) -> np.ndarray:
         return np.asarray(R, dtype=float) @ self.c_ref + np.asarray(t, dtype=float)
+
+    def assemble_stored(self, R, t) -> np.ndarray:
+        """point_to_plane normal equations at pose (R, t) over the residual spec
+        stored by the last pass (the weight / target / normal planes; extra
+        Gauss-Newton iterations of mstep.py:425-459 keep the E step's spec):
+        [H upper 21 | g 6 | sum r^2], all-reduced over the group."""
+        import torch
+        R = torch.as_tensor(np.asarray(R, dtype=float), device=self.dev)
+        t = torch.as_tensor(np.asarray(t, dtype=float), device=self.dev)
+        X = (R @ self.ref.double() + t[:, None]).t().contiguous()       # (m, 3) float64
+        w = self.wtn[0].double().contiguous()
+        T = self.wtn[1:4].double().t().contiguous()
+        N = self.wtn[4:7].double().t().contiguous()
+        valid = (N != 0).any(dim=1).to(torch.uint8).contiguous()
+        sums = torch.empty(28, dtype=torch.float64, device=self.dev)
+        scratch = torch.empty(self.lib.fr_rigid_scratch_doubles(0, 0, self.M),
+                              dtype=torch.float64, device=self.dev)
+        si, _keep = _lib.dptr(1.0 / np.asarray(self.sigma, dtype=float))
+        _lib.check(self.lib.fr_assemble_rigid(_lib.ptr(X), _lib.ptr(w), _lib.ptr(T), self.M, si,
+                                              1, _lib.ptr(N), _lib.ptr(valid), _lib.ptr(sums),
+                                              _lib.ptr(scratch), _lib.stream_handle()))
+        self.reduce_device(sums)
+        return sums.cpu().numpy()
 
     def candidate_objectives(self, poses) -> np.ndarray:
         """0.5 * sum r^2 at each (R, t) under the stored point_to_plane spec."""
@@ -697,11 +724,96 @@ class DeviceEM64:
                 _lib.FR_TERM[int(term.value)])
 
 
+class DeviceEM64PL(DeviceEM64):
+    """The float64 rigid point-to-plane EM loop (fr_em64pl_*): E pass with the
+    stored residual spec, device Cholesky, parallel halving candidates and
+    extra Gauss-Newton iterations in one cooperative launch.  Single GPU."""
+
+    def __init__(self, path: RigidDevicePath, R0, t0, config):
+        import torch
+        if path.group is not None:
+            raise ValueError("the point-to-plane device loop runs on one GPU")
+        self.path = path
+        self.lib = path.lib
+        self.max_iters = int(config.max_em_iters)
+        c = _lib.RigidEmConfig()
+        c.R0[:] = list(np.asarray(R0, dtype=float).reshape(-1))
+        c.t0[:] = list(np.asarray(t0, dtype=float).reshape(-1))
+        c.c_ref[:] = list(path.c_ref)
+        c.sigma_inv[:] = list(1.0 / np.asarray(path.sigma, dtype=float))
+        c.c_prime = path.c_prime
+        c.diameter = path.diameter
+        c.twist_tolerance = float(config.twist_tolerance)
+        ms = config.mstep
+        c.damping = -1.0 if ms.damping is None else float(ms.damping)
+        c.step_tolerance = float(ms.step_tolerance)
+        c.degenerate_mass = 1e-9 * path.M_total
+        c.max_em_iters = self.max_iters
+        c.max_gn_iters = int(ms.max_gn_iters)
+        c.max_halvings = int(ms.max_halvings)
+        c.fast = 0
+        self._cfg = c
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.fr_em64pl_create(path.lattice.handle, _lib.ptr(path.ref), path.M,
+                                             ctypes.byref(c), _lib.stream_handle(),
+                                             ctypes.byref(h)))
+        self.h = h
+        sp = ctypes.c_void_p()
+        w = ctypes.c_int()
+        _lib.check(self.lib.fr_em64pl_sums(h, ctypes.byref(sp), ctypes.byref(w)))
+        self.sums = torch.as_tensor(_DeviceArray(sp.value, w.value), device=path.dev)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.fr_em64pl_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def launch_info(self):
+        g, b = ctypes.c_int(), ctypes.c_int()
+        _lib.check(self.lib.fr_em64pl_launch_info(self.h, ctypes.byref(g), ctypes.byref(b)))
+        return int(g.value), int(b.value)
+
+    def enqueue(self, n: int) -> None:
+        _lib.check(self.lib.fr_em64pl_run(self.h, int(n), _lib.stream_handle()))
+
+    def status(self):
+        d, it, term = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(self.lib.fr_em64pl_status(self.h, ctypes.byref(d), ctypes.byref(it),
+                                             ctypes.byref(term), _lib.stream_handle()))
+        return bool(d.value), int(it.value), _lib.FR_TERM[int(term.value)]
+
+    def run(self) -> None:
+        _lib.check(self.lib.fr_em64pl_run(self.h, 0, _lib.stream_handle()))
+
+    def result(self):
+        n = self.max_iters
+        R = np.zeros(9)
+        t = np.zeros(3)
+        obj, tn, ms = np.zeros(n), np.zeros(n), np.zeros(n)
+        it, term = ctypes.c_int(), ctypes.c_int()
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        _lib.check(self.lib.fr_em64pl_result(self.h, dp(R), dp(t), dp(obj), dp(tn), dp(ms),
+                                             ctypes.byref(it), ctypes.byref(term),
+                                             _lib.stream_handle()))
+        k = min(int(it.value), n)
+        return (R.reshape(3, 3), t, list(obj[:k]), list(tn[:k]), list(ms[:k]), int(it.value),
+                _lib.FR_TERM[int(term.value)])
+
+
 def device_em(path: RigidDevicePath, R0, t0, config):
     """The device EM loop of a path: float64 (DeviceEM64) on float64 planes
     with a dense float64 grid, else the float32-point loop (DeviceEM; a
     lattice whose site box exceeds the float64 grid budget runs DeviceEM's
     all-float64 hash-table pass over float32 copies of the planes)."""
+    if path.mode == _lib.FR_POINT_TO_PLANE:
+        if path.f64 and path.lattice.dense64:
+            return DeviceEM64PL(path, R0, t0, config)
+        raise ValueError("the point-to-plane device loop needs float64 planes and the dense "
+                         "float64 grid")
     if path.f64:
         if path.lattice.dense64:
             return DeviceEM64(path, R0, t0, config)

@@ -464,6 +464,7 @@ struct DenseSliceD {
     int a[3];               // site q minimum per coordinate
     int n[3];               // padded extents (span + 2 * kDensePad)
     int s0, s1;             // cell strides of coordinates 0 and 1
+    int r2;                 // double2 per row: 2 ([1, y]) or 4 ([1, y, n])
 };
 
 // float32 variant of qsimplex3 (packed keys for the hash-slot table)
@@ -580,6 +581,7 @@ struct fr_lattice {
     // dense float64 slice grid (same box; FR_DENSE64_MAX_CELLS) for the float64 EM loop
     double2 *dcells64 = nullptr;
     fr::DenseSliceD dense64{};
+    long long dense64_cells = 0;
     // d >= 4: sorted 128-bit site keys (hi / lo words) and their codec
     unsigned long long *wkh = nullptr, *wkl = nullptr;
     fr::WideCodec wc{};

@@ -17,14 +17,14 @@
 //                 statistics of the M step (mstep.py:102-210), accumulated in
 //                 float64 registers;
 //     block       warp reduce-scatter (31 shuffles for 25 columns) + a fixed-
-//                 order sum over the 8 warps -> one row of partials;
-//     grid        arrival counter; the LAST CTA to arrive sums the rows in a
-//                 fixed order, runs the float64 solve (fr_solve.cuh: normal
+//                 order sum over the warps -> one row of partials;
+//     grid        one arrival barrier (monotone counter, release / acquire);
+//                 then EVERY CTA sums the rows in the same fixed order and
+//                 runs the same float64 solve (fr_solve.cuh: normal
 //                 equations, damped Cholesky with tenfold escalation, step
 //                 halving with closed-form candidate objectives, twist update,
-//                 update magnitude, termination) and publishes the next pose
-//                 with a release increment of a generation word the other CTAs
-//                 spin on (acquire).
+//                 update magnitude, termination) on its shared-memory copy of
+//                 the state -- bit-identical in every CTA, so no broadcast.
 //
 // No launches, host polls or graph replays between iterations; all sums are
 // formed in a fixed order, so reruns are bit-identical.
@@ -38,13 +38,12 @@
 #include "fr_common.cuh"
 #include "fr_reduce.cuh"
 #include "fr_solve.cuh"
+#include "fr_em64.cuh"
 
 namespace fr {
 
 constexpr int kE64Threads = 256;
 constexpr int kE64Stats = 25;        // point-to-point sufficient statistics (_rigid.py)
-constexpr int kE64Row = 32;          // partials row stride (doubles)
-constexpr int kE64MaxSms = 160;      // grid <= MINB x this (the column sums' row registers)
 
 struct Em64Args {
     const double *tiles; // [n_tiles][3][T] centred model points (Morton order), T = threads
@@ -65,48 +64,7 @@ struct Em64Args {
     double cp;           // outlier constant c' (estep.py:99-112)
 };
 
-// pose constants of one iteration, held in registers by every thread
-struct Pose64 {
-    double R[9];
-    double cw[3];        // R c_ref + t
-};
 
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release_add(unsigned *p) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
-}
-
-// 1 / x to ~1 ulp without a slow path: MUFU seed, one cubic and one Newton
-// step (x > 0 finite; x = 0 gives inf, masked by the caller)
-__device__ __forceinline__ double rcp64(double x) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(fma(e, e, e), r, r);
-    e = fma(-x, r, 1.0);
-    return fma(e, r, r);
-}
-
-constexpr double kRoundMagic = 6755399441055744.0;     // 1.5 * 2^52
-
-// p ? a : b as a predicated select (no branch)
-__device__ __forceinline__ double sel64(bool p, double a, double b) {
-    double r;
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
-        : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)p));
-    return r;
-}
 
 // one model point: forward map, simplex, slice, epilogue, statistics
 // (h0, h1, h2) = x_ref - c_ref (the centred tile); valid = 0 for the padding
@@ -121,81 +79,12 @@ __device__ __forceinline__ void e64_point(const Em64Args &a, const Pose64 &k, do
         xt[i] = fma(k.R[3 * i + 2], h2, fma(k.R[3 * i + 1], h1, k.R[3 * i] * h0));
         X[i] = xt[i] + k.cw[i];                          // x = R x_ref + t
     }
-    // elevation E (x / sigma * sf) (permutohedral.py:171-179): row 0 = 1s,
-    // row j: -j at column j-1, 1 at columns >= j
-    const double f0 = X[0] * a.sc[0], f1 = X[1] * a.sc[1], f2 = X[2] * a.sc[2];
-    const double u = f1 + f2;
-    double el[4];
-    el[0] = f0 + u;
-    el[1] = u - f0;
-    el[2] = fma(-2.0, f1, f2);
-    el[3] = -3.0 * f2;
-    // rint(el / 4) (round half to even, as np.rint) by the 1.5 * 2^52 magic
-    // add: the integer sits in the low word; el - rem0 with one rounding
-    // (permutohedral.py:191-193).  Points beyond 2^40 lattice units get no
-    // support.
-    const bool in_range = (fabs(f0) + fabs(f1)) + fabs(f2) < 1e12;
-    int ri[4];
-    double d[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double t = fma(el[i], 0.25, kRoundMagic);
-        ri[i] = __double2loint(t);
-        d[i] = fma(-4.0, t - kRoundMagic, el[i]);
-    }
-    const int h = (ri[0] + ri[1]) + (ri[2] + ri[3]);
-    // stable descending ranks (:194-197): rank_i = #{j: d_j > d_i} + #{j < i: d_j == d_i}
-    const bool c01 = d[1] > d[0], c02 = d[2] > d[0], c03 = d[3] > d[0];
-    const bool c12 = d[2] > d[1], c13 = d[3] > d[1], c23 = d[3] > d[2];
-    int rank[4];
-    rank[0] = (int)c01 + (int)c02 + (int)c03;
-    rank[1] = (int)!c01 + (int)c12 + (int)c13;
-    rank[2] = (int)!c02 + (int)!c12 + (int)c23;
-    rank[3] = (int)!c03 + (int)!c13 + (int)!c23;
-    // vertex cells from the unwrapped ranks: vertex l (remainder class l) of
-    // the wrapped simplex (:198-203, 214) has cell coordinates
-    // q_c = ri_c - floor((rank_c + h + l) / 4); the remainder-0 cell is
-    // clamped into [2, n - 2]: a point clamped there has every vertex in the
-    // zero padding, as a point whose vertices have no site
-    int t[3], base = 0;
-    {
-        const int cq0 = min(max(ri[0] - g.a[0] + kDensePad, 2), g.n[0] - 2);
-        const int cq1 = min(max(ri[1] - g.a[1] + kDensePad, 2), g.n[1] - 2);
-        const int cq2 = min(max(ri[2] - g.a[2] + kDensePad, 2), g.n[2] - 2);
-        base = cq0 * g.s0 + cq1 * g.s1 + cq2;
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) t[c] = rank[c] + h;
-    // single +-(d+1) wrap of the ranks and res = (el - rem0') / (d+1) (:206)
-    double res[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int rk = rank[i] + h;
-        const int adj = (rk > 3) - (rk < 0);             // rem0' = rem0 - 4 adj
-        rank[i] = rk - 4 * adj;
-        res[i] = fma(d[i], 0.25, (double)adj);
-    }
-    double sv[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-        sv[r] = sel64(rank[0] == r, res[0], sel64(rank[1] == r, res[1],
-                                                  sel64(rank[2] == r, res[2], res[3])));
-    double bary[4];
-    bary[0] = (1.0 + sv[3]) - sv[0];                       // (:211-212)
-#pragma unroll
-    for (int l = 1; l < 4; ++l) bary[l] = sv[3 - l] - sv[4 - l];
-    double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-        const int cell = base - ((t[0] + l) >> 2) * g.s0 - ((t[1] + l) >> 2) * g.s1 -
-                         ((t[2] + l) >> 2);
-        const double2 *row = g.cells + 2 * (4 * cell + l);
-        const double2 ra = __ldg(row), rb = __ldg(row + 1);
-        o0 = fma(bary[l], ra.x, o0);
-        o1 = fma(bary[l], ra.y, o1);
-        o2 = fma(bary[l], rb.x, o2);
-        o3 = fma(bary[l], rb.y, o3);
-    }
+    Simplex64 S;
+    e64_simplex(g, a.sc, X, S);
+    double o[4];
+    e64_gather<2>(g, S, o);
+    const double o0 = o[0], o1 = o[1], o2 = o[2], o3 = o[3];
+    const bool in_range = S.in_range;
     // moments epilogue (estep.py:195-205): m0 = max(out0, 0), supported iff
     // m0 >= 1e-12, w = m0 / (m0 + c'), target = m1 / m0; unsupported points
     // get w = 0 and target = x (zero residual).  One reciprocal:
@@ -233,38 +122,6 @@ __device__ __forceinline__ void e64_point(const Em64Args &a, const Pose64 &k, do
     }
 }
 
-// warp reduce-scatter of N <= 32 columns, in place: after the five butterfly
-// steps lane L holds the warp's sum of column L (0 for L >= N).  31 shuffles
-// instead of the 5 N of a per-column tree.  Fixed order (deterministic).
-template <int N>
-__device__ __forceinline__ double warp_reduce_scatter(double (&v)[N]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int k = 16; k >= 1; k >>= 1) {
-        const bool upper = lane & k;
-#pragma unroll
-        for (int i = 0; i < k; ++i) {
-            if (i >= N) break;
-            const double lo = v[i];
-            const double hi = (i + k < N) ? v[i + k] : 0.0;
-            const double send = upper ? lo : hi;
-            const double keep = upper ? hi : lo;
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
-        }
-    }
-    return v[0];
-}
-
-// L2-coherent copy (the last CTA of the previous iteration wrote it from
-// another SM; L1 may hold the old lines)
-template <class T>
-__device__ __forceinline__ void copy_cg(T *dst, const T *src, int lane, int nlanes) {
-    static_assert(sizeof(T) % 8 == 0, "copied as 8-byte words");
-    const unsigned long long *a = reinterpret_cast<const unsigned long long *>(src);
-    unsigned long long *b = reinterpret_cast<unsigned long long *>(dst);
-    for (int w = lane; w < (int)(sizeof(T) / 8); w += nlanes) b[w] = __ldcg(a + w);
-}
-
 // One CTA of the grid-resident loop.  Every CTA keeps the EM state (EmDev)
 // in shared memory and runs the SAME fixed-order reduction and float64 solve
 // on the same partial rows, so all CTAs hold bit-identical poses without a
@@ -273,43 +130,6 @@ __device__ __forceinline__ void copy_cg(T *dst, const T *src, int lane, int nlan
 // state round trip through global memory.  Partial rows are double-buffered
 // by iteration parity (a CTA can only reuse a buffer after every CTA passed
 // the next barrier, i.e. finished reading it).
-// TMA bulk copies into a shared-memory ring (cp.async.bulk + mbarrier
-// transaction counts): one elected thread keeps S tiles in flight -- the
-// point stream needs ~40 KB in flight per SM to cover the HBM latency, far
-// more than one register prefetch per thread holds
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes,
-                                          unsigned long long *bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-    unsigned done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-
 // One CTA of the grid-resident loop.  Every CTA keeps the EM state (EmDev)
 // in shared memory and runs the SAME fixed-order reduction and float64 solve
 // on the same partial rows, so all CTAs hold bit-identical poses without a
@@ -504,7 +324,9 @@ template <int THREADS, int MINB, int S, bool BATCH>
 __global__ void __launch_bounds__(THREADS + (S ? 32 : 0), MINB)
 k_em64(Em64Args a0, const Em64Args *__restrict__ batch) {
     if constexpr (BATCH) {
-        const Em64Args a = batch[blockIdx.y];
+        // a reference (L1-cached loads), not a copy: a local struct copy
+        // would live in local memory
+        const Em64Args &a = batch[blockIdx.y];
         em64_cta<THREADS, MINB, S>(a);
     } else {
         em64_cta<THREADS, MINB, S>(a0);

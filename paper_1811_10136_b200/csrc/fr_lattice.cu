@@ -984,6 +984,7 @@ static void free_slice(fr_lattice *lat) {
     lat->dcells64 = nullptr;
     lat->dense = fr::DenseSliceF{};
     lat->dense64 = fr::DenseSliceD{};
+    lat->dense64_cells = 0;
     lat->dense_cells = 0;
     lat->nvp = 0;
     lat->nf4 = 0;
@@ -1037,7 +1038,8 @@ __global__ void k_dense_fill(long long S, const int *site_keys, const double *va
                     (float)(gain * v[0]));
 }
 
-// float64 rows: gain * (y0, y1 | y2, 1) sums of the value columns [1, y]
+// float64 rows: gain * (y0, y1 | y2, 1 [| n0, n1 | n2, 0]) sums of the value
+// columns [1, y] or [1, y, n]
 __global__ void k_dense_fill64(long long S, const int *site_keys, const double *vals, int nv,
                                double gain, fr::DenseSliceD t, double2 *cells) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1047,9 +1049,13 @@ __global__ void k_dense_fill64(long long S, const int *site_keys, const double *
     const long long c = ((long long)((k[0] >> 2) - t.a[0] + P) * t.s0 +
                          (long long)((k[1] >> 2) - t.a[1] + P) * t.s1 + ((k[2] >> 2) - t.a[2] + P));
     const double *v = vals + i * nv;
-    double2 *row = cells + 2 * (4 * c + (k[0] & 3));
+    double2 *row = cells + t.r2 * (4 * c + (k[0] & 3));
     row[0] = make_double2(gain * v[1], gain * v[2]);
     row[1] = make_double2(gain * v[3], gain * v[0]);
+    if (t.r2 == 4) {          // [1, y, n] (estep.py:153-165): the normal sums
+        row[2] = make_double2(gain * v[4], gain * v[5]);
+        row[3] = make_double2(gain * v[6], 0.0);
+    }
 }
 
 static long long dense64_cell_limit() {
@@ -1062,7 +1068,9 @@ __global__ void k_init_box(int *box) {
 }
 
 static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
-    if (lat->dim != 3 || lat->nv != 4 || lat->n_sites == 0) return FR_OK;
+    // nv = 4 ([1, y]: both grids); nv = 7 ([1, y, n], point-to-plane: the
+    // float64 grid only, 64-byte rows)
+    if (lat->dim != 3 || (lat->nv != 4 && lat->nv != 7) || lat->n_sites == 0) return FR_OK;
     int *dbox = nullptr;
     FR_CUDA(cudaMallocAsync(&dbox, 6 * sizeof(int), s));
     k_init_box<<<1, 32, 0, s>>>(dbox);
@@ -1078,22 +1086,26 @@ static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
         cells *= n[c];
         if (cells > dense_cell_limit()) return FR_OK;     // hash slots only
     }
-    fr::DenseSliceF t{};
-    for (int c = 0; c < 3; ++c) {
-        t.a[c] = box[c];
-        t.span[c] = (unsigned)(box[3 + c] - box[c] + 1);
+    if (lat->nv == 4) {
+        fr::DenseSliceF t{};
+        for (int c = 0; c < 3; ++c) {
+            t.a[c] = box[c];
+            t.span[c] = (unsigned)(box[3 + c] - box[c] + 1);
+        }
+        t.s1 = (int)n[2];
+        t.s0 = (int)(n[1] * n[2]);
+        FR_CUDA(pool_alloc(lat, (void **)&lat->dcells, (size_t)cells * 4 * sizeof(float4)));
+        FR_CUDA(cudaMemsetAsync(lat->dcells, 0, (size_t)cells * 4 * sizeof(float4), s));
+        k_dense_fill<<<grid_for(lat->n_sites), 256, 0, s>>>(lat->n_sites, lat->site_keys,
+                                                            lat->vals, lat->nv, lat->c.gain, t,
+                                                            lat->dcells);
+        FR_CHECK_LAUNCH();
+        t.cells = lat->dcells;
+        lat->dense = t;
+        lat->dense_cells = cells;
     }
-    t.s1 = (int)n[2];
-    t.s0 = (int)(n[1] * n[2]);
-    FR_CUDA(pool_alloc(lat, (void **)&lat->dcells, (size_t)cells * 4 * sizeof(float4)));
-    FR_CUDA(cudaMemsetAsync(lat->dcells, 0, (size_t)cells * 4 * sizeof(float4), s));
-    k_dense_fill<<<grid_for(lat->n_sites), 256, 0, s>>>(lat->n_sites, lat->site_keys, lat->vals,
-                                                        lat->nv, lat->c.gain, t, lat->dcells);
-    FR_CHECK_LAUNCH();
-    t.cells = lat->dcells;
-    lat->dense = t;
-    lat->dense_cells = cells;
-    if (cells <= dense64_cell_limit()) {
+    const int r2 = lat->nv == 4 ? 2 : 4;      // double2 per row
+    if (cells * r2 / 2 <= dense64_cell_limit()) {
         fr::DenseSliceD d{};
         for (int c = 0; c < 3; ++c) {
             d.a[c] = box[c];
@@ -1101,7 +1113,8 @@ static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
         }
         d.s1 = (int)n[2];
         d.s0 = (int)(n[1] * n[2]);
-        const size_t bytes = (size_t)cells * 4 * 2 * sizeof(double2);
+        d.r2 = r2;
+        const size_t bytes = (size_t)cells * 4 * r2 * sizeof(double2);
         FR_CUDA(pool_alloc(lat, (void **)&lat->dcells64, bytes));
         FR_CUDA(cudaMemsetAsync(lat->dcells64, 0, bytes, s));
         k_dense_fill64<<<grid_for(lat->n_sites), 256, 0, s>>>(lat->n_sites, lat->site_keys,
@@ -1110,6 +1123,7 @@ static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
         FR_CHECK_LAUNCH();
         d.cells = lat->dcells64;
         lat->dense64 = d;
+        lat->dense64_cells = cells;
     }
     return FR_OK;
 }
@@ -1591,7 +1605,7 @@ int fr_lattice_dense_cells64(const fr_lattice *lat, int64_t *cells) {
         set_error("null argument");
         return FR_EINVAL;
     }
-    *cells = lat->dcells64 ? lat->dense_cells : 0;
+    *cells = lat->dcells64 ? lat->dense64_cells : 0;
     return FR_OK;
 }
 

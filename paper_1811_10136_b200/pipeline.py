@@ -139,8 +139,6 @@ def _rigid_m_step(path: RigidDevicePath, sums, R, t, s2, opts: MStepOptions):
     else:
         value = 0.5 * float(sums[28])
         H, g = unpack_upper6(sums[1:22]), np.asarray(sums[22:28], dtype=float)
-        if opts.max_gn_iters > 1:
-            raise NotImplementedError("point_to_plane with max_gn_iters > 1 is not in this build")
     diag.objectives.append(value)
     for _ in range(opts.max_gn_iters):
         if not np.any(g):
@@ -191,6 +189,10 @@ def _rigid_m_step(path: RigidDevicePath, sums, R, t, s2, opts: MStepOptions):
         if p2p:
             mom = mom.moved(D, delta, c)
             H, g = mom.normal_equations(c, s2)
+        elif _ + 1 < opts.max_gn_iters:
+            # the same spec at the accepted pose (mstep.py:425-428)
+            st = path.assemble_stored(cand.pose.rotation, cand.pose.translation)
+            H, g = unpack_upper6(st[:21]), np.asarray(st[21:27], dtype=float)
     return current, diag
 
 
@@ -318,16 +320,23 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
         path = ArticulatedDevicePath(reference, observation, config.gmm, config.residual_mode,
                                      initial_model, process_group)
     else:
-        loop = (_path_factory is None and config.residual_mode == "point_to_point"
-                and not config.gmm.update_sigma and not config.record_states)
+        from . import _rigid
+        pl = config.residual_mode == "point_to_plane"
+        # the device-resident loops: point-to-point (any precision, sharded or
+        # not); point-to-plane in float64 on one GPU
+        loop = (_path_factory is None and not config.gmm.update_sigma
+                and not config.record_states
+                and (not pl or (process_group is None and _rigid.PRECISION == "f64")))
         if _path_factory is not None:
             path = _path_factory(reference, observation, config.gmm, config.residual_mode,
                                  process_group)
         else:
-            from . import _rigid
             path = RigidDevicePath(reference, observation, config.gmm, config.residual_mode,
                                    process_group,
                                    precision=_rigid.PRECISION if loop else "f32")
+        if loop and pl and not path.lattice.dense64:
+            loop = False
+            path.demote_f32()                 # site box above the float64 grid budget
         if loop:
             return _register_device_loop(path, initial_model, config, timing)
     model = initial_model

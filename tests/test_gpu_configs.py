@@ -87,7 +87,8 @@ def test_rigid_pebble_config(fr, precision, case):
     np.testing.assert_allclose(res.objectives[:k], g["objectives"][:k], rtol=rtol)
 
 
-def test_c2_point_to_plane_100k(fr):
+@pytest.mark.parametrize("precision", ["f64", "f32"], indirect=True)
+def test_c2_point_to_plane_100k(fr, precision):
     g = load("c2")
     ref = fr.PointCloud(g["X"].astype(np.float64), normals=g["N"].astype(np.float64))
     obs = fr.PointCloud(g["Y"].astype(np.float64), normals=g["YN"].astype(np.float64))
@@ -165,3 +166,24 @@ def test_em64_matches_f32_statistics_at_scale(fr):
     scale = np.array([mass] + [mass * rad] * 3 + [mass * rad ** 2] * 6 + [mass * sigma] * 3
                      + [mass * rad * sigma] * 9 + [mass * sigma ** 2] * 3)
     assert np.all(np.abs(s32 - s64) <= 1e-5 * scale), np.max(np.abs(s32 - s64) / scale)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"], indirect=True)
+def test_point_to_plane_extra_gauss_newton(fr, precision):
+    """max_gn_iters = 3 point-to-plane (mstep.py:421-459: re-assembly at the
+    accepted pose with the E step's spec): the float64 device loop and the
+    host-driven float32 loop against the live reference."""
+    g = load("gn3_pt2pl")
+    ref = fr.PointCloud(g["X"].astype(np.float64), normals=g["N"].astype(np.float64))
+    obs = fr.PointCloud(g["Y"].astype(np.float64), normals=g["YN"].astype(np.float64))
+    cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=float(g["sigma"]), outlier_ratio=0.1),
+                                residual_mode="point_to_plane", max_em_iters=int(g["max_iters"]),
+                                twist_tolerance=1e-4,
+                                mstep=fr.MStepOptions(max_gn_iters=int(g["max_gn_iters"])))
+    res = fr.register(ref, obs, fr.RigidModel(), cfg)
+    assert_pose(res.kinematics.pose.rotation, res.kinematics.pose.translation, g["R"], g["t"],
+                O.bbox_diameter(ref.positions))
+    assert abs(res.iterations - int(g["iterations"])) <= 1
+    k = min(len(res.objectives), len(g["objectives"])) - 1
+    np.testing.assert_allclose(res.objectives[:k], g["objectives"][:k],
+                               rtol=1e-7 if precision == "f64" else 1e-4)

@@ -1,0 +1,67 @@
+"""A fixed launch sequence of the float64 EM loop for ncu / compute-sanitizer:
+setup at P points, then (1) one warm-up 50-iteration registration, (2) the
+50-iteration registration to capture (launch index 1 of k_em64), (3) one
+pass-only launch (index 2).  Optional: the float32 device loop and the batch
+driver on small problems (sanitizer coverage of the cluster / last-block /
+cp.async-ring kernels).
+
+    python tools/em64_capture.py [points] [--iters N] [--f32] [--batch]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1811_10136_b200 as fr  # noqa: E402
+from oracle import filterreg_oracle as O  # noqa: E402  (input generator)
+from paper_1811_10136_b200 import _rigid  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("points", type=int, nargs="?", default=1_000_000)
+ap.add_argument("--iters", type=int, default=50)
+ap.add_argument("--f32", action="store_true")
+ap.add_argument("--batch", action="store_true")
+a = ap.parse_args()
+torch.cuda.set_device(0)
+model, obs, _ = O.pebble_pair(a.points, outlier_ratio=0.05, seed=0)
+X = model.astype(np.float32).astype(float)
+Y = obs.astype(np.float32).astype(float)
+gmm = fr.GmmConfig(sigma=0.05 * O.bbox_diameter(X[:a.points]), outlier_ratio=0.1)
+cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=a.iters, twist_tolerance=1e-30)
+path = _rigid.RigidDevicePath(fr.PointCloud(X), fr.PointCloud(Y), gmm, "point_to_point",
+                              precision="f64")
+for _ in range(2):
+    em = _rigid.DeviceEM64(path, np.eye(3), np.zeros(3), cfg)
+    em.run()
+    torch.cuda.synchronize()
+res = em.result()
+em.pass_only()
+torch.cuda.synchronize()
+print("f64 loop:", res[5], res[6], "R trace", float(np.trace(res[0])), flush=True)
+if a.f32:
+    p32 = _rigid.RigidDevicePath(fr.PointCloud(X), fr.PointCloud(Y), gmm, "point_to_point",
+                                 precision="f32")
+    e32 = _rigid.DeviceEM(p32, np.eye(3), np.zeros(3), cfg)
+    e32.run()
+    r32 = e32.result()
+    print("f32 loop:", r32[5], r32[6], flush=True)
+if a.batch:
+    probs = []
+    for seed in range(4):
+        m, o, _ = O.pebble_pair(3000, outlier_ratio=0.05, seed=seed)
+        probs.append((fr.PointCloud(m.astype(np.float32).astype(float)),
+                      fr.PointCloud(o.astype(np.float32).astype(float)), fr.RigidModel(),
+                      fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.05 * O.bbox_diameter(m[:3000]),
+                                                             outlier_ratio=0.1),
+                                            max_em_iters=30, twist_tolerance=2e-4)))
+    for prec in ("f64", "f32"):
+        old = _rigid.PRECISION
+        _rigid.PRECISION = prec
+        out = fr.register_batch(probs, max_concurrent=2)
+        _rigid.PRECISION = old
+        print("batch", prec, [r.iterations for r in out], flush=True)
+torch.cuda.synchronize()

@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (run in the build container).
 
-    python tools/ncu_summary.py <launches.csv> <pass.ncu-rep> [<other.ncu-rep> ...] --tag r01
+    python tools/ncu_summary.py <launches.csv> <capture.ncu-rep> [<other.ncu-rep> ...] --tag r02
 """
 import csv
 import io
@@ -28,7 +28,14 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
-       "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio"]
+       "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
+       "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+       "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+       "smsp__inst_executed.sum", "sm__cycles_elapsed.avg", "launch__grid_size",
+       "launch__block_size", "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+       "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+       "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum",
+       "lts__t_sectors_srcunit_tex_op_read.sum", "local_load_bytes", "local_store_bytes"]
 
 
 def launches(path):
@@ -47,26 +54,34 @@ def launches(path):
 
 
 def details(rep):
+    """Per captured launch: the WANT rows of the details page and the RAW
+    metrics (one dict per launch, in capture order)."""
     txt = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h = rows[0]
-    d = {}
+    per = defaultdict(dict)
     for r in rows[1:]:
         row = dict(zip(h, r))
+        key = row.get("ID", "0")
         if row.get("Metric Name") in WANT:
-            d[row["Metric Name"]] = f'{row["Metric Value"]} {row["Metric Unit"]}'.strip()
-            d["kernel"] = row.get("Kernel Name", "")[:120]
+            per[key][row["Metric Name"]] = f'{row["Metric Value"]} {row["Metric Unit"]}'.strip()
+            per[key]["kernel"] = row.get("Kernel Name", "")[:120]
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
+    out = []
     if len(rr) > 2:
-        h, units, vals = rr[0], rr[1], rr[2]
-        for name in RAW:
-            if name in h:
-                i = h.index(name)
-                d[name] = f"{vals[i]} {units[i]}".strip()
-    return d
+        h, units = rr[0], rr[1]
+        for vals in rr[2:]:
+            key = vals[h.index("ID")] if "ID" in h else str(len(out))
+            d = dict(per.get(key, {}))
+            for name in RAW:
+                if name in h:
+                    i = h.index(name)
+                    d[name] = f"{vals[i]} {units[i]}".strip()
+            out.append(d)
+    return out
 
 
 def to_bytes(s):
@@ -77,22 +92,15 @@ def to_bytes(s):
 
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    tag = sys.argv[sys.argv.index("--tag") + 1] if "--tag" in sys.argv else "r01"
-    points = int(sys.argv[sys.argv.index("--points") + 1]) if "--points" in sys.argv else 16000000
-    args = [a for a in args if a not in (tag, str(points))]
-    summary = {"launches": launches(args[0]), "kernels": {}}
+    tag = sys.argv[sys.argv.index("--tag") + 1] if "--tag" in sys.argv else "r02"
+    args = [a for a in args if a != tag]
+    summary = {"launches": launches(args[0]), "captures": {}}
     for rep in args[1:]:
-        summary["kernels"][os.path.basename(rep)] = details(rep)
+        summary["captures"][os.path.basename(rep)] = details(rep)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu.json"), "w") as fh:
         json.dump(summary, fh, indent=1)
-    p = summary["kernels"].get(os.path.basename(args[1]), {})
-    if "dram__bytes_read.sum" in p:
-        dram = to_bytes(p["dram__bytes_read.sum"]) + to_bytes(p["dram__bytes_write.sum"])
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as fh:
-            json.dump({"rigid_pass": {"points": points, "dram_bytes": dram,
-                                      "source": f"profiles/{tag}_ncu.json"}}, fh, indent=1)
-    print(json.dumps(summary, indent=1)[:6000])
+    print(json.dumps(summary, indent=1)[:8000])
 
 
 if __name__ == "__main__":
