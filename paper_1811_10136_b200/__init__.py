@@ -30,6 +30,7 @@ from .permutohedral import (PermutohedralLattice, build_lattice, filter_augmente
 from .io import load_cloud, save_cloud
 from .pipeline import (RegistrationConfig, RegistrationResult, alignment_error, default_sigma,
                        log_likelihood, register, register_batch, update_magnitude)
+from .protocol import filterreg_protocol, ladder_result, register_ladder
 
 __version__ = "0.1.0"
 
@@ -41,7 +42,8 @@ __all__ = [
     "RigidTransform", "Skinning", "SolverError", "alignment_error", "apply_twist",
     "articulated_from_dict", "assemble_articulated", "assemble_nodegraph", "assemble_rigid",
     "bind_points_to_nodes", "build_lattice", "build_node_graph", "compute_moments",
-    "default_sigma", "filter_augmented", "forward_points", "gaussian_transform_bruteforce",
+    "default_sigma", "filter_augmented", "filterreg_protocol", "forward_points",
+    "gaussian_transform_bruteforce", "ladder_result", "register_ladder",
     "gn_solve", "load_articulated_model", "log_likelihood", "m_step", "objective",
     "outlier_constant", "load_cloud", "save_cloud", "register", "register_batch", "residuals_from_moments", "rotation_about_axis",
     "twist_exp", "update_magnitude", "update_sigma", "valid_lattice_key",

@@ -187,3 +187,31 @@ def test_point_to_plane_extra_gauss_newton(fr, precision):
     k = min(len(res.objectives), len(g["objectives"])) - 1
     np.testing.assert_allclose(res.objectives[:k], g["objectives"][:k],
                                rtol=1e-7 if precision == "f64" else 1e-4)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"], indirect=True)
+def test_sigma_ladder_protocol(fr, precision):
+    """The reference bench's coarse-to-fine width ladder (bench.py:66-110) on a
+    corrupted pebble trial (10k + 20 % outliers), warm-started rungs with a
+    lattice rebuild per rung, against the live reference's per-rung traces."""
+    g = load("ladder_p10k")
+    n, seed = int(g["n"]), int(g["seed"])
+    model, obs, _ = O.pebble_pair(n, rotation_degrees=50.0, translation_fraction=0.02,
+                                  outlier_ratio=float(g["outlier_ratio"]), seed=seed)
+    X = model.astype(np.float32).astype(np.float64)
+    Y = obs.astype(np.float32).astype(np.float64)
+    diameter = float(g["diameter"])
+    assert abs(O.bbox_diameter(X[:n]) - diameter) <= 1e-15 * diameter
+    rungs = fr.filterreg_protocol(True, diameter, outliers=True)
+    assert [c for _, c, _ in rungs] == list(g["caps"])
+    out = fr.register_ladder(fr.PointCloud(X), fr.PointCloud(Y), rungs)
+    extent = O.bbox_diameter(X)
+    for k, res in enumerate(out):
+        assert abs(res.iterations - int(g["rung_iterations"][k])) <= 1, k
+        assert res.termination == str(g["rung_terminations"][k])
+        assert_pose(res.kinematics.pose.rotation, res.kinematics.pose.translation,
+                    g["rung_R"][k], g["rung_t"][k], extent)
+    full = fr.ladder_result(out)
+    k = min(len(full.objectives), len(g["objectives"]))
+    np.testing.assert_allclose(full.objectives[:k][:60], g["objectives"][:k][:60],
+                               rtol=1e-7 if precision == "f64" else 1e-4)
