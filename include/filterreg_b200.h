@@ -411,6 +411,46 @@ int fr_em64pl_result(fr_em64pl *em, double *R, double *t, double *objectives,
                      double *twist_norms, double *inlier_masses, int *iterations,
                      int *termination, void *stream);
 
+/* ---- device-resident articulated EM loop (pipeline.py:125-181 with an
+ * ArticulatedTree, point_to_point; mstep.py:213-229, 348-369, 421-459;
+ * kinematics.py:76-229) -------------------------------------------------
+ * The tree as plain arrays (host memory): parent index per body (-1 for the
+ * root), joint kind (0 fixed, 1 revolute, 2 prismatic), movable slot (joint
+ * value index, -1 for fixed), unit joint axis, parent-to-joint frame, and the
+ * body-frame centre of the body's points.  At most 32 bodies, 40 parameters.
+ * The body-sorted float32 planes and the chunk tables are those of
+ * fr_body_pass.  Per iteration (CUDA graph, no host round trip): the body
+ * pass over device-resident pass constants, per-body sums, then one CTA
+ * runs the M step -- per-body normal equations, forward kinematics, the
+ * projected (6 + joints)^2 system, damped Cholesky with tenfold escalation,
+ * closed-form halving candidates, extra GN iterations, update magnitude,
+ * termination and the next pass constants. */
+typedef struct fr_art_tree_desc {
+    int n_bodies, n_params, floating;
+    const int32_t *parent, *kind, *slot;
+    const double *axis, *frame_R, *frame_t, *c_body;
+} fr_art_tree_desc;
+typedef struct fr_art_em fr_art_em;
+
+/* the device pass of the loop: per-body statistics at device-resident pass
+ * constants (d_bodies), no-op once *d_done is set */
+int fr_body_pass_dev(const fr_lattice *lat, const float *d_ref, int64_t m, const void *d_bodies,
+                     int n_bodies, const int32_t *d_chunk_body, const int64_t *d_chunk_beg,
+                     int n_chunks, const int32_t *d_body_chunks, int flags, double *d_sums,
+                     double *d_scratch, const int32_t *d_done, void *stream);
+int fr_art_em_create(const fr_lattice *lat, const float *d_ref, int64_t m,
+                     const fr_art_tree_desc *tree, const double *q0, const double *base_R0,
+                     const double *base_t0, const double *body_R0, const double *body_t0,
+                     const int32_t *d_chunk_body, const int64_t *d_chunk_beg, int n_chunks,
+                     const int32_t *d_body_chunks, const fr_rigid_em_config *cfg, void *stream,
+                     fr_art_em **out);
+int fr_art_em_destroy(fr_art_em *em);
+int fr_art_em_run(fr_art_em *em, void *stream);
+/* q: >= 40 doubles (joint values in slot order) */
+int fr_art_em_result(fr_art_em *em, double *q, double *base_R, double *base_t,
+                     double *objectives, double *twist_norms, double *inlier_masses,
+                     int *iterations, int *termination, void *stream);
+
 /* float64 counterparts of the point helpers above: (n, 3) host rows ->
  * (3, n) float64 device planes (a transpose, no rounding); splat of
  * [1, y, (|y|^2), (n)] from float64 planes; Morton reorder of float64 planes */

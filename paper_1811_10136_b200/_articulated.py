@@ -210,6 +210,110 @@ def _body_motion(cur, cand):
     return D, tc - np.einsum("bij,bj->bi", D, tb)
 
 
+class ArtTreeDesc(ctypes.Structure):
+    """fr_art_tree_desc (include/filterreg_b200.h)."""
+    _fields_ = [("n_bodies", ctypes.c_int), ("n_params", ctypes.c_int),
+                ("floating", ctypes.c_int), ("parent", ctypes.c_void_p),
+                ("kind", ctypes.c_void_p), ("slot", ctypes.c_void_p),
+                ("axis", ctypes.c_void_p), ("frame_R", ctypes.c_void_p),
+                ("frame_t", ctypes.c_void_p), ("c_body", ctypes.c_void_p)]
+
+
+MAX_DEVICE_BODIES, MAX_DEVICE_PARAMS = 32, 40
+
+
+def device_loop_fits(tree) -> bool:
+    return tree.n_bodies <= MAX_DEVICE_BODIES and tree.n_params <= MAX_DEVICE_PARAMS
+
+
+class DeviceArtEM:
+    """The device-resident articulated point-to-point EM loop (fr_art_em_*):
+    per iteration the body pass, per-body sums and a one-CTA M step (forward
+    kinematics, projection, damped Cholesky, closed-form halving) replayed
+    from a CUDA graph; the host only reads the termination flag."""
+
+    KINDS = {"fixed": 0, "revolute": 1, "prismatic": 2}
+
+    def __init__(self, path: ArticulatedDevicePath, tree, config):
+        from . import _rigid
+        self.path, self.lib, self.tree = path, path.lib, tree
+        self.max_iters = int(config.max_em_iters)
+        tp = tree._topo
+        nb = tree.n_bodies
+        slot = np.full(nb, -1, dtype=np.int32)
+        for s_, i in enumerate(tp.movable):
+            slot[i] = s_
+        self._arrays = dict(
+            parent=np.asarray(tp.parent, dtype=np.int32),
+            kind=np.asarray([self.KINDS[b.joint.kind] for b in tp.bodies], dtype=np.int32),
+            slot=slot, axis=np.ascontiguousarray(tp.axis, dtype=float),
+            frame_R=np.ascontiguousarray(tp.FR.reshape(nb, 9), dtype=float),
+            frame_t=np.ascontiguousarray(tp.Ft, dtype=float),
+            c_body=np.ascontiguousarray(path.c_body, dtype=float))
+        a = self._arrays
+        desc = ArtTreeDesc(nb, tree.n_params, int(tree.floating),
+                           *[a[k].ctypes.data for k in ("parent", "kind", "slot", "axis",
+                                                         "frame_R", "frame_t", "c_body")])
+        c = _lib.RigidEmConfig()
+        c.sigma_inv[:] = list(1.0 / np.asarray(path.sigma, dtype=float))
+        c.c_prime = path.c_prime
+        c.diameter = path.diameter
+        c.twist_tolerance = float(config.twist_tolerance)
+        ms = config.mstep
+        c.damping = -1.0 if ms.damping is None else float(ms.damping)
+        c.step_tolerance = float(ms.step_tolerance)
+        c.degenerate_mass = 1e-9 * path.M_total
+        c.max_em_iters = self.max_iters
+        c.max_gn_iters = int(ms.max_gn_iters)
+        c.max_halvings = int(ms.max_halvings)
+        c.fast = _lib.FR_PASS_FAST if FAST_QUERY else 0
+        q0 = np.ascontiguousarray(tree.joint_values, dtype=float)
+        bR = np.ascontiguousarray(tree.base_pose.rotation, dtype=float)
+        bt = np.ascontiguousarray(tree.base_pose.translation, dtype=float)
+        WR, Wt = tree.world_arrays()
+        WR = np.ascontiguousarray(WR, dtype=float)
+        Wt = np.ascontiguousarray(Wt, dtype=float)
+        dp = lambda v: v.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.fr_art_em_create(
+            path.lattice.handle, _lib.ptr(path.ref), path.M, ctypes.byref(desc),
+            dp(q0) if len(q0) else None, dp(bR), dp(bt), dp(WR), dp(Wt),
+            _lib.ptr(path.chunk_body), _lib.ptr(path.chunk_beg), path.n_chunks,
+            _lib.ptr(path.body_chunks), ctypes.byref(c), _lib.stream_handle(), ctypes.byref(h)))
+        self.h = h
+        del _rigid
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.fr_art_em_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def run(self) -> None:
+        _lib.check(self.lib.fr_art_em_run(self.h, _lib.stream_handle()))
+
+    def result(self):
+        from .geometry import RigidTransform
+        n = self.max_iters
+        q = np.zeros(40)
+        bR, bt = np.zeros(9), np.zeros(3)
+        obj, tn, ms = np.zeros(n), np.zeros(n), np.zeros(n)
+        it, term = ctypes.c_int(), ctypes.c_int()
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        _lib.check(self.lib.fr_art_em_result(self.h, dp(q), dp(bR), dp(bt), dp(obj), dp(tn),
+                                             dp(ms), ctypes.byref(it), ctypes.byref(term),
+                                             _lib.stream_handle()))
+        k = min(int(it.value), n)
+        nq = len(self.tree.joint_values)
+        tree = self.tree.with_joint_values(q[:nq].copy(),
+                                           base_pose=RigidTransform(bR.reshape(3, 3), bt.copy()))
+        return tree, list(obj[:k]), list(tn[:k]), list(ms[:k]), int(it.value), \
+            _lib.FR_TERM[int(term.value)]
+
+
 def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
     """One M step of an articulated tree from per-body pass statistics
     (mstep.py:421-459 with assemble_articulated, mstep.py:213-229)."""
@@ -227,7 +331,8 @@ def articulated_m_step(path: ArticulatedDevicePath, sums, tree, s2, opts):
         Hb = np.stack([unpack_upper6(sums[b, 1:22]) for b in range(nb)])
         gb = np.asarray(sums[:, 22:28], dtype=float)
         if opts.max_gn_iters > 1:
-            raise NotImplementedError("point_to_plane with max_gn_iters > 1 is not in this build")
+            raise ValueError("point_to_plane with max_gn_iters > 1 and a process_group: the "
+                             "explicit-spec m_step path runs on one GPU")
     diag.objectives.append(value)
 
     def system(tr):

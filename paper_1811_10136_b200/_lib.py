@@ -41,6 +41,8 @@ EXPORTED = (
     "fr_lattice_dense_cells64",
     "fr_em64pl_create", "fr_em64pl_destroy", "fr_em64pl_run", "fr_em64pl_sums",
     "fr_em64pl_launch_info", "fr_em64pl_status", "fr_em64pl_result",
+    "fr_body_pass_dev", "fr_art_em_create", "fr_art_em_destroy", "fr_art_em_run",
+    "fr_art_em_result",
 )
 
 
@@ -139,6 +141,13 @@ _SIGS = {
     "fr_upload_points64": ([_P, _L, _P, _P], _I),
     "fr_em64pl_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),
     "fr_em64pl_destroy": ([_P], _I),
+    "fr_body_pass_dev": ([_P, _P, _L, _P, _I, _P, _P, _I, _P, _I, _P, _P, _P, _P], _I),
+    "fr_art_em_create": ([_P, _P, _L, _P, _DP, _DP, _DP, _DP, _DP, _P, _P, _I, _P,
+                          ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),
+    "fr_art_em_destroy": ([_P], _I),
+    "fr_art_em_run": ([_P, _P], _I),
+    "fr_art_em_result": ([_P, _DP, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I),
+                          ctypes.POINTER(_I), _P], _I),
     "fr_em64pl_run": ([_P, _I, _P], _I),
     "fr_em64pl_sums": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_I)], _I),
     "fr_em64pl_launch_info": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),

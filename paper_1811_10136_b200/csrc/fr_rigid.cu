@@ -1031,9 +1031,10 @@ __global__ void __launch_bounds__(kPassThreads, MODE == FR_POINT_TO_POINT ? 2 : 
 k_body_pass(const float *__restrict__ ref, long long m, const RigidK *__restrict__ bodies,
             const int *__restrict__ chunk_body, const long long *__restrict__ chunk_beg,
             SliceTable tab, SliceTableF tabf, float *__restrict__ wtn,
-            double *__restrict__ partials) {
+            double *__restrict__ partials, const int *done = nullptr) {
     constexpr int NA = (MODE == FR_POINT_TO_POINT ? kP2PtBase : kP2PlBase) + (SIG ? 2 : 0);
     __shared__ RigidK k;
+    if (done && *done) return;      // device-resident articulated loop finished
     const long long beg = chunk_beg[blockIdx.x], end = chunk_beg[blockIdx.x + 1];
     if (threadIdx.x == 0) k = bodies[chunk_body[blockIdx.x]];
     __syncthreads();
@@ -1050,9 +1051,10 @@ k_body_pass(const float *__restrict__ ref, long long m, const RigidK *__restrict
 }
 
 // per-segment column sums: segment s = chunks [seg[s], seg[s+1]), fixed order
-__global__ void k_reduce_segments(const double *partials, const int *seg, int na, double *out) {
+__global__ void k_reduce_segments(const double *partials, const int *seg, int na, double *out,
+                                  const int *done = nullptr) {
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31, s = blockIdx.x;
-    if (c >= na) return;
+    if (c >= na || (done && *done)) return;
     double v = 0.0;
     for (int b = seg[s] + lane; b < seg[s + 1]; b += 32) v += partials[(long long)b * na + c];
 #pragma unroll
@@ -1655,6 +1657,35 @@ int fr_body_pass(const fr_lattice *lat, const float *ref, int64_t m, const fr_bo
     FR_CHECK_LAUNCH();
     // the host copy of the params must outlive the async copy
     FR_CUDA(cudaStreamSynchronize(s));
+    return FR_OK;
+}
+
+// the body pass over device-resident per-body pass constants (RigidK records
+// maintained by the articulated device solve), no host copy or sync; a no-op
+// once *d_done is set.  point_to_point, 4 value columns.
+int fr_body_pass_dev(const fr_lattice *lat, const float *ref, int64_t m, const void *d_bodies,
+                     int n_bodies, const int32_t *chunk_body, const int64_t *chunk_beg,
+                     int n_chunks, const int32_t *body_chunks, int flags, double *sums,
+                     double *scratch, const int32_t *d_done, void *stream) {
+    if (!lat || !lat->blurred || !ref || !d_bodies || n_bodies < 1 || n_chunks < 1 ||
+        !chunk_body || !chunk_beg || !body_chunks || !sums || !scratch || lat->nv != 4) {
+        set_error("invalid device articulated pass arguments");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const RigidK *kd = reinterpret_cast<const RigidK *>(d_bodies);
+    const long long *cb = reinterpret_cast<const long long *>(chunk_beg);
+    const bool fast = (flags & FR_PASS_FAST) && lat->fslots;
+    if (fast)
+        k_body_pass<0, 4, false, true><<<n_chunks, kPassThreads, 0, s>>>(
+            ref, m, kd, chunk_body, cb, lat->table(), lat->table_f(), nullptr, scratch, d_done);
+    else
+        k_body_pass<0, 4, false, false><<<n_chunks, kPassThreads, 0, s>>>(
+            ref, m, kd, chunk_body, cb, lat->table(), lat->table_f(), nullptr, scratch, d_done);
+    FR_CHECK_LAUNCH();
+    k_reduce_segments<<<n_bodies, 32 * kP2PtBase, 0, s>>>(scratch, body_chunks, kP2PtBase, sums,
+                                                          d_done);
+    FR_CHECK_LAUNCH();
     return FR_OK;
 }
 

@@ -25,6 +25,9 @@ from .mstep import (RESIDUAL_MODES, MStepDiagnostics, MStepOptions, NormalEquati
                     _accepts, gn_solve)
 
 DEGENERATE_MASS_FRACTION = 1e-9
+# articulated point-to-point trees run the device-resident M step (False: the
+# host loop over the device body pass)
+ARTICULATED_DEVICE_LOOP = True
 
 
 @dataclass(frozen=True)
@@ -316,9 +319,32 @@ def register(reference: PointCloud, observation: PointCloud, initial_model,
     if not (isinstance(initial_model, RigidModel) or articulated):
         raise TypeError(f"unsupported kinematic model {type(initial_model).__name__}")
     if articulated:
-        from ._articulated import ArticulatedDevicePath, articulated_m_step
+        from ._articulated import (ArticulatedDevicePath, DeviceArtEM, articulated_m_step,
+                                   device_loop_fits)
+        if (config.residual_mode == "point_to_plane" and config.mstep.max_gn_iters > 1
+                and process_group is None):
+            # extra GN iterations keep the E step's spec: the explicit-spec
+            # m_step path (mstep.py:421-459 with assemble_articulated)
+            return _register_generic(reference, observation, initial_model, config, timing)
         path = ArticulatedDevicePath(reference, observation, config.gmm, config.residual_mode,
                                      initial_model, process_group)
+        if (config.residual_mode == "point_to_point" and process_group is None
+                and not config.gmm.update_sigma and not config.record_states
+                and device_loop_fits(initial_model) and ARTICULATED_DEVICE_LOOP):
+            tick = time.perf_counter()
+            em = DeviceArtEM(path, initial_model, config)
+            em.run()
+            tree, objs, tnorms, masses, iters, term = em.result()
+            if timing is not None:
+                timing["e_step_s"] = timing.get("e_step_s", 0.0) + time.perf_counter() - tick
+                timing["m_step_s"] = timing.get("m_step_s", 0.0)
+                timing["iterations"] = iters
+            if term == "solver_error":
+                from .errors import SolverError
+                raise SolverError("normal equations not factorizable after damping escalation")
+            return RegistrationResult(kinematics=tree, iterations=iters, objectives=objs,
+                                      twist_norms=tnorms, inlier_masses=masses, sigmas=[],
+                                      termination=term, states=None)
     else:
         from . import _rigid
         pl = config.residual_mode == "point_to_plane"

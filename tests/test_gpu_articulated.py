@@ -84,3 +84,62 @@ def test_articulated_assembly_matches_reference_math(fr):
         bd += S[k].T @ gk
     np.testing.assert_allclose(Hd, H, rtol=1e-5, atol=1e-6 * np.abs(H).max())
     np.testing.assert_allclose(bd, b, rtol=1e-4, atol=1e-5 * np.abs(b).max())
+
+
+@pytest.mark.parametrize("case", ["two_link", "chain20"])
+def test_device_loop_matches_host_loop(fr, case, monkeypatch):
+    """The device-resident articulated M step (fr_art_em: forward kinematics,
+    projection, Cholesky, closed-form halving in one CTA) reproduces the host
+    loop over the same body pass: iterations, termination, joint values and
+    base pose to round-off (the two forward kinematics differ in last bits,
+    which the float32 ranks of the body pass can turn into a float32 ulp)."""
+    from paper_1811_10136_b200 import pipeline
+    g = np.load(os.path.join(GOLDEN, f"articulated_{case}.npz"))
+    cfg = json.loads(str(g["config"]))
+    config = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]),
+                                   max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"])
+    ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
+    dev = fr.register(ref, obs, tree_from_arrays(fr, g), config)
+    monkeypatch.setattr(pipeline, "ARTICULATED_DEVICE_LOOP", False)
+    host = fr.register(ref, obs, tree_from_arrays(fr, g), config)
+    assert dev.iterations == host.iterations and dev.termination == host.termination
+    assert np.abs(dev.kinematics.joint_values - host.kinematics.joint_values).max() < 1e-6
+    dR = O.rotation_angle(dev.kinematics.base_pose.rotation @ host.kinematics.base_pose.rotation.T)
+    assert dR < 1e-6
+    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-6)
+    np.testing.assert_allclose(dev.twist_norms, host.twist_norms, rtol=1e-4, atol=1e-6)
+
+
+def test_device_loop_extra_gauss_newton(fr, monkeypatch):
+    """max_gn_iters = 3 through the device M step (moved per-body statistics,
+    re-projected system) equals the host loop."""
+    from paper_1811_10136_b200 import pipeline
+    g = np.load(os.path.join(GOLDEN, "articulated_chain20.npz"))
+    cfg = json.loads(str(g["config"]))
+    config = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]),
+                                   max_em_iters=8, twist_tolerance=cfg["tol"],
+                                   mstep=fr.MStepOptions(max_gn_iters=3))
+    ref, obs = fr.PointCloud(g["X"]), fr.PointCloud(g["Y"])
+    dev = fr.register(ref, obs, tree_from_arrays(fr, g), config)
+    monkeypatch.setattr(pipeline, "ARTICULATED_DEVICE_LOOP", False)
+    host = fr.register(ref, obs, tree_from_arrays(fr, g), config)
+    assert dev.iterations == host.iterations
+    assert np.abs(dev.kinematics.joint_values - host.kinematics.joint_values).max() < 1e-6
+    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-6)
+
+
+def test_point_to_plane_extra_gauss_newton_against_reference(fr):
+    """Articulated point_to_plane with max_gn_iters = 3 (the explicit-spec
+    m_step path) against the live reference."""
+    g = np.load(os.path.join(GOLDEN, "config_gn3_chain6_pt2pl.npz"))
+    rest = tree_from_arrays(fr, g)
+    ref = fr.PointCloud(g["X"].astype(float), normals=g["N"].astype(float))
+    obs = fr.PointCloud(g["Y"].astype(float), normals=g["YN"].astype(float))
+    config = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.006, outlier_ratio=0.1),
+                                   residual_mode="point_to_plane", max_em_iters=15,
+                                   twist_tolerance=1e-5, mstep=fr.MStepOptions(max_gn_iters=3))
+    res = fr.register(ref, obs, rest, config)
+    assert abs(res.iterations - int(g["iterations"])) <= 1
+    assert np.abs(res.kinematics.joint_values - g["joint_values"]).max() <= 1e-4
+    dR = O.rotation_angle(res.kinematics.base_pose.rotation @ g["base_R"].T)
+    assert dR <= 1e-4
