@@ -451,6 +451,41 @@ int fr_art_em_result(fr_art_em *em, double *q, double *base_R, double *base_t,
                      double *objectives, double *twist_norms, double *inlier_masses,
                      int *iterations, int *termination, void *stream);
 
+/* ---- device-resident node-graph EM loop (pipeline.py:125-181 with a
+ * NodeGraph; mstep.py:232-369, 421-459; kinematics.py:254-346) -----------
+ * Inputs as fr_graph_pass / fr_graph_blocks (input-order float32 planes,
+ * skinning, gather lists and the co-skinned pair list pair_lo < pair_hi),
+ * plus the node positions, the ARAP edges, a bandwidth-reducing node order
+ * `pos` (node -> band position) with block bandwidth bw, per band slot
+ * (position i, offset d = 0..bw; slot i * (bw + 1) + d) the contribution
+ * list slot_ent[slot_ptr[s] .. slot_ptr[s + 1]) = (kind << 30) | index
+ * (kind 0: pair, 1: edge), per node its incident edges
+ * inc_ent[inc_ptr[v] ..] = edge << 1 | role (0: k, 1: l), and the initial
+ * node poses / dual quaternions.  Per iteration one CUDA graph: E pass and
+ * data blocks, the banded system with the ARAP term, block-banded Cholesky
+ * with the reference's damping escalation (the SuperLU solve of
+ * mstep.py:317-345), all halving candidates in one objective pass, the
+ * first accepted step, extra GN iterations under the stored spec, update
+ * magnitude and termination.  max_halvings <= 15, max_gn_iters <= 8.
+ * Termination 4 of fr_ng_em_result: a dual-quaternion blend degenerated. */
+typedef struct fr_ng_em fr_ng_em;
+
+int fr_ng_em_create(const fr_lattice *lat, const float *d_ref, int64_t m, const int32_t *d_sidx,
+                    const double *d_swt, int K, int n_nodes, const double *node_pos,
+                    const int32_t *edges, int n_edges, const int32_t *d_dptr,
+                    const int32_t *d_dent, const int32_t *d_pptr, const int32_t *d_pent,
+                    int n_pairs, const int32_t *pair_lo, const int32_t *pair_hi,
+                    const int32_t *pos, int bw, const int32_t *slot_ptr,
+                    const int32_t *slot_ent, int n_slot_ent, const int32_t *inc_ptr,
+                    const int32_t *inc_ent, const double *node_R, const double *node_t,
+                    const double *node_dq, int mode, double lambda_reg,
+                    const fr_rigid_em_config *cfg, void *stream, fr_ng_em **out);
+int fr_ng_em_destroy(fr_ng_em *em);
+int fr_ng_em_run(fr_ng_em *em, void *stream);
+int fr_ng_em_result(fr_ng_em *em, double *node_R, double *node_t, double *objectives,
+                    double *twist_norms, double *inlier_masses, int *iterations,
+                    int *termination, void *stream);
+
 /* float64 counterparts of the point helpers above: (n, 3) host rows ->
  * (3, n) float64 device planes (a transpose, no rounding); splat of
  * [1, y, (|y|^2), (n)] from float64 planes; Morton reorder of float64 planes */

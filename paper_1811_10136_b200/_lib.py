@@ -42,7 +42,7 @@ EXPORTED = (
     "fr_em64pl_create", "fr_em64pl_destroy", "fr_em64pl_run", "fr_em64pl_sums",
     "fr_em64pl_launch_info", "fr_em64pl_status", "fr_em64pl_result",
     "fr_body_pass_dev", "fr_art_em_create", "fr_art_em_destroy", "fr_art_em_run",
-    "fr_art_em_result",
+    "fr_art_em_result", "fr_ng_em_create", "fr_ng_em_destroy", "fr_ng_em_run", "fr_ng_em_result",
 )
 
 
@@ -145,6 +145,13 @@ _SIGS = {
     "fr_art_em_create": ([_P, _P, _L, _P, _DP, _DP, _DP, _DP, _DP, _P, _P, _I, _P,
                           ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),
     "fr_art_em_destroy": ([_P], _I),
+    "fr_ng_em_create": ([_P, _P, _L, _P, _P, _I, _I, _P, _P, _I, _P, _P, _P, _P, _I, _P, _P, _P,
+                         _I, _P, _P, _I, _P, _P, _P, _P, _P, _I, _D,
+                         ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),
+    "fr_ng_em_destroy": ([_P], _I),
+    "fr_ng_em_run": ([_P, _P], _I),
+    "fr_ng_em_result": ([_P, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I), ctypes.POINTER(_I),
+                         _P], _I),
     "fr_art_em_run": ([_P, _P], _I),
     "fr_art_em_result": ([_P, _DP, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I),
                           ctypes.POINTER(_I), _P], _I),

@@ -319,6 +319,118 @@ def nodegraph_m_step(path, g4, diag, off, graph, s2, opts):
     return current, diagn
 
 
+# the device-resident loop (fr_ng_em) for single-GPU fixed-width runs whose
+# node order keeps the block bandwidth within the factorisation's window
+DEVICE_LOOP = True
+MAX_DEVICE_BANDWIDTH = 24
+
+
+def band_structure(n, pair_lo, pair_hi, edges):
+    """Bandwidth-reducing node order (reverse Cuthill-McKee over the block
+    graph of co-skinned pairs and ARAP edges), the block bandwidth, the
+    per-band-slot contribution lists (pairs in pair order, then edges in
+    edge order) and the per-node incident-edge lists of fr_ng_em_create."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+    lo = np.concatenate([np.asarray(pair_lo, dtype=np.int64), edges[:, 0].astype(np.int64)])
+    hi = np.concatenate([np.asarray(pair_hi, dtype=np.int64), edges[:, 1].astype(np.int64)])
+    A = sp.csr_matrix((np.ones(2 * len(lo) + n),
+                       (np.concatenate([lo, hi, np.arange(n)]),
+                        np.concatenate([hi, lo, np.arange(n)]))), shape=(n, n))
+    order = np.asarray(reverse_cuthill_mckee(A, symmetric_mode=True), dtype=np.int64)
+    pos = np.empty(n, dtype=np.int64)
+    pos[order] = np.arange(n)
+    pa, pb = pos[lo], pos[hi]
+    bw = int(np.abs(pa - pb).max(initial=0))
+    W = bw + 1
+    slot = np.maximum(pa, pb) * W + np.abs(pa - pb)
+    kind = np.concatenate([np.zeros(len(pair_lo), dtype=np.int64),
+                           np.ones(len(edges), dtype=np.int64)])
+    index = np.concatenate([np.arange(len(pair_lo)), np.arange(len(edges))])
+    o = np.lexsort((index, kind, slot))
+    ent = ((kind[o] << 30) | index[o]).astype(np.int32)
+    counts = np.bincount(slot[o], minlength=n * W)
+    slot_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    ev = np.concatenate([edges[:, 0], edges[:, 1]]).astype(np.int64)
+    ee = np.concatenate([np.arange(len(edges)), np.arange(len(edges))])
+    role = np.concatenate([np.zeros(len(edges), dtype=np.int64),
+                           np.ones(len(edges), dtype=np.int64)])
+    o2 = np.lexsort((ee, ev))
+    inc_ent = ((ee[o2] << 1) | role[o2]).astype(np.int32)
+    inc_ptr = np.concatenate([[0], np.cumsum(np.bincount(ev, minlength=n))]).astype(np.int32)
+    return pos.astype(np.int32), bw, slot_ptr, ent, inc_ptr, inc_ent
+
+
+def register_nodegraph_device(path, graph, config, timing=None):
+    """The device-resident node-graph EM loop (fr_ng_em_*): per iteration
+    one CUDA graph of the E pass, the banded system with the ARAP term, the
+    block-banded damped Cholesky, all halving candidates, the first accepted
+    step, extra GN iterations, update magnitude and termination."""
+    import ctypes
+
+    from .pipeline import RegistrationResult
+    from .kinematics import NodeGraph
+    tick = time.perf_counter()
+    n = graph.n_nodes
+    edges = np.ascontiguousarray(np.asarray(graph.edges, dtype=np.int64).reshape(-1, 2))
+    lo = np.asarray(path.pair_lo, dtype=np.int64)
+    hi = np.asarray(path.pair_hi, dtype=np.int64)
+    pos, bw, slot_ptr, slot_ent, inc_ptr, inc_ent = band_structure(n, lo, hi, edges)
+    c = _lib.RigidEmConfig()
+    c.sigma_inv[:] = list(1.0 / np.asarray(path.sigma, dtype=float))
+    c.c_prime = path.c_prime
+    c.diameter = path.diameter
+    c.twist_tolerance = float(config.twist_tolerance)
+    ms = config.mstep
+    c.damping = -1.0 if ms.damping is None else float(ms.damping)
+    c.step_tolerance = float(ms.step_tolerance)
+    c.degenerate_mass = 1e-9 * path.M_total
+    c.max_em_iters = int(config.max_em_iters)
+    c.max_gn_iters = int(ms.max_gn_iters)
+    c.max_halvings = int(ms.max_halvings)
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)  # noqa: E731
+    f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    keep = dict(P=f64(graph.node_positions), E=i32(edges), lo=i32(lo), hi=i32(hi), pos=pos,
+                sp=slot_ptr, se=slot_ent, ip=inc_ptr, ie=inc_ent,
+                R=f64(graph.node_rotations.reshape(n, 9)), t=f64(graph.node_translations),
+                dq=f64(graph.dual_quaternions))
+    ptr = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    h = ctypes.c_void_p()
+    lib = path.lib
+    _lib.check(lib.fr_ng_em_create(
+        path.lattice.handle, _lib.ptr(path.ref), path.M, _lib.ptr(path.sidx), _lib.ptr(path.swt),
+        path.K, n, ptr(keep["P"]), ptr(keep["E"]), len(edges), _lib.ptr(path.dptr),
+        _lib.ptr(path.dent), _lib.ptr(path.pptr), _lib.ptr(path.pent), path.n_pairs,
+        ptr(keep["lo"]), ptr(keep["hi"]), ptr(keep["pos"]), bw, ptr(keep["sp"]),
+        ptr(keep["se"]), len(slot_ent), ptr(keep["ip"]), ptr(keep["ie"]), ptr(keep["R"]),
+        ptr(keep["t"]), ptr(keep["dq"]), path.mode, float(ms.lambda_reg), ctypes.byref(c),
+        _lib.stream_handle(), ctypes.byref(h)))
+    try:
+        _lib.check(lib.fr_ng_em_run(h, _lib.stream_handle()))
+        k = int(config.max_em_iters)
+        R, t = np.zeros((n, 9)), np.zeros((n, 3))
+        obj, tn, mass = np.zeros(k), np.zeros(k), np.zeros(k)
+        it, term = ctypes.c_int(), ctypes.c_int()
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        _lib.check(lib.fr_ng_em_result(h, dp(R), dp(t), dp(obj), dp(tn), dp(mass),
+                                       ctypes.byref(it), ctypes.byref(term),
+                                       _lib.stream_handle()))
+    finally:
+        lib.fr_ng_em_destroy(h)
+    if int(term.value) == 4:
+        raise DegenerateBlendError("blended real part vanished for some points")
+    iters = int(it.value)
+    kk = min(iters, k)
+    model = NodeGraph._with_poses(graph, R.reshape(n, 3, 3), t)
+    if timing is not None:
+        timing["e_step_s"] = timing.get("e_step_s", 0.0) + time.perf_counter() - tick
+        timing["m_step_s"] = timing.get("m_step_s", 0.0)
+        timing["iterations"] = iters
+    return RegistrationResult(kinematics=model, iterations=iters, objectives=list(obj[:kk]),
+                              twist_norms=list(tn[:kk]), inlier_masses=list(mass[:kk]),
+                              sigmas=[], termination=_lib.FR_TERM[int(term.value)], states=None)
+
+
 def register_nodegraph(reference, observation, graph, config, timing=None, process_group=None):
     """pipeline.py:125-181 for a NodeGraph model."""
     from .pipeline import DEGENERATE_MASS_FRACTION, RegistrationResult, update_magnitude
@@ -327,6 +439,14 @@ def register_nodegraph(reference, observation, graph, config, timing=None, proce
                          "correspondences")
     path = NodeGraphDevicePath(reference, observation, config.gmm, config.residual_mode, graph,
                                process_group)
+    ms = config.mstep
+    if (DEVICE_LOOP and process_group is None and not config.gmm.update_sigma
+            and not config.record_states and ms.max_halvings <= 15 and ms.max_gn_iters <= 8
+            and ms.solve_method in ("auto", "sparse")):
+        edges = np.asarray(graph.edges, dtype=np.int64).reshape(-1, 2)
+        bw = band_structure(graph.n_nodes, path.pair_lo, path.pair_hi, edges)[1]
+        if bw <= MAX_DEVICE_BANDWIDTH:
+            return register_nodegraph_device(path, graph, config, timing)
     model = graph
     sigma_current = path.sigma
     result = RegistrationResult(kinematics=model, iterations=0,

@@ -18,8 +18,11 @@
 // stay on the host, exactly as the reference forms them.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <vector>
 
 #include "fr_reduce.cuh"
+#include "fr_solve.cuh"
 
 namespace fr {
 
@@ -147,7 +150,8 @@ __global__ void __launch_bounds__(kPassThreads, 2)
 k_graph_pass(const float *__restrict__ ref, long long m, const int *__restrict__ sidx,
              const double *__restrict__ swt, const double *__restrict__ dq, GraphK g,
              SliceTable tab, double *__restrict__ rec, double *__restrict__ ete,
-             double *__restrict__ partials, int *bad) {
+             double *__restrict__ partials, int *bad, const int *skip = nullptr) {
+    if (skip && *skip) return;      // device-resident loop: stage not active
     double acc[kGraphAcc] = {0.0, 0.0, 0.0, 0.0};
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
@@ -233,7 +237,9 @@ __global__ void k_graph_blocks(const double *__restrict__ ete, const double *__r
                                int K, const int *__restrict__ dptr, const int *__restrict__ dent,
                                int n_nodes, const int *__restrict__ pptr,
                                const int *__restrict__ pent, int n_pairs,
-                               double *__restrict__ diag, double *__restrict__ off) {
+                               double *__restrict__ diag, double *__restrict__ off,
+                               const int *skip = nullptr) {
+    if (skip && *skip) return;
     const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (wg >= n_nodes + n_pairs) return;
     const bool is_diag = wg < n_nodes;
@@ -283,7 +289,9 @@ __global__ void __launch_bounds__(kPassThreads, 2)
 k_graph_objective(const float *__restrict__ ref, long long m, const int *__restrict__ sidx,
                   const double *__restrict__ swt, int K, const double *__restrict__ cand_dq,
                   int n_nodes, int ncand, const double *__restrict__ rec, int mode, double s0,
-                  double s1, double s2, double *__restrict__ partials, int *bad) {
+                  double s1, double s2, double *__restrict__ partials, int *bad,
+                  const int *skip = nullptr) {
+    if (skip && *skip) return;
     double acc[kGraphMaxCand];
 #pragma unroll
     for (int a = 0; a < kGraphMaxCand; ++a) acc[a] = 0.0;
@@ -340,6 +348,747 @@ __global__ void k_point_rows(const double *__restrict__ X, const double *__restr
     double e[kGraphEte];
     point_rows(mode, sinv, W[p], x, t, n, e);
     for (int q = 0; q < kGraphEte; ++q) ete[p * kGraphEte + q] = e[q];
+}
+
+
+// ===========================================================================
+// Device-resident node-graph EM (pipeline.py:125-181 with a NodeGraph;
+// mstep.py:232-369, 421-459): per EM iteration a fixed kernel sequence,
+// replayed from a CUDA graph with no host round trip --
+//   k_graph_pass / k_graph_blocks    E step + per-node / per-pair data blocks
+//   k_ng_assemble                    data blocks + the ARAP term (mstep.py:
+//                                    290-314, node-only, fixed order per
+//                                    block) into a block-banded matrix over a
+//                                    bandwidth-reducing node order (RCM),
+//                                    objective, degenerate check
+//   k_ng_factor (one CTA)            (A + lam I) x = b by a block-banded
+//                                    Cholesky with the reference's damping
+//                                    and tenfold escalation (replaces SuperLU,
+//                                    mstep.py:317-345: same solution to
+//                                    round-off)
+//   k_ng_cands                       the full step and every halving as
+//                                    candidate node states (per-node
+//                                    exp(twist) o T with polar factor) and
+//                                    their dual quaternions
+//   k_graph_objective                data objectives of all candidates (one
+//                                    pass over the stored spec)
+//   k_ng_select                      + ARAP objectives, first accepted step,
+//                                    state update; extra GN iterations repeat
+//                                    the stages under the stored spec
+//   k_ng_finish                      update magnitude, termination, traces.
+// Stages whose skip flag is set return at once (finished loop / finished
+// Gauss-Newton iterations).
+
+constexpr int kNgThreads = 1024;
+constexpr int kNgMaxCand = 16;
+enum { kNgTermBlend = 4 };
+
+struct NgDev {
+    double sinv[3], cp, diameter, tol, damping, step_tol, degenerate_mass, lambda;
+    int n, n_edges, bw, max_em_iters, max_gn_iters, max_halvings, use_damping, mode;
+    int done, iterations, termination, gn_skip;
+    int gn, ncand, mstep_ran, accepted;
+    double value, value0, arap0, sn;
+};
+
+struct NgBufs {
+    NgDev *st;
+    double *R, *T, *DQ;            // node state (n x 9, 3, 8)
+    double *R0, *T0, *DQ0;         // at the start of the M step
+    const double *P;               // node positions n x 3
+    const int *edges;              // E x 2
+    const int *pos;                // node -> band position
+    const int *node_at;            // band position -> node
+    const int *slot_ptr, *slot_ent;   // per band slot: (kind << 30) | index (kind 0 pair, 1 edge)
+    const int *inc_ptr, *inc_ent;     // per node: incident edges (edge << 1 | role: 0 = k, 1 = l)
+    const int *pair_lo, *pair_hi;
+    const double *gsums;           // E pass sums (objective, mass, ...)
+    const double *diag, *off;      // data blocks (n x 27, pairs x 21)
+    double *band, *bvec;           // assembled system: band [n][bw+1][36], b [n][6] (positions)
+    double *L, *x, *step;          // factor, solution (positions), step (node order, 6n)
+    double *candR, *candT, *candDQ;   // [16][n][9 / 3 / 8]
+    const double *cand_data;       // 16 data objectives
+    double *traces;                // [3][max_iters]
+    int *flag;                     // degenerate blend flag of the passes
+};
+
+__device__ __forceinline__ void ng_jac(const double *x, double J[3][6]) {
+    // point_twist_jacobian: [-[x]x | I]
+    J[0][0] = 0.0;   J[0][1] = x[2];  J[0][2] = -x[1]; J[0][3] = 1.0; J[0][4] = 0.0; J[0][5] = 0.0;
+    J[1][0] = -x[2]; J[1][1] = 0.0;   J[1][2] = x[0];  J[1][3] = 0.0; J[1][4] = 1.0; J[1][5] = 0.0;
+    J[2][0] = x[1];  J[2][1] = -x[0]; J[2][2] = 0.0;   J[2][3] = 0.0; J[2][4] = 0.0; J[2][5] = 1.0;
+}
+
+__device__ __forceinline__ void ng_apply(const double *R, const double *t, const double *p,
+                                         double *x) {
+    for (int i = 0; i < 3; ++i) x[i] = R[3 * i] * p[0] + R[3 * i + 1] * p[1] + R[3 * i + 2] * p[2] + t[i];
+}
+
+// the ARAP rows of edge e at endpoint position p: xk, xl, r = sqrt(lam) (xk - xl)
+__device__ __forceinline__ void ng_arap_rows(const NgBufs &b, int e, int which, const double *R,
+                                             const double *T, double *xk, double *xl,
+                                             double *r) {
+    const int k = b.edges[2 * e], l = b.edges[2 * e + 1];
+    const double *p = b.P + 3 * (which == 0 ? l : k);   // (node_positions[l], then [k])
+    ng_apply(R + 9 * k, T + 3 * k, p, xk);
+    ng_apply(R + 9 * l, T + 3 * l, p, xl);
+    const double root = sqrt(b.st->lambda);
+    for (int i = 0; i < 3; ++i) r[i] = root * (xk[i] - xl[i]);
+}
+
+// rigid pose -> unit dual quaternion [real | dual] (Shepperd, w >= 0; geometry.py:243-283)
+__device__ void ng_dq(const double *R, const double *t, double *dq) {
+    const double tr = (R[0] + R[4]) + R[8];
+    double q[4];
+    if (tr > 0) {
+        const double s = 2.0 * sqrt(tr + 1.0);
+        q[0] = 0.25 * s;
+        q[1] = (R[7] - R[5]) / s;
+        q[2] = (R[2] - R[6]) / s;
+        q[3] = (R[3] - R[1]) / s;
+    } else {
+        int i = 0;
+        if (R[4] > R[0]) i = 1;
+        if (R[8] > R[3 * i + i]) i = 2;
+        const int j = (i + 1) % 3, k = (i + 2) % 3;
+        const double s = 2.0 * sqrt(R[3 * i + i] - R[3 * j + j] - R[3 * k + k] + 1.0);
+        q[0] = (R[3 * k + j] - R[3 * j + k]) / s;
+        q[1 + i] = 0.25 * s;
+        q[1 + j] = (R[3 * j + i] + R[3 * i + j]) / s;
+        q[1 + k] = (R[3 * k + i] + R[3 * i + k]) / s;
+    }
+    if (q[0] < 0) for (int c = 0; c < 4; ++c) q[c] = -q[c];
+    const double nq = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+    for (int c = 0; c < 4; ++c) q[c] /= nq;
+    // dual = 0.5 (0, t) q
+    const double a1 = 0.0, b1 = t[0], c1 = t[1], d1 = t[2];
+    const double a2 = q[0], b2 = q[1], c2 = q[2], d2 = q[3];
+    const double qd[4] = {a1 * a2 - b1 * b2 - c1 * c2 - d1 * d2, a1 * b2 + b1 * a2 + c1 * d2 - d1 * c2,
+                          a1 * c2 - b1 * d2 + c1 * a2 + d1 * b2, a1 * d2 + b1 * c2 - c1 * b2 + d1 * a2};
+    for (int c = 0; c < 4; ++c) {
+        dq[c] = q[c];
+        dq[4 + c] = 0.5 * qd[c];
+    }
+}
+
+// the assembled system at the current node state: data blocks + ARAP
+// (mstep.py:290-314), banded over the node order `pos`; first = 1 also runs
+// the E-step bookkeeping (mass, degenerate test, objective, M-step start)
+constexpr int kNgAsmThreads = 128;
+
+// E-step bookkeeping (first = 1: mass, degenerate test, the M step's start
+// state) and the objective value0 = data + ARAP at the current node state
+__global__ void __launch_bounds__(kNgThreads, 1) k_ng_begin(NgBufs b, int first) {
+    NgDev *st = b.st;
+    if (first ? st->done : st->gn_skip) return;
+    __shared__ double red[kNgThreads / 32];
+    __shared__ int bad;
+    const bool reg = st->lambda > 0.0 && st->n_edges > 0;
+    if (first) {
+        if (threadIdx.x == 0) {
+            bad = 0;
+            const int it = st->iterations;
+            const double mass = b.gsums[1];
+            b.traces[2 * st->max_em_iters + it] = mass;
+            st->mstep_ran = 0;
+            if (*b.flag) {
+                st->termination = kNgTermBlend;
+                st->done = 1;
+                bad = 1;
+            } else if (mass < st->degenerate_mass) {       // pipeline.py:148-154
+                b.traces[it] = CUDART_NAN;
+                b.traces[st->max_em_iters + it] = CUDART_NAN;
+                st->iterations = it + 1;
+                st->termination = kTermDegenerate;
+                st->done = 1;
+                bad = 1;
+            }
+        }
+        __syncthreads();
+        if (bad) {
+            if (threadIdx.x == 0) st->gn_skip = 1;
+            return;
+        }
+        for (int q = threadIdx.x; q < st->n; q += blockDim.x) {
+            for (int c = 0; c < 9; ++c) b.R0[9 * q + c] = b.R[9 * q + c];
+            for (int c = 0; c < 3; ++c) b.T0[3 * q + c] = b.T[3 * q + c];
+            for (int c = 0; c < 8; ++c) b.DQ0[8 * q + c] = b.DQ[8 * q + c];
+        }
+    }
+    // the regulariser objective at the current state (mstep.py:386-401)
+    double part = 0.0;
+    if (reg)
+        for (int e2 = threadIdx.x; e2 < 2 * st->n_edges; e2 += blockDim.x) {
+            double xk[3], xl[3], rr[3];
+            ng_arap_rows(b, e2 >> 1, e2 & 1, b.R, b.T, xk, xl, rr);
+            part += 0.5 * ((rr[0] * rr[0] + rr[1] * rr[1]) + rr[2] * rr[2]);
+        }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0 && first) {
+        double arap = 0.0;
+        for (int w = 0; w < (int)(blockDim.x / 32); ++w) arap += red[w];
+        st->value0 = st->value = b.gsums[0] + arap;
+        st->gn = 0;
+        st->gn_skip = 0;
+        st->mstep_ran = 1;
+    }
+}
+
+// the assembled system at the current node state: data blocks + ARAP
+// (mstep.py:290-314), banded over the node order `pos`, one thread per band
+// slot, each slot's contributions in a fixed order
+__global__ void __launch_bounds__(kNgAsmThreads) k_ng_assemble(NgBufs b) {
+    NgDev *st = b.st;
+    if (st->gn_skip) return;
+    const int n = st->n, bw = st->bw, W = bw + 1;
+    const bool reg = st->lambda > 0.0 && st->n_edges > 0;
+    // per band slot (i, d): d = 0 -> node diagonal block + its incident ARAP
+    // terms; d > 0 -> the listed pair / edge blocks, in list order
+    for (int sidx = blockIdx.x * blockDim.x + threadIdx.x; sidx < n * W;
+         sidx += gridDim.x * blockDim.x) {
+        const int i = sidx / W, d = sidx % W;
+        double blk[36];
+        for (int q = 0; q < 36; ++q) blk[q] = 0.0;
+        if (d == 0) {
+            const int node = b.node_at[i];
+            const double *dg = b.diag + 27 * node;
+            int o = 0;
+            for (int r = 0; r < 6; ++r)
+                for (int c = r; c < 6; ++c) {
+                    blk[6 * r + c] = dg[o];
+                    blk[6 * c + r] = dg[o];
+                    ++o;
+                }
+            double g6[6];
+            for (int q = 0; q < 6; ++q) g6[q] = dg[21 + q];
+            if (reg) {
+                // reference order: for p in (P[l], P[k]): D += grouped(JkJk, k);
+                // D += grouped(JlJl, l) -- per node in edge order per sweep
+                for (int which = 0; which < 2; ++which)
+                    for (int role = 0; role < 2; ++role)
+                        for (int a = b.inc_ptr[node]; a < b.inc_ptr[node + 1]; ++a) {
+                            const int ent = b.inc_ent[a];
+                            if ((ent & 1) != role) continue;
+                            const int e = ent >> 1;
+                            double xk[3], xl[3], rr[3], J[3][6];
+                            ng_arap_rows(b, e, which, b.R, b.T, xk, xl, rr);
+                            const double root = sqrt(st->lambda);
+                            ng_jac(role == 0 ? xk : xl, J);
+                            const double sg = role == 0 ? root : -root;
+                            for (int r = 0; r < 6; ++r) {
+                                for (int c = 0; c < 6; ++c) {
+                                    double v = 0.0;
+                                    for (int q = 0; q < 3; ++q) v += (sg * J[q][r]) * (sg * J[q][c]);
+                                    blk[6 * r + c] += v;
+                                }
+                                double v = 0.0;
+                                for (int q = 0; q < 3; ++q) v += (sg * J[q][r]) * rr[q];
+                                g6[r] += v;
+                            }
+                        }
+            }
+            for (int q = 0; q < 6; ++q) b.bvec[6 * i + q] = g6[q];
+        } else if (i - d >= 0) {
+            const int j = i - d;
+            const int ni = b.node_at[i], nj = b.node_at[j];
+            for (int a = b.slot_ptr[sidx]; a < b.slot_ptr[sidx + 1]; ++a) {
+                const int ent = b.slot_ent[a];
+                const int kind = ent >> 30, idx = ent & 0x3fffffff;
+                double X[36];     // block A[row node][col node] of the contribution
+                int rn;
+                if (kind == 0) {
+                    const double *ob = b.off + 21 * idx;
+                    int o = 0;
+                    for (int r = 0; r < 6; ++r)
+                        for (int c = r; c < 6; ++c) {
+                            X[6 * r + c] = ob[o];
+                            X[6 * c + r] = ob[o];
+                            ++o;
+                        }
+                    rn = b.pair_lo[idx];
+                } else {
+                    // A[k][l] += Jk^T Jl over both endpoint positions
+                    for (int q = 0; q < 36; ++q) X[q] = 0.0;
+                    for (int which = 0; which < 2; ++which) {
+                        double xk[3], xl[3], rr[3], Jk[3][6], Jl[3][6];
+                        ng_arap_rows(b, idx, which, b.R, b.T, xk, xl, rr);
+                        const double root = sqrt(st->lambda);
+                        ng_jac(xk, Jk);
+                        ng_jac(xl, Jl);
+                        for (int r = 0; r < 6; ++r)
+                            for (int c = 0; c < 6; ++c) {
+                                double v = 0.0;
+                                for (int q = 0; q < 3; ++q) v += (root * Jk[q][r]) * (-root * Jl[q][c]);
+                                X[6 * r + c] += v;
+                            }
+                    }
+                    rn = b.edges[2 * idx];
+                }
+                // symmetric pair blocks are stored as the band's A[ni][nj]
+                const bool tr = rn != ni;
+                for (int r = 0; r < 6; ++r)
+                    for (int c = 0; c < 6; ++c) blk[6 * r + c] += tr ? X[6 * c + r] : X[6 * r + c];
+                (void)nj;
+            }
+        }
+        double *dst = b.band + (size_t)sidx * 36;
+        for (int q = 0; q < 36; ++q) dst[q] = blk[q];
+    }
+}
+
+// 6x6 in-place Cholesky (lower) of a diagonal block; false when not SPD
+// 6x6 Cholesky in registers (A row-major, lower triangle out, upper zeroed);
+// rd[j] = 1 / L_jj.  One column per template step so every index is a
+// compile-time constant and A stays in registers.
+template <int J>
+__device__ __forceinline__ bool chol6_col(double (&A)[36], double *rd) {
+    double d = A[6 * J + J];
+#pragma unroll
+    for (int k = 0; k < J; ++k) d -= A[6 * J + k] * A[6 * J + k];
+    const bool good = d > 0.0 && isfinite(d);
+    const double l = sqrt(fmax(d, 1e-300));
+    A[6 * J + J] = l;
+    const double r = 1.0 / l;
+    rd[J] = r;
+#pragma unroll
+    for (int i = J + 1; i < 6; ++i) {
+        double v = A[6 * i + J];
+#pragma unroll
+        for (int k = 0; k < J; ++k) v -= A[6 * i + k] * A[6 * J + k];
+        A[6 * i + J] = v * r;
+    }
+#pragma unroll
+    for (int c = J + 1; c < 6; ++c) A[6 * J + c] = 0.0;
+    return good;
+}
+
+__device__ __forceinline__ bool chol6_reg(double (&A)[36], double *rd) {
+    bool g = chol6_col<0>(A, rd);
+    g &= chol6_col<1>(A, rd);
+    g &= chol6_col<2>(A, rd);
+    g &= chol6_col<3>(A, rd);
+    g &= chol6_col<4>(A, rd);
+    g &= chol6_col<5>(A, rd);
+    return g;
+}
+
+// (A + lam I) x = b by a block-banded Cholesky with the damping escalation
+// of mstep.py:348-369; the step is -x in node order.  The active window --
+// block rows k .. k + bw -- lives in shared memory as a ring of block rows
+// (each row: its diagonal block and bw sub-diagonal blocks); row k leaves
+// the window final (written to L, its forward substitution done) and row
+// k + bw + 1 enters from the assembled band.  Every update of a row comes
+// from steps whose window holds it.
+constexpr int kNgMaxBw = 24;        // window rows x blocks x 36 doubles <= 227 KB
+constexpr int kNgFacThreads = 256;
+
+__global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
+    NgDev *st = b.st;
+    if (st->gn_skip) return;
+    extern __shared__ double win[];            // [W][W][36] ring of block rows
+    const int n = st->n, bw = st->bw, W = bw + 1, P = 6 * n;
+    const int tid = threadIdx.x, NT = blockDim.x;
+    __shared__ int ok, anyb;
+    __shared__ double s_trace, s_lam;
+    __shared__ double red[kNgFacThreads / 32];
+    __shared__ double rd[6];
+    __shared__ double yring[(kNgMaxBw + 2) * 6];   // y_j / x_j of the band's rows
+    __shared__ short pair_i[kNgMaxBw * (kNgMaxBw + 1) / 2], pair_j[kNgMaxBw * (kNgMaxBw + 1) / 2];
+    // (ii >= jj) pairs of the trailing triangle, enumerated once
+    if (tid == 0) {
+        int c = 0;
+        for (int ii = 0; ii < bw; ++ii)
+            for (int jj = 0; jj <= ii; ++jj) {
+                pair_i[c] = (short)ii;
+                pair_j[c] = (short)jj;
+                ++c;
+            }
+    }
+    int nz = 0;
+    double tr = 0.0;
+    for (int q = tid; q < P; q += NT) {
+        nz |= b.bvec[q] != 0.0;
+        const int i = q / 6, r = q % 6;
+        tr += b.band[(size_t)i * W * 36 + 6 * r + r];
+    }
+    nz = __syncthreads_or(nz);
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, o);
+    if ((tid & 31) == 0) red[tid >> 5] = tr;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += red[w];
+        s_trace = t;
+        s_lam = st->use_damping ? st->damping : 1e-6 * t / P;
+        anyb = nz;
+        if (!nz) st->gn_skip = 1;           // zero gradient: no step (mstep.py:429)
+    }
+    __syncthreads();
+    if (!anyb) return;
+    bool solved = false;
+#pragma unroll 1
+    for (int attempt = 0; attempt < 6 && !solved; ++attempt) {
+        const double lam = s_lam;
+        auto load_row = [&](int i) {
+            double *dst = win + (size_t)(i % W) * W * 36;
+            const double *src = b.band + (size_t)i * W * 36;
+            for (int e = tid; e < W * 36; e += NT) {
+                const int d = e / 36, q = e % 36;
+                dst[e] = src[e] + ((d == 0 && q / 6 == q % 6) ? lam : 0.0);
+            }
+        };
+        for (int i = 0; i < min(W, n); ++i) load_row(i);
+        // yring slot i % W: b_i, accumulating -L_ij y_j as the panels of the
+        // rows j < i are formed, then y_i
+        for (int e = tid; e < min(W, n) * 6; e += NT) yring[e] = b.bvec[e];
+        if (tid == 0) ok = 1;
+        __syncthreads();
+        constexpr int kPre = (kNgMaxBw + 1) * 36 / kNgFacThreads + 1;   // row elements per thread
+        int kw = 0;                                                     // k % W
+        for (int k = 0; k < n; ++k, kw = kw + 1 == W ? 0 : kw + 1) {
+            auto slot = [&](int off) { const int q = kw + off; return q >= W ? q - W : q; };
+            // the row entering after this step, loaded now (its latency hides
+            // behind the step's work)
+            double pre[kPre], bpre = 0.0;
+            const bool incoming = k + W < n;
+            if (incoming) {
+                const double *src = b.band + (size_t)(k + W) * W * 36;
+#pragma unroll
+                for (int u = 0; u < kPre; ++u) {
+                    const int e = tid + u * NT;
+                    pre[u] = e < W * 36 ? src[e] : 0.0;
+                }
+                if (tid < 6) bpre = b.bvec[6 * (k + W) + tid];
+            }
+            double *row_k = win + (size_t)kw * W * 36;
+            double *Lkk = row_k;
+            if (tid == 0) {
+                double a[36];
+#pragma unroll
+                for (int q = 0; q < 36; ++q) a[q] = Lkk[q];
+                if (!chol6_reg(a, rd)) {
+                    ok = 0;
+                } else {
+                    // y_k = L_kk^-1 b_k (b_k already holds -sum L_kj y_j)
+                    double *yk_ = yring + 6 * kw, y[6];
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) {
+                        double v = yk_[r];
+#pragma unroll
+                        for (int q = 0; q < r; ++q) v -= a[6 * r + q] * y[q];
+                        y[r] = v * rd[r];
+                    }
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) {
+                        yk_[r] = y[r];
+                        b.x[6 * k + r] = y[r];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 36; ++q) Lkk[q] = a[q];
+                }
+            }
+            __syncthreads();
+            if (!ok) break;
+            const int nrow = min(bw, n - 1 - k);
+            // panel: L_ik = A_ik L_kk^-T, one thread per row of a block, which
+            // also takes its row's share of the forward substitution
+            const double *yk_ = yring + 6 * kw;
+            for (int t = tid; t < nrow * 6; t += NT) {
+                const int off = 1 + t / 6, r = t % 6;
+                const int si = slot(off);
+                double *row = win + ((size_t)si * W + off) * 36 + 6 * r;
+                double v[6];
+#pragma unroll
+                for (int c = 0; c < 6; ++c) v[c] = row[c];
+                double dot = 0.0;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    double u = v[c];
+#pragma unroll
+                    for (int q = 0; q < c; ++q) u -= v[q] * Lkk[6 * c + q];
+                    v[c] = u * rd[c];
+                    dot += v[c] * yk_[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 6; ++c) row[c] = v[c];
+                yring[6 * si + r] -= dot;
+            }
+            __syncthreads();
+            // trailing update A_ij -= L_ik L_jk^T, one thread per (block pair,
+            // row half): 108 FMAs from registers
+            const int npairs = nrow * (nrow + 1) / 2;
+            for (int t = tid; t < 2 * npairs; t += NT) {
+                const int pr = t >> 1, h = t & 1;
+                const int oi = 1 + pair_i[pr], oj = 1 + pair_j[pr];
+                const int si = slot(oi), sj = slot(oj);
+                const double *Li = win + ((size_t)si * W + oi) * 36 + 18 * h;
+                const double *Lj = win + ((size_t)sj * W + oj) * 36;
+                double a[18], c6[36];
+#pragma unroll
+                for (int q = 0; q < 18; ++q) a[q] = Li[q];
+#pragma unroll
+                for (int q = 0; q < 36; ++q) c6[q] = Lj[q];
+                double *dst = win + ((size_t)si * W + (oi - oj)) * 36 + 18 * h;
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        double v = 0.0;
+#pragma unroll
+                        for (int q = 0; q < 6; ++q) v += a[6 * r + q] * c6[6 * c + q];
+                        dst[6 * r + c] -= v;
+                    }
+            }
+            // row k is final: keep it for the backward substitution
+            for (int e = tid; e < W * 36; e += NT) b.L[(size_t)k * W * 36 + e] = row_k[e];
+            __syncthreads();
+            if (incoming) {
+                double *dst = row_k;                       // (k + W) % W == k % W
+#pragma unroll
+                for (int u = 0; u < kPre; ++u) {
+                    const int e = tid + u * NT;
+                    if (e < W * 36) {
+                        const int d = e / 36, q = e % 36;
+                        dst[e] = pre[u] + ((d == 0 && q / 6 == q % 6) ? lam : 0.0);
+                    }
+                }
+                if (tid < 6) yring[6 * kw + tid] = bpre;
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (ok) {
+            // L^T x = y, right-looking: x_k = L_kk^-T y_k, then y_j -= L_kj^T x_k
+            // for the band's j < k (row k of L, one coalesced load per step)
+            // yring slot j % (W + 1) holds y_j for j in [k - W, k]: the band
+            // rows the step updates plus the one entering next (k - W, whose
+            // last update comes from step k - 1)
+            const int W1 = W + 1;
+            for (int e = tid; e < W * 6; e += NT) {
+                const int j = n - 1 - e / 6;
+                if (j >= 0) yring[(j % W1) * 6 + e % 6] = b.x[6 * j + e % 6];
+            }
+            // rows of L double-buffered in the (free) window: row k - 1 is
+            // loaded to registers during step k and stored at its end
+            for (int e = tid; e < W * 36; e += NT)
+                win[((n - 1) & 1) * W * 36 + e] = b.L[(size_t)(n - 1) * W * 36 + e];
+            __syncthreads();
+            int kw1 = (n - 1) % W1;                                 // k % (W + 1)
+            for (int k = n - 1; k >= 0; --k, kw1 = kw1 == 0 ? W : kw1 - 1) {
+                const double *row = win + (k & 1) * W * 36;
+                double pre[kPre], ypre = 0.0;
+                if (k > 0) {
+                    const double *src = b.L + (size_t)(k - 1) * W * 36;
+#pragma unroll
+                    for (int u = 0; u < kPre; ++u) {
+                        const int e = tid + u * NT;
+                        pre[u] = e < W * 36 ? src[e] : 0.0;
+                    }
+                }
+                if (tid < 6 && k - W >= 0) ypre = b.x[6 * (k - W) + tid];
+                double *xk = yring + kw1 * 6;
+                if (tid == 0) {
+                    double x[6];
+#pragma unroll
+                    for (int r = 5; r >= 0; --r) {
+                        double v = xk[r];
+#pragma unroll
+                        for (int q = r + 1; q < 6; ++q) v -= row[6 * q + r] * x[q];
+                        x[r] = v / row[6 * r + r];
+                    }
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) {
+                        xk[r] = x[r];
+                        b.x[6 * k + r] = x[r];
+                    }
+                }
+                __syncthreads();
+                for (int t = tid; t < bw * 6; t += NT) {
+                    const int d = 1 + t / 6, r = t % 6;
+                    if (k - d < 0) continue;
+                    const double *Lkj = row + d * 36;      // block (k, k - d)
+                    double v = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) v += Lkj[6 * q + r] * xk[q];
+                    const int sj = kw1 - d;
+                    yring[(sj < 0 ? sj + W1 : sj) * 6 + r] -= v;
+                }
+                if (tid < 6 && k - W >= 0) {
+                    const int sj = kw1 - W;
+                    yring[(sj < 0 ? sj + W1 : sj) * 6 + tid] = ypre;
+                }
+                if (k > 0) {
+                    double *dst = win + ((k - 1) & 1) * W * 36;
+#pragma unroll
+                    for (int u = 0; u < kPre; ++u) {
+                        const int e = tid + u * NT;
+                        if (e < W * 36) dst[e] = pre[u];
+                    }
+                }
+                __syncthreads();
+            }
+            int fin = 1;
+            for (int q = tid; q < P; q += NT) fin &= isfinite(b.x[q]) ? 1 : 0;
+            fin = __syncthreads_and(fin);
+            solved = fin;
+        }
+        if (!solved && tid == 0)
+            s_lam = s_lam > 0.0 ? s_lam * 10.0 : fmax(s_trace / P, 1.0) * 1e-10;
+        __syncthreads();
+    }
+    if (!solved) {
+        if (tid == 0) {
+            st->termination = kTermSolver;
+            st->done = 1;
+            st->gn_skip = 1;
+            st->iterations += 1;
+        }
+        return;
+    }
+    for (int q = tid; q < P; q += NT) {
+        const int node = q / 6, r = q % 6;
+        b.step[q] = -b.x[6 * b.pos[node] + r];
+    }
+}
+
+static size_t ng_factor_smem(int bw) {
+    // the factor's window, or two rows of L for the backward substitution
+    return (size_t)(bw + 1) * std::max(bw + 1, 2) * 36 * sizeof(double);
+}
+
+// candidate node states exp(0.5^h step) o T for h < ncand (kinematics.py:307-311)
+__global__ void k_ng_cands(NgBufs b) {
+    NgDev *st = b.st;
+    if (st->gn_skip) return;
+    const int n = st->n;
+    const int nc = min(st->max_halvings + 1, kNgMaxCand);
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->ncand = nc;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nc * n; t += gridDim.x * blockDim.x) {
+        const int h = t / n, node = t % n;
+        const double scale = ldexp(1.0, -h);
+        double tw[6];
+        for (int q = 0; q < 6; ++q) tw[q] = scale * b.step[6 * node + q];
+        double R2[9], t2[3];
+        apply_twist_dev(tw, b.R + 9 * node, b.T + 3 * node, R2, t2);
+        double *cR = b.candR + ((size_t)h * n + node) * 9;
+        double *cT = b.candT + ((size_t)h * n + node) * 3;
+        for (int q = 0; q < 9; ++q) cR[q] = R2[q];
+        for (int q = 0; q < 3; ++q) cT[q] = t2[q];
+        ng_dq(R2, t2, b.candDQ + ((size_t)h * n + node) * 8);
+    }
+}
+
+// + ARAP objectives of the candidates, first accepted (mstep.py:443-459),
+// state update, Gauss-Newton continuation
+__global__ void __launch_bounds__(kNgThreads, 1) k_ng_select(NgBufs b) {
+    NgDev *st = b.st;
+    if (st->gn_skip) return;
+    const int n = st->n, nc = st->ncand;
+    __shared__ double red[kNgThreads / 32][kNgMaxCand];
+    __shared__ int acc_h;
+    const bool reg = st->lambda > 0.0 && st->n_edges > 0;
+    double part[kNgMaxCand];
+    for (int h = 0; h < kNgMaxCand; ++h) part[h] = 0.0;
+    if (reg)
+        for (int e2 = threadIdx.x; e2 < 2 * st->n_edges; e2 += blockDim.x)
+            for (int h = 0; h < nc; ++h) {
+                double xk[3], xl[3], rr[3];
+                ng_arap_rows(b, e2 >> 1, e2 & 1, b.candR + (size_t)h * n * 9,
+                             b.candT + (size_t)h * n * 3, xk, xl, rr);
+                part[h] += 0.5 * ((rr[0] * rr[0] + rr[1] * rr[1]) + rr[2] * rr[2]);
+            }
+    for (int h = 0; h < kNgMaxCand; ++h) {
+        double v = part[h];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][h] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        acc_h = -1;
+        if (*b.flag) {
+            st->termination = kNgTermBlend;
+            st->done = 1;
+            st->gn_skip = 1;
+        } else {
+            for (int h = 0; h < nc && acc_h < 0; ++h) {
+                double arap = 0.0;
+                for (int w = 0; w < (int)(blockDim.x / 32); ++w) arap += red[w][h];
+                const double cv = b.cand_data[h] + arap;
+                if (cv <= st->value * (1.0 + 1e-12) + 1e-300) {
+                    acc_h = h;
+                    st->value = cv;
+                }
+            }
+            if (acc_h < 0) {
+                st->gn_skip = 1;                       // no acceptable step (mstep.py:450-451)
+            } else {
+                const double scale = ldexp(1.0, -acc_h);
+                double sn = 0.0;
+                for (int q = 0; q < 6 * n; ++q) sn += (scale * b.step[q]) * (scale * b.step[q]);
+                st->gn += 1;
+                st->gn_skip = (sqrt(sn) <= st->step_tol || st->gn >= st->max_gn_iters) ? 1 : 0;
+            }
+        }
+    }
+    __syncthreads();
+    if (acc_h >= 0)
+        for (int q = threadIdx.x; q < n; q += blockDim.x) {
+            const size_t o = (size_t)acc_h * n + q;
+            for (int c = 0; c < 9; ++c) b.R[9 * q + c] = b.candR[9 * o + c];
+            for (int c = 0; c < 3; ++c) b.T[3 * q + c] = b.candT[3 * o + c];
+            for (int c = 0; c < 8; ++c) b.DQ[8 * q + c] = b.candDQ[8 * o + c];
+        }
+}
+
+// update magnitude (batched form of pipeline.py:79-86) and termination
+// (pipeline.py:167-177)
+__global__ void __launch_bounds__(kNgThreads, 1) k_ng_finish(NgBufs b) {
+    NgDev *st = b.st;
+    if (st->done || !st->mstep_ran) return;
+    const int n = st->n;
+    __shared__ double red[kNgThreads / 32];
+    double worst = 0.0;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        double Rd[9];
+        m3_mul_t(b.R + 9 * q, b.R0 + 9 * q, Rd);
+        const double dx = b.T[3 * q] - b.T0[3 * q], dy = b.T[3 * q + 1] - b.T0[3 * q + 1],
+                     dz = b.T[3 * q + 2] - b.T0[3 * q + 2];
+        worst = fmax(worst, rotation_angle_dev(Rd) + sqrt((dx * dx + dy * dy) + dz * dz) /
+                                                         st->diameter);
+    }
+    for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_down_sync(0xffffffffu, worst, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = worst;
+    __syncthreads();
+    __shared__ int conv;
+    if (threadIdx.x == 0) {
+        double norm = 0.0;
+        for (int w = 0; w < (int)(blockDim.x / 32); ++w) norm = fmax(norm, red[w]);
+        const int it = st->iterations;
+        b.traces[st->max_em_iters + it] = norm;
+        st->iterations = it + 1;
+        conv = norm < st->tol;
+        if (conv) {                 // sub-tolerance motion: dropped (pipeline.py:169-173)
+            b.traces[it] = st->value0;
+            st->termination = kTermConverged;
+            st->done = 1;
+        } else {
+            b.traces[it] = st->value;
+            if (it + 1 >= st->max_em_iters) {
+                st->termination = kTermMaxIters;
+                st->done = 1;
+            }
+        }
+        st->mstep_ran = 0;
+    }
+    __syncthreads();
+    if (conv)
+        for (int q = threadIdx.x; q < n; q += blockDim.x) {
+            for (int c = 0; c < 9; ++c) b.R[9 * q + c] = b.R0[9 * q + c];
+            for (int c = 0; c < 3; ++c) b.T[3 * q + c] = b.T0[3 * q + c];
+            for (int c = 0; c < 8; ++c) b.DQ[8 * q + c] = b.DQ0[8 * q + c];
+        }
 }
 
 }  // namespace fr
@@ -457,6 +1206,329 @@ int fr_graph_objective(const float *ref, int64_t m, const int32_t *sidx, const d
     FR_CHECK_LAUNCH();
     k_reduce_cols<<<1, 32 * kGraphMaxCand, 0, s>>>(scratch, grid, kGraphMaxCand, out, nullptr);
     FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+}  // extern "C"
+
+// ---- device-resident node-graph EM object ---------------------------------
+struct fr_ng_em {
+    const fr_lattice *lat = nullptr;
+    const float *ref = nullptr;
+    long long m = 0;
+    int K = 0, n = 0, n_pairs = 0, mode = 0, max_iters = 0, max_gn = 1, ncand = 1, bw = 0;
+    const int32_t *sidx = nullptr, *dptr = nullptr, *dent = nullptr, *pptr = nullptr,
+                  *pent = nullptr;
+    const double *swt = nullptr;
+    fr::GraphK g{};
+    fr::NgBufs b{};
+    // owned buffers
+    fr::NgDev *d_st = nullptr;
+    double *d_rec = nullptr, *d_ete = nullptr, *d_scratch = nullptr, *d_gsums = nullptr,
+           *d_diag = nullptr, *d_off = nullptr, *d_cdata = nullptr;
+    std::vector<void *> owned;
+    int *d_flag = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
+using namespace fr;
+
+static int ng_iteration(fr_ng_em *em, cudaStream_t s) {
+    const int grid = pass_grid();
+    const SliceTable t = em->lat->table();
+    FR_CUDA(cudaMemsetAsync(em->d_flag, 0, sizeof(int), s));
+    const int *done = &em->d_st->done, *gskip = &em->d_st->gn_skip;
+    const int nv = em->lat->nv;
+#define FR_G(NV, RS, SKIP)                                                                      \
+    k_graph_pass<NV, RS><<<grid, kPassThreads, 0, s>>>(em->ref, em->m, em->sidx, em->swt,         \
+                                                       em->b.DQ, em->g, t, em->d_rec, em->d_ete, \
+                                                       em->d_scratch, em->d_flag, SKIP)
+    switch (nv) {
+        case 4: FR_G(4, false, done); break;
+        case 7: FR_G(7, false, done); break;
+        default: set_error("node-graph device loop: lattice columns %d", nv); return FR_EINVAL;
+    }
+    FR_CHECK_LAUNCH();
+    k_reduce_cols<<<1, 32 * kGraphAcc, 0, s>>>(em->d_scratch, grid, kGraphAcc, em->d_gsums, done);
+    const long long warps = (long long)em->n + em->n_pairs;
+    const unsigned gb = (unsigned)((warps * 32 + 127) / 128);
+    k_graph_blocks<<<gb, 128, 0, s>>>(em->d_ete, em->swt, em->K, em->dptr, em->dent, em->n,
+                                      em->pptr, em->pent, em->n_pairs, em->d_diag, em->d_off, done);
+    FR_CHECK_LAUNCH();
+    const unsigned ga = (unsigned)(((long long)em->n * (em->bw + 1) + kNgAsmThreads - 1) / kNgAsmThreads);
+    k_ng_begin<<<1, kNgThreads, 0, s>>>(em->b, 1);
+    k_ng_assemble<<<ga, kNgAsmThreads, 0, s>>>(em->b);
+    FR_CHECK_LAUNCH();
+    for (int gn = 0; gn < em->max_gn; ++gn) {
+        if (gn > 0) {
+            FR_G(4, true, gskip);
+            FR_CHECK_LAUNCH();
+            k_reduce_cols<<<1, 32 * kGraphAcc, 0, s>>>(em->d_scratch, grid, kGraphAcc,
+                                                      em->d_gsums + 8, gskip);
+            k_graph_blocks<<<gb, 128, 0, s>>>(em->d_ete, em->swt, em->K, em->dptr, em->dent, em->n,
+                                              em->pptr, em->pent, em->n_pairs, em->d_diag,
+                                              em->d_off, gskip);
+            k_ng_assemble<<<ga, kNgAsmThreads, 0, s>>>(em->b);
+            FR_CHECK_LAUNCH();
+        }
+        k_ng_factor<<<1, kNgFacThreads, ng_factor_smem(em->bw), s>>>(em->b);
+        k_ng_cands<<<(unsigned)((kNgMaxCand * em->n + 255) / 256), 256, 0, s>>>(em->b);
+        k_graph_objective<<<grid, kPassThreads, 0, s>>>(
+            em->ref, em->m, em->sidx, em->swt, em->K, em->b.candDQ, em->n, em->ncand, em->d_rec,
+            em->mode, em->g.sinv[0], em->g.sinv[1], em->g.sinv[2], em->d_scratch, em->d_flag,
+            gskip);
+        k_reduce_cols<<<1, 32 * kGraphMaxCand, 0, s>>>(em->d_scratch, grid, kGraphMaxCand,
+                                                        em->d_cdata, gskip);
+        k_ng_select<<<1, kNgThreads, 0, s>>>(em->b);
+        FR_CHECK_LAUNCH();
+    }
+#undef FR_G
+    k_ng_finish<<<1, kNgThreads, 0, s>>>(em->b);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+extern "C" {
+
+int fr_ng_em_create(const fr_lattice *lat, const float *ref, int64_t m, const int32_t *sidx,
+                    const double *swt, int K, int n_nodes, const double *node_pos,
+                    const int32_t *edges, int n_edges, const int32_t *dptr, const int32_t *dent,
+                    const int32_t *pptr, const int32_t *pent, int n_pairs, const int32_t *pair_lo,
+                    const int32_t *pair_hi, const int32_t *pos, int bw, const int32_t *slot_ptr,
+                    const int32_t *slot_ent, int n_slot_ent, const int32_t *inc_ptr,
+                    const int32_t *inc_ent, const double *node_R, const double *node_t,
+                    const double *node_dq, int mode, double lambda_reg,
+                    const fr_rigid_em_config *cfg, void *stream, fr_ng_em **out) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!lat || !lat->blurred || lat->dim != 3 || !ref || !sidx || !swt || K < 1 || K > kMaxK ||
+        n_nodes < 1 || !node_pos || (n_edges > 0 && !edges) || !dptr || !dent || !pos || bw < 0 ||
+        !slot_ptr || !inc_ptr || !node_R || !node_t || !node_dq || !cfg || !out || m <= 0 ||
+        (n_pairs > 0 && (!pptr || !pent || !pair_lo || !pair_hi))) {
+        set_error("invalid node-graph device EM arguments");
+        return FR_EINVAL;
+    }
+    const bool pl = mode == FR_POINT_TO_PLANE;
+    if ((pl && lat->nv != 7) || (!pl && lat->nv != 4)) {
+        set_error("node-graph device loop: lattice value columns (%d) do not match the mode", lat->nv);
+        return FR_EINVAL;
+    }
+    if (bw > kNgMaxBw) {
+        set_error("node-graph device loop: block bandwidth %d above %d", bw, kNgMaxBw);
+        return FR_ECAPACITY;
+    }
+    if (cfg->max_halvings + 1 > kNgMaxCand || cfg->max_gn_iters < 0 || cfg->max_gn_iters > 8 ||
+        cfg->max_em_iters < 1) {
+        set_error("node-graph device loop: max_halvings <= %d, max_gn_iters <= 8", kNgMaxCand - 1);
+        return FR_EINVAL;
+    }
+    if (cudaFuncSetAttribute(k_ng_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ng_factor_smem(kNgMaxBw)) != cudaSuccess) {
+        set_error("node-graph device loop: shared-memory opt-in failed");
+        return FR_ECUDA;
+    }
+    fr_ng_em *em = new fr_ng_em();
+    em->lat = lat;
+    em->ref = ref;
+    em->m = m;
+    em->K = K;
+    em->n = n_nodes;
+    em->n_pairs = n_pairs;
+    em->mode = mode;
+    em->max_iters = cfg->max_em_iters;
+    em->max_gn = std::max(cfg->max_gn_iters, 1);
+    em->ncand = cfg->max_halvings + 1;
+    em->bw = bw;
+    em->sidx = sidx;
+    em->swt = swt;
+    em->dptr = dptr;
+    em->dent = dent;
+    em->pptr = pptr;
+    em->pent = pent;
+    em->stream = s;
+    GraphK &g = em->g;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double e = 0.0;
+            if (i == 0) e = 1.0;
+            else if (j == i - 1) e = -(double)i;
+            else if (j >= i) e = 1.0;
+            g.A[i][j] = e * lat->c.sf[j] / lat->c.sigma[j];
+        }
+    for (int j = 0; j < 3; ++j) g.sinv[j] = cfg->sigma_inv[j];
+    g.cp = cfg->c_prime;
+    g.gain = lat->c.gain;
+    g.mode = mode;
+    g.K = K;
+    g.m2_col = -1;
+    g.ncol = pl ? 4 : -1;
+    NgDev h;
+    memset(&h, 0, sizeof(h));
+    for (int j = 0; j < 3; ++j) h.sinv[j] = cfg->sigma_inv[j];
+    h.cp = cfg->c_prime;
+    h.diameter = cfg->diameter;
+    h.tol = cfg->twist_tolerance;
+    h.use_damping = cfg->damping >= 0.0;
+    h.damping = cfg->damping;
+    h.step_tol = cfg->step_tolerance;
+    h.degenerate_mass = cfg->degenerate_mass;
+    h.lambda = lambda_reg;
+    h.n = n_nodes;
+    h.n_edges = n_edges;
+    h.bw = bw;
+    h.max_em_iters = cfg->max_em_iters;
+    h.max_gn_iters = std::max(cfg->max_gn_iters, 0);
+    h.max_halvings = cfg->max_halvings;
+    h.mode = mode;
+    h.gn_skip = 1;
+    const int W = bw + 1, n = n_nodes;
+    auto dalloc = [&](void **p, size_t bytes) -> bool {
+        if (cudaMallocAsync(p, std::max<size_t>(bytes, 8), s) != cudaSuccess) return false;
+        em->owned.push_back(*p);
+        return true;
+    };
+    auto up = [&](void **p, const void *src, size_t bytes) -> bool {
+        return dalloc(p, bytes) && (bytes == 0 ||
+                                    cudaMemcpyAsync(*p, src, bytes, cudaMemcpyHostToDevice, s) ==
+                                        cudaSuccess);
+    };
+    // band-position inverse
+    std::vector<int32_t> node_at((size_t)n);
+    for (int q = 0; q < n; ++q) node_at[pos[q]] = q;
+    NgBufs &B = em->b;
+    void *p = nullptr;
+    bool ok = true;
+    ok = ok && dalloc((void **)&em->d_st, sizeof(NgDev)) &&
+         cudaMemcpyAsync(em->d_st, &h, sizeof(NgDev), cudaMemcpyHostToDevice, s) == cudaSuccess;
+    B.st = em->d_st;
+    ok = ok && up(&p, node_R, (size_t)n * 9 * 8); B.R = (double *)p;
+    ok = ok && up(&p, node_t, (size_t)n * 3 * 8); B.T = (double *)p;
+    ok = ok && up(&p, node_dq, (size_t)n * 8 * 8); B.DQ = (double *)p;
+    ok = ok && dalloc(&p, (size_t)n * 9 * 8); B.R0 = (double *)p;
+    ok = ok && dalloc(&p, (size_t)n * 3 * 8); B.T0 = (double *)p;
+    ok = ok && dalloc(&p, (size_t)n * 8 * 8); B.DQ0 = (double *)p;
+    ok = ok && up(&p, node_pos, (size_t)n * 3 * 8); B.P = (const double *)p;
+    ok = ok && up(&p, edges, (size_t)n_edges * 2 * 4); B.edges = (const int *)p;
+    ok = ok && up(&p, pos, (size_t)n * 4); B.pos = (const int *)p;
+    ok = ok && up(&p, node_at.data(), (size_t)n * 4); B.node_at = (const int *)p;
+    ok = ok && up(&p, slot_ptr, ((size_t)n * W + 1) * 4); B.slot_ptr = (const int *)p;
+    ok = ok && up(&p, slot_ent, (size_t)n_slot_ent * 4); B.slot_ent = (const int *)p;
+    ok = ok && up(&p, inc_ptr, ((size_t)n + 1) * 4); B.inc_ptr = (const int *)p;
+    ok = ok && up(&p, inc_ent, (size_t)2 * n_edges * 4); B.inc_ent = (const int *)p;
+    ok = ok && up(&p, pair_lo, (size_t)n_pairs * 4); B.pair_lo = (const int *)p;
+    ok = ok && up(&p, pair_hi, (size_t)n_pairs * 4); B.pair_hi = (const int *)p;
+    ok = ok && dalloc((void **)&em->d_gsums, 16 * 8); B.gsums = em->d_gsums;
+    ok = ok && dalloc((void **)&em->d_diag, (size_t)n * 27 * 8); B.diag = em->d_diag;
+    ok = ok && dalloc((void **)&em->d_off, (size_t)std::max(n_pairs, 1) * 21 * 8); B.off = em->d_off;
+    ok = ok && dalloc(&p, (size_t)n * W * 36 * 8); B.band = (double *)p;
+    ok = ok && dalloc(&p, (size_t)n * 6 * 8); B.bvec = (double *)p;
+    ok = ok && dalloc(&p, (size_t)n * W * 36 * 8); B.L = (double *)p;
+    ok = ok && dalloc(&p, (size_t)n * 6 * 8); B.x = (double *)p;
+    ok = ok && dalloc(&p, (size_t)n * 6 * 8); B.step = (double *)p;
+    ok = ok && dalloc(&p, (size_t)kNgMaxCand * n * 9 * 8); B.candR = (double *)p;
+    ok = ok && dalloc(&p, (size_t)kNgMaxCand * n * 3 * 8); B.candT = (double *)p;
+    ok = ok && dalloc(&p, (size_t)kNgMaxCand * n * 8 * 8); B.candDQ = (double *)p;
+    ok = ok && dalloc((void **)&em->d_cdata, kNgMaxCand * 8); B.cand_data = em->d_cdata;
+    ok = ok && dalloc(&p, (size_t)3 * cfg->max_em_iters * 8); B.traces = (double *)p;
+    ok = ok && dalloc((void **)&em->d_flag, sizeof(int)); B.flag = em->d_flag;
+    ok = ok && dalloc((void **)&em->d_rec, (size_t)7 * m * 8);
+    ok = ok && dalloc((void **)&em->d_ete, (size_t)m * kGraphEte * 8);
+    ok = ok && dalloc((void **)&em->d_scratch, (size_t)pass_grid_max() * 32 * 8);
+    ok = ok && cudaMemsetAsync(B.traces, 0, (size_t)3 * cfg->max_em_iters * 8, s) == cudaSuccess;
+    ok = ok && cudaStreamSynchronize(s) == cudaSuccess;
+    if (!ok) {
+        fr_ng_em_destroy(em);
+        set_error("node-graph device EM allocation failed");
+        return FR_ECUDA;
+    }
+    *out = em;
+    return FR_OK;
+}
+
+int fr_ng_em_destroy(fr_ng_em *em) {
+    if (!em) return FR_OK;
+    cudaStreamSynchronize(em->stream);
+    if (em->graph) cudaGraphExecDestroy(em->graph);
+    for (void *p : em->owned) cudaFreeAsync(p, em->stream);
+    delete em;
+    return FR_OK;
+}
+
+int fr_ng_em_run(fr_ng_em *em, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    em->stream = s;
+    if (!em->graph) {
+        cudaStream_t cs;
+        FR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t g;
+        FR_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        const int st = ng_iteration(em, cs);
+        cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        FR_TRY(st);
+        FR_CUDA(cudaGraphInstantiate(&em->graph, g, 0));
+        cudaGraphDestroy(g);
+    }
+    static thread_local int *flags = nullptr;       // [2][4] pinned
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (!flags) {
+        FR_CUDA(cudaHostAlloc((void **)&flags, 8 * sizeof(int), cudaHostAllocDefault));
+        for (int i = 0; i < 2; ++i) FR_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    constexpr int kChunk = 2;
+    int issued = 0, k = 0;
+    auto chunk = [&]() -> int {
+        for (int i = 0; i < kChunk; ++i) FR_CUDA(cudaGraphLaunch(em->graph, s));
+        FR_CUDA(cudaMemcpyAsync(flags + 4 * (k & 1), &em->d_st->done, 3 * sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+        FR_CUDA(cudaEventRecord(ev[k & 1], s));
+        issued += kChunk;
+        ++k;
+        return FR_OK;
+    };
+    FR_TRY(chunk());
+    while (true) {
+        const bool more = issued < em->max_iters + kChunk;
+        if (more) FR_TRY(chunk());
+        const int prev = (k - (more ? 2 : 1)) & 1;
+        FR_CUDA(cudaEventSynchronize(ev[prev]));
+        if (flags[4 * prev] || !more) break;
+    }
+    FR_CUDA(cudaStreamSynchronize(s));
+    return FR_OK;
+}
+
+// node poses (n x 9 / n x 3), traces, iterations, termination (4: a dual
+// quaternion blend degenerated -> DegenerateBlendError)
+int fr_ng_em_result(fr_ng_em *em, double *node_R, double *node_t, double *objectives,
+                    double *twist_norms, double *inlier_masses, int *iterations,
+                    int *termination, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    NgDev h;
+    FR_CUDA(cudaMemcpyAsync(&h, em->d_st, sizeof(NgDev), cudaMemcpyDeviceToHost, s));
+    std::vector<double> tr((size_t)3 * em->max_iters);
+    FR_CUDA(cudaMemcpyAsync(tr.data(), em->b.traces, tr.size() * 8, cudaMemcpyDeviceToHost, s));
+    if (node_R) FR_CUDA(cudaMemcpyAsync(node_R, em->b.R, (size_t)em->n * 9 * 8, cudaMemcpyDeviceToHost, s));
+    if (node_t) FR_CUDA(cudaMemcpyAsync(node_t, em->b.T, (size_t)em->n * 3 * 8, cudaMemcpyDeviceToHost, s));
+    FR_CUDA(cudaStreamSynchronize(s));
+    const int n = std::min(h.iterations, em->max_iters);
+    if (objectives) memcpy(objectives, tr.data(), n * 8);
+    if (twist_norms) memcpy(twist_norms, tr.data() + em->max_iters, n * 8);
+    if (inlier_masses) memcpy(inlier_masses, tr.data() + 2 * em->max_iters, n * 8);
+    if (iterations) *iterations = h.iterations;
+    if (termination) *termination = h.termination;
+    if (h.termination == kTermSolver && h.done) {
+        set_error("normal equations not factorizable after damping escalation");
+        return FR_ESOLVER;
+    }
     return FR_OK;
 }
 

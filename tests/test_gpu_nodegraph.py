@@ -114,3 +114,45 @@ def test_gather_lists_device_equals_host():
     for k in ("pair_lo", "pair_hi", "codes"):
         assert np.array_equal(dev[k], host[k]), k
     assert dev["n_pairs"] == host["n_pairs"]
+
+
+@pytest.mark.parametrize("case", ["strip2k", "strip6k_pt2pl"])
+def test_device_loop_matches_host_loop(fr, case, monkeypatch):
+    """The device-resident node-graph loop (fr_ng_em: banded system with the
+    ARAP term, block-banded damped Cholesky, all halvings in one pass) equals
+    the host loop (SuperLU / dense GPU factorisation, host ARAP) to round-off."""
+    from paper_1811_10136_b200 import _nodegraph
+    g = np.load(os.path.join(GOLDEN, f"nodegraph_{case}.npz"))
+    cfg = json.loads(str(g["config"]))
+    pl = cfg["mode"] == "point_to_plane"
+    ref = fr.PointCloud(g["X"], normals=g["N"] if pl else None)
+    obs = fr.PointCloud(g["Y"], normals=g["YN"] if pl else None)
+    config = fr.RegistrationConfig(
+        gmm=fr.GmmConfig(sigma=cfg["sigma"], outlier_ratio=cfg["w"]), residual_mode=cfg["mode"],
+        max_em_iters=cfg["max_iters"], twist_tolerance=cfg["tol"],
+        mstep=fr.MStepOptions(lambda_reg=cfg["lambda_reg"]))
+    dev = fr.register(ref, obs, graph_from(fr, g), config)
+    monkeypatch.setattr(_nodegraph, "DEVICE_LOOP", False)
+    host = fr.register(ref, obs, graph_from(fr, g), config)
+    assert dev.iterations == host.iterations and dev.termination == host.termination
+    # (entrywise: acos near 1 cannot resolve round-off-level angles)
+    worst = max(float(np.abs(a.rotation - b.rotation).max())
+                for a, b in zip(dev.kinematics.node_transforms, host.kinematics.node_transforms))
+    assert worst < 1e-9
+    np.testing.assert_allclose(dev.objectives, host.objectives, rtol=1e-8)
+
+
+def test_extra_gauss_newton_against_reference(fr):
+    """max_gn_iters = 2 node graph (respec passes between GN iterations)
+    against the live reference."""
+    g = np.load(os.path.join(GOLDEN, "config_gn2_strip2k.npz"))
+    config = fr.RegistrationConfig(
+        gmm=fr.GmmConfig(sigma=0.02, outlier_ratio=0.1), max_em_iters=int(g["max_iters"]),
+        twist_tolerance=1e-5, mstep=fr.MStepOptions(lambda_reg=0.1, max_gn_iters=2))
+    res = fr.register(fr.PointCloud(g["X"].astype(float)), fr.PointCloud(g["Y"].astype(float)),
+                      graph_from(fr, g), config)
+    assert abs(res.iterations - int(g["iterations"])) <= 1
+    ext = O.bbox_diameter(g["X"].astype(float))
+    for T, Rg, tg in zip(res.kinematics.node_transforms, g["node_R"], g["node_t"]):
+        assert O.rotation_angle(T.rotation @ Rg.T) <= 1e-4
+        assert np.linalg.norm(T.translation - tg) <= 1e-5 * ext

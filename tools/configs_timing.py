@@ -1,13 +1,18 @@
-"""BASELINE configs C1-C4 end to end on the GPU, next to the live reference's
-timing on the same inputs (bench_data/, made by tools/make_config_inputs.py).
+"""BASELINE configs C1-C4 (and the C5 1M point) end to end on the GPU, next to
+the live reference's wall time on the same inputs (tests/golden/
+MANIFEST_configs.json, measured by tests/golden/make_golden_configs.py in
+the build container, one BLAS thread per case) and checked against the live
+reference's final poses.
 
-    python tools/configs_timing.py        # on the GPU box
+    python tools/configs_timing.py [--out profiles/r02_configs.json]
 
-Each config: one warm-up registration, then one timed registration through the
-public register() from host float64 clouds (upload, lattice build, EM loop).
-Prints one JSON object per config and writes bench_data/gpu_timing.json.
+Per config: one warm-up registration, then three timed registrations through
+the public register() from host float64 clouds (upload, lattice build, EM
+loop, D2H); the median is reported, with the phase split of register()'s
+`timing` dict (the device loops report the whole loop as e_step_s).
 """
 
+import argparse
 import json
 import os
 import sys
@@ -19,56 +24,108 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1811_10136_b200 as fr  # noqa: E402
+from oracle import filterreg_oracle as O  # noqa: E402  (input generator / pose check)
 from paper_1811_10136_b200.kinematics import NodeGraph, Skinning  # noqa: E402
 from tests.articulated_util import tree_from_arrays  # noqa: E402
 
-DATA = os.path.join(ROOT, "bench_data")
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, f"config_{name}.npz"), allow_pickle=False)
+
+
+def pebble(n):
+    model, obs, _ = O.pebble_pair(n, outlier_ratio=0.05, seed=0)
+    X = model.astype(np.float32).astype(float)
+    Y = obs.astype(np.float32).astype(float)
+    return X, Y, 0.05 * O.bbox_diameter(X[:n])
 
 
 def cases():
-    g = np.load(os.path.join(DATA, "c1.npz"))
-    yield "C1", fr.PointCloud(g["X"]), fr.PointCloud(g["Y"]), lambda: fr.RigidModel(), \
-        fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=float(g["sigma"]), outlier_ratio=0.1),
-                              max_em_iters=250, twist_tolerance=2e-4)
-    g = np.load(os.path.join(DATA, "c2.npz"))
-    yield "C2", fr.PointCloud(g["X"], normals=g["N"]), fr.PointCloud(g["Y"], normals=g["YN"]), \
+    # C1: the reference bench's clean protocol on a 10k pebble (no golden: the
+    # parity of this size is pinned by tests/test_gpu_register.py)
+    X, Y, s = pebble(10000)
+    yield "C1", None, fr.PointCloud(X), fr.PointCloud(Y), lambda: fr.RigidModel(), \
+        fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=s, outlier_ratio=0.1), max_em_iters=250,
+                              twist_tolerance=2e-4)
+    g = load("c2")
+    yield "C2", g, fr.PointCloud(g["X"].astype(float), normals=g["N"].astype(float)), \
+        fr.PointCloud(g["Y"].astype(float), normals=g["YN"].astype(float)), \
         lambda: fr.RigidModel(), \
         fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=float(g["sigma"]), outlier_ratio=0.1),
                               residual_mode="point_to_plane", max_em_iters=50,
                               twist_tolerance=1e-4)
-    g = np.load(os.path.join(DATA, "c3.npz"))
-    yield "C3", fr.PointCloud(g["X"]), fr.PointCloud(g["Y"]), lambda: tree_from_arrays(fr, g), \
+    g = load("c3")
+    yield "C3", g, fr.PointCloud(g["X"].astype(float)), fr.PointCloud(g["Y"].astype(float)), \
+        lambda g=g: tree_from_arrays(fr, g), \
         fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.006, outlier_ratio=0.1),
                               max_em_iters=15, twist_tolerance=1e-5)
-    g = np.load(os.path.join(DATA, "c4.npz"))
-    yield "C4", fr.PointCloud(g["X"]), fr.PointCloud(g["Y"]), \
-        lambda: NodeGraph(g["nodes"], g["edges"], Skinning(g["skin_idx"], g["skin_w"])), \
+    g = load("c4")
+    yield "C4", g, fr.PointCloud(g["X"].astype(float)), fr.PointCloud(g["Y"].astype(float)), \
+        lambda g=g: NodeGraph(g["nodes"], g["edges"], Skinning(g["skin_idx"], g["skin_w"])), \
         fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.02, outlier_ratio=0.1),
                               max_em_iters=10, twist_tolerance=1e-5,
                               mstep=fr.MStepOptions(lambda_reg=0.1))
+    g = load("c5_1m_fixed15")
+    X, Y, s = pebble(1_000_000)
+    yield "C5_1M_15it", g, fr.PointCloud(X), fr.PointCloud(Y), lambda: fr.RigidModel(), \
+        fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=s, outlier_ratio=0.1), max_em_iters=15,
+                              twist_tolerance=1e-30)
+
+
+def pose_check(name, g, res):
+    if g is None:
+        return None
+    est = res.kinematics
+    if name == "C3":
+        return {"joint_err": float(np.abs(est.joint_values - g["joint_values"]).max()),
+                "base_rot_err": float(O.rotation_angle(est.base_pose.rotation @ g["base_R"].T))}
+    if name == "C4":
+        return {"node_rot_err": float(max(O.rotation_angle(a.rotation @ b.T)
+                                          for a, b in zip(est.node_transforms, g["node_R"])))}
+    return {"rot_err": float(O.rotation_angle(est.pose.rotation @ g["R"].T)),
+            "trans_err": float(np.linalg.norm(est.pose.translation - g["t"]))}
 
 
 def main():
-    ref_t = json.load(open(os.path.join(DATA, "reference_timing.json")))
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_configs.json"))
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    manifest = json.load(open(os.path.join(GOLDEN, "MANIFEST_configs.json")))
+    key = {"C2": "c2", "C3": "c3", "C4": "c4", "C5_1M_15it": "c5_1m_fixed15"}
     out = {}
-    for name, ref, obs, model, config in cases():
+    for name, g, ref, obs, model, config in cases():
         fr.register(ref, obs, model(), config)                    # warm-up
         torch.cuda.synchronize()
-        timing = {}
-        t0 = time.perf_counter()
-        res = fr.register(ref, obs, model(), config, timing=timing)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
+        walls, timings, res = [], [], None
+        for _ in range(3):
+            timing = {}
+            t0 = time.perf_counter()
+            res = fr.register(ref, obs, model(), config, timing=timing)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+            timings.append(timing)
+        k = int(np.argsort(walls)[1])
+        wall, timing = walls[k], timings[k]
         it = max(res.iterations, 1)
-        r = ref_t[name]
-        out[name] = {"iterations": res.iterations, "termination": res.termination,
-                     "ref_iterations": r["iterations"], "wall_s": wall,
-                     "em_it_per_s": it / wall, "e_ms_per_iter": 1e3 * timing["e_step_s"] / it,
-                     "m_ms_per_iter": 1e3 * timing["m_step_s"] / it,
-                     "ref_em_it_per_s": r["em_it_per_s"], "ref_wall_s": r["wall_s"],
-                     "speedup_wall": r["wall_s"] / wall}
-        print(name, json.dumps(out[name]), flush=True)
-    with open(os.path.join(DATA, "gpu_timing.json"), "w") as fh:
+        rec = {"points": len(ref), "iterations": res.iterations, "termination": res.termination,
+               "wall_s": wall, "wall_s_reps": walls, "em_it_per_s": it / wall,
+               "ms_per_iter_wall": 1e3 * wall / it,
+               "e_ms_per_iter": 1e3 * timing.get("e_step_s", 0.0) / it,
+               "m_ms_per_iter": 1e3 * timing.get("m_step_s", 0.0) / it,
+               "vs_reference_pose": pose_check(name, g, res)}
+        if name in key:
+            r = manifest[key[name]]
+            rec.update({"ref_iterations": r["iterations"], "ref_wall_s": r["wall_s"],
+                        "speedup_wall": r["wall_s"] / wall,
+                        "ref_note": "live twistreg.register in the build container "
+                                    "(8 cores, one BLAS thread), same inputs"})
+        out[name] = rec
+        print(name, json.dumps(rec), flush=True)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as fh:
         json.dump(out, fh, indent=1)
 
 
