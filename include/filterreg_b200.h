@@ -490,6 +490,17 @@ int fr_ng_em_result(fr_ng_em *em, double *node_R, double *node_t, double *object
  * (3, n) float64 device planes (a transpose, no rounding); splat of
  * [1, y, (|y|^2), (n)] from float64 planes; Morton reorder of float64 planes */
 int fr_upload_points64(const double *host_xyz, int64_t n, double *d_soa, void *stream);
+/* (n, 3) float64 host rows -> (3, n) float64 device planes: a few threads copy the
+ * rows into pinned slots, the DMAs land in d_rows (3 n doubles, device scratch),
+ * one kernel transposes them into d_soa -- all stream-ordered on `stream`
+ * (geometry.py:109-139 PointCloud -> device; no rounding). */
+int fr_upload_rows64(const double *host_xyz, int64_t n, double *d_rows, double *d_soa,
+                     void *stream);
+/* coordinate sums [0:3], minima [3:6], maxima [6:9] of (3, n) float64 planes into
+ * d_out (device, 9 doubles), fixed reduction order; d_work: fr_point_stats64_work_doubles()
+ * doubles (the model cloud's centre and bounding box, pipeline.py / estep.py:97-112) */
+int fr_point_stats64_work_doubles(void);
+int fr_point_stats64(const double *d_soa, int64_t n, double *d_work, double *d_out, void *stream);
 int fr_lattice_splat_points64(fr_lattice *lat, const double *d_pos, const double *d_normals,
                               int64_t n, int value_mode, void *stream);
 int fr_sort_points_morton64(double *d_pos, int64_t n, int planes, int32_t *d_perm, void *stream);

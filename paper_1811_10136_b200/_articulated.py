@@ -47,14 +47,27 @@ class ArticulatedDevicePath(RigidDevicePath):
         lab = labels[order]
         counts = np.bincount(lab, minlength=nb)
         starts = np.concatenate([[0], np.cumsum(counts)])
-        # per-body centres in the body frame (conditioning of the statistics)
+        # per-body centres in the body frame (conditioning of the statistics);
+        # under a process group every rank must take its statistics about the
+        # same centres, so the coordinate sums and counts are all-reduced
         P32 = P.astype(np.float32).astype(float)
+        sums = np.zeros((nb, 4))
+        for b in range(nb):
+            s, e = int(starts[b]), int(starts[b + 1])
+            sums[b, :3] = P32[s:e].sum(axis=0)
+            sums[b, 3] = e - s
+        sums = self._allreduce(sums.ravel(), "sum").reshape(nb, 4)
         self.c_body = np.zeros((nb, 3))
+        has = sums[:, 3] > 0
+        self.c_body[has] = sums[has, :3] / sums[has, 3:4]
+        if process_group is None:
+            for b in range(nb):
+                s, e = int(starts[b]), int(starts[b + 1])
+                if e > s:     # the single-process centres exactly as before
+                    self.c_body[b] = P32[s:e].mean(axis=0)
         chunk_body, chunk_beg, body_chunks = [], [], [0]
         for b in range(nb):
             s, e = int(starts[b]), int(starts[b + 1])
-            if e > s:
-                self.c_body[b] = P32[s:e].mean(axis=0)
             for a in range(s, e, self.CHUNK):
                 chunk_body.append(b)
                 chunk_beg.append(a)

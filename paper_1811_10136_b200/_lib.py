@@ -37,7 +37,8 @@ EXPORTED = (
     "fr_em64_create", "fr_em64_destroy", "fr_em64_run", "fr_em64_run_batch", "fr_em64_pass",
     "fr_em64_solve",
     "fr_em64_sums", "fr_em64_launch_info", "fr_em64_status", "fr_em64_result",
-    "fr_upload_points64", "fr_lattice_splat_points64", "fr_sort_points_morton64",
+    "fr_upload_points64", "fr_upload_rows64", "fr_point_stats64_work_doubles",
+    "fr_point_stats64", "fr_lattice_splat_points64", "fr_sort_points_morton64",
     "fr_lattice_dense_cells64",
     "fr_em64pl_create", "fr_em64pl_destroy", "fr_em64pl_run", "fr_em64pl_sums",
     "fr_em64pl_launch_info", "fr_em64pl_status", "fr_em64pl_result",
@@ -139,6 +140,9 @@ _SIGS = {
     "fr_em64_result": ([_P, _DP, _DP, _DP, _DP, _DP, ctypes.POINTER(_I), ctypes.POINTER(_I), _P],
                        _I),
     "fr_upload_points64": ([_P, _L, _P, _P], _I),
+    "fr_upload_rows64": ([_P, _L, _P, _P, _P], _I),
+    "fr_point_stats64_work_doubles": ([], _I),
+    "fr_point_stats64": ([_P, _L, _P, _P, _P], _I),
     "fr_em64pl_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),
     "fr_em64pl_destroy": ([_P], _I),
     "fr_body_pass_dev": ([_P, _P, _L, _P, _I, _P, _P, _I, _P, _I, _P, _P, _P, _P], _I),

@@ -177,10 +177,19 @@ class NodeGraphDevicePath(RigidDevicePath):
         self.reduce_device(self.diag)
         if self.n_pairs:
             self.reduce_device(self.off)
-        if int(self.flag.item()):
+        if self._degenerate():
             raise DegenerateBlendError("blended real part vanished for some points")
         return (self.gsums[:4].cpu().numpy().copy(), self.diag.cpu().numpy().copy(),
                 self.off[:self.n_pairs].cpu().numpy().copy())
+
+    def _degenerate(self) -> bool:
+        """The degenerate-blend flag, MAX-reduced over the group so every rank
+        raises together (a rank raising alone would leave the others blocked
+        in the next all-reduce)."""
+        if self.group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(self.flag, op=dist.ReduceOp.MAX, group=self.group)
+        return bool(int(self.flag.item()))
 
     def candidate_objectives(self, graphs, s2):
         import torch
@@ -197,7 +206,7 @@ class NodeGraphDevicePath(RigidDevicePath):
                 _lib.ptr(self.gsums), _lib.ptr(self.scratch), _lib.ptr(self.flag),
                 _lib.stream_handle()))
             self.reduce_device(self.gsums)
-            if int(self.flag.item()):
+            if self._degenerate():
                 raise DegenerateBlendError("blended real part vanished for some points")
             out += list(self.gsums[:len(chunk)].cpu().numpy())
         return np.asarray(out)

@@ -173,8 +173,11 @@ def upload_soa64(points, dev):
     import torch
     P = np.ascontiguousarray(points, dtype=np.float64)
     soa = torch.empty((3, P.shape[0]), dtype=torch.float64, device=dev)
-    _lib.check(_lib.load().fr_upload_points64(P.ctypes.data_as(ctypes.c_void_p), P.shape[0],
-                                              _lib.ptr(soa), _lib.stream_handle()))
+    # the rows land in a scratch buffer of the current stream and are
+    # transposed there (freed back to that stream's pool, so reuse is ordered)
+    rows = torch.empty((P.shape[0], 3), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().fr_upload_rows64(P.ctypes.data_as(ctypes.c_void_p), P.shape[0],
+                                            _lib.ptr(rows), _lib.ptr(soa), _lib.stream_handle()))
     return soa
 
 
@@ -303,7 +306,8 @@ class RigidDevicePath:
                               lap if lap.marks else None)
         # the observation upload (the critical path: its splat follows) takes
         # the host memory bandwidth first; the model upload overlaps the splat
-        if residual_mode == "point_to_point" and PIPELINED_SPLAT and not small and not self.f64:
+        if (residual_mode == "point_to_point" and (PIPELINED_SPLAT or self.f64)
+                and not small):
             self._obs_uploaded.wait(timeout=120.0)
         self.ref = upload_soa64(reference.positions, self.dev) if self.f64 \
             else upload_soa(reference.positions, self.dev)
@@ -312,12 +316,23 @@ class RigidDevicePath:
         # global quantities a shard must not compute locally:
         # total model count (outlier constant, degenerate test), the centre of
         # the whole reference cloud and its bounding-box diameter
-        local_sum = self.ref.sum(dim=1, dtype=torch.float64).cpu().numpy()
+        if self.ref.dtype == torch.float64 and self.M > 0:
+            # one fused reduction, one D2H
+            work = torch.empty(self.lib.fr_point_stats64_work_doubles() + 9,
+                               dtype=torch.float64, device=self.dev)
+            _lib.check(self.lib.fr_point_stats64(_lib.ptr(self.ref), self.M, _lib.ptr(work),
+                                                 _lib.ptr(work[-9:]), _lib.stream_handle()))
+            st = work[-9:].cpu().numpy()
+            local_sum, local_lo, local_hi = st[:3], st[3:6], st[6:9]
+        else:
+            local_sum = self.ref.sum(dim=1, dtype=torch.float64).cpu().numpy()
+            local_lo = self.ref.amin(dim=1).double().cpu().numpy()
+            local_hi = self.ref.amax(dim=1).double().cpu().numpy()
         tot = self._allreduce(np.concatenate([[float(self.M)], local_sum]), "sum")
         self.M_total = int(round(tot[0]))
         self.c_ref = tot[1:] / tot[0]
-        lo = self._allreduce(self.ref.amin(dim=1).double().cpu().numpy(), "min")
-        hi = self._allreduce(self.ref.amax(dim=1).double().cpu().numpy(), "max")
+        lo = self._allreduce(local_lo, "min")
+        hi = self._allreduce(local_hi, "max")
         self.diameter = float(np.linalg.norm(hi - lo))
         lap("global_stats")
         if sort and SPATIAL_ORDER and self.M > 1:

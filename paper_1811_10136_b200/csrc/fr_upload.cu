@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -100,6 +101,13 @@ static void convert_rows(const double *r, long long len, double *x, double *y, d
     }
 }
 
+// raw rows: the float64 path keeps the caller's bytes, so the host side is a
+// plain copy into the pinned slot (memcpy-bound) and the transpose to planes
+// runs on the device (k_rows_to_soa64)
+static void copy_rows(const double *r, long long len, double *dst) {
+    std::memcpy(dst, r, (size_t)len * 3 * sizeof(double));
+}
+
 struct WorkerResult {
     int status = FR_OK;
     char msg[256] = {0};
@@ -141,6 +149,90 @@ void worker(int dev, int id, const double *src, long long n, long long a, long l
         res->status = FR_ECUDA;
         snprintf(res->msg, sizeof(res->msg), "point upload: %s", cudaGetErrorString(e));
     }
+}
+
+// rows mode: (n, 3) float64 rows -> the device row buffer, same slots/events
+void worker_rows(int dev, int id, const double *src, long long a, long long b, double *d_rows,
+                 cudaStream_t s, WorkerResult *res) {
+    StagePool &p = pool();
+    constexpr long long kSub = kSubChunk * (long long)sizeof(float) / (long long)sizeof(double);
+    int slot = 0;
+    cudaError_t e = cudaSetDevice(dev);
+    for (long long c = a; c < b && e == cudaSuccess; c += kSub) {
+        const long long len = std::min(kSub, b - c);
+        double *buf = reinterpret_cast<double *>(p.slots[id][slot]);
+        e = cudaEventSynchronize(p.done[id][slot]);
+        if (e == cudaSuccess) {
+            copy_rows(src + 3 * c, len, buf);
+            e = cudaMemcpyAsync(d_rows + 3 * c, buf, (size_t)len * 3 * sizeof(double),
+                                cudaMemcpyHostToDevice, s);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(p.done[id][slot], s);
+        slot ^= 1;
+    }
+    if (e != cudaSuccess) {
+        res->status = FR_ECUDA;
+        snprintf(res->msg, sizeof(res->msg), "point upload: %s", cudaGetErrorString(e));
+    }
+}
+
+// (n, 3) rows -> (3, n) planes; a warp reads 768 contiguous bytes
+__global__ void k_rows_to_soa64(const double *__restrict__ rows, long long n,
+                                double *__restrict__ soa) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double x = rows[3 * i], y = rows[3 * i + 1], z = rows[3 * i + 2];
+        soa[i] = x;
+        soa[n + i] = y;
+        soa[2 * n + i] = z;
+    }
+}
+
+// coordinate sums / minima / maxima of (3, n) float64 planes: fixed grid,
+// fixed order (per-thread strided sums, block tree, then one block over the
+// block partials), so the result is run-to-run identical
+constexpr int kStatBlocks = 148, kStatThreads = 256;
+
+__global__ void __launch_bounds__(kStatThreads) k_point_stats64(const double *__restrict__ soa,
+                                                                long long n, double *part) {
+    __shared__ double sh[9][kStatThreads];
+    double v[9];
+    for (int c = 0; c < 3; ++c) {
+        v[c] = 0.0;
+        v[3 + c] = INFINITY;
+        v[6 + c] = -INFINITY;
+    }
+    for (long long i = blockIdx.x * (long long)kStatThreads + threadIdx.x; i < n;
+         i += (long long)gridDim.x * kStatThreads)
+        for (int c = 0; c < 3; ++c) {
+            const double x = soa[c * n + i];
+            v[c] += x;
+            v[3 + c] = fmin(v[3 + c], x);
+            v[6 + c] = fmax(v[6 + c], x);
+        }
+    for (int q = 0; q < 9; ++q) sh[q][threadIdx.x] = v[q];
+    __syncthreads();
+    for (int h = kStatThreads / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h)
+            for (int c = 0; c < 3; ++c) {
+                sh[c][threadIdx.x] += sh[c][threadIdx.x + h];
+                sh[3 + c][threadIdx.x] = fmin(sh[3 + c][threadIdx.x], sh[3 + c][threadIdx.x + h]);
+                sh[6 + c][threadIdx.x] = fmax(sh[6 + c][threadIdx.x], sh[6 + c][threadIdx.x + h]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x < 9) part[blockIdx.x * 9 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+__global__ void k_point_stats64_final(const double *part, int nb, double *out) {
+    const int q = threadIdx.x;
+    if (q >= 9) return;
+    double v = part[q];
+    for (int b = 1; b < nb; ++b) {
+        const double x = part[b * 9 + q];
+        v = q < 3 ? v + x : (q < 6 ? fmin(v, x) : fmax(v, x));
+    }
+    out[q] = v;
 }
 
 }  // namespace
@@ -202,4 +294,67 @@ extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa,
 
 extern "C" int fr_upload_points64(const double *host_xyz, int64_t n, double *d_soa, void *stream) {
     return fr::upload_impl<double>(host_xyz, n, d_soa, (cudaStream_t)stream, fr::ChunkHook());
+}
+
+extern "C" int fr_upload_rows64(const double *host_xyz, int64_t n, double *d_rows, double *d_soa,
+                                void *stream) {
+    using namespace fr;
+    if (n < 0 || (n > 0 && (!host_xyz || !d_rows || !d_soa))) {
+        set_error("fr_upload_rows64: invalid arguments");
+        return FR_EINVAL;
+    }
+    if (n == 0) return FR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    constexpr long long kSub = kSubChunk / 2;
+    long long cap = 4;          // the copies are memcpy-bound: a few threads fill PCIe
+    if (const char *e = getenv("FR_UPLOAD_WORKERS")) cap = std::max(1, std::min(kMaxWorkers, atoi(e)));
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const long long chunks = (n + kSub - 1) / kSub;
+    const int w = (int)std::max<long long>(1, std::min<long long>({cap, (long long)hw, chunks}));
+    int dev = 0;
+    FR_CUDA(cudaGetDevice(&dev));
+    StagePool &p = pool();
+    {
+        std::lock_guard<std::mutex> lock(p.mu);
+        FR_TRY(p.init());
+        // whole sub-chunks per worker, so every DMA but the last is a full slot
+        const long long per = ((chunks + w - 1) / w) * kSub;
+        std::vector<WorkerResult> res(w);
+        std::vector<std::thread> th;
+        th.reserve(w);
+        for (int i = 0; i < w; ++i) {
+            const long long a = std::min<long long>(n, (long long)i * per);
+            const long long b = std::min<long long>(n, a + per);
+            th.emplace_back(worker_rows, dev, i, host_xyz, a, b, d_rows, s, &res[i]);
+        }
+        for (auto &t : th) t.join();
+        for (const auto &r : res)
+            if (r.status != FR_OK) {
+                set_error("%s", r.msg);
+                return r.status;
+            }
+    }
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_rows_to_soa64<<<blocks, 256, 0, s>>>(d_rows, n, d_soa);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
+}
+
+// d_out[0:3] coordinate sums, [3:6] minima, [6:9] maxima of (3, n) float64
+// planes; d_work holds fr_point_stats64_work_doubles() doubles
+extern "C" int fr_point_stats64_work_doubles(void) { return fr::kStatBlocks * 9; }
+
+extern "C" int fr_point_stats64(const double *d_soa, int64_t n, double *d_work, double *d_out,
+                                void *stream) {
+    using namespace fr;
+    if (n < 0 || !d_work || !d_out || (n > 0 && !d_soa)) {
+        set_error("fr_point_stats64: invalid arguments");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    k_point_stats64<<<kStatBlocks, kStatThreads, 0, s>>>(d_soa, n, d_work);
+    FR_CHECK_LAUNCH();
+    k_point_stats64_final<<<1, 32, 0, s>>>(d_work, kStatBlocks, d_out);
+    FR_CHECK_LAUNCH();
+    return FR_OK;
 }

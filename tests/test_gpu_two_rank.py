@@ -74,3 +74,58 @@ def test_two_rank_device_path_matches_single_process(m):
         np.testing.assert_allclose(objs, single.objectives, rtol=1e-6)
     # identical decisions and poses on every rank (identical reduced sums)
     assert np.array_equal(results[0][0], results[1][0])
+
+
+# -- articulated: per-body statistics about centres every rank agrees on ------
+
+def _art_problem():
+    import os as _os
+    g = dict(np.load(_os.path.join(_os.path.dirname(__file__), "golden", "config_c3.npz")))
+    return g
+
+
+def _art_run(g, lo, hi, group):
+    import paper_1811_10136_b200 as fr
+    from tests.articulated_util import tree_from_arrays
+    gs = dict(g)
+    gs["labels"] = g["labels"][lo:hi]
+    cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=0.006, outlier_ratio=0.1),
+                                max_em_iters=15, twist_tolerance=1e-5)
+    X = g["X"].astype(float)[lo:hi]
+    return fr.register(fr.PointCloud(X), fr.PointCloud(g["Y"].astype(float)),
+                       tree_from_arrays(fr, gs), cfg, process_group=group)
+
+
+def _art_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = _art_problem()
+    b = np.linspace(0, len(g["X"]), world + 1).astype(int)
+    res = _art_run(g, b[rank], b[rank + 1], dist.group.WORLD)
+    out[rank] = (np.asarray(res.kinematics.joint_values), res.kinematics.base_pose.matrix(),
+                 res.iterations, res.termination)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_articulated_matches_single_process():
+    """C3 (50k points, 20 links) split in two contiguous halves: the shards
+    hold different subsets of each body's points, so each rank's own body
+    centres differ -- the statistics must still be taken about the global
+    ones (_articulated.py)."""
+    g = _art_problem()
+    single = _art_run(g, 0, len(g["X"]), None)
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_art_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                           start_method="spawn")
+        results = dict(out)
+    for rank in (0, 1):
+        q, T, iters, term = results[rank]
+        assert iters == single.iterations and term == single.termination
+        assert np.abs(q - np.asarray(single.kinematics.joint_values)).max() < 1e-6
+        np.testing.assert_allclose(T, single.kinematics.base_pose.matrix(), atol=1e-6)
+    assert np.array_equal(results[0][0], results[1][0])

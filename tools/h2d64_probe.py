@@ -48,3 +48,25 @@ def reg_copy():
 print("cudaHostRegister + copy + unregister: %.3f ms" % t(reg_copy))
 pinned = torch.from_numpy(X).pin_memory()
 print("from an already pinned buffer: %.3f ms" % t(lambda: dst.copy_(pinned, non_blocking=True)))
+
+# host-side copy rates into pinned memory (the staged upload's host half)
+import threading  # noqa: E402
+pin_np = pinned.numpy()
+
+
+def copy_threads(k):
+    parts = np.array_split(np.arange(n), k)
+
+    def job(ix):
+        np.copyto(pin_np[ix[0]:ix[-1] + 1], X[ix[0]:ix[-1] + 1])
+    th = [threading.Thread(target=job, args=(p,)) for p in parts]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+
+
+for k in (1, 2, 4, 8):
+    print("host copy into pinned, %d threads: %.3f ms" % (k, t(lambda: copy_threads(k))))
+Z = np.empty_like(X)
+print("host copy pageable->pageable (warm dst), 1 thread: %.3f ms" % t(lambda: np.copyto(Z, X)))
