@@ -48,7 +48,13 @@ enum {
  * (estep.py:153-165). */
 enum {
     FR_VALUES_M2 = 1,       /* append |y|^2 (update_sigma) */
-    FR_VALUES_NORMALS = 2   /* append the observation normal (point_to_plane) */
+    FR_VALUES_NORMALS = 2,  /* append the observation normal (point_to_plane) */
+    /* site sums in np.add.at's flat (point, vertex) order, bit-identical to the
+     * reference's splat (permutohedral.py:241-242).  Without it the point
+     * splats sum each site's entries in a fixed tree order (deterministic,
+     * float64 round-off from the flat order, a serial chain of cnt / 256
+     * adds instead of cnt). */
+    FR_SPLAT_FLAT_ORDER = 256
 };
 
 /* residual modes (mstep.py:33) */

@@ -27,6 +27,7 @@ from .mstep import (MStepOptions, NormalEquations, ResidualSpec, assemble_articu
                     residuals_from_moments)
 from .permutohedral import (PermutohedralLattice, build_lattice, filter_augmented,
                             gaussian_transform_bruteforce, valid_lattice_key)
+from .hostmem import pinned_cloud, pinned_copy, pinned_empty
 from .io import load_cloud, save_cloud
 from .pipeline import (RegistrationConfig, RegistrationResult, alignment_error, default_sigma,
                        log_likelihood, register, register_batch, update_magnitude)
@@ -45,6 +46,7 @@ __all__ = [
     "default_sigma", "filter_augmented", "filterreg_protocol", "forward_points",
     "gaussian_transform_bruteforce", "ladder_result", "register_ladder",
     "gn_solve", "load_articulated_model", "log_likelihood", "m_step", "objective",
-    "outlier_constant", "load_cloud", "save_cloud", "register", "register_batch", "residuals_from_moments", "rotation_about_axis",
+    "outlier_constant", "load_cloud", "save_cloud", "pinned_cloud", "pinned_copy",
+    "pinned_empty", "register", "register_batch", "residuals_from_moments", "rotation_about_axis",
     "twist_exp", "update_magnitude", "update_sigma", "valid_lattice_key",
 ]

@@ -294,6 +294,7 @@ class RigidDevicePath:
         self.normal_col = (5 if self.with_sigma else 4) if normals else -1
         self.lattice = None
         self.sigma = None
+        self._obs_dma = None
         main_stream = torch.cuda.current_stream()
         side = _side_stream()
         # small clouds: the worker thread's handoff costs more than the
@@ -309,6 +310,8 @@ class RigidDevicePath:
         if (residual_mode == "point_to_point" and (PIPELINED_SPLAT or self.f64)
                 and not small):
             self._obs_uploaded.wait(timeout=120.0)
+            if self.f64 and getattr(self, "_obs_dma", None) is not None:
+                main_stream.wait_event(self._obs_dma)
         self.ref = upload_soa64(reference.positions, self.dev) if self.f64 \
             else upload_soa(reference.positions, self.dev)
         self.M = self.ref.shape[1]
@@ -316,24 +319,23 @@ class RigidDevicePath:
         # global quantities a shard must not compute locally:
         # total model count (outlier constant, degenerate test), the centre of
         # the whole reference cloud and its bounding-box diameter
+        stats_ready = None
         if self.ref.dtype == torch.float64 and self.M > 0:
-            # one fused reduction, one D2H
+            # one fused reduction into pinned memory, read once the observation
+            # side is done (a pageable D2H here would stall the host -- and the
+            # observation thread's launches -- behind the model's DMA)
             work = torch.empty(self.lib.fr_point_stats64_work_doubles() + 9,
                                dtype=torch.float64, device=self.dev)
             _lib.check(self.lib.fr_point_stats64(_lib.ptr(self.ref), self.M, _lib.ptr(work),
                                                  _lib.ptr(work[-9:]), _lib.stream_handle()))
-            st = work[-9:].cpu().numpy()
-            local_sum, local_lo, local_hi = st[:3], st[3:6], st[6:9]
+            st_host = torch.empty(9, dtype=torch.float64, pin_memory=True)
+            st_host.copy_(work[-9:], non_blocking=True)
+            stats_ready = torch.cuda.Event()
+            stats_ready.record(main_stream)
         else:
-            local_sum = self.ref.sum(dim=1, dtype=torch.float64).cpu().numpy()
-            local_lo = self.ref.amin(dim=1).double().cpu().numpy()
-            local_hi = self.ref.amax(dim=1).double().cpu().numpy()
-        tot = self._allreduce(np.concatenate([[float(self.M)], local_sum]), "sum")
-        self.M_total = int(round(tot[0]))
-        self.c_ref = tot[1:] / tot[0]
-        lo = self._allreduce(local_lo, "min")
-        hi = self._allreduce(local_hi, "max")
-        self.diameter = float(np.linalg.norm(hi - lo))
+            self._global_stats(self.ref.sum(dim=1, dtype=torch.float64).cpu().numpy(),
+                               self.ref.amin(dim=1).double().cpu().numpy(),
+                               self.ref.amax(dim=1).double().cpu().numpy())
         lap("global_stats")
         if sort and SPATIAL_ORDER and self.M > 1:
             # Morton order of the model points: reduction sums are order-free up
@@ -354,6 +356,10 @@ class RigidDevicePath:
             obs_job.result()          # the side stream is synchronised inside
         finally:
             pool.shutdown(wait=True)
+        if stats_ready is not None:
+            stats_ready.synchronize()
+            st = st_host.numpy()
+            self._global_stats(st[:3].copy(), st[3:6].copy(), st[6:9].copy())
         # later work (passes, rebuilds, frees) is ordered on the caller's stream
         self.obs.record_stream(main_stream)
         if self.obs_n is not None:
@@ -361,6 +367,16 @@ class RigidDevicePath:
         self.lattice.bind_stream(main_stream)
         lap("observation_side")
         self.setup_s = lap.phases
+
+    def _global_stats(self, local_sum, local_lo, local_hi) -> None:
+        """Model count, centre and bounding-box diameter of the whole
+        (possibly sharded) reference cloud."""
+        tot = self._allreduce(np.concatenate([[float(self.M)], local_sum]), "sum")
+        self.M_total = int(round(tot[0]))
+        self.c_ref = tot[1:] / tot[0]
+        lo = self._allreduce(local_lo, "min")
+        hi = self._allreduce(local_hi, "max")
+        self.diameter = float(np.linalg.norm(hi - lo))
 
     def demote_f32(self) -> None:
         """Float32 copies of the float64 planes (for the float32-plane pass
@@ -393,6 +409,10 @@ class RigidDevicePath:
                 self.N, self.obs_n = self.obs.shape[1], None
                 if residual_mode == "point_to_plane":
                     self.obs_n = upload_soa64(observation.normals, self.dev)
+                # the model's DMA queues behind this one on the device (the
+                # observation splat is the critical path: it gets the link first)
+                self._obs_dma = torch.cuda.Event()
+                self._obs_dma.record(stream)
                 self._obs_uploaded.set()
                 if lap is not None:
                     lap("obs_upload")

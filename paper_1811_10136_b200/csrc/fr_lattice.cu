@@ -275,6 +275,68 @@ k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int 
     if (t < nv) run_vals[(long long)r * nv + t] = acc;
 }
 
+// splat phase 2, fixed-tree order (the point splats of the EM path): one
+// block per site, 256 entries per chunk; every thread gathers one entry row
+// (the next chunk's row prefetched into registers), each warp sums its 32
+// rows per column by a shuffle tree, the 8 warp sums are added in warp order
+// and the chunk sums in chunk order.  Deterministic (no atomics, no order
+// that depends on scheduling) but not np.add.at's flat order: site sums
+// differ from it by float64 round-off (the reference's own sums carry the
+// same order of error), and the serial chain is cnt / 256 adds long instead
+// of cnt -- the flat-order kernel's bound at heavy sites.
+template <int NV>
+__device__ __forceinline__ void seg_row(const unsigned *sorted_idx, const double *contrib,
+                                        long long lmajor_n, int D1, int beg, int j, int cnt,
+                                        double (&v)[NV]) {
+    if (j < cnt) {
+        const unsigned e = sorted_idx[beg + j];
+        const size_t rix = lmajor_n ? (size_t)(e % D1) * lmajor_n + e / D1 : e;
+        const double *cr = contrib + rix * NV;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) v[c] = __ldg(cr + c);
+    } else {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) v[c] = 0.0;
+    }
+}
+
+template <int D, int NV>
+__global__ void __launch_bounds__(kSegBlock)
+k_splat_segsum_tree(const unsigned *run_slot, const int *run_off, const int *run_cnt,
+                    const unsigned *sorted_idx, const double *contrib, unsigned sentinel,
+                    double *run_vals, long long lmajor_n) {
+    constexpr int W = kSegBlock / 32;
+    __shared__ double wsum[W][NV];
+    const int r = blockIdx.x;
+    if (run_slot && run_slot[r] == sentinel) return;
+    const int beg = run_off[r], cnt = run_cnt[r];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    double cur[NV], nxt[NV];
+    seg_row<NV>(sorted_idx, contrib, lmajor_n, D + 1, beg, t, cnt, cur);
+    double acc = 0.0;
+    for (int base = 0; base < cnt; base += kSegBlock) {
+        seg_row<NV>(sorted_idx, contrib, lmajor_n, D + 1, beg, base + kSegBlock + t, cnt, nxt);
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            double v = cur[c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) wsum[warp][c] = v;
+        }
+        __syncthreads();
+        if (t < NV) {
+            double sc = wsum[0][t];
+#pragma unroll
+            for (int w = 1; w < W; ++w) sc += wsum[w][t];
+            acc += sc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < NV; ++c) cur[c] = nxt[c];
+    }
+    if (t < NV) run_vals[(long long)r * NV + t] = acc;
+}
+
 __global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentinel,
                            const double *run_vals, int nv, unsigned char *run_live) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -517,20 +579,25 @@ static inline unsigned grid_for(long long n, int block = 256) {
     return (unsigned)std::max<long long>(1, std::min<long long>(g, 1LL << 30));
 }
 
-// FR_SPLAT_TIMING=1: host wall-clock of the splat's phases (device-synchronised)
+// FR_SPLAT_TIMING=1: host wall-clock of the splat's phases (device-synchronised);
+// FR_SPLAT_TIMING=2: host wall-clock only (no synchronisation: where the host
+// thread waits)
 struct PhaseClock {
-    bool on;
+    bool on, sync;
     cudaStream_t s;
     std::chrono::steady_clock::time_point t0;
-    explicit PhaseClock(cudaStream_t st) : on(getenv("FR_SPLAT_TIMING") != nullptr), s(st) {
+    explicit PhaseClock(cudaStream_t st) : s(st) {
+        const char *e = getenv("FR_SPLAT_TIMING");
+        on = e != nullptr;
+        sync = on && e[0] != '2';
         if (on) {
-            cudaStreamSynchronize(s);
+            if (sync) cudaStreamSynchronize(s);
             t0 = std::chrono::steady_clock::now();
         }
     }
     void lap(const char *what) {
         if (!on) return;
-        cudaStreamSynchronize(s);
+        if (sync) cudaStreamSynchronize(s);
         const auto t = std::chrono::steady_clock::now();
         fprintf(stderr, "[splat] %-14s %8.3f ms\n", what,
                 std::chrono::duration<double, std::milli>(t - t0).count());
@@ -759,9 +826,14 @@ static int reserve_sites(fr_lattice *lat, long long need, cudaStream_t s) {
 using EntriesLaunch = std::function<int(long long, long long, cudaStream_t)>;
 using EntriesHook = std::function<int(const EntriesLaunch &)>;
 
+// flat: site sums in np.add.at's flat (point, vertex) order, bit-identical to
+// the reference (the operator API, PermutohedralLattice.splat, and point
+// splats with FR_SPLAT_FLAT_ORDER); else the fixed-tree order of
+// k_splat_segsum_tree
+
 template <int D, class Src>
 static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cudaStream_t s,
-                      const EntriesHook *first = nullptr) {
+                      const EntriesHook *first = nullptr, bool flat = true) {
     if (lat->blurred || lat->splatted) {
         // the reference allows re-splatting an unblurred lattice (it replaces the table)
     }
@@ -865,12 +937,16 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     tmp_bytes = std::max(tmp_bytes, t2);
     FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_cnt, run_off, (int)E, s));
     tmp_bytes = std::max(tmp_bytes, t2);
+    pc.lap("sort_setup");
     void *tmp = sort_tmp;
     if (!tmp || tmp_bytes > sort_bound) FR_TRY(sc.get((char **)&tmp, tmp_bytes));
+    pc.lap("sort_tmp");
     FR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, entry_slot, sorted_slot, entry_idx,
                                             sorted_idx, (int)E, 0, end_bit, s));
+    pc.lap("sort_enqueue");
     FR_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tmp_bytes, sorted_slot, run_slot, run_cnt,
                                                d_nruns, (int)E, s));
+    pc.lap("rle_enqueue");
     int nruns = 0;
     FR_TRY(d2h_sync(&nruns, d_nruns, sizeof(int), s));
     FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, run_cnt, run_off, nruns, s));
@@ -887,7 +963,21 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         const size_t smem = (size_t)kSegStages * kSegBlock * nv * sizeof(double);
         FR_CUDA(cudaFuncSetAttribute(k_splat_segsum<D, Src>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        if (nruns > 0) {
+        const bool tree = !flat && contrib && nv >= 1 && nv <= 8;
+        if (nruns > 0 && tree) {
+            switch (nv) {
+#define FR_SEG_TREE(NVV)                                                                          \
+    case NVV:                                                                                     \
+        k_splat_segsum_tree<D, NVV><<<nruns, kSegBlock, 0, s>>>(run_slot, run_off, run_cnt,       \
+                                                                sorted_idx, contrib, (unsigned)cap, \
+                                                                run_vals, n);                     \
+        break;
+                FR_SEG_TREE(1) FR_SEG_TREE(2) FR_SEG_TREE(3) FR_SEG_TREE(4)
+                FR_SEG_TREE(5) FR_SEG_TREE(6) FR_SEG_TREE(7) FR_SEG_TREE(8)
+#undef FR_SEG_TREE
+            }
+            FR_CHECK_LAUNCH();
+        } else if (nruns > 0) {
             k_splat_segsum<D, Src><<<nruns, kSegBlock, smem, s>>>(
                 src, run_slot, run_off, run_cnt, sorted_idx, entry_bary, contrib, (unsigned)cap,
                 nv, run_vals, n);
@@ -1208,6 +1298,7 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
         set_error("lattice already blurred");
         return FR_ESTATE;
     }
+    PhaseClock pc(s);
     const int nv = lat->nv;
     const long long cap = std::max<long long>(64 * lat->n_sites, 200000);   // permutohedral.py:304
     unsigned long long hc[3];
@@ -1246,14 +1337,17 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
             FR_CHECK_LAUNCH();
             std::swap(lat->vals, lat->vals_alt);
         }
+        pc.lap("blur_axis");
     }
     FR_TRY(compact_nonzero<D>(lat, s));
+    pc.lap("compact");
     pool_free(lat, lat->hkeys);
     pool_free(lat, lat->hsite);
     lat->hkeys = nullptr;
     lat->hsite = nullptr;
     lat->hmask = 0;
     FR_TRY(build_slice_table<D>(lat, s));
+    pc.lap("slice_table");
     lat->blurred = 1;
     return FR_OK;
 }
@@ -1490,7 +1584,8 @@ int fr_lattice_splat_points(fr_lattice *lat, const float *pos, const float *nrm,
     int m2 = (value_mode & FR_VALUES_M2) ? 1 : 0;
     int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
     PointSrc src{pos, nrm, n, m2, nv};
-    return splat_impl<3, PointSrc>(lat, src, n, nv, (cudaStream_t)stream);
+    return splat_impl<3, PointSrc>(lat, src, n, nv, (cudaStream_t)stream, nullptr,
+                                   (value_mode & FR_SPLAT_FLAT_ORDER) != 0);
 }
 
 int fr_lattice_splat_points64(fr_lattice *lat, const double *pos, const double *nrm, int64_t n,
@@ -1511,7 +1606,8 @@ int fr_lattice_splat_points64(fr_lattice *lat, const double *pos, const double *
     int m2 = (value_mode & FR_VALUES_M2) ? 1 : 0;
     int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
     PointSrc64 src{pos, nrm, n, m2, nv};
-    return splat_impl<3, PointSrc64>(lat, src, n, nv, (cudaStream_t)stream);
+    return splat_impl<3, PointSrc64>(lat, src, n, nv, (cudaStream_t)stream, nullptr,
+                                     (value_mode & FR_SPLAT_FLAT_ORDER) != 0);
 }
 
 int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
@@ -1554,7 +1650,7 @@ int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, 
         cudaStreamDestroy(side);
         return st;
     };
-    return splat_impl<3, PointSrc>(lat, src, n, nv, s, &hook);
+    return splat_impl<3, PointSrc>(lat, src, n, nv, s, &hook, (value_mode & FR_SPLAT_FLAT_ORDER) != 0);
 }
 
 int fr_lattice_blur(fr_lattice *lat, void *stream) {

@@ -176,6 +176,20 @@ void worker_rows(int dev, int id, const double *src, long long a, long long b, d
     }
 }
 
+// true when [p, p + bytes) is page-locked host memory (cudaHostAlloc'd or
+// registered): both ends are checked, a failed query is cleared
+bool host_is_pinned(const void *p, size_t bytes) {
+    for (const char *q : {static_cast<const char *>(p), static_cast<const char *>(p) + bytes - 1}) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (at.type != cudaMemoryTypeHost) return false;
+    }
+    return true;
+}
+
 // (n, 3) rows -> (3, n) planes; a warp reads 768 contiguous bytes
 __global__ void k_rows_to_soa64(const double *__restrict__ rows, long long n,
                                 double *__restrict__ soa) {
@@ -224,15 +238,28 @@ __global__ void __launch_bounds__(kStatThreads) k_point_stats64(const double *__
     if (threadIdx.x < 9) part[blockIdx.x * 9 + threadIdx.x] = sh[threadIdx.x][0];
 }
 
+// 16 lanes per statistic each combine every 16th block row (loads issued
+// together), then lane 0 combines the 16 in order: fixed order throughout
 __global__ void k_point_stats64_final(const double *part, int nb, double *out) {
-    const int q = threadIdx.x;
-    if (q >= 9) return;
-    double v = part[q];
-    for (int b = 1; b < nb; ++b) {
-        const double x = part[b * 9 + q];
-        v = q < 3 ? v + x : (q < 6 ? fmin(v, x) : fmax(v, x));
+    __shared__ double sh[9][16];
+    const int q = threadIdx.x / 16, j = threadIdx.x % 16;
+    if (q < 9) {
+        const bool add = q < 3, mn = q >= 3 && q < 6;
+        double v = add ? 0.0 : (mn ? INFINITY : -INFINITY);
+#pragma unroll 4
+        for (int b = j; b < nb; b += 16) {
+            const double x = part[b * 9 + q];
+            v = add ? v + x : (mn ? fmin(v, x) : fmax(v, x));
+        }
+        sh[q][j] = v;
     }
-    out[q] = v;
+    __syncthreads();
+    if (j == 0 && q < 9) {
+        double v = sh[q][0];
+        for (int k = 1; k < 16; ++k)
+            v = q < 3 ? v + sh[q][k] : (q < 6 ? fmin(v, sh[q][k]) : fmax(v, sh[q][k]));
+        out[q] = v;
+    }
 }
 
 }  // namespace
@@ -305,6 +332,16 @@ extern "C" int fr_upload_rows64(const double *host_xyz, int64_t n, double *d_row
     }
     if (n == 0) return FR_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    if (host_is_pinned(host_xyz, (size_t)n * 3 * sizeof(double))) {
+        // page-locked rows (e.g. load_cloud(..., pinned=True)): one DMA at
+        // PCIe rate straight from the caller's buffer, no staging copy
+        FR_CUDA(cudaMemcpyAsync(d_rows, host_xyz, (size_t)n * 3 * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+        k_rows_to_soa64<<<blocks, 256, 0, s>>>(d_rows, n, d_soa);
+        FR_CHECK_LAUNCH();
+        return FR_OK;
+    }
     constexpr long long kSub = kSubChunk / 2;
     long long cap = 4;          // the copies are memcpy-bound: a few threads fill PCIe
     if (const char *e = getenv("FR_UPLOAD_WORKERS")) cap = std::max(1, std::min(kMaxWorkers, atoi(e)));
@@ -334,7 +371,6 @@ extern "C" int fr_upload_rows64(const double *host_xyz, int64_t n, double *d_row
                 return r.status;
             }
     }
-    const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
     k_rows_to_soa64<<<blocks, 256, 0, s>>>(d_rows, n, d_soa);
     FR_CHECK_LAUNCH();
     return FR_OK;
@@ -354,7 +390,7 @@ extern "C" int fr_point_stats64(const double *d_soa, int64_t n, double *d_work, 
     cudaStream_t s = (cudaStream_t)stream;
     k_point_stats64<<<kStatBlocks, kStatThreads, 0, s>>>(d_soa, n, d_work);
     FR_CHECK_LAUNCH();
-    k_point_stats64_final<<<1, 32, 0, s>>>(d_work, kStatBlocks, d_out);
+    k_point_stats64_final<<<1, 144, 0, s>>>(d_work, kStatBlocks, d_out);
     FR_CHECK_LAUNCH();
     return FR_OK;
 }

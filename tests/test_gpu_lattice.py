@@ -58,10 +58,33 @@ def test_point_splat_equals_generic_splat(fr):
     Y = g["features"]
     lat = fr.PermutohedralLattice(3, g["sigma"])
     soa = torch.from_numpy(np.ascontiguousarray(Y.T, dtype=np.float32)).cuda()
-    lat.splat_points(soa, None, _lib.FR_VALUES_M2)
+    lat.splat_points(soa, None, _lib.FR_VALUES_M2 | _lib.FR_SPLAT_FLAT_ORDER)
     lat.blur()
     assert np.array_equal(lat.keys, g["post_keys"].astype(np.int64))
     assert np.array_equal(lat.values, g["post_values"])
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_point_splat_tree_order_within_roundoff(fr, f64):
+    """The EM path's default point splat (fixed-tree site sums): keys and
+    occupied sites bit-exact, values within float64 round-off of np.add.at's
+    flat order, and bit-identical from run to run."""
+    import torch
+    from paper_1811_10136_b200 import _lib
+    g = load("lattice_pebble_s5")
+    Y = g["features"]
+    dt = np.float64 if f64 else np.float32
+    soa = torch.from_numpy(np.ascontiguousarray(Y.T, dtype=dt)).cuda()
+    out = []
+    for _ in range(2):
+        lat = fr.PermutohedralLattice(3, g["sigma"])
+        lat.splat_points(soa, None, _lib.FR_VALUES_M2)
+        lat.blur()
+        out.append((lat.keys, lat.values))
+    assert np.array_equal(out[0][0], g["post_keys"].astype(np.int64))
+    scale = np.abs(g["post_values"]).max(axis=0)
+    assert np.all(np.abs(out[0][1] - g["post_values"]) <= 1e-13 * scale)
+    assert np.array_equal(out[0][1], out[1][1])
 
 
 def test_moments_match_reference(fr):

@@ -2,7 +2,7 @@
 device-synchronised phases of RigidDevicePath; FR_SPLAT_TIMING=1: the splat's
 own phases on stderr), then the EM object, the loop and the result read.
 
-    python tools/setup64_profile.py [points]
+    python tools/setup64_profile.py [points] [--pinned]
 """
 import os
 import sys
@@ -18,13 +18,16 @@ from oracle import filterreg_oracle as O  # noqa: E402  (diagnostic input genera
 import paper_1811_10136_b200 as fr  # noqa: E402
 from paper_1811_10136_b200 import _rigid  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+n = int(args[0]) if args else 1_000_000
 model, obs, _ = O.pebble_pair(n, outlier_ratio=0.05, seed=0)
 X = model.astype(np.float32).astype(float)
 Y = obs.astype(np.float32).astype(float)
 gmm = fr.GmmConfig(sigma=0.05 * O.bbox_diameter(X[:n]), outlier_ratio=0.1)
 cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=50, twist_tolerance=1e-30)
 ref, ob = fr.PointCloud(X), fr.PointCloud(Y)
+if "--pinned" in sys.argv:
+    ref, ob = fr.pinned_cloud(ref), fr.pinned_cloud(ob)
 for rep in range(4):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
