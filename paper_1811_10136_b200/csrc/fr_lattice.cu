@@ -447,6 +447,89 @@ __global__ void k_jacobi(long long S, int axis, const int *site_keys, const doub
     }
 }
 
+// device-resident blur (no host round trip per axis): the site count lives in
+// counters[0], the nonzero count of the axis in counters[1], error flags in
+// counters[2], the extension's loop bound in counters[3]; grid-stride kernels
+// read their bounds from there.  Site rows past the count stay zero in both
+// value buffers (zeroed once up front; the Jacobi pass writes rows < count).
+__global__ void k_count_nonzero_dev(const double *vals, int nv, unsigned long long *ctr) {
+    const long long S = (long long)ctr[0];
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    unsigned long long mine = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
+        bool nz = false;
+        for (int c = 0; c < nv; ++c) nz |= vals[i * nv + c] != 0.0;
+        mine += nz;
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&ctr[1], mine);
+}
+
+// permutohedral.py:304-306: the axis extends only while S + 2 nsrc <= cap
+__global__ void k_blur_decide(unsigned long long *ctr, long long cap) {
+    const unsigned long long S = ctr[0], nsrc = ctr[1];
+    ctr[3] = (S + 2 * nsrc <= (unsigned long long)cap && nsrc > 0) ? S : 0ull;
+}
+
+template <int D>
+__global__ void k_extend_dev(int axis, const double *vals, int nv, BuildHash h, int *site_keys,
+                             unsigned long long *ctr) {
+    const long long S = (long long)ctr[3];
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
+        bool nz = false;
+        for (int c = 0; c < nv; ++c) nz |= vals[i * nv + c] != 0.0;
+        if (!nz) continue;
+        int k[D + 1];
+#pragma unroll
+        for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
+#pragma unroll
+        for (int sgn = -1; sgn <= 1; sgn += 2) {
+            int nk[D + 1];
+#pragma unroll
+            for (int q = 0; q <= D; ++q) nk[q] = k[q] + sgn;
+            nk[axis] -= sgn * (D + 1);
+            bool ok = true;
+#pragma unroll
+            for (int q = 0; q < D; ++q) ok &= (nk[q] > -kKeyLim) && (nk[q] < kKeyLim);
+            if (!ok) { atomicOr(&ctr[2], 1ull); continue; }
+            int created;
+            int sl = hash_insert(h, pack_key<D>(nk), &created);
+            if (sl < 0) { atomicOr(&ctr[2], 2ull); continue; }
+            if (created) {
+                long long id = (long long)atomicAdd(&ctr[0], 1ull);
+                h.site[sl] = (int)id;
+#pragma unroll
+                for (int q = 0; q <= D; ++q) site_keys[id * (D + 1) + q] = nk[q];
+            }
+        }
+    }
+}
+
+template <int D>
+__global__ void k_jacobi_dev(int axis, const int *site_keys, const double *vin, double *vout,
+                             int nv, BuildHash h, const unsigned long long *ctr) {
+    const long long S = (long long)ctr[0];
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
+        int k[D + 1], up[D + 1], dn[D + 1];
+#pragma unroll
+        for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
+#pragma unroll
+        for (int q = 0; q <= D; ++q) { up[q] = k[q] + 1; dn[q] = k[q] - 1; }
+        up[axis] = k[axis] - D;
+        dn[axis] = k[axis] + D;
+        int iu = hash_find(h, pack_key<D>(up));
+        int id = hash_find(h, pack_key<D>(dn));
+        for (int c = 0; c < nv; ++c) {
+            double vu = iu >= 0 ? vin[(long long)iu * nv + c] : 0.0;
+            double vd = id >= 0 ? vin[(long long)id * nv + c] : 0.0;
+            vout[i * nv + c] = __dadd_rn(__dmul_rn(0.5, vin[i * nv + c]),
+                                         __dmul_rn(0.25, __dadd_rn(vu, vd)));
+        }
+    }
+}
+
 template <int D>
 __global__ void k_gather_sites(int S, const int *idx, const int *kin, const double *vin,
                                int nv, int *kout, double *vout) {
@@ -1288,6 +1371,10 @@ static int build_slice_table(fr_lattice *lat, cudaStream_t s) {
     return FR_OK;
 }
 
+// site capacity up to which the blur runs device-resident (its whole capacity
+// and hash allocated up front: <= 4M sites, ~0.5 GB)
+constexpr long long kDeviceBlurMaxSites = 1LL << 22;
+
 template <int D>
 static int blur_impl(fr_lattice *lat, cudaStream_t s) {
     if (!lat->splatted) {
@@ -1302,7 +1389,41 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
     const int nv = lat->nv;
     const long long cap = std::max<long long>(64 * lat->n_sites, 200000);   // permutohedral.py:304
     unsigned long long hc[3];
-    for (int axis = 0; axis <= D; ++axis) {
+    if (cap <= kDeviceBlurMaxSites) {
+        // every site the blur can create fits up front: no host round trip
+        // until the end (one read of the final count and flags)
+        FR_TRY(reserve_sites(lat, cap, s));
+        const long long S0 = lat->n_sites;
+        FR_CUDA(cudaMemsetAsync(lat->vals + S0 * nv, 0, (size_t)(cap - S0) * nv * sizeof(double), s));
+        FR_CUDA(cudaMemsetAsync(lat->vals_alt + S0 * nv, 0,
+                                (size_t)(cap - S0) * nv * sizeof(double), s));
+        const unsigned long long hslots = next_pow2(4ull * (unsigned long long)cap);
+        if (hslots > (unsigned long long)lat->hmask + 1)
+            FR_TRY(rehash_sites<D>(lat, (unsigned)hslots, s));
+        k_fill_u64<<<1, 32, 0, s>>>(lat->d_counters, (unsigned long long)S0, 0ull, 0ull);
+        FR_CHECK_LAUNCH();
+        const BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
+        const unsigned g = 148 * 8;
+        for (int axis = 0; axis <= D; ++axis) {
+            FR_CUDA(cudaMemsetAsync(lat->d_counters + 1, 0, sizeof(unsigned long long), s));
+            k_count_nonzero_dev<<<g, 256, 0, s>>>(lat->vals, nv, lat->d_counters);
+            k_blur_decide<<<1, 1, 0, s>>>(lat->d_counters, cap);
+            k_extend_dev<D><<<g, 256, 0, s>>>(axis, lat->vals, nv, h, lat->site_keys,
+                                              lat->d_counters);
+            k_jacobi_dev<D><<<g, 256, 0, s>>>(axis, lat->site_keys, lat->vals, lat->vals_alt, nv,
+                                              h, lat->d_counters);
+            FR_CHECK_LAUNCH();
+            std::swap(lat->vals, lat->vals_alt);
+        }
+        FR_TRY(read_counters(lat, s, hc));
+        if (hc[2] & 2ull) {
+            set_error("blur hash table overflow");
+            return FR_ECAPACITY;
+        }
+        lat->n_sites = (long long)hc[0];
+        pc.lap("blur_axes");
+    }
+    for (int axis = 0; axis <= D && cap > kDeviceBlurMaxSites; ++axis) {
         long long S = lat->n_sites;
         FR_CUDA(cudaMemsetAsync(lat->d_counters, 0, 3 * sizeof(unsigned long long), s));
         if (S > 0) {
