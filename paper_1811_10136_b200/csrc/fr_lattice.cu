@@ -275,15 +275,18 @@ k_splat_segsum(Src src, const unsigned *run_slot, const int *run_off, const int 
     if (t < nv) run_vals[(long long)r * nv + t] = acc;
 }
 
-// splat phase 2, fixed-tree order (the point splats of the EM path): one
-// block per site, 256 entries per chunk; every thread gathers one entry row
-// (the next chunk's row prefetched into registers), each warp sums its 32
-// rows per column by a shuffle tree, the 8 warp sums are added in warp order
-// and the chunk sums in chunk order.  Deterministic (no atomics, no order
-// that depends on scheduling) but not np.add.at's flat order: site sums
-// differ from it by float64 round-off (the reference's own sums carry the
-// same order of error), and the serial chain is cnt / 256 adds long instead
-// of cnt -- the flat-order kernel's bound at heavy sites.
+// splat phase 2, fixed-tree order (the point splats of the EM path).  Each
+// site's sorted entries are cut into pieces of kSegPiece; one block per piece
+// (a heavy site -- 2e4 entries at C5 1M -- spreads over many SMs): every
+// thread gathers one entry row per 256-entry chunk (the next chunk's row
+// prefetched into registers), each warp sums its 32 rows per column by a
+// shuffle tree, the 8 warp sums add in warp order, the chunk sums in chunk
+// order; k_seg_pieces_combine adds a site's piece sums in piece order.
+// Deterministic (no atomics, no scheduling-dependent order) but not
+// np.add.at's flat order: site sums differ from it by float64 round-off (the
+// reference's own sums carry the same order of error).
+constexpr int kSegPiece = 1024;
+
 template <int NV>
 __device__ __forceinline__ void seg_row(const unsigned *sorted_idx, const double *contrib,
                                         long long lmajor_n, int D1, int beg, int j, int cnt,
@@ -300,17 +303,39 @@ __device__ __forceinline__ void seg_row(const unsigned *sorted_idx, const double
     }
 }
 
+// pieces per run (0 for the sentinel run)
+__global__ void k_seg_piece_counts(int n_runs, const unsigned *run_slot, unsigned sentinel,
+                                   const int *run_cnt, int *pieces) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_runs) return;
+    const bool skip = run_slot && run_slot[r] == sentinel;
+    pieces[r] = skip ? 0 : (run_cnt[r] + kSegPiece - 1) / kSegPiece;
+}
+
 template <int D, int NV>
 __global__ void __launch_bounds__(kSegBlock)
-k_splat_segsum_tree(const unsigned *run_slot, const int *run_off, const int *run_cnt,
-                    const unsigned *sorted_idx, const double *contrib, unsigned sentinel,
-                    double *run_vals, long long lmajor_n) {
+k_splat_segsum_tree(int n_runs, const int *piece_off, const int *run_off, const int *run_cnt,
+                    const unsigned *sorted_idx, const double *contrib, double *piece_vals,
+                    long long lmajor_n) {
     constexpr int W = kSegBlock / 32;
     __shared__ double wsum[W][NV];
-    const int r = blockIdx.x;
-    if (run_slot && run_slot[r] == sentinel) return;
-    const int beg = run_off[r], cnt = run_cnt[r];
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    __shared__ int s_run;
+    const int pc = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) {
+        // the run owning piece pc: last r with piece_off[r] <= pc
+        int lo = 0, hi = n_runs;          // piece_off has n_runs + 1 entries
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (piece_off[mid] <= pc) lo = mid;
+            else hi = mid;
+        }
+        s_run = pc < piece_off[n_runs] ? lo : -1;
+    }
+    __syncthreads();
+    const int r = s_run;
+    if (r < 0) return;
+    const int j0 = (pc - piece_off[r]) * kSegPiece;
+    const int beg = run_off[r] + j0, cnt = min(kSegPiece, run_cnt[r] - j0);
     double cur[NV], nxt[NV];
     seg_row<NV>(sorted_idx, contrib, lmajor_n, D + 1, beg, t, cnt, cur);
     double acc = 0.0;
@@ -334,7 +359,18 @@ k_splat_segsum_tree(const unsigned *run_slot, const int *run_off, const int *run
 #pragma unroll
         for (int c = 0; c < NV; ++c) cur[c] = nxt[c];
     }
-    if (t < NV) run_vals[(long long)r * NV + t] = acc;
+    if (t < NV) piece_vals[(long long)pc * NV + t] = acc;
+}
+
+// run_vals[r] = its pieces' sums in piece order (zero for the sentinel run)
+__global__ void k_seg_pieces_combine(int n_runs, const int *piece_off, const double *piece_vals,
+                                     int nv, double *run_vals) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)n_runs * nv) return;
+    const int r = (int)(q / nv), c = (int)(q % nv);
+    double acc = 0.0;
+    for (int p = piece_off[r]; p < piece_off[r + 1]; ++p) acc += piece_vals[(long long)p * nv + c];
+    run_vals[q] = acc;
 }
 
 __global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentinel,
@@ -1048,17 +1084,36 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const bool tree = !flat && contrib && nv >= 1 && nv <= 8;
         if (nruns > 0 && tree) {
+            // pieces per run -> exclusive offsets (n_runs + 1; the last is the
+            // total); the launch takes the upper bound runs + E / piece
+            int *pieces, *piece_off;
+            double *piece_vals;
+            const long long max_pieces = (long long)nruns + E / kSegPiece + 1;
+            FR_TRY(sc.get(&pieces, (size_t)nruns + 1));
+            FR_TRY(sc.get(&piece_off, (size_t)nruns + 1));
+            FR_TRY(sc.get(&piece_vals, (size_t)max_pieces * nv));
+            FR_CUDA(cudaMemsetAsync(pieces + nruns, 0, sizeof(int), s));
+            k_seg_piece_counts<<<grid_for(nruns), 256, 0, s>>>(nruns, run_slot, (unsigned)cap,
+                                                               run_cnt, pieces);
+            FR_CHECK_LAUNCH();
+            size_t t4 = 0;
+            FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t4, pieces, piece_off, nruns + 1, s));
+            void *tmp4;
+            FR_TRY(sc.get((char **)&tmp4, t4));
+            FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp4, t4, pieces, piece_off, nruns + 1, s));
             switch (nv) {
 #define FR_SEG_TREE(NVV)                                                                          \
     case NVV:                                                                                     \
-        k_splat_segsum_tree<D, NVV><<<nruns, kSegBlock, 0, s>>>(run_slot, run_off, run_cnt,       \
-                                                                sorted_idx, contrib, (unsigned)cap, \
-                                                                run_vals, n);                     \
+        k_splat_segsum_tree<D, NVV><<<(unsigned)max_pieces, kSegBlock, 0, s>>>(                  \
+            nruns, piece_off, run_off, run_cnt, sorted_idx, contrib, piece_vals, n);              \
         break;
                 FR_SEG_TREE(1) FR_SEG_TREE(2) FR_SEG_TREE(3) FR_SEG_TREE(4)
                 FR_SEG_TREE(5) FR_SEG_TREE(6) FR_SEG_TREE(7) FR_SEG_TREE(8)
 #undef FR_SEG_TREE
             }
+            FR_CHECK_LAUNCH();
+            k_seg_pieces_combine<<<grid_for((long long)nruns * nv), 256, 0, s>>>(
+                nruns, piece_off, piece_vals, nv, run_vals);
             FR_CHECK_LAUNCH();
         } else if (nruns > 0) {
             k_splat_segsum<D, Src><<<nruns, kSegBlock, smem, s>>>(
