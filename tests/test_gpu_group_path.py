@@ -48,7 +48,7 @@ def test_group_path_equals_single(nccl_group, m):
                     process_group=nccl_group)
     assert a.iterations == b.iterations and a.termination == b.termination
     Ra, Rb = a.kinematics.pose.rotation, b.kinematics.pose.rotation
-    assert O.rotation_angle(Ra @ Rb.T) < 1e-9
+    assert np.abs(Ra - Rb).max() < 1e-10       # entrywise: acos resolves ~2e-8 at best
     assert np.linalg.norm(a.kinematics.pose.translation - b.kinematics.pose.translation) < \
         1e-9 * O.bbox_diameter(X[:m])
     np.testing.assert_allclose(a.objectives, b.objectives, rtol=1e-10)
