@@ -42,7 +42,6 @@
 
 namespace fr {
 
-constexpr int kE64Threads = 256;
 constexpr int kE64Stats = 25;        // point-to-point sufficient statistics (_rigid.py)
 
 struct Em64Args {
@@ -220,6 +219,36 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
                     if (lane == 0) mbar_arrive(&empty[st]);
                     e64_point(a, pose, cp, h0, h1, h2, pidx < a.m, acc);
                 }
+            } else if (THREADS <= 256) {
+                // two tiles per step: two independent point chains in one
+                // basic block for the scheduler to interleave (the pass is
+                // FP64-latency bound at 8 warps per SM); the next pair is
+                // prefetched into registers
+                double nx[2] = {0.0, 0.0}, ny[2] = {0.0, 0.0}, nz[2] = {0.0, 0.0};
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+                    if (u < nt) {
+                        nx[u] = __ldg(src + u * 3 * THREADS);
+                        ny[u] = __ldg(src + u * 3 * THREADS + THREADS);
+                        nz[u] = __ldg(src + u * 3 * THREADS + 2 * THREADS);
+                    }
+                int tt = 0;
+                for (; tt + 1 < nt; tt += 2, pidx += 2 * THREADS) {
+                    const double a0 = nx[0], a1 = ny[0], a2 = nz[0];
+                    const double b0 = nx[1], b1 = ny[1], b2 = nz[1];
+                    src += 6 * THREADS;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u)
+                        if (tt + 2 + u < nt) {
+                            nx[u] = __ldg(src + u * 3 * THREADS);
+                            ny[u] = __ldg(src + u * 3 * THREADS + THREADS);
+                            nz[u] = __ldg(src + u * 3 * THREADS + 2 * THREADS);
+                        }
+                    e64_point(a, pose, cp, a0, a1, a2, pidx < a.m, acc);
+                    e64_point(a, pose, cp, b0, b1, b2, pidx + THREADS < a.m, acc);
+                }
+                if (tt < nt) e64_point(a, pose, cp, nx[0], ny[0], nz[0], pidx < a.m, acc);
+                n += nt;
             } else {
                 double nx = 0.0, ny = 0.0, nz = 0.0;
                 if (nt > 0) {
@@ -351,10 +380,13 @@ __global__ void k_em64_solve(const double *sums, EmDev *e, double *traces) {
         reinterpret_cast<unsigned long long *>(e)[q] = src[q];
 }
 
-// launch variants (FR_EM64_VARIANT): 0 (default) = 512 consumer threads x 1
-// CTA/SM with a per-thread register prefetch of the next point; 1 = 384 x 1
-// with an 8-stage TMA bulk-copy ring fed by a producer warp (measured slower:
-// the pass is issue / FP64-latency bound, not stream bound)
+// launch variants (FR_EM64_VARIANT): 0 (default) = 256 threads x 1 CTA/SM, 255
+// registers (no spills, the solve inlined), two points per thread and step
+// with the next pair prefetched into registers; 2 = 512 x 1 with one point
+// per step (128 registers: 116 B of spills; 10-20% slower per iteration);
+// 1 = 384 x 1 with an 8-stage TMA bulk-copy ring fed by a producer warp
+// (slower still: the pass is issue / FP64-latency bound, not stream bound;
+// DESIGN.md)
 using E64Kernel = void (*)(Em64Args, const Em64Args *);
 struct E64Variant {
     E64Kernel fn, batch;
@@ -370,7 +402,8 @@ static E64Variant e64_variant() {
         v = e ? atoi(e) : 0;
     }
     if (v == 1) return {k_em64<384, 1, 8, false>, k_em64<384, 1, 8, true>, 384, 1, 8};
-    return {k_em64<512, 1, 0, false>, k_em64<512, 1, 0, true>, 512, 1, 0};
+    if (v == 2) return {k_em64<512, 1, 0, false>, k_em64<512, 1, 0, true>, 512, 1, 0};
+    return {k_em64<256, 1, 0, false>, k_em64<256, 1, 0, true>, 256, 1, 0};
 }
 
 static int e64_grid(const E64Variant &k) {
