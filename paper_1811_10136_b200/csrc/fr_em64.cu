@@ -52,7 +52,7 @@ struct Em64Args {
     EmDev *em;           // state; em->k holds the current pass constants
     double *partials;    // [gridDim.x][kE64Row]
     double *sums;        // [kE64Row] the last pass's reduced statistics
-    double *traces;      // [3][max_iters]
+    double *traces;      // [4][max_iters]: objectives, update magnitudes, masses, cos(angle)
     unsigned *counter;   // arrivals of the current iteration
     unsigned *gen;       // release generation
     int n_iters;         // iterations of this launch (or fewer: termination)
@@ -189,6 +189,8 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     if (producer && lane == 0) produce_until(SS);
     unsigned n = 0;                          // consumed tiles (uniform)
     int it = 0;
+    constexpr bool kInlineSolve = MINB == 1 && THREADS <= 256;
+    const int it0 = se.iterations;           // the state's iteration count at entry
     for (; it < a.n_iters; ++it) {
         if (a.solve && se.done) break;          // identical in every CTA
         if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 0] = gtime();
@@ -322,10 +324,11 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
         if (a.solve) {
             if (tid == 0) {
                 const int n = se.max_em_iters;
-                if (MINB == 1 && THREADS <= 256)   // 255 registers: the solve inlined
-                    rigid_solve_impl(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
-                                     blockIdx.x == 0,
-                                     a.prof && blockIdx.x == 0 ? a.prof + 8 * it + 5 : nullptr);
+                if (kInlineSolve)   // 255 registers: the lean solve inlined
+                    rigid_solve_impl<true>(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
+                                           blockIdx.x == 0,
+                                           a.prof && blockIdx.x == 0 ? a.prof + 8 * it + 5 : nullptr,
+                                           a.traces + 3 * n);
                 else
                     rigid_solve_body(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
                                      blockIdx.x == 0,
@@ -335,6 +338,10 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
         }
         if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 4] = gtime();
     }
+    // the deferred update magnitudes of this launch's iterations (lean solve)
+    if (kInlineSolve && a.solve && blockIdx.x == 0)
+        rigid_finish_tnorms(a.traces + se.max_em_iters, a.traces + 3 * se.max_em_iters, it0,
+                            se.iterations);
     // no bulk copy may still target this CTA's shared memory when it exits
     if (producer && lane == 0)
         for (; n < issued; ++n) mbar_wait(&full[n % SS], (n / SS) & 1);
@@ -547,7 +554,7 @@ int fr_em64_create(const fr_lattice *lat, const double *ref, int64_t m,
         cudaMallocAsync((void **)&em->d_partials,
                         (size_t)2 * kE64MaxSms * kv.minb * kE64Row * sizeof(double), s) !=
             cudaSuccess ||
-        cudaMallocAsync((void **)&em->d_traces, (size_t)3 * cfg->max_em_iters * sizeof(double), s) !=
+        cudaMallocAsync((void **)&em->d_traces, (size_t)4 * cfg->max_em_iters * sizeof(double), s) !=
             cudaSuccess ||
         cudaMallocAsync((void **)&em->d_sync, 2 * sizeof(unsigned), s) != cudaSuccess ||
         cudaMemcpyAsync(em->d_em, &h, sizeof(EmDev), cudaMemcpyHostToDevice, s) != cudaSuccess ||
