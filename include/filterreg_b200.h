@@ -385,6 +385,10 @@ int fr_em64_run(fr_em64 *em, int n_iters, void *stream);
 int fr_em64_run_batch(fr_em64 **ems, int n, void *stream);
 int fr_em64_pass(fr_em64 *em, void *stream);
 int fr_em64_solve(fr_em64 *em, void *stream);
+/* device address of the loop's termination flag (int, non-zero once done):
+ * a sharded driver reads it asynchronously into pinned memory between
+ * replays of its captured pass -> all-reduce -> solve chunks */
+int fr_em64_done_ptr(fr_em64 *em, int **d_done);
 int fr_em64_sums(fr_em64 *em, double **d_sums, int *width);
 /* CTAs and threads per CTA of the grid-resident kernel (launch accounting) */
 int fr_em64_launch_info(const fr_em64 *em, int *grid, int *block);

@@ -567,6 +567,19 @@ class _DeviceArray:
                                          "data": (int(ptr), False), "version": 3}
 
 
+class _DeviceInts:
+    """__cuda_array_interface__ view of a raw device int32 buffer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+# sharded float64 loop over NCCL: replay captured chunks (False: the per-
+# iteration Python loop with a synchronising status poll per chunk)
+GROUP_GRAPH = True
+
+
 class DeviceEM:
     """The whole rigid point-to-point EM loop resident on the GPU
     (fr_rigid_em_*): pass, fixed-order reduction and the float64 solver kernel
@@ -696,12 +709,16 @@ class DeviceEM64:
                                            ctypes.byref(c), _lib.stream_handle(),
                                            ctypes.byref(h)))
         self.h = h
+        self._graph = None
         sp = ctypes.c_void_p()
         w = ctypes.c_int()
         _lib.check(self.lib.fr_em64_sums(h, ctypes.byref(sp), ctypes.byref(w)))
         self.sums = torch.as_tensor(_DeviceArray(sp.value, w.value), device=path.dev)
+        if path.group is not None and type(self) is DeviceEM64 and self._nccl_group():
+            self._capture()
 
     def __del__(self):
+        self._graph = None             # the captured chunk goes before its buffers
         h = getattr(self, "h", None)
         if h is not None and h.value:
             try:
@@ -716,14 +733,61 @@ class DeviceEM64:
         return int(g.value), int(b.value)
 
     def enqueue(self, n: int) -> None:
-        """Enqueue up to n more iterations without synchronising."""
+        """Enqueue up to n more iterations without synchronising (sharded over
+        NCCL: whole chunks as replays of the captured graph)."""
         if self.path.group is None:
             _lib.check(self.lib.fr_em64_run(self.h, int(n), _lib.stream_handle()))
             return
+        n = int(n)
+        if self._graph is not None:
+            q, n = divmod(n, self.CHUNK)
+            for _ in range(q):
+                self._graph.replay()
+        self._enqueue_eager(n)
+
+    def _enqueue_eager(self, n: int) -> None:
         for _ in range(int(n)):
             _lib.check(self.lib.fr_em64_pass(self.h, _lib.stream_handle()))
             self.path.reduce_device(self.sums)
             _lib.check(self.lib.fr_em64_solve(self.h, _lib.stream_handle()))
+
+    def _capture(self) -> None:
+        """CHUNK iterations of pass -> all-reduce -> solve as one CUDA graph
+        (captured at construction: nothing runs; the replays do)."""
+        import torch
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._enqueue_eager(self.CHUNK)
+        self._graph = g
+        dp = ctypes.c_void_p()
+        _lib.check(self.lib.fr_em64_done_ptr(self.h, ctypes.byref(dp)))
+        self._done = torch.as_tensor(_DeviceInts(dp.value, 1), device=self.path.dev)
+        self._flags = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+        self._events = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def _nccl_group(self) -> bool:
+        import torch.distributed as dist
+        return GROUP_GRAPH and dist.get_backend(self.path.group) == "nccl"
+
+    def _run_graph(self) -> None:
+        """Sharded loop over NCCL: replays of the captured chunk (no Python
+        call per iteration); the termination flag is copied into a pinned
+        double buffer after every replay and the previous replay's flag is
+        read while the current one runs.  Every rank replays the same number
+        of chunks (identical reduced sums -> identical flags); passes after
+        termination are no-ops inside the kernel."""
+        import torch
+        chunks = (self.max_iters + self.CHUNK - 1) // self.CHUNK
+        for k in range(chunks + 1):
+            self._graph.replay()
+            self._flags[k % 2:k % 2 + 1].copy_(self._done, non_blocking=True)
+            self._events[k % 2].record()
+            if k >= 1:
+                self._events[(k - 1) % 2].synchronize()
+                if int(self._flags[(k - 1) % 2]):
+                    return
+        torch.cuda.current_stream().synchronize()
 
     def pass_only(self) -> None:
         """One pass + reduction at the current pose (no solve)."""
@@ -738,6 +802,9 @@ class DeviceEM64:
     def run(self) -> None:
         if self.path.group is None:
             _lib.check(self.lib.fr_em64_run(self.h, 0, _lib.stream_handle()))
+            return
+        if self._graph is not None:
+            self._run_graph()
             return
         while True:
             self.enqueue(self.CHUNK)

@@ -12,7 +12,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libfilterreg_b200.so")
+# FR_BUILD_OUT / FR_NVCC_EXTRA: an alternative output and extra nvcc flags
+# (A/B builds of compile-time variants, loaded through FR_LIB)
+OUT = os.environ.get("FR_BUILD_OUT", os.path.join(HERE, "libfilterreg_b200.so"))
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-Xptxas", "-warn-spills"]
 
@@ -40,7 +42,10 @@ def build(force: bool = False, verbose: bool = True) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     with tempfile.TemporaryDirectory(prefix="fr_build_") as tmp:
         objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in sources()]
-        cmds = [[nvcc, *NVCC_FLAGS, "-c", "-o", obj, src] for src, obj in zip(sources(), objs)]
+        import shlex
+        extra = shlex.split(os.environ.get("FR_NVCC_EXTRA", ""))
+        cmds = [[nvcc, *NVCC_FLAGS, *extra, "-c", "-o", obj, src]
+                for src, obj in zip(sources(), objs)]
         if verbose:
             for c in cmds:
                 print(" ".join(c), flush=True)

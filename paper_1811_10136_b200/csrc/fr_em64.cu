@@ -144,6 +144,11 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+#ifndef FR_EM64_PTS
+#define FR_EM64_PTS 2
+#endif
+constexpr int kEmPts = FR_EM64_PTS;     // points per thread and step (256-thread variant)
+
 template <int THREADS, int MINB, int S>
 __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     // S > 0: warp W produces tiles into an S-stage TMA ring; S == 0: every
@@ -192,7 +197,9 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     constexpr bool kInlineSolve = MINB == 1 && THREADS <= 256;
     const int it0 = se.iterations;           // the state's iteration count at entry
     for (; it < a.n_iters; ++it) {
-        if (a.solve && se.done) break;          // identical in every CTA
+        // identical in every CTA; a pass-only launch after termination is a
+        // no-op too (the sharded loop's replayed chunks run past the end)
+        if (se.done) break;
         if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 0] = gtime();
         double acc[kE64Stats];
 #pragma unroll
@@ -222,34 +229,46 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
                     e64_point(a, pose, cp, h0, h1, h2, pidx < a.m, acc);
                 }
             } else if (THREADS <= 256) {
-                // two tiles per step: two independent point chains in one
-                // basic block for the scheduler to interleave (the pass is
-                // FP64-latency bound at 8 warps per SM); the next pair is
+                // kEmPts tiles per step: independent point chains in one basic
+                // block for the scheduler to interleave (the pass is FP64-
+                // latency bound at 8 warps per SM); the next group is
                 // prefetched into registers
-                double nx[2] = {0.0, 0.0}, ny[2] = {0.0, 0.0}, nz[2] = {0.0, 0.0};
+                constexpr int P = kEmPts;
+                double nx[P], ny[P], nz[P];
 #pragma unroll
-                for (int u = 0; u < 2; ++u)
+                for (int u = 0; u < P; ++u) {
+                    nx[u] = ny[u] = nz[u] = 0.0;
                     if (u < nt) {
                         nx[u] = __ldg(src + u * 3 * THREADS);
                         ny[u] = __ldg(src + u * 3 * THREADS + THREADS);
                         nz[u] = __ldg(src + u * 3 * THREADS + 2 * THREADS);
                     }
+                }
                 int tt = 0;
-                for (; tt + 1 < nt; tt += 2, pidx += 2 * THREADS) {
-                    const double a0 = nx[0], a1 = ny[0], a2 = nz[0];
-                    const double b0 = nx[1], b1 = ny[1], b2 = nz[1];
-                    src += 6 * THREADS;
+                for (; tt + P - 1 < nt; tt += P, pidx += P * THREADS) {
+                    double hx[P], hy[P], hz[P];
 #pragma unroll
-                    for (int u = 0; u < 2; ++u)
-                        if (tt + 2 + u < nt) {
+                    for (int u = 0; u < P; ++u) {
+                        hx[u] = nx[u];
+                        hy[u] = ny[u];
+                        hz[u] = nz[u];
+                    }
+                    src += 3 * P * THREADS;
+#pragma unroll
+                    for (int u = 0; u < P; ++u)
+                        if (tt + P + u < nt) {
                             nx[u] = __ldg(src + u * 3 * THREADS);
                             ny[u] = __ldg(src + u * 3 * THREADS + THREADS);
                             nz[u] = __ldg(src + u * 3 * THREADS + 2 * THREADS);
                         }
-                    e64_point(a, pose, cp, a0, a1, a2, pidx < a.m, acc);
-                    e64_point(a, pose, cp, b0, b1, b2, pidx + THREADS < a.m, acc);
+#pragma unroll
+                    for (int u = 0; u < P; ++u)
+                        e64_point(a, pose, cp, hx[u], hy[u], hz[u], pidx + u * THREADS < a.m, acc);
                 }
-                if (tt < nt) e64_point(a, pose, cp, nx[0], ny[0], nz[0], pidx < a.m, acc);
+#pragma unroll
+                for (int u = 0; u < P - 1; ++u)
+                    if (tt + u < nt)
+                        e64_point(a, pose, cp, nx[u], ny[u], nz[u], pidx + u * THREADS < a.m, acc);
                 n += nt;
             } else {
                 double nx = 0.0, ny = 0.0, nz = 0.0;
@@ -666,6 +685,15 @@ int fr_em64_pass(fr_em64 *em, void *stream) {
     }
     em->stream = (cudaStream_t)stream;
     return e64_launch(em, 1, 0, (cudaStream_t)stream);
+}
+
+int fr_em64_done_ptr(fr_em64 *em, int **d_done) {
+    if (!em || !d_done) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    *d_done = &em->d_em->done;
+    return FR_OK;
 }
 
 int fr_em64_solve(fr_em64 *em, void *stream) {
