@@ -39,7 +39,10 @@ for _ in range(2):
     em.run()
     torch.cuda.synchronize()
 res = em.result()
-em.pass_only()
+# the pass alone on a fresh state (a pass-only launch on a finished loop is a
+# no-op by design)
+fresh = _rigid.DeviceEM64(path, np.eye(3), np.zeros(3), cfg)
+fresh.pass_only()
 torch.cuda.synchronize()
 print("f64 loop:", res[5], res[6], "R trace", float(np.trace(res[0])), flush=True)
 if a.f32:
