@@ -648,9 +648,9 @@ __device__ __forceinline__ bool chol6_col(double (&A)[36], double *rd) {
 #pragma unroll
     for (int k = 0; k < J; ++k) d -= A[6 * J + k] * A[6 * J + k];
     const bool good = d > 0.0 && isfinite(d);
-    const double l = sqrt(fmax(d, 1e-300));
-    A[6 * J + J] = l;
-    const double r = 1.0 / l;
+    const double dd = fmax(d, 1e-300);
+    const double r = rsqrt64(dd);            // 1 / l, and l = d / l
+    A[6 * J + J] = dd * r;
     rd[J] = r;
 #pragma unroll
     for (int i = J + 1; i < 6; ++i) {
@@ -675,37 +675,37 @@ __device__ __forceinline__ bool chol6_reg(double (&A)[36], double *rd) {
 }
 
 // (A + lam I) x = b by a block-banded Cholesky with the damping escalation
-// of mstep.py:348-369; the step is -x in node order.  The active window --
-// block rows k .. k + bw -- lives in shared memory as a ring of block rows
-// (each row: its diagonal block and bw sub-diagonal blocks); row k leaves
-// the window final (written to L, its forward substitution done) and row
-// k + bw + 1 enters from the assembled band.  Every update of a row comes
-// from steps whose window holds it.
-constexpr int kNgMaxBw = 24;        // window rows x blocks x 36 doubles <= 227 KB
-constexpr int kNgFacThreads = 256;
+// of mstep.py:348-369; the step is -x in node order.  One CTA; the active
+// window -- block rows k .. k + bw -- is held in REGISTERS: thread t owns the
+// block whose two ring slots are the t-th unordered slot pair, for as long as
+// both of its rows stay in the window (a block leaving with row k is
+// replaced by one of the entering row k + bw + 1 on the same slots).  Per
+// step k: the (k, k) owner factors its 6x6 pivot in registers and
+// forward-substitutes y_k (sync); each (i, k) owner forms L_ik = A_ik
+// L_kk^-T, takes its row's share of the forward substitution and publishes
+// L_ik^T in shared memory (sync); every other owner applies
+// A_ij -= L_ik L_jk^T from the published panel (broadcast reads, no
+// read-modify-write of shared memory).  Rows of L go to global memory for the
+// backward substitution.
+constexpr int kNgMaxBw = 24;
+constexpr int kNgW = kNgMaxBw + 1;
+constexpr int kNgFacThreads = 352;      // >= kNgW (kNgW + 1) / 2 block owners
 
 __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
     NgDev *st = b.st;
     if (st->gn_skip) return;
-    extern __shared__ double win[];            // [W][W][36] ring of block rows
     const int n = st->n, bw = st->bw, W = bw + 1, P = 6 * n;
     const int tid = threadIdx.x, NT = blockDim.x;
     __shared__ int ok, anyb;
     __shared__ double s_trace, s_lam;
     __shared__ double red[kNgFacThreads / 32];
-    __shared__ double rd[6];
-    __shared__ double yring[(kNgMaxBw + 2) * 6];   // y_j / x_j of the band's rows
-    __shared__ short pair_i[kNgMaxBw * (kNgMaxBw + 1) / 2], pair_j[kNgMaxBw * (kNgMaxBw + 1) / 2];
-    // (ii >= jj) pairs of the trailing triangle, enumerated once
-    if (tid == 0) {
-        int c = 0;
-        for (int ii = 0; ii < bw; ++ii)
-            for (int jj = 0; jj <= ii; ++jj) {
-                pair_i[c] = (short)ii;
-                pair_j[c] = (short)jj;
-                ++c;
-            }
-    }
+    __shared__ double rd2[1][6];                           // 1 / pivot
+    __shared__ __align__(16) double Lkk2[1][36];
+    __shared__ __align__(16) double panel2[1][kNgW][36];   // L_{k+d,k}^T (column c at 6c)
+    __shared__ double ybuf[1][6];
+    __shared__ double yring[(kNgW + 1) * 6];
+    __shared__ __align__(16) double brow[2][kNgW * 36];     // backward: rows of L (and the
+                                                            // forward loop's entering row)
     int nz = 0;
     double tr = 0.0;
     for (int q = tid; q < P; q += NT) {
@@ -727,157 +727,171 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
     }
     __syncthreads();
     if (!anyb) return;
+    // this thread's slot pair (pa >= pb): tid = pa (pa + 1) / 2 + pb
+    int pa = 0;
+    while ((pa + 1) * (pa + 2) / 2 <= tid) ++pa;
+    const int pb = tid - pa * (pa + 1) / 2;
+    const bool owner = pa < W;
     bool solved = false;
 #pragma unroll 1
     for (int attempt = 0; attempt < 6 && !solved; ++attempt) {
         const double lam = s_lam;
-        auto load_row = [&](int i) {
-            double *dst = win + (size_t)(i % W) * W * 36;
-            const double *src = b.band + (size_t)i * W * 36;
-            for (int e = tid; e < W * 36; e += NT) {
-                const int d = e / 36, q = e % 36;
-                dst[e] = src[e] + ((d == 0 && q / 6 == q % 6) ? lam : 0.0);
-            }
+        double blk[36];
+        // block (i, i - d) of the assembled band (+ lam on the diagonal)
+        auto load = [&](int i, int d) {
+            const double *src = b.band + ((size_t)i * W + d) * 36;
+#pragma unroll
+            for (int q = 0; q < 36; ++q) blk[q] = src[q] + ((d == 0 && q % 7 == 0) ? lam : 0.0);
         };
-        for (int i = 0; i < min(W, n); ++i) load_row(i);
-        // yring slot i % W: b_i, accumulating -L_ij y_j as the panels of the
-        // rows j < i are formed, then y_i
+#pragma unroll
+        for (int q = 0; q < 36; ++q) blk[q] = 0.0;
+        if (owner && pa < n) load(pa, pa - pb);          // window of k = 0: slot = row
         for (int e = tid; e < min(W, n) * 6; e += NT) yring[e] = b.bvec[e];
         if (tid == 0) ok = 1;
         __syncthreads();
-        constexpr int kPre = (kNgMaxBw + 1) * 36 / kNgFacThreads + 1;   // row elements per thread
-        int kw = 0;                                                     // k % W
-        for (int k = 0; k < n; ++k, kw = kw + 1 == W ? 0 : kw + 1) {
-            auto slot = [&](int off) { const int q = kw + off; return q >= W ? q - W : q; };
-            // the row entering after this step, loaded now (its latency hides
-            // behind the step's work)
-            double pre[kPre], bpre = 0.0;
+        // (dataflow through shared-memory counters instead of the two barriers
+        // per step was measured slower: 1.04 vs 0.72 ms per factorisation --
+        // the spinning warps take issue slots from the trailing updates)
+        int kw = 0;                                     // k % W
+        constexpr int kPreF = kNgW * 36 / kNgFacThreads + 1;   // entering-row doubles per thread
+#pragma unroll 1
+        for (int k = 0; k < n; ++k) {
+            constexpr int par = 0;     // (single buffers: two barriers per step)
+            // the row entering after this step (k + W), loaded now by every
+            // thread (coalesced; latency hidden behind the pivot and panel)
+            double pre[kPreF];
             const bool incoming = k + W < n;
             if (incoming) {
                 const double *src = b.band + (size_t)(k + W) * W * 36;
 #pragma unroll
-                for (int u = 0; u < kPre; ++u) {
+                for (int u = 0; u < kPreF; ++u) {
                     const int e = tid + u * NT;
                     pre[u] = e < W * 36 ? src[e] : 0.0;
                 }
-                if (tid < 6) bpre = b.bvec[6 * (k + W) + tid];
             }
-            double *row_k = win + (size_t)kw * W * 36;
-            double *Lkk = row_k;
-            if (tid == 0) {
-                double a[36];
-#pragma unroll
-                for (int q = 0; q < 36; ++q) a[q] = Lkk[q];
-                if (!chol6_reg(a, rd)) {
+            int oa = pa - kw, ob = pb - kw;
+            oa += oa < 0 ? W : 0;
+            ob += ob < 0 ? W : 0;
+            const int hi = max(oa, ob), lo = min(oa, ob);
+            const int i = k + hi;
+            const bool live = owner && i < n;
+            const int si = kw + hi >= W ? kw + hi - W : kw + hi;     // slot of row i
+            // (1) the pivot
+            if (live && hi == 0) {
+                double *Lg = b.L + (size_t)k * W * 36;
+                if (!chol6_reg(blk, rd2[par])) {
                     ok = 0;
                 } else {
-                    // y_k = L_kk^-1 b_k (b_k already holds -sum L_kj y_j)
-                    double *yk_ = yring + 6 * kw, y[6];
+                    double y[6];
 #pragma unroll
                     for (int r = 0; r < 6; ++r) {
-                        double v = yk_[r];
+                        double v = yring[6 * kw + r];
 #pragma unroll
-                        for (int q = 0; q < r; ++q) v -= a[6 * r + q] * y[q];
-                        y[r] = v * rd[r];
+                        for (int q = 0; q < r; ++q) v -= blk[6 * r + q] * y[q];
+                        y[r] = v * rd2[par][r];
                     }
 #pragma unroll
                     for (int r = 0; r < 6; ++r) {
-                        yk_[r] = y[r];
+                        ybuf[par][r] = y[r];
                         b.x[6 * k + r] = y[r];
+                        if (incoming) yring[6 * kw + r] = b.bvec[6 * (k + W) + r];
                     }
 #pragma unroll
-                    for (int q = 0; q < 36; ++q) Lkk[q] = a[q];
+                    for (int q = 0; q < 36; ++q) {
+                        Lkk2[par][q] = blk[q];
+                        Lg[q] = blk[q];
+                    }
+                    // the reciprocal pivots ride in the stored block's (zero)
+                    // upper triangle: (0, 1..5) and (1, 2); the backward
+                    // substitution multiplies by them
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) Lg[1 + c] = rd2[par][c];
+                    Lg[8] = rd2[par][5];
                 }
             }
             __syncthreads();
             if (!ok) break;
-            const int nrow = min(bw, n - 1 - k);
-            // panel: L_ik = A_ik L_kk^-T, one thread per row of a block, which
-            // also takes its row's share of the forward substitution
-            const double *yk_ = yring + 6 * kw;
-            for (int t = tid; t < nrow * 6; t += NT) {
-                const int off = 1 + t / 6, r = t % 6;
-                const int si = slot(off);
-                double *row = win + ((size_t)si * W + off) * 36 + 6 * r;
-                double v[6];
+            // (2) the panel: L_ik = A_ik L_kk^-T, b_i -= L_ik y_k
+            if (live && lo == 0 && hi > 0) {
+                const double *Lk = Lkk2[par], *rdk = rd2[par], *yk = ybuf[par];
+                double acc[6];
 #pragma unroll
-                for (int c = 0; c < 6; ++c) v[c] = row[c];
-                double dot = 0.0;
-#pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                    double u = v[c];
-#pragma unroll
-                    for (int q = 0; q < c; ++q) u -= v[q] * Lkk[6 * c + q];
-                    v[c] = u * rd[c];
-                    dot += v[c] * yk_[c];
-                }
-#pragma unroll
-                for (int c = 0; c < 6; ++c) row[c] = v[c];
-                yring[6 * si + r] -= dot;
-            }
-            __syncthreads();
-            // trailing update A_ij -= L_ik L_jk^T, one thread per (block pair,
-            // row half): 108 FMAs from registers
-            const int npairs = nrow * (nrow + 1) / 2;
-            for (int t = tid; t < 2 * npairs; t += NT) {
-                const int pr = t >> 1, h = t & 1;
-                const int oi = 1 + pair_i[pr], oj = 1 + pair_j[pr];
-                const int si = slot(oi), sj = slot(oj);
-                const double *Li = win + ((size_t)si * W + oi) * 36 + 18 * h;
-                const double *Lj = win + ((size_t)sj * W + oj) * 36;
-                double a[18], c6[36];
-#pragma unroll
-                for (int q = 0; q < 18; ++q) a[q] = Li[q];
-#pragma unroll
-                for (int q = 0; q < 36; ++q) c6[q] = Lj[q];
-                double *dst = win + ((size_t)si * W + (oi - oj)) * 36 + 18 * h;
-#pragma unroll
-                for (int r = 0; r < 3; ++r)
+                for (int r = 0; r < 6; ++r) {
+                    double dot = 0.0;
 #pragma unroll
                     for (int c = 0; c < 6; ++c) {
-                        double v = 0.0;
+                        double u = blk[6 * r + c];
 #pragma unroll
-                        for (int q = 0; q < 6; ++q) v += a[6 * r + q] * c6[6 * c + q];
-                        dst[6 * r + c] -= v;
+                        for (int q = 0; q < c; ++q) u -= blk[6 * r + q] * Lk[6 * c + q];
+                        u *= rdk[c];
+                        blk[6 * r + c] = u;
+                        dot += u * yk[c];
                     }
-            }
-            // row k is final: keep it for the backward substitution
-            for (int e = tid; e < W * 36; e += NT) b.L[(size_t)k * W * 36 + e] = row_k[e];
-            __syncthreads();
-            if (incoming) {
-                double *dst = row_k;                       // (k + W) % W == k % W
-#pragma unroll
-                for (int u = 0; u < kPre; ++u) {
-                    const int e = tid + u * NT;
-                    if (e < W * 36) {
-                        const int d = e / 36, q = e % 36;
-                        dst[e] = pre[u] + ((d == 0 && q / 6 == q % 6) ? lam : 0.0);
-                    }
+                    acc[r] = dot;
                 }
-                if (tid < 6) yring[6 * kw + tid] = bpre;
+#pragma unroll
+                for (int r = 0; r < 6; ++r) yring[6 * si + r] -= acc[r];
+                double *Lg = b.L + ((size_t)i * W + hi) * 36;
+#pragma unroll
+                for (int r = 0; r < 6; ++r)
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        panel2[par][hi][6 * c + r] = blk[6 * r + c];
+                        Lg[6 * r + c] = blk[6 * r + c];
+                    }
+            }
+            if (incoming) {
+                double *stage = brow[0];
+#pragma unroll
+                for (int u = 0; u < kPreF; ++u) {
+                    const int e = tid + u * NT;
+                    if (e < W * 36) stage[e] = pre[u];
+                }
             }
             __syncthreads();
+            // (3) the trailing update A_ij -= L_ik L_jk^T (both rows below k)
+            if (live && lo > 0) {
+                const double *Pi = panel2[par][hi], *Pj = panel2[par][lo];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    double li[6], lj[6];
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) {
+                        li[r] = Pi[6 * q + r];
+                        lj[r] = Pj[6 * q + r];
+                    }
+#pragma unroll
+                    for (int r = 0; r < 6; ++r)
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) blk[6 * r + c] = fma(-li[r], lj[c], blk[6 * r + c]);
+                }
+            }
+            // (4) row k's blocks leave: their owners take the entering row k + W
+            if (owner && lo == 0 && incoming) {
+                const int d = hi == 0 ? 0 : W - hi;
+                const double *src = brow[0] + d * 36;
+#pragma unroll
+                for (int q = 0; q < 36; ++q) blk[q] = src[q] + ((d == 0 && q % 7 == 0) ? lam : 0.0);
+            }
+            kw = kw + 1 == W ? 0 : kw + 1;
         }
         __syncthreads();
         if (ok) {
             // L^T x = y, right-looking: x_k = L_kk^-T y_k, then y_j -= L_kj^T x_k
-            // for the band's j < k (row k of L, one coalesced load per step)
-            // yring slot j % (W + 1) holds y_j for j in [k - W, k]: the band
-            // rows the step updates plus the one entering next (k - W, whose
-            // last update comes from step k - 1)
+            // for the band's j < k; yring slot j % (W + 1) holds y_j for j in
+            // [k - W, k] (the rows the step updates plus the one entering next)
             const int W1 = W + 1;
             for (int e = tid; e < W * 6; e += NT) {
                 const int j = n - 1 - e / 6;
                 if (j >= 0) yring[(j % W1) * 6 + e % 6] = b.x[6 * j + e % 6];
             }
-            // rows of L double-buffered in the (free) window: row k - 1 is
-            // loaded to registers during step k and stored at its end
             for (int e = tid; e < W * 36; e += NT)
-                win[((n - 1) & 1) * W * 36 + e] = b.L[(size_t)(n - 1) * W * 36 + e];
+                brow[(n - 1) & 1][e] = b.L[(size_t)(n - 1) * W * 36 + e];
             __syncthreads();
+            constexpr int kPre = kNgW * 36 / kNgFacThreads + 1;
             int kw1 = (n - 1) % W1;                                 // k % (W + 1)
             for (int k = n - 1; k >= 0; --k, kw1 = kw1 == 0 ? W : kw1 - 1) {
-                const double *row = win + (k & 1) * W * 36;
+                const double *row = brow[k & 1];
                 double pre[kPre], ypre = 0.0;
                 if (k > 0) {
                     const double *src = b.L + (size_t)(k - 1) * W * 36;
@@ -896,7 +910,8 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
                         double v = xk[r];
 #pragma unroll
                         for (int q = r + 1; q < 6; ++q) v -= row[6 * q + r] * x[q];
-                        x[r] = v / row[6 * r + r];
+                        // 1 / L_rr from the block's upper triangle (forward pass)
+                        x[r] = v * (r < 5 ? row[1 + r] : row[8]);
                     }
 #pragma unroll
                     for (int r = 0; r < 6; ++r) {
@@ -920,7 +935,7 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
                     yring[(sj < 0 ? sj + W1 : sj) * 6 + tid] = ypre;
                 }
                 if (k > 0) {
-                    double *dst = win + ((k - 1) & 1) * W * 36;
+                    double *dst = brow[(k - 1) & 1];
 #pragma unroll
                     for (int u = 0; u < kPre; ++u) {
                         const int e = tid + u * NT;
@@ -951,11 +966,6 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
         const int node = q / 6, r = q % 6;
         b.step[q] = -b.x[6 * b.pos[node] + r];
     }
-}
-
-static size_t ng_factor_smem(int bw) {
-    // the factor's window, or two rows of L for the backward substitution
-    return (size_t)(bw + 1) * std::max(bw + 1, 2) * 36 * sizeof(double);
 }
 
 // candidate node states exp(0.5^h step) o T for h < ncand (kinematics.py:307-311)
@@ -1272,7 +1282,7 @@ static int ng_iteration(fr_ng_em *em, cudaStream_t s) {
             k_ng_assemble<<<ga, kNgAsmThreads, 0, s>>>(em->b);
             FR_CHECK_LAUNCH();
         }
-        k_ng_factor<<<1, kNgFacThreads, ng_factor_smem(em->bw), s>>>(em->b);
+        k_ng_factor<<<1, kNgFacThreads, 0, s>>>(em->b);
         k_ng_cands<<<(unsigned)((kNgMaxCand * em->n + 255) / 256), 256, 0, s>>>(em->b);
         k_graph_objective<<<grid, kPassThreads, 0, s>>>(
             em->ref, em->m, em->sidx, em->swt, em->K, em->b.candDQ, em->n, em->ncand, em->d_rec,
@@ -1321,11 +1331,6 @@ int fr_ng_em_create(const fr_lattice *lat, const float *ref, int64_t m, const in
         cfg->max_em_iters < 1) {
         set_error("node-graph device loop: max_halvings <= %d, max_gn_iters <= 8", kNgMaxCand - 1);
         return FR_EINVAL;
-    }
-    if (cudaFuncSetAttribute(k_ng_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)ng_factor_smem(kNgMaxBw)) != cudaSuccess) {
-        set_error("node-graph device loop: shared-memory opt-in failed");
-        return FR_ECUDA;
     }
     fr_ng_em *em = new fr_ng_em();
     em->lat = lat;
