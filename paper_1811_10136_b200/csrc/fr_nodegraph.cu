@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
     __shared__ double red[kNgFacThreads / 32];
     __shared__ double rd2[1][6];                           // 1 / pivot
     __shared__ __align__(16) double Lkk2[1][36];
-    __shared__ __align__(16) double panel2[1][kNgW][36];   // L_{k+d,k}^T (column c at 6c)
+    __shared__ __align__(16) double panel2[1][kNgW][37];   // L_{k+d,k}^T (column c at 6c); 37: rows on distinct banks
     __shared__ double ybuf[1][6];
     __shared__ double yring[(kNgW + 1) * 6];
     __shared__ __align__(16) double brow[2][kNgW * 36];     // backward: rows of L (and the
