@@ -299,3 +299,29 @@ def test_setup_overlap_small_model_large_observation(fr):
     assert a.iterations >= 1 and np.isfinite(a.objectives[0])
     assert np.array_equal(a.kinematics.pose.matrix(), b.kinematics.pose.matrix())
     assert a.objectives == b.objectives
+
+
+def test_far_from_origin_float64_inputs(fr):
+    """clouds far from the origin.  The default float64 path keeps
+    the caller's float64 bits on both sides (no float32 planes), so a cloud
+    5e4 units from the origin registers as the oracle does (an 8-unit pebble,
+    sigma 0.4; float32 planes would quantise at 4e-3 = 1 % of sigma)."""
+    from paper_1811_10136_b200 import _rigid
+    old = _rigid.PRECISION
+    _rigid.PRECISION = "f64"
+    try:
+        model, obs, _ = O.pebble_pair(8000, outlier_ratio=0.05, seed=4)
+        off = np.array([5.0e4, -3.0e4, 2.0e4])
+        X = model * 100.0 + off
+        Y = obs * 100.0 + off
+        sigma = 0.05 * O.bbox_diameter(X[:8000])
+        tr = O.register_rigid(X, Y, sigma=sigma, outlier_ratio=0.1, max_em_iters=80,
+                              twist_tolerance=2e-4)
+        cfg = fr.RegistrationConfig(gmm=fr.GmmConfig(sigma=sigma, outlier_ratio=0.1),
+                                    max_em_iters=80, twist_tolerance=2e-4)
+        res = fr.register(fr.PointCloud(X), fr.PointCloud(Y), fr.RigidModel(), cfg)
+    finally:
+        _rigid.PRECISION = old
+    assert_pose_parity(res.kinematics.pose.rotation, res.kinematics.pose.translation,
+                       tr["R"], tr["t"], O.bbox_diameter(X))
+    assert abs(res.iterations - tr["iterations"]) <= 1
