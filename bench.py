@@ -441,28 +441,48 @@ def run_b200(args):
                  "dtype": args.precision}
         del path1
 
-    # roofline of the dominant kernel (k_em64, the whole loop): one pass reads
-    # the 24-byte float64 position of every model point (the reference's
-    # float64 arrays); the dense slice grid (~3 MB) is L1/L2-resident and not
-    # counted.  Timed alone (fr_em64_pass: launch + pass + reduction) with L2
-    # flushed, so the points come from HBM.
+    # roofline of the dominant kernel.  The timed region launches ONE kernel
+    # per step (k_em64: the whole 50-iteration registration), so a launch's
+    # algorithmic bytes are 24 B (float64 x, y, z) x model points x 50 passes
+    # -- every pass reads every point; after the first they come from L2 --
+    # and its duration is the step time measured by the CUDA events around
+    # it (the L2 flush sits outside the bracket).  The dense slice grid
+    # (~3 MB) is not counted.  The pass alone (one launch: pass + reduction,
+    # cold and warm) is reported beside it.  The float64 pass is bound by the
+    # FP64 pipe, not HBM: roofline_fp64 counts the pass's FP64 flops per point
+    # from its SASS (61 DFMA x 2 + 26 DADD + 17 DMUL) against the measured
+    # FP64 FMA peak (tools/gpu/fp64_peak.cu -> profiles/fp64_peak.json).
     peak, peak_kind = measured_peak()
     hp = head
-    alg_bytes = (24 if args.precision == "f64" else 12) * M_local
-    kernel_ms = hp.get("pass_cold_ms")
-    roofline = None
-    if kernel_ms:
-        achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "kernel": "k_em64 (float64 grid-resident EM loop; one launch = one pass + "
-                              "fixed-order reduction, timed alone, L2 flushed)",
-                    "alg_bytes_per_launch": alg_bytes, "kernel_ms": kernel_ms,
-                    "kernel_warm_ms": hp.get("pass_warm_ms"),
-                    "em_iteration_ms": hp["ms_per_step"] / EM_PER_STEP,
-                    "peak_source": peak_kind,
-                    "note": "traffic: see profiles/ (ncu dram bytes of the same launch); the "
-                            "float64 pass is bound by the FP64 pipe and issue, not HBM"}
+    bpp = 24 if args.precision == "f64" else 12
+    alg_bytes = bpp * M_local * EM_PER_STEP
+    step_ms = hp["ms_per_step"]
+    achieved = alg_bytes / (step_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": f"k_em64 (one launch = a {EM_PER_STEP}-iteration registration: "
+                          "pass, fixed-order reduction, float64 solve per iteration)",
+                "alg_bytes_per_launch": alg_bytes, "kernel_ms": step_ms,
+                "alg_bytes_per_point_pass": bpp,
+                "em_iteration_ms": step_ms / EM_PER_STEP,
+                "pass_alone": {"cold_ms": hp.get("pass_cold_ms"), "warm_ms": hp.get("pass_warm_ms"),
+                               "alg_bytes": bpp * M_local,
+                               "note": "one launch: pass + grid reduction, no solve; cold = "
+                                       "L2 flushed (points from HBM)"},
+                "peak_source": peak_kind,
+                "note": "traffic null: ncu DRAM bytes of the same launch are in profiles/ "
+                        "(r02_ncu.json: 25.5 MB per registration launch at 1.05M -- the points "
+                        "once, then L2; 403.8 MB per pass at 16.8M); the float64 pass is "
+                        "FP64-bound (roofline_fp64)"}
+    roofline_fp64 = None
+    fp64_peak_path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if args.precision == "f64" and os.path.exists(fp64_peak_path):
+        fpk = json.load(open(fp64_peak_path))["fp64_tflops"]
+        flops_pt = 165
+        ach = flops_pt * M_local * EM_PER_STEP / (step_ms / 1e3) / 1e12
+        roofline_fp64 = {"bound": "fp64", "achieved": ach, "peak": fpk, "unit": "TFLOP/s",
+                         "frac": ach / fpk, "flops_per_point_pass": flops_pt,
+                         "peak_source": "measured (profiles/fp64_peak.json)"}
 
     # end to end through the public API: register() from host float64
     # arrays, H2D of both clouds, sort, lattice build, the EM loop, D2H
@@ -546,7 +566,7 @@ def run_b200(args):
                                       "all-reduce of 25 doubles per iteration)"},
             "em_iters_per_sec": EM_PER_STEP * args.steps / (head["total_ms"] / 1e3),
             "em_iteration_us": 1e3 * head["ms_per_step"] / EM_PER_STEP,
-            "roofline": roofline,
+            "roofline": roofline, "roofline_fp64": roofline_fp64,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": head["launch"]["kernels_per_step"] * args.steps,
