@@ -151,7 +151,8 @@ int fr_gauss_bruteforce(const double *d_q, int64_t m, const double *d_f, int64_t
  * neighbouring threads of the EM pass query neighbouring simplices.  The
  * permutation (new -> old index) is written to d_perm when not NULL.  Used
  * once per registration on the model points: the EM sums are order-
- * independent up to float64 round-off. */
+ * independent up to float64 round-off.  Stream-ordered on `stream` (returns
+ * without waiting for the device). */
 int fr_sort_points_morton(float *d_pos, int64_t n, int planes, int32_t *d_perm, void *stream);
 
 /* ---- E step (estep.py:186-217) ------------------------------------------ */

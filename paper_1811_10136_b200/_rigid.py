@@ -182,6 +182,7 @@ def upload_soa64(points, dev):
 
 
 _SIDE_STREAMS: dict = {}
+_SETUP_POOL = None
 
 # model + observation points below which the setup runs on the calling thread
 SETUP_OVERLAP_MIN = 400_000
@@ -206,8 +207,16 @@ class _InlineExecutor:
     def submit(self, fn, *args):
         return self._Done(fn, args)
 
-    def shutdown(self, wait=True):
-        pass
+
+def _setup_pool():
+    """The process's persistent observation-side workers (spawning a thread
+    per registration cost ~0.1 ms on the setup's critical path).  A job only
+    waits on its own stream, so concurrent registrations queue, not block."""
+    global _SETUP_POOL
+    if _SETUP_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _SETUP_POOL = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fr-obs")
+    return _SETUP_POOL
 
 
 def _side_stream():
@@ -285,7 +294,6 @@ class RigidDevicePath:
         # the observation side (upload, splat, blur: host round trips) runs in
         # a worker thread on its own stream while this thread uploads, reduces
         # and Morton-sorts the model cloud
-        from concurrent.futures import ThreadPoolExecutor
         normals = residual_mode == "point_to_plane"
         self.with_sigma = bool(gmm.update_sigma)
         self.value_mode = (_lib.FR_VALUES_M2 if self.with_sigma else 0) | \
@@ -300,7 +308,7 @@ class RigidDevicePath:
         # small clouds: the worker thread's handoff costs more than the
         # overlap saves (and serialises on the GIL in register_batch)
         small = len(reference.positions) + len(observation.positions) < SETUP_OVERLAP_MIN
-        pool = _InlineExecutor() if small else ThreadPoolExecutor(max_workers=1)
+        pool = _InlineExecutor() if small else _setup_pool()
         import threading
         self._obs_uploaded = threading.Event()
         obs_job = pool.submit(self._build_observation, observation, gmm, residual_mode, side,
@@ -352,10 +360,7 @@ class RigidDevicePath:
         self.wtn = torch.empty((7, self.M), dtype=torch.float32, device=self.dev) \
             if self.mode == _lib.FR_POINT_TO_PLANE and not self.f64 else None
         lap("buffers")
-        try:
-            obs_job.result()          # the side stream is synchronised inside
-        finally:
-            pool.shutdown(wait=True)
+        obs_job.result()              # the side stream is synchronised inside
         if stats_ready is not None:
             stats_ready.synchronize()
             st = st_host.numpy()

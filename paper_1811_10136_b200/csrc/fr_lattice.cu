@@ -929,7 +929,7 @@ static int reserve_sites(fr_lattice *lat, long long need, cudaStream_t s) {
         FR_CUDA(cudaMemcpyAsync(nvals, lat->vals, (size_t)lat->n_sites * nv * sizeof(double),
                                 cudaMemcpyDeviceToDevice, s));
     }
-    FR_CUDA(cudaStreamSynchronize(s));
+    // (no host sync: the pool's frees are stream-ordered behind the copies)
     pool_free(lat, lat->site_keys);
     pool_free(lat, lat->vals);
     pool_free(lat, lat->vals_alt);
@@ -1147,8 +1147,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
                                                         run_vals, nv, lat->site_keys, lat->vals);
             FR_CHECK_LAUNCH();
         }
-        FR_CUDA(cudaStreamSynchronize(s));
-        pool_free(lat, old_keys);
+        pool_free(lat, old_keys);           // stream-ordered behind k_fill_sites
         lat->n_sites = S;
     }
     pc.lap("sites");
@@ -1194,8 +1193,7 @@ static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
         FR_CUDA(cudaMemcpyAsync(lat->vals, nvls, (size_t)keep * lat->nv * sizeof(double),
                                 cudaMemcpyDeviceToDevice, s));
     }
-    FR_CUDA(cudaStreamSynchronize(s));
-    lat->n_sites = keep;
+    lat->n_sites = keep;                    // scratch frees are stream-ordered
     return FR_OK;
 }
 
@@ -1662,8 +1660,7 @@ static int sort_morton_impl(T *pos, int64_t n, int planes, int32_t *perm_out, vo
     FR_CUDA(cudaMemcpyAsync(pos, tmp, (size_t)n * planes * sizeof(T), cudaMemcpyDeviceToDevice, s));
     if (perm_out)
         FR_CUDA(cudaMemcpyAsync(perm_out, perm, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    FR_CUDA(cudaStreamSynchronize(s));
-    return FR_OK;
+    return FR_OK;                           // stream-ordered; scratch frees likewise
 }
 
 extern "C" {
