@@ -343,7 +343,10 @@ def run_b200(args):
 
     world, rank, local = dist_env()
     group = None
-    if world > 1:
+    # FR_BENCH_GROUP=1 drives the sharded (NCCL) path even at one rank: a
+    # world-size-1 group exercises the captured pass -> all-reduce -> solve
+    # chunks on the one GPU available to the builder
+    if world > 1 or os.environ.get("FR_BENCH_GROUP") == "1":
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
@@ -392,7 +395,13 @@ def run_b200(args):
         out["em_kind"] = type(em).__name__
         if isinstance(em, _rigid.DeviceEM64):
             grid, block = em.launch_info()
-            out["launch"] = {"grid": grid, "block": block, "kernels_per_step": 1}
+            # unsharded: one launch per registration; sharded: a pass launch
+            # and a solve launch per iteration (+ NCCL's all-reduce kernel)
+            kps = 1 if group is None else 2 * EM_PER_STEP
+            out["launch"] = {"grid": grid, "block": block, "kernels_per_step": kps}
+            if group is not None:
+                out["launch"]["nccl_allreduce_per_step"] = EM_PER_STEP
+                out["launch"]["graph"] = em._graph is not None
             # the pass alone (one cooperative launch: pass + fixed-order
             # reduction, no solve), cold (L2 flushed) and warm
             cold = []
