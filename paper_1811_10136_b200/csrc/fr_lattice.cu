@@ -191,7 +191,7 @@ __global__ void k_splat_entries(Src src, long long p0, long long p1, long long n
             }
             entry_slot[e] = slot;
             entry_idx[e] = (unsigned)e;
-            entry_bary[e] = s.bary[l];
+            if (!contrib) entry_bary[e] = s.bary[l];      // the product rows carry it
             // the entry's products bary * value (NumPy's single rounding), one
             // row per entry, vertex-major ([l][p] rows): a site's entries share
             // their vertex index l, so for spatially ordered points its rows
@@ -371,6 +371,39 @@ __global__ void k_seg_pieces_combine(int n_runs, const int *piece_off, const dou
     double acc = 0.0;
     for (int p = piece_off[r]; p < piece_off[r + 1]; ++p) acc += piece_vals[(long long)p * nv + c];
     run_vals[q] = acc;
+}
+
+// dense site ids for the sort keys: occupied hash slots numbered in slot
+// order (flags, then an exclusive scan); entry keys rewritten slot -> id (the
+// sentinel -> K, after every id), so the radix sort runs over
+// 1 + floor(log2 K) bits instead of the hash's log2(cap) + 1; the runs'
+// ids are mapped back to slots afterwards
+__global__ void k_slot_flags(unsigned cap, const unsigned long long *keys, int *flags) {
+    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
+        flags[s] = keys[s] != kEmptyKey;
+}
+
+__global__ void k_slot_ids(unsigned cap, const int *flags, const int *ids, int *slot_of_id) {
+    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
+        if (flags[s]) slot_of_id[ids[s]] = (int)s;
+}
+
+__global__ void k_entries_to_ids(long long E, unsigned sentinel, unsigned K, const int *ids,
+                                 unsigned *entry_key) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E;
+         e += (long long)gridDim.x * blockDim.x) {
+        const unsigned sl = entry_key[e];
+        entry_key[e] = sl == sentinel ? K : (unsigned)ids[sl];
+    }
+}
+
+__global__ void k_runs_to_slots(const int *d_nruns, unsigned K, unsigned sentinel,
+                                const int *slot_of_id, unsigned *run_slot) {
+    const int nr = *d_nruns;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
+        const unsigned id = run_slot[r];
+        run_slot[r] = id >= K ? sentinel : (unsigned)slot_of_id[id];
+    }
 }
 
 __global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentinel,
@@ -1038,7 +1071,27 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         cap *= 4;
     }
     pc.lap("entries");
-    const int end_bit = 1 + (int)std::log2((double)cap);
+    // dense site ids as sort keys (K = distinct keys, counted by the inserts)
+    const unsigned K = (unsigned)hc[0];
+    int *slot_of_id = nullptr;
+    {
+        int *flags, *ids;
+        FR_TRY(sc.get(&flags, (size_t)cap));
+        FR_TRY(sc.get(&ids, (size_t)cap));
+        FR_TRY(sc.get(&slot_of_id, (size_t)K + 1));
+        const unsigned g = 148 * 8;
+        k_slot_flags<<<g, 256, 0, s>>>((unsigned)cap, lat->hkeys, flags);
+        FR_CHECK_LAUNCH();
+        size_t t5 = 0;
+        FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t5, flags, ids, (int)cap, s));
+        void *tmp5;
+        FR_TRY(sc.get((char **)&tmp5, t5));
+        FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp5, t5, flags, ids, (int)cap, s));
+        k_slot_ids<<<g, 256, 0, s>>>((unsigned)cap, flags, ids, slot_of_id);
+        k_entries_to_ids<<<g, 256, 0, s>>>(E, (unsigned)cap, K, ids, entry_slot);
+        FR_CHECK_LAUNCH();
+    }
+    const int end_bit = 1 + (int)std::log2((double)std::max(K, 1u));
     // stable radix sort of entries by slot: per-site groups in flat order
     size_t tmp_bytes = 0, t2 = 0;
     FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, entry_slot, sorted_slot,
@@ -1066,6 +1119,8 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     FR_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tmp_bytes, sorted_slot, run_slot, run_cnt,
                                                d_nruns, (int)E, s));
     pc.lap("rle_enqueue");
+    k_runs_to_slots<<<148, 256, 0, s>>>(d_nruns, K, (unsigned)cap, slot_of_id, run_slot);
+    FR_CHECK_LAUNCH();
     int nruns = 0;
     FR_TRY(d2h_sync(&nruns, d_nruns, sizeof(int), s));
     FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, run_cnt, run_off, nruns, s));
