@@ -433,13 +433,20 @@ static E64Variant e64_variant() {
 }
 
 static int e64_grid(const E64Variant &k) {
+    // once per device (attribute + occupancy queries cost ~10 us a call)
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
     cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem());
     cudaFuncSetAttribute(k.batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem());
     int per = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k.fn, k.block(), k.smem()) !=
             cudaSuccess || per < 1)
         per = 1;
-    return std::min(per, k.minb) * std::min(sm_count(), kE64MaxSms);
+    const int g = std::min(per, k.minb) * std::min(sm_count(), kE64MaxSms);
+    if (dev >= 0 && dev < 64) cached[dev] = g;
+    return g;
 }
 
 // centred point tiles: tiles[t][c][j] = ref[c][t T + j] - c_ref[c] (zero past m)
@@ -583,8 +590,7 @@ int fr_em64_create(const fr_lattice *lat, const double *ref, int64_t m,
         cudaMemsetAsync(em->d_sums, 0, kE64Row * sizeof(double), s) != cudaSuccess ||
         (getenv("FR_EM64_PROFILE") && getenv("FR_EM64_PROFILE")[0] == '1' &&
          (cudaMallocAsync((void **)&em->d_prof, (size_t)8 * cfg->max_em_iters * 8, s) != cudaSuccess ||
-          cudaMemsetAsync(em->d_prof, 0, (size_t)8 * cfg->max_em_iters * 8, s) != cudaSuccess)) ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
+          cudaMemsetAsync(em->d_prof, 0, (size_t)8 * cfg->max_em_iters * 8, s) != cudaSuccess))) {
         fr_em64_destroy(em);
         set_error("float64 EM allocation failed");
         return FR_ECUDA;
