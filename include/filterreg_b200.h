@@ -54,7 +54,12 @@ enum {
      * splats sum each site's entries in a fixed tree order (deterministic,
      * float64 round-off from the flat order, a serial chain of cnt / 256
      * adds instead of cnt). */
-    FR_SPLAT_FLAT_ORDER = 256
+    FR_SPLAT_FLAT_ORDER = 256,
+    /* the points are spatially ordered (e.g. Morton-sorted): consecutive
+     * points' vertex contributions are folded per site inside each warp
+     * before the sort (tree order, deterministic; far fewer sort items).  A
+     * cloud without such locality falls back to the per-entry path. */
+    FR_SPLAT_SPATIAL = 512
 };
 
 /* residual modes (mstep.py:33) */
@@ -147,7 +152,7 @@ int fr_gauss_bruteforce(const double *d_q, int64_t m, const double *d_f, int64_t
                         void *stream);
 
 /* Reorder a float32 SoA cloud (d_pos: `planes` planes of n, the first three
- * x, y, z) in place along a 30-bit Morton curve of its bounding box, so that
+ * x, y, z) in place along a 24-bit Morton curve of its bounding box, so that
  * neighbouring threads of the EM pass query neighbouring simplices.  The
  * permutation (new -> old index) is written to d_perm when not NULL.  Used
  * once per registration on the model points: the EM sums are order-

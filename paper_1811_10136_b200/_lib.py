@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("FR_LIB", os.path.join(_HERE, "libfilterreg_b200.so"))
 FR_OK, FR_EINVAL, FR_ESTATE, FR_EDEGEN, FR_ESOLVER, FR_ECAPACITY, FR_ECUDA = range(7)
 FR_VALUES_M2, FR_VALUES_NORMALS = 1, 2
 FR_SPLAT_FLAT_ORDER = 256     # value_mode bit: np.add.at's flat summation order
+FR_SPLAT_SPATIAL = 512        # value_mode bit: spatially ordered points (warp-folded pairs)
 FR_POINT_TO_POINT, FR_POINT_TO_PLANE = 0, 1
 
 # every symbol include/filterreg_b200.h declares

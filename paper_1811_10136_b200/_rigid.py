@@ -453,16 +453,22 @@ class RigidDevicePath:
 
     def build(self, sigma) -> None:
         """(Re)build the observation lattice at kernel width sigma.  The first
-        build splats the points in the caller's order (site sums bit-exact to
-        the reference); sigma re-estimation rebuilds (estep.py:232-259) splat
-        a Morton-ordered copy: the keys and occupied sites are the same, the
-        site sums add in that order (round-off apart, SURVEY 8(a) M0/M1
-        contract) and their row gathers become near-sequential."""
+        build splats the points in the caller's order (per-entry path, site
+        sums in a fixed tree order); sigma re-estimation rebuilds
+        (estep.py:232-259, point-to-point) splat a Morton-ordered copy made
+        once, with the warp-folded pairs (FR_SPLAT_SPATIAL: ~1/20 of the sort
+        items).  Keys and occupied sites are the reference's either way;
+        sums differ from np.add.at's flat order by float64 round-off (the
+        operator API, PermutohedralLattice.splat, keeps the flat order).
+        Measured at 1M: the Morton sort + warp-folded splat on the first
+        build cost more than the per-entry path saves (launch-bound small
+        sorts), at 16.8M sigma re-estimation it saves ~2 ms per rebuild."""
         import torch
         s = np.atleast_1d(np.asarray(sigma, dtype=float))
         if s.size == 1:
             s = np.full(3, s[0])
         pos = self.obs
+        mode = self.value_mode
         if self.lattice is not None and SORTED_REBUILD and self.obs_n is None:
             if getattr(self, "_obs_sorted", None) is None:
                 self._obs_sorted = self.obs.clone()
@@ -470,8 +476,9 @@ class RigidDevicePath:
                     else self.lib.fr_sort_points_morton
                 _lib.check(fn(_lib.ptr(self._obs_sorted), self.N, 3, None, _lib.stream_handle()))
             pos = self._obs_sorted
+            mode |= _lib.FR_SPLAT_SPATIAL
         lat = PermutohedralLattice(3, s)
-        lat.splat_points(pos, self.obs_n, self.value_mode)
+        lat.splat_points(pos, self.obs_n, mode)
         lat.blur()
         self.lattice, self.sigma = lat, s
 

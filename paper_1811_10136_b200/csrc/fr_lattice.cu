@@ -150,7 +150,8 @@ template <int D, class Src>
 __global__ void k_splat_entries(Src src, long long p0, long long p1, long long n_all,
                                 LatticeConsts c, BuildHash h,
                                 unsigned sentinel, unsigned *entry_slot, unsigned *entry_idx,
-                                double *entry_bary, double *contrib, unsigned long long *counters) {
+                                double *entry_bary, double *contrib, unsigned long long *counters,
+                                unsigned *created_list) {
     long long stride = (long long)gridDim.x * blockDim.x;
     for (long long p = p0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += stride) {
         double f[D];
@@ -185,7 +186,12 @@ __global__ void k_splat_entries(Src src, long long p0, long long p1, long long n
                     if (sl < 0) atomicOr(&counters[2], 2ull);
                     else {
                         slot = (unsigned)sl;
-                        if (created) atomicAdd(&counters[0], 1ull);
+                        if (created) {
+                            // the occupied slots, listed (capacity h.mask / 2 + 1:
+                            // beyond it the table is reported full anyway)
+                            const unsigned long long q = atomicAdd(&counters[0], 1ull);
+                            if (q <= (h.mask >> 1)) created_list[q] = (unsigned)sl;
+                        }
                     }
                 }
             }
@@ -373,21 +379,11 @@ __global__ void k_seg_pieces_combine(int n_runs, const int *piece_off, const dou
     run_vals[q] = acc;
 }
 
-// dense site ids for the sort keys: occupied hash slots numbered in slot
-// order (flags, then an exclusive scan); entry keys rewritten slot -> id (the
-// sentinel -> K, after every id), so the radix sort runs over
-// 1 + floor(log2 K) bits instead of the hash's log2(cap) + 1; the runs'
-// ids are mapped back to slots afterwards
-__global__ void k_slot_flags(unsigned cap, const unsigned long long *keys, int *flags) {
-    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
-        flags[s] = keys[s] != kEmptyKey;
-}
-
-__global__ void k_slot_ids(unsigned cap, const int *flags, const int *ids, int *slot_of_id) {
-    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
-        if (flags[s]) slot_of_id[ids[s]] = (int)s;
-}
-
+// dense site ids for the sort keys: the occupied hash slots (listed as they
+// are created) sorted ascending, id = rank (sc_site_ids); entry keys are
+// rewritten slot -> id (the sentinel -> K, after every id), so the radix sort
+// runs over 1 + floor(log2 K) bits instead of the hash's log2(cap) + 1; the
+// runs' ids are mapped back to slots afterwards
 __global__ void k_entries_to_ids(long long E, unsigned sentinel, unsigned K, const int *ids,
                                  unsigned *entry_key) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E;
@@ -404,6 +400,150 @@ __global__ void k_runs_to_slots(const int *d_nruns, unsigned K, unsigned sentine
         const unsigned id = run_slot[r];
         run_slot[r] = id >= K ? sentinel : (unsigned)slot_of_id[id];
     }
+}
+
+// ---------------------------------------------------------------------------
+// warp-aggregated splat (spatially ordered points: the EM path's Morton-
+// sorted observation copies).  A warp takes 32 consecutive points; per
+// simplex vertex the lanes whose vertex hits the same site (match_any) fold
+// their products bary * value in lane order into the group's lowest lane,
+// which emits ONE (site slot, warp-vertex index, sums) pair.  For Morton-
+// ordered points a warp's 32 points share one or two simplices, so the
+// pairs are ~1/20 of the entries: the sort and the site sums run over pairs.
+// Deterministic: the pairs are sorted by (site id, warp-vertex index) before
+// the fixed-order tree sums, whatever order the warps appended them in.
+template <int D, int NV, class Src>
+__global__ void __launch_bounds__(256)
+k_splat_warp_pairs(Src src, long long n, LatticeConsts c, BuildHash h, unsigned *pair_slot,
+                   unsigned *pair_lo, double *pair_vals, long long max_pairs,
+                   unsigned long long *counters, unsigned *created_list) {
+    constexpr unsigned FULL = 0xffffffffu, kNone = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w * 32 < n;
+         w += nwarps) {
+        const long long p = w * 32 + lane;
+        const bool inb = p < n;
+        Simplex<D> sx;
+        double v[NV];
+        bool any_value = false, ovf = false;
+        if (inb) {
+            double f[D];
+            src.template feat<D>(p, f);
+            simplex_exact<D>(f, c, sx);
+            ovf = sx.overflow;
+            if (ovf) atomicOr(&counters[2], 1ull);
+#pragma unroll
+            for (int cc = 0; cc < NV; ++cc) {
+                v[cc] = src.value(p, cc);
+                any_value |= v[cc] != 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int cc = 0; cc < NV; ++cc) v[cc] = 0.0;
+        }
+#pragma unroll
+        for (int l = 0; l <= D; ++l) {
+            unsigned slot = kNone;
+            if (inb && !ovf && any_value && sx.bary[l] != 0.0) {
+                const unsigned long long key = sx.packed(l);
+                const unsigned hs = (unsigned)mix64(key) & h.mask;
+                if (__ldcg(h.keys + hs) == key) {
+                    slot = hs;
+                } else {
+                    int created;
+                    const int sl = hash_insert(h, key, &created);
+                    if (sl < 0) atomicOr(&counters[2], 2ull);
+                    else {
+                        slot = (unsigned)sl;
+                        if (created) {
+                            const unsigned long long q = atomicAdd(&counters[0], 1ull);
+                            if (q <= (h.mask >> 1)) created_list[q] = (unsigned)sl;
+                        }
+                    }
+                }
+            }
+            const unsigned mask = __match_any_sync(FULL, slot);
+            double cv[NV], acc[NV];
+#pragma unroll
+            for (int cc = 0; cc < NV; ++cc) {
+                cv[cc] = slot != kNone ? __dmul_rn(sx.bary[l], v[cc]) : 0.0;
+                acc[cc] = 0.0;
+            }
+            // fold each group's rows: when every group is a contiguous run of
+            // lanes (the rule for spatially ordered points) a segmented
+            // shuffle tree (fixed shape given the runs); else the members in
+            // lane order (all lanes shuffle in lockstep, each from its own
+            // group's next member)
+            const int lo = __ffs(mask) - 1;
+            const unsigned run = mask >> lo;
+            const bool contiguous = slot == kNone || (run & (run + 1u)) == 0u;
+            if (__all_sync(FULL, contiguous)) {
+                const int end = lo + __popc(mask);
+#pragma unroll
+                for (int cc = 0; cc < NV; ++cc) acc[cc] = cv[cc];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                    for (int cc = 0; cc < NV; ++cc) {
+                        const double x = __shfl_down_sync(FULL, acc[cc], o);
+                        if (lane + o < end) acc[cc] = __dadd_rn(acc[cc], x);
+                    }
+                }
+            } else {
+                unsigned rem = slot != kNone ? mask : 0u;
+                while (__any_sync(FULL, rem != 0u)) {
+                    const int from = rem ? __ffs(rem) - 1 : lane;
+#pragma unroll
+                    for (int cc = 0; cc < NV; ++cc) {
+                        const double x = __shfl_sync(FULL, cv[cc], from);
+                        if (rem) acc[cc] = __dadd_rn(acc[cc], x);
+                    }
+                    rem &= rem - 1u;
+                }
+            }
+            const bool leader = slot != kNone && __ffs(mask) - 1 == lane;
+            const unsigned lead = __ballot_sync(FULL, leader);
+            unsigned long long base = 0;
+            if (lane == 0 && lead) base = atomicAdd(&counters[3], (unsigned long long)__popc(lead));
+            base = __shfl_sync(FULL, base, 0);
+            if (leader) {
+                const unsigned long long pos = base + __popc(lead & ((1u << lane) - 1u));
+                if ((long long)pos < max_pairs) {
+                    pair_slot[pos] = slot;
+                    pair_lo[pos] = (unsigned)(w * (D + 1) + l);
+#pragma unroll
+                    for (int cc = 0; cc < NV; ++cc) pair_vals[pos * NV + cc] = acc[cc];
+                } else {
+                    atomicOr(&counters[2], 4ull);     // pair buffer full: caller falls back
+                }
+            }
+        }
+    }
+}
+
+// site ids: the occupied slots sorted ascending, ids[slot] = rank (the same
+// numbering as flags + scan over the table, without touching empty slots)
+__global__ void k_scatter_ids(unsigned K, const unsigned *sorted_slots, int *ids) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x)
+        ids[sorted_slots[i]] = (int)i;
+}
+
+// sort keys (site id << lo_bits) | warp-vertex index, and the identity values
+__global__ void k_pair_keys(long long np, const unsigned *pair_slot, const unsigned *pair_lo,
+                            const int *ids, int lo_bits, unsigned long long *keys, unsigned *idx) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < np;
+         i += (long long)gridDim.x * blockDim.x) {
+        keys[i] = ((unsigned long long)ids[pair_slot[i]] << lo_bits) | pair_lo[i];
+        idx[i] = (unsigned)i;
+    }
+}
+
+__global__ void k_key_ids(long long np, const unsigned long long *keys, int lo_bits,
+                          unsigned *out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < np;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = (unsigned)(keys[i] >> lo_bits);
 }
 
 __global__ void k_run_live(int n_runs, const unsigned *run_slot, unsigned sentinel,
@@ -983,9 +1123,205 @@ using EntriesHook = std::function<int(const EntriesLaunch &)>;
 // splats with FR_SPLAT_FLAT_ORDER); else the fixed-tree order of
 // k_splat_segsum_tree
 
+// site ids from the list of created slots: sorted ascending (the table's
+// slot order), ids[slot] = rank; slot_of_id = the sorted list
+static int sc_site_ids(Scratch &sc, unsigned *created, unsigned K, unsigned cap, int *ids,
+                       int **slot_of_id, cudaStream_t s) {
+    unsigned *sorted;
+    FR_TRY(sc.get(&sorted, (size_t)K + 1));
+    if (K > 0) {
+        int bits = 1;
+        while ((1ull << bits) < cap) ++bits;
+        size_t tb = 0;
+        FR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, created, sorted, (int)K, 0, bits, s));
+        void *tmp;
+        FR_TRY(sc.get((char **)&tmp, tb));
+        FR_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, created, sorted, (int)K, 0, bits, s));
+        k_scatter_ids<<<grid_for(K), 256, 0, s>>>(K, sorted, ids);
+        FR_CHECK_LAUNCH();
+    }
+    *slot_of_id = reinterpret_cast<int *>(sorted);
+    return FR_OK;
+}
+
+constexpr int kAggFallback = 1000;
+
+template <int D, class Src>
+static int splat_agg(fr_lattice *lat, const Src &src, long long n, int nv, cudaStream_t s,
+                     PhaseClock &pc) {
+    const long long E = n * (D + 1);
+    Scratch sc(s);
+    const long long max_pairs = E / 4 + (1LL << 16);
+    unsigned *pair_slot, *pair_lo;
+    double *pair_vals;
+    FR_TRY(sc.get(&pair_slot, (size_t)max_pairs));
+    FR_TRY(sc.get(&pair_lo, (size_t)max_pairs));
+    FR_TRY(sc.get(&pair_vals, (size_t)max_pairs * nv));
+    pc.lap("alloc");
+    unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
+    unsigned long long hc[4];
+    const unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16);
+    unsigned *created = nullptr;
+    for (;;) {
+        FR_TRY(alloc_hash(lat, (unsigned)cap, s));
+        FR_TRY(sc.get(&created, (size_t)cap / 2 + 1));
+        FR_CUDA(cudaMemsetAsync(lat->d_counters, 0, 4 * sizeof(unsigned long long), s));
+        BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
+        switch (nv) {
+#define FR_AGG(NVV)                                                                                \
+    case NVV:                                                                                      \
+        k_splat_warp_pairs<D, NVV, Src><<<g, 256, 0, s>>>(src, n, lat->c, h, pair_slot, pair_lo,  \
+                                                         pair_vals, max_pairs, lat->d_counters,   \
+                                                         created);                                \
+        break;
+            FR_AGG(1) FR_AGG(2) FR_AGG(3) FR_AGG(4) FR_AGG(5) FR_AGG(6) FR_AGG(7) FR_AGG(8)
+#undef FR_AGG
+        }
+        FR_CHECK_LAUNCH();
+        FR_TRY(d2h_sync(hc, lat->d_counters, 4 * sizeof(unsigned long long), s));
+        if (hc[2] & 1ull) {
+            set_error("lattice coordinate outside the packable range (|key| >= %lld); "
+                      "features / sigma too large", (long long)kKeyLim);
+            return FR_ECAPACITY;
+        }
+        if (hc[2] & 4ull) return kAggFallback;          // points not spatially ordered enough
+        const bool full = (hc[2] & 2ull) || hc[0] * 2 > cap;
+        if (!full) break;
+        if (cap >= (1ull << 31)) {
+            set_error("splat hash table exceeded 2^31 slots");
+            return FR_ECAPACITY;
+        }
+        cap *= 4;
+    }
+    pc.lap("pairs");
+    const unsigned K = (unsigned)hc[0];
+    const long long np = (long long)hc[3];
+    if (pc.on) fprintf(stderr, "[splat] %lld points, %lld pairs, %u sites\n", n, np, K);
+    int *slot_of_id, *ids;
+    FR_TRY(sc.get(&ids, (size_t)cap));
+    FR_TRY(sc_site_ids(sc, created, K, (unsigned)cap, ids, &slot_of_id, s));
+    const unsigned gg = 148 * 8;
+    int lo_bits = 1;
+    while ((1LL << lo_bits) < ((n + 31) / 32) * (D + 1)) ++lo_bits;
+    int id_bits = 1;
+    while ((1LL << id_bits) < (long long)K + 1) ++id_bits;
+    unsigned long long *keys, *keys2;
+    unsigned *idx, *idx2, *sid;
+    FR_TRY(sc.get(&keys, (size_t)std::max(np, 1LL)));
+    FR_TRY(sc.get(&keys2, (size_t)std::max(np, 1LL)));
+    FR_TRY(sc.get(&idx, (size_t)std::max(np, 1LL)));
+    FR_TRY(sc.get(&idx2, (size_t)std::max(np, 1LL)));
+    FR_TRY(sc.get(&sid, (size_t)std::max(np, 1LL)));
+    const long long max_runs = (long long)K + 1;
+    unsigned *run_slot;
+    int *run_cnt, *run_off, *d_nruns;
+    FR_TRY(sc.get(&run_slot, (size_t)max_runs));
+    FR_TRY(sc.get(&run_cnt, (size_t)max_runs));
+    FR_TRY(sc.get(&run_off, (size_t)max_runs));
+    FR_TRY(sc.get(&d_nruns, 1));
+    int nruns = 0;
+    if (np > 0) {
+        k_pair_keys<<<gg, 256, 0, s>>>(np, pair_slot, pair_lo, ids, lo_bits, keys, idx);
+        FR_CHECK_LAUNCH();
+        size_t tb = 0, t2 = 0;
+        FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, idx2, (int)np, 0,
+                                                lo_bits + id_bits, s));
+        FR_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, sid, run_slot, run_cnt, d_nruns,
+                                                   (int)np, s));
+        tb = std::max(tb, t2);
+        FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, run_cnt, run_off, (int)max_runs, s));
+        tb = std::max(tb, t2);
+        void *tmp;
+        FR_TRY(sc.get((char **)&tmp, tb));
+        FR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, idx, idx2, (int)np, 0,
+                                                lo_bits + id_bits, s));
+        k_key_ids<<<gg, 256, 0, s>>>(np, keys2, lo_bits, sid);
+        FR_CHECK_LAUNCH();
+        FR_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tb, sid, run_slot, run_cnt, d_nruns,
+                                                   (int)np, s));
+        k_runs_to_slots<<<148, 256, 0, s>>>(d_nruns, K, (unsigned)cap, slot_of_id, run_slot);
+        FR_CHECK_LAUNCH();
+        FR_TRY(d2h_sync(&nruns, d_nruns, sizeof(int), s));
+        FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, run_cnt, run_off, nruns, s));
+    }
+    pc.lap("sort+runs");
+    double *run_vals;
+    unsigned char *run_live;
+    int *live_runs, *iota, *d_nlive;
+    FR_TRY(sc.get(&run_vals, (size_t)std::max(nruns, 1) * nv));
+    FR_TRY(sc.get(&run_live, (size_t)std::max(nruns, 1)));
+    FR_TRY(sc.get(&live_runs, (size_t)std::max(nruns, 1)));
+    FR_TRY(sc.get(&iota, (size_t)std::max(nruns, 1)));
+    FR_TRY(sc.get(&d_nlive, 1));
+    if (nruns > 0) {
+        // the runs' pairs in fixed-size pieces, tree sums, combined in order
+        int *pieces, *piece_off;
+        double *piece_vals;
+        const long long max_pieces = (long long)nruns + np / kSegPiece + 1;
+        FR_TRY(sc.get(&pieces, (size_t)nruns + 1));
+        FR_TRY(sc.get(&piece_off, (size_t)nruns + 1));
+        FR_TRY(sc.get(&piece_vals, (size_t)max_pieces * nv));
+        FR_CUDA(cudaMemsetAsync(pieces + nruns, 0, sizeof(int), s));
+        k_seg_piece_counts<<<grid_for(nruns), 256, 0, s>>>(nruns, nullptr, 0u, run_cnt, pieces);
+        FR_CHECK_LAUNCH();
+        size_t t4 = 0;
+        FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t4, pieces, piece_off, nruns + 1, s));
+        void *tmp4;
+        FR_TRY(sc.get((char **)&tmp4, t4));
+        FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp4, t4, pieces, piece_off, nruns + 1, s));
+        switch (nv) {
+#define FR_SEG_TREE(NVV)                                                                          \
+    case NVV:                                                                                     \
+        k_splat_segsum_tree<D, NVV><<<(unsigned)max_pieces, kSegBlock, 0, s>>>(                  \
+            nruns, piece_off, run_off, run_cnt, idx2, pair_vals, piece_vals, 0);                  \
+        break;
+            FR_SEG_TREE(1) FR_SEG_TREE(2) FR_SEG_TREE(3) FR_SEG_TREE(4)
+            FR_SEG_TREE(5) FR_SEG_TREE(6) FR_SEG_TREE(7) FR_SEG_TREE(8)
+#undef FR_SEG_TREE
+        }
+        FR_CHECK_LAUNCH();
+        k_seg_pieces_combine<<<grid_for((long long)nruns * nv), 256, 0, s>>>(
+            nruns, piece_off, piece_vals, nv, run_vals);
+        FR_CHECK_LAUNCH();
+        k_run_live<<<grid_for(nruns), 256, 0, s>>>(nruns, run_slot, (unsigned)cap, run_vals, nv,
+                                                   run_live);
+        FR_CHECK_LAUNCH();
+    }
+    pc.lap("segsum");
+    int S = 0;
+    if (nruns > 0) {
+        k_iota<<<grid_for(nruns), 256, 0, s>>>(nruns, iota);
+        FR_CHECK_LAUNCH();
+        size_t t3 = 0;
+        FR_CUDA(cub::DeviceSelect::Flagged(nullptr, t3, iota, run_live, live_runs, d_nlive,
+                                           nruns, s));
+        void *tmp3;
+        FR_TRY(sc.get((char **)&tmp3, t3));
+        FR_CUDA(cub::DeviceSelect::Flagged(tmp3, t3, iota, run_live, live_runs, d_nlive, nruns,
+                                           s));
+        FR_TRY(d2h_sync(&S, d_nlive, sizeof(int), s));
+    }
+    unsigned long long *old_keys = lat->hkeys;
+    lat->hkeys = nullptr;   // keep the splat hash alive for k_fill_sites
+    FR_TRY(reserve_sites(lat, std::max(S, 1), s));
+    if (S > 0) {
+        k_fill_sites<D><<<grid_for(S), 256, 0, s>>>(S, live_runs, run_slot, old_keys, run_vals,
+                                                    nv, lat->site_keys, lat->vals);
+        FR_CHECK_LAUNCH();
+    }
+    pool_free(lat, old_keys);
+    lat->n_sites = S;
+    pc.lap("sites");
+    FR_TRY(rehash_sites<D>(lat, next_pow2(2ull * (unsigned long long)lat->n_sites), s));
+    unsigned long long hc3[3];
+    FR_TRY(read_counters(lat, s, hc3));
+    pc.lap("rehash");
+    return FR_OK;
+}
+
 template <int D, class Src>
 static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cudaStream_t s,
-                      const EntriesHook *first = nullptr, bool flat = true) {
+                      const EntriesHook *first = nullptr, bool flat = true, bool agg = false) {
     if (lat->blurred || lat->splatted) {
         // the reference allows re-splatting an unblurred lattice (it replaces the table)
     }
@@ -1006,6 +1342,13 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     if (E >= (1LL << 31) - 1) {
         set_error("too many points for one splat (%lld)", n);
         return FR_EINVAL;
+    }
+    if (agg && !flat && !first && nv <= 8) {
+        const int st = splat_agg<D, Src>(lat, src, n, nv, s, pc);
+        if (st != kAggFallback) return st;
+        free_build(lat);                   // too many pairs: the per-entry path below
+        lat->n_sites = 0;
+        lat->site_cap = 0;
     }
     Scratch sc(s);
     unsigned *entry_slot, *entry_idx, *sorted_slot, *sorted_idx;
@@ -1040,8 +1383,10 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     // hash sized for the unique-key count; grown x4 on overflow
     unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
     unsigned long long hc[3];
+    unsigned *created = nullptr;
     for (int attempt = 0;; ++attempt) {
         FR_TRY(alloc_hash(lat, (unsigned)cap, s));
+        FR_TRY(sc.get(&created, (size_t)cap / 2 + 1));
         FR_CUDA(cudaMemsetAsync(lat->d_counters, 0, 3 * sizeof(unsigned long long), s));
         BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
         if (attempt == 0 && first) {
@@ -1050,7 +1395,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
             const auto launch = [&](long long a, long long b, cudaStream_t st) -> int {
                 k_splat_entries<D, Src><<<grid_for(b - a), 256, 0, st>>>(
                     src, a, b, n, lat->c, h, (unsigned)cap, entry_slot, entry_idx, entry_bary,
-                    contrib, lat->d_counters);
+                    contrib, lat->d_counters, created);
                 FR_CHECK_LAUNCH();     // on the launching (worker) thread
                 return FR_OK;
             };
@@ -1058,7 +1403,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         } else {
             k_splat_entries<D, Src><<<grid_for(n), 256, 0, s>>>(src, 0, n, n, lat->c, h, (unsigned)cap,
                                                                 entry_slot, entry_idx, entry_bary,
-                                                                contrib, lat->d_counters);
+                                                                contrib, lat->d_counters, created);
         }
         FR_CHECK_LAUNCH();
         FR_TRY(read_counters(lat, s, hc));
@@ -1075,20 +1420,10 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     const unsigned K = (unsigned)hc[0];
     int *slot_of_id = nullptr;
     {
-        int *flags, *ids;
-        FR_TRY(sc.get(&flags, (size_t)cap));
+        int *ids;
         FR_TRY(sc.get(&ids, (size_t)cap));
-        FR_TRY(sc.get(&slot_of_id, (size_t)K + 1));
-        const unsigned g = 148 * 8;
-        k_slot_flags<<<g, 256, 0, s>>>((unsigned)cap, lat->hkeys, flags);
-        FR_CHECK_LAUNCH();
-        size_t t5 = 0;
-        FR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t5, flags, ids, (int)cap, s));
-        void *tmp5;
-        FR_TRY(sc.get((char **)&tmp5, t5));
-        FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp5, t5, flags, ids, (int)cap, s));
-        k_slot_ids<<<g, 256, 0, s>>>((unsigned)cap, flags, ids, slot_of_id);
-        k_entries_to_ids<<<g, 256, 0, s>>>(E, (unsigned)cap, K, ids, entry_slot);
+        FR_TRY(sc_site_ids(sc, created, K, (unsigned)cap, ids, &slot_of_id, s));
+        k_entries_to_ids<<<148 * 8, 256, 0, s>>>(E, (unsigned)cap, K, ids, entry_slot);
         FR_CHECK_LAUNCH();
     }
     const int end_bit = 1 + (int)std::log2((double)std::max(K, 1u));
@@ -1613,20 +1948,66 @@ __device__ __forceinline__ unsigned spread10(unsigned v) {
     return v;
 }
 
+// 8 bits per axis (a 24-bit code: three radix passes); within a cell the
+// stable sort keeps the input order -- the cells (1/256 of the box per axis)
+// are far below the kernel width for the EM path's lattices
+constexpr int kMortonBits = 8;
+
 template <class T>
-__global__ void k_morton(const T *pos, long long n, const T *lo, const T *hi,
-                         unsigned *codes, unsigned *idx) {
+__global__ void k_morton(const T *pos, long long n, const T *lohi, unsigned *codes,
+                         unsigned *idx) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    constexpr float kQ = (float)((1 << kMortonBits) - 1);
     unsigned c = 0;
     for (int a = 0; a < 3; ++a) {
-        const float span = fmaxf((float)(hi[a] - lo[a]), 1e-30f);
-        const float u = (float)(pos[a * n + i] - lo[a]) / span;
-        const unsigned q = (unsigned)fminf(fmaxf(u * 1023.0f, 0.0f), 1023.0f);
+        const float span = fmaxf((float)(lohi[3 + a] - lohi[a]), 1e-30f);
+        const float u = (float)(pos[a * n + i] - lohi[a]) / span;
+        const unsigned q = (unsigned)fminf(fmaxf(u * kQ, 0.0f), kQ);
         c |= spread10(q) << (2 - a);
     }
     codes[i] = c;
     idx[i] = (unsigned)i;
+}
+
+// per-axis min / max of 3 planes: block partials, then one block combines
+template <class T>
+__global__ void k_bbox_part(const T *pos, long long n, T *part) {
+    __shared__ T sh[6][256];
+    T v[6];
+    for (int a = 0; a < 3; ++a) {
+        v[a] = (T)INFINITY;
+        v[3 + a] = (T)-INFINITY;
+    }
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+        for (int a = 0; a < 3; ++a) {
+            const T x = pos[a * n + i];
+            v[a] = x < v[a] ? x : v[a];
+            v[3 + a] = x > v[3 + a] ? x : v[3 + a];
+        }
+    for (int q = 0; q < 6; ++q) sh[q][threadIdx.x] = v[q];
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h)
+            for (int q = 0; q < 6; ++q) {
+                const T o = sh[q][threadIdx.x + h], m = sh[q][threadIdx.x];
+                sh[q][threadIdx.x] = q < 3 ? (o < m ? o : m) : (o > m ? o : m);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+template <class T>
+__global__ void k_bbox_final(const T *part, int nb, T *lohi) {
+    const int q = threadIdx.x;
+    if (q >= 6) return;
+    T v = part[q];
+    for (int b = 1; b < nb; ++b) {
+        const T o = part[b * 6 + q];
+        v = q < 3 ? (o < v ? o : v) : (o > v ? o : v);
+    }
+    lohi[q] = v;
 }
 
 template <class T>
@@ -1695,21 +2076,20 @@ static int sort_morton_impl(T *pos, int64_t n, int planes, int32_t *perm_out, vo
     FR_TRY(sc.get(&idx, n));
     FR_TRY(sc.get(&perm, n));
     FR_TRY(sc.get(&tmp, (size_t)n * planes));
-    size_t tb = 0, t2 = 0;
-    FR_CUDA(cub::DeviceReduce::Min(nullptr, tb, pos, lohi, (int)n, s));
-    FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, codes, codes2, idx, perm, (int)n, 0, 30, s));
+    constexpr int kBoxBlocks = 148 * 2;
+    T *part;
+    FR_TRY(sc.get(&part, (size_t)kBoxBlocks * 6));
+    size_t t2 = 0;
+    FR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, codes, codes2, idx, perm, (int)n, 0,
+                                            3 * kMortonBits, s));
     void *tmpb;
-    FR_TRY(sc.get((char **)&tmpb, std::max(tb, t2)));
-    for (int a = 0; a < 3; ++a) {
-        size_t tt = std::max(tb, t2);
-        FR_CUDA(cub::DeviceReduce::Min(tmpb, tt, pos + a * n, lohi + a, (int)n, s));
-        tt = std::max(tb, t2);
-        FR_CUDA(cub::DeviceReduce::Max(tmpb, tt, pos + a * n, lohi + 3 + a, (int)n, s));
-    }
-    k_morton<<<grid_for(n), 256, 0, s>>>(pos, n, lohi, lohi + 3, codes, idx);
+    FR_TRY(sc.get((char **)&tmpb, t2));
+    k_bbox_part<T><<<kBoxBlocks, 256, 0, s>>>(pos, n, part);
+    k_bbox_final<T><<<1, 32, 0, s>>>(part, kBoxBlocks, lohi);
+    k_morton<<<grid_for(n), 256, 0, s>>>(pos, n, lohi, codes, idx);
     FR_CHECK_LAUNCH();
-    size_t tt = std::max(tb, t2);
-    FR_CUDA(cub::DeviceRadixSort::SortPairs(tmpb, tt, codes, codes2, idx, perm, (int)n, 0, 30, s));
+    FR_CUDA(cub::DeviceRadixSort::SortPairs(tmpb, t2, codes, codes2, idx, perm, (int)n, 0,
+                                            3 * kMortonBits, s));
     k_gather_planes<<<grid_for(n), 256, 0, s>>>(pos, n, planes, perm, tmp);
     FR_CHECK_LAUNCH();
     FR_CUDA(cudaMemcpyAsync(pos, tmp, (size_t)n * planes * sizeof(T), cudaMemcpyDeviceToDevice, s));
@@ -1813,7 +2193,8 @@ int fr_lattice_splat_points(fr_lattice *lat, const float *pos, const float *nrm,
     int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
     PointSrc src{pos, nrm, n, m2, nv};
     return splat_impl<3, PointSrc>(lat, src, n, nv, (cudaStream_t)stream, nullptr,
-                                   (value_mode & FR_SPLAT_FLAT_ORDER) != 0);
+                                   (value_mode & FR_SPLAT_FLAT_ORDER) != 0,
+                                   (value_mode & FR_SPLAT_SPATIAL) != 0);
 }
 
 int fr_lattice_splat_points64(fr_lattice *lat, const double *pos, const double *nrm, int64_t n,
@@ -1835,7 +2216,8 @@ int fr_lattice_splat_points64(fr_lattice *lat, const double *pos, const double *
     int nv = 4 + m2 + ((value_mode & FR_VALUES_NORMALS) ? 3 : 0);
     PointSrc64 src{pos, nrm, n, m2, nv};
     return splat_impl<3, PointSrc64>(lat, src, n, nv, (cudaStream_t)stream, nullptr,
-                                     (value_mode & FR_SPLAT_FLAT_ORDER) != 0);
+                                     (value_mode & FR_SPLAT_FLAT_ORDER) != 0,
+                                     (value_mode & FR_SPLAT_SPATIAL) != 0);
 }
 
 int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
