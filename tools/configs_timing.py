@@ -96,6 +96,9 @@ def main():
     args = ap.parse_args()
     torch.cuda.set_device(0)
     manifest = json.load(open(os.path.join(GOLDEN, "MANIFEST_configs.json")))
+    r01_path = os.path.join(ROOT, "profiles", "r01_configs.json")
+    r01_ref = json.load(open(r01_path))["reference"].get("C1") if os.path.exists(r01_path) \
+        else None
     key = {"C2": "c2", "C3": "c3", "C4": "c4", "C5_1M_15it": "c5_1m_fixed15"}
     out = {}
     for name, g, ref, obs, model, config in cases():
@@ -125,6 +128,16 @@ def main():
                         "speedup_wall": r["wall_s"] / wall,
                         "ref_note": "live twistreg.register in the build container "
                                     "(8 cores, one BLAS thread), same inputs"})
+        elif name == "C1" and r01_ref is not None:
+            # C1 has no golden pose (tests/test_gpu_register.py pins the pose at
+            # this size against the oracle); its live-reference wall time was
+            # measured in round 1 by tools/make_config_inputs.py on the same
+            # inputs (synthesize_pair pebble 10k, seed 0 -- bit-identical to
+            # the oracle generator used here)
+            rec.update({"ref_iterations": r01_ref["iterations"], "ref_wall_s": r01_ref["wall_s"],
+                        "speedup_wall": r01_ref["wall_s"] / wall,
+                        "ref_note": "live twistreg.register, build container (8 cores), same "
+                                    "inputs; profiles/r01_configs.json"})
         out[name] = rec
         print(name, json.dumps(rec), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
