@@ -395,9 +395,10 @@ def run_b200(args):
         out["em_kind"] = type(em).__name__
         if isinstance(em, _rigid.DeviceEM64):
             grid, block = em.launch_info()
-            # unsharded: one launch per registration; sharded: a pass launch
-            # and a solve launch per iteration (+ NCCL's all-reduce kernel)
-            kps = 1 if group is None else 2 * EM_PER_STEP
+            # unsharded: one launch per registration; sharded: one fused
+            # (solve-first + pass) launch per iteration and a final solve
+            # (+ NCCL's all-reduce kernel per iteration)
+            kps = 1 if group is None else (EM_PER_STEP + 1 if em._fused else 2 * EM_PER_STEP)
             out["launch"] = {"grid": grid, "block": block, "kernels_per_step": kps}
             if group is not None:
                 out["launch"]["nccl_allreduce_per_step"] = EM_PER_STEP

@@ -391,6 +391,12 @@ int fr_em64_run(fr_em64 *em, int n_iters, void *stream);
 int fr_em64_run_batch(fr_em64 **ems, int n, void *stream);
 int fr_em64_pass(fr_em64 *em, void *stream);
 int fr_em64_solve(fr_em64 *em, void *stream);
+/* Sharded loop, fused: one cooperative launch that first solves the previous
+ * pass's sums (all-reduced in place in fr_em64_sums' buffer between the
+ * launches; every CTA solves them, as in the unsharded loop), then runs this
+ * iteration's pass + reduction.  Per iteration: this launch + one all-reduce;
+ * fr_em64_solve after the last launch takes the final pending solve. */
+int fr_em64_pass_solve(fr_em64 *em, void *stream);
 /* device address of the loop's termination flag (int, non-zero once done):
  * a sharded driver reads it asynchronously into pinned memory between
  * replays of its captured pass -> all-reduce -> solve chunks */

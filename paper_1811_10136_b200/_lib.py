@@ -37,7 +37,7 @@ EXPORTED = (
     "fr_body_objective", "fr_graph_pass", "fr_graph_blocks", "fr_graph_objective",
     "fr_point_rows", "fr_upload_points", "fr_rigid_em_persistent", "fr_rigid_em_run_batch",
     "fr_em64_create", "fr_em64_destroy", "fr_em64_run", "fr_em64_run_batch", "fr_em64_pass",
-    "fr_em64_solve", "fr_em64_done_ptr",
+    "fr_em64_solve", "fr_em64_done_ptr", "fr_em64_pass_solve",
     "fr_em64_sums", "fr_em64_launch_info", "fr_em64_status", "fr_em64_result",
     "fr_upload_points64", "fr_upload_rows64", "fr_point_stats64_work_doubles",
     "fr_point_stats64", "fr_lattice_splat_points64", "fr_sort_points_morton64",
@@ -144,6 +144,7 @@ _SIGS = {
     "fr_upload_points64": ([_P, _L, _P, _P], _I),
     "fr_upload_rows64": ([_P, _L, _P, _P, _P], _I),
     "fr_em64_done_ptr": ([_P, _P], _I),
+    "fr_em64_pass_solve": ([_P, _P], _I),
     "fr_point_stats64_work_doubles": ([], _I),
     "fr_point_stats64": ([_P, _L, _P, _P, _P], _I),
     "fr_em64pl_create": ([_P, _P, _L, ctypes.POINTER(RigidEmConfig), _P, ctypes.POINTER(_P)], _I),

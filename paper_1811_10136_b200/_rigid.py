@@ -590,6 +590,8 @@ class _DeviceInts:
 # sharded float64 loop over NCCL: replay captured chunks (False: the per-
 # iteration Python loop with a synchronising status poll per chunk)
 GROUP_GRAPH = True
+# sharded iteration as one fused launch (solve-first) + the all-reduce
+FUSED_SHARDED = True
 
 
 class DeviceEM:
@@ -726,6 +728,10 @@ class DeviceEM64:
         w = ctypes.c_int()
         _lib.check(self.lib.fr_em64_sums(h, ctypes.byref(sp), ctypes.byref(w)))
         self.sums = torch.as_tensor(_DeviceArray(sp.value, w.value), device=path.dev)
+        # sharded: one fused launch per iteration (solve of the previous
+        # sums, then the pass) + one all-reduce; FUSED_SHARDED = False: pass,
+        # all-reduce, solve kernel
+        self._fused = path.group is not None and FUSED_SHARDED
         if path.group is not None and type(self) is DeviceEM64 and self._nccl_group():
             self._capture()
 
@@ -756,12 +762,20 @@ class DeviceEM64:
             for _ in range(q):
                 self._graph.replay()
         self._enqueue_eager(n)
+        if self._fused:
+            # the last pass's all-reduced sums still await their solve
+            _lib.check(self.lib.fr_em64_solve(self.h, _lib.stream_handle()))
 
     def _enqueue_eager(self, n: int) -> None:
         for _ in range(int(n)):
-            _lib.check(self.lib.fr_em64_pass(self.h, _lib.stream_handle()))
-            self.path.reduce_device(self.sums)
-            _lib.check(self.lib.fr_em64_solve(self.h, _lib.stream_handle()))
+            if self._fused:
+                # solve of the previous pass's sums + this pass: one launch
+                _lib.check(self.lib.fr_em64_pass_solve(self.h, _lib.stream_handle()))
+                self.path.reduce_device(self.sums)
+            else:
+                _lib.check(self.lib.fr_em64_pass(self.h, _lib.stream_handle()))
+                self.path.reduce_device(self.sums)
+                _lib.check(self.lib.fr_em64_solve(self.h, _lib.stream_handle()))
 
     def _capture(self) -> None:
         """CHUNK iterations of pass -> all-reduce -> solve as one CUDA graph

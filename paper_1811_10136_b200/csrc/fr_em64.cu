@@ -56,7 +56,8 @@ struct Em64Args {
     unsigned *counter;   // arrivals of the current iteration
     unsigned *gen;       // release generation
     int n_iters;         // iterations of this launch (or fewer: termination)
-    int solve;           // 0: pass + reduction only
+    int solve;           // 0: pass + reduction only; 1: + the solve (unsharded loop);
+                         // 2: solve the pending all-reduced sums first (sharded)
     unsigned long long *prof;   // optional phase timestamps [n_iters][8] (FR_EM64_PROFILE)
     // pose-independent constants (kernel parameters: constant-bank operands)
     double sc[3];        // sf_j / sigma_j: f = x * sc (permutohedral.py:172)
@@ -197,6 +198,21 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     constexpr bool kInlineSolve = MINB == 1 && THREADS <= 256;
     const int it0 = se.iterations;           // the state's iteration count at entry
     for (; it < a.n_iters; ++it) {
+        // solve == 2 (sharded, fused): the previous pass's sums, all-reduced
+        // across ranks between the launches, are solved first -- by every
+        // CTA, as in the unsharded loop -- then this launch's pass
+        if (a.solve == 2 && se.pending) {
+            if (tid < kE64Stats) tsum[tid] = __ldcg(a.sums + tid);
+            __syncthreads();
+            if (tid == 0) {
+                const int n = se.max_em_iters;
+                se.pending = 0;
+                rigid_solve_impl<kInlineSolve>(tsum, &se, a.traces, a.traces + n,
+                                               a.traces + 2 * n, blockIdx.x == 0, nullptr,
+                                               a.traces + 3 * n);
+            }
+            __syncthreads();
+        }
         // identical in every CTA; a pass-only launch after termination is a
         // no-op too (the sharded loop's replayed chunks run past the end)
         if (se.done) break;
@@ -309,7 +325,8 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
         }
         __syncthreads();
         if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 2] = gtime();
-        if (!a.solve && blockIdx.x != 0) continue;
+        if (a.solve == 2 && tid == 0) se.pending = 1;     // solved by the next launch
+        if (a.solve != 1 && blockIdx.x != 0) continue;
         // fixed-order column sums: thread (g, c) adds the rows g, g + W, ...
         // of column c with every load issued up front (one L2 round trip),
         // then the W group sums in order -- the same order in every CTA
@@ -340,7 +357,7 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
         }
         __syncthreads();
         if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 3] = gtime();
-        if (a.solve) {
+        if (a.solve == 1) {
             if (tid == 0) {
                 const int n = se.max_em_iters;
                 if (kInlineSolve)   // 255 registers: the lean solve inlined
@@ -398,6 +415,7 @@ __global__ void k_em64_solve(const double *sums, EmDev *e, double *traces) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const int n = se.max_em_iters;
+        se.pending = 0;
         rigid_solve_body(ts, &se, traces, traces + n, traces + 2 * n, true);
     }
     __syncthreads();
@@ -691,6 +709,15 @@ int fr_em64_pass(fr_em64 *em, void *stream) {
     }
     em->stream = (cudaStream_t)stream;
     return e64_launch(em, 1, 0, (cudaStream_t)stream);
+}
+
+int fr_em64_pass_solve(fr_em64 *em, void *stream) {
+    if (!em) {
+        set_error("null EM object");
+        return FR_EINVAL;
+    }
+    em->stream = (cudaStream_t)stream;
+    return e64_launch(em, 1, 2, (cudaStream_t)stream);
 }
 
 int fr_em64_done_ptr(fr_em64 *em, int **d_done) {
