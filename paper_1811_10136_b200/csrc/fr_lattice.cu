@@ -1196,7 +1196,8 @@ static int splat_agg(fr_lattice *lat, const Src &src, long long n, int nv, cudaS
     pc.lap("pairs");
     const unsigned K = (unsigned)hc[0];
     const long long np = (long long)hc[3];
-    if (pc.on) fprintf(stderr, "[splat] %lld points, %lld pairs, %u sites\n", n, np, K);
+    if (pc.on) fprintf(stderr, "[splat] %lld points, %lld pairs, %u sites in %llu slots (load %.4f)\n",
+                       n, np, K, cap, (double)K / (double)cap);
     int *slot_of_id, *ids;
     FR_TRY(sc.get(&ids, (size_t)cap));
     FR_TRY(sc_site_ids(sc, created, K, (unsigned)cap, ids, &slot_of_id, s));
@@ -1418,6 +1419,8 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     pc.lap("entries");
     // dense site ids as sort keys (K = distinct keys, counted by the inserts)
     const unsigned K = (unsigned)hc[0];
+    if (pc.on) fprintf(stderr, "[splat] %lld points, %lld entries, %u sites in %llu slots "
+                       "(load %.4f)\n", n, E, K, cap, (double)K / (double)cap);
     int *slot_of_id = nullptr;
     {
         int *ids;
