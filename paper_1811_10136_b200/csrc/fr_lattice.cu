@@ -1144,6 +1144,15 @@ static int sc_site_ids(Scratch &sc, unsigned *created, unsigned K, unsigned cap,
     return FR_OK;
 }
 
+// initial splat hash size: FR_SPLAT_HASH_SHIFT (default 0) divides the
+// entry-based bound (2E, at most 2^22 slots) by 2^shift, at least 2^15 slots;
+// a table that fills grows x4 and the pass reruns
+static unsigned long long splat_hash_cap(long long E) {
+    static const int shift = getenv("FR_SPLAT_HASH_SHIFT") ? atoi(getenv("FR_SPLAT_HASH_SHIFT")) : 0;
+    const unsigned long long full = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
+    return std::max<unsigned long long>(full >> std::max(0, std::min(shift, 20)), 1ull << 15);
+}
+
 constexpr int kAggFallback = 1000;
 
 template <int D, class Src>
@@ -1158,7 +1167,7 @@ static int splat_agg(fr_lattice *lat, const Src &src, long long n, int nv, cudaS
     FR_TRY(sc.get(&pair_lo, (size_t)max_pairs));
     FR_TRY(sc.get(&pair_vals, (size_t)max_pairs * nv));
     pc.lap("alloc");
-    unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
+    unsigned long long cap = splat_hash_cap(E);
     unsigned long long hc[4];
     const unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16);
     unsigned *created = nullptr;
@@ -1382,7 +1391,7 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     }
     pc.lap("alloc");
     // hash sized for the unique-key count; grown x4 on overflow
-    unsigned long long cap = next_pow2((unsigned long long)std::min<long long>(2 * E, 1LL << 22));
+    unsigned long long cap = splat_hash_cap(E);
     unsigned long long hc[3];
     unsigned *created = nullptr;
     for (int attempt = 0;; ++attempt) {
