@@ -370,7 +370,7 @@ def band_structure(n, pair_lo, pair_hi, edges):
     return pos.astype(np.int32), bw, slot_ptr, ent, inc_ptr, inc_ent
 
 
-def register_nodegraph_device(path, graph, config, timing=None):
+def register_nodegraph_device(path, graph, config, timing=None, band=None):
     """The device-resident node-graph EM loop (fr_ng_em_*): per iteration
     one CUDA graph of the E pass, the banded system with the ARAP term, the
     block-banded damped Cholesky, all halving candidates, the first accepted
@@ -384,7 +384,8 @@ def register_nodegraph_device(path, graph, config, timing=None):
     edges = np.ascontiguousarray(np.asarray(graph.edges, dtype=np.int64).reshape(-1, 2))
     lo = np.asarray(path.pair_lo, dtype=np.int64)
     hi = np.asarray(path.pair_hi, dtype=np.int64)
-    pos, bw, slot_ptr, slot_ent, inc_ptr, inc_ent = band_structure(n, lo, hi, edges)
+    pos, bw, slot_ptr, slot_ent, inc_ptr, inc_ent = band if band is not None else \
+        band_structure(n, lo, hi, edges)
     c = _lib.RigidEmConfig()
     c.sigma_inv[:] = list(1.0 / np.asarray(path.sigma, dtype=float))
     c.c_prime = path.c_prime
@@ -452,10 +453,11 @@ def register_nodegraph(reference, observation, graph, config, timing=None, proce
     if (DEVICE_LOOP and process_group is None and not config.gmm.update_sigma
             and not config.record_states and ms.max_halvings <= 15 and ms.max_gn_iters <= 8
             and ms.solve_method in ("auto", "sparse")):
-        edges = np.asarray(graph.edges, dtype=np.int64).reshape(-1, 2)
-        bw = band_structure(graph.n_nodes, path.pair_lo, path.pair_hi, edges)[1]
-        if bw <= MAX_DEVICE_BANDWIDTH:
-            return register_nodegraph_device(path, graph, config, timing)
+        edges = np.ascontiguousarray(np.asarray(graph.edges, dtype=np.int64).reshape(-1, 2))
+        band = band_structure(graph.n_nodes, np.asarray(path.pair_lo, dtype=np.int64),
+                              np.asarray(path.pair_hi, dtype=np.int64), edges)
+        if band[1] <= MAX_DEVICE_BANDWIDTH:
+            return register_nodegraph_device(path, graph, config, timing, band=band)
     model = graph
     sigma_current = path.sigma
     result = RegistrationResult(kinematics=model, iterations=0,

@@ -290,8 +290,8 @@ k_graph_objective(const float *__restrict__ ref, long long m, const int *__restr
                   const double *__restrict__ swt, int K, const double *__restrict__ cand_dq,
                   int n_nodes, int ncand, const double *__restrict__ rec, int mode, double s0,
                   double s1, double s2, double *__restrict__ partials, int *bad,
-                  const int *skip = nullptr) {
-    if (skip && *skip) return;
+                  const int *skip = nullptr, int c0 = 0, const int *skip2 = nullptr) {
+    if ((skip && *skip) || (skip2 && *skip2)) return;
     double acc[kGraphMaxCand];
 #pragma unroll
     for (int a = 0; a < kGraphMaxCand; ++a) acc[a] = 0.0;
@@ -304,7 +304,8 @@ k_graph_objective(const float *__restrict__ ref, long long m, const int *__restr
         const double n[3] = {rec[4 * m + p], rec[5 * m + p], rec[6 * m + p]};
 #pragma unroll
         for (int c = 0; c < kGraphMaxCand; ++c) {
-            if (c >= ncand) break;
+            if (c >= c0 + ncand) break;
+            if (c < c0) continue;                  // candidates [c0, c0 + ncand)
             double x[3];
             point_forward(ref, m, p, sidx, swt, K, cand_dq + (size_t)c * n_nodes * 8, x, bad);
             const double d[3] = {x[0] - tg[0], x[1] - tg[1], x[2] - tg[2]};
@@ -974,7 +975,10 @@ __global__ void k_ng_cands(NgBufs b) {
     if (st->gn_skip) return;
     const int n = st->n;
     const int nc = min(st->max_halvings + 1, kNgMaxCand);
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->ncand = nc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->ncand = nc;
+        st->accepted = 0;                       // this GN step's candidate not yet decided
+    }
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nc * n; t += gridDim.x * blockDim.x) {
         const int h = t / n, node = t % n;
         const double scale = ldexp(1.0, -h);
@@ -992,18 +996,23 @@ __global__ void k_ng_cands(NgBufs b) {
 
 // + ARAP objectives of the candidates, first accepted (mstep.py:443-459),
 // state update, Gauss-Newton continuation
-__global__ void __launch_bounds__(kNgThreads, 1) k_ng_select(NgBufs b) {
+__global__ void __launch_bounds__(kNgThreads, 1) k_ng_select(NgBufs b, int h0, int h1) {
+    // candidates [h0, h1) in halving order; the first launch takes h = 0
+    // alone (the usual outcome: the full step is accepted, and the other
+    // candidates' passes are skipped), the second the rest
     NgDev *st = b.st;
-    if (st->gn_skip) return;
+    if (st->gn_skip || st->accepted) return;
     const int n = st->n, nc = st->ncand;
+    h1 = min(h1, nc);
     __shared__ double red[kNgThreads / 32][kNgMaxCand];
     __shared__ int acc_h;
+    __shared__ double s_sn;
     const bool reg = st->lambda > 0.0 && st->n_edges > 0;
     double part[kNgMaxCand];
     for (int h = 0; h < kNgMaxCand; ++h) part[h] = 0.0;
     if (reg)
         for (int e2 = threadIdx.x; e2 < 2 * st->n_edges; e2 += blockDim.x)
-            for (int h = 0; h < nc; ++h) {
+            for (int h = h0; h < h1; ++h) {
                 double xk[3], xl[3], rr[3];
                 ng_arap_rows(b, e2 >> 1, e2 & 1, b.candR + (size_t)h * n * 9,
                              b.candT + (size_t)h * n * 3, xk, xl, rr);
@@ -1022,7 +1031,7 @@ __global__ void __launch_bounds__(kNgThreads, 1) k_ng_select(NgBufs b) {
             st->done = 1;
             st->gn_skip = 1;
         } else {
-            for (int h = 0; h < nc && acc_h < 0; ++h) {
+            for (int h = h0; h < h1 && acc_h < 0; ++h) {
                 double arap = 0.0;
                 for (int w = 0; w < (int)(blockDim.x / 32); ++w) arap += red[w][h];
                 const double cv = b.cand_data[h] + arap;
@@ -1031,25 +1040,32 @@ __global__ void __launch_bounds__(kNgThreads, 1) k_ng_select(NgBufs b) {
                     st->value = cv;
                 }
             }
-            if (acc_h < 0) {
-                st->gn_skip = 1;                       // no acceptable step (mstep.py:450-451)
-            } else {
-                const double scale = ldexp(1.0, -acc_h);
-                double sn = 0.0;
-                for (int q = 0; q < 6 * n; ++q) sn += (scale * b.step[q]) * (scale * b.step[q]);
-                st->gn += 1;
-                st->gn_skip = (sqrt(sn) <= st->step_tol || st->gn >= st->max_gn_iters) ? 1 : 0;
-            }
+            if (acc_h >= 0 || h1 >= nc) st->accepted = 1;     // decided
+            if (acc_h < 0 && h1 >= nc) st->gn_skip = 1;      // no acceptable step (mstep.py:450-451)
         }
     }
     __syncthreads();
-    if (acc_h >= 0)
-        for (int q = threadIdx.x; q < n; q += blockDim.x) {
-            const size_t o = (size_t)acc_h * n + q;
-            for (int c = 0; c < 9; ++c) b.R[9 * q + c] = b.candR[9 * o + c];
-            for (int c = 0; c < 3; ++c) b.T[3 * q + c] = b.candT[3 * o + c];
-            for (int c = 0; c < 8; ++c) b.DQ[8 * q + c] = b.candDQ[8 * o + c];
-        }
+    if (acc_h < 0) return;
+    // the accepted step's norm (block tree) and the node states
+    const double scale = ldexp(1.0, -acc_h);
+    double sn = 0.0;
+    for (int q = threadIdx.x; q < 6 * n; q += blockDim.x) sn += (scale * b.step[q]) * (scale * b.step[q]);
+    for (int o = 16; o > 0; o >>= 1) sn += __shfl_down_sync(0xffffffffu, sn, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][0] = sn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w][0];
+        s_sn = t;
+        st->gn += 1;
+        st->gn_skip = (sqrt(t) <= st->step_tol || st->gn >= st->max_gn_iters) ? 1 : 0;
+    }
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        const size_t o = (size_t)acc_h * n + q;
+        for (int c = 0; c < 9; ++c) b.R[9 * q + c] = b.candR[9 * o + c];
+        for (int c = 0; c < 3; ++c) b.T[3 * q + c] = b.candT[3 * o + c];
+        for (int c = 0; c < 8; ++c) b.DQ[8 * q + c] = b.candDQ[8 * o + c];
+    }
 }
 
 // update magnitude (batched form of pipeline.py:79-86) and termination
@@ -1284,13 +1300,24 @@ static int ng_iteration(fr_ng_em *em, cudaStream_t s) {
         }
         k_ng_factor<<<1, kNgFacThreads, 0, s>>>(em->b);
         k_ng_cands<<<(unsigned)((kNgMaxCand * em->n + 255) / 256), 256, 0, s>>>(em->b);
+        // the full step first; the halved candidates only if it is rejected
+        const int *decided = &em->d_st->accepted;
         k_graph_objective<<<grid, kPassThreads, 0, s>>>(
-            em->ref, em->m, em->sidx, em->swt, em->K, em->b.candDQ, em->n, em->ncand, em->d_rec,
+            em->ref, em->m, em->sidx, em->swt, em->K, em->b.candDQ, em->n, 1, em->d_rec,
             em->mode, em->g.sinv[0], em->g.sinv[1], em->g.sinv[2], em->d_scratch, em->d_flag,
-            gskip);
+            gskip, 0, decided);
         k_reduce_cols<<<1, 32 * kGraphMaxCand, 0, s>>>(em->d_scratch, grid, kGraphMaxCand,
-                                                        em->d_cdata, gskip);
-        k_ng_select<<<1, kNgThreads, 0, s>>>(em->b);
+                                                        em->d_cdata, gskip, decided);
+        k_ng_select<<<1, kNgThreads, 0, s>>>(em->b, 0, 1);
+        if (em->ncand > 1) {
+            k_graph_objective<<<grid, kPassThreads, 0, s>>>(
+                em->ref, em->m, em->sidx, em->swt, em->K, em->b.candDQ, em->n, em->ncand - 1,
+                em->d_rec, em->mode, em->g.sinv[0], em->g.sinv[1], em->g.sinv[2], em->d_scratch,
+                em->d_flag, gskip, 1, decided);
+            k_reduce_cols<<<1, 32 * kGraphMaxCand, 0, s>>>(em->d_scratch, grid, kGraphMaxCand,
+                                                            em->d_cdata, gskip, decided);
+            k_ng_select<<<1, kNgThreads, 0, s>>>(em->b, 1, em->ncand);
+        }
         FR_CHECK_LAUNCH();
     }
 #undef FR_G

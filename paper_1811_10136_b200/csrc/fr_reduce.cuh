@@ -33,8 +33,8 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NA], double *ds
 // column c of partials[nblk][na] reduced by warp c in a fixed order; skipped
 // when *done is set (device-resident EM loop finished)
 static __global__ void k_reduce_cols(const double *partials, int nblk, int na, double *out,
-                                     const int *done) {
-    if (done && *done) return;
+                                     const int *done, const int *done2 = nullptr) {
+    if ((done && *done) || (done2 && *done2)) return;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (c >= na) return;
     double v = 0.0;
