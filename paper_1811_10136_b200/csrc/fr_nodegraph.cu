@@ -283,6 +283,78 @@ __global__ void k_graph_blocks(const double *__restrict__ ete, const double *__r
     }
 }
 
+// the device loop's block gather in fixed pieces of kGraphPiece entries (one
+// warp per piece: the 195 node blocks of C4 hold ~2,000 entries each, one
+// warp per block left the gather latency bound), each piece's 27 / 21 sums
+// by a warp tree; k_graph_pieces_combine adds a block's pieces in order
+constexpr int kGraphPiece = 256;
+
+__global__ void k_graph_block_pieces(const double *__restrict__ ete, const double *__restrict__ swt,
+                                     int K, const int *__restrict__ dent,
+                                     const int *__restrict__ pent, int n_nodes,
+                                     const int *__restrict__ piece_blk,
+                                     const int *__restrict__ piece_beg,
+                                     const int *__restrict__ piece_end, int n_pieces,
+                                     double *__restrict__ piece_vals, const int *skip) {
+    if (skip && *skip) return;
+    const int pc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (pc >= n_pieces) return;
+    const int blk = piece_blk[pc];
+    const bool is_diag = blk < n_nodes;
+    const int beg = piece_beg[pc], end = piece_end[pc];
+    double acc[27];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) acc[q] = 0.0;
+    for (int e = beg + lane; e < end; e += 32) {
+        double f1, f2;
+        long long p;
+        if (is_diag) {
+            const int code = dent[e];                // p * K + slot
+            p = code / K;
+            const double wa = swt[code];
+            f1 = wa * wa;
+            f2 = wa;
+        } else {
+            p = (unsigned)pent[2 * e];
+            const int sa = pent[2 * e + 1] & 0xff, sc = (pent[2 * e + 1] >> 8) & 0xff;
+            f1 = swt[p * K + sa] * swt[p * K + sc];
+            f2 = 0.0;
+        }
+        const double *src = ete + p * kGraphEte;
+#pragma unroll
+        for (int q = 0; q < 21; ++q) acc[q] = fma(f1, src[q], acc[q]);
+        if (is_diag)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) acc[21 + q] = fma(f2, src[21 + q], acc[21 + q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 27; ++q) {
+        double v = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        acc[q] = v;
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 27; ++q) piece_vals[(long long)pc * 27 + q] = acc[q];
+}
+
+__global__ void k_graph_pieces_combine(const int *__restrict__ blk_piece0, int n_nodes,
+                                       int n_pairs, const double *__restrict__ piece_vals,
+                                       double *__restrict__ diag, double *__restrict__ off,
+                                       const int *skip) {
+    if (skip && *skip) return;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)(n_nodes + n_pairs) * 27) return;
+    const int blk = (int)(t / 27), q = (int)(t % 27);
+    const bool is_diag = blk < n_nodes;
+    if (!is_diag && q >= 21) return;
+    double v = 0.0;
+    for (int pc = blk_piece0[blk]; pc < blk_piece0[blk + 1]; ++pc) v += piece_vals[(long long)pc * 27 + q];
+    if (is_diag) diag[(long long)blk * 27 + q] = v;
+    else off[(long long)(blk - n_nodes) * 21 + q] = v;
+}
+
 constexpr int kGraphMaxCand = 16;
 
 __global__ void __launch_bounds__(kPassThreads, 2)
@@ -1254,11 +1326,26 @@ struct fr_ng_em {
            *d_diag = nullptr, *d_off = nullptr, *d_cdata = nullptr;
     std::vector<void *> owned;
     int *d_flag = nullptr;
+    int *d_piece_blk = nullptr, *d_piece_beg = nullptr, *d_piece_end = nullptr,
+        *d_blk_piece0 = nullptr;
+    double *d_piece_vals = nullptr;
+    int n_pieces = 0;
     cudaGraphExec_t graph = nullptr;
     cudaStream_t stream = nullptr;
 };
 
 using namespace fr;
+
+static void ng_blocks(fr_ng_em *em, const int *skip, cudaStream_t s) {
+    const unsigned g = (unsigned)(((long long)em->n_pieces * 32 + 127) / 128);
+    k_graph_block_pieces<<<g, 128, 0, s>>>(em->d_ete, em->swt, em->K, em->dent, em->pent, em->n,
+                                           em->d_piece_blk, em->d_piece_beg, em->d_piece_end,
+                                           em->n_pieces,
+                                           em->d_piece_vals, skip);
+    const long long t = (long long)(em->n + em->n_pairs) * 27;
+    k_graph_pieces_combine<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(
+        em->d_blk_piece0, em->n, em->n_pairs, em->d_piece_vals, em->d_diag, em->d_off, skip);
+}
 
 static int ng_iteration(fr_ng_em *em, cudaStream_t s) {
     const int grid = pass_grid();
@@ -1279,8 +1366,8 @@ static int ng_iteration(fr_ng_em *em, cudaStream_t s) {
     k_reduce_cols<<<1, 32 * kGraphAcc, 0, s>>>(em->d_scratch, grid, kGraphAcc, em->d_gsums, done);
     const long long warps = (long long)em->n + em->n_pairs;
     const unsigned gb = (unsigned)((warps * 32 + 127) / 128);
-    k_graph_blocks<<<gb, 128, 0, s>>>(em->d_ete, em->swt, em->K, em->dptr, em->dent, em->n,
-                                      em->pptr, em->pent, em->n_pairs, em->d_diag, em->d_off, done);
+    (void)gb;
+    ng_blocks(em, done, s);
     FR_CHECK_LAUNCH();
     const unsigned ga = (unsigned)(((long long)em->n * (em->bw + 1) + kNgAsmThreads - 1) / kNgAsmThreads);
     k_ng_begin<<<1, kNgThreads, 0, s>>>(em->b, 1);
@@ -1292,9 +1379,7 @@ static int ng_iteration(fr_ng_em *em, cudaStream_t s) {
             FR_CHECK_LAUNCH();
             k_reduce_cols<<<1, 32 * kGraphAcc, 0, s>>>(em->d_scratch, grid, kGraphAcc,
                                                       em->d_gsums + 8, gskip);
-            k_graph_blocks<<<gb, 128, 0, s>>>(em->d_ete, em->swt, em->K, em->dptr, em->dent, em->n,
-                                              em->pptr, em->pent, em->n_pairs, em->d_diag,
-                                              em->d_off, gskip);
+            ng_blocks(em, gskip, s);
             k_ng_assemble<<<ga, kNgAsmThreads, 0, s>>>(em->b);
             FR_CHECK_LAUNCH();
         }
@@ -1449,6 +1534,34 @@ int fr_ng_em_create(const fr_lattice *lat, const float *ref, int64_t m, const in
     ok = ok && up(&p, inc_ent, (size_t)2 * n_edges * 4); B.inc_ent = (const int *)p;
     ok = ok && up(&p, pair_lo, (size_t)n_pairs * 4); B.pair_lo = (const int *)p;
     ok = ok && up(&p, pair_hi, (size_t)n_pairs * 4); B.pair_hi = (const int *)p;
+    {
+        // the block gather's pieces (fixed: the entry lists are set at create)
+        std::vector<int32_t> hd((size_t)n + 1), hp((size_t)n_pairs + 1);
+        ok = ok && cudaMemcpyAsync(hd.data(), dptr, hd.size() * 4, cudaMemcpyDeviceToHost, s) ==
+                       cudaSuccess &&
+             (n_pairs == 0 || cudaMemcpyAsync(hp.data(), pptr, hp.size() * 4,
+                                              cudaMemcpyDeviceToHost, s) == cudaSuccess) &&
+             cudaStreamSynchronize(s) == cudaSuccess;
+        std::vector<int32_t> pblk, pbeg, pend, bp0((size_t)n + n_pairs + 1);
+        if (ok)
+            for (int blk = 0; blk < n + n_pairs; ++blk) {
+                const int b0 = blk < n ? hd[blk] : hp[blk - n];
+                const int b1 = blk < n ? hd[blk + 1] : hp[blk - n + 1];
+                bp0[blk] = (int32_t)pblk.size();
+                for (int e = b0; e < b1; e += kGraphPiece) {
+                    pblk.push_back(blk);
+                    pbeg.push_back(e);
+                    pend.push_back(std::min(e + kGraphPiece, b1));
+                }
+            }
+        bp0[(size_t)n + n_pairs] = (int32_t)pblk.size();
+        em->n_pieces = (int)pblk.size();
+        ok = ok && up((void **)&em->d_piece_blk, pblk.data(), pblk.size() * 4) &&
+             up((void **)&em->d_piece_beg, pbeg.data(), pbeg.size() * 4) &&
+             up((void **)&em->d_piece_end, pend.data(), pend.size() * 4) &&
+             up((void **)&em->d_blk_piece0, bp0.data(), bp0.size() * 4) &&
+             dalloc((void **)&em->d_piece_vals, (size_t)std::max(em->n_pieces, 1) * 27 * 8);
+    }
     ok = ok && dalloc((void **)&em->d_gsums, 16 * 8); B.gsums = em->d_gsums;
     ok = ok && dalloc((void **)&em->d_diag, (size_t)n * 27 * 8); B.diag = em->d_diag;
     ok = ok && dalloc((void **)&em->d_off, (size_t)std::max(n_pairs, 1) * 21 * 8); B.off = em->d_off;
