@@ -772,10 +772,8 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
     __shared__ int ok, anyb;
     __shared__ double s_trace, s_lam;
     __shared__ double red[kNgFacThreads / 32];
-    __shared__ double rd2[1][6];                           // 1 / pivot
-    __shared__ __align__(16) double Lkk2[1][36];
+    __shared__ __align__(16) double Akk_s[36];            // the next pivot block
     __shared__ __align__(16) double panel2[1][kNgW][37];   // L_{k+d,k}^T (column c at 6c); 37: rows on distinct banks
-    __shared__ double ybuf[1][6];
     __shared__ double yring[(kNgW + 1) * 6];
     __shared__ __align__(16) double brow[2][kNgW * 36];     // backward: rows of L (and the
                                                             // forward loop's entering row)
@@ -819,6 +817,9 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
 #pragma unroll
         for (int q = 0; q < 36; ++q) blk[q] = 0.0;
         if (owner && pa < n) load(pa, pa - pb);          // window of k = 0: slot = row
+        if (owner && pa == 0 && n > 0)
+#pragma unroll
+            for (int q = 0; q < 36; ++q) Akk_s[q] = blk[q];   // the first pivot block
         for (int e = tid; e < min(W, n) * 6; e += NT) yring[e] = b.bvec[e];
         if (tid == 0) ok = 1;
         __syncthreads();
@@ -849,69 +850,67 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
             const int i = k + hi;
             const bool live = owner && i < n;
             const int si = kw + hi >= W ? kw + hi - W : kw + hi;     // slot of row i
-            // (1) the pivot
-            if (live && hi == 0) {
-                double *Lg = b.L + (size_t)k * W * 36;
-                if (!chol6_reg(blk, rd2[par])) {
-                    ok = 0;
-                } else {
-                    double y[6];
+            // (1) the column k: every owner of a block (i, k) -- the pivot's
+            //     and the panel's -- factors the published pivot block A_kk
+            //     itself (no barrier between pivot and panel), forms
+            //     y_k = L_kk^-1 b_k, then its own block row of L
+            __syncthreads();                            // A_kk (and b_k) published
+            if (live && lo == 0) {
+                double Lk[36], rdk[6], yk[6];
 #pragma unroll
-                    for (int r = 0; r < 6; ++r) {
-                        double v = yring[6 * kw + r];
-#pragma unroll
-                        for (int q = 0; q < r; ++q) v -= blk[6 * r + q] * y[q];
-                        y[r] = v * rd2[par][r];
-                    }
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) {
-                        ybuf[par][r] = y[r];
-                        b.x[6 * k + r] = y[r];
-                        if (incoming) yring[6 * kw + r] = b.bvec[6 * (k + W) + r];
-                    }
-#pragma unroll
-                    for (int q = 0; q < 36; ++q) {
-                        Lkk2[par][q] = blk[q];
-                        Lg[q] = blk[q];
-                    }
-                    // the reciprocal pivots ride in the stored block's (zero)
-                    // upper triangle: (0, 1..5) and (1, 2); the backward
-                    // substitution multiplies by them
-#pragma unroll
-                    for (int c = 0; c < 5; ++c) Lg[1 + c] = rd2[par][c];
-                    Lg[8] = rd2[par][5];
-                }
-            }
-            __syncthreads();
-            if (!ok) break;
-            // (2) the panel: L_ik = A_ik L_kk^-T, b_i -= L_ik y_k
-            if (live && lo == 0 && hi > 0) {
-                const double *Lk = Lkk2[par], *rdk = rd2[par], *yk = ybuf[par];
-                double acc[6];
+                for (int q = 0; q < 36; ++q) Lk[q] = Akk_s[q];
+                const bool good = chol6_reg(Lk, rdk);
 #pragma unroll
                 for (int r = 0; r < 6; ++r) {
-                    double dot = 0.0;
+                    double v = yring[6 * kw + r];
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) {
-                        double u = blk[6 * r + c];
-#pragma unroll
-                        for (int q = 0; q < c; ++q) u -= blk[6 * r + q] * Lk[6 * c + q];
-                        u *= rdk[c];
-                        blk[6 * r + c] = u;
-                        dot += u * yk[c];
-                    }
-                    acc[r] = dot;
+                    for (int q = 0; q < r; ++q) v -= Lk[6 * r + q] * yk[q];
+                    yk[r] = v * rdk[r];
                 }
+                if (hi == 0) {
+                    if (!good) {
+                        ok = 0;
+                    } else {
+                        double *Lg = b.L + (size_t)k * W * 36;
 #pragma unroll
-                for (int r = 0; r < 6; ++r) yring[6 * si + r] -= acc[r];
-                double *Lg = b.L + ((size_t)i * W + hi) * 36;
+                        for (int r = 0; r < 6; ++r) b.x[6 * k + r] = yk[r];
 #pragma unroll
-                for (int r = 0; r < 6; ++r)
+                        for (int q = 0; q < 36; ++q) Lg[q] = Lk[q];
+                        // the reciprocal pivots ride in the stored block's
+                        // (zero) upper triangle: (0, 1..5) and (1, 2); the
+                        // backward substitution multiplies by them
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) {
-                        panel2[par][hi][6 * c + r] = blk[6 * r + c];
-                        Lg[6 * r + c] = blk[6 * r + c];
+                        for (int c = 0; c < 5; ++c) Lg[1 + c] = rdk[c];
+                        Lg[8] = rdk[5];
                     }
+                } else if (good) {
+                    // L_ik = A_ik L_kk^-T, b_i -= L_ik y_k
+                    double acc[6];
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) {
+                        double dot = 0.0;
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) {
+                            double u = blk[6 * r + c];
+#pragma unroll
+                            for (int q = 0; q < c; ++q) u -= blk[6 * r + q] * Lk[6 * c + q];
+                            u *= rdk[c];
+                            blk[6 * r + c] = u;
+                            dot += u * yk[c];
+                        }
+                        acc[r] = dot;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) yring[6 * si + r] -= acc[r];
+                    double *Lg = b.L + ((size_t)i * W + hi) * 36;
+#pragma unroll
+                    for (int r = 0; r < 6; ++r)
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) {
+                            panel2[par][hi][6 * c + r] = blk[6 * r + c];
+                            Lg[6 * r + c] = blk[6 * r + c];
+                        }
+                }
             }
             if (incoming) {
                 double *stage = brow[0];
@@ -922,7 +921,9 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
                 }
             }
             __syncthreads();
-            // (3) the trailing update A_ij -= L_ik L_jk^T (both rows below k)
+            if (!ok) break;
+            // (3) the trailing update A_ij -= L_ik L_jk^T (both rows below k);
+            //     the owner of (k + 1, k + 1) publishes it as the next pivot
             if (live && lo > 0) {
                 const double *Pi = panel2[par][hi], *Pj = panel2[par][lo];
 #pragma unroll
@@ -938,13 +939,19 @@ __global__ void __launch_bounds__(kNgFacThreads, 1) k_ng_factor(NgBufs b) {
 #pragma unroll
                         for (int c = 0; c < 6; ++c) blk[6 * r + c] = fma(-li[r], lj[c], blk[6 * r + c]);
                 }
+                if (hi == 1 && lo == 1)
+#pragma unroll
+                    for (int q = 0; q < 36; ++q) Akk_s[q] = blk[q];
             }
             // (4) row k's blocks leave: their owners take the entering row k + W
+            //     (slot kw; its right-hand side replaces b_k, read in (1))
             if (owner && lo == 0 && incoming) {
                 const int d = hi == 0 ? 0 : W - hi;
                 const double *src = brow[0] + d * 36;
 #pragma unroll
                 for (int q = 0; q < 36; ++q) blk[q] = src[q] + ((d == 0 && q % 7 == 0) ? lam : 0.0);
+                if (hi == 0)
+                    for (int r = 0; r < 6; ++r) yring[6 * kw + r] = b.bvec[6 * (k + W) + r];
             }
             kw = kw + 1 == W ? 0 : kw + 1;
         }
