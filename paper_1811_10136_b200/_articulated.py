@@ -59,12 +59,7 @@ class ArticulatedDevicePath(RigidDevicePath):
         sums = self._allreduce(sums.ravel(), "sum").reshape(nb, 4)
         self.c_body = np.zeros((nb, 3))
         has = sums[:, 3] > 0
-        self.c_body[has] = sums[has, :3] / sums[has, 3:4]
-        if process_group is None:
-            for b in range(nb):
-                s, e = int(starts[b]), int(starts[b + 1])
-                if e > s:     # the single-process centres exactly as before
-                    self.c_body[b] = P32[s:e].mean(axis=0)
+        self.c_body[has] = sums[has, :3] / sums[has, 3:4]      # = mean (np.add.reduce / n)
         chunk_body, chunk_beg, body_chunks = [], [], [0]
         for b in range(nb):
             s, e = int(starts[b]), int(starts[b + 1])
