@@ -739,6 +739,112 @@ __global__ void k_jacobi_dev(int axis, const int *site_keys, const double *vin, 
     }
 }
 
+// the device-resident blur as ONE cooperative launch (the per-axis counts,
+// the reference's extension decision, the extension and the Jacobi pass,
+// for all d + 1 axes, separated by grid barriers instead of 16 launches);
+// counters as in the per-kernel version, nonzero counts per axis in nz[axis]
+__device__ __forceinline__ void blur_grid_sync(unsigned *bar, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v < target) __nanosleep(20);
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
+            unsigned long long *ctr, unsigned long long *nz, long long cap, unsigned *bar) {
+    const unsigned nb = gridDim.x;
+    unsigned phase = 0;
+    const long long tid0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    double *vin = vals, *vout = vals_alt;
+    for (int axis = 0; axis <= D; ++axis) {
+        // nonzero sites of this axis's input
+        {
+            const long long S = (long long)*(volatile unsigned long long *)&ctr[0];
+            unsigned long long mine = 0;
+            for (long long i = tid0; i < S; i += stride) {
+                bool z = false;
+                for (int c = 0; c < nv; ++c) z |= vin[i * nv + c] != 0.0;
+                mine += z;
+            }
+            for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+            if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&nz[axis], mine);
+        }
+        blur_grid_sync(bar, nb * ++phase);
+        if (tid0 == 0) {
+            // permutohedral.py:304-306: extend only while S + 2 nsrc <= cap
+            const unsigned long long S = ctr[0], nsrc = nz[axis];
+            ctr[3] = (S + 2 * nsrc <= (unsigned long long)cap && nsrc > 0) ? S : 0ull;
+        }
+        blur_grid_sync(bar, nb * ++phase);
+        {
+            const long long S = (long long)*(volatile unsigned long long *)&ctr[3];
+            for (long long i = tid0; i < S; i += stride) {
+                bool z = false;
+                for (int c = 0; c < nv; ++c) z |= vin[i * nv + c] != 0.0;
+                if (!z) continue;
+                int k[D + 1];
+#pragma unroll
+                for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
+#pragma unroll
+                for (int sgn = -1; sgn <= 1; sgn += 2) {
+                    int nk[D + 1];
+#pragma unroll
+                    for (int q = 0; q <= D; ++q) nk[q] = k[q] + sgn;
+                    nk[axis] -= sgn * (D + 1);
+                    bool ok = true;
+#pragma unroll
+                    for (int q = 0; q < D; ++q) ok &= (nk[q] > -kKeyLim) && (nk[q] < kKeyLim);
+                    if (!ok) { atomicOr(&ctr[2], 1ull); continue; }
+                    int created;
+                    const int sl = hash_insert(h, pack_key<D>(nk), &created);
+                    if (sl < 0) { atomicOr(&ctr[2], 2ull); continue; }
+                    if (created) {
+                        const long long id = (long long)atomicAdd(&ctr[0], 1ull);
+                        h.site[sl] = (int)id;
+#pragma unroll
+                        for (int q = 0; q <= D; ++q) site_keys[id * (D + 1) + q] = nk[q];
+                    }
+                }
+            }
+        }
+        blur_grid_sync(bar, nb * ++phase);
+        {
+            const long long S = (long long)*(volatile unsigned long long *)&ctr[0];
+            for (long long i = tid0; i < S; i += stride) {
+                int k[D + 1], up[D + 1], dn[D + 1];
+#pragma unroll
+                for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
+#pragma unroll
+                for (int q = 0; q <= D; ++q) { up[q] = k[q] + 1; dn[q] = k[q] - 1; }
+                up[axis] = k[axis] - D;
+                dn[axis] = k[axis] + D;
+                const int iu = hash_find(h, pack_key<D>(up));
+                const int id = hash_find(h, pack_key<D>(dn));
+                for (int c = 0; c < nv; ++c) {
+                    const double vu = iu >= 0 ? vin[(long long)iu * nv + c] : 0.0;
+                    const double vd = id >= 0 ? vin[(long long)id * nv + c] : 0.0;
+                    vout[i * nv + c] = __dadd_rn(__dmul_rn(0.5, vin[i * nv + c]),
+                                                 __dmul_rn(0.25, __dadd_rn(vu, vd)));
+                }
+            }
+        }
+        blur_grid_sync(bar, nb * ++phase);
+        double *t = vin;
+        vin = vout;
+        vout = t;
+    }
+}
+
 template <int D>
 __global__ void k_gather_sites(int S, const int *idx, const int *kin, const double *vin,
                                int nv, int *kout, double *vout) {
@@ -1858,17 +1964,34 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
         k_fill_u64<<<1, 32, 0, s>>>(lat->d_counters, (unsigned long long)S0, 0ull, 0ull);
         FR_CHECK_LAUNCH();
         const BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
-        const unsigned g = 148 * 8;
-        for (int axis = 0; axis <= D; ++axis) {
-            FR_CUDA(cudaMemsetAsync(lat->d_counters + 1, 0, sizeof(unsigned long long), s));
-            k_count_nonzero_dev<<<g, 256, 0, s>>>(lat->vals, nv, lat->d_counters);
-            k_blur_decide<<<1, 1, 0, s>>>(lat->d_counters, cap);
-            k_extend_dev<D><<<g, 256, 0, s>>>(axis, lat->vals, nv, h, lat->site_keys,
-                                              lat->d_counters);
-            k_jacobi_dev<D><<<g, 256, 0, s>>>(axis, lat->site_keys, lat->vals, lat->vals_alt, nv,
-                                              h, lat->d_counters);
-            FR_CHECK_LAUNCH();
-            std::swap(lat->vals, lat->vals_alt);
+        {
+            // one cooperative launch: scratch = [nz[D + 1] | barrier counter]
+            Scratch bsc(s);
+            unsigned long long *nzc;
+            FR_TRY(bsc.get(&nzc, (size_t)D + 2));
+            FR_CUDA(cudaMemsetAsync(nzc, 0, (size_t)(D + 2) * sizeof(unsigned long long), s));
+            unsigned *bar = reinterpret_cast<unsigned *>(nzc + D + 1);
+            static int coop_blocks = 0;
+            if (!coop_blocks) {
+                int per = 0, sms = 148, dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blur_coop<D>, 256, 0) !=
+                        cudaSuccess || per < 1)
+                    per = 1;
+                coop_blocks = sms * std::min(per, 4);
+            }
+            double *v0 = lat->vals, *v1 = lat->vals_alt;
+            int *keys = lat->site_keys;
+            unsigned long long *ctr = lat->d_counters;
+            long long capl = cap;
+            int nvv = nv;
+            BuildHash hh = h;
+            void *args[] = {&v0, &v1, &nvv, &hh, &keys, &ctr, &nzc, &capl, &bar};
+            FR_CUDA(cudaLaunchCooperativeKernel((const void *)k_blur_coop<D>, dim3(coop_blocks),
+                                                dim3(256), args, 0, s));
+            // d + 1 swaps: the result is in vals after an even count
+            if ((D + 1) & 1) std::swap(lat->vals, lat->vals_alt);
         }
         FR_TRY(read_counters(lat, s, hc));
         if (hc[2] & 2ull) {
