@@ -657,88 +657,9 @@ __global__ void k_jacobi(long long S, int axis, const int *site_keys, const doub
 }
 
 // device-resident blur (no host round trip per axis): the site count lives in
-// counters[0], the nonzero count of the axis in counters[1], error flags in
-// counters[2], the extension's loop bound in counters[3]; grid-stride kernels
-// read their bounds from there.  Site rows past the count stay zero in both
-// value buffers (zeroed once up front; the Jacobi pass writes rows < count).
-__global__ void k_count_nonzero_dev(const double *vals, int nv, unsigned long long *ctr) {
-    const long long S = (long long)ctr[0];
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    unsigned long long mine = 0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
-        bool nz = false;
-        for (int c = 0; c < nv; ++c) nz |= vals[i * nv + c] != 0.0;
-        mine += nz;
-    }
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
-    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&ctr[1], mine);
-}
-
-// permutohedral.py:304-306: the axis extends only while S + 2 nsrc <= cap
-__global__ void k_blur_decide(unsigned long long *ctr, long long cap) {
-    const unsigned long long S = ctr[0], nsrc = ctr[1];
-    ctr[3] = (S + 2 * nsrc <= (unsigned long long)cap && nsrc > 0) ? S : 0ull;
-}
-
-template <int D>
-__global__ void k_extend_dev(int axis, const double *vals, int nv, BuildHash h, int *site_keys,
-                             unsigned long long *ctr) {
-    const long long S = (long long)ctr[3];
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
-        bool nz = false;
-        for (int c = 0; c < nv; ++c) nz |= vals[i * nv + c] != 0.0;
-        if (!nz) continue;
-        int k[D + 1];
-#pragma unroll
-        for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
-#pragma unroll
-        for (int sgn = -1; sgn <= 1; sgn += 2) {
-            int nk[D + 1];
-#pragma unroll
-            for (int q = 0; q <= D; ++q) nk[q] = k[q] + sgn;
-            nk[axis] -= sgn * (D + 1);
-            bool ok = true;
-#pragma unroll
-            for (int q = 0; q < D; ++q) ok &= (nk[q] > -kKeyLim) && (nk[q] < kKeyLim);
-            if (!ok) { atomicOr(&ctr[2], 1ull); continue; }
-            int created;
-            int sl = hash_insert(h, pack_key<D>(nk), &created);
-            if (sl < 0) { atomicOr(&ctr[2], 2ull); continue; }
-            if (created) {
-                long long id = (long long)atomicAdd(&ctr[0], 1ull);
-                h.site[sl] = (int)id;
-#pragma unroll
-                for (int q = 0; q <= D; ++q) site_keys[id * (D + 1) + q] = nk[q];
-            }
-        }
-    }
-}
-
-template <int D>
-__global__ void k_jacobi_dev(int axis, const int *site_keys, const double *vin, double *vout,
-                             int nv, BuildHash h, const unsigned long long *ctr) {
-    const long long S = (long long)ctr[0];
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
-        int k[D + 1], up[D + 1], dn[D + 1];
-#pragma unroll
-        for (int q = 0; q <= D; ++q) k[q] = site_keys[i * (D + 1) + q];
-#pragma unroll
-        for (int q = 0; q <= D; ++q) { up[q] = k[q] + 1; dn[q] = k[q] - 1; }
-        up[axis] = k[axis] - D;
-        dn[axis] = k[axis] + D;
-        int iu = hash_find(h, pack_key<D>(up));
-        int id = hash_find(h, pack_key<D>(dn));
-        for (int c = 0; c < nv; ++c) {
-            double vu = iu >= 0 ? vin[(long long)iu * nv + c] : 0.0;
-            double vd = id >= 0 ? vin[(long long)id * nv + c] : 0.0;
-            vout[i * nv + c] = __dadd_rn(__dmul_rn(0.5, vin[i * nv + c]),
-                                         __dmul_rn(0.25, __dadd_rn(vu, vd)));
-        }
-    }
-}
-
+// counters[0], error flags in counters[2], the extension's loop bound in
+// counters[3]; site rows past the count stay zero in both value buffers
+// (zeroed once up front; the Jacobi pass writes rows < count).
 // the device-resident blur as ONE cooperative launch (the per-axis counts,
 // the reference's extension decision, the extension and the Jacobi pass,
 // for all d + 1 axes, separated by grid barriers instead of 16 launches);

@@ -1,5 +1,7 @@
+"""Fixed per-call cost of register(): one-iteration registrations at 2k / 20k /
+1M points from pinned clouds, and a cProfile of 20 calls (diagnostic)."""
 import sys, time, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from oracle import filterreg_oracle as O
 import paper_1811_10136_b200 as fr
 for n in (2000, 20000, 1000000):

@@ -1,5 +1,7 @@
+"""Registration wall time with and without the observation-side setup overlap
+(SETUP_OVERLAP_MIN) at 2k / 10k / 100k points (diagnostic)."""
 import sys, time, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from oracle import filterreg_oracle as O
 import paper_1811_10136_b200 as fr
 from paper_1811_10136_b200 import _rigid

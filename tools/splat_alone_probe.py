@@ -1,5 +1,7 @@
+"""The observation lattice build alone (float64 planes of the C5 1M
+observation cloud, four builds; FR_SPLAT_TIMING=1|2 prints the phases)."""
 import os, sys, numpy as np, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from oracle import filterreg_oracle as O
 import paper_1811_10136_b200 as fr
 from paper_1811_10136_b200 import _rigid
