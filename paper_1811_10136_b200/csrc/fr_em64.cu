@@ -129,14 +129,6 @@ __device__ __forceinline__ void e64_point(const Em64Args &a, const Pose64 &k, do
 // release/acquire) and one read of the partial rows -- no release hop, no
 // state round trip through global memory.  Partial rows are double-buffered
 // by iteration parity (a CTA can only reuse a buffer after every CTA passed
-// the next barrier, i.e. finished reading it).
-// One CTA of the grid-resident loop.  Every CTA keeps the EM state (EmDev)
-// in shared memory and runs the SAME fixed-order reduction and float64 solve
-// on the same partial rows, so all CTAs hold bit-identical poses without a
-// broadcast: an iteration costs one arrival barrier (monotone counter,
-// release/acquire) and one read of the partial rows -- no release hop, no
-// state round trip through global memory.  Partial rows are double-buffered
-// by iteration parity (a CTA can only reuse a buffer after every CTA passed
 // the next barrier, i.e. finished reading it).  The CTA's tiles stream
 // through an S-stage TMA ring that runs ahead across iteration boundaries
 // (the points do not depend on the pose), so the next iteration's first
@@ -171,6 +163,10 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     const int nt = (int)max(0LL, min((long long)a.tiles_per_cta, n_tiles_all - t0));
     const double cp = a.cp;
     copy_cg(&se, a.em, tid, NT);
+    // the state's iteration count at entry (shared: a register live across
+    // the whole loop would be spilled)
+    __shared__ int it0;
+    if (tid == 0) it0 = __ldcg(&a.em->iterations);
     if (S && tid == 0) {
         for (int q = 0; q < S; ++q) {
             mbar_init(&full[q], 1);
@@ -196,26 +192,35 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     unsigned n = 0;                          // consumed tiles (uniform)
     int it = 0;
     constexpr bool kInlineSolve = MINB == 1 && THREADS <= 256;
-    const int it0 = se.iterations;           // the state's iteration count at entry
-    for (; it < a.n_iters; ++it) {
-        // solve == 2 (sharded, fused): the previous pass's sums, all-reduced
-        // across ranks between the launches, are solved first -- by every
-        // CTA, as in the unsharded loop -- then this launch's pass
-        if (a.solve == 2 && se.pending) {
-            if (tid < kE64Stats) tsum[tid] = __ldcg(a.sums + tid);
+    // ONE solve site at the top of the loop (a second inlined copy of the
+    // serial solve costs the pass its registers): solve == 1 solves the
+    // previous iteration's reduced sums (tsum) there, one trip past the last
+    // pass; solve == 2 (sharded, fused: one pass per launch) the previous
+    // launch's sums, all-reduced across ranks between the launches, then runs
+    // this launch's pass
+    for (;; ++it) {
+        const bool solve_now = a.solve == 1 ? it > 0 : (a.solve == 2 && it == 0 && se.pending);
+        if (solve_now) {
+            if (a.solve == 2 && tid < kE64Stats) tsum[tid] = __ldcg(a.sums + tid);
             __syncthreads();
             if (tid == 0) {
                 const int n = se.max_em_iters;
+                unsigned long long *st =
+                    a.prof && blockIdx.x == 0 && a.solve == 1 ? a.prof + 8 * (it - 1) + 5 : nullptr;
                 se.pending = 0;
-                rigid_solve_impl<kInlineSolve>(tsum, &se, a.traces, a.traces + n,
-                                               a.traces + 2 * n, blockIdx.x == 0, nullptr,
-                                               a.traces + 3 * n);
+                if (kInlineSolve)   // 255 registers: the lean solve inlined
+                    rigid_solve_impl<true>(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
+                                           blockIdx.x == 0, st, a.traces + 3 * n);
+                else
+                    rigid_solve_body(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
+                                     blockIdx.x == 0, st);
+                if (st) a.prof[8 * (it - 1) + 4] = gtime();
             }
             __syncthreads();
         }
         // identical in every CTA; a pass-only launch after termination is a
         // no-op too (the sharded loop's replayed chunks run past the end)
-        if (se.done) break;
+        if (it >= a.n_iters || se.done) break;
         if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 0] = gtime();
         double acc[kE64Stats];
 #pragma unroll
@@ -357,22 +362,6 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
         }
         __syncthreads();
         if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 3] = gtime();
-        if (a.solve == 1) {
-            if (tid == 0) {
-                const int n = se.max_em_iters;
-                if (kInlineSolve)   // 255 registers: the lean solve inlined
-                    rigid_solve_impl<true>(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
-                                           blockIdx.x == 0,
-                                           a.prof && blockIdx.x == 0 ? a.prof + 8 * it + 5 : nullptr,
-                                           a.traces + 3 * n);
-                else
-                    rigid_solve_body(tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
-                                     blockIdx.x == 0,
-                                     a.prof && blockIdx.x == 0 ? a.prof + 8 * it + 5 : nullptr);
-            }
-            __syncthreads();
-        }
-        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 4] = gtime();
     }
     // the deferred update magnitudes of this launch's iterations (lean solve)
     if (kInlineSolve && a.solve && blockIdx.x == 0)
