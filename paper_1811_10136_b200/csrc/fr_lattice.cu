@@ -393,6 +393,15 @@ __global__ void k_entries_to_ids(long long E, unsigned sentinel, unsigned K, con
     }
 }
 
+// row K of the run arrays as an empty sentinel run (overwritten by the RLE
+// when the sentinel run exists)
+__global__ void k_run_pad(unsigned K, unsigned sentinel, unsigned *run_slot, int *run_cnt) {
+    if (threadIdx.x == 0) {
+        run_slot[K] = sentinel;
+        run_cnt[K] = 0;
+    }
+}
+
 __global__ void k_runs_to_slots(const int *d_nruns, unsigned K, unsigned sentinel,
                                 const int *slot_of_id, unsigned *run_slot) {
     const int nr = *d_nruns;
@@ -656,14 +665,14 @@ __global__ void k_jacobi(long long S, int axis, const int *site_keys, const doub
     }
 }
 
-// device-resident blur (no host round trip per axis): the site count lives in
-// counters[0], error flags in counters[2], the extension's loop bound in
-// counters[3]; site rows past the count stay zero in both value buffers
-// (zeroed once up front; the Jacobi pass writes rows < count).
-// the device-resident blur as ONE cooperative launch (the per-axis counts,
-// the reference's extension decision, the extension and the Jacobi pass,
-// for all d + 1 axes, separated by grid barriers instead of 16 launches);
-// counters as in the per-kernel version, nonzero counts per axis in nz[axis]
+// the device-resident blur as ONE cooperative launch (no host round trip per
+// axis): per axis the reference's extension decision (taken by every CTA
+// from the same counts), the extension, and the Jacobi pass (which also
+// counts the next axis's nonzero inputs), separated by 2 grid barriers (8 in
+// all for d = 3) instead of launches.  The site count lives in counters[0],
+// error flags in counters[2], nonzero counts per axis in nz[axis]; site rows
+// past the count stay zero in both value buffers (zeroed once up front; the
+// Jacobi pass writes rows < count).
 __device__ __forceinline__ void blur_grid_sync(unsigned *bar, unsigned target) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -688,9 +697,13 @@ k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
     const long long stride = (long long)gridDim.x * blockDim.x;
     double *vin = vals, *vout = vals_alt;
     for (int axis = 0; axis <= D; ++axis) {
-        // nonzero sites of this axis's input
-        {
-            const long long S = (long long)*(volatile unsigned long long *)&ctr[0];
+        // the axis's input site count: nothing changes ctr[0] until the
+        // extension below, which every CTA reaches only after the barrier
+        const long long S_in = (long long)*(volatile unsigned long long *)&ctr[0];
+        // nonzero sites of this axis's input (axis > 0: counted by the
+        // previous axis's Jacobi pass as it wrote them)
+        if (axis == 0) {
+            const long long S = S_in;
             unsigned long long mine = 0;
             for (long long i = tid0; i < S; i += stride) {
                 bool z = false;
@@ -700,15 +713,13 @@ k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
             for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
             if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&nz[axis], mine);
         }
-        blur_grid_sync(bar, nb * ++phase);
-        if (tid0 == 0) {
-            // permutohedral.py:304-306: extend only while S + 2 nsrc <= cap
-            const unsigned long long S = ctr[0], nsrc = nz[axis];
-            ctr[3] = (S + 2 * nsrc <= (unsigned long long)cap && nsrc > 0) ? S : 0ull;
-        }
-        blur_grid_sync(bar, nb * ++phase);
+        if (axis == 0) blur_grid_sync(bar, nb * ++phase);
         {
-            const long long S = (long long)*(volatile unsigned long long *)&ctr[3];
+            // permutohedral.py:304-306: extend only while S + 2 nsrc <= cap
+            // (decided by every CTA from the same counts: no extra barrier)
+            const unsigned long long nsrc = *(volatile unsigned long long *)&nz[axis];
+            const long long S = ((unsigned long long)S_in + 2 * nsrc <= (unsigned long long)cap &&
+                                 nsrc > 0) ? S_in : 0;
             for (long long i = tid0; i < S; i += stride) {
                 bool z = false;
                 for (int c = 0; c < nv; ++c) z |= vin[i * nv + c] != 0.0;
@@ -741,6 +752,7 @@ k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
         blur_grid_sync(bar, nb * ++phase);
         {
             const long long S = (long long)*(volatile unsigned long long *)&ctr[0];
+            unsigned long long mine = 0;
             for (long long i = tid0; i < S; i += stride) {
                 int k[D + 1], up[D + 1], dn[D + 1];
 #pragma unroll
@@ -751,15 +763,24 @@ k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
                 dn[axis] = k[axis] + D;
                 const int iu = hash_find(h, pack_key<D>(up));
                 const int id = hash_find(h, pack_key<D>(dn));
+                bool z = false;
                 for (int c = 0; c < nv; ++c) {
                     const double vu = iu >= 0 ? vin[(long long)iu * nv + c] : 0.0;
                     const double vd = id >= 0 ? vin[(long long)id * nv + c] : 0.0;
-                    vout[i * nv + c] = __dadd_rn(__dmul_rn(0.5, vin[i * nv + c]),
-                                                 __dmul_rn(0.25, __dadd_rn(vu, vd)));
+                    const double o = __dadd_rn(__dmul_rn(0.5, vin[i * nv + c]),
+                                               __dmul_rn(0.25, __dadd_rn(vu, vd)));
+                    vout[i * nv + c] = o;
+                    z |= o != 0.0;
                 }
+                mine += z;
+            }
+            // the next axis's nonzero input count
+            if (axis < D) {
+                for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+                if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&nz[axis + 1], mine);
             }
         }
-        blur_grid_sync(bar, nb * ++phase);
+        if (axis < D) blur_grid_sync(bar, nb * ++phase);   // the kernel's end orders the last
         double *t = vin;
         vin = vout;
         vout = t;
@@ -1487,6 +1508,8 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     void *tmp = sort_tmp;
     if (!tmp || tmp_bytes > sort_bound) FR_TRY(sc.get((char **)&tmp, tmp_bytes));
     pc.lap("sort_tmp");
+    k_run_pad<<<1, 32, 0, s>>>(K, (unsigned)cap, run_slot, run_cnt);
+    FR_CHECK_LAUNCH();
     FR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, entry_slot, sorted_slot, entry_idx,
                                             sorted_idx, (int)E, 0, end_bit, s));
     pc.lap("sort_enqueue");
@@ -1495,8 +1518,11 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
     pc.lap("rle_enqueue");
     k_runs_to_slots<<<148, 256, 0, s>>>(d_nruns, K, (unsigned)cap, slot_of_id, run_slot);
     FR_CHECK_LAUNCH();
-    int nruns = 0;
-    FR_TRY(d2h_sync(&nruns, d_nruns, sizeof(int), s));
+    // the runs are the K sites (every created slot holds its creator's entry)
+    // plus the sentinel run when some entry has none: K + 1 rows with row K
+    // padded as an empty sentinel run when the RLE wrote only K -- no host
+    // read of the run count
+    const int nruns = (int)K + 1;
     FR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, run_cnt, run_off, nruns, s));
     pc.lap("sort+runs");
     double *run_vals;
@@ -1580,8 +1606,8 @@ static int splat_impl(fr_lattice *lat, const Src &src, long long n, int nv, cuda
         lat->n_sites = S;
     }
     pc.lap("sites");
+    // 2 S slots for S distinct keys: the inserts cannot fail, no flag read
     FR_TRY(rehash_sites<D>(lat, next_pow2(2ull * (unsigned long long)lat->n_sites), s));
-    FR_TRY(read_counters(lat, s, hc));
     pc.lap("rehash");
     return FR_OK;
 }
@@ -1892,16 +1918,21 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
             FR_TRY(bsc.get(&nzc, (size_t)D + 2));
             FR_CUDA(cudaMemsetAsync(nzc, 0, (size_t)(D + 2) * sizeof(unsigned long long), s));
             unsigned *bar = reinterpret_cast<unsigned *>(nzc + D + 1);
-            static int coop_blocks = 0;
-            if (!coop_blocks) {
+            static int coop_max = 0;
+            if (!coop_max) {
                 int per = 0, sms = 148, dev = 0;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blur_coop<D>, 256, 0) !=
                         cudaSuccess || per < 1)
                     per = 1;
-                coop_blocks = sms * std::min(per, 4);
+                coop_max = sms * std::min(per, 4);
             }
+            // grid sized by the work (the sites grow ~3x over the axes): each
+            // grid barrier costs about one arrival per CTA, so a few thousand
+            // sites take a few dozen CTAs, not the whole co-resident grid
+            const int coop_blocks = (int)std::min<long long>(
+                coop_max, std::max<long long>(16, (3 * S0 + 255) / 256));
             double *v0 = lat->vals, *v1 = lat->vals_alt;
             int *keys = lat->site_keys;
             unsigned long long *ctr = lat->d_counters;
@@ -2056,14 +2087,20 @@ __global__ void k_bbox_part(const T *pos, long long n, T *part) {
 
 template <class T>
 __global__ void k_bbox_final(const T *part, int nb, T *lohi) {
-    const int q = threadIdx.x;
+    // warp q combines column q (6 warps): lanes stride over the block rows,
+    // then a shuffle tree (min / max are exact, any order gives the same value)
+    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (q >= 6) return;
-    T v = part[q];
-    for (int b = 1; b < nb; ++b) {
+    T v = q < 3 ? (T)INFINITY : (T)-INFINITY;
+    for (int b = lane; b < nb; b += 32) {
         const T o = part[b * 6 + q];
         v = q < 3 ? (o < v ? o : v) : (o > v ? o : v);
     }
-    lohi[q] = v;
+    for (int o = 16; o > 0; o >>= 1) {
+        const T w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = q < 3 ? (w < v ? w : v) : (w > v ? w : v);
+    }
+    if (lane == 0) lohi[q] = v;
 }
 
 template <class T>
@@ -2141,7 +2178,7 @@ static int sort_morton_impl(T *pos, int64_t n, int planes, int32_t *perm_out, vo
     void *tmpb;
     FR_TRY(sc.get((char **)&tmpb, t2));
     k_bbox_part<T><<<kBoxBlocks, 256, 0, s>>>(pos, n, part);
-    k_bbox_final<T><<<1, 32, 0, s>>>(part, kBoxBlocks, lohi);
+    k_bbox_final<T><<<1, 192, 0, s>>>(part, kBoxBlocks, lohi);
     k_morton<<<grid_for(n), 256, 0, s>>>(pos, n, lohi, codes, idx);
     FR_CHECK_LAUNCH();
     FR_CUDA(cub::DeviceRadixSort::SortPairs(tmpb, t2, codes, codes2, idx, perm, (int)n, 0,
