@@ -366,7 +366,7 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     // the deferred update magnitudes of this launch's iterations (lean solve)
     if (kInlineSolve && a.solve && blockIdx.x == 0)
         rigid_finish_tnorms(a.traces + se.max_em_iters, a.traces + 3 * se.max_em_iters, it0,
-                            se.iterations);
+                            se.iterations, se.diameter);
     // no bulk copy may still target this CTA's shared memory when it exits
     if (producer && lane == 0)
         for (; n < issued; ++n) mbar_wait(&full[n % SS], (n / SS) & 1);
@@ -574,6 +574,8 @@ int fr_em64_create(const fr_lattice *lat, const double *ref, int64_t m,
     h.gain = lat->c.gain;
     h.diameter = cfg->diameter;
     h.tol = cfg->twist_tolerance;
+    h.conv_q = cfg->twist_tolerance * cfg->diameter * (cfg->twist_tolerance * cfg->diameter) *
+               (1.0 + 1e-9);
     h.use_damping = cfg->damping >= 0.0;
     h.damping = cfg->damping;
     h.step_tol = cfg->step_tolerance;
