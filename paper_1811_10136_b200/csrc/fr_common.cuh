@@ -585,6 +585,12 @@ struct fr_lattice {
     // d >= 4: sorted 128-bit site keys (hi / lo words) and their codec
     unsigned long long *wkh = nullptr, *wkl = nullptr;
     fr::WideCodec wc{};
+    // set by the device-resident blur (its one host read): the nonzero site
+    // count after the last axis (-1: unknown) and, for d = 3, the q = k >> 2
+    // box of those sites' first three coordinates (lo[3], hi[3])
+    long long blur_keep = -1;
+    int blur_box[6] = {0, 0, 0, 0, 0, 0};
+    int box_valid = 0;
     // device counters / flags
     unsigned long long *d_counters = nullptr;   // [0] sites, [1] src count, [2] overflow
     cudaStream_t stream = nullptr;              // stream of the last build call (pool ordering)

@@ -687,10 +687,18 @@ __device__ __forceinline__ void blur_grid_sync(unsigned *bar, unsigned target) {
     __syncthreads();
 }
 
+// the cooperative blur's scratch: nz[0..n_nz), the barrier word, the box
+__global__ void k_blur_scratch_init(unsigned long long *nz, int n_nz, int *box) {
+    const int t = threadIdx.x;
+    if (t < n_nz) nz[t] = 0ull;
+    if (t < 6) box[t] = t < 3 ? INT_MAX : INT_MIN;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256)
 k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
-            unsigned long long *ctr, unsigned long long *nz, long long cap, unsigned *bar) {
+            unsigned long long *ctr, unsigned long long *nz, long long cap, unsigned *bar,
+            int *box) {
     const unsigned nb = gridDim.x;
     unsigned phase = 0;
     const long long tid0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -753,6 +761,7 @@ k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
         {
             const long long S = (long long)*(volatile unsigned long long *)&ctr[0];
             unsigned long long mine = 0;
+            int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
             for (long long i = tid0; i < S; i += stride) {
                 int k[D + 1], up[D + 1], dn[D + 1];
 #pragma unroll
@@ -773,11 +782,31 @@ k_blur_coop(double *vals, double *vals_alt, int nv, BuildHash h, int *site_keys,
                     z |= o != 0.0;
                 }
                 mine += z;
+                if (D == 3 && axis == D && z) {
+#pragma unroll
+                    for (int c = 0; c < 3 && c <= D; ++c) {
+                        lo[c] = min(lo[c], k[c] >> 2);
+                        hi[c] = max(hi[c], k[c] >> 2);
+                    }
+                }
             }
-            // the next axis's nonzero input count
-            if (axis < D) {
-                for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
-                if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&nz[axis + 1], mine);
+            // the next axis's nonzero input count; after the last axis the
+            // nonzero rows that survive the final drop (nz[D + 1]) and their box
+            for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+            if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&nz[axis + 1], mine);
+            if (D == 3 && axis == D) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        lo[c] = min(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+                        hi[c] = max(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+                    }
+                    if ((threadIdx.x & 31) == 0 && lo[c] <= hi[c]) {
+                        atomicMin(box + c, lo[c]);
+                        atomicMax(box + 3 + c, hi[c]);
+                    }
+                }
             }
         }
         if (axis < D) blur_grid_sync(bar, nb * ++phase);   // the kernel's end orders the last
@@ -1616,6 +1645,10 @@ template <int D>
 static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
     long long S = lat->n_sites;
     if (S == 0) return FR_OK;
+    // the device-resident blur counted the surviving rows: nothing to drop
+    // (the usual case), or the count without a host read
+    const long long known = lat->blur_keep;
+    if (known == S) return FR_OK;
     Scratch sc(s);
     unsigned char *flags;
     int *iota, *sel, *d_n;
@@ -1632,8 +1665,8 @@ static int compact_nonzero(fr_lattice *lat, cudaStream_t s) {
     void *tmp;
     FR_TRY(sc.get((char **)&tmp, t));
     FR_CUDA(cub::DeviceSelect::Flagged(tmp, t, iota, flags, sel, d_n, (int)S, s));
-    int keep = 0;
-    FR_TRY(d2h_sync(&keep, d_n, sizeof(int), s));
+    int keep = (int)known;
+    if (known < 0) FR_TRY(d2h_sync(&keep, d_n, sizeof(int), s));
     if (keep == S) return FR_OK;
     int *nk;
     double *nvls;
@@ -1752,15 +1785,21 @@ static int build_dense_grid(fr_lattice *lat, cudaStream_t s) {
     // nv = 4 ([1, y]: both grids); nv = 7 ([1, y, n], point-to-plane: the
     // float64 grid only, 64-byte rows)
     if (lat->dim != 3 || (lat->nv != 4 && lat->nv != 7) || lat->n_sites == 0) return FR_OK;
-    int *dbox = nullptr;
-    FR_CUDA(cudaMallocAsync(&dbox, 6 * sizeof(int), s));
-    k_init_box<<<1, 32, 0, s>>>(dbox);
-    k_site_qbox<<<std::min<long long>(grid_for(lat->n_sites), 1184), 256, 0, s>>>(
-        lat->n_sites, lat->site_keys, dbox);
-    FR_CHECK_LAUNCH();
     int box[6];
-    FR_TRY(d2h_sync(box, dbox, sizeof(box), s));
-    FR_CUDA(cudaFreeAsync(dbox, s));
+    if (lat->box_valid) {
+        // from the device-resident blur's read (the same sites: the final
+        // drop keeps exactly the rows the box was taken over)
+        memcpy(box, lat->blur_box, sizeof(box));
+    } else {
+        int *dbox = nullptr;
+        FR_CUDA(cudaMallocAsync(&dbox, 6 * sizeof(int), s));
+        k_init_box<<<1, 32, 0, s>>>(dbox);
+        k_site_qbox<<<std::min<long long>(grid_for(lat->n_sites), 1184), 256, 0, s>>>(
+            lat->n_sites, lat->site_keys, dbox);
+        FR_CHECK_LAUNCH();
+        FR_TRY(d2h_sync(box, dbox, sizeof(box), s));
+        FR_CUDA(cudaFreeAsync(dbox, s));
+    }
     long long n[3], cells = 1;
     for (int c = 0; c < 3; ++c) {
         n[c] = (long long)box[3 + c] - box[c] + 1 + 2 * fr::kDensePad;
@@ -1894,6 +1933,8 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
         return FR_ESTATE;
     }
     PhaseClock pc(s);
+    lat->blur_keep = -1;
+    lat->box_valid = 0;
     const int nv = lat->nv;
     const long long cap = std::max<long long>(64 * lat->n_sites, 200000);   // permutohedral.py:304
     unsigned long long hc[3];
@@ -1911,13 +1952,15 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
         k_fill_u64<<<1, 32, 0, s>>>(lat->d_counters, (unsigned long long)S0, 0ull, 0ull);
         FR_CHECK_LAUNCH();
         const BuildHash h{lat->hkeys, lat->hsite, lat->hmask};
+        Scratch bsc(s);
+        unsigned long long *nzc;
         {
-            // one cooperative launch: scratch = [nz[D + 1] | barrier counter]
-            Scratch bsc(s);
-            unsigned long long *nzc;
-            FR_TRY(bsc.get(&nzc, (size_t)D + 2));
-            FR_CUDA(cudaMemsetAsync(nzc, 0, (size_t)(D + 2) * sizeof(unsigned long long), s));
-            unsigned *bar = reinterpret_cast<unsigned *>(nzc + D + 1);
+            // one cooperative launch: scratch = [nz[D + 2] | barrier | box[6]]
+            FR_TRY(bsc.get(&nzc, (size_t)D + 6));
+            unsigned *bar = reinterpret_cast<unsigned *>(nzc + D + 2);
+            int *box = reinterpret_cast<int *>(nzc + D + 3);
+            k_blur_scratch_init<<<1, 32, 0, s>>>(nzc, D + 3, box);
+            FR_CHECK_LAUNCH();
             static int coop_max = 0;
             if (!coop_max) {
                 int per = 0, sms = 148, dev = 0;
@@ -1939,18 +1982,41 @@ static int blur_impl(fr_lattice *lat, cudaStream_t s) {
             long long capl = cap;
             int nvv = nv;
             BuildHash hh = h;
-            void *args[] = {&v0, &v1, &nvv, &hh, &keys, &ctr, &nzc, &capl, &bar};
+            void *args[] = {&v0, &v1, &nvv, &hh, &keys, &ctr, &nzc, &capl, &bar, &box};
             FR_CUDA(cudaLaunchCooperativeKernel((const void *)k_blur_coop<D>, dim3(coop_blocks),
                                                 dim3(256), args, 0, s));
             // d + 1 swaps: the result is in vals after an even count
             if ((D + 1) & 1) std::swap(lat->vals, lat->vals_alt);
         }
-        FR_TRY(read_counters(lat, s, hc));
-        if (hc[2] & 2ull) {
+        // ONE host read: counters, the final nonzero count and the box
+        unsigned long long hx[4 + 1 + 3];
+        {
+            unsigned long long *pin = static_cast<unsigned long long *>(pinned_scratch());
+            unsigned long long *dst = pin ? pin : hx;
+            FR_CUDA(cudaMemcpyAsync(dst, lat->d_counters, 3 * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, s));
+            FR_CUDA(cudaMemcpyAsync(dst + 4, nzc + D + 1, sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, s));
+            FR_CUDA(cudaMemcpyAsync(dst + 5, nzc + D + 3, 3 * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, s));
+            FR_CUDA(cudaStreamSynchronize(s));
+            if (pin) memcpy(hx, pin, sizeof(hx));
+        }
+        if (hx[2] & 1ull) {
+            set_error("lattice coordinate outside the packable range (|key| >= %lld); "
+                      "features / sigma too large", (long long)kKeyLim);
+            return FR_ECAPACITY;
+        }
+        if (hx[2] & 2ull) {
             set_error("blur hash table overflow");
             return FR_ECAPACITY;
         }
-        lat->n_sites = (long long)hc[0];
+        lat->n_sites = (long long)hx[0];
+        lat->blur_keep = (long long)hx[4];
+        if (D == 3) {
+            memcpy(lat->blur_box, hx + 5, sizeof(lat->blur_box));
+            lat->box_valid = lat->blur_keep > 0;
+        }
         pc.lap("blur_axes");
     }
     for (int axis = 0; axis <= D && cap > kDeviceBlurMaxSites; ++axis) {
