@@ -66,40 +66,43 @@ struct Em64Args {
 
 
 
-// one model point: forward map, simplex, slice, epilogue, statistics
-// (h0, h1, h2) = x_ref - c_ref (the centred tile); valid = 0 for the padding
-// of the last tile (computed, contributes nothing: no branch)
-__device__ __forceinline__ void e64_point(const Em64Args &a, const Pose64 &k, double cp,
-                                          double h0, double h1, double h2, bool valid,
-                                          double (&acc)[kE64Stats]) {
+// the record (w, r, x - c_world) of one model point: forward map, simplex,
+// slice, epilogue.  (h0, h1, h2) = x_ref - c_ref (the centred tile); valid = 0
+// for the padding of the last tile (computed, contributes nothing: no branch).
+// Moments epilogue (estep.py:195-205): m0 = max(out0, 0), supported iff
+// m0 >= 1e-12, w = m0 / (m0 + c'), target = m1 / m0; unsupported points get
+// w = 0 and target = x (zero residual).  One reciprocal: q = 1 / (m0 (m0 + c')),
+// 1 / m0 = (m0 + c') q, w = m0^2 q.
+__device__ __forceinline__ void e64_record(const Em64Args &a, const Pose64 &k, double cp,
+                                           double h0, double h1, double h2, bool valid,
+                                           double &w, double (&r)[3], double (&xt)[3]) {
     const DenseSliceD &g = a.g;
-    double xt[3], X[3];
+    double X[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         xt[i] = fma(k.R[3 * i + 2], h2, fma(k.R[3 * i + 1], h1, k.R[3 * i] * h0));
-        X[i] = xt[i] + k.cw[i];                          // x = R x_ref + t
+        X[i] = xt[i] + k.cw[i];
     }
     Simplex64 S;
     e64_simplex(g, a.sc, X, S);
     double o[4];
     e64_gather<2>(g, S, o);
-    const double o0 = o[0], o1 = o[1], o2 = o[2], o3 = o[3];
-    const bool in_range = S.in_range;
-    // moments epilogue (estep.py:195-205): m0 = max(out0, 0), supported iff
-    // m0 >= 1e-12, w = m0 / (m0 + c'), target = m1 / m0; unsupported points
-    // get w = 0 and target = x (zero residual).  One reciprocal:
-    // q = 1 / (m0 (m0 + c')), 1 / m0 = (m0 + c') q, w = m0^2 q.
-    const double m0 = o3 > 0.0 ? o3 : 0.0;
-    const bool sup = m0 >= 1e-12 && in_range && valid;
+    const double m0 = o[3] > 0.0 ? o[3] : 0.0;
+    const bool sup = m0 >= 1e-12 && S.in_range && valid;
     const double den = m0 + cp;
     const double q = rcp64(m0 * den);
     const double inv = den * q;
-    const double w = sup ? (cp > 0.0 ? (m0 * m0) * q : 1.0) : 0.0;
-    double r[3];
-    r[0] = sup ? fma(-o0, inv, X[0]) : 0.0;
-    r[1] = sup ? fma(-o1, inv, X[1]) : 0.0;
-    r[2] = sup ? fma(-o2, inv, X[2]) : 0.0;
-    // sufficient statistics about c_world (layout: _rigid.py)
+    w = sup ? (cp > 0.0 ? (m0 * m0) * q : 1.0) : 0.0;
+    r[0] = sup ? fma(-o[0], inv, X[0]) : 0.0;
+    r[1] = sup ? fma(-o[1], inv, X[1]) : 0.0;
+    r[2] = sup ? fma(-o[2], inv, X[2]) : 0.0;
+}
+
+// the 25 point-to-point sufficient statistics of one record, about c_world
+// (layout: _rigid.py)
+__device__ __forceinline__ void e64_accumulate(double w, const double (&r)[3],
+                                               const double (&xt)[3],
+                                               double (&acc)[kE64Stats]) {
     double wy[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) wy[j] = w * xt[j];
@@ -120,6 +123,15 @@ __device__ __forceinline__ void e64_point(const Em64Args &a, const Pose64 &k, do
         for (int q2 = 0; q2 < 3; ++q2) acc[13 + 3 * j + q2] = fma(wr, xt[q2], acc[13 + 3 * j + q2]);
         acc[22 + j] = fma(wr, r[j], acc[22 + j]);
     }
+}
+
+// one model point: its record, then its statistics
+__device__ __forceinline__ void e64_point(const Em64Args &a, const Pose64 &k, double cp,
+                                          double h0, double h1, double h2, bool valid,
+                                          double (&acc)[kE64Stats]) {
+    double w, r[3], xt[3];
+    e64_record(a, k, cp, h0, h1, h2, valid, w, r, xt);
+    e64_accumulate(w, r, xt, acc);
 }
 
 // One CTA of the grid-resident loop.  Every CTA keeps the EM state (EmDev)
@@ -378,6 +390,233 @@ __device__ __forceinline__ void em64_cta(const Em64Args &a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised CTA (FR_EM64_VARIANT=4): 384 threads.  Warpgroups 0-1 (256
+// "record" threads, setmaxnreg 208) run the forward map, simplex, gather and
+// epilogue of P points per step and hand each point's record (w, r, x -
+// c_world: 7 doubles) to warpgroup 2 (128 "statistics" threads, setmaxnreg
+// 88) through a 2-stage shared-memory ring (named barriers: full = records
+// written, empty = records consumed); the statistics threads hold the 25
+// accumulators, so the record side keeps its registers for P independent
+// point chains.  Reduction, grid barrier and solve as in em64_cta.
+constexpr int kWsE = 256, kWsM = 128, kWsThreads = kWsE + kWsM;
+constexpr int kWsRec = 7, kWsStages = 2;
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct WsShared {
+    double red[kWsThreads / 32][32];
+    double tsum[kE64Row];
+    EmDev se;
+    int it0;
+};
+
+// the whole loop of one role (kStat: the statistics warpgroup), so each
+// role's code sits after its own setmaxnreg; both roles pass the same
+// sequence of CTA barriers
+template <int P, bool kStat>
+__device__ __forceinline__ void em64_ws_loop(const Em64Args &a, WsShared &sh, double *ring) {
+    constexpr int NT = kWsThreads, W = NT / 32, WM = kWsM / 32;
+    EmDev &se = sh.se;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nb = (int)gridDim.x;
+    const long long t0 = (long long)blockIdx.x * a.tiles_per_cta;
+    const long long n_tiles_all = (a.m + kWsE - 1) / kWsE;
+    const int nt = (int)max(0LL, min((long long)a.tiles_per_cta, n_tiles_all - t0));
+    const int steps = (nt + P - 1) / P;
+    const double cp = a.cp;
+    int it = 0;
+    for (;; ++it) {
+        const bool solve_now = a.solve == 1 ? it > 0 : (a.solve == 2 && it == 0 && se.pending);
+        if (solve_now) {
+            if (a.solve == 2 && tid < kE64Stats) sh.tsum[tid] = __ldcg(a.sums + tid);
+            __syncthreads();
+            if (!kStat && tid == 0) {
+                const int n = se.max_em_iters;
+                unsigned long long *st =
+                    a.prof && blockIdx.x == 0 && a.solve == 1 ? a.prof + 8 * (it - 1) + 5 : nullptr;
+                se.pending = 0;
+                rigid_solve_impl<true>(sh.tsum, &se, a.traces, a.traces + n, a.traces + 2 * n,
+                                       blockIdx.x == 0, st, a.traces + 3 * n);
+                if (st) a.prof[8 * (it - 1) + 4] = gtime();
+            }
+            __syncthreads();
+        }
+        if (it >= a.n_iters || se.done) break;
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 0] = gtime();
+        if constexpr (!kStat) {
+            Pose64 pose;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) pose.R[q] = se.k.R[q];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) pose.cw[q] = se.k.c_world[q];
+            const double *src = a.tiles + t0 * 3 * kWsE + tid;
+            long long pidx = t0 * kWsE + tid;
+            double nx[P], ny[P], nz[P];
+#pragma unroll
+            for (int u = 0; u < P; ++u) {
+                nx[u] = ny[u] = nz[u] = 0.0;
+                if (u < nt) {
+                    nx[u] = __ldg(src + u * 3 * kWsE);
+                    ny[u] = __ldg(src + u * 3 * kWsE + kWsE);
+                    nz[u] = __ldg(src + u * 3 * kWsE + 2 * kWsE);
+                }
+            }
+            for (int st = 0; st < steps; ++st, pidx += P * kWsE) {
+                double hx[P], hy[P], hz[P];
+#pragma unroll
+                for (int u = 0; u < P; ++u) {
+                    hx[u] = nx[u];
+                    hy[u] = ny[u];
+                    hz[u] = nz[u];
+                }
+                src += 3 * P * kWsE;
+#pragma unroll
+                for (int u = 0; u < P; ++u)
+                    if ((st + 1) * P + u < nt) {
+                        nx[u] = __ldg(src + u * 3 * kWsE);
+                        ny[u] = __ldg(src + u * 3 * kWsE + kWsE);
+                        nz[u] = __ldg(src + u * 3 * kWsE + 2 * kWsE);
+                    }
+                const int stage = st & 1;
+                if (st >= kWsStages) named_sync(3 + stage, NT);      // records consumed
+                double *slot = ring + (size_t)stage * P * kWsRec * kWsE + tid;
+#pragma unroll
+                for (int u = 0; u < P; ++u) {
+                    double w, r[3], xt[3];
+                    const bool valid = st * P + u < nt && pidx + u * kWsE < a.m;
+                    e64_record(a, pose, cp, hx[u], hy[u], hz[u], valid, w, r, xt);
+                    double *rec = slot + u * kWsRec * kWsE;
+                    rec[0] = w;
+                    rec[kWsE] = r[0];
+                    rec[2 * kWsE] = r[1];
+                    rec[3 * kWsE] = r[2];
+                    rec[4 * kWsE] = xt[0];
+                    rec[5 * kWsE] = xt[1];
+                    rec[6 * kWsE] = xt[2];
+                }
+                named_arrive(1 + stage, NT);                        // records written
+            }
+            // balance the empty barrier: one wait per consumed stage
+            for (int st = max(steps - kWsStages, 0); st < steps; ++st) named_sync(3 + (st & 1), NT);
+        } else {
+            double acc[kE64Stats];
+#pragma unroll
+            for (int q = 0; q < kE64Stats; ++q) acc[q] = 0.0;
+            const int mt = tid - kWsE;
+            for (int st = 0; st < steps; ++st) {
+                const int stage = st & 1;
+                named_sync(1 + stage, NT);
+                const double *slot = ring + (size_t)stage * P * kWsRec * kWsE + mt;
+#pragma unroll
+                for (int u = 0; u < P; ++u)
+#pragma unroll
+                    for (int hh = 0; hh < kWsE / kWsM; ++hh) {
+                        const double *rec = slot + u * kWsRec * kWsE + hh * kWsM;
+                        const double r[3] = {rec[kWsE], rec[2 * kWsE], rec[3 * kWsE]};
+                        const double xt[3] = {rec[4 * kWsE], rec[5 * kWsE], rec[6 * kWsE]};
+                        e64_accumulate(rec[0], r, xt, acc);
+                    }
+                named_arrive(3 + stage, NT);
+            }
+            sh.red[warp - kWsE / 32][lane] = warp_reduce_scatter(acc);
+        }
+        __syncthreads();
+        double *rows = a.partials + (long long)(it & 1) * nb * kE64Row;
+        if (tid < kE64Stats) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < WM; ++w) s += sh.red[w][tid];
+            rows[(long long)blockIdx.x * kE64Row + tid] = s;
+            __threadfence();             // the row before this CTA's arrival
+        }
+        __syncthreads();
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 1] = gtime();
+        if (tid == 0) {
+            const unsigned target = (unsigned)nb * (unsigned)(it + 1);
+            atomicAdd(a.counter, 1u);
+            while (ld_acquire(a.counter) < target) __nanosleep(20);
+        }
+        __syncthreads();
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 2] = gtime();
+        if (a.solve == 2 && tid == 0) se.pending = 1;     // solved by the next launch
+        if (a.solve != 1 && blockIdx.x != 0) continue;
+        {
+            const int c = lane, grp = warp;
+            double s = 0.0;
+            if (c < kE64Stats) {
+                constexpr int kMaxRows = (kE64MaxSms + W - 1) / W;
+                double r[kMaxRows];
+#pragma unroll
+                for (int u = 0; u < kMaxRows; ++u) {
+                    const int b = grp + W * u;
+                    r[u] = b < nb ? __ldcg(rows + (long long)b * kE64Row + c) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kMaxRows; ++u) s += r[u];
+            }
+            __syncthreads();             // red[] reuse
+            sh.red[grp][c] = s;
+        }
+        __syncthreads();
+        if (tid < kE64Stats) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < W; ++j) s += sh.red[j][tid];
+            sh.tsum[tid] = s;
+            if (blockIdx.x == 0) a.sums[tid] = s;
+        }
+        __syncthreads();
+        if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[8 * it + 3] = gtime();
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void em64_cta_ws(const Em64Args &a) {
+    extern __shared__ __align__(128) double ring[];     // [kWsStages][P][kWsRec][kWsE]
+    __shared__ WsShared sh;
+    const int tid = threadIdx.x;
+    copy_cg(&sh.se, a.em, tid, kWsThreads);
+    if (tid == 0) sh.it0 = __ldcg(&a.em->iterations);
+    __syncthreads();
+    if (tid >= kWsE) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+        em64_ws_loop<P, true>(a, sh, ring);
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+        em64_ws_loop<P, false>(a, sh, ring);
+    }
+    __syncthreads();
+    if (a.solve && blockIdx.x == 0)
+        rigid_finish_tnorms(a.traces + sh.se.max_em_iters, a.traces + 3 * sh.se.max_em_iters,
+                            sh.it0, sh.se.iterations, sh.se.diameter);
+    if (blockIdx.x == 0 && a.solve) {
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&sh.se);
+        for (int q = tid; q < (int)(sizeof(EmDev) / 8); q += kWsThreads)
+            reinterpret_cast<unsigned long long *>(a.em)[q] = src[q];
+    }
+}
+
+#ifndef FR_EM64_WS_PTS
+#define FR_EM64_WS_PTS 2
+#endif
+
+template <bool BATCH>
+__global__ void __launch_bounds__(kWsThreads, 1)
+k_em64_ws(Em64Args a0, const Em64Args *__restrict__ batch) {
+    if constexpr (BATCH) {
+        const Em64Args &a = batch[blockIdx.y];
+        em64_cta_ws<FR_EM64_WS_PTS>(a);
+    } else {
+        em64_cta_ws<FR_EM64_WS_PTS>(a0);
+    }
+}
+
 // the kernel: one problem (parameters by value: constant-bank operands), or a
 // batch of independent problems, blockIdx.y = problem (replicas, no
 // collectives; every problem has its own state, partial rows and counter)
@@ -413,7 +652,11 @@ __global__ void k_em64_solve(const double *sums, EmDev *e, double *traces) {
         reinterpret_cast<unsigned long long *>(e)[q] = src[q];
 }
 
-// launch variants (FR_EM64_VARIANT): 0 (default) = 256 threads x 1 CTA/SM, 255
+// launch variants (FR_EM64_VARIANT): 4 = warp-specialised (em64_cta_ws: 256
+// record threads at 208 registers + 128 statistics threads at 88, setmaxnreg;
+// measured at 1M: pass 17.7 / 18.6 / 17.8 us with 2 / 3 / 4 points per record
+// thread vs 16.0-16.4 for variant 0 -- the ring's stores and barriers cost
+// more than the freed registers buy); 0 (default) = 256 threads x 1 CTA/SM, 255
 // registers (no spills, the solve inlined), two points per thread and step
 // with the next pair prefetched into registers; 2 = 512 x 1 with one point
 // per step (128 registers: 116 B of spills; 10-20% slower per iteration);
@@ -424,8 +667,12 @@ using E64Kernel = void (*)(Em64Args, const Em64Args *);
 struct E64Variant {
     E64Kernel fn, batch;
     int threads, minb, stages;
-    int block() const { return threads + (stages ? 32 : 0); }
-    size_t smem() const { return (size_t)stages * 3 * threads * sizeof(double); }
+    int ws = 0;              // warp-specialised (threads = record side; + kWsM statistics threads)
+    int block() const { return threads + (stages ? 32 : 0) + (ws ? kWsM : 0); }
+    size_t smem() const {
+        return ws ? (size_t)kWsStages * FR_EM64_WS_PTS * kWsRec * kWsE * sizeof(double)
+                  : (size_t)stages * 3 * threads * sizeof(double);
+    }
 };
 
 static E64Variant e64_variant() {
@@ -436,6 +683,7 @@ static E64Variant e64_variant() {
     }
     if (v == 1) return {k_em64<384, 1, 8, false>, k_em64<384, 1, 8, true>, 384, 1, 8};
     if (v == 2) return {k_em64<512, 1, 0, false>, k_em64<512, 1, 0, true>, 512, 1, 0};
+    if (v == 4) return {k_em64_ws<false>, k_em64_ws<true>, kWsE, 1, 0, 1};
     return {k_em64<256, 1, 0, false>, k_em64<256, 1, 0, true>, 256, 1, 0};
 }
 
