@@ -109,6 +109,18 @@ int fr_lattice_splat_points(fr_lattice *lat, const float *d_pos, const float *d_
 int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
                             float *d_soa, void *stream, void (*uploaded)(void *), void *ctx);
 
+/* fr_upload_rows64 + fr_lattice_splat_points on the float64 planes (positions
+ * in the caller's order, value columns [1, y] or [1, y, |y|^2]) in one call.
+ * Page-locked rows of >= 256k points go out as up to 8 back-to-back copies on
+ * `stream`; each range's transpose into d_soa and its splat entries run on a
+ * side stream as soon as the range lands, under the remaining copies.
+ * `uploaded` (nullable) is called with `ctx` once every copy is enqueued
+ * (work enqueued on `stream` afterwards queues behind the copies only).
+ * Sums, keys and sites are those of fr_upload_rows64 + fr_lattice_splat_points. */
+int fr_lattice_splat_rows64(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
+                            double *d_rows, double *d_soa, void *stream,
+                            void (*uploaded)(void *), void *ctx);
+
 /* (n, 3) float64 host rows (pageable) -> (3, n) float32 device planes, the
  * boundary conversion of PointCloud.positions / normals (geometry.py:109-139,
  * "convert once to fp32 SoA device tensors").  Rounds to

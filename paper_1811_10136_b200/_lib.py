@@ -24,7 +24,8 @@ FR_POINT_TO_POINT, FR_POINT_TO_PLANE = 0, 1
 # every symbol include/filterreg_b200.h declares
 EXPORTED = (
     "fr_abi_version", "fr_last_error", "fr_lattice_create", "fr_lattice_destroy",
-    "fr_lattice_splat", "fr_lattice_splat_points", "fr_lattice_splat_upload", "fr_lattice_blur",
+    "fr_lattice_splat", "fr_lattice_splat_points", "fr_lattice_splat_upload",
+    "fr_lattice_splat_rows64", "fr_lattice_blur",
     "fr_lattice_info", "fr_lattice_dense_cells", "fr_lattice_set_stream",
     "fr_lattice_export", "fr_lattice_slice", "fr_simplex", "fr_gauss_bruteforce",
     "fr_moments", "fr_rigid_pass_width", "fr_rigid_scratch_doubles", "fr_rigid_pass",
@@ -89,6 +90,7 @@ _SIGS = {
     "fr_lattice_splat": ([_P, _P, _P, _L, _I, _P], _I),
     "fr_lattice_splat_points": ([_P, _P, _P, _L, _I, _P], _I),
     "fr_lattice_splat_upload": ([_P, _P, _L, _I, _P, _P, _P, _P], _I),
+    "fr_lattice_splat_rows64": ([_P, _P, _L, _I, _P, _P, _P, _P, _P], _I),
     "fr_lattice_blur": ([_P, _P], _I),
     "fr_lattice_info": ([_P, ctypes.POINTER(_L), ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "fr_lattice_dense_cells": ([_P, ctypes.POINTER(_L)], _I),

@@ -189,6 +189,11 @@ _SETUP_POOL = None
 # per registration overlapped; at 10k neither way is faster)
 SETUP_OVERLAP_MIN = 50_000
 
+# float64 point-to-point observation: upload and splat in one call
+# (fr_lattice_splat_rows64: page-locked clouds of >= 256k points overlap the
+# splat entries with the copies)
+CHUNKED_F64_SPLAT = True
+
 
 class _InlineExecutor:
     """ThreadPoolExecutor stand-in that runs the job on submit."""
@@ -410,7 +415,32 @@ class RigidDevicePath:
     def _build_observation_on(self, observation, gmm, residual_mode, stream, lap) -> None:
         import torch
         with torch.cuda.stream(stream):
-            if self.f64:
+            if self.f64 and residual_mode == "point_to_point" and CHUNKED_F64_SPLAT:
+                # float64 planes, splat from them (keys bit-exact for any input);
+                # page-locked rows go out in ranges whose splat entries run
+                # under the remaining copies (fr_lattice_splat_rows64)
+                P = np.ascontiguousarray(observation.positions, dtype=np.float64)
+                n = len(P)
+                self.obs = torch.empty((3, n), dtype=torch.float64, device=self.dev)
+                rows = torch.empty((n, 3), dtype=torch.float64, device=self.dev)
+                self.N, self.obs_n = n, None
+                s = np.atleast_1d(np.asarray(gmm.sigma, dtype=float))
+                s = np.full(3, s[0]) if s.size == 1 else s
+                lat = PermutohedralLattice(3, s)
+
+                def copied():
+                    # the model's DMA queues behind the observation copies only
+                    self._obs_dma = torch.cuda.Event()
+                    self._obs_dma.record(stream)
+                    self._obs_uploaded.set()
+
+                lat.splat_rows64(P, rows, self.obs, self.value_mode, uploaded=copied)
+                if lap is not None:
+                    lap("obs_upload")
+                lat.blur()
+                del rows
+                self.lattice, self.sigma = lat, s
+            elif self.f64:
                 # float64 planes, splat from them (keys bit-exact for any input)
                 self.obs = upload_soa64(observation.positions, self.dev)
                 self.N, self.obs_n = self.obs.shape[1], None

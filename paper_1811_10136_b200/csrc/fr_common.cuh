@@ -21,6 +21,11 @@ namespace fr {
 using ChunkHook = std::function<int(long long, long long, cudaEvent_t)>;
 int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cudaStream_t s,
                          const ChunkHook &hook);
+// page-locked host range (cudaPointerGetAttributes); rows [a, b) of (n, 3)
+// float64 device rows -> the (3, n) planes, on `s` (fr_upload.cu)
+bool host_is_pinned(const void *p, size_t bytes);
+void rows_to_soa64_range(const double *rows, long long n, double *soa, long long a, long long b,
+                         cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // errors

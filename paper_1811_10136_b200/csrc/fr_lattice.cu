@@ -2422,6 +2422,74 @@ int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, 
     return splat_impl<3, PointSrc>(lat, src, n, nv, s, &hook, (value_mode & FR_SPLAT_FLAT_ORDER) != 0);
 }
 
+int fr_lattice_splat_rows64(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
+                            double *d_rows, double *d_soa, void *stream,
+                            void (*uploaded)(void *), void *ctx) {
+    if (!lat || (n > 0 && (!host_xyz || !d_rows || !d_soa))) {
+        set_error("null argument");
+        return FR_EINVAL;
+    }
+    if (lat->dim != 3) {
+        set_error("point splat needs a 3-D lattice");
+        return FR_EINVAL;
+    }
+    if (value_mode & (FR_VALUES_NORMALS | FR_SPLAT_SPATIAL)) {
+        set_error("fr_lattice_splat_rows64 takes positions in the caller's order only");
+        return FR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    lat->stream = s;
+    const int m2 = (value_mode & FR_VALUES_M2) ? 1 : 0;
+    const int nv = 4 + m2;
+    const bool flat = (value_mode & FR_SPLAT_FLAT_ORDER) != 0;
+    PointSrc64 src{d_soa, nullptr, n, m2, nv};
+    // chunks of >= 128k points: below that the DMA is too short to hide anything
+    constexpr long long kChunkMin = 1LL << 17;
+    const int chunks = (int)std::min<long long>(8, n / kChunkMin);
+    if (chunks < 2 || !host_is_pinned(host_xyz, (size_t)n * 3 * sizeof(double))) {
+        FR_TRY(fr_upload_rows64(host_xyz, n, d_rows, d_soa, stream));
+        if (uploaded) uploaded(ctx);
+        return splat_impl<3, PointSrc64>(lat, src, n, nv, s, nullptr, flat, false);
+    }
+    // page-locked rows: the copies of `chunks` ranges go out on `s` back to
+    // back (the link stays busy); each range's transpose and splat entries
+    // run on a side stream as soon as its copy lands, under the next copies
+    const EntriesHook hook = [&](const EntriesLaunch &launch) -> int {
+        cudaStream_t side;
+        FR_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        std::vector<cudaEvent_t> landed(chunks, nullptr);
+        std::vector<long long> lo(chunks + 1);
+        for (int k = 0; k <= chunks; ++k) lo[k] = n * k / chunks;
+        int st = FR_OK;
+        for (int k = 0; k < chunks && st == FR_OK; ++k) {
+            if (cudaEventCreateWithFlags(&landed[k], cudaEventDisableTiming) != cudaSuccess ||
+                cudaMemcpyAsync(d_rows + 3 * lo[k], host_xyz + 3 * lo[k],
+                                (size_t)(lo[k + 1] - lo[k]) * 3 * sizeof(double),
+                                cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                cudaEventRecord(landed[k], s) != cudaSuccess) {
+                set_error("CUDA error: %s", cudaGetErrorString(cudaGetLastError()));
+                st = FR_ECUDA;
+            }
+        }
+        if (uploaded) uploaded(ctx);     // every copy enqueued: later work may queue behind
+        for (int k = 0; k < chunks && st == FR_OK; ++k) {
+            cudaStreamWaitEvent(side, landed[k], 0);
+            rows_to_soa64_range(d_rows, n, d_soa, lo[k], lo[k + 1], side);
+            st = launch(lo[k], lo[k + 1], side);
+        }
+        cudaEvent_t done;
+        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        cudaEventRecord(done, side);
+        cudaStreamWaitEvent(s, done, 0);
+        cudaEventDestroy(done);
+        for (int k = 0; k < chunks; ++k)
+            if (landed[k]) cudaEventDestroy(landed[k]);
+        cudaStreamDestroy(side);
+        return st;
+    };
+    return splat_impl<3, PointSrc64>(lat, src, n, nv, s, &hook, flat, false);
+}
+
 int fr_lattice_blur(fr_lattice *lat, void *stream) {
     if (!lat) {
         set_error("null lattice");

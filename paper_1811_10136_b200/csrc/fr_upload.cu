@@ -178,7 +178,7 @@ void worker_rows(int dev, int id, const double *src, long long a, long long b, d
 
 // true when [p, p + bytes) is page-locked host memory (cudaHostAlloc'd or
 // registered): both ends are checked, a failed query is cleared
-bool host_is_pinned(const void *p, size_t bytes) {
+bool host_is_pinned_impl(const void *p, size_t bytes) {
     for (const char *q : {static_cast<const char *>(p), static_cast<const char *>(p) + bytes - 1}) {
         cudaPointerAttributes at;
         if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
@@ -313,6 +313,26 @@ int upload_points_hooked(const double *host_xyz, long long n, float *d_soa, cuda
     return upload_impl<float>(host_xyz, n, d_soa, s, hook);
 }
 
+__global__ void k_rows_to_soa64_range(const double *__restrict__ rows, long long n,
+                                      double *__restrict__ soa, long long a, long long b) {
+    for (long long i = a + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < b;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double x = rows[3 * i], y = rows[3 * i + 1], z = rows[3 * i + 2];
+        soa[i] = x;
+        soa[n + i] = y;
+        soa[2 * n + i] = z;
+    }
+}
+
+void rows_to_soa64_range(const double *rows, long long n, double *soa, long long a, long long b,
+                         cudaStream_t s) {
+    if (b <= a) return;
+    const int blocks = (int)std::min<long long>((b - a + 255) / 256, 148LL * 16);
+    k_rows_to_soa64_range<<<blocks, 256, 0, s>>>(rows, n, soa, a, b);
+}
+
+bool host_is_pinned(const void *p, size_t bytes) { return host_is_pinned_impl(p, bytes); }
+
 }  // namespace fr
 
 extern "C" int fr_upload_points(const double *host_xyz, int64_t n, float *d_soa, void *stream) {
@@ -333,7 +353,7 @@ extern "C" int fr_upload_rows64(const double *host_xyz, int64_t n, double *d_row
     if (n == 0) return FR_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
-    if (host_is_pinned(host_xyz, (size_t)n * 3 * sizeof(double))) {
+    if (host_is_pinned_impl(host_xyz, (size_t)n * 3 * sizeof(double))) {
         // page-locked rows (e.g. load_cloud(..., pinned=True)): one DMA at
         // PCIe rate straight from the caller's buffer, no staging copy
         FR_CUDA(cudaMemcpyAsync(d_rows, host_xyz, (size_t)n * 3 * sizeof(double),

@@ -206,6 +206,22 @@ class PermutohedralLattice:
         self._splatted = True
         self._export = None
 
+    def splat_rows64(self, host_positions, out_rows, out_soa, value_mode: int = 0,
+                     uploaded=None) -> None:
+        """Upload (n, 3) float64 host positions (rows into `out_rows`, planes
+        into `out_soa` (3, n), no rounding) and splat [1, y, (|y|^2)] from the
+        planes; page-locked rows are copied in ranges whose splat entries run
+        under the remaining copies.  `uploaded()` runs once every copy is
+        enqueued on the current stream."""
+        P = np.ascontiguousarray(host_positions, dtype=np.float64)
+        cb = _UPLOADED_CB((lambda _ctx: uploaded()) if uploaded is not None else (lambda _ctx: None))
+        _lib.check(self._lib.fr_lattice_splat_rows64(
+            self._h, P.ctypes.data_as(ctypes.c_void_p), len(P), value_mode, _lib.ptr(out_rows),
+            _lib.ptr(out_soa), _lib.stream_handle(), ctypes.cast(cb, ctypes.c_void_p), None))
+        self.blurred = False
+        self._splatted = True
+        self._export = None
+
     def bind_stream(self, stream) -> None:
         """Stream the lattice's stream-ordered frees go behind (after a side-
         stream build has completed)."""
