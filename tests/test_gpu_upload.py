@@ -104,3 +104,39 @@ def test_pinned_load_cloud_registers_identically(tmp_path):
     torch.cuda.synchronize()
     assert r1.iterations == r2.iterations
     assert np.array_equal(r1.kinematics.pose.matrix(), r2.kinematics.pose.matrix())
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("value_mode_name", ["tree", "flat_m2"])
+def test_splat_rows64_matches_two_step(pinned, value_mode_name):
+    """fr_lattice_splat_rows64 (float64 rows in ranges, each range's transpose
+    and splat entries under the remaining copies when page-locked) ==
+    fr_upload_rows64 + fr_lattice_splat_points on the float64 planes: planes
+    bit-exact, pre- and post-blur site tables bit-exact."""
+    import torch
+    import paper_1811_10136_b200 as fr
+    from paper_1811_10136_b200 import _lib
+    from paper_1811_10136_b200.permutohedral import PermutohedralLattice
+    from paper_1811_10136_b200._rigid import upload_soa64
+    mode = 0 if value_mode_name == "tree" else _lib.FR_VALUES_M2 | _lib.FR_SPLAT_FLAT_ORDER
+    model, obs, _ = O.pebble_pair(700_000, outlier_ratio=0.05, seed=3)
+    Y = obs.astype(np.float32).astype(float) + 0.125 * obs.astype(float) * 1e-7
+    P = fr.pinned_copy(Y) if pinned else np.ascontiguousarray(Y)
+    sigma = np.full(3, 0.03 * O.bbox_diameter(Y))
+    dev = torch.device("cuda", 0)
+    planes = torch.empty((3, len(Y)), dtype=torch.float64, device=dev)
+    rows = torch.empty((len(Y), 3), dtype=torch.float64, device=dev)
+    seen = []
+    a = PermutohedralLattice(3, sigma)
+    a.splat_rows64(P, rows, planes, mode, uploaded=lambda: seen.append(1))
+    assert seen == [1]
+    assert np.array_equal(planes.cpu().numpy(), Y.T)
+    b = PermutohedralLattice(3, sigma)
+    b.splat_points(upload_soa64(Y, dev), None, mode)
+    for stage in ("splat", "blur"):
+        if stage == "blur":
+            a.blur()
+            b.blur()
+        assert a.num_sites == b.num_sites
+        assert np.array_equal(a.keys, b.keys)
+        assert np.array_equal(a.values, b.values)

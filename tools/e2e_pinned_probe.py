@@ -19,7 +19,8 @@ for n in [int(a) for a in sys.argv[1:]] or [1_000_000]:
     X = model.astype(np.float32).astype(float)
     Y = obs.astype(np.float32).astype(float)
     gmm = fr.GmmConfig(sigma=0.05 * O.bbox_diameter(X[:n]), outlier_ratio=0.1)
-    cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=50, twist_tolerance=1e-30)
+    iters = int(os.environ.get("ITERS", "50"))
+    cfg = fr.RegistrationConfig(gmm=gmm, max_em_iters=iters, twist_tolerance=1e-30)
     a, b = fr.pinned_cloud(fr.PointCloud(X)), fr.pinned_cloud(fr.PointCloud(Y))
     ts = {True: [], False: []}
     R = {}
@@ -33,6 +34,6 @@ for n in [int(a) for a in sys.argv[1:]] or [1_000_000]:
         if rep >= 3:
             ts[flag].append(time.perf_counter() - t0)
         R[flag] = res.kinematics.pose.matrix()
-    print(f"{len(X)} pinned e2e register (50 iterations): chunked {1e3 * np.median(ts[True]):.3f} ms, "
+    print(f"{len(X)} pinned e2e register ({iters} iterations): chunked {1e3 * np.median(ts[True]):.3f} ms, "
           f"one copy {1e3 * np.median(ts[False]):.3f} ms; pose max diff "
           f"{np.abs(R[True] - R[False]).max():.2e}", flush=True)
