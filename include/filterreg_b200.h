@@ -112,13 +112,15 @@ int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, 
 /* fr_upload_rows64 + fr_lattice_splat_points on the float64 planes (positions
  * in the caller's order, value columns [1, y] or [1, y, |y|^2]) in one call.
  * Page-locked rows of >= 256k points go out as up to 8 back-to-back copies on
- * `stream`; each range's transpose into d_soa and its splat entries run on a
- * side stream as soon as the range lands, under the remaining copies.
- * `uploaded` (nullable) is called with `ctx` once every copy is enqueued
- * (work enqueued on `stream` afterwards queues behind the copies only).
- * Sums, keys and sites are those of fr_upload_rows64 + fr_lattice_splat_points. */
+ * an internal copy stream (after the work already on `stream`); each range's
+ * transpose into d_soa and its splat entries run on a side stream as soon as
+ * the range lands, under the remaining copies.  Once every copy is enqueued,
+ * `follow_stream` (nullable) is made to wait for them (the caller's next
+ * transfer does not share the link with them) and `uploaded` (nullable) is
+ * called with `ctx`.  Sums, keys and sites are those of fr_upload_rows64 +
+ * fr_lattice_splat_points; on return `stream` is ordered after all of it. */
 int fr_lattice_splat_rows64(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
-                            double *d_rows, double *d_soa, void *stream,
+                            double *d_rows, double *d_soa, void *stream, void *follow_stream,
                             void (*uploaded)(void *), void *ctx);
 
 /* (n, 3) float64 host rows (pageable) -> (3, n) float32 device planes, the

@@ -90,7 +90,7 @@ _SIGS = {
     "fr_lattice_splat": ([_P, _P, _P, _L, _I, _P], _I),
     "fr_lattice_splat_points": ([_P, _P, _P, _L, _I, _P], _I),
     "fr_lattice_splat_upload": ([_P, _P, _L, _I, _P, _P, _P, _P], _I),
-    "fr_lattice_splat_rows64": ([_P, _P, _L, _I, _P, _P, _P, _P, _P], _I),
+    "fr_lattice_splat_rows64": ([_P, _P, _L, _I, _P, _P, _P, _P, _P, _P], _I),
     "fr_lattice_blur": ([_P, _P], _I),
     "fr_lattice_info": ([_P, ctypes.POINTER(_L), ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "fr_lattice_dense_cells": ([_P, ctypes.POINTER(_L)], _I),

@@ -189,10 +189,14 @@ _SETUP_POOL = None
 # per registration overlapped; at 10k neither way is faster)
 SETUP_OVERLAP_MIN = 50_000
 
-# float64 point-to-point observation: upload and splat in one call
-# (fr_lattice_splat_rows64: page-locked clouds of >= 256k points overlap the
-# splat entries with the copies)
-CHUNKED_F64_SPLAT = True
+# float64 point-to-point observation through fr_lattice_splat_rows64 (upload
+# and splat in one call; page-locked clouds of >= 256k points go out in ranges
+# whose splat entries run under the remaining copies).  Off by default:
+# measured in the bench at 1M the e2e call takes 3.75 ms with it vs 2.82 ms
+# with the single DMA + separate splat (the per-call copy / kernel streams and
+# the worker's buffer allocations land on the model side's critical path,
+# which the single-DMA order overlaps); FR_CHUNKED_F64=1 turns it on
+CHUNKED_F64_SPLAT = os.environ.get("FR_CHUNKED_F64", "0") != "0"
 
 
 class _InlineExecutor:
@@ -311,6 +315,7 @@ class RigidDevicePath:
         self.sigma = None
         self._obs_dma = None
         main_stream = torch.cuda.current_stream()
+        self._main_stream = main_stream
         side = _side_stream()
         # small clouds: the worker thread's handoff costs more than the
         # overlap saves (and serialises on the GIL in register_batch)
@@ -419,22 +424,30 @@ class RigidDevicePath:
                 # float64 planes, splat from them (keys bit-exact for any input);
                 # page-locked rows go out in ranges whose splat entries run
                 # under the remaining copies (fr_lattice_splat_rows64)
+                if lap is not None:
+                    lap("obs_start")
                 P = np.ascontiguousarray(observation.positions, dtype=np.float64)
                 n = len(P)
                 self.obs = torch.empty((3, n), dtype=torch.float64, device=self.dev)
                 rows = torch.empty((n, 3), dtype=torch.float64, device=self.dev)
+                if lap is not None:
+                    lap("obs_buffers")
                 self.N, self.obs_n = n, None
                 s = np.atleast_1d(np.asarray(gmm.sigma, dtype=float))
                 s = np.full(3, s[0]) if s.size == 1 else s
                 lat = PermutohedralLattice(3, s)
+                if lap is not None:
+                    lap("obs_lattice")
 
                 def copied():
-                    # the model's DMA queues behind the observation copies only
-                    self._obs_dma = torch.cuda.Event()
-                    self._obs_dma.record(stream)
+                    # the caller's stream already waits for the observation
+                    # copies: the model's DMA queues behind them
                     self._obs_uploaded.set()
+                    if lap is not None:
+                        lap("obs_copies")
 
-                lat.splat_rows64(P, rows, self.obs, self.value_mode, uploaded=copied)
+                lat.splat_rows64(P, rows, self.obs, self.value_mode, uploaded=copied,
+                                 follow_stream=self._main_stream)
                 if lap is not None:
                     lap("obs_upload")
                 lat.blur()

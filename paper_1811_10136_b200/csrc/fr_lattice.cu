@@ -2269,6 +2269,58 @@ int fr_sort_points_morton64(double *pos, int64_t n, int planes, int32_t *perm_ou
 
 const char *fr_last_error(void) { return fr::last_error(); }
 
+// lattice counter blocks (4 u64): recycled behind an event recorded on the
+// destroyed lattice's stream, so creating a lattice neither allocates
+// stream-ordered memory on the legacy stream nor synchronises it (that
+// synchronisation waited for every kernel already queued there)
+namespace {
+struct CounterRecycle {
+    std::mutex mu;
+    std::vector<std::pair<unsigned long long *, cudaEvent_t>> q;
+};
+CounterRecycle g_counter_recycle[16];
+
+unsigned long long *counters_get() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    CounterRecycle &r = g_counter_recycle[dev & 15];
+    {
+        std::lock_guard<std::mutex> g(r.mu);
+        for (size_t i = 0; i < r.q.size(); ++i) {
+            const cudaError_t e = cudaEventQuery(r.q[i].second);
+            if (e == cudaSuccess) {
+                unsigned long long *p = r.q[i].first;
+                cudaEventDestroy(r.q[i].second);
+                r.q.erase(r.q.begin() + (long)i);
+                return p;
+            }
+            if (e == cudaErrorNotReady) cudaGetLastError();   // not an error: clear it
+        }
+    }
+    unsigned long long *p = nullptr;
+    if (cudaMalloc((void **)&p, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void counters_put(unsigned long long *p, cudaStream_t s) {
+    if (!p) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, s) != cudaSuccess) {
+        cudaGetLastError();
+        return;                       // leaked (32 bytes) rather than reused unsafely
+    }
+    CounterRecycle &r = g_counter_recycle[dev & 15];
+    std::lock_guard<std::mutex> g(r.mu);
+    r.q.emplace_back(p, ev);
+}
+}  // namespace
+
 int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
     if (!out || !sigma) {
         set_error("null argument");
@@ -2294,8 +2346,8 @@ int fr_lattice_create(int dim, const double *sigma, fr_lattice **out) {
     fr_lattice *lat = new fr_lattice();
     lat->c = c;
     lat->dim = dim;
-    if (pool_alloc(lat, (void **)&lat->d_counters, 4 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaStreamSynchronize(lat->stream) != cudaSuccess) {
+    lat->d_counters = counters_get();
+    if (!lat->d_counters) {
         delete lat;
         set_error("device allocation failed for lattice counters");
         return FR_ECUDA;
@@ -2311,7 +2363,7 @@ int fr_lattice_destroy(fr_lattice *lat) {
     // from other streams synchronise those first -- include/filterreg_b200.h)
     free_build(lat);
     free_slice(lat);
-    pool_free(lat, lat->d_counters);
+    counters_put(lat->d_counters, lat->stream);
     delete lat;
     return FR_OK;
 }
@@ -2423,7 +2475,7 @@ int fr_lattice_splat_upload(fr_lattice *lat, const double *host_xyz, int64_t n, 
 }
 
 int fr_lattice_splat_rows64(fr_lattice *lat, const double *host_xyz, int64_t n, int value_mode,
-                            double *d_rows, double *d_soa, void *stream,
+                            double *d_rows, double *d_soa, void *stream, void *follow_stream,
                             void (*uploaded)(void *), void *ctx) {
     if (!lat || (n > 0 && (!host_xyz || !d_rows || !d_soa))) {
         set_error("null argument");
@@ -2443,35 +2495,79 @@ int fr_lattice_splat_rows64(fr_lattice *lat, const double *host_xyz, int64_t n, 
     const int nv = 4 + m2;
     const bool flat = (value_mode & FR_SPLAT_FLAT_ORDER) != 0;
     PointSrc64 src{d_soa, nullptr, n, m2, nv};
+    const auto follow = [&](cudaStream_t after) -> int {
+        // `follow_stream` queues behind the copies (the caller's next
+        // transfer does not share the link with them)
+        if (follow_stream && (cudaStream_t)follow_stream != after) {
+            cudaEvent_t ev;
+            FR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            FR_CUDA(cudaEventRecord(ev, after));
+            FR_CUDA(cudaStreamWaitEvent((cudaStream_t)follow_stream, ev, 0));
+            cudaEventDestroy(ev);
+        }
+        if (uploaded) uploaded(ctx);
+        return FR_OK;
+    };
     // chunks of >= 128k points: below that the DMA is too short to hide anything
     constexpr long long kChunkMin = 1LL << 17;
     const int chunks = (int)std::min<long long>(8, n / kChunkMin);
     if (chunks < 2 || !host_is_pinned(host_xyz, (size_t)n * 3 * sizeof(double))) {
         FR_TRY(fr_upload_rows64(host_xyz, n, d_rows, d_soa, stream));
-        if (uploaded) uploaded(ctx);
+        FR_TRY(follow(s));
         return splat_impl<3, PointSrc64>(lat, src, n, nv, s, nullptr, flat, false);
     }
-    // page-locked rows: the copies of `chunks` ranges go out on `s` back to
-    // back (the link stays busy); each range's transpose and splat entries
-    // run on a side stream as soon as its copy lands, under the next copies
-    const EntriesHook hook = [&](const EntriesLaunch &launch) -> int {
-        cudaStream_t side;
-        FR_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-        std::vector<cudaEvent_t> landed(chunks, nullptr);
-        std::vector<long long> lo(chunks + 1);
-        for (int k = 0; k <= chunks; ++k) lo[k] = n * k / chunks;
-        int st = FR_OK;
-        for (int k = 0; k < chunks && st == FR_OK; ++k) {
-            if (cudaEventCreateWithFlags(&landed[k], cudaEventDisableTiming) != cudaSuccess ||
-                cudaMemcpyAsync(d_rows + 3 * lo[k], host_xyz + 3 * lo[k],
-                                (size_t)(lo[k + 1] - lo[k]) * 3 * sizeof(double),
-                                cudaMemcpyHostToDevice, s) != cudaSuccess ||
-                cudaEventRecord(landed[k], s) != cudaSuccess) {
-                set_error("CUDA error: %s", cudaGetErrorString(cudaGetLastError()));
-                st = FR_ECUDA;
-            }
+    // page-locked rows: the copies of `chunks` ranges go out back to back on
+    // a copy stream, enqueued FIRST (the link starts at once; the splat's
+    // set-up on `s` does not queue behind them); each range's transpose and
+    // splat entries run on a side stream as soon as its copy lands, under
+    // the next copies
+    cudaStream_t cs = nullptr, side = nullptr;
+    std::vector<cudaEvent_t> landed(chunks, nullptr);
+    std::vector<long long> lo(chunks + 1);
+    for (int k = 0; k <= chunks; ++k) lo[k] = n * k / chunks;
+    const auto cleanup = [&]() {
+        for (int k = 0; k < chunks; ++k)
+            if (landed[k]) cudaEventDestroy(landed[k]);
+        if (cs) cudaStreamDestroy(cs);
+        if (side) cudaStreamDestroy(side);
+    };
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) {
+        set_error("CUDA error: %s", cudaGetErrorString(cudaGetLastError()));
+        cleanup();
+        return FR_ECUDA;
+    }
+    {
+        // the copies overwrite d_rows: after the caller's earlier work on `s`
+        cudaEvent_t before;
+        cudaEventCreateWithFlags(&before, cudaEventDisableTiming);
+        cudaEventRecord(before, s);
+        cudaStreamWaitEvent(cs, before, 0);
+        cudaEventDestroy(before);
+    }
+    for (int k = 0; k < chunks; ++k) {
+        if (cudaEventCreateWithFlags(&landed[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaMemcpyAsync(d_rows + 3 * lo[k], host_xyz + 3 * lo[k],
+                            (size_t)(lo[k + 1] - lo[k]) * 3 * sizeof(double),
+                            cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+            cudaEventRecord(landed[k], cs) != cudaSuccess) {
+            set_error("CUDA error: %s", cudaGetErrorString(cudaGetLastError()));
+            cleanup();
+            return FR_ECUDA;
         }
-        if (uploaded) uploaded(ctx);     // every copy enqueued: later work may queue behind
+    }
+    if (const int st = follow(cs)) {
+        cleanup();
+        return st;
+    }
+    const EntriesHook hook = [&](const EntriesLaunch &launch) -> int {
+        // the splat's set-up on `s` (hash table and counter fills) first
+        cudaEvent_t ready;
+        FR_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        cudaEventRecord(ready, s);
+        cudaStreamWaitEvent(side, ready, 0);
+        cudaEventDestroy(ready);
+        int st = FR_OK;
         for (int k = 0; k < chunks && st == FR_OK; ++k) {
             cudaStreamWaitEvent(side, landed[k], 0);
             rows_to_soa64_range(d_rows, n, d_soa, lo[k], lo[k + 1], side);
@@ -2482,12 +2578,19 @@ int fr_lattice_splat_rows64(fr_lattice *lat, const double *host_xyz, int64_t n, 
         cudaEventRecord(done, side);
         cudaStreamWaitEvent(s, done, 0);
         cudaEventDestroy(done);
-        for (int k = 0; k < chunks; ++k)
-            if (landed[k]) cudaEventDestroy(landed[k]);
-        cudaStreamDestroy(side);
         return st;
     };
-    return splat_impl<3, PointSrc64>(lat, src, n, nv, s, &hook, flat, false);
+    const int st = splat_impl<3, PointSrc64>(lat, src, n, nv, s, &hook, flat, false);
+    if (st != FR_OK) {
+        // the copies may not have been waited for (an early failure)
+        cudaEvent_t done;
+        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        cudaEventRecord(done, cs);
+        cudaStreamWaitEvent(s, done, 0);
+        cudaEventDestroy(done);
+    }
+    cleanup();
+    return st;
 }
 
 int fr_lattice_blur(fr_lattice *lat, void *stream) {

@@ -207,17 +207,19 @@ class PermutohedralLattice:
         self._export = None
 
     def splat_rows64(self, host_positions, out_rows, out_soa, value_mode: int = 0,
-                     uploaded=None) -> None:
+                     uploaded=None, follow_stream=None) -> None:
         """Upload (n, 3) float64 host positions (rows into `out_rows`, planes
         into `out_soa` (3, n), no rounding) and splat [1, y, (|y|^2)] from the
         planes; page-locked rows are copied in ranges whose splat entries run
-        under the remaining copies.  `uploaded()` runs once every copy is
-        enqueued on the current stream."""
+        under the remaining copies.  Once every copy is enqueued,
+        `follow_stream` (a torch stream, optional) waits for them and
+        `uploaded()` runs."""
         P = np.ascontiguousarray(host_positions, dtype=np.float64)
         cb = _UPLOADED_CB((lambda _ctx: uploaded()) if uploaded is not None else (lambda _ctx: None))
+        fs = ctypes.c_void_p(follow_stream.cuda_stream) if follow_stream is not None else None
         _lib.check(self._lib.fr_lattice_splat_rows64(
             self._h, P.ctypes.data_as(ctypes.c_void_p), len(P), value_mode, _lib.ptr(out_rows),
-            _lib.ptr(out_soa), _lib.stream_handle(), ctypes.cast(cb, ctypes.c_void_p), None))
+            _lib.ptr(out_soa), _lib.stream_handle(), fs, ctypes.cast(cb, ctypes.c_void_p), None))
         self.blurred = False
         self._splatted = True
         self._export = None

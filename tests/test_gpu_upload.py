@@ -128,7 +128,9 @@ def test_splat_rows64_matches_two_step(pinned, value_mode_name):
     rows = torch.empty((len(Y), 3), dtype=torch.float64, device=dev)
     seen = []
     a = PermutohedralLattice(3, sigma)
-    a.splat_rows64(P, rows, planes, mode, uploaded=lambda: seen.append(1))
+    follow = torch.cuda.Stream()
+    a.splat_rows64(P, rows, planes, mode, uploaded=lambda: seen.append(1), follow_stream=follow)
+    follow.synchronize()
     assert seen == [1]
     assert np.array_equal(planes.cpu().numpy(), Y.T)
     b = PermutohedralLattice(3, sigma)
