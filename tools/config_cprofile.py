@@ -28,5 +28,5 @@ for name, g, ref, obs, model, config in C.cases():
     fr.register(ref, obs, m, config)
     torch.cuda.synchronize()
     pr.disable()
-    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    pstats.Stats(pr).sort_stats(os.environ.get("SORT", "tottime")).print_stats(int(os.environ.get("TOP", "25")))
     break
