@@ -1399,9 +1399,8 @@ static int splat_agg(fr_lattice *lat, const Src &src, long long n, int nv, cudaS
     pool_free(lat, old_keys);
     lat->n_sites = S;
     pc.lap("sites");
+    // 2 S slots for S distinct keys: the inserts cannot fail, no flag read
     FR_TRY(rehash_sites<D>(lat, next_pow2(2ull * (unsigned long long)lat->n_sites), s));
-    unsigned long long hc3[3];
-    FR_TRY(read_counters(lat, s, hc3));
     pc.lap("rehash");
     return FR_OK;
 }
