@@ -772,13 +772,23 @@ class DeviceEM64:
         sp = ctypes.c_void_p()
         w = ctypes.c_int()
         _lib.check(self.lib.fr_em64_sums(h, ctypes.byref(sp), ctypes.byref(w)))
-        self.sums = torch.as_tensor(_DeviceArray(sp.value, w.value), device=path.dev)
+        self._sums_ptr = (sp.value, w.value)
+        self._sums = None
         # sharded: one fused launch per iteration (solve of the previous
         # sums, then the pass) + one all-reduce; FUSED_SHARDED = False: pass,
         # all-reduce, solve kernel
         self._fused = path.group is not None and FUSED_SHARDED
         if path.group is not None and type(self) is DeviceEM64 and self._nccl_group():
             self._capture()
+
+    @property
+    def sums(self):
+        """The device sums as a tensor (made on first use: only the sharded
+        loop all-reduces them, and the wrapper costs tens of microseconds)."""
+        if self._sums is None:
+            import torch
+            self._sums = torch.as_tensor(_DeviceArray(*self._sums_ptr), device=self.path.dev)
+        return self._sums
 
     def __del__(self):
         self._graph = None             # the captured chunk goes before its buffers
@@ -934,7 +944,8 @@ class DeviceEM64PL(DeviceEM64):
         sp = ctypes.c_void_p()
         w = ctypes.c_int()
         _lib.check(self.lib.fr_em64pl_sums(h, ctypes.byref(sp), ctypes.byref(w)))
-        self.sums = torch.as_tensor(_DeviceArray(sp.value, w.value), device=path.dev)
+        self._sums_ptr = (sp.value, w.value)
+        self._sums = None
 
     def __del__(self):
         h = getattr(self, "h", None)
